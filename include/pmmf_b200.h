@@ -1,0 +1,179 @@
+/*
+ * pmmf_b200.h — C-ABI of the B200-native pMMF stage loop.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or C++
+ * types.  Each entry point replaces one reference interface of
+ * /root/reference/proj/include/pmmf (cited per function).  The C++ shim in
+ * include/pmmf_b200/dropin.hpp and the Python mirror in
+ * paper_1507_04396_b200/api.py are thin layers over these calls.
+ *
+ * Conventions
+ *   - every call returns a pmmf_b200_status; on failure a NUL-terminated
+ *     message is written to err[0..errlen) when err != NULL.  The status
+ *     maps 1:1 onto the reference's exception types (types.hpp:24-32,
+ *     factorizer.hpp:44-50, :404-408, :573-576, blocked_matrix.hpp:143-149).
+ *   - indices are int64 global ids (types.hpp:11 `index_t`), values fp64.
+ *   - dense k x k rotation blocks and the g x g core are row-major, like
+ *     pmmf::DenseMatrix (dense.hpp:36).
+ *   - multi right-hand-side vectors are stored rhs-major: rhs r occupies
+ *     [r*n, (r+1)*n).
+ */
+#ifndef PMMF_B200_H
+#define PMMF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum pmmf_b200_status {
+  PMMF_OK = 0,
+  PMMF_INVALID_ARGUMENT = 1, /* std::invalid_argument               */
+  PMMF_OUT_OF_RANGE = 2,     /* std::out_of_range                   */
+  PMMF_NUMERIC = 3,          /* pmmf::NumericError                  */
+  PMMF_DATA = 4,             /* pmmf::DataError                     */
+  PMMF_CUDA = 5,             /* device / driver failure             */
+  PMMF_INTERNAL = 6          /* anything else (bug)                 */
+} pmmf_b200_status;
+
+/* FactorizeParams (factorizer.hpp:35-51) with its nested ClusterParams
+ * (clustering.hpp:28-41).  cluster.seed is accepted but, as in the
+ * reference (factorizer.hpp:435-436), re-derived per stage. */
+typedef struct pmmf_b200_params {
+  int32_t k;              /* rotation order, 2 = Givens                 */
+  int32_t n_stages;       /* P                                          */
+  double eta;             /* rotations per cluster: floor(eta * c)      */
+  int64_t m_target;       /* m                                          */
+  int64_t c_min;
+  int64_t c_max;
+  int32_t d_max;          /* D_max                                      */
+  int32_t bypass_enabled;
+  uint64_t cluster_seed;  /* ignored (re-derived per stage)             */
+  int64_t core_min;
+  int64_t core_cap;
+  uint64_t seed;
+} pmmf_b200_params;
+
+/* Input matrix in coordinate form plus its block partition: the data of
+ * BlockedSparseMatrix::from_triplets(n, entries, partition)
+ * (blocked_matrix.hpp:133-156).  n_clusters == 0 means Partition::trivial(n)
+ * (partition.hpp:57-61).  Duplicates are summed in input order. */
+typedef struct pmmf_b200_coo {
+  int64_t n;
+  int64_t nnz;
+  const int64_t* rows;
+  const int64_t* cols;
+  const double* vals;
+  int64_t n_clusters;
+  const int64_t* cluster_offsets; /* n_clusters + 1 entries           */
+  const int64_t* cluster_members; /* cluster_offsets[n_clusters] ids  */
+  int32_t on_device;              /* rows/cols/vals are CUDA pointers */
+  int32_t device;                 /* CUDA ordinal for the computation */
+} pmmf_b200_coo;
+
+/* Scalar view of MmfFactorization (factorizer.hpp:111-118) and
+ * FactorizeStats::trivial (:105-109). */
+typedef struct pmmf_b200_summary {
+  int64_t n;
+  int64_t n_stages;
+  int64_t k;
+  int64_t core_size;      /* |h.core_indices|                            */
+  int64_t n_diagonal;     /* |h.diagonal|                                */
+  int64_t trivial;
+  double residual_sq;
+} pmmf_b200_summary;
+
+/* Sizes of one Stage (factorizer.hpp:65-70). */
+typedef struct pmmf_b200_stage_sizes {
+  int64_t n_clusters;     /* stage partition, bypass cluster included */
+  int64_t partition_size;
+  int64_t n_rotations;
+  int64_t n_eliminated;
+  int64_t n_bypassed;
+} pmmf_b200_stage_sizes;
+
+/* SolveConfig (solver.hpp:73-86); the preconditioner is chosen by passing
+ * an operator (pmmf) or NULL (none) to pmmf_b200_solve. */
+typedef struct pmmf_b200_solve_config {
+  double tol;
+  int32_t max_iter;
+  int32_t rhs_count;
+  uint64_t seed;
+} pmmf_b200_solve_config;
+
+/* ---- factorization: pmmf::factorize (factorizer.hpp:397-595) -------- */
+
+/* Runs the stage loop on the GPU given by a->device.  *out receives an
+ * opaque result handle (free with pmmf_b200_result_free). */
+int pmmf_b200_factorize(const pmmf_b200_coo* a, const pmmf_b200_params* p, void** out,
+                        char* err, size_t errlen);
+
+/* MmfFactorization scalars. */
+int pmmf_b200_result_summary(void* h, pmmf_b200_summary* out);
+/* f.active_history (factorizer.hpp:116): n_stages + 1 entries. */
+int pmmf_b200_result_active_history(void* h, int64_t* out);
+/* f.stages[s] sizes and contents.  Rotations are cluster-major
+ * (factorizer.hpp:67): rot_indices is n_rotations x k, rot_matrices is
+ * n_rotations x k x k row-major.  Eliminations in stage order (:68). */
+int pmmf_b200_result_stage_sizes(void* h, int64_t s, pmmf_b200_stage_sizes* out);
+int pmmf_b200_result_stage(void* h, int64_t s, int64_t* cluster_offsets, int64_t* members,
+                           int64_t* rot_indices, double* rot_matrices, int64_t* elim_index,
+                           double* elim_diagonal, double* elim_off_mass_sq, int64_t* bypassed);
+/* f.h (CoreDiagonal, factorizer.hpp:72-84): core_indices ascending,
+ * core g x g row-major, retired diagonal ascending by index. */
+int pmmf_b200_result_core(void* h, int64_t* core_indices, double* core, int64_t* diag_index,
+                          double* diag_value);
+/* FactorizeStats (factorizer.hpp:86-109): phases = {clustering, gram,
+ * rotations, apply, reblocking, total} in ms; stage_info is n_stages x 7
+ * {stage, clusters, bypassed, rotations, eliminated, active_after, depth}. */
+int pmmf_b200_result_stats(void* h, double* phases, int64_t* stage_info);
+void pmmf_b200_result_free(void* h);
+
+/* ---- MmfOperator (transform_ops.hpp:30-137) ------------------------- */
+
+enum { PMMF_APPLY_FORWARD = 0, PMMF_APPLY_INVERSE = 1, PMMF_APPLY_INV_SQRT = 2 };
+
+/* Builds the operator for a factorization (core eigensystem,
+ * transform_ops.hpp:34-41).  The result handle may be freed afterwards. */
+int pmmf_b200_operator_create(void* result, double zero_threshold, void** op, char* err,
+                              size_t errlen);
+/* out = Q^T H^(mode) Q in for nrhs vectors (transform_ops.hpp:51-67).
+ * in/out are host pointers unless on_device != 0. */
+int pmmf_b200_operator_apply(void* op, int32_t mode, int64_t nrhs, const double* in,
+                             double* out, int32_t on_device, char* err, size_t errlen);
+/* inv_sqrt_zeroed_negatives() (transform_ops.hpp:47-49). */
+int pmmf_b200_operator_zeroed_negatives(void* op, int64_t* out);
+void pmmf_b200_operator_free(void* op);
+
+/* ---- solver: run_solve_experiment (solver.hpp:368-416) -------------- */
+
+/* Split-preconditioned CG (pcg_symmetric, solver.hpp:112-167) with
+ * K^-1 = K^-T = op->apply(inv_sqrt) (pmmf_preconditioner, :343-349), or
+ * plain CG when op == NULL (solver.hpp:170-).  All rhs_count right-hand
+ * sides are solved together.  Outputs: iterations/converged/breakdown per
+ * rhs; residuals is rhs_count x (max_iter + 1), residuals[r][it] =
+ * ||b - A x_it|| (NaN past the end of run r); wall_ms = total. */
+int pmmf_b200_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_config* cfg,
+                    int32_t* iterations, int32_t* converged, int32_t* breakdown, double* residuals,
+                    double* wall_ms, char* err, size_t errlen);
+
+/* ---- misc ----------------------------------------------------------- */
+
+/* rotation_from_gram (factorizer.hpp:150-171) on one k x k row-major
+ * block; host-side helper used for the known-answer tests. */
+int pmmf_b200_rotation_from_gram(int32_t k, const double* g, double* q, char* err, size_t errlen);
+
+/* Number of CUDA kernels this library launched since load (evidence for
+ * bench.py's gpu_launches).  Counts every launch site in csrc/. */
+int64_t pmmf_b200_kernel_launches(void);
+
+/* Library version string. */
+const char* pmmf_b200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PMMF_B200_H */
