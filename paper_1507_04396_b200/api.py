@@ -1,0 +1,244 @@
+"""Python mirror of the reference's public interface for the stage-loop path.
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/pmmf:
+  * ``ClusterParams`` / ``FactorizeParams``  (clustering.hpp:28-41, factorizer.hpp:35-51)
+  * ``Partition``                           (partition.hpp:19-93)
+  * ``BlockedSparseMatrix.from_triplets``   (blocked_matrix.hpp:133-156)
+  * ``factorize``                           (factorizer.hpp:397-595)
+  * ``MmfOperator`` / ``apply*``            (transform_ops.hpp:30-153)
+  * ``run_solve_experiment``                (solver.hpp:368-416)
+Everything executes in ``libpmmf_b200.so`` (hand-written sm_100a kernels);
+there is no CPU fallback: a missing library or device raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmmf_b200.so")
+
+_ABI: Optional[abi.FlatAbi] = None
+
+
+def library() -> abi.FlatAbi:
+    """Loads libpmmf_b200.so (fails loudly when it has not been built)."""
+    global _ABI
+    if _ABI is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libpmmf_b200.so is not built ({LIB_PATH}); run __graft_entry__.build()")
+        _ABI = abi.FlatAbi(LIB_PATH, "pmmf_b200_")
+        L = _ABI.lib
+        L.pmmf_b200_kernel_launches.restype = ctypes.c_int64
+        L.pmmf_b200_version.restype = ctypes.c_char_p
+        for name in ("rmat", "dense_spd", "rbf", "aniso_grid"):
+            getattr(L, "pmmf_b200_workload_" + name).restype = ctypes.c_int
+        L.pmmf_b200_workload_free.argtypes = [ctypes.POINTER(abi.Workload)]
+    return _ABI
+
+
+def kernel_launches() -> int:
+    return int(library().lib.pmmf_b200_kernel_launches())
+
+
+# ------------------------------------------------------------------ params
+@dataclass
+class ClusterParams:
+    m_target: int = 2
+    c_min: int = 10
+    c_max: int = 5000
+    d_max: int = 500
+    bypass_enabled: bool = True
+    seed: int = 0
+
+
+@dataclass
+class FactorizeParams:
+    k: int = 2
+    n_stages: int = 15
+    eta: float = 0.5
+    cluster: ClusterParams = field(default_factory=ClusterParams)
+    core_min: int = 10
+    core_cap: int = 4096
+    seed: int = 0
+
+    def to_c(self) -> abi.Params:
+        c = self.cluster
+        return abi.make_params(
+            k=self.k,
+            n_stages=self.n_stages,
+            eta=self.eta,
+            m_target=c.m_target,
+            c_min=c.c_min,
+            c_max=c.c_max,
+            d_max=c.d_max,
+            bypass_enabled=c.bypass_enabled,
+            core_min=self.core_min,
+            core_cap=self.core_cap,
+            seed=self.seed,
+            cluster_seed=c.seed,
+        )
+
+
+# --------------------------------------------------------------- matrices
+class Partition:
+    """Ordered clusters of global ids (partition.hpp:19-93)."""
+
+    def __init__(self, clusters: Sequence[Sequence[int]]):
+        self.clusters = [np.asarray(c, np.int64) for c in clusters]
+
+    @staticmethod
+    def trivial(n: int) -> "Partition":
+        return Partition([np.arange(n, dtype=np.int64)])
+
+    @staticmethod
+    def single(indices) -> "Partition":
+        return Partition([indices])
+
+    def num_clusters(self) -> int:
+        return len(self.clusters)
+
+    def size(self) -> int:
+        return int(sum(len(c) for c in self.clusters))
+
+    def cluster(self, u: int) -> np.ndarray:
+        return self.clusters[u]
+
+
+class BlockedSparseMatrix:
+    """Coordinate data + partition handed to the device as-is.
+
+    ``from_triplets`` keeps the reference semantics (duplicates summed in
+    input order, range / finiteness / coverage checks); the checks run on the
+    device when ``factorize`` is called.  ``rows/cols/vals`` may be host
+    numpy arrays or CUDA torch tensors (device-resident input)."""
+
+    def __init__(self, n: int, rows, cols, vals, partition: Optional[Partition] = None):
+        self.n = int(n)
+        self.rows, self.cols, self.vals = rows, cols, vals
+        self.partition = partition
+
+    @staticmethod
+    def from_triplets(n: int, rows, cols, vals, partition: Optional[Partition] = None) -> "BlockedSparseMatrix":
+        return BlockedSparseMatrix(n, rows, cols, vals, partition)
+
+    @property
+    def on_device(self) -> bool:
+        return hasattr(self.rows, "data_ptr")
+
+    def coo(self, device: int = 0):
+        clusters = None
+        if self.partition is not None:
+            clusters = self.partition.clusters
+        return abi.make_coo(self.n, self.rows, self.cols, self.vals, clusters, on_device=self.on_device, device=device)
+
+
+# ----------------------------------------------------------- factorization
+@dataclass
+class Rotation:
+    indices: np.ndarray
+    matrix: np.ndarray
+    stage: int
+
+
+class MmfFactorization(abi.FlatFactorization):
+    """``MmfFactorization`` (factorizer.hpp:111-118) in flat arrays, with the
+    reference-style accessors on top."""
+
+    def rotations(self, stage: int) -> List[Rotation]:
+        st = self.stages[stage]
+        return [Rotation(st.rot_indices[t], st.rot_matrices[t], stage + 1) for t in range(len(st.rot_indices))]
+
+    def diagonal_value(self, i: int) -> float:
+        pos = np.searchsorted(self.diag_index, i)
+        if pos >= len(self.diag_index) or self.diag_index[pos] != i:
+            raise IndexError("CoreDiagonal: index not retired")
+        return float(self.diag_value[pos])
+
+
+def factorize(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int = 0) -> MmfFactorization:
+    """pmmf::factorize on the GPU (factorizer.hpp:397-595)."""
+    lib = library()
+    coo, keep = matrix.coo(device)
+    p = params.to_c()
+    h = ctypes.c_void_p()
+    err = lib.errbuf()
+    abi.raise_for(lib.factorize(ctypes.byref(coo), ctypes.byref(p), ctypes.byref(h), err, len(err)), err)
+    try:
+        flat = lib.read_result(h)
+    finally:
+        lib.result_free(h)
+    out = MmfFactorization.__new__(MmfFactorization)
+    out.__dict__.update(flat.__dict__)
+    out.params = params
+    return out
+
+
+def factorize_handle(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int = 0) -> ctypes.c_void_p:
+    """Raw result handle (caller frees with library().result_free)."""
+    lib = library()
+    coo, keep = matrix.coo(device)
+    p = params.to_c()
+    h = ctypes.c_void_p()
+    err = lib.errbuf()
+    abi.raise_for(lib.factorize(ctypes.byref(coo), ctypes.byref(p), ctypes.byref(h), err, len(err)), err)
+    return h
+
+
+# -------------------------------------------------------------- workloads
+def _take(w: abi.Workload):
+    m = w.nnz
+    if m:
+        rows = np.ctypeslib.as_array(w.rows, (m,)).copy()
+        cols = np.ctypeslib.as_array(w.cols, (m,)).copy()
+        vals = np.ctypeslib.as_array(w.vals, (m,)).copy()
+    else:
+        rows = np.zeros(0, np.int64)
+        cols = np.zeros(0, np.int64)
+        vals = np.zeros(0, np.float64)
+    n = w.n
+    library().lib.pmmf_b200_workload_free(ctypes.byref(w))
+    return n, rows, cols, vals
+
+
+def workload_rmat(scale: int, edges_per_vertex: int, seed: int = 42, shift: float = 1e-2):
+    w = abi.Workload()
+    rc = library().lib.pmmf_b200_workload_rmat(
+        ctypes.c_int32(scale), ctypes.c_int32(edges_per_vertex), ctypes.c_uint64(seed), ctypes.c_double(shift), ctypes.byref(w)
+    )
+    if rc:
+        raise ValueError("workload_rmat: bad arguments")
+    return _take(w)
+
+
+def workload_dense_spd(n: int, d: int, seed: int = 42, shift: float = 1e-3):
+    w = abi.Workload()
+    rc = library().lib.pmmf_b200_workload_dense_spd(ctypes.c_int64(n), ctypes.c_int64(d), ctypes.c_uint64(seed), ctypes.c_double(shift), ctypes.byref(w))
+    if rc:
+        raise ValueError("workload_dense_spd: bad arguments")
+    return _take(w)
+
+
+def workload_rbf(n: int, dim: int = 10, bandwidth: float = 0.5, seed: int = 42, shift: float = 1e-4):
+    w = abi.Workload()
+    rc = library().lib.pmmf_b200_workload_rbf(
+        ctypes.c_int64(n), ctypes.c_int32(dim), ctypes.c_double(bandwidth), ctypes.c_uint64(seed), ctypes.c_double(shift), ctypes.byref(w)
+    )
+    if rc:
+        raise ValueError("workload_rbf: bad arguments")
+    return _take(w)
+
+
+def workload_aniso_grid(side: int, ax: float = 100.0, ay: float = 1.0):
+    w = abi.Workload()
+    rc = library().lib.pmmf_b200_workload_aniso_grid(ctypes.c_int64(side), ctypes.c_double(ax), ctypes.c_double(ay), ctypes.byref(w))
+    if rc:
+        raise ValueError("workload_aniso_grid: bad arguments")
+    return _take(w)

@@ -1,0 +1,142 @@
+// abi.cu — the C-ABI of include/pmmf_b200.h: status mapping, the
+// factorization entry point and the MmfFactorization accessors.
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "result.cuh"
+#include "rotation.cuh"
+
+using namespace pmmf_b200;
+
+namespace {
+
+void set_err(char* err, size_t n, const std::string& m) {
+  if (!err || !n) return;
+  const size_t k = std::min(n - 1, m.size());
+  std::memcpy(err, m.data(), k);
+  err[k] = '\0';
+}
+
+}  // namespace
+
+namespace pmmf_b200 {
+int guarded_call(char* err, size_t errlen, void (*fn)(void*), void* ctx) {
+  try {
+    fn(ctx);
+    return PMMF_OK;
+  } catch (const Error& e) {
+    set_err(err, errlen, e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_err(err, errlen, "host allocation failed");
+    return PMMF_INTERNAL;
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return PMMF_INTERNAL;
+  }
+}
+}  // namespace pmmf_b200
+
+template <typename F>
+static int guarded(char* err, size_t errlen, F&& f) {
+  return guarded_call(err, errlen, [](void* c) { (*static_cast<F*>(c))(); }, &f);
+}
+
+extern "C" {
+
+int pmmf_b200_factorize(const pmmf_b200_coo* a, const pmmf_b200_params* p, void** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!a || !p || !out) fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_factorize: null argument");
+    *out = factorize_device(a, *p).release();
+  });
+}
+
+int pmmf_b200_result_summary(void* h, pmmf_b200_summary* o) {
+  auto* r = static_cast<Result*>(h);
+  o->n = r->n;
+  o->n_stages = static_cast<int64_t>(r->stages.size());
+  o->k = r->k;
+  o->core_size = static_cast<int64_t>(r->core_idx.size());
+  o->n_diagonal = static_cast<int64_t>(r->diag.size());
+  o->trivial = r->trivial;
+  o->residual_sq = r->residual_sq;
+  return PMMF_OK;
+}
+
+int pmmf_b200_result_active_history(void* h, int64_t* o) {
+  auto* r = static_cast<Result*>(h);
+  std::copy(r->hist.begin(), r->hist.end(), o);
+  return PMMF_OK;
+}
+
+int pmmf_b200_result_stage_sizes(void* h, int64_t s, pmmf_b200_stage_sizes* o) {
+  auto* r = static_cast<Result*>(h);
+  if (s < 0 || s >= static_cast<int64_t>(r->stages.size())) return PMMF_OUT_OF_RANGE;
+  const auto& st = r->stages[s];
+  o->n_clusters = static_cast<int64_t>(st.off.size()) - 1;
+  o->partition_size = static_cast<int64_t>(st.members.size());
+  o->n_rotations = static_cast<int64_t>(st.rot_idx.size()) / r->k;
+  o->n_eliminated = static_cast<int64_t>(st.elim_idx.size());
+  o->n_bypassed = static_cast<int64_t>(st.bypassed.size());
+  return PMMF_OK;
+}
+
+int pmmf_b200_result_stage(void* h, int64_t s, int64_t* offs, int64_t* mem, int64_t* ri, double* rq, int64_t* ei,
+                           double* ed, double* em, int64_t* by) {
+  auto* r = static_cast<Result*>(h);
+  if (s < 0 || s >= static_cast<int64_t>(r->stages.size())) return PMMF_OUT_OF_RANGE;
+  const auto& st = r->stages[s];
+  std::copy(st.off.begin(), st.off.end(), offs);
+  std::copy(st.members.begin(), st.members.end(), mem);
+  std::copy(st.rot_idx.begin(), st.rot_idx.end(), ri);
+  std::copy(st.rot_q.begin(), st.rot_q.end(), rq);
+  std::copy(st.elim_idx.begin(), st.elim_idx.end(), ei);
+  std::copy(st.elim_diag.begin(), st.elim_diag.end(), ed);
+  std::copy(st.elim_mass.begin(), st.elim_mass.end(), em);
+  std::copy(st.bypassed.begin(), st.bypassed.end(), by);
+  return PMMF_OK;
+}
+
+int pmmf_b200_result_core(void* h, int64_t* ci, double* core, int64_t* di, double* dv) {
+  auto* r = static_cast<Result*>(h);
+  std::copy(r->core_idx.begin(), r->core_idx.end(), ci);
+  std::copy(r->core.begin(), r->core.end(), core);
+  for (size_t i = 0; i < r->diag.size(); ++i) {
+    di[i] = r->diag[i].first;
+    dv[i] = r->diag[i].second;
+  }
+  return PMMF_OK;
+}
+
+int pmmf_b200_result_stats(void* h, double* phases, int64_t* info) {
+  auto* r = static_cast<Result*>(h);
+  std::copy(r->phases, r->phases + 6, phases);
+  for (size_t s = 0; s < r->info.size(); ++s) std::copy(r->info[s].begin(), r->info[s].end(), info + 7 * s);
+  return PMMF_OK;
+}
+
+void pmmf_b200_result_free(void* h) { delete static_cast<Result*>(h); }
+
+int pmmf_b200_rotation_from_gram(int32_t k, const double* g, double* q, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (k < 1 || k > kMaxK) fail(PMMF_INVALID_ARGUMENT, "rotation_from_gram: not square");
+    double gs[kMaxK][kMaxK], qs[kMaxK][kMaxK];
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) gs[a][b] = g[a * k + b];
+    if (k == 1) {
+      qs[0][0] = 1.0;
+    } else if (!rotation_from_gram(gs, k, qs)) {
+      fail(PMMF_INVALID_ARGUMENT, "rotation_from_gram: input not symmetric");
+    }
+    for (int a = 0; a < k; ++a)
+      for (int b = 0; b < k; ++b) q[a * k + b] = qs[a][b];
+  });
+}
+
+int64_t pmmf_b200_kernel_launches(void) { return launch_counter().load(); }
+
+const char* pmmf_b200_version(void) { return "pmmf_b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,437 @@
+// cluster.cu — randomized anchor clustering (clustering.hpp:85-225) with the
+// data-parallel parts on the device:
+//   * column norms, summed per block row of the PRE-reblock matrix then over
+//     blocks (blocked_matrix.hpp:203-209),
+//   * normalized scores |<A_j,A_a>| / (|A_j| |A_a|) of every pool column
+//     against the m anchors and the strict-> argmax with ties to the lowest
+//     anchor (clustering.hpp:62-83, P3/P4).  A warp owns a column; the
+//     anchors are inverted into a row -> (anchor, value) index, so the work
+//     is sum over the column's entries of the anchors sharing that row
+//     (a sparse 2-hop gather), and each (column, anchor) dot keeps the
+//     reference's two-level summation order exactly.
+// The control flow that consumes the RNG stream (anchor draws, round-robin,
+// undersize repair, oversize recursion) runs on the host, as in the
+// reference, over device-computed scores.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+
+#include "engine.cuh"
+#include "rng.cuh"
+
+namespace pmmf_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// Two-level column norm (thread per column; columns listed by stage id).
+__global__ void k_norms(i64 P, const int32_t* __restrict__ cols, const i64* __restrict__ ptr,
+                        const int32_t* __restrict__ row, const double* __restrict__ val,
+                        const int32_t* __restrict__ blk, double* __restrict__ norm) {
+  const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (p >= P) return;
+  const int32_t j = cols[p];
+  double s = 0.0, inner = 0.0;
+  int32_t cur = -1;
+  for (i64 e = ptr[j]; e < ptr[j + 1]; ++e) {
+    const int32_t b = blk[row[e]];
+    if (b != cur) {
+      if (cur >= 0) s = dadd(s, inner);
+      inner = 0.0;
+      cur = b;
+    }
+    const double v = val[e];
+    inner = dadd(inner, dmul(v, v));
+  }
+  if (cur >= 0) s = dadd(s, inner);
+  norm[p] = sqrt(s);
+}
+
+// Row -> anchor index: count, then scatter (order inside a row is free:
+// each anchor appears at most once per row).
+__global__ void k_anchor_count(int m, const int32_t* __restrict__ anchors, const i64* __restrict__ ptr,
+                               const int32_t* __restrict__ row, int32_t* __restrict__ cnt) {
+  const int a = blockIdx.x;
+  const int32_t j = anchors[a];
+  for (i64 e = ptr[j] + threadIdx.x; e < ptr[j + 1]; e += blockDim.x) atomicAdd(&cnt[row[e]], 1);
+}
+__global__ void k_anchor_scatter(int m, const int32_t* __restrict__ anchors, const i64* __restrict__ ptr,
+                                 const int32_t* __restrict__ row, const double* __restrict__ val,
+                                 const i64* __restrict__ rptr, int32_t* __restrict__ cursor,
+                                 int32_t* __restrict__ ent_a, double* __restrict__ ent_v) {
+  const int a = blockIdx.x;
+  const int32_t j = anchors[a];
+  for (i64 e = ptr[j] + threadIdx.x; e < ptr[j + 1]; e += blockDim.x) {
+    const int32_t r = row[e];
+    const i64 pos = rptr[r] + atomicAdd(&cursor[r], 1);
+    ent_a[pos] = a;
+    ent_v[pos] = val[e];
+  }
+}
+__global__ void k_widen(i64 N, const int32_t* __restrict__ in, i64* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < N) out[i] = in[i];
+  if (i == N) out[i] = 0;
+}
+
+struct ScoreArgs {
+  i64 P;
+  const int32_t* cols;    // pool columns (stage ids)
+  const double* cnorm;    // their norms
+  int m;
+  const double* anorm;    // anchor norms
+  const int32_t* self;    // stage id -> anchor position or -1 (assignment mode)
+  const i64* ptr;
+  const int32_t* row;
+  const double* val;
+  const int32_t* blk;
+  const i64* arptr;       // row -> anchor entries
+  const int32_t* ent_a;
+  const double* ent_v;
+  int32_t* assign;        // assignment mode: best anchor or -1
+  double* rows;           // rows mode: P x m scores (nullptr in assignment mode)
+  double* g_scratch;      // per-warp state when shared memory is too small
+};
+
+__device__ __forceinline__ bool better(double s, int a, double bs, int ba) {
+  return s > bs || (s == bs && a < ba);
+}
+
+// Warp per pool column.  Per-warp state (m anchors): block partial p, total
+// t, last block seen, plus a touched list.
+__global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
+  extern __shared__ unsigned char smem[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 warp = blockIdx.x * static_cast<i64>(warps_per_block) + wib;
+  const int m = A.m;
+  const size_t stride = static_cast<size_t>(m) * 24 + 16;
+  unsigned char* base = use_smem ? smem + stride * wib
+                                 : reinterpret_cast<unsigned char*>(A.g_scratch) + stride * static_cast<size_t>(warp);
+  double* p = reinterpret_cast<double*>(base);
+  double* t = p + m;
+  int32_t* last = reinterpret_cast<int32_t*>(t + m);
+  int32_t* touched = last + m;
+  int32_t* ntouched = touched + m;
+  if (warp >= A.P) return;
+  for (int a = lane; a < m; a += 32) {
+    p[a] = 0.0;
+    t[a] = 0.0;
+    last[a] = -1;
+  }
+  if (lane == 0) *ntouched = 0;
+  __syncwarp();
+  const int32_t j = A.cols[warp];
+  if (A.rows == nullptr && A.self[j] >= 0) {
+    if (lane == 0) A.assign[warp] = A.self[j];
+    return;
+  }
+  const i64 e0 = A.ptr[j], e1 = A.ptr[j + 1];
+  for (i64 base_e = e0; base_e < e1; base_e += 32) {
+    const i64 e = base_e + lane;
+    double v = 0.0;
+    int32_t b = 0;
+    i64 beg = 0, end = 0;
+    if (e < e1) {
+      const int32_t r = A.row[e];
+      v = A.val[e];
+      b = A.blk[r];
+      beg = A.arptr[r];
+      end = A.arptr[r + 1];
+    }
+    unsigned hits = __ballot_sync(0xffffffffu, end > beg);
+    while (hits) {
+      const int src = __ffs(hits) - 1;
+      hits &= hits - 1;
+      const double vs = __shfl_sync(0xffffffffu, v, src);
+      const int32_t bs = __shfl_sync(0xffffffffu, b, src);
+      const i64 bg = __shfl_sync(0xffffffffu, beg, src);
+      const i64 en = __shfl_sync(0xffffffffu, end, src);
+      for (i64 q = bg + lane; q < en; q += 32) {
+        const int32_t a = A.ent_a[q];
+        const double prod = dmul(vs, A.ent_v[q]);
+        if (last[a] != bs) {
+          if (last[a] < 0) {
+            touched[atomicAdd(ntouched, 1)] = a;
+          } else {
+            t[a] = dadd(t[a], p[a]);
+          }
+          p[a] = 0.0;
+          last[a] = bs;
+        }
+        p[a] = dadd(p[a], prod);
+      }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  const int nt = *ntouched;
+  const double nj = A.cnorm[warp];
+  double best = 0.0;
+  int ba = 0x7fffffff;
+  for (int i = lane; i < nt; i += 32) {
+    const int a = touched[i];
+    const double dot = dadd(t[a], p[a]);
+    const double na = A.anorm[a];
+    double s = 0.0;
+    if (nj > 0.0 && na > 0.0) s = fabs(dot) / dmul(nj, na);
+    if (A.rows) A.rows[static_cast<size_t>(warp) * m + a] = s;
+    if (s > 0.0 && better(s, a, best, ba)) {
+      best = s;
+      ba = a;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double os = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, ba, o);
+    if (better(os, oa, best, ba)) {
+      best = os;
+      ba = oa;
+    }
+  }
+  if (lane == 0 && A.rows == nullptr) A.assign[warp] = best > 0.0 ? ba : -1;
+}
+
+struct Scorer {
+  const Csc& a;
+  const Numbering& nb;
+  cudaStream_t s;
+  DBuf<int32_t> self;  // stage id -> anchor pos (assignment mode)
+
+  Scorer(const Csc& mat, const Numbering& numbering, cudaStream_t st) : a(mat), nb(numbering), s(st) {
+    self.alloc(std::max<i64>(a.N, 1), s);
+    self.fill_bytes(0xff);
+  }
+
+  // Scores of `pool` (stage ids) against `anchors` (stage ids, ascending
+  // global).  Assignment mode returns best anchor or -1 per pool column;
+  // rows mode returns the full P x m score table.
+  void run(const std::vector<int32_t>& pool, const std::vector<double>& pool_norm,
+           const std::vector<int32_t>& anchors, const std::vector<double>& anchor_norm, bool rows_mode,
+           std::vector<int32_t>* assign, std::vector<double>* rows) {
+    const i64 P = static_cast<i64>(pool.size());
+    const int m = static_cast<int>(anchors.size());
+    if (P == 0) return;
+    DBuf<int32_t> dpool(P, s), danch(m, s);
+    DBuf<double> dpn(P, s), dan(m, s);
+    dpool.upload(pool);
+    dpn.upload(pool_norm);
+    danch.upload(anchors);
+    dan.upload(anchor_norm);
+    // row -> anchor index
+    DBuf<int32_t> cnt(a.N + 1, s), cursor(a.N + 1, s);
+    cnt.zero();
+    cursor.zero();
+    PMMF_LAUNCH(k_anchor_count, static_cast<unsigned>(m), 128, 0, s, m, danch.get(), a.ptr.get(), a.row.get(), cnt.get());
+    DBuf<i64> cnt64(a.N + 1, s), rptr(a.N + 1, s);
+    PMMF_LAUNCH(k_widen, blocks_for(a.N + 1, kThreads), kThreads, 0, s, a.N, cnt.get(), cnt64.get());
+    {
+      size_t tmp = 0;
+      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt64.get(), rptr.get(), static_cast<int64_t>(a.N + 1), s));
+      DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, cnt64.get(), rptr.get(), static_cast<int64_t>(a.N + 1), s));
+    }
+    i64 total = 0;
+    PMMF_CUDA(cudaMemcpyAsync(&total, rptr.get() + a.N, sizeof(i64), cudaMemcpyDeviceToHost, s));
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    DBuf<int32_t> ent_a(std::max<i64>(total, 1), s);
+    DBuf<double> ent_v(std::max<i64>(total, 1), s);
+    PMMF_LAUNCH(k_anchor_scatter, static_cast<unsigned>(m), 128, 0, s, m, danch.get(), a.ptr.get(), a.row.get(),
+                a.val.get(), rptr.get(), cursor.get(), ent_a.get(), ent_v.get());
+    if (!rows_mode) {
+      std::vector<int32_t> pos(static_cast<size_t>(m));
+      std::iota(pos.begin(), pos.end(), 0);
+      // mark anchors (self-assignment, clustering.hpp:118-122)
+      DBuf<int32_t> dpos(m, s);
+      dpos.upload(pos);
+      set_self(danch, dpos, m, true);
+    }
+    const size_t stride = static_cast<size_t>(m) * 24 + 16;
+    int wpb = static_cast<int>(std::min<size_t>(8, (96 * 1024) / stride));
+    const bool use_smem = wpb >= 1;
+    if (!use_smem) wpb = 4;
+    DBuf<double> scratch;
+    if (!use_smem) scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(P) + 7) / 8), s);
+    DBuf<int32_t> dassign(P, s);
+    DBuf<double> drows;
+    if (rows_mode) {
+      drows.alloc(P * m, s);
+      drows.zero();
+    }
+    ScoreArgs args{P,           dpool.get(), dpn.get(),        m,           dan.get(),   self.get(),
+                   a.ptr.get(), a.row.get(), a.val.get(),      nb.d_blk.get(), rptr.get(), ent_a.get(),
+                   ent_v.get(), dassign.get(), rows_mode ? drows.get() : nullptr, scratch.get()};
+    const size_t smem = use_smem ? stride * static_cast<size_t>(wpb) : 0;
+    if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    PMMF_LAUNCH(k_score, static_cast<unsigned>((P + wpb - 1) / wpb), 32 * wpb, smem, s, args, wpb, use_smem);
+    if (!rows_mode) {
+      set_self(danch, danch, m, false);
+      *assign = dassign.to_host(P);
+    } else {
+      *rows = drows.to_host(P * m);
+    }
+  }
+
+  void set_self(const DBuf<int32_t>& anchors, const DBuf<int32_t>& pos, int m, bool on);
+};
+
+__global__ void k_set_self(int m, const int32_t* __restrict__ anchors, const int32_t* __restrict__ pos, bool on,
+                           int32_t* __restrict__ self) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < m) self[anchors[a]] = on ? pos[a] : -1;
+}
+
+void Scorer::set_self(const DBuf<int32_t>& anchors, const DBuf<int32_t>& pos, int m, bool on) {
+  PMMF_LAUNCH(k_set_self, blocks_for(m, kThreads), kThreads, 0, s, m, anchors.get(), pos.get(), on, self.get());
+}
+
+struct Ctx {
+  Scorer* sc;
+  const Numbering* nb;
+  const std::vector<double>* norm;  // by global id
+  i64 c_min, c_max;
+  int d_max;
+  int max_depth = 0;
+};
+
+void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro& rng,
+             std::vector<std::vector<i64>>& out) {  // clustering.hpp:85-177
+  ctx.max_depth = std::max(ctx.max_depth, depth);
+  if (pool.empty()) return;
+  const auto& norm = *ctx.norm;
+  std::vector<i64> shuffled;
+  shuffled.reserve(pool.size());
+  for (i64 g : pool)
+    if (norm[g] > 0.0) shuffled.push_back(g);
+  if (shuffled.empty()) {
+    out.push_back(std::move(pool));
+    return;
+  }
+  const size_t m = static_cast<size_t>(std::min<i64>(m_request, static_cast<i64>(shuffled.size())));
+  for (size_t t = 0; t < m; ++t) std::swap(shuffled[t], shuffled[t + rng.uniform_below(shuffled.size() - t)]);
+  std::vector<i64> anchors(shuffled.begin(), shuffled.begin() + static_cast<std::ptrdiff_t>(m));
+  std::sort(anchors.begin(), anchors.end());
+
+  const auto& g2s = ctx.nb->g2s;
+  std::vector<int32_t> dpool(pool.size()), danch(m);
+  std::vector<double> pn(pool.size()), an(m);
+  for (size_t i = 0; i < pool.size(); ++i) {
+    dpool[i] = static_cast<int32_t>(g2s[pool[i]]);
+    pn[i] = norm[pool[i]];
+  }
+  for (size_t a = 0; a < m; ++a) {
+    danch[a] = static_cast<int32_t>(g2s[anchors[a]]);
+    an[a] = norm[anchors[a]];
+  }
+  std::vector<int32_t> assign;
+  ctx.sc->run(dpool, pn, danch, an, false, &assign, nullptr);
+
+  std::vector<std::vector<i64>> clusters(m);
+  std::vector<size_t> owner(pool.size());
+  size_t rr = 0;
+  for (size_t p = 0; p < pool.size(); ++p) {
+    size_t a = assign[p] >= 0 ? static_cast<size_t>(assign[p]) : (rr++) % m;
+    clusters[a].push_back(pool[p]);
+    owner[p] = a;
+  }
+
+  // Undersize repair (clustering.hpp:138-163).  Orphans are always members
+  // of clusters that started below c_min (clusters only grow), so their
+  // scores against every anchor are computed once, up front.
+  std::vector<size_t> alive(m);
+  std::iota(alive.begin(), alive.end(), size_t{0});
+  std::vector<int64_t> cand_row(pool.size(), -1);
+  std::vector<double> table;
+  {
+    std::vector<int32_t> cand;
+    std::vector<double> cn;
+    for (size_t p = 0; p < pool.size(); ++p)
+      if (static_cast<i64>(clusters[owner[p]].size()) < ctx.c_min && m > 1) {
+        cand_row[p] = static_cast<int64_t>(cand.size());
+        cand.push_back(dpool[p]);
+        cn.push_back(pn[p]);
+      }
+    if (!cand.empty()) ctx.sc->run(cand, cn, danch, an, true, nullptr, &table);
+  }
+  std::vector<int64_t> pos_of;  // global -> pool position, for orphans
+  auto pool_pos = [&](i64 g) {
+    return static_cast<size_t>(std::lower_bound(pool.begin(), pool.end(), g) - pool.begin());
+  };
+  while (alive.size() > 1) {
+    size_t worst = alive[0];
+    for (size_t a : alive)
+      if (clusters[a].size() < clusters[worst].size()) worst = a;
+    if (static_cast<i64>(clusters[worst].size()) >= ctx.c_min) break;
+    alive.erase(std::find(alive.begin(), alive.end(), worst));
+    std::vector<i64> orphans = std::move(clusters[worst]);
+    clusters[worst].clear();
+    size_t orr = 0;
+    for (i64 o : orphans) {
+      const int64_t row = cand_row[pool_pos(o)];
+      if (row < 0) fail(PMMF_INTERNAL, "clustering: orphan without a precomputed score row");
+      const double* sr = table.data() + static_cast<size_t>(row) * m;
+      size_t best = 0;
+      double bs = 0.0;
+      for (size_t i = 0; i < alive.size(); ++i) {
+        const double s = sr[alive[i]];
+        if (s > bs) {
+          bs = s;
+          best = i;
+        }
+      }
+      const size_t a = bs > 0.0 ? best : (orr++) % alive.size();
+      clusters[alive[a]].push_back(o);
+    }
+    for (size_t a : alive) std::sort(clusters[a].begin(), clusters[a].end());
+  }
+  for (size_t a : alive) {  // oversize recursion (clustering.hpp:165-176)
+    auto& mem = clusters[a];
+    if (mem.empty()) continue;
+    if (static_cast<i64>(mem.size()) > ctx.c_max && depth < ctx.d_max) {
+      const i64 sub = (static_cast<i64>(mem.size()) + ctx.c_max - 1) / ctx.c_max;
+      recurse(ctx, std::move(mem), sub, depth + 1, rng, out);
+    } else {
+      out.push_back(std::move(mem));
+    }
+  }
+}
+
+}  // namespace
+
+ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vector<i64>& active, i64 n,
+                               i64 m_target, i64 c_min, i64 c_max, int d_max, bool bypass, uint64_t seed,
+                               cudaStream_t s) {
+  if (active.empty()) fail(PMMF_INVALID_ARGUMENT, "cluster_columns: empty active set");
+  ClusterOut res;
+  // Norms of the active columns (clustering.hpp:189-195).
+  const i64 P = static_cast<i64>(active.size());
+  std::vector<int32_t> ids(static_cast<size_t>(P));
+  for (i64 i = 0; i < P; ++i) ids[i] = static_cast<int32_t>(nb.g2s[active[i]]);
+  DBuf<int32_t> dids(P, s);
+  dids.upload(ids);
+  DBuf<double> dnorm(P, s);
+  PMMF_LAUNCH(k_norms, blocks_for(P, kThreads), kThreads, 0, s, P, dids.get(), a.ptr.get(), a.row.get(), a.val.get(),
+              nb.d_blk.get(), dnorm.get());
+  std::vector<double> hn = dnorm.to_host(P);
+  std::vector<double> norm(static_cast<size_t>(n), 0.0);
+  std::vector<i64> pool;
+  pool.reserve(active.size());
+  for (i64 i = 0; i < P; ++i) {
+    norm[active[i]] = hn[i];
+    if (!bypass || hn[i] > 0.0) pool.push_back(active[i]);
+    else res.bypassed.push_back(active[i]);
+  }
+  if (!pool.empty()) {
+    Scorer sc(a, nb, s);
+    Ctx ctx{&sc, &nb, &norm, c_min, c_max, d_max};
+    Xoshiro rng(seed);
+    recurse(ctx, std::move(pool), m_target, 0, rng, res.clusters);
+    res.max_depth = ctx.max_depth;
+  }
+  std::sort(res.bypassed.begin(), res.bypassed.end());
+  return res;
+}
+
+}  // namespace pmmf_b200

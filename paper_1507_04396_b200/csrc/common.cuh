@@ -1,0 +1,122 @@
+// common.cuh — error model, device buffers and launch accounting shared by
+// every translation unit of libpmmf_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/pmmf_b200.h"
+
+namespace pmmf_b200 {
+
+using i64 = int64_t;
+
+// Mirrors the reference's exception taxonomy (types.hpp:24-32); the C-ABI
+// turns it into a pmmf_b200_status.
+struct Error {
+  int code;
+  std::string msg;
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error{code, m}; }
+
+#define PMMF_CUDA(call)                                                                     \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      ::pmmf_b200::fail(PMMF_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_) +     \
+                                       " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
+  } while (0)
+
+// Every kernel launch in csrc/ goes through PMMF_LAUNCH so the library can
+// report how many of its own kernels ran (bench.py "gpu_launches").
+std::atomic<int64_t>& launch_counter();
+#define PMMF_LAUNCH(kernel, grid, block, smem, stream, ...)                  \
+  do {                                                                       \
+    if ((grid) > 0) {                                                        \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
+      ::pmmf_b200::launch_counter().fetch_add(1, std::memory_order_relaxed); \
+      PMMF_CUDA(cudaGetLastError());                                         \
+    }                                                                        \
+  } while (0)
+
+// Stream-ordered device buffer (cudaMallocAsync from the device pool).
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  i64 n = 0;
+  cudaStream_t s = nullptr;
+  DBuf() = default;
+  DBuf(i64 count, cudaStream_t st) { alloc(count, st); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      s = o.s;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(i64 count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count > 0) PMMF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count), st));
+  }
+  void release() noexcept {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+  void zero() const {
+    if (n) PMMF_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * static_cast<size_t>(n), s));
+  }
+  void fill_bytes(int v) const {
+    if (n) PMMF_CUDA(cudaMemsetAsync(p, v, sizeof(T) * static_cast<size_t>(n), s));
+  }
+  void upload(const T* h, i64 count) const {
+    if (count) PMMF_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * static_cast<size_t>(count), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& h) const { upload(h.data(), static_cast<i64>(h.size())); }
+  void download(T* h, i64 count) const {
+    if (count) PMMF_CUDA(cudaMemcpyAsync(h, p, sizeof(T) * static_cast<size_t>(count), cudaMemcpyDeviceToHost, s));
+  }
+  std::vector<T> to_host(i64 count) const {
+    std::vector<T> h(static_cast<size_t>(count));
+    download(h.data(), count);
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    return h;
+  }
+};
+
+inline unsigned blocks_for(i64 n, int threads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+inline int bits_for(i64 x) {  // smallest b with 2^b > x (x >= 0)
+  int b = 0;
+  while (b < 63 && (i64{1} << b) <= x) ++b;
+  return b;
+}
+
+// Exact fp64 arithmetic without contraction: every product and sum rounds
+// separately, as the reference's x86-64 -O2 build does.
+#ifdef __CUDACC__
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+#endif
+
+}  // namespace pmmf_b200

@@ -1,0 +1,128 @@
+// engine.cuh — device data model of the stage loop and the host entry
+// points of each kernel family.
+//
+// Data layout in HBM:
+//   * "stage numbering": id = cluster offset + position in the cluster of
+//     the current stage Partition (partition.hpp:19-93).  Row and column ids
+//     share it, so block (u,v) of BlockedSparseMatrix (blocked_matrix.hpp:
+//     106-118) is the id rectangle [off_u,off_u+1) x [off_v,off_v+1).
+//   * Csc: contiguous column-compressed fp64 matrix over stage ids, int32
+//     rows sorted ascending inside a column, no stored zeros (value-neutral,
+//     SURVEY.md App. A P12).
+//   * Paged: the same matrix while rotations rewrite columns: per-column
+//     (offset,len) into an append-only arena.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pmmf_b200 {
+
+struct Csc {
+  i64 N = 0;    // ids
+  i64 nnz = 0;
+  DBuf<i64> ptr;     // N+1
+  DBuf<int32_t> row;
+  DBuf<double> val;
+};
+
+struct Paged {
+  i64 N = 0;
+  DBuf<i64> off;      // N
+  DBuf<int32_t> len;  // N
+  DBuf<int32_t> row;  // arena
+  DBuf<double> val;
+  i64 cap = 0;
+  DBuf<unsigned long long> cursor;  // 1: arena fill
+};
+
+// A stage numbering on the device plus its host mirror.
+struct Numbering {
+  std::vector<i64> s2g, off, g2s;  // host: stage->global, cluster offsets, global->stage (-1)
+  DBuf<int32_t> d_blk;             // stage id -> cluster (row block)
+  DBuf<int32_t> d_s2g;             // stage id -> global
+  i64 size() const { return static_cast<i64>(s2g.size()); }
+  i64 clusters() const { return static_cast<i64>(off.size()) - 1; }
+  void build(const std::vector<std::vector<i64>>& clusters, i64 n, cudaStream_t s);
+};
+
+// ---- matrix.cu
+// from_triplets (blocked_matrix.hpp:138-156) on the device: validates in
+// input order, stable-sorts by (col,row), sums duplicates in input order,
+// drops exact zeros.  rows/cols/vals are device pointers.
+void csc_from_coo(Csc& out, const Numbering& nb, i64 n, i64 nnz, const int64_t* rows, const int64_t* cols,
+                  const double* vals, cudaStream_t s);
+// max_asymmetry (blocked_matrix.hpp:447-463) and frobenius_norm_sq.
+void csc_symmetry(const Csc& a, const Numbering& nb, double* max_asym, double* fro_sq, cudaStream_t s);
+// Paged view of a contiguous matrix (takes ownership of its arrays).
+void paged_from_csc(Paged& p, Csc&& a, i64 extra_capacity, cudaStream_t s);
+// Transpose of a paged matrix into a contiguous one (stable row sort).
+void transpose_paged(Csc& out, const Paged& p, cudaStream_t s);
+// Reblock (blocked_matrix.hpp:318-367): ids of `from` relabelled through
+// map[old id] -> new id (-1 = dropped), columns gathered, rows re-sorted.
+void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_t>& new2old, i64 n_new,
+             cudaStream_t s);
+
+// ---- cluster.cu
+struct ClusterOut {
+  std::vector<std::vector<i64>> clusters;  // DFS order, members ascending global
+  std::vector<i64> bypassed;
+  int max_depth = 0;
+};
+// cluster_columns (clustering.hpp:183-225) over the pre-reblock matrix a
+// (numbering nb); active ascending global ids.
+ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vector<i64>& active, i64 n,
+                               i64 m_target, i64 c_min, i64 c_max, int d_max, bool bypass, uint64_t seed,
+                               cudaStream_t s);
+
+// ---- gram.cu
+// Dense c_u x c_u column-major tiles of G_u (blocked_matrix.hpp:238-254)
+// and D_u (:257-266) for clusters [u0,u1) at tile offsets tile_off[u]-tile_off[u0].
+void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const std::vector<i64>& tile_off,
+                double* G, double* D, cudaStream_t s);
+
+// ---- search.cu
+struct SearchBatch {
+  // per cluster u in [u0,u1):
+  DBuf<int64_t> c;         // cluster size
+  DBuf<int64_t> tile;      // tile offset (elements) into G/D
+  DBuf<int64_t> budget;    // elimination cap (factorizer.hpp:463-479)
+  DBuf<uint64_t> seed;     // derive(seed,{0xF0,p,u})
+  DBuf<int64_t> out_base;  // first rotation / elimination slot
+};
+struct SearchOut {
+  DBuf<int32_t> nrot, nelim;   // per cluster
+  DBuf<int32_t> rot_loc;       // R x k local indices
+  DBuf<double> rot_q;          // R x k x k
+  DBuf<int32_t> rot_level;     // R: dependency level in the apply, 0 = exact identity
+  DBuf<int32_t> elim_loc;      // R local indices, elimination order
+  DBuf<int32_t> error;         // 1: non-symmetric sub-Gram (invalid_argument)
+};
+// Clusters [u0, u0+nclusters): per-cluster arrays of b are batch-relative,
+// out.nrot/out.nelim are indexed by absolute cluster u, slots are absolute.
+void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double eta, double* G, double* D,
+                     i64 max_c, SearchOut& out, cudaStream_t s);
+
+// ---- apply.cu
+// One rotation stream applied to the columns of a paged matrix
+// (factorizer.hpp:362-380, sparse.hpp:123-156): rotation t acts on ids
+// col_ids[t*k .. t*k+k) with q = rot_q[t]; rotations are grouped in levels
+// of mutually independent rotations (level_start).
+struct LevelPlan {
+  i64 R = 0;                 // rotation slots
+  int k = 2;
+  int max_level = 0;
+  DBuf<int32_t> ids;         // R x k stage ids
+  const double* q = nullptr; // R x k x k (non-owning)
+  DBuf<int32_t> order;       // slots sorted by level (level-0 slots first, skipped)
+  std::vector<i64> level_start;  // host: [level-1 start] for levels 1..max_level, plus end
+};
+// Builds the level plan from a search result: slot = out_base[u] + t for
+// t < nrot[u]; stage id = cluster_off[u] + local.
+void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_base,
+                const DBuf<int64_t>& cluster_off, i64 nclusters, i64 R, int k, cudaStream_t s);
+void apply_levels(Paged& p, const LevelPlan& plan, cudaStream_t s);
+
+}  // namespace pmmf_b200

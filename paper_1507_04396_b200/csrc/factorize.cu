@@ -1,0 +1,421 @@
+// factorize.cu — the stage loop of pmmf::factorize (factorizer.hpp:397-595)
+// driving the device kernels, plus the result half of the C-ABI.
+//
+// Per stage p (all matrix data stays in HBM):
+//   cluster (cluster.cu, on the PRE-reblock matrix, factorizer.hpp:437)
+//   -> reblock into stage numbering (matrix.cu, :456)
+//   -> budgets (host, :463-479)
+//   -> Gram + diagonal tiles (gram.cu, :485-488) -> search (search.cu, :494-504)
+//   -> apply: column pass, transpose, column pass, transpose (apply.cu, :513)
+//   -> residual / retired diagonals (k_residual, :521-547) -> shrink (:550-557)
+// The host keeps only what the reference keeps on its control path: the
+// active list, the partitions, the RNG stream of the clustering, and the
+// materialised outputs (rotations, eliminations).
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "engine.cuh"
+#include "result.cuh"
+#include "rng.cuh"
+#include "rotation.cuh"
+
+namespace pmmf_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// Residual accounting for the stage's eliminations in order r
+// (factorizer.hpp:529-542): mass = sum of v^2 over column g's entries whose
+// row is still active or retired later in the stage; diag = A'[g][g].
+__global__ void k_residual(i64 R, const int32_t* __restrict__ elim_sid, const i64* __restrict__ ptr,
+                           const int32_t* __restrict__ row, const double* __restrict__ val,
+                           const int32_t* __restrict__ s2g, const uint8_t* __restrict__ is_active,
+                           const int32_t* __restrict__ rank, double* __restrict__ mass, double* __restrict__ diag) {
+  const i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (r >= R) return;
+  const int32_t j = elim_sid[r];
+  double m = 0.0, d = 0.0;
+  for (i64 e = ptr[j]; e < ptr[j + 1]; ++e) {
+    const int32_t sr = row[e];
+    if (sr == j) {
+      d = val[e];
+      continue;
+    }
+    const int32_t l = s2g[sr];
+    if (is_active[l] || rank[l] > r) m = dadd(m, dmul(val[e], val[e]));
+  }
+  mass[r] = m;
+  diag[r] = d;
+}
+
+__global__ void k_mark(i64 R, const int32_t* __restrict__ g, uint8_t* __restrict__ is_active,
+                       int32_t* __restrict__ rank, int set_rank) {
+  const i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (r >= R) return;
+  is_active[g[r]] = 0;
+  rank[g[r]] = set_rank ? static_cast<int32_t>(r) : -1;
+}
+
+// Core: core(a, b) = A[active[a]][active[b]] (factorizer.hpp:578-588).
+__global__ void k_core(i64 g, const int32_t* __restrict__ col_sid, const i64* __restrict__ ptr,
+                       const int32_t* __restrict__ row, const double* __restrict__ val,
+                       const int32_t* __restrict__ pos_of_sid, double* __restrict__ core) {
+  const i64 b = blockIdx.x;
+  if (b >= g) return;
+  const int32_t j = col_sid[b];
+  for (i64 e = ptr[j] + threadIdx.x; e < ptr[j + 1]; e += blockDim.x) {
+    const int32_t a = pos_of_sid[row[e]];
+    if (a >= 0) core[static_cast<i64>(a) * g + b] = val[e];
+  }
+}
+
+using clk = std::chrono::steady_clock;
+double ms_since(clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); }
+
+void validate(const pmmf_b200_params& p) {  // factorizer.hpp:44-50, clustering.hpp:36-40
+  if (p.k < 2 || p.k > 8) fail(PMMF_INVALID_ARGUMENT, "FactorizeParams: k must be in [2, 8]");
+  if (p.n_stages < 1) fail(PMMF_INVALID_ARGUMENT, "FactorizeParams: n_stages < 1");
+  if (!(p.eta > 0.0 && p.eta < 1.0)) fail(PMMF_INVALID_ARGUMENT, "FactorizeParams: eta not in (0,1)");
+  if (p.core_min < 1) fail(PMMF_INVALID_ARGUMENT, "FactorizeParams: core_min < 1");
+  if (p.m_target < 1) fail(PMMF_INVALID_ARGUMENT, "ClusterParams: m_target < 1");
+  if (p.c_min > p.c_max) fail(PMMF_INVALID_ARGUMENT, "ClusterParams: c_min > c_max");
+  if (p.d_max < 0) fail(PMMF_INVALID_ARGUMENT, "ClusterParams: d_max < 0");
+}
+
+struct StreamGuard {
+  cudaStream_t s = nullptr;
+  StreamGuard() { PMMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~StreamGuard() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+}  // namespace
+
+std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b200_params& p) {
+  PMMF_CUDA(cudaSetDevice(in->device));
+  {
+    // Keep freed blocks in the pool between stages.
+    cudaMemPool_t pool;
+    PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, in->device));
+    uint64_t thr = ~uint64_t{0};
+    PMMF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  }
+  StreamGuard sg;
+  cudaStream_t s = sg.s;
+  const i64 n = in->n;
+  if (n >= (i64{1} << 31) - 1) fail(PMMF_INVALID_ARGUMENT, "factorize: dimension exceeds 2^31 - 1");
+  auto R = std::make_unique<Result>();
+  R->n = n;
+  R->k = p.k;
+
+  // ---- input partition and from_triplets
+  Numbering cur;
+  {
+    std::vector<std::vector<i64>> init;
+    if (in->n_clusters == 0) {
+      init.emplace_back(static_cast<size_t>(std::max<i64>(n, 0)));
+      std::iota(init[0].begin(), init[0].end(), i64{0});
+    } else {
+      for (i64 u = 0; u < in->n_clusters; ++u)
+        init.emplace_back(in->cluster_members + in->cluster_offsets[u], in->cluster_members + in->cluster_offsets[u + 1]);
+    }
+    cur.build(init, std::max<i64>(n, 0), s);
+  }
+  Csc A;
+  {
+    const int64_t* rows = in->rows;
+    const int64_t* cols = in->cols;
+    const double* vals = in->vals;
+    DBuf<int64_t> drow, dcol;
+    DBuf<double> dval;
+    if (!in->on_device && in->nnz > 0) {
+      drow.alloc(in->nnz, s);
+      dcol.alloc(in->nnz, s);
+      dval.alloc(in->nnz, s);
+      drow.upload(in->rows, in->nnz);
+      dcol.upload(in->cols, in->nnz);
+      dval.upload(in->vals, in->nnz);
+      rows = drow.get();
+      cols = dcol.get();
+      vals = dval.get();
+    }
+    csc_from_coo(A, cur, std::max<i64>(n, 0), in->nnz, rows, cols, vals, s);
+  }
+  validate(p);
+  if (n < 1) fail(PMMF_INVALID_ARGUMENT, "factorize: empty matrix");
+  {
+    double asym = 0.0, fro = 0.0;
+    csc_symmetry(A, cur, &asym, &fro, s);
+    if (asym > 1e-9 * std::max(std::sqrt(fro), 1e-300))
+      fail(PMMF_INVALID_ARGUMENT, "factorize: input matrix is not symmetric");
+  }
+
+  const auto run_start = clk::now();
+  std::vector<i64> active;
+  for (i64 g = 0; g < n; ++g)
+    if (cur.g2s[g] >= 0) active.push_back(g);
+  R->hist.push_back(static_cast<i64>(active.size()));
+  DBuf<uint8_t> d_active(n, s);
+  DBuf<int32_t> d_rank(n, s);
+  {
+    std::vector<uint8_t> h(static_cast<size_t>(n), 0);
+    for (i64 g : active) h[g] = 1;
+    d_active.upload(h);
+    d_rank.fill_bytes(0xff);
+  }
+  R->trivial = static_cast<i64>(active.size()) <= p.core_min;
+
+  for (int stage_no = 1; stage_no <= p.n_stages && !R->trivial; ++stage_no) {
+    if (static_cast<i64>(active.size()) <= p.core_min) break;
+    // ---- clustering on the pre-reblock matrix
+    auto t0 = clk::now();
+    const uint64_t cpath[2] = {0xC1u, static_cast<uint64_t>(stage_no)};
+    ClusterOut co = cluster_columns_dev(A, cur, active, n, p.m_target, p.c_min, p.c_max, p.d_max,
+                                        p.bypass_enabled != 0, derive(p.seed, cpath), s);
+    R->phases[0] += ms_since(t0);
+    const i64 rc = static_cast<i64>(co.clusters.size());
+    std::vector<std::vector<i64>> stage_clusters = std::move(co.clusters);
+    if (!co.bypassed.empty()) stage_clusters.push_back(co.bypassed);
+
+    // ---- reblock to the stage numbering
+    t0 = clk::now();
+    Numbering nxt;
+    nxt.build(stage_clusters, n, s);
+    {
+      std::vector<int32_t> map(static_cast<size_t>(cur.size())), new2old(static_cast<size_t>(nxt.size()));
+      for (i64 r = 0; r < cur.size(); ++r) map[r] = static_cast<int32_t>(nxt.g2s[cur.s2g[r]]);
+      for (i64 J = 0; J < nxt.size(); ++J) {
+        const i64 old = cur.g2s[nxt.s2g[J]];
+        if (old < 0) fail(PMMF_INVALID_ARGUMENT, "reblock: new partition references an absent index");
+        new2old[J] = static_cast<int32_t>(old);
+      }
+      DBuf<int32_t> dmap(std::max<i64>(cur.size(), 1), s), dn2o(std::max<i64>(nxt.size(), 1), s);
+      dmap.upload(map);
+      dn2o.upload(new2old);
+      Csc B;
+      reblock(B, A, dmap, dn2o, nxt.size(), s);
+      A = std::move(B);
+    }
+    cur = std::move(nxt);
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    R->phases[4] += ms_since(t0);
+
+    Result::Stage st;
+    st.off = cur.off;
+    st.members = cur.s2g;
+    st.bypassed = co.bypassed;
+
+    // ---- budgets (factorizer.hpp:463-479)
+    std::vector<i64> budget(static_cast<size_t>(rc), 0);
+    i64 planned = 0;
+    for (i64 u = 0; u < rc; ++u) {
+      const i64 c = cur.off[u + 1] - cur.off[u];
+      i64 b = c < p.k ? 0 : static_cast<i64>(std::floor(p.eta * static_cast<double>(c)));
+      b = std::min(b, std::max<i64>(0, c - (p.k - 1)));
+      budget[u] = b;
+      planned += b;
+    }
+    const i64 allowance = std::max<i64>(0, static_cast<i64>(active.size()) - p.core_min);
+    while (planned > allowance) {
+      i64 arg = 0;
+      for (i64 u = 1; u < rc; ++u)
+        if (budget[u] > budget[arg]) arg = u;
+      --budget[arg];
+      --planned;
+    }
+    std::vector<int64_t> out_base(static_cast<size_t>(rc) + 1, 0);
+    for (i64 u = 0; u < rc; ++u) out_base[u + 1] = out_base[u] + budget[u];
+    const i64 slots = out_base[rc];
+
+    // ---- Gram + search, in batches of clusters whose tiles fit in memory
+    SearchOut so;
+    so.nrot.alloc(std::max<i64>(rc, 1), s);
+    so.nelim.alloc(std::max<i64>(rc, 1), s);
+    so.nrot.zero();
+    so.nelim.zero();
+    so.rot_loc.alloc(std::max<i64>(slots * p.k, 1), s);
+    so.rot_q.alloc(std::max<i64>(slots * p.k * p.k, 1), s);
+    so.rot_level.alloc(std::max<i64>(slots, 1), s);
+    so.elim_loc.alloc(std::max<i64>(slots, 1), s);
+    so.error.alloc(1, s);
+    so.error.zero();
+    DBuf<int64_t> d_out_base(rc + 1, s), d_coff(rc + 1, s);
+    d_out_base.upload(out_base);
+    d_coff.upload(cur.off.data(), rc + 1);
+    {
+      size_t free_b = 0, total_b = 0;
+      PMMF_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const i64 budget_elems = std::max<i64>(i64{1} << 20, static_cast<i64>(free_b * 0.55) / 16);
+      i64 u0 = 0;
+      double gram_ms = 0.0, search_ms = 0.0;
+      while (u0 < rc) {
+        i64 u1 = u0, elems = 0, max_c = 0;
+        std::vector<i64> tile_off(1, 0);
+        while (u1 < rc) {
+          const i64 c = cur.off[u1 + 1] - cur.off[u1];
+          if (u1 > u0 && elems + c * c > budget_elems) break;
+          elems += c * c;
+          max_c = std::max(max_c, c);
+          tile_off.push_back(elems);
+          ++u1;
+        }
+        auto tg = clk::now();
+        DBuf<double> G(std::max<i64>(elems, 1), s), D(std::max<i64>(elems, 1), s);
+        G.zero();
+        D.zero();
+        // gram_tiles wants tile_off indexed by absolute u
+        std::vector<i64> toff(static_cast<size_t>(u1) + 1, 0);
+        for (i64 u = u0; u <= u1; ++u) toff[u] = tile_off[u - u0];
+        gram_tiles(A, cur.off, u0, u1, toff, G.get(), D.get(), s);
+        PMMF_CUDA(cudaStreamSynchronize(s));
+        gram_ms += ms_since(tg);
+        auto ts = clk::now();
+        const i64 nb = u1 - u0;
+        SearchBatch sb;
+        std::vector<int64_t> hc(nb), ht(nb), hb(nb), hob(nb);
+        std::vector<uint64_t> hs(nb);
+        for (i64 u = u0; u < u1; ++u) {
+          hc[u - u0] = cur.off[u + 1] - cur.off[u];
+          ht[u - u0] = tile_off[u - u0];
+          hb[u - u0] = budget[u];
+          hob[u - u0] = out_base[u];
+          const uint64_t spath[3] = {0xF0u, static_cast<uint64_t>(stage_no), static_cast<uint64_t>(u)};
+          hs[u - u0] = derive(p.seed, spath);
+        }
+        sb.c.alloc(nb, s);
+        sb.tile.alloc(nb, s);
+        sb.budget.alloc(nb, s);
+        sb.seed.alloc(nb, s);
+        sb.out_base.alloc(nb, s);
+        sb.c.upload(hc);
+        sb.tile.upload(ht);
+        sb.budget.upload(hb);
+        sb.seed.upload(hs);
+        sb.out_base.upload(hob);
+        search_clusters(sb, u0, nb, p.k, p.eta, G.get(), D.get(), std::max<i64>(max_c, 1), so, s);
+        PMMF_CUDA(cudaStreamSynchronize(s));
+        search_ms += ms_since(ts);
+        u0 = u1;
+      }
+      R->phases[1] += gram_ms;
+      R->phases[2] += search_ms;
+    }
+    if (so.error.to_host(1)[0]) fail(PMMF_INVALID_ARGUMENT, "rotation_from_gram: input not symmetric");
+    std::vector<int32_t> nrot = so.nrot.to_host(std::max<i64>(rc, 1));
+    std::vector<int32_t> nelim = so.nelim.to_host(std::max<i64>(rc, 1));
+    std::vector<int32_t> rot_loc = so.rot_loc.to_host(std::max<i64>(slots * p.k, 1));
+    std::vector<double> rot_q = so.rot_q.to_host(std::max<i64>(slots * p.k * p.k, 1));
+    std::vector<int32_t> elim_loc = so.elim_loc.to_host(std::max<i64>(slots, 1));
+    std::vector<int32_t> order_sid;  // eliminated stage ids, stage elimination order
+    std::vector<int32_t> order_g;
+    for (i64 u = 0; u < rc; ++u) {
+      for (i64 t = 0; t < nrot[u]; ++t) {
+        const i64 sl = out_base[u] + t;
+        for (int a = 0; a < p.k; ++a) st.rot_idx.push_back(cur.s2g[cur.off[u] + rot_loc[sl * p.k + a]]);
+        st.rot_q.insert(st.rot_q.end(), rot_q.begin() + sl * p.k * p.k, rot_q.begin() + (sl + 1) * p.k * p.k);
+      }
+      for (i64 e = 0; e < nelim[u]; ++e) {
+        const i64 sid = cur.off[u] + elim_loc[out_base[u] + e];
+        order_sid.push_back(static_cast<int32_t>(sid));
+        order_g.push_back(static_cast<int32_t>(cur.s2g[sid]));
+      }
+    }
+
+    // ---- stage apply: column side, transpose, row side, transpose
+    t0 = clk::now();
+    {
+      LevelPlan plan;
+      build_plan(plan, so, d_out_base, d_coff, rc, slots, p.k, s);
+      if (plan.max_level > 0) {
+        Paged P;
+        paged_from_csc(P, std::move(A), 2 * A.nnz + (i64{1} << 20), s);
+        apply_levels(P, plan, s);
+        Csc T;
+        transpose_paged(T, P, s);
+        P = Paged();
+        Paged P2;
+        const i64 tn = T.nnz;
+        paged_from_csc(P2, std::move(T), 2 * tn + (i64{1} << 20), s);
+        apply_levels(P2, plan, s);
+        Csc B;
+        transpose_paged(B, P2, s);
+        A = std::move(B);
+      }
+    }
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    R->phases[3] += ms_since(t0);
+
+    // ---- residual accounting against the end-of-stage matrix
+    const i64 ne = static_cast<i64>(order_g.size());
+    if (ne > 0) {
+      DBuf<int32_t> dsid(ne, s), dg(ne, s);
+      dsid.upload(order_sid);
+      dg.upload(order_g);
+      PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 1);
+      DBuf<double> mass(ne, s), diag(ne, s);
+      PMMF_LAUNCH(k_residual, blocks_for(ne, kThreads), kThreads, 0, s, ne, dsid.get(), A.ptr.get(), A.row.get(),
+                  A.val.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(), diag.get());
+      PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
+      std::vector<double> hm = mass.to_host(ne), hd = diag.to_host(ne);
+      for (i64 r = 0; r < ne; ++r) {
+        st.elim_idx.push_back(order_g[r]);
+        st.elim_diag.push_back(hd[r]);
+        st.elim_mass.push_back(hm[r]);
+        R->residual_sq += 2.0 * hm[r];
+        R->diag.push_back({order_g[r], hd[r]});
+      }
+    }
+    {
+      std::vector<uint8_t> gone(static_cast<size_t>(n), 0);
+      for (int32_t g : order_g) gone[g] = 1;
+      std::vector<i64> next;
+      next.reserve(active.size() - order_g.size());
+      for (i64 g : active)
+        if (!gone[g]) next.push_back(g);
+      active = std::move(next);
+    }
+    R->hist.push_back(static_cast<i64>(active.size()));
+    R->info.push_back({stage_no, rc, static_cast<i64>(st.bypassed.size()),
+                       static_cast<i64>(st.rot_idx.size()) / p.k, ne, static_cast<i64>(active.size()),
+                       static_cast<i64>(co.max_depth)});
+    R->stages.push_back(std::move(st));
+  }
+
+  if (static_cast<i64>(active.size()) > p.core_cap)
+    fail(PMMF_NUMERIC, "factorize: core of size " + std::to_string(active.size()) + " exceeds the cap of " +
+                           std::to_string(p.core_cap) + "; raise core_cap or add stages");
+  const i64 g = static_cast<i64>(active.size());
+  R->core_idx = active;
+  R->core.assign(static_cast<size_t>(g * g), 0.0);
+  if (g > 0) {
+    std::vector<int32_t> col_sid(static_cast<size_t>(g)), pos(static_cast<size_t>(cur.size()), -1);
+    for (i64 a = 0; a < g; ++a) {
+      col_sid[a] = static_cast<int32_t>(cur.g2s[active[a]]);
+      pos[col_sid[a]] = static_cast<int32_t>(a);
+    }
+    DBuf<int32_t> dcs(g, s), dpos(std::max<i64>(cur.size(), 1), s);
+    dcs.upload(col_sid);
+    dpos.upload(pos);
+    DBuf<double> dcore(g * g, s);
+    dcore.zero();
+    PMMF_LAUNCH(k_core, static_cast<unsigned>(g), 128, 0, s, g, dcs.get(), A.ptr.get(), A.row.get(), A.val.get(),
+                dpos.get(), dcore.get());
+    R->core = dcore.to_host(g * g);
+  }
+  std::sort(R->diag.begin(), R->diag.end());
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  R->phases[5] = ms_since(run_start);
+  return R;
+}
+
+}  // namespace pmmf_b200

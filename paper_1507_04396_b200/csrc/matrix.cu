@@ -1,0 +1,400 @@
+// matrix.cu — blocked-matrix plumbing of the stage loop on the device:
+// from_triplets, symmetry check, paged<->contiguous transposes and reblock.
+// All of it is HBM-bound integer/byte movement: coalesced warp-per-column
+// gathers plus CUB radix / segmented sorts (row-key only, so the sorts run
+// over ceil(log2 N)/8 digit passes, not a full 64-bit key).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "engine.cuh"
+
+namespace pmmf_b200 {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------ numbering
+__global__ void k_fill_blk(const int64_t* off, i64 m, int32_t* blk) {
+  const i64 u = blockIdx.x;
+  if (u >= m) return;
+  for (i64 i = off[u] + threadIdx.x; i < off[u + 1]; i += blockDim.x) blk[i] = static_cast<int32_t>(u);
+}
+
+// ------------------------------------------------------------ from_coo
+__global__ void k_coo_keys(i64 n, i64 nnz, const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
+                           const double* __restrict__ vals, const int32_t* __restrict__ g2s, uint64_t N,
+                           uint64_t* __restrict__ keys, unsigned long long* __restrict__ first_err) {
+  const i64 t = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (t >= nnz) return;
+  const i64 r = rows[t], c = cols[t];
+  const double v = vals[t];
+  unsigned code = 0;
+  i64 sr = -1, sc = -1;
+  if (r < 0 || r >= n || c < 0 || c >= n) {
+    code = 1;  // out_of_range: index out of range
+  } else if (!isfinite(v)) {
+    code = 2;  // invalid_argument: non-finite value
+  } else {
+    sr = g2s[r];
+    sc = g2s[c];
+    if (sr < 0 || sc < 0) code = 3;  // out_of_range: not covered
+  }
+  if (code) {
+    atomicMin(first_err, (static_cast<unsigned long long>(t) << 2) | code);
+    keys[t] = 0;
+    return;
+  }
+  keys[t] = static_cast<uint64_t>(sc) * N + static_cast<uint64_t>(sr);
+}
+
+// Sum runs of equal keys in their (stable) order; flag the kept heads.
+__global__ void k_sum_dups(i64 m, const uint64_t* __restrict__ keys, const double* __restrict__ vals,
+                           double* __restrict__ sums, int32_t* __restrict__ keep) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  if (i > 0 && keys[i - 1] == keys[i]) {
+    keep[i] = 0;
+    return;
+  }
+  double s = vals[i];
+  for (i64 j = i + 1; j < m && keys[j] == keys[i]; ++j) s = dadd(s, vals[j]);
+  sums[i] = s;
+  keep[i] = s != 0.0 ? 1 : 0;
+}
+
+__global__ void k_scatter_kept(i64 m, const uint64_t* __restrict__ keys, const double* __restrict__ sums,
+                               const int32_t* __restrict__ keep, const i64* __restrict__ pos, uint64_t N,
+                               int32_t* __restrict__ out_col, int32_t* __restrict__ out_row,
+                               double* __restrict__ out_val) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= m || !keep[i]) return;
+  const i64 p = pos[i];
+  out_col[p] = static_cast<int32_t>(keys[i] / N);
+  out_row[p] = static_cast<int32_t>(keys[i] % N);
+  out_val[p] = sums[i];
+}
+
+// ptr[c] = first position whose column >= c, for a column-sorted list.
+__global__ void k_ptr_from_cols(i64 m, const int32_t* __restrict__ col, i64 N, i64* __restrict__ ptr) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i > m) return;
+  const i64 prev = i == 0 ? -1 : col[i - 1];
+  const i64 cur = i == m ? N : col[i];
+  for (i64 c = prev + 1; c <= cur; ++c) ptr[c] = i;
+}
+
+// ---------------------------------------------------------- symmetry
+__global__ void k_symmetry(i64 N, const i64* __restrict__ ptr, const int32_t* __restrict__ row,
+                           const double* __restrict__ val, const int32_t* __restrict__ blk,
+                           unsigned long long* __restrict__ worst, double* __restrict__ col_fro) {
+  const i64 j = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (j >= N) return;
+  double fro = 0.0, w = 0.0;
+  const int32_t bj = blk[j];
+  for (i64 e = ptr[j]; e < ptr[j + 1]; ++e) {
+    const double v = val[e];
+    fro = dadd(fro, dmul(v, v));
+    const int32_t r = row[e];
+    if (blk[r] > bj) continue;
+    // mirror value A[j][r]: row j of column r
+    i64 lo = ptr[r], hi = ptr[r + 1];
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (row[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    const double mv = (lo < ptr[r + 1] && row[lo] == j) ? val[lo] : 0.0;
+    w = fmax(w, fabs(dsub(v, mv)));
+  }
+  col_fro[j] = fro;
+  if (w > 0.0) atomicMax(worst, static_cast<unsigned long long>(__double_as_longlong(w)));
+}
+
+// ----------------------------------------------------------- paged
+__global__ void k_paged_init(i64 N, const i64* __restrict__ ptr, i64* __restrict__ off, int32_t* __restrict__ len) {
+  const i64 j = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (j >= N) return;
+  off[j] = ptr[j];
+  len[j] = static_cast<int32_t>(ptr[j + 1] - ptr[j]);
+}
+
+__global__ void k_len64(i64 N, const int32_t* __restrict__ len, i64* __restrict__ out) {
+  const i64 j = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (j < N) out[j] = len[j];
+  if (j == N) out[j] = 0;
+}
+
+// Gather the paged columns in column order into (row<<cb | col, val).
+__global__ void k_gather_keys(i64 N, const i64* __restrict__ off, const int32_t* __restrict__ len,
+                              const int32_t* __restrict__ arow, const double* __restrict__ aval,
+                              const i64* __restrict__ pos, int cb, uint64_t* __restrict__ keys,
+                              double* __restrict__ vals) {
+  const i64 warp = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= N) return;
+  const i64 src = off[warp], dst = pos[warp];
+  const int32_t L = len[warp];
+  for (int32_t i = lane; i < L; i += 32) {
+    keys[dst + i] = (static_cast<uint64_t>(arow[src + i]) << cb) | static_cast<uint64_t>(warp);
+    vals[dst + i] = aval[src + i];
+  }
+}
+
+__global__ void k_split_keys(i64 m, const uint64_t* __restrict__ keys, int cb, int32_t* __restrict__ major,
+                             int32_t* __restrict__ minor) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  const uint64_t k = keys[i];
+  major[i] = static_cast<int32_t>(k >> cb);
+  minor[i] = static_cast<int32_t>(k & ((uint64_t{1} << cb) - 1));
+}
+
+// ----------------------------------------------------------- reblock
+__global__ void k_reblock_count(i64 Nn, const int32_t* __restrict__ new2old, const i64* __restrict__ ptr,
+                                const int32_t* __restrict__ row, const int32_t* __restrict__ map,
+                                i64* __restrict__ cnt) {
+  const i64 warp = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp > Nn) return;
+  if (warp == Nn) {
+    if (lane == 0) cnt[Nn] = 0;
+    return;
+  }
+  const int32_t j = new2old[warp];
+  int c = 0;
+  for (i64 e = ptr[j] + lane; e < ptr[j + 1]; e += 32) c += map[row[e]] >= 0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[warp] = c;
+}
+
+__global__ void k_reblock_fill(i64 Nn, const int32_t* __restrict__ new2old, const i64* __restrict__ ptr,
+                               const int32_t* __restrict__ row, const double* __restrict__ val,
+                               const int32_t* __restrict__ map, const i64* __restrict__ nptr,
+                               int32_t* __restrict__ nrow, double* __restrict__ nval) {
+  const i64 warp = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= Nn) return;
+  const int32_t j = new2old[warp];
+  i64 out = nptr[warp];
+  for (i64 base = ptr[j]; base < ptr[j + 1]; base += 32) {
+    const i64 e = base + lane;
+    int32_t nr = -1;
+    double v = 0.0;
+    if (e < ptr[j + 1]) {
+      nr = map[row[e]];
+      v = val[e];
+    }
+    const unsigned keep = __ballot_sync(0xffffffffu, nr >= 0);
+    if (nr >= 0) {
+      const int p = __popc(keep & ((1u << lane) - 1));
+      nrow[out + p] = nr;
+      nval[out + p] = v;
+    }
+    out += __popc(keep);
+  }
+}
+
+template <typename T>
+void exclusive_scan(const T* in, T* out, i64 n, cudaStream_t s) {
+  size_t tmp = 0;
+  PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(n), s));
+  DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+  PMMF_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, in, out, static_cast<int64_t>(n), s));
+}
+
+void sort_pairs(DBuf<uint64_t>& keys, DBuf<double>& vals, i64 m, int begin_bit, int end_bit, cudaStream_t s) {
+  if (m <= 1 || end_bit <= begin_bit) return;
+  DBuf<uint64_t> k2(m, s);
+  DBuf<double> v2(m, s);
+  cub::DoubleBuffer<uint64_t> kb(keys.get(), k2.get());
+  cub::DoubleBuffer<double> vb(vals.get(), v2.get());
+  size_t tmp = 0;
+  PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int64_t>(m), begin_bit, end_bit, s));
+  DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+  PMMF_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kb, vb, static_cast<int64_t>(m), begin_bit, end_bit, s));
+  if (kb.Current() != keys.get()) {
+    std::swap(keys.p, k2.p);
+    std::swap(vals.p, v2.p);
+  }
+}
+
+}  // namespace
+
+std::atomic<int64_t>& launch_counter() {
+  static std::atomic<int64_t> c{0};
+  return c;
+}
+
+void Numbering::build(const std::vector<std::vector<i64>>& cls, i64 n, cudaStream_t s) {
+  s2g.clear();
+  off.assign(1, 0);
+  g2s.assign(static_cast<size_t>(std::max<i64>(n, 0)), -1);
+  for (const auto& cl : cls) {
+    for (i64 g : cl) {
+      if (g < 0) fail(PMMF_INVALID_ARGUMENT, "Partition: negative index");
+      if (g >= n) fail(PMMF_OUT_OF_RANGE, "Partition: index beyond matrix dimension");
+      if (g2s[g] >= 0) fail(PMMF_INVALID_ARGUMENT, "Partition: duplicate index across clusters");
+      g2s[g] = static_cast<i64>(s2g.size());
+      s2g.push_back(g);
+    }
+    off.push_back(static_cast<i64>(s2g.size()));
+  }
+  const i64 N = size();
+  d_blk.alloc(std::max<i64>(N, 1), s);
+  d_s2g.alloc(std::max<i64>(N, 1), s);
+  std::vector<int32_t> s2g32(s2g.begin(), s2g.end());
+  d_s2g.upload(s2g32);
+  DBuf<int64_t> doff(clusters() + 1, s);
+  doff.upload(off);
+  PMMF_LAUNCH(k_fill_blk, static_cast<unsigned>(clusters()), 256, 0, s, doff.get(), clusters(), d_blk.get());
+}
+
+void csc_from_coo(Csc& out, const Numbering& nb, i64 n, i64 nnz, const int64_t* rows, const int64_t* cols,
+                  const double* vals, cudaStream_t s) {
+  const i64 N = nb.size();
+  out.N = N;
+  DBuf<int32_t> g2s(std::max<i64>(n, 1), s);
+  {
+    std::vector<int32_t> h(nb.g2s.begin(), nb.g2s.end());
+    g2s.upload(h);
+  }
+  DBuf<uint64_t> keys(std::max<i64>(nnz, 1), s);
+  DBuf<double> v(std::max<i64>(nnz, 1), s);
+  DBuf<unsigned long long> ferr(1, s);
+  ferr.fill_bytes(0xff);
+  if (nnz > 0) {
+    PMMF_CUDA(cudaMemcpyAsync(v.get(), vals, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, s));
+    PMMF_LAUNCH(k_coo_keys, blocks_for(nnz, kThreads), kThreads, 0, s, n, nnz, rows, cols, vals, g2s.get(),
+                static_cast<uint64_t>(std::max<i64>(N, 1)), keys.get(), ferr.get());
+  }
+  const unsigned long long fe = ferr.to_host(1)[0];
+  if (fe != ~0ull) {
+    const unsigned code = fe & 3u;
+    if (code == 1) fail(PMMF_OUT_OF_RANGE, "from_triplets: index out of range");
+    if (code == 2) fail(PMMF_INVALID_ARGUMENT, "from_triplets: non-finite value");
+    fail(PMMF_OUT_OF_RANGE, "from_triplets: index not covered by partition");
+  }
+  const int kb = bits_for(std::max<i64>(N, 1) * std::max<i64>(N, 1) - 1);
+  sort_pairs(keys, v, nnz, 0, std::max(kb, 1), s);
+  DBuf<double> sums(std::max<i64>(nnz, 1), s);
+  DBuf<int32_t> keep(nnz + 1, s);
+  DBuf<i64> keep64(nnz + 1, s), pos(nnz + 1, s);
+  keep.zero();
+  PMMF_LAUNCH(k_sum_dups, blocks_for(nnz, kThreads), kThreads, 0, s, nnz, keys.get(), v.get(), sums.get(), keep.get());
+  // widen flags to int64 and scan
+  PMMF_LAUNCH(k_len64, blocks_for(nnz + 1, kThreads), kThreads, 0, s, nnz, keep.get(), keep64.get());
+  exclusive_scan(keep64.get(), pos.get(), nnz + 1, s);
+  i64 m = 0;
+  PMMF_CUDA(cudaMemcpyAsync(&m, pos.get() + nnz, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  DBuf<int32_t> col(std::max<i64>(m, 1), s);
+  out.row.alloc(std::max<i64>(m, 1), s);
+  out.val.alloc(std::max<i64>(m, 1), s);
+  PMMF_LAUNCH(k_scatter_kept, blocks_for(nnz, kThreads), kThreads, 0, s, nnz, keys.get(), sums.get(), keep.get(),
+              pos.get(), static_cast<uint64_t>(std::max<i64>(N, 1)), col.get(), out.row.get(), out.val.get());
+  out.nnz = m;
+  out.ptr.alloc(N + 1, s);
+  PMMF_LAUNCH(k_ptr_from_cols, blocks_for(m + 1, kThreads), kThreads, 0, s, m, col.get(), N, out.ptr.get());
+}
+
+void csc_symmetry(const Csc& a, const Numbering& nb, double* max_asym, double* fro_sq, cudaStream_t s) {
+  DBuf<unsigned long long> worst(1, s);
+  worst.zero();
+  DBuf<double> colfro(std::max<i64>(a.N, 1), s), total(1, s);
+  colfro.zero();
+  PMMF_LAUNCH(k_symmetry, blocks_for(a.N, kThreads), kThreads, 0, s, a.N, a.ptr.get(), a.row.get(), a.val.get(),
+              nb.d_blk.get(), worst.get(), colfro.get());
+  size_t tmp = 0;
+  PMMF_CUDA(cub::DeviceReduce::Sum(nullptr, tmp, colfro.get(), total.get(), static_cast<int64_t>(std::max<i64>(a.N, 1)), s));
+  DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+  PMMF_CUDA(cub::DeviceReduce::Sum(t.get(), tmp, colfro.get(), total.get(), static_cast<int64_t>(std::max<i64>(a.N, 1)), s));
+  unsigned long long w = 0;
+  PMMF_CUDA(cudaMemcpyAsync(&w, worst.get(), sizeof(w), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaMemcpyAsync(fro_sq, total.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  double wd;
+  std::memcpy(&wd, &w, sizeof(wd));
+  *max_asym = wd;
+}
+
+void paged_from_csc(Paged& p, Csc&& a, i64 extra_capacity, cudaStream_t s) {
+  p.N = a.N;
+  p.off.alloc(std::max<i64>(a.N, 1), s);
+  p.len.alloc(std::max<i64>(a.N, 1), s);
+  PMMF_LAUNCH(k_paged_init, blocks_for(a.N, kThreads), kThreads, 0, s, a.N, a.ptr.get(), p.off.get(), p.len.get());
+  p.cap = a.nnz + std::max<i64>(extra_capacity, 1024);
+  p.row.alloc(p.cap, s);
+  p.val.alloc(p.cap, s);
+  if (a.nnz) {
+    PMMF_CUDA(cudaMemcpyAsync(p.row.get(), a.row.get(), sizeof(int32_t) * a.nnz, cudaMemcpyDeviceToDevice, s));
+    PMMF_CUDA(cudaMemcpyAsync(p.val.get(), a.val.get(), sizeof(double) * a.nnz, cudaMemcpyDeviceToDevice, s));
+  }
+  p.cursor.alloc(1, s);
+  const unsigned long long c0 = static_cast<unsigned long long>(a.nnz);
+  PMMF_CUDA(cudaMemcpyAsync(p.cursor.get(), &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));  // c0 lives on the stack
+  a.ptr.release();
+  a.row.release();
+  a.val.release();
+}
+
+void transpose_paged(Csc& out, const Paged& p, cudaStream_t s) {
+  const i64 N = p.N;
+  DBuf<i64> len64(N + 1, s), pos(N + 1, s);
+  PMMF_LAUNCH(k_len64, blocks_for(N + 1, kThreads), kThreads, 0, s, N, p.len.get(), len64.get());
+  exclusive_scan(len64.get(), pos.get(), N + 1, s);
+  i64 m = 0;
+  PMMF_CUDA(cudaMemcpyAsync(&m, pos.get() + N, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  const int cb = std::max(1, bits_for(std::max<i64>(N - 1, 1)));
+  DBuf<uint64_t> keys(std::max<i64>(m, 1), s);
+  DBuf<double> vals(std::max<i64>(m, 1), s);
+  PMMF_LAUNCH(k_gather_keys, blocks_for(N * 32, kThreads), kThreads, 0, s, N, p.off.get(), p.len.get(), p.row.get(),
+              p.val.get(), pos.get(), cb, keys.get(), vals.get());
+  // Stable sort on the row bits only: the gather is in (col,row) order, so
+  // the result is in (row,col) order.
+  sort_pairs(keys, vals, m, cb, 2 * cb, s);
+  out.N = N;
+  out.nnz = m;
+  DBuf<int32_t> major(std::max<i64>(m, 1), s);
+  out.row.alloc(std::max<i64>(m, 1), s);
+  PMMF_LAUNCH(k_split_keys, blocks_for(m, kThreads), kThreads, 0, s, m, keys.get(), cb, major.get(), out.row.get());
+  out.val = std::move(vals);
+  out.ptr.alloc(N + 1, s);
+  PMMF_LAUNCH(k_ptr_from_cols, blocks_for(m + 1, kThreads), kThreads, 0, s, m, major.get(), N, out.ptr.get());
+}
+
+void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_t>& new2old, i64 n_new,
+             cudaStream_t s) {
+  DBuf<i64> cnt(n_new + 1, s), nptr(n_new + 1, s);
+  PMMF_LAUNCH(k_reblock_count, blocks_for((n_new + 1) * 32, kThreads), kThreads, 0, s, n_new, new2old.get(),
+              a.ptr.get(), a.row.get(), map.get(), cnt.get());
+  exclusive_scan(cnt.get(), nptr.get(), n_new + 1, s);
+  i64 m = 0;
+  PMMF_CUDA(cudaMemcpyAsync(&m, nptr.get() + n_new, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  DBuf<int32_t> r1(std::max<i64>(m, 1), s);
+  DBuf<double> v1(std::max<i64>(m, 1), s);
+  PMMF_LAUNCH(k_reblock_fill, blocks_for(n_new * 32, kThreads), kThreads, 0, s, n_new, new2old.get(), a.ptr.get(),
+              a.row.get(), a.val.get(), map.get(), nptr.get(), r1.get(), v1.get());
+  out.N = n_new;
+  out.nnz = m;
+  out.row.alloc(std::max<i64>(m, 1), s);
+  out.val.alloc(std::max<i64>(m, 1), s);
+  if (m > 0 && n_new > 0) {
+    size_t tmp = 0;
+    PMMF_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp, r1.get(), out.row.get(), v1.get(), out.val.get(),
+                                                  static_cast<int64_t>(m), static_cast<int64_t>(n_new), nptr.get(),
+                                                  nptr.get() + 1, s));
+    DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+    PMMF_CUDA(cub::DeviceSegmentedSort::SortPairs(t.get(), tmp, r1.get(), out.row.get(), v1.get(), out.val.get(),
+                                                  static_cast<int64_t>(m), static_cast<int64_t>(n_new), nptr.get(),
+                                                  nptr.get() + 1, s));
+  }
+  out.ptr = std::move(nptr);
+}
+
+}  // namespace pmmf_b200

@@ -1,0 +1,147 @@
+// rotation.cuh — k x k rotation arithmetic, bit-exact with the reference,
+// usable from the search kernel's scalar lane and from the host C-ABI.
+//   jacobi_angle        dense.hpp:132-138
+//   jacobi_diagonalize  dense.hpp:144-183 (cyclic, rel_tol 1e-15, 64 sweeps)
+//   rotation_from_gram  factorizer.hpp:150-171 (+ fix_row_signs :130-144)
+//   corner conjugation  sparse.hpp:403 via DenseMatrix::multiply (dense.hpp:55-65)
+// Compiled with -fmad=false: every product and sum rounds separately.
+#pragma once
+
+#include <cmath>
+
+#ifdef __CUDACC__
+#define PMMF_HDI __host__ __device__ inline
+#else
+#define PMMF_HDI inline
+#endif
+
+namespace pmmf_b200 {
+
+constexpr int kMaxK = 8;
+
+PMMF_HDI void jacobi_angle(double gpp, double grr, double gpr, double& c, double& s) {
+  if (gpr == 0.0) {
+    c = 1.0;
+    s = 0.0;
+    return;
+  }
+  const double tau = (grr - gpp) / (2.0 * gpr);
+  const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+  c = 1.0 / sqrt(1.0 + t * t);
+  s = t * c;
+}
+
+// a (n x n, row-major stride kMaxK) is diagonalized in place; q returned.
+PMMF_HDI void jacobi_diagonalize(double (*a)[kMaxK], int n, double (*q)[kMaxK]) {
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) q[i][j] = i == j ? 1.0 : 0.0;
+  double fro = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) fro += a[i][j] * a[i][j];
+  const double scale = sqrt(fro);
+  if (scale == 0.0 || n < 2) return;
+  const double stop = 1e-15 * scale;
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = i + 1; j < n; ++j) off += 2.0 * a[i][j] * a[i][j];
+    if (sqrt(off) <= stop) break;
+    for (int p = 0; p < n; ++p)
+      for (int r = p + 1; r < n; ++r) {
+        if (a[p][r] == 0.0) continue;
+        double c, s;
+        jacobi_angle(a[p][p], a[r][r], a[p][r], c, s);
+        for (int t = 0; t < n; ++t) {
+          const double ap = a[p][t], ar = a[r][t];
+          a[p][t] = c * ap - s * ar;
+          a[r][t] = s * ap + c * ar;
+        }
+        for (int t = 0; t < n; ++t) {
+          const double ap = a[t][p], ar = a[t][r];
+          a[t][p] = c * ap - s * ar;
+          a[t][r] = s * ap + c * ar;
+        }
+        a[p][r] = 0.0;
+        a[r][p] = 0.0;
+        for (int t = 0; t < n; ++t) {
+          const double qp = q[p][t], qr = q[r][t];
+          q[p][t] = c * qp - s * qr;
+          q[r][t] = s * qp + c * qr;
+        }
+      }
+  }
+}
+
+// Returns false when g is not symmetric within 1e-9 * max(1, max|g|)
+// (the reference throws std::invalid_argument there).
+PMMF_HDI bool rotation_from_gram(const double (*g)[kMaxK], int k, double (*q)[kMaxK]) {
+  double asym = 0.0, mx = 0.0;
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) {
+      mx = fmax(mx, fabs(g[i][j]));
+      if (j > i) asym = fmax(asym, fabs(g[i][j] - g[j][i]));
+    }
+  if (asym > 1e-9 * fmax(1.0, mx)) return false;
+  double w[kMaxK][kMaxK];
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) w[i][j] = 0.5 * (g[i][j] + g[j][i]);
+  if (k == 2) {
+    double c, s;
+    jacobi_angle(w[0][0], w[1][1], w[0][1], c, s);
+    q[0][0] = c;
+    q[0][1] = -s;
+    q[1][0] = s;
+    q[1][1] = c;
+  } else {
+    jacobi_diagonalize(w, k, q);
+  }
+  for (int i = 0; i < k; ++i) {
+    int arg = 0;
+    double best = fabs(q[i][0]);
+    for (int j = 1; j < k; ++j)
+      if (fabs(q[i][j]) > best) {
+        best = fabs(q[i][j]);
+        arg = j;
+      }
+    if (q[i][arg] < 0.0)
+      for (int j = 0; j < k; ++j) q[i][j] = -q[i][j];
+  }
+  return true;
+}
+
+// out = (q * C) * q^T with DenseMatrix::multiply's loop order and its
+// zero-left-factor skip.
+PMMF_HDI void conjugate_corner(const double (*q)[kMaxK], const double (*C)[kMaxK], int k, double (*out)[kMaxK]) {
+  double p[kMaxK][kMaxK];
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) p[i][j] = 0.0;
+  for (int i = 0; i < k; ++i)
+    for (int t = 0; t < k; ++t) {
+      const double x = q[i][t];
+      if (x == 0.0) continue;
+      for (int j = 0; j < k; ++j) p[i][j] += x * C[t][j];
+    }
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) out[i][j] = 0.0;
+  for (int i = 0; i < k; ++i)
+    for (int t = 0; t < k; ++t) {
+      const double x = p[i][t];
+      if (x == 0.0) continue;
+      for (int j = 0; j < k; ++j) out[i][j] += x * q[j][t];  // q^T(t, j) = q(j, t)
+    }
+}
+
+PMMF_HDI bool is_exact_identity(const double (*q)[kMaxK], int k) {
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j)
+      if (q[i][j] != (i == j ? 1.0 : 0.0)) return false;
+  return true;
+}
+
+// off_diag_norm_sq (factorizer.hpp:122-124) with std::max's NaN behaviour.
+PMMF_HDI double off_diag_norm_sq(double ns, double d) {
+  const double x = ns - d * d;
+  return (0.0 < x) ? x : 0.0;
+}
+
+}  // namespace pmmf_b200

@@ -1,0 +1,72 @@
+"""Test-only access to the two CPU checkers (never imported by the product):
+  * oracle/liboracle.so          — CPU restatement (prefix pmmf_oracle_)
+  * oracle/_ref/libpmmf_ref.so   — the reference compiled in place (prefix pmmf_ref_)
+"""
+import ctypes
+import os
+
+import numpy as np
+
+from paper_1507_04396_b200 import abi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE = os.path.join(ROOT, "oracle", "liboracle.so")
+REF = os.path.join(ROOT, "oracle", "_ref", "libpmmf_ref.so")
+
+_cache = {}
+
+
+def load(which: str) -> abi.FlatAbi:
+    if which not in _cache:
+        if which == "oracle":
+            _cache[which] = abi.FlatAbi(ORACLE, "pmmf_oracle_")
+        elif which == "ref":
+            a = abi.FlatAbi(REF, "pmmf_ref_")
+            a.lib.pmmf_ref_set_threads.argtypes = [ctypes.c_int32]
+            a.lib.pmmf_ref_residual_frobenius.argtypes = [
+                ctypes.c_void_p, ctypes.POINTER(abi.Coo), abi.c_f64p, abi.c_f64p, ctypes.c_char_p, ctypes.c_size_t]
+            _cache[which] = a
+        elif which == "gpu":
+            from paper_1507_04396_b200 import api
+            _cache[which] = api.library()
+        else:
+            raise KeyError(which)
+    return _cache[which]
+
+
+def available(which: str) -> bool:
+    return os.path.exists({"oracle": ORACLE, "ref": REF}[which])
+
+
+def factorize(which, inp, params, clusters=None):
+    """Runs one factorization through a flat ABI; returns FlatFactorization."""
+    lib = load(which)
+    n, rows, cols, vals = inp
+    coo, keep = abi.make_coo(n, rows, cols, vals, clusters)
+    h = ctypes.c_void_p()
+    err = lib.errbuf()
+    abi.raise_for(lib.factorize(ctypes.byref(coo), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+    try:
+        return lib.read_result(h)
+    finally:
+        lib.result_free(h)
+
+
+def assert_same(a, b, check_mass=True):
+    """Bit-for-bit comparison of two flat factorizations; raises with the first difference."""
+    assert a.n == b.n and a.k == b.k
+    assert np.array_equal(a.active_history, b.active_history), (a.active_history, b.active_history)
+    assert len(a.stages) == len(b.stages)
+    for s, (x, y) in enumerate(zip(a.stages, b.stages)):
+        for f in ["cluster_offsets", "members", "rot_indices", "rot_matrices", "elim_index", "elim_diagonal", "bypassed"]:
+            u, v = getattr(x, f), getattr(y, f)
+            if not (u.shape == v.shape and np.array_equal(u, v)):
+                raise AssertionError(f"stage {s + 1}: field {f} differs")
+        if check_mass and not np.array_equal(x.elim_off_mass_sq, y.elim_off_mass_sq):
+            raise AssertionError(f"stage {s + 1}: elim_off_mass_sq differs")
+    assert np.array_equal(a.core_indices, b.core_indices)
+    assert np.array_equal(a.core, b.core), "core differs"
+    assert np.array_equal(a.diag_index, b.diag_index)
+    assert np.array_equal(a.diag_value, b.diag_value), "retired diagonal differs"
+    if check_mass:
+        assert a.residual_sq == b.residual_sq, (a.residual_sq, b.residual_sq)
