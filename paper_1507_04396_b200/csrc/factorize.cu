@@ -15,6 +15,8 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -76,6 +78,21 @@ __global__ void k_core(i64 g, const int32_t* __restrict__ col_sid, const i64* __
 }
 
 using clk = std::chrono::steady_clock;
+
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PMMF_B200_TRACE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+#define PMMF_TRACE(...)                 \
+  do {                                  \
+    if (trace_on()) {                   \
+      std::fprintf(stderr, __VA_ARGS__); \
+      std::fflush(stderr);              \
+    }                                   \
+  } while (0)
 double ms_since(clk::time_point t) { return std::chrono::duration<double, std::milli>(clk::now() - t).count(); }
 
 void validate(const pmmf_b200_params& p) {  // factorizer.hpp:44-50, clustering.hpp:36-40
@@ -309,6 +326,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       }
       R->phases[1] += gram_ms;
       R->phases[2] += search_ms;
+      PMMF_TRACE("[pmmf] stage %d: gram %.2f ms, search %.2f ms\n", stage_no, gram_ms, search_ms);
     }
     if (so.error.to_host(1)[0]) fail(PMMF_INVALID_ARGUMENT, "rotation_from_gram: input not symmetric");
     std::vector<int32_t> nrot = so.nrot.to_host(std::max<i64>(rc, 1));
@@ -336,12 +354,15 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     {
       LevelPlan plan;
       build_plan(plan, so, d_out_base, d_coff, rc, slots, p.k, s);
+      PMMF_TRACE("[pmmf] stage %d: clusters=%lld slots=%lld levels=%d nnz_in=%lld\n", stage_no,
+                 static_cast<long long>(rc), static_cast<long long>(slots), plan.max_level, static_cast<long long>(A.nnz));
       if (plan.max_level > 0) {
         Paged P;
         paged_from_csc(P, std::move(A), 2 * A.nnz + (i64{1} << 20), s);
         apply_levels(P, plan, s);
         Csc T;
         transpose_paged(T, P, s);
+        const i64 cap1 = P.cap;
         P = Paged();
         Paged P2;
         const i64 tn = T.nnz;
@@ -349,11 +370,15 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         apply_levels(P2, plan, s);
         Csc B;
         transpose_paged(B, P2, s);
+        PMMF_TRACE("[pmmf] stage %d: nnz after column pass=%lld, after row pass=%lld (arena caps %lld, %lld)\n",
+                   stage_no, static_cast<long long>(tn), static_cast<long long>(B.nnz), static_cast<long long>(cap1),
+                   static_cast<long long>(P2.cap));
         A = std::move(B);
       }
     }
     PMMF_CUDA(cudaStreamSynchronize(s));
     R->phases[3] += ms_since(t0);
+    PMMF_TRACE("[pmmf] stage %d: apply %.2f ms\n", stage_no, ms_since(t0));
 
     // ---- residual accounting against the end-of-stage matrix
     const i64 ne = static_cast<i64>(order_g.size());

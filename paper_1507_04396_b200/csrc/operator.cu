@@ -1,9 +1,733 @@
-// operator.cu — placeholder, replaced below
+// operator.cu — MmfOperator (transform_ops.hpp:30-137) and the
+// preconditioned CG harness (solver.hpp:112-167, :343-349, :368-416) on the
+// device.
+//
+// apply(mode): v <- Q v (stages first to last), v <- H^(mode) v, v <- Q^T v
+// (stages last to first).  Inside a stage, rotations of different clusters
+// touch disjoint indices; inside a cluster they are replayed level by level
+// (a level = mutually independent rotations), so one CTA per (cluster, rhs
+// chunk) stages the cluster's slice of the vectors in shared memory, applies
+// all of its levels with __syncthreads between levels and writes the slice
+// back: one HBM read + write of the vectors per stage and direction, rotation
+// arithmetic bit-identical to rotate_forward / rotate_transposed.
+// Vectors are kept index-major (v[i * nrhs + r]) so a rotation touches
+// contiguous rhs lanes.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+
+#include "engine.cuh"
 #include "result.cuh"
-extern "C" {
-int pmmf_b200_operator_create(void*, double, void**, char*, size_t) { return PMMF_INTERNAL; }
-int pmmf_b200_operator_apply(void*, int32_t, int64_t, const double*, double*, int32_t, char*, size_t) { return PMMF_INTERNAL; }
-int pmmf_b200_operator_zeroed_negatives(void*, int64_t*) { return PMMF_INTERNAL; }
-void pmmf_b200_operator_free(void*) {}
-int pmmf_b200_solve(const pmmf_b200_coo*, void*, const pmmf_b200_solve_config*, int32_t*, int32_t*, int32_t*, double*, double*, char*, size_t) { return PMMF_INTERNAL; }
+#include "rng.cuh"
+#include "rotation.cuh"
+
+namespace pmmf_b200 {
+
+int guarded_call(char* err, size_t errlen, void (*fn)(void*), void* ctx);
+
+namespace {
+
+template <typename F>
+int guarded(char* err, size_t errlen, F&& f) {
+  return guarded_call(err, errlen, [](void* c) { (*static_cast<F*>(c))(); }, &f);
 }
+
+constexpr int kThreads = 256;
+constexpr size_t kSmemBudget = 200 * 1024;
+
+// ------------------------------------------------------------- host Jacobi
+// jacobi_eigensystem (dense.hpp:144-199) for the g x g core, row-major.
+void jacobi_eig(std::vector<double> a, int64_t n, std::vector<double>& values, std::vector<double>& vectors) {
+  std::vector<double> q(static_cast<size_t>(n * n), 0.0);
+  for (int64_t i = 0; i < n; ++i) q[i * n + i] = 1.0;
+  double fro = 0.0;
+  for (double v : a) fro += v * v;
+  const double scale = std::sqrt(fro);
+  if (!(scale == 0.0 || n < 2)) {
+    const double stop = 1e-15 * scale;
+    for (int sweep = 0; sweep < 64; ++sweep) {
+      double off = 0.0;
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = i + 1; j < n; ++j) off += 2.0 * a[i * n + j] * a[i * n + j];
+      if (std::sqrt(off) <= stop) break;
+      for (int64_t p = 0; p < n; ++p)
+        for (int64_t r = p + 1; r < n; ++r) {
+          if (a[p * n + r] == 0.0) continue;
+          double c = 1.0, s = 0.0;
+          {
+            const double gpp = a[p * n + p], grr = a[r * n + r], gpr = a[p * n + r];
+            const double tau = (grr - gpp) / (2.0 * gpr);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (std::abs(tau) + std::sqrt(1.0 + tau * tau));
+            c = 1.0 / std::sqrt(1.0 + t * t);
+            s = t * c;
+          }
+          for (int64_t t = 0; t < n; ++t) {
+            const double ap = a[p * n + t], ar = a[r * n + t];
+            a[p * n + t] = c * ap - s * ar;
+            a[r * n + t] = s * ap + c * ar;
+          }
+          for (int64_t t = 0; t < n; ++t) {
+            const double ap = a[t * n + p], ar = a[t * n + r];
+            a[t * n + p] = c * ap - s * ar;
+            a[t * n + r] = s * ap + c * ar;
+          }
+          a[p * n + r] = 0.0;
+          a[r * n + p] = 0.0;
+          for (int64_t t = 0; t < n; ++t) {
+            const double qp = q[p * n + t], qr = q[r * n + t];
+            q[p * n + t] = c * qp - s * qr;
+            q[r * n + t] = s * qp + c * qr;
+          }
+        }
+    }
+  }
+  values.resize(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) values[i] = a[i * n + i];
+  vectors.assign(static_cast<size_t>(n * n), 0.0);  // eigenvectors as columns: vectors(a,e) = q(e,a)
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) vectors[i * n + j] = q[j * n + i];
+}
+
+double scalar_factor(int mode, double d, double thr) {  // transform_ops.hpp:76-86
+  if (mode == PMMF_APPLY_FORWARD) return d;
+  if (mode == PMMF_APPLY_INVERSE) return std::abs(d) < thr ? 0.0 : 1.0 / d;
+  return d < thr ? 0.0 : 1.0 / std::sqrt(d);
+}
+
+// ------------------------------------------------------------- kernels
+struct StageDev {
+  int64_t nclusters = 0;
+  int64_t max_c = 0;
+  DBuf<int32_t> members;   // stage partition, global ids
+  DBuf<int64_t> coff;      // cluster offsets
+  DBuf<int64_t> rot_ptr;   // per cluster [rot_ptr[u], rot_ptr[u+1]) in level order
+  DBuf<int64_t> lvl_ptr;   // per cluster level boundaries: lvl_ptr[lvl_base[u] + L]
+  DBuf<int64_t> lvl_base;  // per cluster
+  DBuf<int32_t> nlev;      // per cluster
+  DBuf<int32_t> loc;       // R x k local positions
+  DBuf<double> q;          // R x k x k
+};
+
+template <bool kTransposed>
+__global__ void k_stage_apply(int k, int nrhs, int rc, const int64_t* __restrict__ coff,
+                              const int32_t* __restrict__ members, const int64_t* __restrict__ rot_ptr,
+                              const int64_t* __restrict__ lvl_ptr, const int64_t* __restrict__ lvl_base,
+                              const int32_t* __restrict__ nlev, const int32_t* __restrict__ loc,
+                              const double* __restrict__ qs, double* __restrict__ V, bool smem_ok) {
+  extern __shared__ double sm[];
+  const int u = blockIdx.x;
+  const int r0 = blockIdx.y * rc;
+  const int nr = min(rc, nrhs - r0);
+  if (rot_ptr[u + 1] == rot_ptr[u] || nr <= 0) return;
+  const int64_t off = coff[u];
+  const int c = static_cast<int>(coff[u + 1] - off);
+  const int L = nlev[u];
+  const int64_t* lp = lvl_ptr + lvl_base[u];
+  if (smem_ok) {
+    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(c) * nr; i += blockDim.x) {
+      const int64_t li = i / nr, r = i % nr;
+      sm[li * rc + r] = V[static_cast<int64_t>(members[off + li]) * nrhs + r0 + r];
+    }
+    __syncthreads();
+  }
+  for (int lv = 0; lv < L; ++lv) {
+    const int l = kTransposed ? (L - 1 - lv) : lv;
+    const int64_t b = lp[l], e = lp[l + 1];
+    for (int64_t i = threadIdx.x; i < (e - b) * nr; i += blockDim.x) {
+      const int64_t t = b + i / nr;
+      const int r = static_cast<int>(i % nr);
+      double vals[kMaxK];
+      int64_t addr[kMaxK];
+      for (int x = 0; x < k; ++x) {
+        const int li = loc[t * k + x];
+        addr[x] = smem_ok ? static_cast<int64_t>(li) * rc + r
+                          : static_cast<int64_t>(members[off + li]) * nrhs + r0 + r;
+        vals[x] = smem_ok ? sm[addr[x]] : V[addr[x]];
+      }
+      const double* q = qs + t * k * k;
+      for (int a = 0; a < k; ++a) {
+        double acc = 0.0;
+        for (int x = 0; x < k; ++x) acc = dadd(acc, dmul(kTransposed ? q[x * k + a] : q[a * k + x], vals[x]));
+        if (smem_ok)
+          sm[addr[a]] = acc;
+        else
+          V[addr[a]] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  if (smem_ok) {
+    for (int64_t i = threadIdx.x; i < static_cast<int64_t>(c) * nr; i += blockDim.x) {
+      const int64_t li = i / nr, r = i % nr;
+      V[static_cast<int64_t>(members[off + li]) * nrhs + r0 + r] = sm[li * rc + r];
+    }
+  }
+}
+
+// Core: y = E f(lambda) E^T x on the core indices (transform_ops.hpp:88-106),
+// one CTA per rhs.
+__global__ void k_core_apply(int64_t g, int nrhs, const int32_t* __restrict__ cidx, const double* __restrict__ E,
+                             const double* __restrict__ f, double* __restrict__ V) {
+  extern __shared__ double sm[];
+  double* x = sm;
+  double* dot = sm + g;
+  const int r = blockIdx.x;
+  for (int64_t a = threadIdx.x; a < g; a += blockDim.x) x[a] = V[static_cast<int64_t>(cidx[a]) * nrhs + r];
+  __syncthreads();
+  for (int64_t e = threadIdx.x; e < g; e += blockDim.x) {
+    double d = 0.0;
+    for (int64_t a = 0; a < g; ++a) d = dadd(d, dmul(E[a * g + e], x[a]));
+    dot[e] = dmul(d, f[e]);
+  }
+  __syncthreads();
+  for (int64_t a = threadIdx.x; a < g; a += blockDim.x) {
+    double y = 0.0;
+    for (int64_t e = 0; e < g; ++e) y = dadd(y, dmul(E[a * g + e], dot[e]));
+    V[static_cast<int64_t>(cidx[a]) * nrhs + r] = y;
+  }
+}
+
+__global__ void k_diag_scale(int64_t nd, int nrhs, const int32_t* __restrict__ idx, const double* __restrict__ f,
+                             double* __restrict__ V) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nd * nrhs) return;
+  const int64_t d = i / nrhs;
+  const int r = static_cast<int>(i % nrhs);
+  double& v = V[static_cast<int64_t>(idx[d]) * nrhs + r];
+  v = dmul(v, f[d]);
+}
+
+// rhs-major <-> index-major
+__global__ void k_to_imaj(int64_t n, int nrhs, const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n * nrhs) return;
+  const int64_t idx = i / nrhs, r = i % nrhs;
+  out[i] = in[r * n + idx];
+}
+__global__ void k_from_imaj(int64_t n, int nrhs, const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n * nrhs) return;
+  const int64_t r = i / n, idx = i % n;
+  out[i] = in[idx * nrhs + r];
+}
+
+}  // namespace
+
+// ============================================================== Operator
+struct Operator {
+  int device = 0;
+  int64_t n = 0;
+  int k = 2;
+  double thr = 1e-12;
+  int64_t neg = 0;
+  std::vector<StageDev> stages;
+  int64_t g = 0;
+  DBuf<int32_t> core_idx;
+  DBuf<double> E;
+  DBuf<double> core_f[3];
+  int64_t nd = 0;
+  DBuf<int32_t> diag_idx;
+  DBuf<double> diag_f[3];
+  cudaStream_t s = nullptr;
+
+  ~Operator() {
+    stages.clear();
+    core_idx.release();
+    E.release();
+    for (auto& x : core_f) x.release();
+    diag_idx.release();
+    for (auto& x : diag_f) x.release();
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+
+  void build(const Result& f) {
+    PMMF_CUDA(cudaGetDevice(&device));
+    PMMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    n = f.n;
+    k = f.k;
+    for (const auto& st : f.stages) {
+      StageDev sd;
+      const int64_t m = static_cast<int64_t>(st.off.size()) - 1;
+      sd.nclusters = m;
+      std::vector<int64_t> pos_of(static_cast<size_t>(n), -1), cl_of(static_cast<size_t>(n), -1);
+      for (int64_t u = 0; u < m; ++u) {
+        sd.max_c = std::max<int64_t>(sd.max_c, st.off[u + 1] - st.off[u]);
+        for (int64_t i = st.off[u]; i < st.off[u + 1]; ++i) {
+          pos_of[st.members[i]] = i - st.off[u];
+          cl_of[st.members[i]] = u;
+        }
+      }
+      const int64_t R = static_cast<int64_t>(st.rot_idx.size()) / k;
+      // per cluster: non-identity rotations with their dependency level
+      std::vector<std::vector<std::pair<int32_t, int64_t>>> per(static_cast<size_t>(m));  // (level, t)
+      std::vector<int32_t> lastlvl(static_cast<size_t>(n), 0);
+      for (int64_t t = 0; t < R; ++t) {
+        const double* q = st.rot_q.data() + t * k * k;
+        bool ident = true;
+        for (int a = 0; a < k; ++a)
+          for (int b = 0; b < k; ++b) ident = ident && q[a * k + b] == (a == b ? 1.0 : 0.0);
+        if (ident) continue;  // value-neutral
+        const int64_t u = cl_of[st.rot_idx[t * k]];
+        if (u < 0) fail(PMMF_INVALID_ARGUMENT, "MmfOperator: rotation index not in its stage partition");
+        int32_t lv = 0;
+        for (int a = 0; a < k; ++a) {
+          if (cl_of[st.rot_idx[t * k + a]] != u) fail(PMMF_INVALID_ARGUMENT, "MmfOperator: rotation spans clusters");
+          lv = std::max(lv, lastlvl[st.rot_idx[t * k + a]]);
+        }
+        ++lv;
+        for (int a = 0; a < k; ++a) lastlvl[st.rot_idx[t * k + a]] = lv;
+        per[u].push_back({lv, t});
+      }
+      std::vector<int64_t> rot_ptr(1, 0), lvl_ptr, lvl_base, coff(st.off.begin(), st.off.end());
+      std::vector<int32_t> nlev, loc, mem(st.members.begin(), st.members.end());
+      std::vector<double> qv;
+      for (int64_t u = 0; u < m; ++u) {
+        auto& v = per[u];
+        std::stable_sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        lvl_base.push_back(static_cast<int64_t>(lvl_ptr.size()));
+        const int32_t L = v.empty() ? 0 : v.back().first;
+        nlev.push_back(L);
+        int64_t cur = rot_ptr.back();
+        size_t i = 0;
+        for (int32_t lv = 1; lv <= L; ++lv) {
+          lvl_ptr.push_back(cur);
+          while (i < v.size() && v[i].first == lv) {
+            const int64_t t = v[i].second;
+            for (int a = 0; a < k; ++a) loc.push_back(static_cast<int32_t>(pos_of[st.rot_idx[t * k + a]]));
+            qv.insert(qv.end(), st.rot_q.begin() + t * k * k, st.rot_q.begin() + (t + 1) * k * k);
+            ++cur;
+            ++i;
+          }
+        }
+        lvl_ptr.push_back(cur);
+        rot_ptr.push_back(cur);
+      }
+      auto up64 = [&](DBuf<int64_t>& d, const std::vector<int64_t>& h) {
+        d.alloc(std::max<int64_t>(1, static_cast<int64_t>(h.size())), s);
+        d.upload(h);
+      };
+      auto up32 = [&](DBuf<int32_t>& d, const std::vector<int32_t>& h) {
+        d.alloc(std::max<int64_t>(1, static_cast<int64_t>(h.size())), s);
+        d.upload(h);
+      };
+      up32(sd.members, mem);
+      up64(sd.coff, coff);
+      up64(sd.rot_ptr, rot_ptr);
+      up64(sd.lvl_ptr, lvl_ptr);
+      up64(sd.lvl_base, lvl_base);
+      up32(sd.nlev, nlev);
+      up32(sd.loc, loc);
+      sd.q.alloc(std::max<int64_t>(1, static_cast<int64_t>(qv.size())), s);
+      sd.q.upload(qv);
+      PMMF_CUDA(cudaStreamSynchronize(s));
+      stages.push_back(std::move(sd));
+    }
+    // core eigensystem (transform_ops.hpp:34-41)
+    g = static_cast<int64_t>(f.core_idx.size());
+    std::vector<double> vals, vecs;
+    jacobi_eig(f.core, g, vals, vecs);
+    for (double l : vals)
+      if (l < -thr) ++neg;
+    for (const auto& d : f.diag)
+      if (d.second < -thr) ++neg;
+    if (g > 0) {
+      std::vector<int32_t> ci(f.core_idx.begin(), f.core_idx.end());
+      core_idx.alloc(g, s);
+      core_idx.upload(ci);
+      E.alloc(g * g, s);
+      E.upload(vecs);
+      for (int mode = 0; mode < 3; ++mode) {
+        std::vector<double> fv(static_cast<size_t>(g));
+        for (int64_t e = 0; e < g; ++e) fv[e] = scalar_factor(mode, vals[e], thr);
+        core_f[mode].alloc(g, s);
+        core_f[mode].upload(fv);
+      }
+    }
+    nd = static_cast<int64_t>(f.diag.size());
+    if (nd > 0) {
+      std::vector<int32_t> di(static_cast<size_t>(nd));
+      for (int64_t i = 0; i < nd; ++i) di[i] = static_cast<int32_t>(f.diag[i].first);
+      diag_idx.alloc(nd, s);
+      diag_idx.upload(di);
+      for (int mode = 0; mode < 3; ++mode) {
+        std::vector<double> fv(static_cast<size_t>(nd));
+        for (int64_t i = 0; i < nd; ++i) fv[i] = scalar_factor(mode, f.diag[i].second, thr);
+        diag_f[mode].alloc(nd, s);
+        diag_f[mode].upload(fv);
+      }
+    }
+    PMMF_CUDA(cudaStreamSynchronize(s));
+  }
+
+  void run_stage(const StageDev& sd, bool transposed, int nrhs, double* V, cudaStream_t st) const {
+    if (sd.nclusters == 0) return;
+    int rc = std::min(nrhs, 8);
+    while (rc > 1 && static_cast<size_t>(sd.max_c) * rc * 8 > kSmemBudget) rc >>= 1;
+    const bool smem_ok = static_cast<size_t>(sd.max_c) * rc * 8 <= kSmemBudget;
+    const size_t smem = smem_ok ? static_cast<size_t>(sd.max_c) * rc * 8 : 0;
+    dim3 grid(static_cast<unsigned>(sd.nclusters), static_cast<unsigned>((nrhs + rc - 1) / rc));
+    auto kern = transposed ? k_stage_apply<true> : k_stage_apply<false>;
+    if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kern<<<grid, kThreads, smem, st>>>(k, nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(), sd.lvl_ptr.get(),
+                                       sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(), sd.q.get(), V, smem_ok);
+    launch_counter().fetch_add(1, std::memory_order_relaxed);
+    PMMF_CUDA(cudaGetLastError());
+  }
+
+  // V: index-major n x nrhs on the device.
+  void apply_dev(int mode, int nrhs, double* V, cudaStream_t st) const {
+    for (const auto& sd : stages) run_stage(sd, false, nrhs, V, st);
+    if (g > 0) {
+      const size_t smem = static_cast<size_t>(2 * g) * 8;
+      if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(k_core_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      PMMF_LAUNCH(k_core_apply, static_cast<unsigned>(nrhs), kThreads, smem, st, g, nrhs, core_idx.get(), E.get(),
+                  core_f[mode].get(), V);
+    }
+    if (nd > 0)
+      PMMF_LAUNCH(k_diag_scale, blocks_for(nd * nrhs, kThreads), kThreads, 0, st, nd, nrhs, diag_idx.get(),
+                  diag_f[mode].get(), V);
+    for (auto it = stages.rbegin(); it != stages.rend(); ++it) run_stage(*it, true, nrhs, V, st);
+  }
+};
+
+// ====================================================== CG (solver.hpp)
+namespace {
+
+// y[g(row)*nrhs + r] = sum over the row's columns (input-partition order) of
+// a * x, skipping x == 0 (multiply_flat, blocked_matrix.hpp:390-407).
+// Warp per row, lane per rhs.
+__global__ void k_spmv(int64_t N, int nrhs, const int64_t* __restrict__ ptr, const int32_t* __restrict__ col,
+                       const double* __restrict__ val, const int32_t* __restrict__ s2g, const double* __restrict__ X,
+                       double* __restrict__ Y) {
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= N) return;
+  const int64_t gr = s2g[w];
+  for (int r = lane; r < nrhs; r += 32) {
+    double acc = 0.0;
+    for (int64_t e = ptr[w]; e < ptr[w + 1]; ++e) {
+      const double x = X[static_cast<int64_t>(s2g[col[e]]) * nrhs + r];
+      if (x == 0.0) continue;
+      acc = dadd(acc, dmul(val[e], x));
+    }
+    Y[gr * nrhs + r] = acc;
+  }
+}
+
+// Deterministic per-rhs dot products: fixed grid of partials, then a fixed
+// order final pass (no atomics).
+constexpr int kDotBlocks = 296;
+__global__ void k_dot_partial(int64_t n, int nrhs, const double* __restrict__ a, const double* __restrict__ b,
+                              double* __restrict__ part) {
+  __shared__ double red[kThreads];
+  for (int r = 0; r < nrhs; ++r) {
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+      s = dadd(s, dmul(a[i * nrhs + r], b[i * nrhs + r]));
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] = dadd(red[threadIdx.x], red[threadIdx.x + o]);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part[static_cast<int64_t>(r) * gridDim.x + blockIdx.x] = red[0];
+    __syncthreads();
+  }
+}
+__global__ void k_dot_final(int nrhs, int nparts, const double* __restrict__ part, double* __restrict__ out) {
+  const int r = threadIdx.x;
+  if (r >= nrhs) return;
+  double s = 0.0;
+  for (int p = 0; p < nparts; ++p) s = dadd(s, part[static_cast<int64_t>(r) * nparts + p]);
+  out[r] = s;
+}
+
+struct CgState {
+  double* rr;
+  double* pap;
+  double* res;
+  double* rrn;
+  double* alpha;
+  double* bnorm;
+  int32_t* active;
+  int32_t* iters;
+  int32_t* conv;
+  int32_t* brk;
+  double* trace;
+  int stride;
+  double tol;
+};
+
+__global__ void k_cg_alpha(int nrhs, CgState S) {
+  const int r = threadIdx.x;
+  if (r >= nrhs || !S.active[r]) return;
+  if (!(S.pap[r] > 0.0)) {
+    S.brk[r] = 1;
+    S.active[r] = 0;
+    S.alpha[r] = 0.0;
+    return;
+  }
+  S.alpha[r] = S.rr[r] / S.pap[r];
+}
+// y += alpha p; r -= alpha w (active rhs only; alpha = 0 otherwise is not used)
+__global__ void k_cg_update(int64_t n, int nrhs, const int32_t* __restrict__ active, const double* __restrict__ alpha,
+                            const double* __restrict__ p, const double* __restrict__ w, double* __restrict__ y,
+                            double* __restrict__ rv) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n * nrhs) return;
+  const int r = static_cast<int>(i % nrhs);
+  if (!active[r]) return;
+  y[i] = dadd(y[i], dmul(alpha[r], p[i]));
+  rv[i] = dsub(rv[i], dmul(alpha[r], w[i]));
+}
+__global__ void k_sub(int64_t m, const double* __restrict__ b, const double* __restrict__ t, double* __restrict__ o) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < m) o[i] = dsub(b[i], t[i]);
+}
+__global__ void k_cg_check(int nrhs, int it, CgState S) {
+  const int r = threadIdx.x;
+  if (r >= nrhs || !S.active[r]) return;
+  const double res = sqrt(S.res[r]);
+  S.trace[static_cast<int64_t>(r) * S.stride + it] = res;
+  S.iters[r] = it;
+  if (res / S.bnorm[r] <= S.tol) {
+    S.conv[r] = 1;
+    S.active[r] = 0;
+  }
+}
+__global__ void k_cg_beta(int64_t n, int nrhs, const int32_t* __restrict__ active, const double* __restrict__ rrn,
+                          double* __restrict__ rr, const double* __restrict__ rv, double* __restrict__ p) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n * nrhs) return;
+  const int r = static_cast<int>(i % nrhs);
+  if (!active[r]) return;
+  const double beta = rrn[r] / rr[r];
+  p[i] = dadd(rv[i], dmul(beta, p[i]));
+}
+__global__ void k_cg_rr(int nrhs, const int32_t* __restrict__ active, const double* __restrict__ rrn, double* __restrict__ rr) {
+  const int r = threadIdx.x;
+  if (r < nrhs && active[r]) rr[r] = rrn[r];
+}
+
+}  // namespace
+}  // namespace pmmf_b200
+
+using namespace pmmf_b200;
+
+extern "C" {
+
+int pmmf_b200_operator_create(void* result, double zero_threshold, void** op, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!result || !op) fail(PMMF_INVALID_ARGUMENT, "operator_create: null argument");
+    auto o = std::make_unique<Operator>();
+    o->thr = zero_threshold;
+    o->build(*static_cast<Result*>(result));
+    *op = o.release();
+  });
+}
+
+int pmmf_b200_operator_apply(void* opv, int32_t mode, int64_t nrhs, const double* in, double* out, int32_t on_device,
+                             char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto* o = static_cast<Operator*>(opv);
+    if (mode < 0 || mode > 2) fail(PMMF_INVALID_ARGUMENT, "MmfOperator::apply: bad mode");
+    if (nrhs < 1) return;
+    PMMF_CUDA(cudaSetDevice(o->device));
+    cudaStream_t s = o->s;
+    const int64_t m = o->n * nrhs;
+    DBuf<double> a(m, s), b(m, s);
+    if (on_device)
+      PMMF_CUDA(cudaMemcpyAsync(a.get(), in, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    else
+      a.upload(in, m);
+    PMMF_LAUNCH(k_to_imaj, blocks_for(m, kThreads), kThreads, 0, s, o->n, static_cast<int>(nrhs), a.get(), b.get());
+    o->apply_dev(mode, static_cast<int>(nrhs), b.get(), s);
+    PMMF_LAUNCH(k_from_imaj, blocks_for(m, kThreads), kThreads, 0, s, o->n, static_cast<int>(nrhs), b.get(), a.get());
+    if (on_device)
+      PMMF_CUDA(cudaMemcpyAsync(out, a.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    else
+      a.download(out, m);
+    PMMF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int pmmf_b200_operator_zeroed_negatives(void* op, int64_t* out) {
+  *out = static_cast<Operator*>(op)->neg;
+  return PMMF_OK;
+}
+
+void pmmf_b200_operator_free(void* op) { delete static_cast<Operator*>(op); }
+
+int pmmf_b200_solve(const pmmf_b200_coo* a, void* opv, const pmmf_b200_solve_config* cfg, int32_t* iterations,
+                    int32_t* converged, int32_t* breakdown, double* residuals, double* wall_ms, char* err,
+                    size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!(cfg->tol > 0.0)) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: tol must be positive");
+    if (cfg->max_iter < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: max_iter < 1");
+    if (cfg->rhs_count < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: rhs_count < 1");
+    if (cfg->rhs_count > 1024) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: rhs_count > 1024 unsupported");
+    auto* o = static_cast<Operator*>(opv);
+    PMMF_CUDA(cudaSetDevice(a->device));
+    cudaStream_t s;
+    PMMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    } sg{s};
+    const auto start = std::chrono::steady_clock::now();
+    const int64_t n = a->n;
+    const int nr = cfg->rhs_count;
+    if (o && o->n != n) fail(PMMF_INVALID_ARGUMENT, "pcg_symmetric: operator dimension mismatch");
+    // Matrix rows in input-partition order for y = A x.
+    Numbering nb;
+    {
+      std::vector<std::vector<int64_t>> init;
+      if (a->n_clusters == 0) {
+        init.emplace_back(static_cast<size_t>(n));
+        std::iota(init[0].begin(), init[0].end(), int64_t{0});
+      } else {
+        for (int64_t u = 0; u < a->n_clusters; ++u)
+          init.emplace_back(a->cluster_members + a->cluster_offsets[u], a->cluster_members + a->cluster_offsets[u + 1]);
+      }
+      nb.build(init, n, s);
+    }
+    Csc A;
+    {
+      const int64_t* rows = a->rows;
+      const int64_t* cols = a->cols;
+      const double* vals = a->vals;
+      DBuf<int64_t> dr, dc;
+      DBuf<double> dv;
+      if (!a->on_device && a->nnz > 0) {
+        dr.alloc(a->nnz, s);
+        dc.alloc(a->nnz, s);
+        dv.alloc(a->nnz, s);
+        dr.upload(a->rows, a->nnz);
+        dc.upload(a->cols, a->nnz);
+        dv.upload(a->vals, a->nnz);
+        rows = dr.get();
+        cols = dc.get();
+        vals = dv.get();
+      }
+      csc_from_coo(A, nb, n, a->nnz, rows, cols, vals, s);
+    }
+    Csc Arow;  // transpose: per row (stage id), columns ascending in stage order
+    {
+      Paged P;
+      const int64_t nz = A.nnz;
+      paged_from_csc(P, std::move(A), 1, s);
+      (void)nz;
+      transpose_paged(Arow, P, s);
+    }
+    // right-hand sides (solver.hpp:375-381), bnorm on the host in order
+    std::vector<double> hb(static_cast<size_t>(n * nr)), bimaj(static_cast<size_t>(n * nr)), bn(static_cast<size_t>(nr));
+    for (int r = 0; r < nr; ++r) {
+      const uint64_t path[2] = {0xB0u, static_cast<uint64_t>(r)};
+      Xoshiro rng(derive(cfg->seed, path));
+      double* b = hb.data() + static_cast<int64_t>(r) * n;
+      for (int64_t i = 0; i < n; ++i) b[i] = normal_draw(rng);
+      double sq = 0.0;
+      for (int64_t i = 0; i < n; ++i) sq += b[i] * b[i];
+      const double norm = std::sqrt(sq);
+      if (norm > 0.0)
+        for (int64_t i = 0; i < n; ++i) b[i] /= norm;
+      double s2 = 0.0;
+      for (int64_t i = 0; i < n; ++i) s2 += b[i] * b[i];
+      bn[r] = std::sqrt(s2);
+      for (int64_t i = 0; i < n; ++i) bimaj[i * nr + r] = b[i];
+    }
+    const int stride = cfg->max_iter + 1;
+    for (int64_t i = 0; i < static_cast<int64_t>(nr) * stride; ++i) residuals[i] = NAN;
+    std::vector<int32_t> act(static_cast<size_t>(nr), 1), zero(static_cast<size_t>(nr), 0);
+    for (int r = 0; r < nr; ++r) {
+      residuals[static_cast<int64_t>(r) * stride] = bn[r];
+      iterations[r] = 0;
+      converged[r] = 0;
+      breakdown[r] = 0;
+      if (bn[r] == 0.0) {
+        converged[r] = 1;
+        act[r] = 0;
+      }
+    }
+    const int64_t m = n * nr;
+    DBuf<double> B(m, s), Y(m, s), Rv(m, s), Pv(m, s), W(m, s), T1(m, s), T2(m, s), X(m, s);
+    B.upload(bimaj);
+    Y.zero();
+    DBuf<double> part(static_cast<int64_t>(kDotBlocks) * nr, s);
+    DBuf<double> rr(nr, s), pap(nr, s), res(nr, s), rrn(nr, s), alpha(nr, s), dbn(nr, s);
+    DBuf<int32_t> dact(nr, s), diters(nr, s), dconv(nr, s), dbrk(nr, s);
+    DBuf<double> trace(static_cast<int64_t>(nr) * stride, s);
+    dbn.upload(bn);
+    dact.upload(act);
+    diters.upload(zero);
+    dconv.upload(zero);
+    dbrk.upload(zero);
+    trace.fill_bytes(0xff);  // NaN pattern
+    auto pre = [&](const DBuf<double>& in, DBuf<double>& out) {
+      PMMF_CUDA(cudaMemcpyAsync(out.get(), in.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+      if (o) o->apply_dev(PMMF_APPLY_INV_SQRT, nr, out.get(), s);
+    };
+    auto spmv = [&](const DBuf<double>& x, DBuf<double>& y) {
+      y.zero();
+      PMMF_LAUNCH(k_spmv, blocks_for(Arow.N * 32, kThreads), kThreads, 0, s, Arow.N, nr, Arow.ptr.get(), Arow.row.get(),
+                  Arow.val.get(), nb.d_s2g.get(), x.get(), y.get());
+    };
+    auto dot = [&](const DBuf<double>& x, const DBuf<double>& y, DBuf<double>& out) {
+      PMMF_LAUNCH(k_dot_partial, kDotBlocks, kThreads, 0, s, n, nr, x.get(), y.get(), part.get());
+      PMMF_LAUNCH(k_dot_final, 1, std::max(32, ((nr + 31) / 32) * 32), 0, s, nr, kDotBlocks, part.get(), out.get());
+    };
+    CgState S{rr.get(), pap.get(), res.get(), rrn.get(), alpha.get(), dbn.get(), dact.get(), diters.get(),
+              dconv.get(), dbrk.get(), trace.get(), stride, cfg->tol};
+    const int th = std::max(32, ((nr + 31) / 32) * 32);
+    pre(B, Rv);  // r = K^-1 b
+    PMMF_CUDA(cudaMemcpyAsync(Pv.get(), Rv.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    dot(Rv, Rv, rr);
+    for (int it = 1; it <= cfg->max_iter; ++it) {
+      pre(Pv, T1);
+      spmv(T1, T2);
+      pre(T2, W);
+      dot(Pv, W, pap);
+      PMMF_LAUNCH(k_cg_alpha, 1, th, 0, s, nr, S);
+      PMMF_LAUNCH(k_cg_update, blocks_for(m, kThreads), kThreads, 0, s, n, nr, dact.get(), alpha.get(), Pv.get(),
+                  W.get(), Y.get(), Rv.get());
+      pre(Y, X);
+      spmv(X, T2);
+      PMMF_LAUNCH(k_sub, blocks_for(m, kThreads), kThreads, 0, s, m, B.get(), T2.get(), T1.get());
+      dot(T1, T1, res);
+      PMMF_LAUNCH(k_cg_check, 1, th, 0, s, nr, it, S);
+      dot(Rv, Rv, rrn);
+      PMMF_LAUNCH(k_cg_beta, blocks_for(m, kThreads), kThreads, 0, s, n, nr, dact.get(), rrn.get(), rr.get(), Rv.get(),
+                  Pv.get());
+      PMMF_LAUNCH(k_cg_rr, 1, th, 0, s, nr, dact.get(), rrn.get(), rr.get());
+      if (it % 8 == 0 || it == cfg->max_iter) {
+        std::vector<int32_t> h = dact.to_host(nr);
+        bool any = false;
+        for (int r = 0; r < nr; ++r) any |= h[r] != 0;
+        if (!any) break;
+      }
+    }
+    std::vector<int32_t> hi = diters.to_host(nr), hc = dconv.to_host(nr), hbk = dbrk.to_host(nr);
+    std::vector<double> ht = trace.to_host(static_cast<int64_t>(nr) * stride);
+    for (int r = 0; r < nr; ++r) {
+      if (bn[r] == 0.0) continue;
+      iterations[r] = hi[r];
+      converged[r] = hc[r];
+      breakdown[r] = hbk[r];
+      for (int i = 1; i < stride; ++i) residuals[static_cast<int64_t>(r) * stride + i] = ht[static_cast<int64_t>(r) * stride + i];
+    }
+    *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+  });
+}
+
+}  // extern "C"

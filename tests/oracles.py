@@ -70,3 +70,63 @@ def assert_same(a, b, check_mass=True):
     assert np.array_equal(a.diag_value, b.diag_value), "retired diagonal differs"
     if check_mass:
         assert a.residual_sq == b.residual_sq, (a.residual_sq, b.residual_sq)
+
+
+def result_handle(which, inp, params, clusters=None):
+    lib = load(which)
+    n, rows, cols, vals = inp
+    coo, keep = abi.make_coo(n, rows, cols, vals, clusters)
+    h = ctypes.c_void_p()
+    err = lib.errbuf()
+    abi.raise_for(lib.factorize(ctypes.byref(coo), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+    return lib, h
+
+
+def operator_apply(which, inp, params, mode, vecs, thr=1e-12, clusters=None):
+    """Factorize, build the MmfOperator, apply `mode` to the rhs-major vecs."""
+    lib, h = result_handle(which, inp, params, clusters)
+    op = ctypes.c_void_p()
+    err = lib.errbuf()
+    try:
+        abi.raise_for(lib.operator_create(h, thr, ctypes.byref(op), err, len(err)), err)
+    finally:
+        lib.result_free(h)
+    try:
+        vecs = np.ascontiguousarray(vecs, np.float64)
+        out = np.zeros_like(vecs)
+        nrhs = vecs.shape[0]
+        abi.raise_for(lib.operator_apply(op, mode, nrhs, vecs.ctypes.data, out.ctypes.data, 0, err, len(err)), err)
+        neg = ctypes.c_int64()
+        lib.operator_zeroed_negatives(op, ctypes.byref(neg))
+        return out, neg.value
+    finally:
+        lib.operator_free(op)
+
+
+def solve(which, inp, params, tol, max_iter, rhs_count, seed, precondition=True):
+    """run_solve_experiment through a flat ABI: returns (iters, conv, brk, traces, wall_ms)."""
+    lib, h = result_handle(which, inp, params) if precondition else (load(which), None)
+    op = ctypes.c_void_p()
+    err = lib.errbuf()
+    if precondition:
+        try:
+            abi.raise_for(lib.operator_create(h, 1e-12, ctypes.byref(op), err, len(err)), err)
+        finally:
+            lib.result_free(h)
+    n, rows, cols, vals = inp
+    coo, keep = abi.make_coo(n, rows, cols, vals)
+    cfg = abi.SolveConfig(tol, max_iter, rhs_count, seed)
+    it = np.zeros(rhs_count, np.int32)
+    cv = np.zeros(rhs_count, np.int32)
+    bk = np.zeros(rhs_count, np.int32)
+    tr = np.zeros((rhs_count, max_iter + 1))
+    wall = ctypes.c_double()
+    try:
+        abi.raise_for(
+            lib.solve(ctypes.byref(coo), op if precondition else None, ctypes.byref(cfg),
+                      it.ctypes.data_as(abi.c_i32p), cv.ctypes.data_as(abi.c_i32p), bk.ctypes.data_as(abi.c_i32p),
+                      tr.ctypes.data_as(abi.c_f64p), ctypes.byref(wall), err, len(err)), err)
+    finally:
+        if precondition:
+            lib.operator_free(op)
+    return it, cv, bk, tr, wall.value

@@ -1,0 +1,48 @@
+"""GPU MmfOperator (transform_ops.hpp:30-137) and CG harness (solver.hpp)
+against the CPU oracle on the same seeded factorizations.
+
+apply/apply_inverse/apply_inv_sqrt are bit-for-bit (same rotation
+arithmetic, same core Jacobi).  CG traces use deterministic tree
+reductions for the dot products instead of the reference's sequential sums
+over n, so they agree to a tolerance (stated per assertion), not bitwise."""
+import numpy as np
+import pytest
+
+import cases
+import oracles
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["grid32_m16", "rmat12_m16", "rbf256_k3", "dense256_m2", "partitioned_input", "zero_cols_bypass"])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_apply_bitwise(name, mode):
+    inp, params, part = cases.build(name)
+    rng = np.random.default_rng(17)
+    vecs = rng.standard_normal((5, inp[0]))
+    g, gneg = oracles.operator_apply("gpu", inp, params, mode, vecs, clusters=part)
+    o, oneg = oracles.operator_apply("oracle", inp, params, mode, vecs, clusters=part)
+    assert gneg == oneg
+    assert np.array_equal(g, o)
+
+
+def test_apply_matches_reference_library():
+    inp, params, part = cases.build("grid64_m16")
+    vecs = np.random.default_rng(3).standard_normal((3, inp[0]))
+    g, _ = oracles.operator_apply("gpu", inp, params, 2, vecs)
+    r, _ = oracles.operator_apply("ref", inp, params, 2, vecs)
+    assert np.array_equal(g, r)
+
+
+@pytest.mark.parametrize("precondition", [True, False])
+def test_cg_traces(precondition):
+    inp = cases.api.workload_aniso_grid(48)
+    params = cases.make_params(m_target=16, seed=42)
+    gi, gc, gb, gt, _ = oracles.solve("gpu", inp, params, 1e-8, 3000, 4, 5, precondition)
+    oi, oc, ob, ot, _ = oracles.solve("oracle", inp, params, 1e-8, 3000, 4, 5, precondition)
+    assert np.array_equal(gc, oc) and np.array_equal(gb, ob)
+    # iteration counts within 2% (rounding of the dot products differs)
+    assert np.all(np.abs(gi - oi) <= np.maximum(2, 0.02 * oi)), (gi, oi)
+    # the first 20 residuals agree to 1e-9 relative
+    k = 20
+    assert np.allclose(gt[:, :k], ot[:, :k], rtol=1e-9, atol=0)
