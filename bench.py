@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""bench.py — pMMF factorization throughput on BASELINE.json config 4.
+
+Workload (BASELINE.json configs[3]): R-MAT scale 20
+(n = 1,048,576, 16·n edge samples, a,b,c,d = .57,.19,.19,.05, seed 42),
+normalized Laplacian + 1e-2·I (nnz ≈ 3.2e7, fp64), factorized with k=2, P=15,
+m=512, eta=0.5, c_min=10, c_max=10000, D_max=500, bypass on, seed 42.
+A step = one complete pmmf::factorize (every stage: clustering, reblock,
+Gram, search, apply, residual, core) of that matrix.
+
+  value : rotations/s with the input triplets already resident in HBM
+          (C-ABI call with device pointers), max step time over ranks.
+  e2e   : the same through the C-ABI with HOST buffers: H2D of the triplets
+          and D2H of the whole MmfFactorization inside the timed region.
+  roofline : the dominant kernel (rotation stream write pass), algorithmic
+          bytes per SURVEY.md §8(d) ÷ its CUDA-event time, against the
+          measured HBM copy bandwidth (MEASURED_PEAKS.json).
+  cpu_baseline : the reference compiled in place (oracle/_ref) on the host
+          cores, on a bounded sample of the same recipe (R-MAT scale 14, m=512).
+
+Multi-GPU (--gpus N under torchrun): every rank factorizes its own replica
+(weak scaling, "replicas"; cluster sharding with an NCCL reblock is not built
+yet — DESIGN.md §6).  --impl reference runs the reference's CPU path instead.
+"""
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pMMF factorization throughput, R-MAT n=1M (config 4)"
+UNIT = "rotations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=20, help="R-MAT scale (20 = BASELINE config 4)")
+    ap.add_argument("--cpu-scale", type=int, default=14, help="R-MAT scale of the bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def config_params():
+    from paper_1507_04396_b200.abi import make_params
+
+    return make_params(k=2, n_stages=15, eta=0.5, m_target=512, c_min=10, c_max=10000, d_max=500,
+                       bypass_enabled=True, core_min=10, core_cap=4096, seed=42)
+
+
+def workload(scale):
+    from paper_1507_04396_b200 import api
+
+    return api.workload_rmat(scale, 32, 42, 1e-2)
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_reference_run(scale, threads, steps=1, warmup=0):
+    """The reference compiled in place (oracle/_ref) on a bounded R-MAT sample."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracles
+
+    ref = oracles.load("ref")
+    ref.lib.pmmf_ref_set_threads(threads)
+    inp = workload(scale)
+    params = config_params()
+    times, rots = [], 0
+    for i in range(warmup + steps):
+        t = time.perf_counter()
+        f = oracles.factorize("ref", inp, params)
+        dt = time.perf_counter() - t
+        rots = sum(len(s.rot_indices) for s in f.stages)
+        if i >= warmup:
+            times.append(dt)
+    return rots, times, inp
+
+
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return world, rank, local, dist
+
+
+def main():
+    args = parse()
+    world, rank, local, dist = dist_init(args)
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        threads = os.cpu_count() or 1
+        rots, times, inp = cpu_reference_run(args.cpu_scale, threads, steps=args.steps, warmup=args.warmup)
+        best = max(times)
+        v = rots / best
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT recipe, SURVEY.md §8(d))",
+                "impl": "reference",
+                "config": {"workload": f"R-MAT scale {args.cpu_scale} (bounded sample of config 4), m=512, k=2, P=15",
+                           "n": int(inp[0]), "nnz": int(len(inp[1]))},
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                                 "sample": f"R-MAT scale {args.cpu_scale}, epv 32, m=512 (config-4 recipe at n=2^{args.cpu_scale}); the reference cannot hold n=2^20 (OOM, SURVEY.md §6)"},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    from paper_1507_04396_b200 import abi, api
+
+    lib = api.library()
+    L = lib.lib
+    L.pmmf_b200_profile_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double)]
+    L.pmmf_b200_profile_enable.argtypes = [ctypes.c_int32]
+    params = config_params()
+    n, rows, cols, vals = workload(args.scale)
+    d_rows = torch.from_numpy(rows).cuda()
+    d_cols = torch.from_numpy(cols).cuda()
+    d_vals = torch.from_numpy(vals).cuda()
+    torch.cuda.synchronize()
+    coo_dev, keep_dev = abi.make_coo(n, d_rows, d_cols, d_vals, on_device=True, device=local)
+    coo_host, keep_host = abi.make_coo(n, rows, cols, vals, device=local)
+    err = lib.errbuf()
+
+    def run_device():
+        h = ctypes.c_void_p()
+        abi.raise_for(lib.factorize(ctypes.byref(coo_dev), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+        s = abi.Summary()
+        lib.result_summary(h, ctypes.byref(s))
+        rots = 0
+        for st in range(s.n_stages):
+            sz = abi.StageSizes()
+            lib.result_stage_sizes(h, st, ctypes.byref(sz))
+            rots += sz.n_rotations
+        lib.result_free(h)
+        return rots
+
+    def run_e2e():
+        h = ctypes.c_void_p()
+        abi.raise_for(lib.factorize(ctypes.byref(coo_host), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+        f = lib.read_result(h)
+        lib.result_free(h)
+        out_bytes = sum(a.nbytes for st in f.stages for a in (st.cluster_offsets, st.members, st.rot_indices, st.rot_matrices,
+                                                              st.elim_index, st.elim_diagonal, st.elim_off_mass_sq, st.bypassed))
+        out_bytes += f.core.nbytes + f.core_indices.nbytes + f.diag_index.nbytes + f.diag_value.nbytes
+        return sum(len(st.rot_indices) for st in f.stages), out_bytes
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        run_device()
+    # ---- timed region: device-resident input
+    clocks = Clocks(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    L.pmmf_b200_profile_enable(1)
+    launches0 = api.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms, rots = [], 0
+    for _ in range(args.steps):
+        ev0.record()
+        rots = run_device()
+        ev1.record()
+        torch.cuda.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+    launches = api.kernel_launches() - launches0
+    barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    prof = {}
+    for name in ("rotate_write", "rotate_count"):
+        c, ms, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
+        if L.pmmf_b200_profile_read(name.encode(), ctypes.byref(c), ctypes.byref(ms), ctypes.byref(by)) == 0:
+            prof[name] = (c.value, ms.value, by.value)
+    L.pmmf_b200_profile_enable(0)
+    total_ms = max_over_ranks(sum(step_ms))
+    ms_per_step = total_ms / args.steps
+    value = world * rots / (ms_per_step / 1e3)
+
+    # ---- e2e: host buffers through the C-ABI, H2D + D2H inside the step
+    barrier()
+    e2e_ms = []
+    out_bytes = 0
+    for _ in range(max(1, min(args.steps, 2))):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        _, out_bytes = run_e2e()
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t) * 1e3)
+    e2e_step = max_over_ranks(sum(e2e_ms) / len(e2e_ms))
+    e2e = {"value": world * rots / (e2e_step / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(rows.nbytes + cols.nbytes + vals.nbytes), "d2h_bytes_per_step": int(out_bytes),
+           "ms_per_step": e2e_step}
+
+    peak, peak_src = peaks()
+    roof = None
+    if "rotate_write" in prof:
+        c, ms, by = prof["rotate_write"]
+        achieved = (by / 1e9) / (ms / 1e3) if ms > 0 else 0.0
+        roof = {"bound": "hbm", "kernel": "k_merge<2,true> (rotation stream, write pass)", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "launches": c, "kernel_ms_total": ms, "algorithmic_bytes_total": by, "peak_source": peak_src,
+                "share_of_step": ms / sum(step_ms)}
+        if "rotate_count" in prof:
+            c2, ms2, by2 = prof["rotate_count"]
+            roof["count_pass"] = {"launches": c2, "ms": ms2, "achieved_GBs": (by2 / 1e9) / (ms2 / 1e3) if ms2 else 0.0}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            crots, ctimes, cinp = cpu_reference_run(args.cpu_scale, threads)
+            cpu = {"value": crots / ctimes[0], "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"reference (oracle/_ref) on R-MAT scale {args.cpu_scale} epv 32 m=512 (n={cinp[0]}, "
+                             f"nnz={len(cinp[1])}), {ctimes[0]:.1f} s, {threads} threads"}
+        except Exception as e:  # the checker is optional on the box
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded R-MAT recipe, SURVEY.md §8(d)); inputs > L2 (no flush needed)",
+                "config": {"workload": f"config 4: R-MAT scale {args.scale} epv 32, normalized Laplacian + 1e-2 I",
+                           "n": int(n), "nnz": int(len(vals)), "k": 2, "P": 15, "m": 512, "c_max": 10000,
+                           "rotations_per_step": int(rots), "parallelism": f"replicas x{world}",
+                           "l2": "working set >> 126 MB L2"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk, "step_ms": step_ms}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -169,6 +169,13 @@ int pmmf_b200_rotation_from_gram(int32_t k, const double* g, double* q, char* er
  * bench.py's gpu_launches).  Counts every launch site in csrc/. */
 int64_t pmmf_b200_kernel_launches(void);
 
+/* Live kernel accounting for benchmarks: when enabled, instrumented launch
+ * sites ("rotate_write", "rotate_count", ...) bracket their kernels with CUDA
+ * events on the launching stream and accumulate device time and algorithmic
+ * bytes.  Enabling resets the counters. */
+void pmmf_b200_profile_enable(int32_t on);
+int pmmf_b200_profile_read(const char* name, int64_t* launches, double* ms, double* bytes);
+
 /* Library version string. */
 const char* pmmf_b200_version(void);
 

@@ -2,6 +2,8 @@
 // factorization entry point and the MmfFactorization accessors.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 
@@ -22,6 +24,40 @@ void set_err(char* err, size_t n, const std::string& m) {
 }  // namespace
 
 namespace pmmf_b200 {
+namespace {
+std::mutex& prof_mu() {
+  static std::mutex m;
+  return m;
+}
+std::map<std::string, ProfStat>& prof_map() {
+  static std::map<std::string, ProfStat> m;
+  return m;
+}
+std::atomic<bool>& prof_flag() {
+  static std::atomic<bool> f{false};
+  return f;
+}
+}  // namespace
+bool prof_enabled() { return prof_flag().load(std::memory_order_relaxed); }
+void prof_set(bool on) {
+  std::lock_guard<std::mutex> g(prof_mu());
+  prof_flag() = on;
+  prof_map().clear();
+}
+bool prof_get(const char* name, ProfStat* out) {
+  std::lock_guard<std::mutex> g(prof_mu());
+  auto it = prof_map().find(name);
+  if (it == prof_map().end()) return false;
+  *out = it->second;
+  return true;
+}
+void prof_add(const char* name, double ms, double bytes) {
+  std::lock_guard<std::mutex> g(prof_mu());
+  ProfStat& s = prof_map()[name];
+  ++s.launches;
+  s.ms += ms;
+  s.bytes += bytes;
+}
 int guarded_call(char* err, size_t errlen, void (*fn)(void*), void* ctx) {
   try {
     fn(ctx);
@@ -136,6 +172,17 @@ int pmmf_b200_rotation_from_gram(int32_t k, const double* g, double* q, char* er
 }
 
 int64_t pmmf_b200_kernel_launches(void) { return launch_counter().load(); }
+
+void pmmf_b200_profile_enable(int32_t on) { prof_set(on != 0); }
+
+int pmmf_b200_profile_read(const char* name, int64_t* launches, double* ms, double* bytes) {
+  ProfStat st;
+  if (!prof_get(name, &st)) return PMMF_OUT_OF_RANGE;
+  *launches = st.launches;
+  *ms = st.ms;
+  *bytes = st.bytes;
+  return PMMF_OK;
+}
 
 const char* pmmf_b200_version(void) { return "pmmf_b200 0.1 (sm_100a)"; }
 

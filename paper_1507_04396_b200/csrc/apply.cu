@@ -1,17 +1,23 @@
 // apply.cu — the stage apply A <- Q A Q^T (factorizer.hpp:336-394) as
-// column rotation streams.
+// column rotation streams, plus the memory-lean transposes between passes.
 //
-// Rotations of one stage are grouped into dependency levels (computed by the
-// search kernel): a level's rotations touch pairwise disjoint ids, so they
-// run concurrently, one warp per rotation, and levels run in order.  For a
-// rotation on ids (j_0..j_k-1) the warp merges the k sorted sparse columns
-// window by window (32 rows per list per step), forms
-//   out_a = ((0 + q(a,0) v_0) + q(a,1) v_1) + ...            (sparse.hpp:123-156)
-// over the union support with absent entries = 0.0, drops exact zeros
-// (value-neutral) and appends the k new columns to the
-// arena.  The row side is the same kernel on the transpose (App. A P12,
-// "transpose trick").  HBM-bound streaming: every input entry is read once
-// and every output entry written once per rotation.
+// A pass applies one stage's rotations to the columns of a matrix
+// (sparse.hpp:123-156): rotation t on ids (j_0..j_k-1) replaces them by
+//   out_a = ((0 + q(a,0) v_0) + q(a,1) v_1) + ...
+// over the union support (absent = 0.0), exact zeros dropped (value-neutral,
+// SURVEY.md App. A P12).  The row side is the same pass on the transpose
+// (App. A P12, "transpose trick").
+//
+// Scheduling.  Rotations are grouped in dependency levels (search.cu); a
+// level's rotations touch disjoint ids.  Every rotation of a level is cut
+// into row-range partitions of <= kChunk rows of its longest input, so a
+// hub column with 10^6 entries is spread over hundreds of warps instead of
+// one.  Each partition is merged twice by one warp: a count pass (kept
+// outputs per column), an exclusive scan that yields exact arena offsets,
+// then a write pass.  Columns are processed in batches of clusters; a batch
+// works in its own arena (superseded versions are garbage), and its final
+// columns are copied into a compact Piece, optionally dropping rows that no
+// later consumer reads (lean mode).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -24,6 +30,7 @@ namespace pmmf_b200 {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kChunk = 1024;  // rows of the longest input per partition
 
 __device__ __forceinline__ int warp_lower_bound(int w, int r) {
   int lo = 0;
@@ -37,44 +44,64 @@ __device__ __forceinline__ int warp_lower_bound(int w, int r) {
   return lo;  // number of window rows < r, in [0, 32]
 }
 
+__device__ __forceinline__ i64 lower_bound_g(const int32_t* __restrict__ a, i64 lo, i64 hi, int key) {
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+struct PassArgs {
+  const int32_t* rots;   // rotation slots of this level
+  const int32_t* ids;    // slot x K stage ids (global stage numbering)
+  const double* qs;      // slot x K x K
+  i64 col0;              // batch column base (local id = stage id - col0)
+  const i64* off;        // batch paged table
+  const int32_t* len;
+  const int32_t* arow;
+  const double* aval;
+  const int64_t* ioff;   // per level-rotation: first partition index (exclusive scan of nparts)
+  i64 nrot;              // rotations in level
+  i64 nitems;            // total partitions
+  int64_t* cnt;          // K * nitems kept counts, layout [K*ioff_t + a*np_t + p]
+  const int64_t* pos;    // exclusive scan of cnt (write pass)
+  i64 base;              // arena offset of this level's outputs (write pass)
+  int32_t* wrow;
+  double* wval;
+};
+
+// Row range of partition p of rotation t: split points are rows of the
+// longest input at multiples of kChunk.
 template <int K>
-__global__ void k_rotate_level(i64 n, const int32_t* __restrict__ order, const int32_t* __restrict__ ids,
-                               const double* __restrict__ qs, i64* __restrict__ off, int32_t* __restrict__ len,
-                               int32_t* __restrict__ arow, double* __restrict__ aval,
-                               unsigned long long* __restrict__ cursor, i64 cap, int32_t* __restrict__ overflow,
-                               uint8_t* __restrict__ done) {
-  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= n) return;
-  if (*reinterpret_cast<volatile int32_t*>(overflow)) return;
-  const int t = order[w];
-  if (done[t]) return;
-  i64 src[K];
-  int L[K], p[K];
-  int id[K];
-  double q[K][K];
-  i64 S = 0;
+__device__ void partition_range(const PassArgs& A, int t, i64 p, i64 np, const int* id, i64 (&lo)[K], i64 (&hi)[K]) {
+  int longest = 0;
+  int Lmax = -1;
 #pragma unroll
   for (int b = 0; b < K; ++b) {
-    id[b] = ids[static_cast<i64>(t) * K + b];
-    src[b] = off[id[b]];
-    L[b] = len[id[b]];
-    p[b] = 0;
-    S += L[b];
-#pragma unroll
-    for (int a = 0; a < K; ++a) q[b][a] = qs[(static_cast<i64>(t) * K + b) * K + a];
+    const int L = A.len[id[b]];
+    if (L > Lmax) {
+      Lmax = L;
+      longest = b;
+    }
   }
-  unsigned long long base = 0;
-  if (lane == 0) {
-    base = atomicAdd(cursor, static_cast<unsigned long long>(K) * static_cast<unsigned long long>(S));
-    if (static_cast<i64>(base) + K * S > cap) atomicExch(overflow, 1);
-  }
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (static_cast<i64>(base) + K * S > cap) return;
-  int written[K];
+  const i64 lsrc = A.off[id[longest]];
+  const int r_lo = p == 0 ? INT_MIN : A.arow[lsrc + p * kChunk];
+  const int r_hi = p == np - 1 ? INT_MAX : A.arow[lsrc + (p + 1) * kChunk];
 #pragma unroll
-  for (int a = 0; a < K; ++a) written[a] = 0;
+  for (int b = 0; b < K; ++b) {
+    const i64 s = A.off[id[b]], e = s + A.len[id[b]];
+    lo[b] = (p == 0) ? s : lower_bound_g(A.arow, s, e, r_lo);
+    hi[b] = (p == np - 1) ? e : lower_bound_g(A.arow, s, e, r_hi);
+  }
+}
 
+// Windowed k-way union merge of one partition, one warp.  kWrite = false
+// counts kept outputs per column; true writes them.
+template <int K, bool kWrite>
+__device__ void merge_partition(const PassArgs& A, const double (&q)[K][K], i64 (&p)[K], const i64 (&hi)[K],
+                                int (&kept)[K], const i64 (&dst)[K]) {
+  const int lane = threadIdx.x & 31;
   for (;;) {
     int row[K];
     double val[K];
@@ -82,22 +109,20 @@ __global__ void k_rotate_level(i64 n, const int32_t* __restrict__ order, const i
     bool any = false;
 #pragma unroll
     for (int b = 0; b < K; ++b) {
-      const int e = p[b] + lane;
-      row[b] = e < L[b] ? arow[src[b] + e] : INT_MAX;
-      val[b] = e < L[b] ? aval[src[b] + e] : 0.0;
-      const int last = __shfl_sync(0xffffffffu, row[b], 31);
-      frontier = min(frontier, last);
-      any |= p[b] < L[b];
+      const i64 e = p[b] + lane;
+      row[b] = e < hi[b] ? A.arow[e] : INT_MAX;
+      val[b] = e < hi[b] ? A.aval[e] : 0.0;
+      frontier = min(frontier, __shfl_sync(0xffffffffu, row[b], 31));
+      any |= p[b] < hi[b];
     }
     if (!any) break;
     bool valid[K];
-    unsigned nvalid[K];
+    int nvalid[K];
 #pragma unroll
     for (int b = 0; b < K; ++b) {
       valid[b] = row[b] != INT_MAX && row[b] <= frontier;
       nvalid[b] = __popc(__ballot_sync(0xffffffffu, valid[b]));
     }
-    // lb[b][b2]: rows of window b2 below row[b] (own window: lane)
     int lb[K][K];
     bool present[K][K];
 #pragma unroll
@@ -110,7 +135,9 @@ __global__ void k_rotate_level(i64 n, const int32_t* __restrict__ order, const i
         } else {
           const int l = warp_lower_bound(row[b2], row[b]);
           lb[b][b2] = l;
-          present[b][b2] = __shfl_sync(0xffffffffu, row[b2], l & 31) == row[b] && l < 32;
+          // the shuffle must run on all 32 lanes (no short-circuit)
+          const int cand = __shfl_sync(0xffffffffu, row[b2], l & 31);
+          present[b][b2] = (cand == row[b]) && (l < 32);
         }
       }
     unsigned F[K];
@@ -123,9 +150,8 @@ __global__ void k_rotate_level(i64 n, const int32_t* __restrict__ order, const i
       first[b] = f;
       F[b] = __ballot_sync(0xffffffffu, f);
     }
-    // union rank and mixed values of every first occurrence
     int rank[K];
-    double out[K][K];  // out[b][a]: output a for the row owned by window b
+    double out[K][K];
 #pragma unroll
     for (int b = 0; b < K; ++b) {
       int rk = 0;
@@ -149,7 +175,6 @@ __global__ void k_rotate_level(i64 n, const int32_t* __restrict__ order, const i
         out[b][a] = acc;
       }
     }
-    // zero-drop compaction in union-rank order, per output column
 #pragma unroll
     for (int a = 0; a < K; ++a) {
       unsigned words[K];
@@ -164,42 +189,169 @@ __global__ void k_rotate_level(i64 n, const int32_t* __restrict__ order, const i
       int total = 0;
 #pragma unroll
       for (int wd = 0; wd < K; ++wd) total += __popc(words[wd]);
+      if (kWrite) {
 #pragma unroll
-      for (int b = 0; b < K; ++b) {
-        if (first[b] && out[b][a] != 0.0) {
-          int pos = 0;
-          const int wd = rank[b] >> 5, bit = rank[b] & 31;
+        for (int b = 0; b < K; ++b) {
+          if (first[b] && out[b][a] != 0.0) {
+            int pos = 0;
+            const int wd = rank[b] >> 5, bit = rank[b] & 31;
 #pragma unroll
-          for (int x = 0; x < K; ++x)
-            if (x < wd) pos += __popc(words[x]);
-          pos += __popc(words[wd] & ((1u << bit) - 1u));
-          const i64 dst = static_cast<i64>(base) + static_cast<i64>(a) * S + written[a] + pos;
-          arow[dst] = row[b];
-          aval[dst] = out[b][a];
+            for (int x = 0; x < K; ++x)
+              if (x < wd) pos += __popc(words[x]);
+            pos += __popc(words[wd] & ((1u << bit) - 1u));
+            const i64 d = dst[a] + kept[a] + pos;
+            A.wrow[d] = row[b];
+            A.wval[d] = out[b][a];
+          }
         }
       }
-      written[a] += total;
+      kept[a] += total;
     }
 #pragma unroll
-    for (int b = 0; b < K; ++b) p[b] += static_cast<int>(nvalid[b]);
-  }
-  __syncwarp();
-  if (lane == 0) {
-#pragma unroll
-    for (int a = 0; a < K; ++a) {
-      off[id[a]] = static_cast<i64>(base) + static_cast<i64>(a) * S;
-      len[id[a]] = written[a];
-    }
-    done[t] = 1;
+    for (int b = 0; b < K; ++b) p[b] += nvalid[b];
   }
 }
 
-// Compaction of the live columns into a fresh arena.
+template <int K>
+__global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long long* __restrict__ in_entries) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= A.nrot) return;
+  const int t = A.rots[i];
+  int Lmax = 0;
+  unsigned long long S = 0;
+#pragma unroll
+  for (int b = 0; b < K; ++b) {
+    const int L = A.len[A.ids[static_cast<i64>(t) * K + b] - A.col0];
+    Lmax = max(Lmax, L);
+    S += static_cast<unsigned long long>(L);
+  }
+  nparts[i] = max(1, (Lmax + kChunk - 1) / kChunk);
+  atomicAdd(in_entries, S);
+}
+
+template <int K, bool kWrite>
+__global__ void k_merge(PassArgs A) {
+  const i64 item = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  if (item >= A.nitems) return;
+  // rotation of this partition: last i with ioff[i] <= item
+  i64 lo = 0, hi = A.nrot;
+  while (hi - lo > 1) {
+    const i64 mid = (lo + hi) >> 1;
+    if (A.ioff[mid] <= item) lo = mid; else hi = mid;
+  }
+  const i64 ri = lo;
+  const i64 p = item - A.ioff[ri];
+  const i64 np = (ri + 1 < A.nrot ? A.ioff[ri + 1] : A.nitems) - A.ioff[ri];
+  const int t = A.rots[ri];
+  int id[K];
+  double q[K][K];
+#pragma unroll
+  for (int b = 0; b < K; ++b) {
+    id[b] = A.ids[static_cast<i64>(t) * K + b] - static_cast<int>(A.col0);
+#pragma unroll
+    for (int a = 0; a < K; ++a) q[b][a] = A.qs[(static_cast<i64>(t) * K + b) * K + a];
+  }
+  i64 beg[K], end[K];
+  partition_range<K>(A, t, p, np, id, beg, end);
+  int kept[K];
+  i64 dst[K];
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    kept[a] = 0;
+    dst[a] = kWrite ? A.base + A.pos[K * A.ioff[ri] + a * np + p] : 0;
+  }
+  merge_partition<K, kWrite>(A, q, beg, end, kept, dst);
+  if (!kWrite && (threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int a = 0; a < K; ++a) A.cnt[K * A.ioff[ri] + a * np + p] = kept[a];
+  }
+}
+
+// New (off, len) of every output column of the level.
+template <int K>
+__global__ void k_commit(PassArgs A, i64* __restrict__ off, int32_t* __restrict__ len, i64 total) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= A.nrot) return;
+  const int t = A.rots[i];
+  const i64 np = (i + 1 < A.nrot ? A.ioff[i + 1] : A.nitems) - A.ioff[i];
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    const i64 f = K * A.ioff[i] + a * np;
+    const i64 b = A.pos[f];
+    const i64 e = (f + np < K * A.nitems) ? A.pos[f + np] : total;
+    const int id = A.ids[static_cast<i64>(t) * K + a] - static_cast<int>(A.col0);
+    off[id] = A.base + b;
+    len[id] = static_cast<int32_t>(e - b);
+  }
+}
+
 __global__ void k_len64(i64 N, const int32_t* __restrict__ len, i64* __restrict__ out) {
   const i64 j = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (j < N) out[j] = len[j];
   if (j == N) out[j] = 0;
 }
+
+// Count / copy the live columns of a batch, optionally keeping only rows
+// flagged in keep_row (lean mode: rows the next stage reads) unless the
+// column itself is flagged in keep_all_col.
+__global__ void k_final_count(i64 N, i64 col0, const i64* __restrict__ off, const int32_t* __restrict__ len,
+                              const int32_t* __restrict__ arow, const uint8_t* __restrict__ keep_row,
+                              const uint8_t* __restrict__ keep_all_col, i64* __restrict__ cnt) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w > N) return;
+  if (w == N) {
+    if (lane == 0) cnt[N] = 0;
+    return;
+  }
+  const bool all = keep_row == nullptr || keep_all_col[col0 + w];
+  if (all) {
+    if (lane == 0) cnt[w] = len[w];
+    return;
+  }
+  int c = 0;
+  for (int i = lane; i < len[w]; i += 32) c += keep_row[arow[off[w] + i]];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[w] = c;
+}
+__global__ void k_final_copy(i64 N, i64 col0, const i64* __restrict__ off, const int32_t* __restrict__ len,
+                             const int32_t* __restrict__ arow, const double* __restrict__ aval,
+                             const uint8_t* __restrict__ keep_row, const uint8_t* __restrict__ keep_all_col,
+                             const i64* __restrict__ pos, int32_t* __restrict__ orow, double* __restrict__ oval) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= N) return;
+  const bool all = keep_row == nullptr || keep_all_col[col0 + w];
+  i64 o = pos[w];
+  const i64 s = off[w];
+  for (int base = 0; base < len[w]; base += 32) {
+    const int i = base + lane;
+    int r = 0;
+    double v = 0.0;
+    bool k = false;
+    if (i < len[w]) {
+      r = arow[s + i];
+      v = aval[s + i];
+      k = all || keep_row[r];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, k);
+    if (k) {
+      const i64 d = o + __popc(m & ((1u << lane) - 1u));
+      orow[d] = r;
+      oval[d] = v;
+    }
+    o += __popc(m);
+  }
+}
+
+__global__ void k_paged_init_local(i64 N, const i64* __restrict__ ptr, i64 col0, i64 e0, i64* __restrict__ off,
+                                   int32_t* __restrict__ len) {
+  const i64 j = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (j >= N) return;
+  off[j] = ptr[col0 + j] - e0;
+  len[j] = static_cast<int32_t>(ptr[col0 + j + 1] - ptr[col0 + j]);
+}
+
 __global__ void k_compact(i64 N, i64* __restrict__ off, const int32_t* __restrict__ len, const i64* __restrict__ pos,
                           const int32_t* __restrict__ r0, const double* __restrict__ v0, int32_t* __restrict__ r1,
                           double* __restrict__ v1) {
@@ -215,41 +367,96 @@ __global__ void k_compact(i64 N, i64* __restrict__ off, const int32_t* __restric
   if (lane == 0) off[w] = d;
 }
 
-void compact(Paged& P, i64 min_free, cudaStream_t s) {
-  DBuf<i64> l64(P.N + 1, s), pos(P.N + 1, s);
-  PMMF_LAUNCH(k_len64, blocks_for(P.N + 1, kThreads), kThreads, 0, s, P.N, P.len.get(), l64.get());
+template <typename T>
+void exscan(const T* in, T* out, i64 n, cudaStream_t s) {
   size_t tmp = 0;
-  PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, l64.get(), pos.get(), static_cast<int64_t>(P.N + 1), s));
+  PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(n), s));
   DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
-  PMMF_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, l64.get(), pos.get(), static_cast<int64_t>(P.N + 1), s));
-  i64 live = 0;
-  PMMF_CUDA(cudaMemcpyAsync(&live, pos.get() + P.N, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  PMMF_CUDA(cudaStreamSynchronize(s));
-  const i64 cap = std::max<i64>(2 * live, live + min_free) + 1024;
-  DBuf<int32_t> r1(cap, s);
-  DBuf<double> v1(cap, s);
-  PMMF_LAUNCH(k_compact, blocks_for(P.N * 32, kThreads), kThreads, 0, s, P.N, P.off.get(), P.len.get(), pos.get(),
-              P.row.get(), P.val.get(), r1.get(), v1.get());
-  P.row = std::move(r1);
-  P.val = std::move(v1);
-  P.cap = cap;
-  const unsigned long long c0 = static_cast<unsigned long long>(live);
-  PMMF_CUDA(cudaMemcpyAsync(P.cursor.get(), &c0, sizeof(c0), cudaMemcpyHostToDevice, s));
-  PMMF_CUDA(cudaStreamSynchronize(s));
+  PMMF_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, in, out, static_cast<int64_t>(n), s));
 }
 
+i64 read_i64(const i64* p, cudaStream_t s) {
+  i64 v = 0;
+  PMMF_CUDA(cudaMemcpyAsync(&v, p, sizeof(v), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  return v;
+}
+
+// Batch working set: paged view of columns [col0, col0+N) in an arena.
+struct Batch {
+  i64 col0 = 0, N = 0;
+  DBuf<i64> off;
+  DBuf<int32_t> len;
+  DBuf<int32_t> row;
+  DBuf<double> val;
+  i64 cap = 0, used = 0;
+
+  void compact(i64 need, cudaStream_t s) {
+    DBuf<i64> l64(N + 1, s), pos(N + 1, s);
+    PMMF_LAUNCH(k_len64, blocks_for(N + 1, kThreads), kThreads, 0, s, N, len.get(), l64.get());
+    exscan(l64.get(), pos.get(), N + 1, s);
+    const i64 live = read_i64(pos.get() + N, s);
+    const i64 ncap = std::max<i64>(live + need, (live + need) + (live + need) / 2) + 1024;
+    DBuf<int32_t> r1(ncap, s);
+    DBuf<double> v1(ncap, s);
+    PMMF_LAUNCH(k_compact, blocks_for(N * 32, kThreads), kThreads, 0, s, N, off.get(), len.get(), pos.get(), row.get(),
+                val.get(), r1.get(), v1.get());
+    row = std::move(r1);
+    val = std::move(v1);
+    cap = ncap;
+    used = live;
+  }
+};
+
 template <int K>
-void launch_level(Paged& P, const LevelPlan& plan, i64 begin, i64 count, DBuf<int32_t>& overflow,
-                  DBuf<uint8_t>& done, cudaStream_t s) {
-  PMMF_LAUNCH(k_rotate_level<K>, blocks_for(count * 32, kThreads), kThreads, 0, s, count, plan.order.get() + begin,
-              plan.ids.get(), plan.q, P.off.get(), P.len.get(), P.row.get(), P.val.get(), P.cursor.get(), P.cap,
-              overflow.get(), done.get());
+void run_level(Batch& B, const LevelPlan& plan, const int32_t* rots, i64 nrot, cudaStream_t s) {
+  PassArgs A{};
+  A.rots = rots;
+  A.ids = plan.ids.get();
+  A.qs = plan.q;
+  A.col0 = B.col0;
+  A.nrot = nrot;
+  DBuf<int64_t> np(nrot, s), ioff(nrot + 1, s);
+  DBuf<unsigned long long> in_entries(1, s);
+  in_entries.zero();
+  A.off = B.off.get();
+  A.len = B.len.get();
+  PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, np.get(), in_entries.get());
+  exscan(np.get(), ioff.get(), nrot, s);
+  const i64 items = read_i64(ioff.get() + nrot - 1, s) + read_i64(np.get() + nrot - 1, s);
+  A.ioff = ioff.get();
+  A.nitems = items;
+  DBuf<int64_t> cnt(K * items, s), pos(K * items, s);
+  A.cnt = cnt.get();
+  A.arow = B.row.get();
+  A.aval = B.val.get();
+  ProfScope pc("rotate_count", s);
+  PMMF_LAUNCH((k_merge<K, false>), blocks_for(items * 32, kThreads), kThreads, 0, s, A);
+  const double in_bytes = 12.0 * static_cast<double>(in_entries.to_host(1)[0]);
+  pc.finish(in_bytes);
+  exscan(cnt.get(), pos.get(), K * items, s);
+  const i64 total = read_i64(pos.get() + K * items - 1, s) + read_i64(cnt.get() + K * items - 1, s);
+  if (B.used + total > B.cap) B.compact(total, s);
+  A.off = B.off.get();
+  A.arow = B.row.get();
+  A.aval = B.val.get();
+  A.pos = pos.get();
+  A.base = B.used;
+  A.wrow = B.row.get();
+  A.wval = B.val.get();
+  ProfScope pw("rotate_write", s);
+  PMMF_LAUNCH((k_merge<K, true>), blocks_for(items * 32, kThreads), kThreads, 0, s, A);
+  // algorithmic bytes: inputs read once, outputs written
+  // once (12 B per entry), rotation blocks (8k^2 + 4k per rotation)
+  pw.finish(in_bytes + 12.0 * static_cast<double>(total) + static_cast<double>(nrot) * (8.0 * K * K + 4.0 * K));
+  PMMF_LAUNCH(k_commit<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, B.off.get(), B.len.get(), total);
+  B.used += total;
 }
 
 __global__ void k_plan(const int32_t* __restrict__ nrot, const int64_t* __restrict__ base,
                        const int64_t* __restrict__ coff, const int32_t* __restrict__ rot_loc,
                        const int32_t* __restrict__ rot_level, int k, int32_t* __restrict__ ids,
-                       int32_t* __restrict__ lvl, int32_t* __restrict__ slot) {
+                       int32_t* __restrict__ lvl) {
   const int u = blockIdx.x;
   const i64 b = base[u];
   for (int t = threadIdx.x; t < nrot[u]; t += blockDim.x) {
@@ -272,6 +479,8 @@ __global__ void k_level_bounds(i64 n, const int32_t* __restrict__ lv, int maxl, 
 
 }  // namespace
 
+// Level plan of a stage (rotation slots sorted by dependency level; stable,
+// so slots stay ascending inside a level).
 void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_base,
                 const DBuf<int64_t>& cluster_off, i64 nclusters, i64 R, int k, cudaStream_t s) {
   plan.R = R;
@@ -279,12 +488,13 @@ void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_b
   plan.q = so.rot_q.get();
   plan.max_level = 0;
   plan.level_start.assign(1, 0);
+  plan.h_order.clear();
   if (R == 0 || nclusters == 0) return;
   plan.ids.alloc(R * k, s);
   DBuf<int32_t> lvl(R, s), slot(R, s), lvl2(R, s);
   lvl.zero();
   PMMF_LAUNCH(k_plan, static_cast<unsigned>(nclusters), 256, 0, s, so.nrot.get(), out_base.get(), cluster_off.get(),
-              so.rot_loc.get(), so.rot_level.get(), k, plan.ids.get(), lvl.get(), slot.get());
+              so.rot_loc.get(), so.rot_level.get(), k, plan.ids.get(), lvl.get());
   PMMF_LAUNCH(k_iota, blocks_for(R, kThreads), kThreads, 0, s, R, slot.get());
   plan.order.alloc(R, s);
   {
@@ -302,37 +512,80 @@ void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_b
   DBuf<i64> start(maxl + 2, s);
   PMMF_LAUNCH(k_level_bounds, blocks_for(R + 1, kThreads), kThreads, 0, s, R, lvl2.get(), maxl, start.get());
   std::vector<i64> h = start.to_host(maxl + 2);
-  // level L (1-based) occupies [h[L], h[L+1]) of the sorted order
-  plan.level_start.assign(h.begin() + 1, h.end());
+  plan.level_start.assign(h.begin() + 1, h.end());  // level L occupies [level_start[L-1], level_start[L])
+  plan.h_order = plan.order.to_host(R);
 }
 
-void apply_levels(Paged& P, const LevelPlan& plan, cudaStream_t s) {
-  if (plan.R == 0 || plan.max_level == 0) return;
-  DBuf<int32_t> overflow(1, s);
-  DBuf<uint8_t> done(plan.R, s);
-  overflow.zero();
-  done.zero();
-  for (int attempt = 0;; ++attempt) {
-    for (int L = 1; L <= plan.max_level; ++L) {
-      const i64 b = plan.level_start[L - 1], cnt = plan.level_start[L] - b;
+void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
+                 const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
+                 const uint8_t* keep_all_col, i64 batch_nnz, cudaStream_t s) {
+  out.clear();
+  const i64 m = static_cast<i64>(off.size()) - 1;
+  // host copy of ptr at cluster boundaries
+  std::vector<i64> eptr(static_cast<size_t>(m + 1));
+  for (i64 u = 0; u <= m; ++u)
+    PMMF_CUDA(cudaMemcpyAsync(&eptr[u], in.ptr.get() + off[u], sizeof(i64), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  i64 u0 = 0;
+  while (u0 < m) {
+    i64 u1 = u0 + 1;
+    while (u1 < m && eptr[u1 + 1] - eptr[u0] <= batch_nnz) ++u1;
+    Batch B;
+    B.col0 = off[u0];
+    B.N = off[u1] - off[u0];
+    const i64 e0 = eptr[u0], ne = eptr[u1] - eptr[u0];
+    B.cap = std::max<i64>(4 * ne, ne + (i64{1} << 22));
+    B.used = ne;
+    B.off.alloc(std::max<i64>(B.N, 1), s);
+    B.len.alloc(std::max<i64>(B.N, 1), s);
+    B.row.alloc(B.cap, s);
+    B.val.alloc(B.cap, s);
+    if (ne) {
+      PMMF_CUDA(cudaMemcpyAsync(B.row.get(), in.row.get() + e0, sizeof(int32_t) * ne, cudaMemcpyDeviceToDevice, s));
+      PMMF_CUDA(cudaMemcpyAsync(B.val.get(), in.val.get() + e0, sizeof(double) * ne, cudaMemcpyDeviceToDevice, s));
+    }
+    PMMF_LAUNCH(k_paged_init_local, blocks_for(B.N, kThreads), kThreads, 0, s, B.N, in.ptr.get(), B.col0, e0,
+                B.off.get(), B.len.get());
+    // levels restricted to the batch's rotation slots
+    const i64 sb = slot_base[u0], se = slot_base[u1];
+    for (int L = 1; L <= plan.max_level && se > sb; ++L) {
+      const i64 b = plan.level_start[L - 1], e = plan.level_start[L];
+      if (e <= b) continue;
+      // the plan's order is sorted by (level, slot): the batch's slots are a
+      // contiguous sub-range found on the host copy
+      const i64 lo = std::lower_bound(plan.h_order.begin() + b, plan.h_order.begin() + e, static_cast<int32_t>(sb)) -
+                     plan.h_order.begin();
+      const i64 hi = std::lower_bound(plan.h_order.begin() + b, plan.h_order.begin() + e, static_cast<int32_t>(se)) -
+                     plan.h_order.begin();
+      if (hi <= lo) continue;
+      const int32_t* rots = plan.order.get() + lo;
       switch (plan.k) {
-        case 2: launch_level<2>(P, plan, b, cnt, overflow, done, s); break;
-        case 3: launch_level<3>(P, plan, b, cnt, overflow, done, s); break;
-        case 4: launch_level<4>(P, plan, b, cnt, overflow, done, s); break;
-        case 5: launch_level<5>(P, plan, b, cnt, overflow, done, s); break;
-        case 6: launch_level<6>(P, plan, b, cnt, overflow, done, s); break;
-        case 7: launch_level<7>(P, plan, b, cnt, overflow, done, s); break;
-        case 8: launch_level<8>(P, plan, b, cnt, overflow, done, s); break;
+        case 2: run_level<2>(B, plan, rots, hi - lo, s); break;
+        case 3: run_level<3>(B, plan, rots, hi - lo, s); break;
+        case 4: run_level<4>(B, plan, rots, hi - lo, s); break;
+        case 5: run_level<5>(B, plan, rots, hi - lo, s); break;
+        case 6: run_level<6>(B, plan, rots, hi - lo, s); break;
+        case 7: run_level<7>(B, plan, rots, hi - lo, s); break;
+        case 8: run_level<8>(B, plan, rots, hi - lo, s); break;
         default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
       }
     }
-    int32_t of = 0;
-    PMMF_CUDA(cudaMemcpyAsync(&of, overflow.get(), sizeof(of), cudaMemcpyDeviceToHost, s));
-    PMMF_CUDA(cudaStreamSynchronize(s));
-    if (!of) return;
-    if (attempt > 40) fail(PMMF_INTERNAL, "apply: arena compaction did not converge");
-    compact(P, P.cap, s);  // at least double the free space
-    overflow.zero();
+    // finalize into a compact piece
+    Piece P;
+    P.c0 = B.col0;
+    P.c1 = B.col0 + B.N;
+    DBuf<i64> cnt(B.N + 1, s);
+    P.ptr.alloc(B.N + 1, s);
+    PMMF_LAUNCH(k_final_count, blocks_for((B.N + 1) * 32, kThreads), kThreads, 0, s, B.N, B.col0, B.off.get(),
+                B.len.get(), B.row.get(), keep_row, keep_all_col, cnt.get());
+    exscan(cnt.get(), P.ptr.get(), B.N + 1, s);
+    P.nnz = read_i64(P.ptr.get() + B.N, s);
+    P.row.alloc(std::max<i64>(P.nnz, 1), s);
+    P.val.alloc(std::max<i64>(P.nnz, 1), s);
+    PMMF_LAUNCH(k_final_copy, blocks_for(B.N * 32, kThreads), kThreads, 0, s, B.N, B.col0, B.off.get(), B.len.get(),
+                B.row.get(), B.val.get(), keep_row, keep_all_col, P.ptr.get(), P.row.get(), P.val.get());
+    out.push_back(std::move(P));
+    u0 = u1;
   }
 }
 

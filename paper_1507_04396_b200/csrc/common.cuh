@@ -45,6 +45,49 @@ std::atomic<int64_t>& launch_counter();
     }                                                                        \
   } while (0)
 
+// Live per-kernel accounting for bench.py's roofline: when enabled, the
+// instrumented launch sites bracket their kernel with CUDA events on the
+// launching stream and add the algorithmic bytes they moved.
+struct ProfStat {
+  int64_t launches = 0;
+  double ms = 0.0;
+  double bytes = 0.0;
+};
+bool prof_enabled();
+void prof_set(bool on);
+bool prof_get(const char* name, ProfStat* out);
+void prof_add(const char* name, double ms, double bytes);
+struct ProfScope {
+  const char* name;
+  cudaStream_t s;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  ProfScope(const char* n, cudaStream_t st) : name(n), s(st) {
+    if (prof_enabled()) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, s);
+    }
+  }
+  // call after the launch; bytes known by then or passed later via finish
+  void finish(double bytes) {
+    if (!e0) return;
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    prof_add(name, ms, bytes);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    e0 = e1 = nullptr;
+  }
+  ~ProfScope() {
+    if (e0) {
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+  }
+};
+
 // Stream-ordered device buffer (cudaMallocAsync from the device pool).
 template <typename T>
 struct DBuf {

@@ -118,11 +118,41 @@ struct LevelPlan {
   const double* q = nullptr; // R x k x k (non-owning)
   DBuf<int32_t> order;       // slots sorted by level (level-0 slots first, skipped)
   std::vector<i64> level_start;  // host: [level-1 start] for levels 1..max_level, plus end
+  std::vector<int32_t> h_order;  // host copy of order
 };
+
+// A compact column range [c0, c1) of a matrix (ptr local, starting at 0).
+struct Piece {
+  i64 c0 = 0, c1 = 0, nnz = 0;
+  DBuf<i64> ptr;
+  DBuf<int32_t> row;
+  DBuf<double> val;
+};
+
+// One pass of a stage's rotations over the columns of `in` (stage
+// numbering, cluster offsets `off`, rotation slots of cluster u in
+// [slot_base[u], slot_base[u+1])), batch by batch of clusters holding at
+// most batch_nnz input entries.  The final columns are returned as pieces;
+// when keep_row != nullptr, a column c keeps only rows r with keep_row[r]
+// unless keep_all_col[c].
+void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
+                 const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
+                 const uint8_t* keep_all_col, i64 batch_nnz, cudaStream_t s);
+// Transpose of a matrix given as pieces covering [0, N), keeping only rows
+// r with keep_row[r] (all when nullptr); sorted in chunks of <= chunk_nnz
+// entries so the sort buffers stay bounded.
+void transpose_pieces(Csc& out, const std::vector<Piece>& in, i64 N, const uint8_t* keep_row, i64 chunk_nnz,
+                      cudaStream_t s);
+// Residual accounting (factorizer.hpp:521-547) straight from the rotated
+// transpose: column g of A' (= row g of the pieces) for every retired stage
+// id g, reduced chunk by chunk without materialising it.  mass/diag are
+// indexed by elimination rank (zero-initialised by the caller).
+void retired_masses(const std::vector<Piece>& in, i64 N, const uint8_t* is_retired, const int32_t* s2g,
+                    const uint8_t* is_active, const int32_t* rank, double* mass, double* diag, i64 chunk_nnz,
+                    cudaStream_t s);
 // Builds the level plan from a search result: slot = out_base[u] + t for
 // t < nrot[u]; stage id = cluster_off[u] + local.
 void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_base,
                 const DBuf<int64_t>& cluster_off, i64 nclusters, i64 R, int k, cudaStream_t s);
-void apply_levels(Paged& p, const LevelPlan& plan, cudaStream_t s);
 
 }  // namespace pmmf_b200

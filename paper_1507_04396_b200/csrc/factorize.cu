@@ -35,25 +35,56 @@ constexpr int kThreads = 256;
 // Residual accounting for the stage's eliminations in order r
 // (factorizer.hpp:529-542): mass = sum of v^2 over column g's entries whose
 // row is still active or retired later in the stage; diag = A'[g][g].
+__device__ __forceinline__ void residual_column(i64 r, int32_t j, const int32_t* __restrict__ row,
+                                                const double* __restrict__ val, i64 b, i64 e,
+                                                const int32_t* __restrict__ s2g, const uint8_t* __restrict__ is_active,
+                                                const int32_t* __restrict__ rank, double* __restrict__ mass,
+                                                double* __restrict__ diag) {
+  // warp: lanes classify 32 entries at a time, lane 0 accumulates them in
+  // row order (sequential sum, as the reference does)
+  const int lane = threadIdx.x & 31;
+  double m = 0.0, d = 0.0;
+  for (i64 x = b; x < e; x += 32) {
+    const i64 i = x + lane;
+    double sq = 0.0;
+    bool take = false, isdiag = false;
+    double v = 0.0;
+    if (i < e) {
+      const int32_t sr = row[i];
+      v = val[i];
+      if (sr == j) {
+        isdiag = true;
+      } else {
+        const int32_t l = s2g[sr];
+        take = is_active[l] || rank[l] > r;
+        sq = dmul(v, v);
+      }
+    }
+    const unsigned tk = __ballot_sync(0xffffffffu, take);
+    const unsigned dg = __ballot_sync(0xffffffffu, isdiag);
+    if (dg) d = __shfl_sync(0xffffffffu, v, __ffs(dg) - 1);
+    for (unsigned mm = tk; mm; mm &= mm - 1) {
+      const int src = __ffs(mm) - 1;
+      m = dadd(m, __shfl_sync(0xffffffffu, sq, src));
+    }
+  }
+  if (lane == 0) {
+    mass[r] = m;
+    diag[r] = d;
+  }
+}
+
+// Residual accounting for the stage's eliminations in order r
+// (factorizer.hpp:529-542): mass = sum of v^2 over column g's entries whose
+// row is still active or retired later in the stage; diag = A'[g][g].
 __global__ void k_residual(i64 R, const int32_t* __restrict__ elim_sid, const i64* __restrict__ ptr,
                            const int32_t* __restrict__ row, const double* __restrict__ val,
                            const int32_t* __restrict__ s2g, const uint8_t* __restrict__ is_active,
                            const int32_t* __restrict__ rank, double* __restrict__ mass, double* __restrict__ diag) {
-  const i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  const i64 r = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   if (r >= R) return;
   const int32_t j = elim_sid[r];
-  double m = 0.0, d = 0.0;
-  for (i64 e = ptr[j]; e < ptr[j + 1]; ++e) {
-    const int32_t sr = row[e];
-    if (sr == j) {
-      d = val[e];
-      continue;
-    }
-    const int32_t l = s2g[sr];
-    if (is_active[l] || rank[l] > r) m = dadd(m, dmul(val[e], val[e]));
-  }
-  mass[r] = m;
-  diag[r] = d;
+  residual_column(r, j, row, val, ptr[j], ptr[j + 1], s2g, is_active, rank, mass, diag);
 }
 
 __global__ void k_mark(i64 R, const int32_t* __restrict__ g, uint8_t* __restrict__ is_active,
@@ -86,6 +117,11 @@ bool trace_on() {
   }();
   return on;
 }
+size_t mem_used_mb() {
+  size_t f = 0, t = 0;
+  cudaMemGetInfo(&f, &t);
+  return (t - f) >> 20;
+}
 #define PMMF_TRACE(...)                 \
   do {                                  \
     if (trace_on()) {                   \
@@ -103,6 +139,19 @@ void validate(const pmmf_b200_params& p) {  // factorizer.hpp:44-50, clustering.
   if (p.m_target < 1) fail(PMMF_INVALID_ARGUMENT, "ClusterParams: m_target < 1");
   if (p.c_min > p.c_max) fail(PMMF_INVALID_ARGUMENT, "ClusterParams: c_min > c_max");
   if (p.d_max < 0) fail(PMMF_INVALID_ARGUMENT, "ClusterParams: d_max < 0");
+}
+
+i64 available_bytes() {
+  size_t f = 0, t = 0;
+  PMMF_CUDA(cudaMemGetInfo(&f, &t));
+  int dev = 0;
+  PMMF_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t reserved = 0, used = 0;
+  PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  return static_cast<i64>(f) + static_cast<i64>(reserved - used);
 }
 
 struct StreamGuard {
@@ -351,29 +400,65 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
 
     // ---- stage apply: column side, transpose, row side, transpose
     t0 = clk::now();
+    const i64 ne = static_cast<i64>(order_g.size());
+    DBuf<int32_t> dsid(std::max<i64>(ne, 1), s), dg(std::max<i64>(ne, 1), s);
+    dsid.upload(order_sid);
+    dg.upload(order_g);
+    DBuf<double> mass(std::max<i64>(ne, 1), s), diag(std::max<i64>(ne, 1), s);
+    bool residual_done = false;
     {
       LevelPlan plan;
       build_plan(plan, so, d_out_base, d_coff, rc, slots, p.k, s);
-      PMMF_TRACE("[pmmf] stage %d: clusters=%lld slots=%lld levels=%d nnz_in=%lld\n", stage_no,
-                 static_cast<long long>(rc), static_cast<long long>(slots), plan.max_level, static_cast<long long>(A.nnz));
       if (plan.max_level > 0) {
-        Paged P;
-        paged_from_csc(P, std::move(A), 2 * A.nnz + (i64{1} << 20), s);
-        apply_levels(P, plan, s);
+        const i64 N = cur.size();
+        std::vector<i64> slot_base(static_cast<size_t>(cur.clusters()) + 1, slots);
+        for (i64 u = 0; u <= rc; ++u) slot_base[u] = out_base[u];
+        const i64 avail = available_bytes();
+        i64 chunk = std::max<i64>(i64{1} << 22, avail / 10 / 32);
+        if (const char* e = std::getenv("PMMF_B200_CHUNK_NNZ")) chunk = std::atoll(e);  // test hook
+        std::vector<Piece> pieces;
+        rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, s);
+        A = Csc();
         Csc T;
-        transpose_paged(T, P, s);
-        const i64 cap1 = P.cap;
-        P = Paged();
-        Paged P2;
+        transpose_pieces(T, pieces, N, nullptr, chunk, s);
+        pieces.clear();
         const i64 tn = T.nnz;
-        paged_from_csc(P2, std::move(T), 2 * tn + (i64{1} << 20), s);
-        apply_levels(P2, plan, s);
-        Csc B;
-        transpose_paged(B, P2, s);
-        PMMF_TRACE("[pmmf] stage %d: nnz after column pass=%lld, after row pass=%lld (arena caps %lld, %lld)\n",
-                   stage_no, static_cast<long long>(tn), static_cast<long long>(B.nnz), static_cast<long long>(cap1),
-                   static_cast<long long>(P2.cap));
-        A = std::move(B);
+        // Retired ids: their rotated rows/columns feed only the residual.
+        DBuf<uint8_t> keep_row(N, s), retired(N, s);
+        {
+          std::vector<uint8_t> kr(static_cast<size_t>(N), 1), rt(static_cast<size_t>(N), 0);
+          for (int32_t sid : order_sid) {
+            kr[sid] = 0;
+            rt[sid] = 1;
+          }
+          keep_row.upload(kr);
+          retired.upload(rt);
+        }
+        i64 batch = std::max<i64>(i64{1} << 24, avail / 4 / 144);
+        if (const char* e = std::getenv("PMMF_B200_BATCH_NNZ")) batch = std::atoll(e);  // test hook
+        PMMF_TRACE("[pmmf] stage %d: column pass -> %lld entries, batch=%lld mem=%zuMB\n", stage_no,
+                   static_cast<long long>(tn), static_cast<long long>(batch), mem_used_mb());
+        rotate_pass(pieces, T, cur.off, slot_base, plan, nullptr, nullptr, batch, s);
+        T = Csc();
+        i64 stored = 0;
+        for (const Piece& P : pieces) stored += P.nnz;
+        PMMF_TRACE("[pmmf] stage %d: row pass stored %lld entries in %zu pieces, mem=%zuMB\n", stage_no,
+                   static_cast<long long>(stored), pieces.size(), mem_used_mb());
+        if (ne > 0) {
+          // Exact residual masses: columns g of A' for the retired g, reduced
+          // chunk by chunk from the rotated transpose (never materialised).
+          mass.zero();
+          diag.zero();
+          PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 1);
+          retired_masses(pieces, N, retired.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(),
+                         diag.get(), chunk, s);
+          PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
+          residual_done = true;
+        }
+        // The next stage reads only the surviving columns of A' (all rows).
+        transpose_pieces(A, pieces, N, keep_row.get(), chunk, s);
+        PMMF_TRACE("[pmmf] stage %d: A' %lld entries, mem=%zuMB\n", stage_no, static_cast<long long>(A.nnz),
+                   mem_used_mb());
       }
     }
     PMMF_CUDA(cudaStreamSynchronize(s));
@@ -381,16 +466,13 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     PMMF_TRACE("[pmmf] stage %d: apply %.2f ms\n", stage_no, ms_since(t0));
 
     // ---- residual accounting against the end-of-stage matrix
-    const i64 ne = static_cast<i64>(order_g.size());
     if (ne > 0) {
-      DBuf<int32_t> dsid(ne, s), dg(ne, s);
-      dsid.upload(order_sid);
-      dg.upload(order_g);
-      PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 1);
-      DBuf<double> mass(ne, s), diag(ne, s);
-      PMMF_LAUNCH(k_residual, blocks_for(ne, kThreads), kThreads, 0, s, ne, dsid.get(), A.ptr.get(), A.row.get(),
-                  A.val.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(), diag.get());
-      PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
+      if (!residual_done) {
+        PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 1);
+        PMMF_LAUNCH(k_residual, blocks_for(ne * 32, kThreads), kThreads, 0, s, ne, dsid.get(), A.ptr.get(), A.row.get(),
+                    A.val.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(), diag.get());
+        PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
+      }
       std::vector<double> hm = mass.to_host(ne), hd = diag.to_host(ne);
       for (i64 r = 0; r < ne; ++r) {
         st.elim_idx.push_back(order_g[r]);

@@ -197,6 +197,80 @@ __global__ void k_reblock_fill(i64 Nn, const int32_t* __restrict__ new2old, cons
   }
 }
 
+// ---------------------------------------------------- chunked transpose
+__global__ void k_row_hist(i64 N, const i64* __restrict__ ptr, const int32_t* __restrict__ row,
+                           const uint8_t* __restrict__ keep_row, int32_t* __restrict__ hist) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= N) return;
+  for (i64 e = ptr[w] + lane; e < ptr[w + 1]; e += 32) {
+    const int32_t r = row[e];
+    if (keep_row == nullptr || keep_row[r]) atomicAdd(&hist[r], 1);
+  }
+}
+__device__ __forceinline__ i64 lb_rows(const int32_t* __restrict__ a, i64 lo, i64 hi, int key) {
+  while (lo < hi) {
+    const i64 mid = (lo + hi) >> 1;
+    if (a[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+// Entries of piece column w with row in [r0, r1) (and kept by the filter).
+__global__ void k_chunk_count(i64 N, i64 c0, const i64* __restrict__ ptr, const int32_t* __restrict__ row,
+                              const uint8_t* __restrict__ keep_row, int r0, int r1, i64* __restrict__ cnt) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= N) return;
+  const i64 lo = lb_rows(row, ptr[w], ptr[w + 1], r0), hi = lb_rows(row, lo, ptr[w + 1], r1);
+  int c = 0;
+  if (keep_row == nullptr) {
+    c = lane == 0 ? static_cast<int>(hi - lo) : 0;
+  } else {
+    for (i64 e = lo + lane; e < hi; e += 32) c += keep_row[row[e]];
+  }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) cnt[c0 + w] = c;
+}
+__global__ void k_chunk_gather(i64 N, i64 c0, const i64* __restrict__ ptr, const int32_t* __restrict__ row,
+                               const double* __restrict__ val, const uint8_t* __restrict__ keep_row, int r0, int r1,
+                               const i64* __restrict__ pos, int cb, uint64_t* __restrict__ keys,
+                               double* __restrict__ vals) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= N) return;
+  const i64 lo = lb_rows(row, ptr[w], ptr[w + 1], r0), hi = lb_rows(row, lo, ptr[w + 1], r1);
+  i64 o = pos[c0 + w];
+  const uint64_t col = static_cast<uint64_t>(c0 + w);
+  for (i64 b = lo; b < hi; b += 32) {
+    const i64 e = b + lane;
+    int32_t r = 0;
+    bool k = false;
+    if (e < hi) {
+      r = row[e];
+      k = keep_row == nullptr || keep_row[r];
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, k);
+    if (k) {
+      const i64 d = o + __popc(m & ((1u << lane) - 1u));
+      keys[d] = (static_cast<uint64_t>(r - r0) << cb) | col;
+      vals[d] = val[e];
+    }
+    o += __popc(m);
+  }
+}
+__global__ void k_chunk_emit(i64 m, const uint64_t* __restrict__ keys, const double* __restrict__ vals, int cb,
+                             int32_t* __restrict__ out_row, double* __restrict__ out_val) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= m) return;
+  out_row[i] = static_cast<int32_t>(keys[i] & ((uint64_t{1} << cb) - 1));
+  out_val[i] = vals[i];
+}
+__global__ void k_hist_widen(i64 N, const int32_t* __restrict__ h, i64* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < N) out[i] = h[i];
+  if (i == N) out[i] = 0;
+}
+
 template <typename T>
 void exclusive_scan(const T* in, T* out, i64 n, cudaStream_t s) {
   size_t tmp = 0;
@@ -365,6 +439,150 @@ void transpose_paged(Csc& out, const Paged& p, cudaStream_t s) {
   out.val = std::move(vals);
   out.ptr.alloc(N + 1, s);
   PMMF_LAUNCH(k_ptr_from_cols, blocks_for(m + 1, kThreads), kThreads, 0, s, m, major.get(), N, out.ptr.get());
+}
+
+// Row-chunked transpose of pieces: rows [r0, r1) at a time are gathered in
+// column order, stable-sorted by row, and handed to `sink` (keys hold
+// (row - r0) << cb | column).  Memory: the row histogram plus one chunk.
+template <typename Sink>
+void transpose_chunks(const std::vector<Piece>& in, i64 N, const uint8_t* keep_row, i64 chunk_nnz,
+                      std::vector<i64>& hp, cudaStream_t s, Sink&& sink) {
+  DBuf<int32_t> hist(N + 1, s);
+  hist.zero();
+  for (const Piece& P : in) {
+    const i64 n = P.c1 - P.c0;
+    PMMF_LAUNCH(k_row_hist, blocks_for(n * 32, kThreads), kThreads, 0, s, n, P.ptr.get(), P.row.get(), keep_row,
+                hist.get());
+  }
+  DBuf<i64> h64(N + 1, s), ptr(N + 1, s);
+  PMMF_LAUNCH(k_hist_widen, blocks_for(N + 1, kThreads), kThreads, 0, s, N, hist.get(), h64.get());
+  exclusive_scan(h64.get(), ptr.get(), N + 1, s);
+  hist.release();
+  h64.release();
+  hp = ptr.to_host(N + 1);
+  const i64 m = hp[N];
+  if (m == 0) return;
+  chunk_nnz = std::max<i64>(chunk_nnz, 1 << 8);
+  DBuf<i64> cnt(N + 1, s), pos(N + 1, s);
+  DBuf<uint64_t> keys(std::min(m, chunk_nnz) + 1, s);
+  DBuf<double> vals(std::min(m, chunk_nnz) + 1, s);
+  const int cb = std::max(1, bits_for(std::max<i64>(N - 1, 1)));
+  i64 r0 = 0;
+  while (r0 < N) {
+    i64 r1 = r0 + 1;
+    while (r1 < N && hp[r1 + 1] - hp[r0] <= chunk_nnz) ++r1;
+    const i64 cm = hp[r1] - hp[r0];
+    if (cm > 0) {
+      if (cm > keys.n) {  // a single huge row
+        keys.alloc(cm, s);
+        vals.alloc(cm, s);
+      }
+      cnt.zero();
+      for (const Piece& P : in) {
+        const i64 n = P.c1 - P.c0;
+        PMMF_LAUNCH(k_chunk_count, blocks_for(n * 32, kThreads), kThreads, 0, s, n, P.c0, P.ptr.get(), P.row.get(),
+                    keep_row, static_cast<int>(r0), static_cast<int>(r1), cnt.get());
+      }
+      exclusive_scan(cnt.get(), pos.get(), N + 1, s);
+      for (const Piece& P : in) {
+        const i64 n = P.c1 - P.c0;
+        PMMF_LAUNCH(k_chunk_gather, blocks_for(n * 32, kThreads), kThreads, 0, s, n, P.c0, P.ptr.get(), P.row.get(),
+                    P.val.get(), keep_row, static_cast<int>(r0), static_cast<int>(r1), pos.get(), cb, keys.get(),
+                    vals.get());
+      }
+      const int rb = std::max(1, bits_for(std::max<i64>(r1 - r0 - 1, 1)));
+      DBuf<uint64_t> k2(cm, s);
+      DBuf<double> v2(cm, s);
+      cub::DoubleBuffer<uint64_t> kb(keys.get(), k2.get());
+      cub::DoubleBuffer<double> vb(vals.get(), v2.get());
+      size_t tmp = 0;
+      PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int64_t>(cm), cb, cb + rb, s));
+      DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+      PMMF_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kb, vb, static_cast<int64_t>(cm), cb, cb + rb, s));
+      sink(r0, r1, cm, cb, kb.Current(), vb.Current(), ptr.get());
+    }
+    r0 = r1;
+  }
+}
+
+void transpose_pieces(Csc& out, const std::vector<Piece>& in, i64 N, const uint8_t* keep_row, i64 chunk_nnz,
+                      cudaStream_t s) {
+  out.N = N;
+  std::vector<i64> hp;
+  // sizes first (the histogram pass of transpose_chunks), then the chunks
+  out.ptr.alloc(N + 1, s);
+  bool allocated = false;
+  transpose_chunks(in, N, keep_row, chunk_nnz, hp, s,
+                   [&](i64 r0, i64, i64 cm, int cb, const uint64_t* keys, const double* vals, const i64*) {
+                     if (!allocated) {
+                       out.row.alloc(std::max<i64>(hp[N], 1), s);
+                       out.val.alloc(std::max<i64>(hp[N], 1), s);
+                       allocated = true;
+                     }
+                     PMMF_LAUNCH(k_chunk_emit, blocks_for(cm, kThreads), kThreads, 0, s, cm, keys, vals, cb,
+                                 out.row.get() + hp[r0], out.val.get() + hp[r0]);
+                   });
+  out.nnz = hp.empty() ? 0 : hp[N];
+  if (!allocated) {
+    out.row.alloc(std::max<i64>(out.nnz, 1), s);
+    out.val.alloc(std::max<i64>(out.nnz, 1), s);
+  }
+  if (!hp.empty()) out.ptr.upload(hp);
+}
+
+namespace {
+// Residual accounting (factorizer.hpp:529-542) for retired rows g of the
+// rotated transpose, i.e. columns g of A': warp per g, entries in column
+// (stage) order, lane 0 sums v^2 sequentially over qualifying rows.
+__global__ void k_chunk_masses(i64 r0, i64 r1, const i64* __restrict__ ptr, const uint64_t* __restrict__ keys,
+                               const double* __restrict__ vals, int cb, const int32_t* __restrict__ s2g,
+                               const uint8_t* __restrict__ is_active, const int32_t* __restrict__ rank,
+                               double* __restrict__ mass, double* __restrict__ diag) {
+  const i64 g = r0 + ((blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (g >= r1) return;
+  const i64 b = ptr[g] - ptr[r0], e = ptr[g + 1] - ptr[r0];
+  if (e == b) return;
+  const int32_t rg = rank[s2g[g]];
+  if (rg < 0) return;
+  const uint64_t cmask = (uint64_t{1} << cb) - 1;
+  double m = 0.0, d = 0.0;
+  for (i64 x = b; x < e; x += 32) {
+    const i64 i = x + lane;
+    double sq = 0.0, v = 0.0;
+    bool take = false, isdiag = false;
+    if (i < e) {
+      const int32_t c = static_cast<int32_t>(keys[i] & cmask);
+      v = vals[i];
+      if (c == g) {
+        isdiag = true;
+      } else {
+        const int32_t l = s2g[c];
+        take = is_active[l] || rank[l] > rg;
+        sq = dmul(v, v);
+      }
+    }
+    const unsigned tk = __ballot_sync(0xffffffffu, take);
+    const unsigned dg = __ballot_sync(0xffffffffu, isdiag);
+    if (dg) d = __shfl_sync(0xffffffffu, v, __ffs(dg) - 1);
+    for (unsigned mm = tk; mm; mm &= mm - 1) m = dadd(m, __shfl_sync(0xffffffffu, sq, __ffs(mm) - 1));
+  }
+  if (lane == 0) {
+    mass[rg] = m;
+    diag[rg] = d;
+  }
+}
+}  // namespace
+
+void retired_masses(const std::vector<Piece>& in, i64 N, const uint8_t* is_retired, const int32_t* s2g,
+                    const uint8_t* is_active, const int32_t* rank, double* mass, double* diag, i64 chunk_nnz,
+                    cudaStream_t s) {
+  std::vector<i64> hp;
+  transpose_chunks(in, N, is_retired, chunk_nnz, hp, s,
+                   [&](i64 r0, i64 r1, i64, int cb, const uint64_t* keys, const double* vals, const i64* ptr) {
+                     PMMF_LAUNCH(k_chunk_masses, blocks_for((r1 - r0) * 32, kThreads), kThreads, 0, s, r0, r1, ptr,
+                                 keys, vals, cb, s2g, is_active, rank, mass, diag);
+                   });
 }
 
 void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_t>& new2old, i64 n_new,

@@ -145,3 +145,92 @@ PMMF_HDI double off_diag_norm_sq(double ns, double d) {
 }
 
 }  // namespace pmmf_b200
+
+namespace pmmf_b200 {
+
+// ---- compile-time-K variants (register resident in device code) --------
+template <int K>
+PMMF_HDI bool rotation_from_gram_k(const double (&g)[K][K], double (&q)[K][K]) {
+  double gg[kMaxK][kMaxK], qq[kMaxK][kMaxK];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) gg[i][j] = g[i][j];
+  const bool ok = rotation_from_gram(gg, K, qq);
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) q[i][j] = qq[i][j];
+  return ok;
+}
+
+template <>
+PMMF_HDI bool rotation_from_gram_k<2>(const double (&g)[2][2], double (&q)[2][2]) {
+  const double asym = fabs(g[0][1] - g[1][0]);
+  const double mx = fmax(fmax(fabs(g[0][0]), fabs(g[0][1])), fmax(fabs(g[1][0]), fabs(g[1][1])));
+  if (asym > 1e-9 * fmax(1.0, mx)) return false;
+  const double w00 = 0.5 * (g[0][0] + g[0][0]);
+  const double w11 = 0.5 * (g[1][1] + g[1][1]);
+  const double w01 = 0.5 * (g[0][1] + g[1][0]);
+  double c, s;
+  jacobi_angle(w00, w11, w01, c, s);
+  q[0][0] = c;
+  q[0][1] = -s;
+  q[1][0] = s;
+  q[1][1] = c;
+  // fix_row_signs (factorizer.hpp:130-144)
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int arg = fabs(q[i][1]) > fabs(q[i][0]) ? 1 : 0;
+    if (q[i][arg] < 0.0) {
+      q[i][0] = -q[i][0];
+      q[i][1] = -q[i][1];
+    }
+  }
+  return true;
+}
+
+template <int K>
+PMMF_HDI void conjugate_corner_k(const double (&q)[K][K], const double (&C)[K][K], double (&out)[K][K]) {
+  double p[K][K];
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) p[i][j] = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const double x = q[i][t];
+      if (x != 0.0) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) p[i][j] += x * C[t][j];
+      }
+    }
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) out[i][j] = 0.0;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int t = 0; t < K; ++t) {
+      const double x = p[i][t];
+      if (x != 0.0) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) out[i][j] += x * q[j][t];
+      }
+    }
+}
+
+template <int K>
+PMMF_HDI bool is_exact_identity_k(const double (&q)[K][K]) {
+  bool id = true;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+#pragma unroll
+    for (int j = 0; j < K; ++j) id = id && q[i][j] == (i == j ? 1.0 : 0.0);
+  return id;
+}
+
+}  // namespace pmmf_b200

@@ -18,3 +18,14 @@ def test_factorize_matches_oracle(name):
     gpu = oracles.factorize("gpu", inp, params, part)
     ref = oracles.factorize("oracle", inp, params, part)
     oracles.assert_same(gpu, ref)
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf512_k4", "zero_cols_bypass",
+                                  "partitioned_input", "k3_sparse"])
+def test_small_batches_and_chunks(name, monkeypatch):
+    """Force many cluster batches in the row pass and tiny transpose chunks
+    (the paths config 4 takes for memory) — still bit-exact."""
+    monkeypatch.setenv("PMMF_B200_BATCH_NNZ", "2000")
+    monkeypatch.setenv("PMMF_B200_CHUNK_NNZ", "3000")
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
