@@ -1,0 +1,214 @@
+// pmmf_b200/dropin.hpp — C++20 drop-in for pmmf::factorize and
+// pmmf::MmfOperator on the GPU.
+//
+// Include AFTER the reference headers (pmmf/factorizer.hpp,
+// pmmf/transform_ops.hpp) and link libpmmf_b200.so.  The functions take and
+// return the reference's own types, so existing callers only swap the
+// namespace:
+//
+//   pmmf::MmfFactorization f = pmmf_b200::factorize(a, params, &stats);
+//       // replaces pmmf::factorize (factorizer.hpp:397-398)
+//   pmmf_b200::GpuOperator op(f);      // replaces pmmf::MmfOperator (transform_ops.hpp:30-41)
+//   op.apply(pmmf::MmfOperator::Mode::inv_sqrt, in, out);
+//
+// Errors are rethrown as the reference's exception types.
+#pragma once
+
+#include <pmmf/factorizer.hpp>
+#include <pmmf/transform_ops.hpp>
+
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../pmmf_b200.h"
+
+namespace pmmf_b200 {
+
+inline void rethrow(int status, const char* err) {
+  const std::string msg(err);
+  switch (status) {
+    case PMMF_OK: return;
+    case PMMF_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case PMMF_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case PMMF_NUMERIC: throw pmmf::NumericError(msg);
+    case PMMF_DATA: throw pmmf::DataError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+struct ResultHandle {
+  void* h = nullptr;
+  ~ResultHandle() {
+    if (h) pmmf_b200_result_free(h);
+  }
+};
+
+// BlockedSparseMatrix -> triplets + partition (blocked_matrix.hpp:421-436).
+inline void to_coo(const pmmf::BlockedSparseMatrix& a, std::vector<int64_t>& r, std::vector<int64_t>& c,
+                   std::vector<double>& v, std::vector<int64_t>& off, std::vector<int64_t>& mem) {
+  for (const pmmf::Triplet& t : a.to_triplets()) {
+    r.push_back(t.row);
+    c.push_back(t.col);
+    v.push_back(t.value);
+  }
+  const pmmf::Partition& p = a.partition();
+  off.assign(1, 0);
+  for (pmmf::index_t u = 0; u < p.num_clusters(); ++u) {
+    auto cl = p.cluster(u);
+    mem.insert(mem.end(), cl.begin(), cl.end());
+    off.push_back(static_cast<int64_t>(mem.size()));
+  }
+}
+
+inline pmmf_b200_params to_params(const pmmf::FactorizeParams& p) {
+  pmmf_b200_params q{};
+  q.k = p.k;
+  q.n_stages = p.n_stages;
+  q.eta = p.eta;
+  q.m_target = p.cluster.m_target;
+  q.c_min = p.cluster.c_min;
+  q.c_max = p.cluster.c_max;
+  q.d_max = p.cluster.d_max;
+  q.bypass_enabled = p.cluster.bypass_enabled ? 1 : 0;
+  q.cluster_seed = p.cluster.seed;
+  q.core_min = p.core_min;
+  q.core_cap = p.core_cap;
+  q.seed = p.seed;
+  return q;
+}
+
+// Runs the GPU stage loop; returns the raw handle (owned by the caller).
+inline void* factorize_handle(const pmmf::BlockedSparseMatrix& input, const pmmf::FactorizeParams& params,
+                              int device = 0) {
+  std::vector<int64_t> r, c, off, mem;
+  std::vector<double> v;
+  to_coo(input, r, c, v, off, mem);
+  pmmf_b200_coo coo{};
+  coo.n = input.dim();
+  coo.nnz = static_cast<int64_t>(v.size());
+  coo.rows = r.data();
+  coo.cols = c.data();
+  coo.vals = v.data();
+  coo.n_clusters = static_cast<int64_t>(off.size()) - 1;
+  coo.cluster_offsets = off.data();
+  coo.cluster_members = mem.data();
+  coo.on_device = 0;
+  coo.device = device;
+  const pmmf_b200_params p = to_params(params);
+  char err[4096] = {0};
+  void* h = nullptr;
+  rethrow(pmmf_b200_factorize(&coo, &p, &h, err, sizeof(err)), err);
+  return h;
+}
+
+// Materialises the reference's MmfFactorization / FactorizeStats
+// (factorizer.hpp:56-118) from a result handle.
+inline pmmf::MmfFactorization materialize(void* h, const pmmf::FactorizeParams& params,
+                                          pmmf::FactorizeStats* stats_out) {
+  pmmf_b200_summary s{};
+  pmmf_b200_result_summary(h, &s);
+  pmmf::MmfFactorization f;
+  f.n = s.n;
+  f.params = params;
+  f.residual_sq = s.residual_sq;
+  f.active_history.resize(static_cast<size_t>(s.n_stages + 1));
+  pmmf_b200_result_active_history(h, f.active_history.data());
+  const int64_t k = s.k;
+  for (int64_t st = 0; st < s.n_stages; ++st) {
+    pmmf_b200_stage_sizes z{};
+    pmmf_b200_result_stage_sizes(h, st, &z);
+    std::vector<int64_t> off(z.n_clusters + 1), mem(std::max<int64_t>(z.partition_size, 1)),
+        ri(std::max<int64_t>(z.n_rotations * k, 1)), ei(std::max<int64_t>(z.n_eliminated, 1)),
+        by(std::max<int64_t>(z.n_bypassed, 1));
+    std::vector<double> rq(std::max<int64_t>(z.n_rotations * k * k, 1)), ed(ei.size()), em(ei.size());
+    pmmf_b200_result_stage(h, st, off.data(), mem.data(), ri.data(), rq.data(), ei.data(), ed.data(), em.data(),
+                           by.data());
+    pmmf::Stage stage;
+    std::vector<std::vector<pmmf::index_t>> cl;
+    for (int64_t u = 0; u < z.n_clusters; ++u) cl.emplace_back(mem.begin() + off[u], mem.begin() + off[u + 1]);
+    stage.partition = std::make_shared<const pmmf::Partition>(std::move(cl));
+    for (int64_t t = 0; t < z.n_rotations; ++t) {
+      pmmf::Rotation rot;
+      rot.stage = static_cast<int>(st + 1);
+      rot.matrix = pmmf::DenseMatrix(k, k);
+      for (int64_t a = 0; a < k; ++a) {
+        rot.indices.push_back(ri[t * k + a]);
+        for (int64_t b = 0; b < k; ++b) rot.matrix(a, b) = rq[(t * k + a) * k + b];
+      }
+      stage.rotations.push_back(std::move(rot));
+    }
+    for (int64_t e = 0; e < z.n_eliminated; ++e) stage.eliminated.push_back({ei[e], ed[e], em[e]});
+    stage.bypassed.assign(by.begin(), by.begin() + z.n_bypassed);
+    f.stages.push_back(std::move(stage));
+  }
+  const int64_t g = s.core_size;
+  std::vector<int64_t> ci(std::max<int64_t>(g, 1)), di(std::max<int64_t>(s.n_diagonal, 1));
+  std::vector<double> core(std::max<int64_t>(g * g, 1)), dv(di.size());
+  pmmf_b200_result_core(h, ci.data(), core.data(), di.data(), dv.data());
+  f.h.core_indices.assign(ci.begin(), ci.begin() + g);
+  f.h.core = pmmf::DenseMatrix(g, g);
+  for (int64_t a = 0; a < g; ++a)
+    for (int64_t b = 0; b < g; ++b) f.h.core(a, b) = core[a * g + b];
+  for (int64_t i = 0; i < s.n_diagonal; ++i) f.h.diagonal.emplace_back(di[i], dv[i]);
+  if (stats_out) {
+    double ph[6];
+    std::vector<int64_t> info(std::max<int64_t>(7 * s.n_stages, 1));
+    pmmf_b200_result_stats(h, ph, info.data());
+    stats_out->phases = {ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]};
+    stats_out->stages.clear();
+    for (int64_t st = 0; st < s.n_stages; ++st) {
+      const int64_t* o = info.data() + 7 * st;
+      stats_out->stages.push_back({static_cast<int>(o[0]), o[1], o[2], o[3], o[4], o[5], static_cast<int>(o[6])});
+    }
+    stats_out->trivial = s.trivial != 0;
+  }
+  return f;
+}
+
+// Drop-in for pmmf::factorize (factorizer.hpp:397-595).
+inline pmmf::MmfFactorization factorize(const pmmf::BlockedSparseMatrix& input, const pmmf::FactorizeParams& params,
+                                        pmmf::FactorizeStats* stats_out = nullptr, int device = 0) {
+  ResultHandle r;
+  r.h = factorize_handle(input, params, device);
+  return materialize(r.h, params, stats_out);
+}
+
+// Drop-in for pmmf::MmfOperator (transform_ops.hpp:30-137) on the GPU.
+class GpuOperator {
+ public:
+  explicit GpuOperator(const pmmf::BlockedSparseMatrix& input, const pmmf::FactorizeParams& params,
+                       double zero_threshold = 1e-12, int device = 0) {
+    ResultHandle r;
+    r.h = factorize_handle(input, params, device);
+    n_ = input.dim();
+    char err[4096] = {0};
+    rethrow(pmmf_b200_operator_create(r.h, zero_threshold, &op_, err, sizeof(err)), err);
+  }
+  GpuOperator(const GpuOperator&) = delete;
+  GpuOperator& operator=(const GpuOperator&) = delete;
+  ~GpuOperator() {
+    if (op_) pmmf_b200_operator_free(op_);
+  }
+  pmmf::index_t dim() const { return n_; }
+  void apply(pmmf::MmfOperator::Mode mode, std::span<const double> in, std::span<double> out) const {
+    if (static_cast<pmmf::index_t>(in.size()) != n_ || static_cast<pmmf::index_t>(out.size()) != n_)
+      throw std::invalid_argument("MmfOperator::apply: dimension mismatch");
+    char err[4096] = {0};
+    rethrow(pmmf_b200_operator_apply(op_, static_cast<int32_t>(mode), 1, in.data(), out.data(), 0, err, sizeof(err)),
+            err);
+  }
+  int inv_sqrt_zeroed_negatives() const {
+    int64_t v = 0;
+    pmmf_b200_operator_zeroed_negatives(op_, &v);
+    return static_cast<int>(v);
+  }
+
+ private:
+  void* op_ = nullptr;
+  pmmf::index_t n_ = 0;
+};
+
+}  // namespace pmmf_b200

@@ -1,0 +1,67 @@
+// oracle/dropin_check.cpp — TEST INFRASTRUCTURE.
+// Compiles the C++ drop-in (include/pmmf_b200/dropin.hpp) against the
+// reference headers and checks pmmf_b200::factorize == pmmf::factorize and
+// GpuOperator::apply == MmfOperator::apply bit-for-bit on a seeded R-MAT
+// input (the reference's own operator== on Rotation / Elimination /
+// Partition).  Built by oracle/Makefile into oracle/_ref/dropin_check; run
+// on the GPU box by tests/test_dropin.py.
+#include <pmmf/factorizer.hpp>
+#include <pmmf/transform_ops.hpp>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../include/pmmf_b200/dropin.hpp"
+#include "../include/pmmf_b200_workloads.h"
+
+int main(int argc, char** argv) {
+  const int scale = argc > 1 ? std::atoi(argv[1]) : 11;
+  pmmf_b200_workload w{};
+  if (pmmf_b200_workload_rmat(scale, 16, 42, 1e-2, &w)) return 2;
+  std::vector<pmmf::Triplet> t(static_cast<size_t>(w.nnz));
+  for (int64_t i = 0; i < w.nnz; ++i) t[i] = {w.rows[i], w.cols[i], w.vals[i]};
+  auto a = pmmf::BlockedSparseMatrix::from_triplets(w.n, t, pmmf::Partition::trivial(w.n));
+  pmmf_b200_workload_free(&w);
+  pmmf::FactorizeParams p;
+  p.cluster.m_target = 16;
+  p.seed = 42;
+  pmmf::FactorizeStats s_ref, s_gpu;
+  const pmmf::MmfFactorization ref = pmmf::factorize(a, p, &s_ref);
+  const pmmf::MmfFactorization gpu = pmmf_b200::factorize(a, p, &s_gpu);
+  int bad = 0;
+  auto check = [&](bool ok, const char* what) {
+    if (!ok) {
+      std::printf("MISMATCH %s\n", what);
+      ++bad;
+    }
+  };
+  check(ref.n == gpu.n, "n");
+  check(ref.stages.size() == gpu.stages.size(), "stage count");
+  for (size_t s = 0; s < std::min(ref.stages.size(), gpu.stages.size()); ++s) {
+    check(*ref.stages[s].partition == *gpu.stages[s].partition, "partition");
+    check(ref.stages[s].rotations == gpu.stages[s].rotations, "rotations");
+    check(ref.stages[s].eliminated == gpu.stages[s].eliminated, "eliminated");
+    check(ref.stages[s].bypassed == gpu.stages[s].bypassed, "bypassed");
+  }
+  check(ref.h.core_indices == gpu.h.core_indices, "core indices");
+  check(ref.h.core == gpu.h.core, "core");
+  check(ref.h.diagonal == gpu.h.diagonal, "diagonal");
+  check(ref.residual_sq == gpu.residual_sq, "residual_sq");
+  check(ref.active_history == gpu.active_history, "active_history");
+  check(s_ref.stages.size() == s_gpu.stages.size(), "stats stages");
+  // operator
+  pmmf::MmfOperator op_ref(std::make_shared<const pmmf::MmfFactorization>(ref));
+  pmmf_b200::GpuOperator op_gpu(a, p);
+  std::vector<double> v(static_cast<size_t>(a.dim())), o1(v.size()), o2(v.size());
+  for (size_t i = 0; i < v.size(); ++i) v[i] = std::sin(0.37 * static_cast<double>(i) + 1.0);
+  for (auto mode : {pmmf::MmfOperator::Mode::forward, pmmf::MmfOperator::Mode::inverse,
+                    pmmf::MmfOperator::Mode::inv_sqrt}) {
+    op_ref.apply(mode, v, o1);
+    op_gpu.apply(mode, v, o2);
+    check(o1 == o2, "operator apply");
+  }
+  std::printf("%s: %zu stages, %zu rotations in stage 1\n", bad ? "FAIL" : "PASS", gpu.stages.size(),
+              gpu.stages.empty() ? size_t{0} : gpu.stages[0].rotations.size());
+  return bad ? 1 : 0;
+}
