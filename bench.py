@@ -200,11 +200,17 @@ def main():
     coo_host, keep_host = abi.make_coo(n, rows, cols, vals, device=local)
     err = lib.errbuf()
 
+    last_phases = np.zeros(6)
+
     def run_device():
         h = ctypes.c_void_p()
         abi.raise_for(lib.factorize(ctypes.byref(coo_dev), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
         s = abi.Summary()
         lib.result_summary(h, ctypes.byref(s))
+        ph = np.zeros(6)
+        info = np.zeros((max(s.n_stages, 1), 7), np.int64)
+        lib.result_stats(h, ph.ctypes.data_as(abi.c_f64p), info.ctypes.data_as(abi.c_i64p))
+        last_phases[:] = ph
         rots = 0
         for st in range(s.n_stages):
             sz = abi.StageSizes()
@@ -314,7 +320,9 @@ def main():
                            "rotations_per_step": int(rots), "parallelism": f"replicas x{world}",
                            "l2": "working set >> 126 MB L2"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clk, "step_ms": step_ms}
+                "clocks": clk, "step_ms": step_ms,
+                "phases_ms_last_step": dict(zip(["clustering", "gram", "search", "apply", "reblock", "total"],
+                                                [round(float(x), 1) for x in last_phases]))}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

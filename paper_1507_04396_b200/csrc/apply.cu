@@ -382,6 +382,15 @@ i64 read_i64(const i64* p, cudaStream_t s) {
   return v;
 }
 
+// a[0] + b[0] with a single synchronisation
+i64 read_sum2(const i64* a, const i64* b, cudaStream_t s) {
+  i64 v[2] = {0, 0};
+  PMMF_CUDA(cudaMemcpyAsync(&v[0], a, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaMemcpyAsync(&v[1], b, sizeof(i64), cudaMemcpyDeviceToHost, s));
+  PMMF_CUDA(cudaStreamSynchronize(s));
+  return v[0] + v[1];
+}
+
 // Batch working set: paged view of columns [col0, col0+N) in an arena.
 struct Batch {
   i64 col0 = 0, N = 0;
@@ -423,7 +432,7 @@ void run_level(Batch& B, const LevelPlan& plan, const int32_t* rots, i64 nrot, c
   A.len = B.len.get();
   PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, np.get(), in_entries.get());
   exscan(np.get(), ioff.get(), nrot, s);
-  const i64 items = read_i64(ioff.get() + nrot - 1, s) + read_i64(np.get() + nrot - 1, s);
+  const i64 items = read_sum2(ioff.get() + nrot - 1, np.get() + nrot - 1, s);
   A.ioff = ioff.get();
   A.nitems = items;
   DBuf<int64_t> cnt(K * items, s), pos(K * items, s);
@@ -432,10 +441,10 @@ void run_level(Batch& B, const LevelPlan& plan, const int32_t* rots, i64 nrot, c
   A.aval = B.val.get();
   ProfScope pc("rotate_count", s);
   PMMF_LAUNCH((k_merge<K, false>), blocks_for(items * 32, kThreads), kThreads, 0, s, A);
-  const double in_bytes = 12.0 * static_cast<double>(in_entries.to_host(1)[0]);
+  const double in_bytes = prof_enabled() ? 12.0 * static_cast<double>(in_entries.to_host(1)[0]) : 0.0;
   pc.finish(in_bytes);
   exscan(cnt.get(), pos.get(), K * items, s);
-  const i64 total = read_i64(pos.get() + K * items - 1, s) + read_i64(cnt.get() + K * items - 1, s);
+  const i64 total = read_sum2(pos.get() + K * items - 1, cnt.get() + K * items - 1, s);
   if (B.used + total > B.cap) B.compact(total, s);
   A.off = B.off.get();
   A.arow = B.row.get();

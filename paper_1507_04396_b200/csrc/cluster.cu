@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <numeric>
 
 #include "engine.cuh"
@@ -94,104 +95,144 @@ struct ScoreArgs {
   int32_t* assign;        // assignment mode: best anchor or -1
   double* rows;           // rows mode: P x m scores (nullptr in assignment mode)
   double* g_scratch;      // per-warp state when shared memory is too small
+  unsigned long long* stats;  // trace: {hit rows, anchor entries} (nullable)
 };
 
 __device__ __forceinline__ bool better(double s, int a, double bs, int ba) {
   return s > bs || (s == bs && a < ba);
 }
 
-// Warp per pool column.  Per-warp state (m anchors): block partial p, total
-// t, last block seen, plus a touched list.
+constexpr int kPrefetch = 8;  // anchor entries of a hit row staged in shared memory
+
+// Per-warp shared state: block partial p[m], total t[m], last block seen
+// last[m], touched list touched[m] + count, and the prefetch buffers.
+__host__ __device__ constexpr size_t score_stride(int m) {
+  return static_cast<size_t>(m) * 24 + 16 + 32 * kPrefetch * 12;
+}
+
+// Warps loop over pool columns.  For every chunk of 32 entries of the
+// column, each lane stages the first kPrefetch (anchor, value) pairs of its
+// row in shared memory; then the rows with anchors are replayed in row
+// order (the reference's summation order per anchor), lanes spread over the
+// row's anchors, updating the two-level accumulators of distinct anchors.
 __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
   extern __shared__ unsigned char smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const i64 warp = blockIdx.x * static_cast<i64>(warps_per_block) + wib;
+  const i64 gwarp = blockIdx.x * static_cast<i64>(warps_per_block) + wib;
+  const i64 nwarps = static_cast<i64>(gridDim.x) * warps_per_block;
   const int m = A.m;
-  const size_t stride = static_cast<size_t>(m) * 24 + 16;
+  const size_t stride = score_stride(m);
   unsigned char* base = use_smem ? smem + stride * wib
-                                 : reinterpret_cast<unsigned char*>(A.g_scratch) + stride * static_cast<size_t>(warp);
+                                 : reinterpret_cast<unsigned char*>(A.g_scratch) + stride * static_cast<size_t>(gwarp);
   double* p = reinterpret_cast<double*>(base);
   double* t = p + m;
   int32_t* last = reinterpret_cast<int32_t*>(t + m);
   int32_t* touched = last + m;
   int32_t* ntouched = touched + m;
-  if (warp >= A.P) return;
+  double* pf_v = reinterpret_cast<double*>(base + static_cast<size_t>(m) * 24 + 16);
+  int32_t* pf_a = reinterpret_cast<int32_t*>(pf_v + 32 * kPrefetch);
   for (int a = lane; a < m; a += 32) {
     p[a] = 0.0;
     t[a] = 0.0;
     last[a] = -1;
   }
-  if (lane == 0) *ntouched = 0;
   __syncwarp();
-  const int32_t j = A.cols[warp];
-  if (A.rows == nullptr && A.self[j] >= 0) {
-    if (lane == 0) A.assign[warp] = A.self[j];
-    return;
-  }
-  const i64 e0 = A.ptr[j], e1 = A.ptr[j + 1];
-  for (i64 base_e = e0; base_e < e1; base_e += 32) {
-    const i64 e = base_e + lane;
-    double v = 0.0;
-    int32_t b = 0;
-    i64 beg = 0, end = 0;
-    if (e < e1) {
-      const int32_t r = A.row[e];
-      v = A.val[e];
-      b = A.blk[r];
-      beg = A.arptr[r];
-      end = A.arptr[r + 1];
+  for (i64 w = gwarp; w < A.P; w += nwarps) {
+    const int32_t j = A.cols[w];
+    if (A.rows == nullptr && A.self[j] >= 0) {
+      if (lane == 0) A.assign[w] = A.self[j];
+      continue;
     }
-    unsigned hits = __ballot_sync(0xffffffffu, end > beg);
-    while (hits) {
-      const int src = __ffs(hits) - 1;
-      hits &= hits - 1;
-      const double vs = __shfl_sync(0xffffffffu, v, src);
-      const int32_t bs = __shfl_sync(0xffffffffu, b, src);
-      const i64 bg = __shfl_sync(0xffffffffu, beg, src);
-      const i64 en = __shfl_sync(0xffffffffu, end, src);
-      for (i64 q = bg + lane; q < en; q += 32) {
-        const int32_t a = A.ent_a[q];
-        const double prod = dmul(vs, A.ent_v[q]);
-        if (last[a] != bs) {
-          if (last[a] < 0) {
-            touched[atomicAdd(ntouched, 1)] = a;
-          } else {
-            t[a] = dadd(t[a], p[a]);
-          }
-          p[a] = 0.0;
-          last[a] = bs;
-        }
-        p[a] = dadd(p[a], prod);
+    int nt = 0;  // touched count (warp-uniform)
+    const i64 e0 = A.ptr[j], e1 = A.ptr[j + 1];
+    for (i64 base_e = e0; base_e < e1; base_e += 32) {
+      const i64 e = base_e + lane;
+      double v = 0.0;
+      int32_t b = 0;
+      i64 beg = 0, cnt = 0;
+      if (e < e1) {
+        const int32_t r = A.row[e];
+        v = A.val[e];
+        b = A.blk[r];
+        beg = A.arptr[r];
+        cnt = A.arptr[r + 1] - beg;
+      }
+      for (int k = 0; k < kPrefetch && k < cnt; ++k) {
+        pf_a[lane * kPrefetch + k] = A.ent_a[beg + k];
+        pf_v[lane * kPrefetch + k] = A.ent_v[beg + k];
       }
       __syncwarp();
+      unsigned hits = __ballot_sync(0xffffffffu, cnt > 0);
+      while (hits) {
+        const int src = __ffs(hits) - 1;
+        hits &= hits - 1;
+        const double vs = __shfl_sync(0xffffffffu, v, src);
+        const int32_t bs = __shfl_sync(0xffffffffu, b, src);
+        const i64 bg = __shfl_sync(0xffffffffu, beg, src);
+        const i64 n = __shfl_sync(0xffffffffu, cnt, src);
+        if (A.stats && lane == 0) {
+          atomicAdd(&A.stats[0], 1ull);
+          atomicAdd(&A.stats[1], static_cast<unsigned long long>(n));
+        }
+        for (i64 q0 = 0; q0 < n; q0 += 32) {
+          const i64 q = q0 + lane;
+          bool fresh = false;
+          int32_t a = 0;
+          if (q < n) {
+            double av;
+            if (q < kPrefetch) {
+              a = pf_a[src * kPrefetch + q];
+              av = pf_v[src * kPrefetch + q];
+            } else {
+              a = A.ent_a[bg + q];
+              av = A.ent_v[bg + q];
+            }
+            const double prod = dmul(vs, av);
+            const int32_t la = last[a];
+            if (la != bs) {
+              if (la < 0) fresh = true; else t[a] = dadd(t[a], p[a]);
+              p[a] = 0.0;
+              last[a] = bs;
+            }
+            p[a] = dadd(p[a], prod);
+          }
+          const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+          if (fresh) touched[nt + __popc(fm & ((1u << lane) - 1u))] = a;
+          nt += __popc(fm);
+        }
+        __syncwarp();
+      }
     }
-  }
-  __syncwarp();
-  const int nt = *ntouched;
-  const double nj = A.cnorm[warp];
-  double best = 0.0;
-  int ba = 0x7fffffff;
-  for (int i = lane; i < nt; i += 32) {
-    const int a = touched[i];
-    const double dot = dadd(t[a], p[a]);
-    const double na = A.anorm[a];
-    double s = 0.0;
-    if (nj > 0.0 && na > 0.0) s = fabs(dot) / dmul(nj, na);
-    if (A.rows) A.rows[static_cast<size_t>(warp) * m + a] = s;
-    if (s > 0.0 && better(s, a, best, ba)) {
-      best = s;
-      ba = a;
+    __syncwarp();
+    const double nj = A.cnorm[w];
+    double best = 0.0;
+    int ba = 0x7fffffff;
+    for (int i = lane; i < nt; i += 32) {
+      const int a = touched[i];
+      const double dot = dadd(t[a], p[a]);
+      const double na = A.anorm[a];
+      double sc = 0.0;
+      if (nj > 0.0 && na > 0.0) sc = fabs(dot) / dmul(nj, na);
+      if (A.rows) A.rows[static_cast<size_t>(w) * m + a] = sc;
+      if (sc > 0.0 && better(sc, a, best, ba)) {
+        best = sc;
+        ba = a;
+      }
+      p[a] = 0.0;  // reset for the next column
+      t[a] = 0.0;
+      last[a] = -1;
     }
-  }
-  for (int o = 16; o; o >>= 1) {
-    const double os = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oa = __shfl_xor_sync(0xffffffffu, ba, o);
-    if (better(os, oa, best, ba)) {
-      best = os;
-      ba = oa;
+    for (int o = 16; o; o >>= 1) {
+      const double os = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, ba, o);
+      if (better(os, oa, best, ba)) {
+        best = os;
+        ba = oa;
+      }
     }
+    if (lane == 0 && A.rows == nullptr) A.assign[w] = best > 0.0 ? ba : -1;
+    __syncwarp();
   }
-  if (lane == 0 && A.rows == nullptr) A.assign[warp] = best > 0.0 ? ba : -1;
 }
 
 struct Scorer {
@@ -248,12 +289,13 @@ struct Scorer {
       dpos.upload(pos);
       set_self(danch, dpos, m, true);
     }
-    const size_t stride = static_cast<size_t>(m) * 24 + 16;
-    int wpb = static_cast<int>(std::min<size_t>(8, (96 * 1024) / stride));
+    const size_t stride = score_stride(m);
+    int wpb = static_cast<int>(std::min<size_t>(8, (100 * 1024) / stride));
     const bool use_smem = wpb >= 1;
     if (!use_smem) wpb = 4;
     DBuf<double> scratch;
-    if (!use_smem) scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(P) + 7) / 8), s);
+    if (!use_smem)  // one state slot per launched warp (grid rounded up to whole blocks)
+      scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(((P + wpb - 1) / wpb) * wpb) + 7) / 8), s);
     DBuf<int32_t> dassign(P, s);
     DBuf<double> drows;
     if (rows_mode) {
@@ -262,10 +304,23 @@ struct Scorer {
     }
     ScoreArgs args{P,           dpool.get(), dpn.get(),        m,           dan.get(),   self.get(),
                    a.ptr.get(), a.row.get(), a.val.get(),      nb.d_blk.get(), rptr.get(), ent_a.get(),
-                   ent_v.get(), dassign.get(), rows_mode ? drows.get() : nullptr, scratch.get()};
+                   ent_v.get(), dassign.get(), rows_mode ? drows.get() : nullptr, scratch.get(), nullptr};
+    DBuf<unsigned long long> stats;
+    if (trace_enabled()) {
+      stats.alloc(2, s);
+      stats.zero();
+      args.stats = stats.get();
+    }
     const size_t smem = use_smem ? stride * static_cast<size_t>(wpb) : 0;
     if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    PMMF_LAUNCH(k_score, static_cast<unsigned>((P + wpb - 1) / wpb), 32 * wpb, smem, s, args, wpb, use_smem);
+    // persistent-style grid: warps loop over the pool
+    const i64 blocks = std::min<i64>((P + wpb - 1) / wpb, use_smem ? 148 * 16 : (P + wpb - 1) / wpb);
+    PMMF_LAUNCH(k_score, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb, use_smem);
+    if (trace_enabled()) {
+      std::vector<unsigned long long> h = stats.to_host(2);
+      std::fprintf(stderr, "[pmmf]   score: pool=%lld anchors=%d pool_nnz~ hit_rows=%llu anchor_entries=%llu\n",
+                   static_cast<long long>(P), m, h[0], h[1]);
+    }
     if (!rows_mode) {
       set_self(danch, danch, m, false);
       *assign = dassign.to_host(P);

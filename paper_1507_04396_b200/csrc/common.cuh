@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -87,6 +88,15 @@ struct ProfScope {
     }
   }
 };
+
+// PMMF_B200_TRACE=1 prints per-stage diagnostics to stderr.
+inline bool trace_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PMMF_B200_TRACE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
 
 // Stream-ordered device buffer (cudaMallocAsync from the device pool).
 template <typename T>

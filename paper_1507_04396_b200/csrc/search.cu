@@ -25,6 +25,8 @@
 // Everything is exact fp64 without contraction (-fmad=false).
 #include <algorithm>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "engine.cuh"
 #include "rng.cuh"
@@ -99,15 +101,17 @@ struct KArgs {
   int32_t* rot_level;
   int32_t* elim_loc;
   int32_t* error;
+  unsigned long long* timing;  // optional: 8 clock64 phase totals per cluster
 };
 
 template <int K>
-__global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
+__global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
   extern __shared__ unsigned char smem[];
   __shared__ Best red[2][kWarps];
   __shared__ int sh_loc[K];
   __shared__ double sh_q[K][K];
   __shared__ int sh_victim;
+  __shared__ int sh_oldts[K];
   const int u = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const i64 c64 = A.c[u];
@@ -129,9 +133,16 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
   if (A.diag_in_smem) {
     gd = reinterpret_cast<double*>(smem + ((static_cast<size_t>(nwords) * 4 + 15) / 16) * 16);
   } else {
-    gd = A.diag_scratch + static_cast<i64>(u) * 2 * A.max_c;
+    gd = A.diag_scratch + static_cast<i64>(u) * 3 * A.max_c;
   }
   dd = gd + c;
+  // ts[i]: rotation counter of the last rotation that rewrote column i.
+  // Entry (row a, column b) lives in column b, unless a was rotated later
+  // than b, in which case it lives in column a (at row b): the reference's
+  // mirror write (sparse.hpp:433-439) stores the same value in both places,
+  // and corner pairs (equal ts) keep their own, possibly asymmetric, copy.
+  // So no strided mirror writes are needed.
+  int32_t* ts = reinterpret_cast<int32_t*>(dd + c);
   int32_t* level = A.level_scratch + static_cast<i64>(u) * A.max_c;
   double* G = A.G + A.tile[u];
   double* D = A.D + A.tile[u];
@@ -142,16 +153,25 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
   for (int l = tid; l < c; l += kSearchThreads) {
     gd[l] = G[static_cast<i64>(l) * c + l];
     dd[l] = D[static_cast<i64>(l) * c + l];
+    ts[l] = 0;
     level[l] = 0;
   }
   Xoshiro rng(A.seed[u]);  // every thread advances an identical copy
   int count = c, nrot = 0, nelim = 0, par = 0;
+  unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0}, tprev = clock64();
+#define TMARK(i)                                   \
+  if (A.timing && tid == 0) {                      \
+    const unsigned long long now_ = clock64();     \
+    tacc[i] += now_ - tprev;                       \
+    tprev = now_;                                  \
+  }
   __syncthreads();
 
   for (i64 s = 0; s < budget; ++s) {
     if (count <= K - 1) break;
     const int idx = static_cast<int>(rng.uniform_below(static_cast<uint64_t>(count)));
     const int draw = warp_select(bits, nwords, idx);
+    TMARK(0)
     if (gd[draw] <= 0.0) {  // vanished column: retire without a rotation (:234-238)
       __syncthreads();      // everyone has read bits for this draw
       if (tid == 0) {
@@ -168,6 +188,7 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
     loc[0] = draw;
     int npart = 0;
     const double* gcol = G + static_cast<i64>(draw) * c;
+    const int tsd = ts[draw];
 #pragma unroll 1
     for (int round = 0; round < K - 1; ++round) {
       double bs = 0.0;
@@ -176,8 +197,11 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
         double gv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+          // G(l, draw): column draw, or column l when l was rotated later
           const int l = l0 + j * kSearchThreads;
-          gv[j] = l < c ? gcol[l] : 0.0;
+          gv[j] = 0.0;
+          if (l < c && is_on(bits, l))
+            gv[j] = ts[l] > tsd ? G[static_cast<i64>(l) * c + draw] : gcol[l];
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -235,6 +259,7 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
         }
       }
     }
+    TMARK(1)
     // ---- rotation + corners + victim (warp 0; lane 0 writes)
     if (wid == 0) {
       double gs[K][K], cd[K][K], q[K][K], ng[K][K], nd[K][K];
@@ -242,8 +267,11 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
       for (int a = 0; a < K; ++a)
 #pragma unroll
         for (int b = 0; b < K; ++b) {
-          gs[a][b] = G[static_cast<i64>(loc[b]) * c + loc[a]];
-          cd[a][b] = D[static_cast<i64>(loc[b]) * c + loc[a]];
+          // entry (row loc[a], column loc[b]) under the timestamp rule
+          const bool rowcol = ts[loc[a]] > ts[loc[b]];
+          const i64 at = rowcol ? static_cast<i64>(loc[a]) * c + loc[b] : static_cast<i64>(loc[b]) * c + loc[a];
+          gs[a][b] = G[at];
+          cd[a][b] = D[at];
         }
       const bool ok = rotation_from_gram_k<K>(gs, q);
       conjugate_corner_k<K>(q, gs, ng);
@@ -298,9 +326,17 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
         }
         sh_victim = victim;
         A.elim_loc[base + nelim] = victim;
+        // old timestamps of the rotated columns for the row pass below; the
+        // rotated columns become authoritative for every row
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          sh_oldts[a] = ts[loc[a]];
+          ts[loc[a]] = nrot + 1;
+        }
       }
     }
     __syncthreads();
+    TMARK(2)
     // Other warps may still have been reading the bitmask (partner fill)
     // before barrier 2; retire the victim only now.
     if (tid == 0) bits[sh_victim >> 5] &= ~(1u << (sh_victim & 31));
@@ -311,37 +347,60 @@ __global__ void __launch_bounds__(kSearchThreads) k_search(KArgs A) {
       for (int a = 0; a < K; ++a)
 #pragma unroll
         for (int b = 0; b < K; ++b) q[a][b] = sh_q[a][b];
-      for (int r = tid; r < c; r += kSearchThreads) {
-        bool corner = false;
+      // kRows rows per thread per round: all column loads are issued before
+      // any store, so a round costs one memory round trip.
+      constexpr int kRows = (K <= 3) ? 4 : 2;
+      int oldts[K];
 #pragma unroll
-        for (int a = 0; a < K; ++a) corner |= loc[a] == r;
-        if (corner) continue;
-        double vg[K], vd[K];
+      for (int b = 0; b < K; ++b) oldts[b] = sh_oldts[b];
+      for (int r0 = tid; r0 < c; r0 += kRows * kSearchThreads) {
+        double vg[kRows][K], vd[kRows][K];
+        bool ok[kRows];
 #pragma unroll
-        for (int b = 0; b < K; ++b) {
-          vg[b] = G[static_cast<i64>(loc[b]) * c + r];
-          vd[b] = D[static_cast<i64>(loc[b]) * c + r];
-        }
+        for (int j = 0; j < kRows; ++j) {
+          const int r = r0 + j * kSearchThreads;
+          // Rows of retired indices are never read again by any decision
+          // (partners, corners and victims involve active indices only).
+          bool skip = r >= c || !is_on(bits, r);
 #pragma unroll
-        for (int a = 0; a < K; ++a) {
-          double ag = 0.0, ad = 0.0;
+          for (int a = 0; a < K; ++a) skip |= loc[a] == r;
+          ok[j] = !skip;
+          const int tr = ok[j] ? ts[r] : 0;
 #pragma unroll
           for (int b = 0; b < K; ++b) {
-            ag = dadd(ag, dmul(q[a][b], vg[b]));
-            ad = dadd(ad, dmul(q[a][b], vd[b]));
+            const i64 at = tr > oldts[b] ? static_cast<i64>(r) * c + loc[b] : static_cast<i64>(loc[b]) * c + r;
+            vg[j][b] = ok[j] ? G[at] : 0.0;
+            vd[j][b] = ok[j] ? D[at] : 0.0;
           }
-          G[static_cast<i64>(loc[a]) * c + r] = ag;
-          G[static_cast<i64>(r) * c + loc[a]] = ag;
-          D[static_cast<i64>(loc[a]) * c + r] = ad;
-          D[static_cast<i64>(r) * c + loc[a]] = ad;
+        }
+#pragma unroll
+        for (int j = 0; j < kRows; ++j) {
+          if (!ok[j]) continue;
+          const int r = r0 + j * kSearchThreads;
+#pragma unroll
+          for (int a = 0; a < K; ++a) {
+            double ag = 0.0, ad = 0.0;
+#pragma unroll
+            for (int b = 0; b < K; ++b) {
+              ag = dadd(ag, dmul(q[a][b], vg[j][b]));
+              ad = dadd(ad, dmul(q[a][b], vd[j][b]));
+            }
+            G[static_cast<i64>(loc[a]) * c + r] = ag;
+            D[static_cast<i64>(loc[a]) * c + r] = ad;
+          }
         }
       }
     }
+    TMARK(3)
     --count;
     ++nrot;
     ++nelim;
     __syncthreads();
+    TMARK(4)
   }
+  if (A.timing && tid == 0)
+    for (int i = 0; i < 6; ++i) A.timing[static_cast<i64>(u) * 8 + i] = tacc[i];
+#undef TMARK
   if (tid == 0) {
     A.nrot[u] = nrot;
     A.nelim[u] = nelim;
@@ -362,16 +421,23 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
   if (nclusters <= 0) return;
   const i64 nwords = (max_c + 31) / 32;
   const size_t bits_bytes = ((static_cast<size_t>(nwords) * 4 + 15) / 16) * 16;
-  const size_t diag_bytes = static_cast<size_t>(max_c) * 16;
+  const size_t diag_bytes = static_cast<size_t>(max_c) * 20;  // gd, dd (fp64) + ts (int32)
   const bool diag_in_smem = bits_bytes + diag_bytes <= 180 * 1024;
   const size_t smem = bits_bytes + (diag_in_smem ? diag_bytes : 0);
   DBuf<double> diag_scratch;
-  if (!diag_in_smem) diag_scratch.alloc(nclusters * 2 * max_c, s);
+  if (!diag_in_smem) diag_scratch.alloc(nclusters * 3 * max_c, s);
   DBuf<int32_t> level_scratch(nclusters * max_c, s);
   KArgs a{b.c.get(),           b.tile.get(),        b.budget.get(),       b.seed.get(),        b.out_base.get(),
           eta,                 G,                   D,                    diag_scratch.get(),  level_scratch.get(),
           max_c,               diag_in_smem,        out.nrot.get() + u0,  out.nelim.get() + u0, out.rot_loc.get(),
-          out.rot_q.get(),     out.rot_level.get(), out.elim_loc.get(),   out.error.get()};
+          out.rot_q.get(),     out.rot_level.get(), out.elim_loc.get(),   out.error.get(), nullptr};
+  DBuf<unsigned long long> timing;
+  const bool tm = std::getenv("PMMF_B200_SEARCH_TIMING") != nullptr;
+  if (tm) {
+    timing.alloc(nclusters * 8, s);
+    timing.zero();
+    a.timing = timing.get();
+  }
   switch (k) {
     case 2: launch<2>(a, nclusters, smem, s); break;
     case 3: launch<3>(a, nclusters, smem, s); break;
@@ -381,6 +447,22 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
     case 7: launch<7>(a, nclusters, smem, s); break;
     case 8: launch<8>(a, nclusters, smem, s); break;
     default: fail(PMMF_INVALID_ARGUMENT, "FactorizeParams: k must be in [2, 8]");
+  }
+  if (tm) {
+    std::vector<unsigned long long> h = timing.to_host(nclusters * 8);
+    unsigned long long tot[6] = {0, 0, 0, 0, 0, 0}, mx = 0;
+    i64 arg = 0;
+    for (i64 u = 0; u < nclusters; ++u) {
+      unsigned long long t = 0;
+      for (int i = 0; i < 6; ++i) t += h[u * 8 + i];
+      if (t > mx) {
+        mx = t;
+        arg = u;
+      }
+    }
+    std::fprintf(stderr, "[pmmf] search timing (slowest cluster %lld of %lld): select %llu partner %llu rot %llu offcorner %llu barrier %llu cycles\n",
+                 static_cast<long long>(arg), static_cast<long long>(nclusters), h[arg * 8 + 0], h[arg * 8 + 1],
+                 h[arg * 8 + 2], h[arg * 8 + 3], h[arg * 8 + 4]);
   }
 }
 

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT/tests
+timeout 300 python -m pytest -x -q test_gpu_parity.py test_golden.py -m gpu 2>&1 | tail -3
+cd ..
+PMMF_B200_TRACE=1 timeout 300 python scripts/one_factorize.py c4 2>&1 | grep -E "score|stage [1-4]: (gram|apply)|wall|rror" | head -60
