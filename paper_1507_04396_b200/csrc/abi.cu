@@ -58,6 +58,13 @@ void prof_add(const char* name, double ms, double bytes) {
   s.ms += ms;
   s.bytes += bytes;
 }
+void prof_add_n(const char* name, int64_t launches, double ms, double bytes) {
+  std::lock_guard<std::mutex> g(prof_mu());
+  ProfStat& s = prof_map()[name];
+  s.launches += launches;
+  s.ms += ms;
+  s.bytes += bytes;
+}
 int guarded_call(char* err, size_t errlen, void (*fn)(void*), void* ctx) {
   try {
     fn(ctx);

@@ -69,6 +69,7 @@ struct PassArgs {
   i64 base;              // arena offset of this level's outputs (write pass)
   int32_t* wrow;
   double* wval;
+  unsigned long long* out_entries;  // profiling: outputs allocated
 };
 
 // Row range of partition p of rotation t: split points are rows of the
@@ -227,6 +228,124 @@ __global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long
   }
   nparts[i] = max(1, (Lmax + kChunk - 1) / kChunk);
   atomicAdd(in_entries, S);
+}
+
+// nitems = ioff[nrot-1] + nparts[nrot-1], on the device (no host sync).
+__global__ void k_items(i64 nrot, const int64_t* __restrict__ ioff, const int64_t* __restrict__ np,
+                        int64_t* __restrict__ nitems) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *nitems = ioff[nrot - 1] + np[nrot - 1];
+}
+
+// Per rotation: exclusive scan of its partitions' kept counts per output
+// column, one arena allocation (atomicAdd on the cursor) for all K outputs,
+// absolute write offsets per partition.  Overflow marks the level as not
+// committed; the host compacts and resumes at that level.
+template <int K>
+__global__ void k_rot_alloc(PassArgs A, const int64_t* __restrict__ nitems_d, unsigned long long* __restrict__ cursor,
+                            i64 cap, int32_t* __restrict__ ovf, int level, int64_t* __restrict__ pos,
+                            i64* __restrict__ rbase, int32_t* __restrict__ rlen) {
+  const i64 i = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= A.nrot || *reinterpret_cast<volatile int32_t*>(ovf) != INT_MAX) return;
+  const i64 nitems = *nitems_d;
+  const i64 np = (i + 1 < A.nrot ? A.ioff[i + 1] : nitems) - A.ioff[i];
+  i64 tot[K];
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    const i64 f = K * A.ioff[i] + a * np;
+    i64 run = 0;
+    for (i64 p0 = 0; p0 < np; p0 += 32) {
+      const i64 p = p0 + lane;
+      const i64 c = p < np ? A.cnt[f + p] : 0;
+      i64 incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const i64 v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (p < np) pos[f + p] = run + incl - c;  // within-column offset
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    tot[a] = run;
+  }
+  i64 all = 0;
+#pragma unroll
+  for (int a = 0; a < K; ++a) all += tot[a];
+  unsigned long long b = 0;
+  if (lane == 0) b = atomicAdd(cursor, static_cast<unsigned long long>(all));
+  b = __shfl_sync(0xffffffffu, b, 0);
+  if (static_cast<i64>(b) + all > cap) {
+    if (lane == 0) atomicMin(ovf, level);
+    return;
+  }
+  if (lane == 0) atomicAdd(A.out_entries, static_cast<unsigned long long>(all));
+  i64 col = static_cast<i64>(b);
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    const i64 f = K * A.ioff[i] + a * np;
+    for (i64 p = lane; p < np; p += 32) pos[f + p] += col;
+    if (lane == 0) {
+      rbase[K * i + a] = col;
+      rlen[K * i + a] = static_cast<int32_t>(tot[a]);
+    }
+    col += tot[a];
+  }
+}
+
+template <int K>
+__global__ void k_commit_level(PassArgs A, const i64* __restrict__ rbase, const int32_t* __restrict__ rlen,
+                               const int32_t* __restrict__ ovf, i64* __restrict__ off, int32_t* __restrict__ len) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= A.nrot || *reinterpret_cast<volatile const int32_t*>(ovf) != INT_MAX) return;
+  const int t = A.rots[i];
+#pragma unroll
+  for (int a = 0; a < K; ++a) {
+    const int id = A.ids[static_cast<i64>(t) * K + a] - static_cast<int>(A.col0);
+    off[id] = rbase[K * i + a];
+    len[id] = rlen[K * i + a];
+  }
+}
+
+// Persistent variant: warps stride over the level's partitions; the
+// partition count is read from the device.
+template <int K, bool kWrite>
+__global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, const int32_t* __restrict__ ovf) {
+  if (*reinterpret_cast<volatile const int32_t*>(ovf) != INT_MAX) return;
+  const i64 nitems = *nitems_d;
+  const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+  for (i64 item = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5; item < nitems; item += nw) {
+    i64 lo = 0, hi = A.nrot;
+    while (hi - lo > 1) {
+      const i64 mid = (lo + hi) >> 1;
+      if (A.ioff[mid] <= item) lo = mid; else hi = mid;
+    }
+    const i64 ri = lo;
+    const i64 p = item - A.ioff[ri];
+    const i64 np = (ri + 1 < A.nrot ? A.ioff[ri + 1] : nitems) - A.ioff[ri];
+    const int t = A.rots[ri];
+    int id[K];
+    double q[K][K];
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      id[b] = A.ids[static_cast<i64>(t) * K + b] - static_cast<int>(A.col0);
+#pragma unroll
+      for (int a = 0; a < K; ++a) q[b][a] = A.qs[(static_cast<i64>(t) * K + b) * K + a];
+    }
+    i64 beg[K], end[K];
+    partition_range<K>(A, t, p, np, id, beg, end);
+    int kept[K];
+    i64 dst[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      kept[a] = 0;
+      dst[a] = kWrite ? A.pos[K * A.ioff[ri] + a * np + p] : 0;
+    }
+    merge_partition<K, kWrite>(A, q, beg, end, kept, dst);
+    if (!kWrite && (threadIdx.x & 31) == 0) {
+#pragma unroll
+      for (int a = 0; a < K; ++a) A.cnt[K * A.ioff[ri] + a * np + p] = kept[a];
+    }
+  }
 }
 
 template <int K, bool kWrite>
@@ -417,49 +536,65 @@ struct Batch {
   }
 };
 
+// Per-batch device scratch for the asynchronous level pipeline.
+struct LevelScratch {
+  i64 max_rot = 0, max_items = 0;
+  DBuf<int64_t> np, ioff, nitems, cnt, pos;
+  DBuf<i64> rbase;
+  DBuf<int32_t> rlen, ovf;
+  DBuf<unsigned long long> cursor, in_entries;
+  DBuf<unsigned char> scan_tmp;
+  size_t scan_bytes = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // profiled write passes
+  double rot_bytes = 0.0;
+};
+
+constexpr int kPersistentBlocks = 148 * 8;
+
+// One dependency level of a batch, entirely on the device (no host sync).
 template <int K>
-void run_level(Batch& B, const LevelPlan& plan, const int32_t* rots, i64 nrot, cudaStream_t s) {
+void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* rots, i64 nrot, int level,
+               cudaStream_t s) {
   PassArgs A{};
   A.rots = rots;
   A.ids = plan.ids.get();
   A.qs = plan.q;
   A.col0 = B.col0;
   A.nrot = nrot;
-  DBuf<int64_t> np(nrot, s), ioff(nrot + 1, s);
-  DBuf<unsigned long long> in_entries(1, s);
-  in_entries.zero();
   A.off = B.off.get();
   A.len = B.len.get();
-  PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, np.get(), in_entries.get());
-  exscan(np.get(), ioff.get(), nrot, s);
-  const i64 items = read_sum2(ioff.get() + nrot - 1, np.get() + nrot - 1, s);
-  A.ioff = ioff.get();
-  A.nitems = items;
-  DBuf<int64_t> cnt(K * items, s), pos(K * items, s);
-  A.cnt = cnt.get();
   A.arow = B.row.get();
   A.aval = B.val.get();
-  ProfScope pc("rotate_count", s);
-  PMMF_LAUNCH((k_merge<K, false>), blocks_for(items * 32, kThreads), kThreads, 0, s, A);
-  const double in_bytes = prof_enabled() ? 12.0 * static_cast<double>(in_entries.to_host(1)[0]) : 0.0;
-  pc.finish(in_bytes);
-  exscan(cnt.get(), pos.get(), K * items, s);
-  const i64 total = read_sum2(pos.get() + K * items - 1, cnt.get() + K * items - 1, s);
-  if (B.used + total > B.cap) B.compact(total, s);
-  A.off = B.off.get();
-  A.arow = B.row.get();
-  A.aval = B.val.get();
-  A.pos = pos.get();
-  A.base = B.used;
   A.wrow = B.row.get();
   A.wval = B.val.get();
-  ProfScope pw("rotate_write", s);
-  PMMF_LAUNCH((k_merge<K, true>), blocks_for(items * 32, kThreads), kThreads, 0, s, A);
-  // algorithmic bytes: inputs read once, outputs written
-  // once (12 B per entry), rotation blocks (8k^2 + 4k per rotation)
-  pw.finish(in_bytes + 12.0 * static_cast<double>(total) + static_cast<double>(nrot) * (8.0 * K * K + 4.0 * K));
-  PMMF_LAUNCH(k_commit<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, B.off.get(), B.len.get(), total);
-  B.used += total;
+  A.ioff = S.ioff.get();
+  A.cnt = S.cnt.get();
+  A.pos = S.pos.get();
+  A.nitems = S.max_items;  // bound; kernels read the exact count from S.nitems
+  A.out_entries = S.in_entries.get() + 1;
+  PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
+  {
+    size_t tmp = S.scan_bytes;
+    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
+  }
+  PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
+  PMMF_LAUNCH((k_merge_p<K, false>), kPersistentBlocks, kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  PMMF_LAUNCH(k_rot_alloc<K>, blocks_for(nrot * 32, kThreads), kThreads, 0, s, A, S.nitems.get(), S.cursor.get(), B.cap,
+              S.ovf.get(), level, S.pos.get(), S.rbase.get(), S.rlen.get());
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof_enabled()) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+  }
+  PMMF_LAUNCH((k_merge_p<K, true>), kPersistentBlocks, kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  if (e0) {
+    cudaEventRecord(e1, s);
+    S.ev.push_back({e0, e1});
+    S.rot_bytes += static_cast<double>(nrot) * (8.0 * K * K + 4.0 * K);
+  }
+  PMMF_LAUNCH(k_commit_level<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.rbase.get(), S.rlen.get(), S.ovf.get(),
+              B.off.get(), B.len.get());
 }
 
 __global__ void k_plan(const int32_t* __restrict__ nrot, const int64_t* __restrict__ base,
@@ -555,29 +690,94 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     }
     PMMF_LAUNCH(k_paged_init_local, blocks_for(B.N, kThreads), kThreads, 0, s, B.N, in.ptr.get(), B.col0, e0,
                 B.off.get(), B.len.get());
-    // levels restricted to the batch's rotation slots
+    // levels restricted to the batch's rotation slots: the plan's order is
+    // sorted by (level, slot), so the batch's slots are a contiguous
+    // sub-range of every level (found on the host copy)
     const i64 sb = slot_base[u0], se = slot_base[u1];
+    std::vector<std::pair<i64, i64>> range(static_cast<size_t>(plan.max_level) + 1, {0, 0});
+    i64 max_rot = 1;
     for (int L = 1; L <= plan.max_level && se > sb; ++L) {
       const i64 b = plan.level_start[L - 1], e = plan.level_start[L];
       if (e <= b) continue;
-      // the plan's order is sorted by (level, slot): the batch's slots are a
-      // contiguous sub-range found on the host copy
       const i64 lo = std::lower_bound(plan.h_order.begin() + b, plan.h_order.begin() + e, static_cast<int32_t>(sb)) -
                      plan.h_order.begin();
       const i64 hi = std::lower_bound(plan.h_order.begin() + b, plan.h_order.begin() + e, static_cast<int32_t>(se)) -
                      plan.h_order.begin();
-      if (hi <= lo) continue;
-      const int32_t* rots = plan.order.get() + lo;
-      switch (plan.k) {
-        case 2: run_level<2>(B, plan, rots, hi - lo, s); break;
-        case 3: run_level<3>(B, plan, rots, hi - lo, s); break;
-        case 4: run_level<4>(B, plan, rots, hi - lo, s); break;
-        case 5: run_level<5>(B, plan, rots, hi - lo, s); break;
-        case 6: run_level<6>(B, plan, rots, hi - lo, s); break;
-        case 7: run_level<7>(B, plan, rots, hi - lo, s); break;
-        case 8: run_level<8>(B, plan, rots, hi - lo, s); break;
-        default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
+      range[L] = {lo, hi};
+      max_rot = std::max(max_rot, hi - lo);
+    }
+    LevelScratch S;
+    const int K = plan.k;
+    auto size_items = [&] {
+      S.max_items = max_rot + B.cap / kChunk + 1;
+      S.cnt.alloc(K * S.max_items, s);
+      S.pos.alloc(K * S.max_items, s);
+    };
+    S.max_rot = max_rot;
+    S.np.alloc(max_rot, s);
+    S.ioff.alloc(max_rot + 1, s);
+    S.nitems.alloc(1, s);
+    S.rbase.alloc(K * max_rot, s);
+    S.rlen.alloc(K * max_rot, s);
+    S.ovf.alloc(1, s);
+    S.cursor.alloc(1, s);
+    S.in_entries.alloc(2, s);
+    S.in_entries.zero();
+    {
+      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, S.scan_bytes, S.np.get(), S.ioff.get(),
+                                              static_cast<int64_t>(max_rot), s));
+      S.scan_tmp.alloc(static_cast<i64>(S.scan_bytes) + 1, s);
+    }
+    size_items();
+    auto set_scalar = [&](auto& buf, auto v) {
+      PMMF_CUDA(cudaMemcpyAsync(buf.get(), &v, sizeof(v), cudaMemcpyHostToDevice, s));
+      PMMF_CUDA(cudaStreamSynchronize(s));
+    };
+    set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));
+    set_scalar(S.cursor, static_cast<unsigned long long>(ne));
+    int Lstart = 1;
+    for (;;) {
+      for (int L = Lstart; L <= plan.max_level; ++L) {
+        const auto [lo, hi] = range[L];
+        if (hi <= lo) continue;
+        const int32_t* rots = plan.order.get() + lo;
+        switch (K) {
+          case 2: run_level<2>(B, S, plan, rots, hi - lo, L, s); break;
+          case 3: run_level<3>(B, S, plan, rots, hi - lo, L, s); break;
+          case 4: run_level<4>(B, S, plan, rots, hi - lo, L, s); break;
+          case 5: run_level<5>(B, S, plan, rots, hi - lo, L, s); break;
+          case 6: run_level<6>(B, S, plan, rots, hi - lo, L, s); break;
+          case 7: run_level<7>(B, S, plan, rots, hi - lo, L, s); break;
+          case 8: run_level<8>(B, S, plan, rots, hi - lo, L, s); break;
+          default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
+        }
       }
+      int32_t ovf = 0;
+      PMMF_CUDA(cudaMemcpyAsync(&ovf, S.ovf.get(), sizeof(ovf), cudaMemcpyDeviceToHost, s));
+      PMMF_CUDA(cudaStreamSynchronize(s));
+      if (ovf == INT_MAX) break;
+      // Level `ovf` did not fit: nothing of it was committed.  Compact the
+      // live columns into a larger arena and resume there.
+      B.compact(std::max<i64>(B.cap, i64{1} << 22), s);
+      size_items();
+      set_scalar(S.cursor, static_cast<unsigned long long>(B.used));
+      set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));
+      Lstart = ovf;
+    }
+    if (prof_enabled() && !S.ev.empty()) {
+      double ms = 0.0;
+      for (auto& [e0, e1] : S.ev) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        ms += t;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+      }
+      std::vector<unsigned long long> io = S.in_entries.to_host(2);
+      // algorithmic bytes: inputs read once, outputs written
+      // once (12 B per entry), rotation blocks (8k^2 + 4k per rotation)
+      prof_add_n("rotate_write", static_cast<int64_t>(S.ev.size()), ms,
+                 12.0 * static_cast<double>(io[0] + io[1]) + S.rot_bytes);
     }
     // finalize into a compact piece
     Piece P;

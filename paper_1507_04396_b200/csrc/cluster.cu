@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <numeric>
@@ -255,6 +256,7 @@ struct Scorer {
     const i64 P = static_cast<i64>(pool.size());
     const int m = static_cast<int>(anchors.size());
     if (P == 0) return;
+    const auto t_start = std::chrono::steady_clock::now();
     DBuf<int32_t> dpool(P, s), danch(m, s);
     DBuf<double> dpn(P, s), dan(m, s);
     dpool.upload(pool);
@@ -318,8 +320,9 @@ struct Scorer {
     PMMF_LAUNCH(k_score, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb, use_smem);
     if (trace_enabled()) {
       std::vector<unsigned long long> h = stats.to_host(2);
-      std::fprintf(stderr, "[pmmf]   score: pool=%lld anchors=%d pool_nnz~ hit_rows=%llu anchor_entries=%llu\n",
-                   static_cast<long long>(P), m, h[0], h[1]);
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+      std::fprintf(stderr, "[pmmf]   score: pool=%lld anchors=%d hit_rows=%llu anchor_entries=%llu %.2f ms\n",
+                   static_cast<long long>(P), m, h[0], h[1], ms);
     }
     if (!rows_mode) {
       set_self(danch, danch, m, false);
@@ -478,6 +481,7 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
     if (!bypass || hn[i] > 0.0) pool.push_back(active[i]);
     else res.bypassed.push_back(active[i]);
   }
+  const auto t_norms = std::chrono::steady_clock::now();
   if (!pool.empty()) {
     Scorer sc(a, nb, s);
     Ctx ctx{&sc, &nb, &norm, c_min, c_max, d_max};
@@ -485,6 +489,10 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
     recurse(ctx, std::move(pool), m_target, 0, rng, res.clusters);
     res.max_depth = ctx.max_depth;
   }
+  if (trace_enabled())
+    std::fprintf(stderr, "[pmmf]   clustering: %.2f ms after norms (pool %lld, nnz %lld)\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_norms).count(),
+                 static_cast<long long>(P), static_cast<long long>(a.nnz));
   std::sort(res.bypassed.begin(), res.bypassed.end());
   return res;
 }

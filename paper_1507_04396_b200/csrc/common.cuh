@@ -58,6 +58,7 @@ bool prof_enabled();
 void prof_set(bool on);
 bool prof_get(const char* name, ProfStat* out);
 void prof_add(const char* name, double ms, double bytes);
+void prof_add_n(const char* name, int64_t launches, double ms, double bytes);
 struct ProfScope {
   const char* name;
   cudaStream_t s;
