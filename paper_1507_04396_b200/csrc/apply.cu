@@ -662,7 +662,7 @@ void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_b
 
 void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
                  const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
-                 const uint8_t* keep_all_col, i64 batch_nnz, cudaStream_t s) {
+                 const uint8_t* keep_all_col, i64 batch_nnz, double growth, cudaStream_t s) {
   out.clear();
   const i64 m = static_cast<i64>(off.size()) - 1;
   // host copy of ptr at cluster boundaries
@@ -678,7 +678,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     B.col0 = off[u0];
     B.N = off[u1] - off[u0];
     const i64 e0 = eptr[u0], ne = eptr[u1] - eptr[u0];
-    B.cap = std::max<i64>(4 * ne, ne + (i64{1} << 22));
+    B.cap = std::max<i64>(static_cast<i64>(static_cast<double>(ne) * std::max(growth, 2.0)), ne + (i64{1} << 22));
     B.used = ne;
     B.off.alloc(std::max<i64>(B.N, 1), s);
     B.len.alloc(std::max<i64>(B.N, 1), s);
@@ -759,6 +759,9 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       // Level `ovf` did not fit: nothing of it was committed.  Compact the
       // live columns into a larger arena and resume there.
       B.compact(std::max<i64>(B.cap, i64{1} << 22), s);
+      if (trace_enabled())
+        std::fprintf(stderr, "[pmmf]   arena overflow at level %d: compacted to %lld live, cap %lld\n", ovf,
+                     static_cast<long long>(B.used), static_cast<long long>(B.cap));
       size_items();
       set_scalar(S.cursor, static_cast<unsigned long long>(B.used));
       set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));

@@ -29,27 +29,43 @@ namespace {
 
 constexpr int kThreads = 256;
 
-// Two-level column norm (thread per column; columns listed by stage id).
+// Two-level column norm, warp per column (columns listed by stage id):
+// lanes load 32 consecutive entries (coalesced) and square them; every lane
+// then replays the reference's sequential order (inner sum per block row,
+// flushed into the outer sum at block changes) through shuffles.
 __global__ void k_norms(i64 P, const int32_t* __restrict__ cols, const i64* __restrict__ ptr,
                         const int32_t* __restrict__ row, const double* __restrict__ val,
                         const int32_t* __restrict__ blk, double* __restrict__ norm) {
-  const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  const i64 p = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (p >= P) return;
   const int32_t j = cols[p];
   double s = 0.0, inner = 0.0;
   int32_t cur = -1;
-  for (i64 e = ptr[j]; e < ptr[j + 1]; ++e) {
-    const int32_t b = blk[row[e]];
-    if (b != cur) {
-      if (cur >= 0) s = dadd(s, inner);
-      inner = 0.0;
-      cur = b;
+  const i64 e1 = ptr[j + 1];
+  for (i64 e0 = ptr[j]; e0 < e1; e0 += 32) {
+    const i64 e = e0 + lane;
+    double sq = 0.0;
+    int32_t b = -1;
+    if (e < e1) {
+      const double v = val[e];
+      sq = dmul(v, v);
+      b = blk[row[e]];
     }
-    const double v = val[e];
-    inner = dadd(inner, dmul(v, v));
+    const int n = e1 - e0 < 32 ? static_cast<int>(e1 - e0) : 32;
+    for (int i = 0; i < n; ++i) {
+      const int32_t bi = __shfl_sync(0xffffffffu, b, i);
+      const double si = __shfl_sync(0xffffffffu, sq, i);
+      if (bi != cur) {
+        if (cur >= 0) s = dadd(s, inner);
+        inner = 0.0;
+        cur = bi;
+      }
+      inner = dadd(inner, si);
+    }
   }
   if (cur >= 0) s = dadd(s, inner);
-  norm[p] = sqrt(s);
+  if (lane == 0) norm[p] = sqrt(s);
 }
 
 // Row -> anchor index: count, then scatter (order inside a row is free:
@@ -146,21 +162,45 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
     }
     int nt = 0;  // touched count (warp-uniform)
     const i64 e0 = A.ptr[j], e1 = A.ptr[j + 1];
-    for (i64 base_e = e0; base_e < e1; base_e += 32) {
-      const i64 e = base_e + lane;
-      double v = 0.0;
-      int32_t b = 0;
-      i64 beg = 0, cnt = 0;
+    // chunk loads are software-pipelined one chunk ahead
+    double nv = 0.0;
+    int32_t nb = 0;
+    i64 nbeg = 0, ncnt = 0;
+    {
+      const i64 e = e0 + lane;
       if (e < e1) {
         const int32_t r = A.row[e];
-        v = A.val[e];
-        b = A.blk[r];
-        beg = A.arptr[r];
-        cnt = A.arptr[r + 1] - beg;
+        nv = A.val[e];
+        nb = A.blk[r];
+        nbeg = A.arptr[r];
+        ncnt = A.arptr[r + 1] - nbeg;
       }
-      for (int k = 0; k < kPrefetch && k < cnt; ++k) {
-        pf_a[lane * kPrefetch + k] = A.ent_a[beg + k];
-        pf_v[lane * kPrefetch + k] = A.ent_v[beg + k];
+    }
+    for (i64 base_e = e0; base_e < e1; base_e += 32) {
+      const double v = nv;
+      const int32_t b = nb;
+      const i64 beg = nbeg, cnt = ncnt;
+      {
+        const i64 e = base_e + 32 + lane;
+        nv = 0.0;
+        nb = 0;
+        nbeg = 0;
+        ncnt = 0;
+        if (e < e1) {
+          const int32_t r = A.row[e];
+          nv = A.val[e];
+          nb = A.blk[r];
+          nbeg = A.arptr[r];
+          ncnt = A.arptr[r + 1] - nbeg;
+        }
+      }
+      if (cnt <= kPrefetch) {
+#pragma unroll
+        for (int k = 0; k < kPrefetch; ++k)
+          if (k < cnt) {
+            pf_a[lane * kPrefetch + k] = A.ent_a[beg + k];
+            pf_v[lane * kPrefetch + k] = A.ent_v[beg + k];
+          }
       }
       __syncwarp();
       unsigned hits = __ballot_sync(0xffffffffu, cnt > 0);
@@ -175,31 +215,40 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
           atomicAdd(&A.stats[0], 1ull);
           atomicAdd(&A.stats[1], static_cast<unsigned long long>(n));
         }
-        for (i64 q0 = 0; q0 < n; q0 += 32) {
-          const i64 q = q0 + lane;
-          bool fresh = false;
-          int32_t a = 0;
-          if (q < n) {
-            double av;
-            if (q < kPrefetch) {
-              a = pf_a[src * kPrefetch + q];
-              av = pf_v[src * kPrefetch + q];
-            } else {
-              a = A.ent_a[bg + q];
-              av = A.ent_v[bg + q];
+        // one update of anchor a with product prod (distinct a per lane)
+        // one update of anchor a (distinct a per lane within a row):
+        // block partial p restarts at 0.0 on a new block row, the finished
+        // partial is flushed into the total t (two-level order, P3); the
+        // three shared-memory slots are read together, no branches.
+        auto update = [&](bool on, int32_t a, double av) {
+          if (!on) return;
+          const double prod = dmul(vs, av);
+          const int32_t la = last[a];
+          const double pa = p[a], ta = t[a];
+          const bool same = la == bs;
+          t[a] = (same || la < 0) ? ta : dadd(ta, pa);
+          p[a] = dadd(same ? pa : 0.0, prod);
+          last[a] = bs;
+        };
+        if (n <= kPrefetch) {
+          const bool on = lane < n;
+          update(on, on ? pf_a[src * kPrefetch + lane] : 0, on ? pf_v[src * kPrefetch + lane] : 0.0);
+        } else {
+          // hub row: issue all of a 256-entry batch's loads before any update
+          constexpr int kB = 8;
+          for (i64 q0 = 0; q0 < n; q0 += 32 * kB) {
+            int32_t ra[kB];
+            double rv[kB];
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+              const i64 q = q0 + k * 32 + lane;
+              ra[k] = q < n ? A.ent_a[bg + q] : 0;
+              rv[k] = q < n ? A.ent_v[bg + q] : 0.0;
             }
-            const double prod = dmul(vs, av);
-            const int32_t la = last[a];
-            if (la != bs) {
-              if (la < 0) fresh = true; else t[a] = dadd(t[a], p[a]);
-              p[a] = 0.0;
-              last[a] = bs;
-            }
-            p[a] = dadd(p[a], prod);
+#pragma unroll
+            for (int k = 0; k < kB; ++k)
+              if (q0 + k * 32 < n) update(q0 + k * 32 + lane < n, ra[k], rv[k]);
           }
-          const unsigned fm = __ballot_sync(0xffffffffu, fresh);
-          if (fresh) touched[nt + __popc(fm & ((1u << lane) - 1u))] = a;
-          nt += __popc(fm);
         }
         __syncwarp();
       }
@@ -208,8 +257,8 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
     const double nj = A.cnorm[w];
     double best = 0.0;
     int ba = 0x7fffffff;
-    for (int i = lane; i < nt; i += 32) {
-      const int a = touched[i];
+    for (int a = lane; a < m; a += 32) {
+      if (last[a] < 0) continue;  // untouched: dot 0, score 0
       const double dot = dadd(t[a], p[a]);
       const double na = A.anorm[a];
       double sc = 0.0;
@@ -470,7 +519,7 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
   DBuf<int32_t> dids(P, s);
   dids.upload(ids);
   DBuf<double> dnorm(P, s);
-  PMMF_LAUNCH(k_norms, blocks_for(P, kThreads), kThreads, 0, s, P, dids.get(), a.ptr.get(), a.row.get(), a.val.get(),
+  PMMF_LAUNCH(k_norms, blocks_for(P * 32, kThreads), kThreads, 0, s, P, dids.get(), a.ptr.get(), a.row.get(), a.val.get(),
               nb.d_blk.get(), dnorm.get());
   std::vector<double> hn = dnorm.to_host(P);
   std::vector<double> norm(static_cast<size_t>(n), 0.0);

@@ -92,11 +92,8 @@ struct ProfScope {
 
 // PMMF_B200_TRACE=1 prints per-stage diagnostics to stderr.
 inline bool trace_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PMMF_B200_TRACE");
-    return e && *e && *e != '0';
-  }();
-  return on;
+  const char* e = std::getenv("PMMF_B200_TRACE");  // read per call: cheap, and togglable
+  return e && *e && *e != '0';
 }
 
 // Stream-ordered device buffer (cudaMallocAsync from the device pool).

@@ -91,6 +91,7 @@ struct SearchBatch {
   DBuf<int64_t> budget;    // elimination cap (factorizer.hpp:463-479)
   DBuf<uint64_t> seed;     // derive(seed,{0xF0,p,u})
   DBuf<int64_t> out_base;  // first rotation / elimination slot
+  DBuf<int32_t> order;     // CTA launch order: batch-relative clusters by decreasing size
 };
 struct SearchOut {
   DBuf<int32_t> nrot, nelim;   // per cluster
@@ -135,9 +136,12 @@ struct Piece {
 // most batch_nnz input entries.  The final columns are returned as pieces;
 // when keep_row != nullptr, a column c keeps only rows r with keep_row[r]
 // unless keep_all_col[c].
+// `growth` is the expected arena/input ratio of a batch (final columns plus
+// superseded versions); the arena starts at that size so that compactions
+// (copy + re-map) stay rare.
 void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
                  const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
-                 const uint8_t* keep_all_col, i64 batch_nnz, cudaStream_t s);
+                 const uint8_t* keep_all_col, i64 batch_nnz, double growth, cudaStream_t s);
 // Transpose of a matrix given as pieces covering [0, N), keeping only rows
 // r with keep_row[r] (all when nullptr); sorted in chunks of <= chunk_nnz
 // entries so the sort buffers stay bounded.

@@ -110,13 +110,7 @@ __global__ void k_core(i64 g, const int32_t* __restrict__ col_sid, const i64* __
 
 using clk = std::chrono::steady_clock;
 
-bool trace_on() {
-  static const bool on = [] {
-    const char* e = std::getenv("PMMF_B200_TRACE");
-    return e && *e && *e != '0';
-  }();
-  return on;
-}
+bool trace_on() { return trace_enabled(); }
 size_t mem_used_mb() {
   size_t f = 0, t = 0;
   cudaMemGetInfo(&f, &t);
@@ -368,6 +362,15 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         sb.budget.upload(hb);
         sb.seed.upload(hs);
         sb.out_base.upload(hob);
+        {
+          // largest clusters first: the search is quadratic in c and the
+          // kernel ends with its slowest CTA
+          std::vector<int32_t> ord(static_cast<size_t>(nb));
+          std::iota(ord.begin(), ord.end(), 0);
+          std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) { return hc[x] > hc[y]; });
+          sb.order.alloc(nb, s);
+          sb.order.upload(ord);
+        }
         search_clusters(sb, u0, nb, p.k, p.eta, G.get(), D.get(), std::max<i64>(max_c, 1), so, s);
         PMMF_CUDA(cudaStreamSynchronize(s));
         search_ms += ms_since(ts);
@@ -416,12 +419,24 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         const i64 avail = available_bytes();
         i64 chunk = std::max<i64>(i64{1} << 22, avail / 10 / 32);
         if (const char* e = std::getenv("PMMF_B200_CHUNK_NNZ")) chunk = std::atoll(e);  // test hook
+        // trace-mode sub-phase timer (synchronises only when tracing)
+        auto tl = clk::now();
+        auto lap = [&](const char* what) {
+          if (!trace_on()) return;
+          PMMF_CUDA(cudaStreamSynchronize(s));
+          PMMF_TRACE("[pmmf]   apply.%s %.2f ms\n", what, ms_since(tl));
+          tl = clk::now();
+        };
+        lap("plan");
         std::vector<Piece> pieces;
-        rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, s);
+        const i64 nnz_in = std::max<i64>(A.nnz, 1);
+        rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, 24.0, s);
+        lap("column_pass");
         A = Csc();
         Csc T;
         transpose_pieces(T, pieces, N, nullptr, chunk, s);
         pieces.clear();
+        lap("transpose_1");
         const i64 tn = T.nnz;
         // Retired ids: their rotated rows/columns feed only the residual.
         DBuf<uint8_t> keep_row(N, s), retired(N, s);
@@ -434,12 +449,16 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           keep_row.upload(kr);
           retired.upload(rt);
         }
-        i64 batch = std::max<i64>(i64{1} << 24, avail / 4 / 144);
+        // The row pass grows its columns about as much as the column pass did
+        // (measured ratio); size its arena and batches from that.
+        const double growth = 1.4 * std::max(2.0, static_cast<double>(tn) / static_cast<double>(nnz_in));
+        i64 batch = std::max<i64>(i64{1} << 24, static_cast<i64>(0.35 * static_cast<double>(avail) / (12.0 * growth)));
         if (const char* e = std::getenv("PMMF_B200_BATCH_NNZ")) batch = std::atoll(e);  // test hook
         PMMF_TRACE("[pmmf] stage %d: column pass -> %lld entries, batch=%lld mem=%zuMB\n", stage_no,
                    static_cast<long long>(tn), static_cast<long long>(batch), mem_used_mb());
-        rotate_pass(pieces, T, cur.off, slot_base, plan, nullptr, nullptr, batch, s);
+        rotate_pass(pieces, T, cur.off, slot_base, plan, nullptr, nullptr, batch, growth, s);
         T = Csc();
+        lap("row_pass");
         i64 stored = 0;
         for (const Piece& P : pieces) stored += P.nnz;
         PMMF_TRACE("[pmmf] stage %d: row pass stored %lld entries in %zu pieces, mem=%zuMB\n", stage_no,
@@ -455,8 +474,10 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
           residual_done = true;
         }
+        lap("masses");
         // The next stage reads only the surviving columns of A' (all rows).
         transpose_pieces(A, pieces, N, keep_row.get(), chunk, s);
+        lap("transpose_2");
         PMMF_TRACE("[pmmf] stage %d: A' %lld entries, mem=%zuMB\n", stage_no, static_cast<long long>(A.nnz),
                    mem_used_mb());
       }

@@ -102,6 +102,7 @@ struct KArgs {
   int32_t* elim_loc;
   int32_t* error;
   unsigned long long* timing;  // optional: 8 clock64 phase totals per cluster
+  const int32_t* order;        // CTA -> cluster, largest clusters first (LPT)
 };
 
 template <int K>
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
   __shared__ double sh_q[K][K];
   __shared__ int sh_victim;
   __shared__ int sh_oldts[K];
-  const int u = blockIdx.x;
+  const int u = A.order[blockIdx.x];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const i64 c64 = A.c[u];
   if (c64 < K) {
@@ -430,7 +431,8 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
   KArgs a{b.c.get(),           b.tile.get(),        b.budget.get(),       b.seed.get(),        b.out_base.get(),
           eta,                 G,                   D,                    diag_scratch.get(),  level_scratch.get(),
           max_c,               diag_in_smem,        out.nrot.get() + u0,  out.nelim.get() + u0, out.rot_loc.get(),
-          out.rot_q.get(),     out.rot_level.get(), out.elim_loc.get(),   out.error.get(), nullptr};
+          out.rot_q.get(),     out.rot_level.get(), out.elim_loc.get(),   out.error.get(), nullptr,
+          b.order.get()};
   DBuf<unsigned long long> timing;
   const bool tm = std::getenv("PMMF_B200_SEARCH_TIMING") != nullptr;
   if (tm) {
