@@ -519,12 +519,14 @@ struct Batch {
   DBuf<double> val;
   i64 cap = 0, used = 0;
 
-  void compact(i64 need, cudaStream_t s) {
+  // Copies the live column versions into a fresh arena of at least
+  // `min_cap` entries and 1.5x the live size (peak: old + new arena).
+  void compact(i64 min_cap, cudaStream_t s) {
     DBuf<i64> l64(N + 1, s), pos(N + 1, s);
     PMMF_LAUNCH(k_len64, blocks_for(N + 1, kThreads), kThreads, 0, s, N, len.get(), l64.get());
     exscan(l64.get(), pos.get(), N + 1, s);
     const i64 live = read_i64(pos.get() + N, s);
-    const i64 ncap = std::max<i64>(live + need, (live + need) + (live + need) / 2) + 1024;
+    const i64 ncap = std::max<i64>(min_cap, live + live / 2) + 1024;
     DBuf<int32_t> r1(ncap, s);
     DBuf<double> v1(ncap, s);
     PMMF_LAUNCH(k_compact, blocks_for(N * 32, kThreads), kThreads, 0, s, N, off.get(), len.get(), pos.get(), row.get(),
@@ -735,7 +737,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     };
     set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));
     set_scalar(S.cursor, static_cast<unsigned long long>(ne));
-    int Lstart = 1;
+    int Lstart = 1, repeat = 0, last_ovf = -1;
     for (;;) {
       for (int L = Lstart; L <= plan.max_level; ++L) {
         const auto [lo, hi] = range[L];
@@ -758,7 +760,11 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       if (ovf == INT_MAX) break;
       // Level `ovf` did not fit: nothing of it was committed.  Compact the
       // live columns into a larger arena and resume there.
-      B.compact(std::max<i64>(B.cap, i64{1} << 22), s);
+      // Same-size arena when most of it was superseded versions; doubled
+      // while the same level keeps failing.
+      repeat = ovf == last_ovf ? repeat + 1 : 0;
+      last_ovf = ovf;
+      B.compact(std::max<i64>(B.cap << std::min(repeat, 8), i64{1} << 22), s);
       if (trace_enabled())
         std::fprintf(stderr, "[pmmf]   arena overflow at level %d: compacted to %lld live, cap %lld\n", ovf,
                      static_cast<long long>(B.used), static_cast<long long>(B.cap));

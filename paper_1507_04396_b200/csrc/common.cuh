@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -96,6 +97,26 @@ inline bool trace_enabled() {
   return e && *e && *e != '0';
 }
 
+// Stream-ordered allocation from the device pool.  The pool keeps freed
+// blocks mapped (mapping is the expensive part), so a large request can fail
+// on fragmentation alone: then the stream is drained, the pool trimmed back to
+// what is in use, and the request retried once.
+inline void pool_alloc(void** p, size_t bytes, cudaStream_t st) {
+  cudaError_t e = cudaMallocAsync(p, bytes, st);
+  if (e == cudaErrorMemoryAllocation) {
+    (void)cudaGetLastError();
+    PMMF_CUDA(cudaStreamSynchronize(st));
+    int dev = 0;
+    PMMF_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    PMMF_CUDA(cudaMemPoolTrimTo(pool, 0));
+    if (trace_enabled()) std::fprintf(stderr, "[pmmf]   pool trimmed for a %zu MB request\n", bytes >> 20);
+    e = cudaMallocAsync(p, bytes, st);
+  }
+  PMMF_CUDA(e);
+}
+
 // Stream-ordered device buffer (cudaMallocAsync from the device pool).
 template <typename T>
 struct DBuf {
@@ -123,7 +144,7 @@ struct DBuf {
     release();
     s = st;
     n = count;
-    if (count > 0) PMMF_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count), st));
+    if (count > 0) pool_alloc(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count), st);
   }
   void release() noexcept {
     if (p) cudaFreeAsync(p, s);

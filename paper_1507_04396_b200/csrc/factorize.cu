@@ -164,10 +164,14 @@ struct StreamGuard {
 std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b200_params& p) {
   PMMF_CUDA(cudaSetDevice(in->device));
   {
-    // Keep freed blocks in the pool between stages.
+    // The stream-ordered pool keeps freed blocks mapped across
+    // synchronisations (re-mapping tens of GB per stage costs seconds);
+    // pool_alloc trims it when fragmentation alone fails a request.
     cudaMemPool_t pool;
     PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, in->device));
     uint64_t thr = ~uint64_t{0};
+    if (const char* e = std::getenv("PMMF_B200_POOL_KEEP_GB"))
+      thr = static_cast<uint64_t>(std::atof(e) * 1073741824.0);
     PMMF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
   StreamGuard sg;
@@ -452,7 +456,11 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         // The row pass grows its columns about as much as the column pass did
         // (measured ratio); size its arena and batches from that.
         const double growth = 1.4 * std::max(2.0, static_cast<double>(tn) / static_cast<double>(nnz_in));
-        i64 batch = std::max<i64>(i64{1} << 24, static_cast<i64>(0.35 * static_cast<double>(avail) / (12.0 * growth)));
+        // (free memory re-read: T and the retired masks now hold their share)
+        const i64 avail_row = available_bytes();
+        double frac = 0.2;  // share of free memory for one batch's arena
+        if (const char* e = std::getenv("PMMF_B200_ARENA_FRAC")) frac = std::atof(e);
+        i64 batch = std::max<i64>(i64{1} << 24, static_cast<i64>(frac * static_cast<double>(avail_row) / (12.0 * growth)));
         if (const char* e = std::getenv("PMMF_B200_BATCH_NNZ")) batch = std::atoll(e);  // test hook
         PMMF_TRACE("[pmmf] stage %d: column pass -> %lld entries, batch=%lld mem=%zuMB\n", stage_no,
                    static_cast<long long>(tn), static_cast<long long>(batch), mem_used_mb());

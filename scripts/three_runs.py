@@ -7,5 +7,5 @@ inp = api.workload_rmat(20, 32, 42)
 p = FactorizeParams(seed=42, cluster=ClusterParams(m_target=512, c_max=10000))
 m = BlockedSparseMatrix.from_triplets(*inp)
 for i in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
-    if i >= 1: os.environ["PMMF_B200_TRACE"] = "1"
+    if i >= 0: os.environ["PMMF_B200_TRACE"] = "1"
     t = time.time(); f = api.factorize(m, p); print("run", i, round(time.time() - t, 3), f.phases.round(0), flush=True)
