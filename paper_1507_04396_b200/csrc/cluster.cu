@@ -113,6 +113,12 @@ struct ScoreArgs {
   double* rows;           // rows mode: P x m scores (nullptr in assignment mode)
   double* g_scratch;      // per-warp state when shared memory is too small
   unsigned long long* stats;  // trace: {hit rows, anchor entries} (nullable)
+  long long* col_cycles;      // trace: cycles per pool column (nullable)
+  long long* warp_cycles;     // trace: busy cycles per warp (nullable)
+  const int32_t* anchors;     // anchor stage ids (dense path)
+  const int32_t* list;        // pool positions handled by k_score, heaviest first
+  i64 nlist;
+  unsigned long long* next;   // work counter over list
 };
 
 __device__ __forceinline__ bool better(double s, int a, double bs, int ba) {
@@ -154,10 +160,19 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
     last[a] = -1;
   }
   __syncwarp();
-  for (i64 w = gwarp; w < A.P; w += nwarps) {
+  long long busy = 0;
+  (void)nwarps;
+  for (;;) {  // columns fetched dynamically, heaviest first
+    i64 idx = 0;
+    if (lane == 0) idx = static_cast<i64>(atomicAdd(A.next, 1ull));
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= A.nlist) break;
+    const i64 w = A.list[idx];
+    const long long c_start = A.col_cycles ? clock64() : 0;
     const int32_t j = A.cols[w];
     if (A.rows == nullptr && A.self[j] >= 0) {
       if (lane == 0) A.assign[w] = A.self[j];
+      if (A.col_cycles && lane == 0) A.col_cycles[w] = 0;
       continue;
     }
     int nt = 0;  // touched count (warp-uniform)
@@ -282,7 +297,146 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
     }
     if (lane == 0 && A.rows == nullptr) A.assign[w] = best > 0.0 ? ba : -1;
     __syncwarp();
+    if (A.col_cycles && lane == 0) {
+      const long long c = clock64() - c_start;
+      A.col_cycles[w] = c;
+      busy += c;
+    }
   }
+  if (A.warp_cycles && lane == 0) A.warp_cycles[gwarp] = busy;
+}
+
+// Serial work of a pool column in k_score (self-assigned anchors cost
+// nothing).  Sort key for the work list.
+__global__ void k_col_cost(i64 P, const int32_t* __restrict__ cols, const int32_t* __restrict__ self, bool rows_mode,
+                           const i64* __restrict__ ptr, const int32_t* __restrict__ row, const int32_t* __restrict__ cnt,
+                           int32_t* __restrict__ key, int32_t* __restrict__ idx) {
+  const i64 p = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= P) return;
+  const int32_t j = cols[p];
+  i64 c = 0;  // warp steps: one per hit row plus one per 16 anchor entries
+  if (rows_mode || self[j] < 0)
+    for (i64 e = ptr[j] + lane; e < ptr[j + 1]; e += 32) {
+      const int32_t n = cnt[row[e]];
+      c += n > 0 ? 1 + n / 16 : 0;
+    }
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) {
+    key[p] = static_cast<int32_t>(c < 0x7fffffff ? c : 0x7fffffff);
+    idx[p] = static_cast<int32_t>(p);
+  }
+}
+__global__ void k_count_above(i64 n, const int32_t* __restrict__ key, int32_t thr, int32_t* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  // keys sorted descending: the boundary is where key crosses thr
+  if (i < n && key[i] > thr && (i + 1 == n || key[i + 1] <= thr)) *out = static_cast<int32_t>(i + 1);
+}
+
+// Dense path for the heaviest pool columns (hub columns hit by most rows).
+// A batch of D such columns is scattered into X (row-major N x D, zero
+// elsewhere); then a warp owns (anchor a, 32 consecutive batch columns) and
+// walks a's entries once in row order: the row, value and block are
+// warp-uniform, X[r, d..d+31] is one coalesced load, and each lane keeps the
+// two-level (block partial, total) sum of its column.  Rows outside a
+// column give zero products; adding a zero never changes a non-zero partial
+// and only the sign of a zero dot can differ, which |dot| removes, so the
+// scores equal the sparse path's bit for bit.
+__global__ void k_dense_scatter(const int32_t* __restrict__ dcols, const int32_t* __restrict__ cols,
+                                const i64* __restrict__ ptr, const int32_t* __restrict__ row,
+                                const double* __restrict__ val, int D, bool clear, double* __restrict__ X) {
+  const int d = blockIdx.x;
+  const int32_t j = cols[dcols[d]];
+  for (i64 e = ptr[j] + threadIdx.x; e < ptr[j + 1]; e += blockDim.x)
+    X[static_cast<i64>(row[e]) * D + d] = clear ? 0.0 : val[e];
+}
+
+__global__ void __launch_bounds__(256) k_score_spmm(ScoreArgs A, const int32_t* __restrict__ aorder, int G,
+                                                    const int32_t* __restrict__ dcols, int Dcur, int D,
+                                                    const double* __restrict__ X, double* __restrict__ S) {
+  const i64 gw = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= static_cast<i64>(A.m) * G) return;
+  const int a = aorder[gw / G];
+  const int d = static_cast<int>(gw % G) * 32 + lane;
+  const int32_t aj = A.anchors[a];
+  const i64 f0 = A.ptr[aj], f1 = A.ptr[aj + 1];
+  const double* xc = X + (d < D ? d : D - 1);
+  double tot = 0.0, inner = 0.0;
+  int32_t cur = -1;
+  // 32 entries per round: all 32 X loads are issued before the sum chain
+  for (i64 fb = f0; fb < f1; fb += 32) {
+    const i64 f = fb + lane;
+    int32_t r = 0, b = -1;
+    double v = 0.0;
+    if (f < f1) {
+      r = A.row[f];
+      v = A.val[f];
+      b = A.blk[r];
+    }
+    const int n = f1 - fb < 32 ? static_cast<int>(f1 - fb) : 32;
+    double xv[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) xv[k] = xc[static_cast<i64>(__shfl_sync(0xffffffffu, r, k)) * D];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const double vk = __shfl_sync(0xffffffffu, v, k);
+      const int32_t bk = __shfl_sync(0xffffffffu, b, k);
+      if (k < n) {
+        const double prod = dmul(xv[k], vk);
+        if (bk != cur) {
+          if (cur >= 0) tot = dadd(tot, inner);
+          inner = 0.0;
+          cur = bk;
+        }
+        inner = dadd(inner, prod);
+      }
+    }
+  }
+  if (d >= Dcur) return;
+  const double dot = cur >= 0 ? dadd(tot, inner) : 0.0;
+  const i64 w = dcols[d];
+  const double nj = A.cnorm[w], na = A.anorm[a];
+  const double sc = (nj > 0.0 && na > 0.0) ? fabs(dot) / dmul(nj, na) : 0.0;
+  if (A.rows)
+    A.rows[static_cast<size_t>(w) * A.m + a] = sc;
+  else
+    S[static_cast<i64>(d) * A.m + a] = sc;
+}
+
+// Strict argmax over the anchors of a dense batch column (ties: lowest anchor).
+__global__ void k_dense_argmax(ScoreArgs A, const int32_t* __restrict__ dcols, int Dcur,
+                               const double* __restrict__ S) {
+  const i64 d = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (d >= Dcur) return;
+  double best = 0.0;
+  int ba = 0x7fffffff;
+  for (int a = lane; a < A.m; a += 32) {
+    const double sc = S[d * A.m + a];
+    if (sc > 0.0 && better(sc, a, best, ba)) {
+      best = sc;
+      ba = a;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double os = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, ba, o);
+    if (better(os, oa, best, ba)) {
+      best = os;
+      ba = oa;
+    }
+  }
+  if (lane == 0) A.assign[dcols[d]] = best > 0.0 ? ba : -1;
+}
+
+__global__ void k_anchor_nnz(int m, const int32_t* __restrict__ anchors, const i64* __restrict__ ptr,
+                             int32_t* __restrict__ nnz, int32_t* __restrict__ idx) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  const i64 c = ptr[anchors[a] + 1] - ptr[anchors[a]];
+  nnz[a] = static_cast<int32_t>(c < 0x7fffffff ? c : 0x7fffffff);
+  idx[a] = a;
 }
 
 struct Scorer {
@@ -355,23 +509,132 @@ struct Scorer {
     }
     ScoreArgs args{P,           dpool.get(), dpn.get(),        m,           dan.get(),   self.get(),
                    a.ptr.get(), a.row.get(), a.val.get(),      nb.d_blk.get(), rptr.get(), ent_a.get(),
-                   ent_v.get(), dassign.get(), rows_mode ? drows.get() : nullptr, scratch.get(), nullptr};
+                   ent_v.get(), dassign.get(), rows_mode ? drows.get() : nullptr, scratch.get(), nullptr,
+                   nullptr, nullptr, danch.get(), nullptr, 0, nullptr};
+    // Work list: pool positions by decreasing serial cost (rows hit); the
+    // heaviest, above a share of the anchors' total size, take the dense path.
+    DBuf<int32_t> key(P, s), key2(P, s), idx(P, s), list(P, s), nd_d(1, s);
+    PMMF_LAUNCH(k_col_cost, blocks_for(P * 32, kThreads), kThreads, 0, s, P, dpool.get(), self.get(), rows_mode,
+                a.ptr.get(), a.row.get(), cnt.get(), key.get(), idx.get());
+    {
+      size_t tmp = 0;
+      PMMF_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, key.get(), key2.get(), idx.get(), list.get(),
+                                                          static_cast<int64_t>(P), 0, 32, s));
+      DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+      PMMF_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.get(), tmp, key.get(), key2.get(), idx.get(), list.get(),
+                                                          static_cast<int64_t>(P), 0, 32, s));
+    }
+    double thr_d = std::max<double>(64.0, static_cast<double>(total) / 150.0);
+    if (const char* e = std::getenv("PMMF_B200_DENSE_DIV")) {  // test hook: no floor, <= 0 disables
+      const double div = std::atof(e);
+      thr_d = div > 0.0 ? static_cast<double>(total) / div : 1e18;
+    }
+    const int32_t thr = static_cast<int32_t>(std::min<double>(0x7ffffffe, thr_d));
+    nd_d.zero();
+    PMMF_LAUNCH(k_count_above, blocks_for(P, kThreads), kThreads, 0, s, P, key2.get(), thr, nd_d.get());
+    const i64 nd = nd_d.to_host(1)[0];
+    DBuf<unsigned long long> next(1, s);
+    next.zero();
+    args.list = list.get() + nd;
+    args.nlist = P - nd;
+    args.next = next.get();
+    const size_t smem = use_smem ? stride * static_cast<size_t>(wpb) : 0;
+    if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    // persistent-style grid: warps loop over the pool
+    const i64 blocks = std::min<i64>((P + wpb - 1) / wpb, use_smem ? 148 * 16 : (P + wpb - 1) / wpb);
     DBuf<unsigned long long> stats;
+    DBuf<long long> ccyc, wcyc;
+    const bool timing = trace_enabled() && std::getenv("PMMF_B200_SCORE_TIMING");
     if (trace_enabled()) {
       stats.alloc(2, s);
       stats.zero();
       args.stats = stats.get();
     }
-    const size_t smem = use_smem ? stride * static_cast<size_t>(wpb) : 0;
-    if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    // persistent-style grid: warps loop over the pool
-    const i64 blocks = std::min<i64>((P + wpb - 1) / wpb, use_smem ? 148 * 16 : (P + wpb - 1) / wpb);
-    PMMF_LAUNCH(k_score, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb, use_smem);
+    if (timing) {
+      ccyc.alloc(P, s);
+      ccyc.zero();
+      wcyc.alloc(blocks * wpb, s);
+      wcyc.zero();
+      args.col_cycles = ccyc.get();
+      args.warp_cycles = wcyc.get();
+    }
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    if (timing)
+      for (auto& e : ev) cudaEventCreate(&e);
+    if (timing) cudaEventRecord(ev[0], s);
+    int dense_D = 0, max_annz = 0;
+    if (nd > 0) {
+      // anchors by decreasing size (longest walks start first)
+      DBuf<int32_t> ann(m, s), ann2(m, s), aidx(m, s), aorder(m, s);
+      PMMF_LAUNCH(k_anchor_nnz, blocks_for(m, kThreads), kThreads, 0, s, m, danch.get(), a.ptr.get(), ann.get(),
+                  aidx.get());
+      {
+        size_t tmp = 0;
+        PMMF_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, ann.get(), ann2.get(), aidx.get(),
+                                                            aorder.get(), m, 0, 32, s));
+        DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+        PMMF_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.get(), tmp, ann.get(), ann2.get(), aidx.get(),
+                                                            aorder.get(), m, 0, 32, s));
+      }
+      // batch width: X (N x D fp64) within a fifth of free memory, a multiple
+      // of 32 (each batch re-walks every anchor: fewer, wider batches)
+      const i64 budget = std::max<i64>(i64{1} << 30, available_bytes() / 5);
+      const i64 dmax = std::max<i64>(32, budget / (8 * std::max<i64>(a.N, 1)) / 32 * 32);
+      const int D = static_cast<int>(std::min<i64>(dmax, (nd + 31) / 32 * 32));
+      const int G = D / 32;
+      dense_D = D;
+      if (timing) max_annz = ann2.to_host(1)[0];
+      DBuf<double> X(static_cast<i64>(D) * a.N, s), S;
+      X.zero();
+      if (!rows_mode) S.alloc(static_cast<i64>(D) * m, s);
+      for (i64 d0 = 0; d0 < nd; d0 += D) {
+        const int Dcur = static_cast<int>(std::min<i64>(D, nd - d0));
+        const int32_t* dcols = list.get() + d0;
+        PMMF_LAUNCH(k_dense_scatter, static_cast<unsigned>(Dcur), 256, 0, s, dcols, dpool.get(), a.ptr.get(),
+                    a.row.get(), a.val.get(), D, false, X.get());
+        PMMF_LAUNCH(k_score_spmm, blocks_for(static_cast<i64>(m) * G * 32, 256), 256, 0, s, args, aorder.get(), G,
+                    dcols, Dcur, D, X.get(), S.get());
+        if (!rows_mode)
+          PMMF_LAUNCH(k_dense_argmax, blocks_for(static_cast<i64>(Dcur) * 32, kThreads), kThreads, 0, s, args, dcols,
+                      Dcur, S.get());
+        PMMF_LAUNCH(k_dense_scatter, static_cast<unsigned>(Dcur), 256, 0, s, dcols, dpool.get(), a.ptr.get(),
+                    a.row.get(), a.val.get(), D, true, X.get());
+      }
+    }
+    if (timing) cudaEventRecord(ev[1], s);
+    if (args.nlist > 0)
+      PMMF_LAUNCH(k_score, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb, use_smem);
+    if (timing) cudaEventRecord(ev[2], s);
     if (trace_enabled()) {
       std::vector<unsigned long long> h = stats.to_host(2);
       const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
-      std::fprintf(stderr, "[pmmf]   score: pool=%lld anchors=%d hit_rows=%llu anchor_entries=%llu %.2f ms\n",
-                   static_cast<long long>(P), m, h[0], h[1], ms);
+      std::fprintf(stderr, "[pmmf]   score: pool=%lld anchors=%d dense=%lld hit_rows=%llu anchor_entries=%llu %.2f ms\n",
+                   static_cast<long long>(P), m, static_cast<long long>(nd), h[0], h[1], ms);
+      if (timing) {
+        std::vector<long long> cc = ccyc.to_host(P), wc = wcyc.to_host(blocks * wpb);
+        std::vector<long long> dc;
+        for (long long& c : cc)
+          if (c < 0) {
+            dc.push_back(-c);
+            c = 0;
+          }
+        const double csum = std::accumulate(cc.begin(), cc.end(), 0.0);
+        const double dsum = std::accumulate(dc.begin(), dc.end(), 0.0);
+        std::sort(cc.begin(), cc.end(), std::greater<long long>());
+        std::sort(dc.begin(), dc.end(), std::greater<long long>());
+        const long long wmax = *std::max_element(wc.begin(), wc.end());
+        float t1 = 0.f, t2 = 0.f;
+        cudaEventElapsedTime(&t1, ev[0], ev[1]);
+        cudaEventElapsedTime(&t2, ev[1], ev[2]);
+        std::fprintf(stderr,
+                     "[pmmf]     score: dense %.2f ms (thr %d, E_anchor %lld, max %d, D %d) sparse %.2f ms"
+                     " (sum %.3g cyc, top %lld %lld %lld, warps %lld max %lld mean %.3g)\n",
+                     t1, thr, static_cast<long long>(total), max_annz, dense_D, t2, csum, cc[0],
+                     cc[std::min<i64>(1, P - 1)], cc[std::min<i64>(10, P - 1)], static_cast<long long>(blocks * wpb),
+                     wmax, csum / static_cast<double>(blocks * wpb));
+      }
+      for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
     }
     if (!rows_mode) {
       set_self(danch, danch, m, false);

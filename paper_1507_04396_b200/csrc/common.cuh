@@ -97,6 +97,21 @@ inline bool trace_enabled() {
   return e && *e && *e != '0';
 }
 
+// Device memory a new allocation can still get: free memory plus the pool's
+// reserved-but-unused blocks.
+inline i64 available_bytes() {
+  size_t f = 0, t = 0;
+  PMMF_CUDA(cudaMemGetInfo(&f, &t));
+  int dev = 0;
+  PMMF_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t reserved = 0, used = 0;
+  PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  return static_cast<i64>(f) + static_cast<i64>(reserved - used);
+}
+
 // Stream-ordered allocation from the device pool.  The pool keeps freed
 // blocks mapped (mapping is the expensive part), so a large request can fail
 // on fragmentation alone: then the stream is drained, the pool trimmed back to

@@ -135,19 +135,6 @@ void validate(const pmmf_b200_params& p) {  // factorizer.hpp:44-50, clustering.
   if (p.d_max < 0) fail(PMMF_INVALID_ARGUMENT, "ClusterParams: d_max < 0");
 }
 
-i64 available_bytes() {
-  size_t f = 0, t = 0;
-  PMMF_CUDA(cudaMemGetInfo(&f, &t));
-  int dev = 0;
-  PMMF_CUDA(cudaGetDevice(&dev));
-  cudaMemPool_t pool;
-  PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-  uint64_t reserved = 0, used = 0;
-  PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
-  PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
-  return static_cast<i64>(f) + static_cast<i64>(reserved - used);
-}
-
 struct StreamGuard {
   cudaStream_t s = nullptr;
   StreamGuard() { PMMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
@@ -317,9 +304,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     d_out_base.upload(out_base);
     d_coff.upload(cur.off.data(), rc + 1);
     {
-      size_t free_b = 0, total_b = 0;
-      PMMF_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      const i64 budget_elems = std::max<i64>(i64{1} << 20, static_cast<i64>(free_b * 0.55) / 16);
+      const i64 budget_elems =
+          std::max<i64>(i64{1} << 20, static_cast<i64>(static_cast<double>(available_bytes()) * 0.55) / 16);
       i64 u0 = 0;
       double gram_ms = 0.0, search_ms = 0.0;
       while (u0 < rc) {

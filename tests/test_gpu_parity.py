@@ -29,3 +29,14 @@ def test_small_batches_and_chunks(name, monkeypatch):
     monkeypatch.setenv("PMMF_B200_CHUNK_NNZ", "3000")
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf512_k4", "zero_cols_bypass",
+                                  "partitioned_input", "k3_sparse"])
+@pytest.mark.parametrize("div", ["1e9", "3"])
+def test_dense_scoring_path(name, div, monkeypatch):
+    """Route every (div=1e9) or only the heaviest (div=3) pool columns through
+    the dense-gather scorer (hub columns on config 4) — still bit-exact."""
+    monkeypatch.setenv("PMMF_B200_DENSE_DIV", div)
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
