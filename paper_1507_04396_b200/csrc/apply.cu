@@ -21,6 +21,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <climits>
 
 #include "engine.cuh"
@@ -423,7 +425,7 @@ __global__ void k_final_count(i64 N, i64 col0, const i64* __restrict__ off, cons
     if (lane == 0) cnt[N] = 0;
     return;
   }
-  const bool all = keep_row == nullptr || keep_all_col[col0 + w];
+  const bool all = keep_row == nullptr || (keep_all_col != nullptr && keep_all_col[col0 + w]);
   if (all) {
     if (lane == 0) cnt[w] = len[w];
     return;
@@ -440,7 +442,7 @@ __global__ void k_final_copy(i64 N, i64 col0, const i64* __restrict__ off, const
   const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= N) return;
-  const bool all = keep_row == nullptr || keep_all_col[col0 + w];
+  const bool all = keep_row == nullptr || (keep_all_col != nullptr && keep_all_col[col0 + w]);
   i64 o = pos[w];
   const i64 s = off[w];
   for (int base = 0; base < len[w]; base += 32) {
@@ -537,6 +539,81 @@ struct Batch {
     used = live;
   }
 };
+
+// ---- residual masses from a batch's final columns (see MassSpec)
+// Per column c: the entries of retired rows g that it contributes to the
+// mass of g (c taken when it survives or retires after g); the diagonal
+// entry (g == c) goes to diag.
+__global__ void k_mass_count(i64 N, i64 col0, const i64* __restrict__ off, const int32_t* __restrict__ len,
+                             const int32_t* __restrict__ arow, const double* __restrict__ aval, MassSpec M,
+                             i64* __restrict__ cnt) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w > N) return;
+  if (w == N) {
+    if (lane == 0) cnt[N] = 0;
+    return;
+  }
+  const int32_t c = static_cast<int32_t>(col0 + w);
+  const int32_t key = M.col_key[c];
+  const i64 s0 = off[w];
+  int n = 0;
+  for (int i = lane; i < len[w]; i += 32) {
+    const int32_t g = arow[s0 + i];
+    const int32_t rg = M.row_rank[g];
+    if (rg < 0) continue;
+    if (g == c)
+      M.diag[rg] = aval[s0 + i];
+    else
+      n += key > rg;
+  }
+  for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if (lane == 0) cnt[w] = n;
+}
+// Columns [w0, w1) of the batch: (g, v^2) of the taken entries, column-major.
+__global__ void k_mass_gather(i64 w0, i64 w1, i64 col0, const i64* __restrict__ off,
+                              const int32_t* __restrict__ len, const int32_t* __restrict__ arow,
+                              const double* __restrict__ aval, MassSpec M, const i64* __restrict__ pos,
+                              int32_t* __restrict__ okey, double* __restrict__ osq) {
+  const i64 w = w0 + ((blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= w1) return;
+  const int32_t c = static_cast<int32_t>(col0 + w);
+  const int32_t key = M.col_key[c];
+  const i64 s0 = off[w];
+  i64 o = pos[w] - pos[w0];
+  for (int b = 0; b < len[w]; b += 32) {
+    const int i = b + lane;
+    int32_t g = 0;
+    bool take = false;
+    if (i < len[w]) {
+      g = arow[s0 + i];
+      const int32_t rg = M.row_rank[g];
+      take = rg >= 0 && g != c && key > rg;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (take) {
+      const i64 d = o + __popc(m & ((1u << lane) - 1u));
+      const double v = aval[s0 + i];
+      okey[d] = g;
+      osq[d] = dmul(v, v);
+    }
+    o += __popc(m);
+  }
+}
+// One thread per row run of the (g-sorted, column order kept) chunk: the
+// running sum of g continues sequentially (factorizer.hpp:529-542 order).
+__global__ void k_mass_runs(const int* __restrict__ nruns, const int32_t* __restrict__ ukey,
+                            const int* __restrict__ rlen, const int* __restrict__ roff,
+                            const double* __restrict__ sq, MassSpec M) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= *nruns) return;
+  const int32_t rg = M.row_rank[ukey[r]];
+  double m = M.mass[rg];
+  const int b = roff[r], e = b + rlen[r];
+  for (int i = b; i < e; ++i) m = dadd(m, sq[i]);
+  M.mass[rg] = m;
+}
 
 // Per-batch device scratch for the asynchronous level pipeline.
 struct LevelScratch {
@@ -662,9 +739,94 @@ void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_b
   plan.h_order = plan.order.to_host(R);
 }
 
+namespace {
+// Masses of the retired rows over the final columns of batch B, in column
+// chunks of <= chunk_nnz taken entries (ascending column order).
+void batch_masses(const Batch& B, const MassSpec& M, i64 n_ids, cudaStream_t s) {
+  const bool tr = trace_enabled();
+  double tms[5] = {0, 0, 0, 0, 0};
+  auto tl = std::chrono::steady_clock::now();
+  auto lap = [&](int k) {
+    if (!tr) return;
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    tms[k] += std::chrono::duration<double, std::milli>(now - tl).count();
+    tl = now;
+  };
+  DBuf<i64> cnt(B.N + 1, s), pos(B.N + 1, s);
+  PMMF_LAUNCH(k_mass_count, blocks_for((B.N + 1) * 32, kThreads), kThreads, 0, s, B.N, B.col0, B.off.get(),
+              B.len.get(), B.row.get(), B.val.get(), M, cnt.get());
+  exscan(cnt.get(), pos.get(), B.N + 1, s);
+  const std::vector<i64> hp = pos.to_host(B.N + 1);
+  if (hp[B.N] == 0) return;
+  const i64 chunk = std::max<i64>(256, std::min<i64>(M.chunk_nnz, i64{1} << 30));
+  const i64 cap = std::min<i64>(hp[B.N], chunk);
+  const int kb = std::max(1, bits_for(std::max<i64>(n_ids - 1, 1)));
+  DBuf<int32_t> k1, k2, uk;
+  DBuf<double> v1, v2;
+  DBuf<int> rl, ro, nr(1, s);
+  DBuf<unsigned char> tmp;
+  i64 have = 0;
+  auto ensure = [&](i64 n) {
+    if (n <= have) return;
+    k1.alloc(n, s);
+    k2.alloc(n, s);
+    uk.alloc(n, s);
+    v1.alloc(n, s);
+    v2.alloc(n, s);
+    rl.alloc(n, s);
+    ro.alloc(n, s);
+    size_t a = 0, b = 0, c = 0;
+    cub::DoubleBuffer<int32_t> kd(k1.get(), k2.get());
+    cub::DoubleBuffer<double> vd(v1.get(), v2.get());
+    PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, a, kd, vd, static_cast<int64_t>(n), 0, kb, s));
+    PMMF_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b, k1.get(), uk.get(), rl.get(), nr.get(), static_cast<int>(n), s));
+    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, c, rl.get(), ro.get(), static_cast<int>(n), s));
+    tmp.alloc(static_cast<i64>(std::max({a, b, c})) + 1, s);
+    have = n;
+  };
+  ensure(cap);
+  lap(0);
+  int nchunks = 0;
+  i64 w0 = 0;
+  while (w0 < B.N) {
+    i64 w1 = w0 + 1;
+    while (w1 < B.N && hp[w1 + 1] - hp[w0] <= chunk) ++w1;
+    const i64 n = hp[w1] - hp[w0];
+    if (n > 0) {
+      ensure(n);  // a single column above the chunk size
+      ++nchunks;
+      PMMF_LAUNCH(k_mass_gather, blocks_for((w1 - w0) * 32, kThreads), kThreads, 0, s, w0, w1, B.col0, B.off.get(),
+                  B.len.get(), B.row.get(), B.val.get(), M, pos.get(), k1.get(), v1.get());
+      lap(1);
+      cub::DoubleBuffer<int32_t> kd(k1.get(), k2.get());
+      cub::DoubleBuffer<double> vd(v1.get(), v2.get());
+      size_t t = static_cast<size_t>(tmp.n);
+      PMMF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), t, kd, vd, static_cast<int64_t>(n), 0, kb, s));
+      lap(2);
+      t = static_cast<size_t>(tmp.n);
+      PMMF_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), t, kd.Current(), uk.get(), rl.get(), nr.get(),
+                                                   static_cast<int>(n), s));
+      t = static_cast<size_t>(tmp.n);
+      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), t, rl.get(), ro.get(), static_cast<int>(n), s));
+      lap(3);
+      // runs <= n; the kernel reads the exact count on the device
+      PMMF_LAUNCH(k_mass_runs, blocks_for(n, kThreads), kThreads, 0, s, nr.get(), uk.get(), rl.get(), ro.get(),
+                  vd.Current(), M);
+      lap(4);
+    }
+    w0 = w1;
+  }
+  if (tr)
+    std::fprintf(stderr, "[pmmf]     masses: %lld taken in %d chunks: count %.1f gather %.1f sort %.1f rle %.1f runs %.1f ms\n",
+                 static_cast<long long>(hp[B.N]), nchunks, tms[0], tms[1], tms[2], tms[3], tms[4]);
+}
+}  // namespace
+
 void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
                  const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
-                 const uint8_t* keep_all_col, i64 batch_nnz, double growth, cudaStream_t s) {
+                 const uint8_t* keep_all_col, i64 batch_nnz, double growth, const MassSpec* ms,
+                 cudaStream_t s) {
   out.clear();
   const i64 m = static_cast<i64>(off.size()) - 1;
   // host copy of ptr at cluster boundaries
@@ -788,6 +950,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       prof_add_n("rotate_write", static_cast<int64_t>(S.ev.size()), ms,
                  12.0 * static_cast<double>(io[0] + io[1]) + S.rot_bytes);
     }
+    if (ms) batch_masses(B, *ms, in.N, s);
     // finalize into a compact piece
     Piece P;
     P.c0 = B.col0;

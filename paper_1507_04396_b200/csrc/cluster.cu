@@ -127,32 +127,34 @@ __device__ __forceinline__ bool better(double s, int a, double bs, int ba) {
 
 constexpr int kPrefetch = 8;  // anchor entries of a hit row staged in shared memory
 
-// Per-warp shared state: block partial p[m], total t[m], last block seen
-// last[m], touched list touched[m] + count, and the prefetch buffers.
-__host__ __device__ constexpr size_t score_stride(int m) {
-  return static_cast<size_t>(m) * 24 + 16 + 32 * kPrefetch * 12;
-}
+// Per-warp state: block partial p[m], total t[m], last block seen last[m],
+// then the prefetch buffers (16-byte aligned).
+__host__ __device__ constexpr size_t score_pf_off(int m) { return (static_cast<size_t>(m) * 20 + 15) / 16 * 16; }
+__host__ __device__ constexpr size_t score_stride(int m) { return score_pf_off(m) + 32 * kPrefetch * 12; }
 
 // Warps loop over pool columns.  For every chunk of 32 entries of the
 // column, each lane stages the first kPrefetch (anchor, value) pairs of its
 // row in shared memory; then the rows with anchors are replayed in row
 // order (the reference's summation order per anchor), lanes spread over the
 // row's anchors, updating the two-level accumulators of distinct anchors.
-__global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
-  extern __shared__ unsigned char smem[];
+// kSmem: per-warp state in shared memory (else in a global scratch slot,
+// for anchor counts whose state exceeds shared memory).
+template <bool kSmem>
+__global__ void k_score(ScoreArgs A, int warps_per_block) {
+  extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const i64 gwarp = blockIdx.x * static_cast<i64>(warps_per_block) + wib;
-  const i64 nwarps = static_cast<i64>(gridDim.x) * warps_per_block;
   const int m = A.m;
   const size_t stride = score_stride(m);
-  unsigned char* base = use_smem ? smem + stride * wib
-                                 : reinterpret_cast<unsigned char*>(A.g_scratch) + stride * static_cast<size_t>(gwarp);
+  unsigned char* base;
+  if constexpr (kSmem)
+    base = smem + stride * wib;
+  else
+    base = reinterpret_cast<unsigned char*>(A.g_scratch) + stride * static_cast<size_t>(gwarp);
   double* p = reinterpret_cast<double*>(base);
   double* t = p + m;
   int32_t* last = reinterpret_cast<int32_t*>(t + m);
-  int32_t* touched = last + m;
-  int32_t* ntouched = touched + m;
-  double* pf_v = reinterpret_cast<double*>(base + static_cast<size_t>(m) * 24 + 16);
+  double* pf_v = reinterpret_cast<double*>(base + score_pf_off(m));
   int32_t* pf_a = reinterpret_cast<int32_t*>(pf_v + 32 * kPrefetch);
   for (int a = lane; a < m; a += 32) {
     p[a] = 0.0;
@@ -161,7 +163,7 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
   }
   __syncwarp();
   long long busy = 0;
-  (void)nwarps;
+  unsigned long long st_rows = 0, st_ent = 0;  // trace counters, flushed once per warp
   for (;;) {  // columns fetched dynamically, heaviest first
     i64 idx = 0;
     if (lane == 0) idx = static_cast<i64>(atomicAdd(A.next, 1ull));
@@ -175,7 +177,6 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
       if (A.col_cycles && lane == 0) A.col_cycles[w] = 0;
       continue;
     }
-    int nt = 0;  // touched count (warp-uniform)
     const i64 e0 = A.ptr[j], e1 = A.ptr[j + 1];
     // chunk loads are software-pipelined one chunk ahead
     double nv = 0.0;
@@ -226,10 +227,8 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
         const int32_t bs = __shfl_sync(0xffffffffu, b, src);
         const i64 bg = __shfl_sync(0xffffffffu, beg, src);
         const i64 n = __shfl_sync(0xffffffffu, cnt, src);
-        if (A.stats && lane == 0) {
-          atomicAdd(&A.stats[0], 1ull);
-          atomicAdd(&A.stats[1], static_cast<unsigned long long>(n));
-        }
+        st_rows += 1;
+        st_ent += static_cast<unsigned long long>(n);
         // one update of anchor a with product prod (distinct a per lane)
         // one update of anchor a (distinct a per lane within a row):
         // block partial p restarts at 0.0 on a new block row, the finished
@@ -304,6 +303,10 @@ __global__ void k_score(ScoreArgs A, int warps_per_block, bool use_smem) {
     }
   }
   if (A.warp_cycles && lane == 0) A.warp_cycles[gwarp] = busy;
+  if (A.stats && lane == 0) {
+    atomicAdd(&A.stats[0], st_rows);
+    atomicAdd(&A.stats[1], st_ent);
+  }
 }
 
 // Serial work of a pool column in k_score (self-assigned anchors cost
@@ -494,13 +497,24 @@ struct Scorer {
       dpos.upload(pos);
       set_self(danch, dpos, m, true);
     }
+    // warps per block: most resident warps per SM under the shared-memory
+    // limit (227 KB per SM, 1 KB reserved per block)
     const size_t stride = score_stride(m);
-    int wpb = static_cast<int>(std::min<size_t>(8, (100 * 1024) / stride));
+    int wpb = 0, best_w = 0;
+    for (int w : {1, 2, 4, 8}) {
+      const size_t per_block = stride * static_cast<size_t>(w);
+      if (per_block > 200 * 1024) break;
+      const int bps = std::min<int>(32, static_cast<int>((227 * 1024) / (per_block + 1024)));
+      if (w * bps > best_w) {
+        best_w = w * bps;
+        wpb = w;
+      }
+    }
     const bool use_smem = wpb >= 1;
     if (!use_smem) wpb = 4;
     DBuf<double> scratch;
-    if (!use_smem)  // one state slot per launched warp (grid rounded up to whole blocks)
-      scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(((P + wpb - 1) / wpb) * wpb) + 7) / 8), s);
+    if (!use_smem)  // one state slot per launched warp (persistent grid of 148 x 8 blocks)
+      scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(148 * 8 * wpb) + 7) / 8), s);
     DBuf<int32_t> dassign(P, s);
     DBuf<double> drows;
     if (rows_mode) {
@@ -539,9 +553,10 @@ struct Scorer {
     args.nlist = P - nd;
     args.next = next.get();
     const size_t smem = use_smem ? stride * static_cast<size_t>(wpb) : 0;
-    if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(k_score, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    // persistent-style grid: warps loop over the pool
-    const i64 blocks = std::min<i64>((P + wpb - 1) / wpb, use_smem ? 148 * 16 : (P + wpb - 1) / wpb);
+    if (smem > 48 * 1024)
+      PMMF_CUDA(cudaFuncSetAttribute(k_score<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    // persistent grid: resident warps loop over the work list
+    const i64 blocks = std::min<i64>((P + wpb - 1) / wpb, use_smem ? 148 * std::max(1, best_w / wpb) : 148 * 8);
     DBuf<unsigned long long> stats;
     DBuf<long long> ccyc, wcyc;
     const bool timing = trace_enabled() && std::getenv("PMMF_B200_SCORE_TIMING");
@@ -602,8 +617,12 @@ struct Scorer {
       }
     }
     if (timing) cudaEventRecord(ev[1], s);
-    if (args.nlist > 0)
-      PMMF_LAUNCH(k_score, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb, use_smem);
+    if (args.nlist > 0) {
+      if (use_smem)
+        PMMF_LAUNCH(k_score<true>, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb);
+      else
+        PMMF_LAUNCH(k_score<false>, static_cast<unsigned>(blocks), 32 * wpb, 0, s, args, wpb);
+    }
     if (timing) cudaEventRecord(ev[2], s);
     if (trace_enabled()) {
       std::vector<unsigned long long> h = stats.to_host(2);

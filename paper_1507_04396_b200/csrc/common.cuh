@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -97,8 +99,79 @@ inline bool trace_enabled() {
   return e && *e && *e != '0';
 }
 
-// Device memory a new allocation can still get: free memory plus the pool's
-// reserved-but-unused blocks.
+// Large blocks (>= kBigBytes) are cached whole instead of going back to the
+// stream-ordered pool: a fresh mapping of tens of GB costs ~80 ms per GB
+// (measured), and the pool, fragmented by the stage's mixed lifetimes, would
+// otherwise re-map the row-pass arenas, Gram tiles and sort buffers every
+// stage.  A cached block serves a request of at most its size and at least
+// 2/3 of it; it is reused on any stream after the event recorded at its
+// release.  On allocation failure the cache is emptied and the pool trimmed.
+constexpr size_t kBigBytes = size_t{256} << 20;
+
+struct BigCache {
+  struct Blk {
+    void* p;
+    size_t bytes;
+    int dev;
+    cudaEvent_t ready;
+  };
+  std::mutex mu;
+  std::vector<Blk> blocks;
+  size_t cached = 0;
+  static BigCache& get() {
+    static BigCache c;
+    return c;
+  }
+  // Best fit among cached blocks; nullptr if none qualifies.
+  void* take(size_t bytes, int dev, cudaStream_t st, size_t* got) {
+    std::lock_guard<std::mutex> g(mu);
+    size_t best = blocks.size();
+    for (size_t i = 0; i < blocks.size(); ++i) {
+      const Blk& b = blocks[i];
+      if (b.dev != dev || b.bytes < bytes || b.bytes > bytes + bytes / 2) continue;
+      if (best == blocks.size() || b.bytes < blocks[best].bytes) best = i;
+    }
+    if (best == blocks.size()) return nullptr;
+    Blk b = blocks[best];
+    blocks.erase(blocks.begin() + static_cast<std::ptrdiff_t>(best));
+    cached -= b.bytes;
+    cudaStreamWaitEvent(st, b.ready, 0);
+    cudaEventDestroy(b.ready);
+    *got = b.bytes;
+    return b.p;
+  }
+  void give(void* p, size_t bytes, int dev, cudaStream_t st) {
+    cudaEvent_t ev = nullptr;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, st);
+    std::lock_guard<std::mutex> g(mu);
+    blocks.push_back({p, bytes, dev, ev});
+    cached += bytes;
+  }
+  // Returns every cached block of `dev` to the pool (after its last use).
+  void drain(int dev, cudaStream_t st) {
+    std::lock_guard<std::mutex> g(mu);
+    std::vector<Blk> keep;
+    for (Blk& b : blocks) {
+      if (b.dev != dev) {
+        keep.push_back(b);
+        continue;
+      }
+      cudaEventSynchronize(b.ready);
+      cudaEventDestroy(b.ready);
+      cudaFreeAsync(b.p, st);
+      cached -= b.bytes;
+    }
+    blocks.swap(keep);
+  }
+  size_t cached_bytes() {
+    std::lock_guard<std::mutex> g(mu);
+    return cached;
+  }
+};
+
+// Device memory a new allocation can still get: free memory, the pool's
+// reserved-but-unused blocks and the cached large blocks.
 inline i64 available_bytes() {
   size_t f = 0, t = 0;
   PMMF_CUDA(cudaMemGetInfo(&f, &t));
@@ -109,27 +182,58 @@ inline i64 available_bytes() {
   uint64_t reserved = 0, used = 0;
   PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
   PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
-  return static_cast<i64>(f) + static_cast<i64>(reserved - used);
+  return static_cast<i64>(f) + static_cast<i64>(reserved - used) + static_cast<i64>(BigCache::get().cached_bytes());
 }
 
-// Stream-ordered allocation from the device pool.  The pool keeps freed
-// blocks mapped (mapping is the expensive part), so a large request can fail
-// on fragmentation alone: then the stream is drained, the pool trimmed back to
-// what is in use, and the request retried once.
-inline void pool_alloc(void** p, size_t bytes, cudaStream_t st) {
-  cudaError_t e = cudaMallocAsync(p, bytes, st);
+// Stream-ordered allocation.  Large requests are rounded up to 64 MB and
+// served from the block cache when possible.  A failed request drains the
+// cache, trims the pool and is retried once.  *bytes is updated to the size
+// actually held.
+inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
+  int dev = 0;
+  PMMF_CUDA(cudaGetDevice(&dev));
+  if (*bytes >= kBigBytes) {
+    *bytes = (*bytes + (size_t{64} << 20) - 1) / (size_t{64} << 20) * (size_t{64} << 20);
+    size_t got = 0;
+    if (void* q = BigCache::get().take(*bytes, dev, st, &got)) {
+      *p = q;
+      *bytes = got;
+      return;
+    }
+  }
+  const bool timed = *bytes >= (size_t{1} << 30) && trace_enabled();
+  std::chrono::steady_clock::time_point t0;
+  if (timed) {
+    cudaStreamSynchronize(st);
+    t0 = std::chrono::steady_clock::now();
+  }
+  cudaError_t e = cudaMallocAsync(p, *bytes, st);
   if (e == cudaErrorMemoryAllocation) {
     (void)cudaGetLastError();
     PMMF_CUDA(cudaStreamSynchronize(st));
-    int dev = 0;
-    PMMF_CUDA(cudaGetDevice(&dev));
+    BigCache::get().drain(dev, st);
+    PMMF_CUDA(cudaStreamSynchronize(st));
     cudaMemPool_t pool;
     PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     PMMF_CUDA(cudaMemPoolTrimTo(pool, 0));
-    if (trace_enabled()) std::fprintf(stderr, "[pmmf]   pool trimmed for a %zu MB request\n", bytes >> 20);
-    e = cudaMallocAsync(p, bytes, st);
+    if (trace_enabled()) std::fprintf(stderr, "[pmmf]   pool trimmed for a %zu MB request\n", *bytes >> 20);
+    e = cudaMallocAsync(p, *bytes, st);
   }
   PMMF_CUDA(e);
+  if (timed) {
+    cudaStreamSynchronize(st);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > 2.0) std::fprintf(stderr, "[pmmf]   slow alloc: %zu MB in %.1f ms\n", *bytes >> 20, ms);
+  }
+}
+inline void pool_free(void* p, size_t bytes, cudaStream_t st) {
+  if (bytes >= kBigBytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    BigCache::get().give(p, bytes, dev, st);
+  } else {
+    cudaFreeAsync(p, st);
+  }
 }
 
 // Stream-ordered device buffer (cudaMallocAsync from the device pool).
@@ -137,6 +241,7 @@ template <typename T>
 struct DBuf {
   T* p = nullptr;
   i64 n = 0;
+  size_t held = 0;  // bytes held (>= n * sizeof(T))
   cudaStream_t s = nullptr;
   DBuf() = default;
   DBuf(i64 count, cudaStream_t st) { alloc(count, st); }
@@ -148,9 +253,11 @@ struct DBuf {
       release();
       p = o.p;
       n = o.n;
+      held = o.held;
       s = o.s;
       o.p = nullptr;
       o.n = 0;
+      o.held = 0;
     }
     return *this;
   }
@@ -159,12 +266,16 @@ struct DBuf {
     release();
     s = st;
     n = count;
-    if (count > 0) pool_alloc(reinterpret_cast<void**>(&p), sizeof(T) * static_cast<size_t>(count), st);
+    if (count > 0) {
+      held = sizeof(T) * static_cast<size_t>(count);
+      pool_alloc(reinterpret_cast<void**>(&p), &held, st);
+    }
   }
   void release() noexcept {
-    if (p) cudaFreeAsync(p, s);
+    if (p) pool_free(p, held, s);
     p = nullptr;
     n = 0;
+    held = 0;
   }
   T* get() const { return p; }
   void zero() const {

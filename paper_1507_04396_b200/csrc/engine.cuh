@@ -130,6 +130,20 @@ struct Piece {
   DBuf<double> val;
 };
 
+// Residual accounting fused into the row pass (factorizer.hpp:521-547):
+// the final columns c of the row pass are the rows of A', so row g of them
+// is column g of A'.  For retired g the masses sum v^2 over c in ascending
+// order (columns are finalised batch by batch, chunk by chunk, in that
+// order; the running sums are carried in `mass`), taking c when it survives
+// or retires later than g.
+struct MassSpec {
+  const int32_t* row_rank = nullptr;  // stage id -> elimination rank, -1 if not retired
+  const int32_t* col_key = nullptr;   // stage id -> INT_MAX if surviving, else its rank
+  double* mass = nullptr;             // by rank (zero-initialised by the caller)
+  double* diag = nullptr;             // by rank
+  i64 chunk_nnz = 0;                  // entries sorted at once
+};
+
 // One pass of a stage's rotations over the columns of `in` (stage
 // numbering, cluster offsets `off`, rotation slots of cluster u in
 // [slot_base[u], slot_base[u+1])), batch by batch of clusters holding at
@@ -138,10 +152,12 @@ struct Piece {
 // unless keep_all_col[c].
 // `growth` is the expected arena/input ratio of a batch (final columns plus
 // superseded versions); the arena starts at that size so that compactions
-// (copy + re-map) stay rare.
+// (copy + re-map) stay rare.  With `ms`, the residual masses are taken from
+// the final columns before they are filtered into pieces.
 void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
                  const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
-                 const uint8_t* keep_all_col, i64 batch_nnz, double growth, cudaStream_t s);
+                 const uint8_t* keep_all_col, i64 batch_nnz, double growth, const MassSpec* ms,
+                 cudaStream_t s);
 // Transpose of a matrix given as pieces covering [0, N), keeping only rows
 // r with keep_row[r] (all when nullptr); sorted in chunks of <= chunk_nnz
 // entries so the sort buffers stay bounded.

@@ -95,6 +95,16 @@ __global__ void k_mark(i64 R, const int32_t* __restrict__ g, uint8_t* __restrict
   rank[g[r]] = set_rank ? static_cast<int32_t>(r) : -1;
 }
 
+// Residual keys by stage id: the rank of a retired id (row_rank, else -1)
+// and the column key (its rank, or 0x7f7f7f7f for a survivor).
+__global__ void k_mass_keys(i64 R, const int32_t* __restrict__ sid, int32_t* __restrict__ row_rank,
+                            int32_t* __restrict__ col_key) {
+  const i64 r = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (r >= R) return;
+  row_rank[sid[r]] = static_cast<int32_t>(r);
+  col_key[sid[r]] = static_cast<int32_t>(r);
+}
+
 // Core: core(a, b) = A[active[a]][active[b]] (factorizer.hpp:578-588).
 __global__ void k_core(i64 g, const int32_t* __restrict__ col_sid, const i64* __restrict__ ptr,
                        const int32_t* __restrict__ row, const double* __restrict__ val,
@@ -260,6 +270,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     cur = std::move(nxt);
     PMMF_CUDA(cudaStreamSynchronize(s));
     R->phases[4] += ms_since(t0);
+    PMMF_TRACE("[pmmf] stage %d: reblock %.2f ms (%lld entries)\n", stage_no + 1, ms_since(t0),
+               static_cast<long long>(A.nnz));
 
     Result::Stage st;
     st.off = cur.off;
@@ -420,7 +432,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         lap("plan");
         std::vector<Piece> pieces;
         const i64 nnz_in = std::max<i64>(A.nnz, 1);
-        rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, 24.0, s);
+        rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, 24.0, nullptr, s);
         lap("column_pass");
         A = Csc();
         Csc T;
@@ -429,15 +441,11 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         lap("transpose_1");
         const i64 tn = T.nnz;
         // Retired ids: their rotated rows/columns feed only the residual.
-        DBuf<uint8_t> keep_row(N, s), retired(N, s);
+        DBuf<uint8_t> keep_row(N, s);
         {
-          std::vector<uint8_t> kr(static_cast<size_t>(N), 1), rt(static_cast<size_t>(N), 0);
-          for (int32_t sid : order_sid) {
-            kr[sid] = 0;
-            rt[sid] = 1;
-          }
+          std::vector<uint8_t> kr(static_cast<size_t>(N), 1);
+          for (int32_t sid : order_sid) kr[sid] = 0;
           keep_row.upload(kr);
-          retired.upload(rt);
         }
         // The row pass grows its columns about as much as the column pass did
         // (measured ratio); size its arena and batches from that.
@@ -450,27 +458,37 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         if (const char* e = std::getenv("PMMF_B200_BATCH_NNZ")) batch = std::atoll(e);  // test hook
         PMMF_TRACE("[pmmf] stage %d: column pass -> %lld entries, batch=%lld mem=%zuMB\n", stage_no,
                    static_cast<long long>(tn), static_cast<long long>(batch), mem_used_mb());
-        rotate_pass(pieces, T, cur.off, slot_base, plan, nullptr, nullptr, batch, growth, s);
+        // Row pass with the residual masses taken from its final columns
+        // (rows of A'), which then keep only the surviving rows.
+        MassSpec ms;
+        DBuf<int32_t> row_rank(N, s), col_key(N, s);
+        if (ne > 0) {
+          row_rank.fill_bytes(0xff);
+          col_key.fill_bytes(0x7f);
+          PMMF_LAUNCH(k_mass_keys, blocks_for(ne, kThreads), kThreads, 0, s, ne, dsid.get(), row_rank.get(),
+                      col_key.get());
+          mass.zero();
+          diag.zero();
+          ms.row_rank = row_rank.get();
+          ms.col_key = col_key.get();
+          ms.mass = mass.get();
+          ms.diag = diag.get();
+          ms.chunk_nnz = chunk;
+        }
+        rotate_pass(pieces, T, cur.off, slot_base, plan, keep_row.get(), nullptr, batch, growth,
+                    ne > 0 ? &ms : nullptr, s);
         T = Csc();
         lap("row_pass");
         i64 stored = 0;
         for (const Piece& P : pieces) stored += P.nnz;
         PMMF_TRACE("[pmmf] stage %d: row pass stored %lld entries in %zu pieces, mem=%zuMB\n", stage_no,
                    static_cast<long long>(stored), pieces.size(), mem_used_mb());
-        if (ne > 0) {
-          // Exact residual masses: columns g of A' for the retired g, reduced
-          // chunk by chunk from the rotated transpose (never materialised).
-          mass.zero();
-          diag.zero();
-          PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 1);
-          retired_masses(pieces, N, retired.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(),
-                         diag.get(), chunk, s);
+        if (ne > 0) {  // retired ids leave the active set
           PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
           residual_done = true;
         }
-        lap("masses");
         // The next stage reads only the surviving columns of A' (all rows).
-        transpose_pieces(A, pieces, N, keep_row.get(), chunk, s);
+        transpose_pieces(A, pieces, N, nullptr, chunk, s);
         lap("transpose_2");
         PMMF_TRACE("[pmmf] stage %d: A' %lld entries, mem=%zuMB\n", stage_no, static_cast<long long>(A.nnz),
                    mem_used_mb());

@@ -6,12 +6,20 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 
 #include "engine.cuh"
 
 namespace pmmf_b200 {
+
+namespace {
+double ms_since_tp(std::chrono::steady_clock::time_point t) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+}
+}  // namespace
 
 namespace {
 
@@ -595,6 +603,7 @@ void retired_masses(const std::vector<Piece>& in, i64 N, const uint8_t* is_retir
 
 void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_t>& new2old, i64 n_new,
              cudaStream_t s) {
+  const auto t_start = std::chrono::steady_clock::now();
   DBuf<i64> cnt(n_new + 1, s), nptr(n_new + 1, s);
   PMMF_LAUNCH(k_reblock_count, blocks_for((n_new + 1) * 32, kThreads), kThreads, 0, s, n_new, new2old.get(),
               a.ptr.get(), a.row.get(), map.get(), cnt.get());
@@ -606,6 +615,12 @@ void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_
   DBuf<double> v1(std::max<i64>(m, 1), s);
   PMMF_LAUNCH(k_reblock_fill, blocks_for(n_new * 32, kThreads), kThreads, 0, s, n_new, new2old.get(), a.ptr.get(),
               a.row.get(), a.val.get(), map.get(), nptr.get(), r1.get(), v1.get());
+  double t_fill = 0.0;
+  if (trace_enabled()) {
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    t_fill = ms_since_tp(t_start);
+  }
+  const auto t_sort0 = std::chrono::steady_clock::now();
   out.N = n_new;
   out.nnz = m;
   out.row.alloc(std::max<i64>(m, 1), s);
@@ -621,6 +636,10 @@ void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_
                                                   nptr.get() + 1, s));
   }
   out.ptr = std::move(nptr);
+  if (trace_enabled()) {
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "[pmmf]   reblock: count+fill %.2f ms, sort %.2f ms\n", t_fill, ms_since_tp(t_sort0));
+  }
 }
 
 }  // namespace pmmf_b200
