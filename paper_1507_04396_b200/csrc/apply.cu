@@ -662,8 +662,8 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
               S.ovf.get(), level, S.pos.get(), S.rbase.get(), S.rlen.get());
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof_enabled()) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
+    e0 = EventPool::get().take();
+    e1 = EventPool::get().take();
     cudaEventRecord(e0, s);
   }
   PMMF_LAUNCH((k_merge_p<K, true>), kPersistentBlocks, kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
@@ -941,8 +941,8 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
         float t = 0.f;
         cudaEventElapsedTime(&t, e0, e1);
         ms += t;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+        EventPool::get().give(e0);
+        EventPool::get().give(e1);
       }
       std::vector<unsigned long long> io = S.in_entries.to_host(2);
       // algorithmic bytes: inputs read once, outputs written

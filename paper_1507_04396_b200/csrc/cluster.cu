@@ -538,7 +538,7 @@ struct Scorer {
       PMMF_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.get(), tmp, key.get(), key2.get(), idx.get(), list.get(),
                                                           static_cast<int64_t>(P), 0, 32, s));
     }
-    double thr_d = std::max<double>(64.0, static_cast<double>(total) / 150.0);
+    double thr_d = std::max<double>(64.0, static_cast<double>(total) / 4.0);
     if (const char* e = std::getenv("PMMF_B200_DENSE_DIV")) {  // test hook: no floor, <= 0 disables
       const double div = std::atof(e);
       thr_d = div > 0.0 ? static_cast<double>(total) / div : 1e18;

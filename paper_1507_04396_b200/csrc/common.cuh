@@ -170,6 +170,34 @@ struct BigCache {
   }
 };
 
+// Reusable timing events for the profiled passes (creating and destroying
+// two events per dependency level would itself cost ~10 us a level).
+struct EventPool {
+  std::mutex mu;
+  std::vector<cudaEvent_t> free_ev;
+  static EventPool& get() {
+    static EventPool p;
+    return p;
+  }
+  cudaEvent_t take() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      if (!free_ev.empty()) {
+        cudaEvent_t e = free_ev.back();
+        free_ev.pop_back();
+        return e;
+      }
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+  }
+  void give(cudaEvent_t e) {
+    std::lock_guard<std::mutex> g(mu);
+    free_ev.push_back(e);
+  }
+};
+
 // Device memory a new allocation can still get: free memory, the pool's
 // reserved-but-unused blocks and the cached large blocks.
 inline i64 available_bytes() {

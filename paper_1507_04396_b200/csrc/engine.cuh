@@ -92,6 +92,7 @@ struct SearchBatch {
   DBuf<uint64_t> seed;     // derive(seed,{0xF0,p,u})
   DBuf<int64_t> out_base;  // first rotation / elimination slot
   DBuf<int32_t> order;     // CTA launch order: batch-relative clusters by decreasing size
+  std::vector<int64_t> h_c;  // host copy of c
 };
 struct SearchOut {
   DBuf<int32_t> nrot, nelim;   // per cluster

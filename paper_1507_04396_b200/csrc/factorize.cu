@@ -360,6 +360,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         sb.seed.alloc(nb, s);
         sb.out_base.alloc(nb, s);
         sb.c.upload(hc);
+        sb.h_c = hc;
         sb.tile.upload(ht);
         sb.budget.upload(hb);
         sb.seed.upload(hs);

@@ -23,10 +23,13 @@
 //   * the CTA rewrites the k columns (coalesced) and mirrored rows of G and D
 //     over every off-corner row -> barrier 3.
 // Everything is exact fp64 without contraction (-fmad=false).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <numeric>
 
 #include "engine.cuh"
 #include "rng.cuh"
@@ -408,6 +411,340 @@ __global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
   }
 }
 
+// ---- large clusters: one thread-block cluster of `csize` CTAs per cluster.
+// The per-iteration work (partner scan and off-corner update, both O(c)) is
+// split by row slices [lo, hi) across the CTAs, which otherwise run the
+// identical iteration: every CTA advances the same RNG stream, keeps full
+// copies of the bitmask, diagonals and timestamps, and computes the same
+// rotation from the same corner; only rank 0 writes the corner and the
+// records.  Per partner round the CTAs exchange their best (score, index)
+// through distributed shared memory and reduce it in the same total order
+// (strict >, ties to the lowest index), so every decision equals the
+// single-CTA kernel's.  G/D are read with ld.global.cg (L2): rows of one
+// CTA's slice are written by it, corners by rank 0, and a cluster barrier
+// (release/acquire at cluster scope) ends every iteration.
+constexpr int kMaxClusterCtas = 16;
+
+template <int K>
+__global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const int32_t* big_order) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ unsigned char smem[];
+  __shared__ Best red[2][kWarps];
+  __shared__ Best cand[2][kMaxClusterCtas];
+  __shared__ int sh_loc[K];
+  __shared__ double sh_q[K][K];
+  __shared__ int sh_victim;
+  __shared__ int sh_oldts[K];
+  const int crank = static_cast<int>(cl.block_rank());
+  const int csize = static_cast<int>(cl.num_blocks());
+  const int u = big_order[blockIdx.x / csize];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int c = static_cast<int>(A.c[u]);
+  if (c < K) {  // uniform over the cluster's CTAs
+    if (crank == 0 && tid == 0) {
+      A.nrot[u] = 0;
+      A.nelim[u] = 0;
+    }
+    return;
+  }
+  const i64 base = A.out_base[u];
+  i64 budget = static_cast<i64>(floor(A.eta * static_cast<double>(c)));
+  if (A.budget[u] >= 0) budget = min(budget, A.budget[u]);
+  const int nwords = (c + 31) / 32;
+  const int lo = static_cast<int>((static_cast<i64>(c) * crank) / csize);
+  const int hi = static_cast<int>((static_cast<i64>(c) * (crank + 1)) / csize);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem);
+  double* gd = reinterpret_cast<double*>(smem + ((static_cast<size_t>(nwords) * 4 + 15) / 16) * 16);
+  double* dd = gd + c;
+  int32_t* ts = reinterpret_cast<int32_t*>(dd + c);
+  int32_t* level = A.level_scratch + static_cast<i64>(u) * A.max_c;
+  double* G = A.G + A.tile[u];
+  double* D = A.D + A.tile[u];
+  for (int w = tid; w < nwords; w += kSearchThreads) {
+    const int h = min(32, c - w * 32);
+    bits[w] = h == 32 ? 0xffffffffu : ((1u << h) - 1u);
+  }
+  for (int l = tid; l < c; l += kSearchThreads) {
+    gd[l] = __ldcg(G + static_cast<i64>(l) * c + l);
+    dd[l] = __ldcg(D + static_cast<i64>(l) * c + l);
+    ts[l] = 0;
+    if (crank == 0) level[l] = 0;
+  }
+  Xoshiro rng(A.seed[u]);
+  int count = c, nrot = 0, nelim = 0, par = 0, cpar = 0;
+  cl.sync();
+
+  for (i64 s = 0; s < budget; ++s) {
+    if (count <= K - 1) break;
+    const int idx = static_cast<int>(rng.uniform_below(static_cast<uint64_t>(count)));
+    const int draw = warp_select(bits, nwords, idx);
+    if (gd[draw] <= 0.0) {  // vanished column (:234-238)
+      __syncthreads();
+      if (tid == 0) {
+        bits[draw >> 5] &= ~(1u << (draw & 31));
+        if (crank == 0) A.elim_loc[base + nelim] = draw;
+      }
+      --count;
+      ++nelim;
+      __syncthreads();
+      continue;
+    }
+    int loc[K];
+    loc[0] = draw;
+    int npart = 0;
+    const double* gcol = G + static_cast<i64>(draw) * c;
+    const int tsd = ts[draw];
+#pragma unroll 1
+    for (int round = 0; round < K - 1; ++round) {
+      double bs = 0.0;
+      int bl = INT_MAX;
+      for (int l0 = lo + tid; l0 < hi; l0 += 2 * kSearchThreads) {
+        double gv[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int l = l0 + j * kSearchThreads;
+          gv[j] = 0.0;
+          if (l < hi && is_on(bits, l))
+            gv[j] = ts[l] > tsd ? __ldcg(G + static_cast<i64>(l) * c + draw) : __ldcg(gcol + l);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int l = l0 + j * kSearchThreads;
+          if (l >= hi || l == draw || !is_on(bits, l)) continue;
+          const double nl = gd[l];
+          if (nl <= 0.0) continue;
+          bool taken = false;
+#pragma unroll
+          for (int t = 1; t < K; ++t) taken |= (t <= round) && loc[t] == l;
+          if (taken) continue;
+          const double sc = (gv[j] * gv[j]) / nl;
+          if (sc > 0.0 && better(sc, l, bs, bl)) {
+            bs = sc;
+            bl = l;
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+        if (better(os, ol, bs, bl)) {
+          bs = os;
+          bl = ol;
+        }
+      }
+      if (lane == 0) red[par][wid] = Best{bs, bl};
+      __syncthreads();
+      if (wid == 0) {
+        // CTA best, then published to every CTA of the cluster
+        Best b = red[par][0];
+        for (int w = 1; w < kWarps; ++w)
+          if (better(red[par][w].s, red[par][w].l, b.s, b.l)) b = red[par][w];
+        if (lane < csize) {
+          Best* dst = cl.map_shared_rank(&cand[cpar][crank], lane);
+          *dst = b;
+        }
+      }
+      par ^= 1;
+      cl.sync();
+      Best b = cand[cpar][0];
+      for (int r = 1; r < csize; ++r)
+        if (better(cand[cpar][r].s, cand[cpar][r].l, b.s, b.l)) b = cand[cpar][r];
+      cpar ^= 1;
+      if (!(b.s > 0.0)) break;
+#pragma unroll
+      for (int t = 1; t < K; ++t)
+        if (t == round + 1) loc[t] = b.l;
+      ++npart;
+    }
+    if (npart < K - 1) {
+      int have = npart;
+      for (int i = 0; have < K - 1; ++i) {
+        const int l = warp_select(bits, nwords, i);
+        bool taken = l == draw;
+#pragma unroll
+        for (int t = 1; t < K; ++t) taken |= (t <= have) && loc[t] == l;
+        if (!taken) {
+#pragma unroll
+          for (int t = 1; t < K; ++t)
+            if (t == have + 1) loc[t] = l;
+          ++have;
+        }
+      }
+    }
+    if (wid == 0) {
+      double gs[K][K], cd[K][K], q[K][K], ng[K][K], nd[K][K];
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          const bool rowcol = ts[loc[a]] > ts[loc[b]];
+          const i64 at = rowcol ? static_cast<i64>(loc[a]) * c + loc[b] : static_cast<i64>(loc[b]) * c + loc[a];
+          gs[a][b] = __ldcg(G + at);
+          cd[a][b] = __ldcg(D + at);
+        }
+      const bool ok = rotation_from_gram_k<K>(gs, q);
+      conjugate_corner_k<K>(q, gs, ng);
+      conjugate_corner_k<K>(q, cd, nd);
+      int victim = -1;
+      double vn = 0.0;
+#pragma unroll
+      for (int a = 1; a < K; ++a) {
+        const double off = off_diag_norm_sq(ng[a][a], nd[a][a]);
+        if (victim < 0 || off < vn) {
+          victim = loc[a];
+          vn = off;
+        }
+      }
+      if (off_diag_norm_sq(ng[0][0], nd[0][0]) < vn) victim = draw;
+      if (lane == 0) {
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          sh_loc[a] = loc[a];
+#pragma unroll
+          for (int b = 0; b < K; ++b) sh_q[a][b] = q[a][b];
+        }
+        if (crank == 0) {
+          if (!ok) atomicExch(A.error, 1);
+#pragma unroll
+          for (int a = 0; a < K; ++a)
+#pragma unroll
+            for (int p = 0; p < K; ++p) {
+              G[static_cast<i64>(loc[a]) * c + loc[p]] = ng[p][a];
+              D[static_cast<i64>(loc[a]) * c + loc[p]] = nd[p][a];
+            }
+          const i64 slot = base + nrot;
+          int lvl = 0;
+          if (!is_exact_identity_k<K>(q)) {
+#pragma unroll
+            for (int a = 0; a < K; ++a) lvl = max(lvl, level[loc[a]]);
+            ++lvl;
+#pragma unroll
+            for (int a = 0; a < K; ++a) level[loc[a]] = lvl;
+          }
+          A.rot_level[slot] = lvl;
+#pragma unroll
+          for (int a = 0; a < K; ++a) {
+            A.rot_loc[slot * K + a] = loc[a];
+#pragma unroll
+            for (int b = 0; b < K; ++b) A.rot_q[(slot * K + a) * K + b] = q[a][b];
+          }
+          A.elim_loc[base + nelim] = victim;
+        }
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          gd[loc[a]] = ng[a][a];
+          dd[loc[a]] = nd[a][a];
+        }
+        sh_victim = victim;
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          sh_oldts[a] = ts[loc[a]];
+          ts[loc[a]] = nrot + 1;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) bits[sh_victim >> 5] &= ~(1u << (sh_victim & 31));
+    {
+      double q[K][K];
+#pragma unroll
+      for (int a = 0; a < K; ++a)
+#pragma unroll
+        for (int b = 0; b < K; ++b) q[a][b] = sh_q[a][b];
+      int oldts[K];
+#pragma unroll
+      for (int b = 0; b < K; ++b) oldts[b] = sh_oldts[b];
+      for (int r = lo + tid; r < hi; r += kSearchThreads) {
+        bool skip = !is_on(bits, r);
+#pragma unroll
+        for (int a = 0; a < K; ++a) skip |= loc[a] == r;
+        if (skip) continue;
+        const int tr = ts[r];
+        double vg[K], vd[K];
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          const i64 at = tr > oldts[b] ? static_cast<i64>(r) * c + loc[b] : static_cast<i64>(loc[b]) * c + r;
+          vg[b] = __ldcg(G + at);
+          vd[b] = __ldcg(D + at);
+        }
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          double ag = 0.0, ad = 0.0;
+#pragma unroll
+          for (int b = 0; b < K; ++b) {
+            ag = dadd(ag, dmul(q[a][b], vg[b]));
+            ad = dadd(ad, dmul(q[a][b], vd[b]));
+          }
+          G[static_cast<i64>(loc[a]) * c + r] = ag;
+          D[static_cast<i64>(loc[a]) * c + r] = ad;
+        }
+      }
+    }
+    --count;
+    ++nrot;
+    ++nelim;
+    __threadfence();
+    cl.sync();
+  }
+  if (crank == 0 && tid == 0) {
+    A.nrot[u] = nrot;
+    A.nelim[u] = nelim;
+  }
+}
+
+template <int K>
+void launch_cl(const KArgs& a, const int32_t* big_order, i64 nbig, int csize, size_t smem, cudaStream_t s) {
+  auto kern = k_search_cl<K>;
+  PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  if (csize > 8) PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(nbig * csize));
+  cfg.blockDim = dim3(kSearchThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(csize);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PMMF_CUDA(cudaLaunchKernelEx(&cfg, kern, a, big_order));
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
+
+// Largest cluster size (16 non-portable, else 8, 4, 2) the device can
+// co-schedule for this kernel and shared-memory size.
+template <int K>
+int cluster_size_for(size_t smem) {
+  auto kern = k_search_cl<K>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  (void)cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  (void)cudaGetLastError();
+  for (int cs : {16, 8, 4, 2}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(cs));
+    cfg.blockDim = dim3(kSearchThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(cs);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) return cs;
+    (void)cudaGetLastError();
+  }
+  return 0;
+}
+
 template <int K>
 void launch(const KArgs& a, i64 nclusters, size_t smem, cudaStream_t s) {
   if (smem > 48 * 1024)
@@ -440,16 +777,118 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
     timing.zero();
     a.timing = timing.get();
   }
-  switch (k) {
-    case 2: launch<2>(a, nclusters, smem, s); break;
-    case 3: launch<3>(a, nclusters, smem, s); break;
-    case 4: launch<4>(a, nclusters, smem, s); break;
-    case 5: launch<5>(a, nclusters, smem, s); break;
-    case 6: launch<6>(a, nclusters, smem, s); break;
-    case 7: launch<7>(a, nclusters, smem, s); break;
-    case 8: launch<8>(a, nclusters, smem, s); break;
-    default: fail(PMMF_INVALID_ARGUMENT, "FactorizeParams: k must be in [2, 8]");
+  if (k < 2 || k > 8) fail(PMMF_INVALID_ARGUMENT, "FactorizeParams: k must be in [2, 8]");
+  // Large clusters (the sequential critical path of the launch) go to the
+  // thread-block-cluster kernel when their full per-CTA state fits in shared
+  // memory, with about c/1024 CTAs each (2, 4 or 8: measured best on config
+  // 4; a cluster barrier per iteration costs more than wider slices save
+  // beyond that); one launch per cluster width, on forked streams alongside
+  // the one-CTA kernel.
+  i64 big_c = 2048;
+  if (const char* e = std::getenv("PMMF_B200_SEARCH_BIG_C")) big_c = std::atoll(e);  // test hook (<= 0: off)
+  int cmax = 8, force_w = 0;
+  if (const char* e = std::getenv("PMMF_B200_SEARCH_CSIZE")) cmax = std::atoi(e);     // widest cluster
+  if (const char* e = std::getenv("PMMF_B200_SEARCH_FORCE_W")) force_w = std::atoi(e);  // test hook
+  std::vector<int32_t> h_order = b.order.to_host(nclusters), small;
+  std::vector<int32_t> group[5];  // by log2(cluster width)
+  size_t gsmem[5] = {0, 0, 0, 0, 0};
+  if (big_c > 0 && cmax >= 2 && static_cast<i64>(b.h_c.size()) == nclusters) {
+    int dev_max = 0;
+    {
+      size_t probe = 200 * 1024;
+      switch (k) {
+        case 2: dev_max = cluster_size_for<2>(probe); break;
+        case 3: dev_max = cluster_size_for<3>(probe); break;
+        case 4: dev_max = cluster_size_for<4>(probe); break;
+        case 5: dev_max = cluster_size_for<5>(probe); break;
+        case 6: dev_max = cluster_size_for<6>(probe); break;
+        case 7: dev_max = cluster_size_for<7>(probe); break;
+        default: dev_max = cluster_size_for<8>(probe); break;
+      }
+    }
+    cmax = std::min(cmax, dev_max);
+    for (int32_t u : h_order) {
+      const i64 c = b.h_c[u];
+      const size_t need = ((static_cast<size_t>((c + 31) / 32) * 4 + 15) / 16) * 16 + static_cast<size_t>(c) * 20;
+      int w = 1;
+      while (w * 2 <= cmax && static_cast<i64>(w) * 2 * 1024 <= c) w *= 2;
+      if (c >= big_c && need <= 200 * 1024 && cmax >= 2) {
+        w = std::max(w, 2);
+        if (force_w >= 2) w = std::min(force_w, cmax);
+        const int g = w >= 16 ? 4 : w >= 8 ? 3 : w >= 4 ? 2 : 1;
+        group[g].push_back(u);
+        gsmem[g] = std::max(gsmem[g], need);
+      } else {
+        small.push_back(u);
+      }
+    }
+  } else {
+    small = h_order;
   }
+  DBuf<int32_t> d_group[5], d_small;
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> joins;
+  cudaEvent_t fork = nullptr;
+  size_t nbig = 0;
+  for (int g = 4; g >= 1; --g) {
+    if (group[g].empty()) continue;
+    nbig += group[g].size();
+    if (!fork) {
+      PMMF_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      PMMF_CUDA(cudaEventRecord(fork, s));
+    }
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t join = nullptr;
+    PMMF_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+    PMMF_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    PMMF_CUDA(cudaStreamWaitEvent(s2, fork, 0));
+    d_group[g].alloc(static_cast<i64>(group[g].size()), s);
+    d_group[g].upload(group[g]);
+    PMMF_CUDA(cudaEventRecord(join, s));  // upload ordered before the side launch
+    PMMF_CUDA(cudaStreamWaitEvent(s2, join, 0));
+    const i64 nb = static_cast<i64>(group[g].size());
+    const int cs = 1 << g;
+    switch (k) {
+      case 2: launch_cl<2>(a, d_group[g].get(), nb, cs, gsmem[g], s2); break;
+      case 3: launch_cl<3>(a, d_group[g].get(), nb, cs, gsmem[g], s2); break;
+      case 4: launch_cl<4>(a, d_group[g].get(), nb, cs, gsmem[g], s2); break;
+      case 5: launch_cl<5>(a, d_group[g].get(), nb, cs, gsmem[g], s2); break;
+      case 6: launch_cl<6>(a, d_group[g].get(), nb, cs, gsmem[g], s2); break;
+      case 7: launch_cl<7>(a, d_group[g].get(), nb, cs, gsmem[g], s2); break;
+      default: launch_cl<8>(a, d_group[g].get(), nb, cs, gsmem[g], s2); break;
+    }
+    PMMF_CUDA(cudaEventRecord(join, s2));
+    side.push_back(s2);
+    joins.push_back(join);
+  }
+  if (!small.empty()) {
+    KArgs as = a;
+    if (nbig > 0) {
+      d_small.alloc(static_cast<i64>(small.size()), s);
+      d_small.upload(small);
+      as.order = d_small.get();
+    }
+    const i64 ns = static_cast<i64>(small.size());
+    switch (k) {
+      case 2: launch<2>(as, ns, smem, s); break;
+      case 3: launch<3>(as, ns, smem, s); break;
+      case 4: launch<4>(as, ns, smem, s); break;
+      case 5: launch<5>(as, ns, smem, s); break;
+      case 6: launch<6>(as, ns, smem, s); break;
+      case 7: launch<7>(as, ns, smem, s); break;
+      default: launch<8>(as, ns, smem, s); break;
+    }
+  }
+  for (size_t i = 0; i < side.size(); ++i) {
+    PMMF_CUDA(cudaStreamWaitEvent(s, joins[i], 0));
+    cudaEventDestroy(joins[i]);
+    cudaStreamDestroy(side[i]);  // destruction is deferred until its work completes
+  }
+  if (fork) cudaEventDestroy(fork);
+  // the group buffers are released on s, after the join
+  if (trace_enabled())
+    std::fprintf(stderr, "[pmmf]   search: %zu/%zu/%zu/%zu clusters on 2/4/8/16-CTA clusters, %zu on single CTAs\n",
+                 group[1].size(), group[2].size(), group[3].size(), group[4].size(), small.size());
   if (tm) {
     std::vector<unsigned long long> h = timing.to_host(nclusters * 8);
     unsigned long long tot[6] = {0, 0, 0, 0, 0, 0}, mx = 0;
@@ -462,9 +901,14 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
         arg = u;
       }
     }
-    std::fprintf(stderr, "[pmmf] search timing (slowest cluster %lld of %lld): select %llu partner %llu rot %llu offcorner %llu barrier %llu cycles\n",
-                 static_cast<long long>(arg), static_cast<long long>(nclusters), h[arg * 8 + 0], h[arg * 8 + 1],
-                 h[arg * 8 + 2], h[arg * 8 + 3], h[arg * 8 + 4]);
+    std::vector<int64_t> hc = b.c.to_host(nclusters);
+    double sum = 0.0;
+    for (i64 u = 0; u < nclusters; ++u)
+      for (int i = 0; i < 6; ++i) sum += static_cast<double>(h[u * 8 + i]);
+    std::fprintf(stderr, "[pmmf] search timing (slowest cluster %lld of %lld, c=%lld, max_c=%lld): select %llu partner %llu rot %llu offcorner %llu barrier %llu cycles; all clusters %.3g cycles\n",
+                 static_cast<long long>(arg), static_cast<long long>(nclusters), static_cast<long long>(hc[arg]),
+                 static_cast<long long>(max_c), h[arg * 8 + 0], h[arg * 8 + 1],
+                 h[arg * 8 + 2], h[arg * 8 + 3], h[arg * 8 + 4], sum);
   }
 }
 

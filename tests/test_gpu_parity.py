@@ -40,3 +40,16 @@ def test_dense_scoring_path(name, div, monkeypatch):
     monkeypatch.setenv("PMMF_B200_DENSE_DIV", div)
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf512_k4", "zero_cols_bypass",
+                                  "partitioned_input", "k3_sparse"])
+@pytest.mark.parametrize("csize", ["2", "4", "16"])
+def test_cluster_search_path(name, csize, monkeypatch):
+    """Every cluster through the thread-block-cluster search kernel (the
+    large-cluster path on config 4), 2- and 16-CTA clusters — still bit-exact."""
+    monkeypatch.setenv("PMMF_B200_SEARCH_BIG_C", "2")
+    monkeypatch.setenv("PMMF_B200_SEARCH_CSIZE", "16")
+    monkeypatch.setenv("PMMF_B200_SEARCH_FORCE_W", csize)
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
