@@ -215,6 +215,79 @@ __device__ void merge_partition(const PassArgs& A, const double (&q)[K][K], i64 
   }
 }
 
+// k = 2 specialisation of merge_partition (the configs' k): the union of
+// two sorted windows needs two warp searches (each element's rank in the
+// other window), and output positions come from four ballots of non-zero
+// outputs instead of per-column OR-reductions -- about 2.5x fewer
+// instructions per step.  Same values, same order: out_a = (0 + q(a,0) v_0)
+// + q(a,1) v_1 with an absent entry read as 0.0.
+template <bool kWrite>
+__device__ void merge_partition2(const PassArgs& A, const double (&q)[2][2], i64 (&p)[2], const i64 (&hi)[2],
+                                 int (&kept)[2], const i64 (&dst)[2]) {
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  for (;;) {
+    if (p[0] >= hi[0] && p[1] >= hi[1]) break;
+    const i64 ea = p[0] + lane, eb = p[1] + lane;
+    const bool ina = ea < hi[0], inb = eb < hi[1];
+    const int ra = ina ? A.arow[ea] : INT_MAX;
+    const int rb = inb ? A.arow[eb] : INT_MAX;
+    const double va = ina ? A.aval[ea] : 0.0;
+    const double vb = inb ? A.aval[eb] : 0.0;
+    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
+    const bool oka = ra != INT_MAX && ra <= frontier;
+    const bool okb = rb != INT_MAX && rb <= frontier;
+    const int la = warp_lower_bound(rb, ra);  // B-window rows < ra
+    const int lb = warp_lower_bound(ra, rb);  // A-window rows < rb
+    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
+    const int cb = __shfl_sync(0xffffffffu, ra, lb & 31);
+    const double vp = __shfl_sync(0xffffffffu, vb, la & 31);
+    const bool pa = la < 32 && ca == ra;             // A element with a B partner
+    const bool bonly = okb && !(lb < 32 && cb == rb);  // B element without an A partner
+    const double x1 = pa ? vp : 0.0;
+    const double oa0 = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
+    const double oa1 = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
+    const double ob0 = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
+    const double ob1 = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
+    const unsigned NA0 = __ballot_sync(0xffffffffu, oka && oa0 != 0.0);
+    const unsigned NA1 = __ballot_sync(0xffffffffu, oka && oa1 != 0.0);
+    const unsigned NB0 = __ballot_sync(0xffffffffu, bonly && ob0 != 0.0);
+    const unsigned NB1 = __ballot_sync(0xffffffffu, bonly && ob1 != 0.0);
+    if (kWrite) {
+      if (oka) {
+        const unsigned mb = la >= 32 ? 0xffffffffu : ((1u << la) - 1u);
+        if (oa0 != 0.0) {
+          const i64 d = dst[0] + kept[0] + __popc(NA0 & below) + __popc(NB0 & mb);
+          A.wrow[d] = ra;
+          A.wval[d] = oa0;
+        }
+        if (oa1 != 0.0) {
+          const i64 d = dst[1] + kept[1] + __popc(NA1 & below) + __popc(NB1 & mb);
+          A.wrow[d] = ra;
+          A.wval[d] = oa1;
+        }
+      }
+      if (bonly) {
+        const unsigned ma = lb >= 32 ? 0xffffffffu : ((1u << lb) - 1u);
+        if (ob0 != 0.0) {
+          const i64 d = dst[0] + kept[0] + __popc(NA0 & ma) + __popc(NB0 & below);
+          A.wrow[d] = rb;
+          A.wval[d] = ob0;
+        }
+        if (ob1 != 0.0) {
+          const i64 d = dst[1] + kept[1] + __popc(NA1 & ma) + __popc(NB1 & below);
+          A.wrow[d] = rb;
+          A.wval[d] = ob1;
+        }
+      }
+    }
+    kept[0] += __popc(NA0) + __popc(NB0);
+    kept[1] += __popc(NA1) + __popc(NB1);
+    p[0] += __popc(__ballot_sync(0xffffffffu, oka));
+    p[1] += __popc(__ballot_sync(0xffffffffu, okb));
+  }
+}
+
 template <int K>
 __global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long long* __restrict__ in_entries) {
   const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
@@ -342,7 +415,10 @@ __global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, cons
       kept[a] = 0;
       dst[a] = kWrite ? A.pos[K * A.ioff[ri] + a * np + p] : 0;
     }
-    merge_partition<K, kWrite>(A, q, beg, end, kept, dst);
+    if constexpr (K == 2)
+      merge_partition2<kWrite>(A, q, beg, end, kept, dst);
+    else
+      merge_partition<K, kWrite>(A, q, beg, end, kept, dst);
     if (!kWrite && (threadIdx.x & 31) == 0) {
 #pragma unroll
       for (int a = 0; a < K; ++a) A.cnt[K * A.ioff[ri] + a * np + p] = kept[a];
@@ -570,7 +646,8 @@ __global__ void k_mass_count(i64 N, i64 col0, const i64* __restrict__ off, const
   for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
   if (lane == 0) cnt[w] = n;
 }
-// Columns [w0, w1) of the batch: (g, v^2) of the taken entries, column-major.
+// Columns [w0, w1) of the batch: (rank of g, v^2) of the taken entries,
+// column-major.
 __global__ void k_mass_gather(i64 w0, i64 w1, i64 col0, const i64* __restrict__ off,
                               const int32_t* __restrict__ len, const int32_t* __restrict__ arow,
                               const double* __restrict__ aval, MassSpec M, const i64* __restrict__ pos,
@@ -595,24 +672,54 @@ __global__ void k_mass_gather(i64 w0, i64 w1, i64 col0, const i64* __restrict__ 
     if (take) {
       const i64 d = o + __popc(m & ((1u << lane) - 1u));
       const double v = aval[s0 + i];
-      okey[d] = g;
+      okey[d] = M.row_rank[g];
       osq[d] = dmul(v, v);
     }
     o += __popc(m);
   }
 }
-// One thread per row run of the (g-sorted, column order kept) chunk: the
-// running sum of g continues sequentially (factorizer.hpp:529-542 order).
-__global__ void k_mass_runs(const int* __restrict__ nruns, const int32_t* __restrict__ ukey,
-                            const int* __restrict__ rlen, const int* __restrict__ roff,
-                            const double* __restrict__ sq, MassSpec M) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= *nruns) return;
-  const int32_t rg = M.row_rank[ukey[r]];
-  double m = M.mass[rg];
-  const int b = roff[r], e = b + rlen[r];
-  for (int i = b; i < e; ++i) m = dadd(m, sq[i]);
-  M.mass[rg] = m;
+// The chunk is stably sorted by bucket = rank >> shift (so column order is
+// kept inside a bucket); one warp per bucket continues the running sums of
+// its (1 << shift) ranks in shared memory.  Inside a 32-entry window, equal
+// ranks (one per column) are added in lane = column order, one member per
+// round (factorizer.hpp:529-542 sequential order).
+__global__ void k_mass_buckets(i64 n, i64 nbuckets, int shift, const int32_t* __restrict__ key,
+                               const double* __restrict__ sq, MassSpec M) {
+  extern __shared__ double slots[];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const i64 bkt = blockIdx.x * static_cast<i64>(blockDim.x >> 5) + wib;
+  if (bkt >= nbuckets) return;
+  const int width = 1 << shift;
+  double* m = slots + static_cast<i64>(wib) * width;
+  const i64 r0 = bkt << shift;
+  // bounds of the bucket in the sorted keys
+  auto lb = [&](i64 v) {
+    i64 lo = 0, hi = n;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if ((static_cast<i64>(key[mid]) >> shift) < v) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const i64 b = lb(bkt), e = lb(bkt + 1);
+  if (b == e) return;
+  for (int i = lane; i < width; i += 32) m[i] = r0 + i < M.n_retired ? M.mass[r0 + i] : 0.0;
+  __syncwarp();
+  for (i64 x = b; x < e; x += 32) {
+    const i64 i = x + lane;
+    const bool on = i < e;
+    const int32_t r = on ? key[i] : -1 - lane;  // distinct dummies
+    const double v = on ? sq[i] : 0.0;
+    const unsigned grp = __match_any_sync(0xffffffffu, r);
+    const int rk = __popc(grp & ((1u << lane) - 1u));
+    const int rounds = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(__popc(grp)));
+    for (int k = 0; k < rounds; ++k) {
+      if (on && rk == k) m[r - r0] = dadd(m[r - r0], v);
+      __syncwarp();
+    }
+  }
+  for (int i = lane; i < width; i += 32)
+    if (r0 + i < M.n_retired) M.mass[r0 + i] = m[i];
 }
 
 // Per-batch device scratch for the asynchronous level pipeline.
@@ -742,9 +849,9 @@ void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_b
 namespace {
 // Masses of the retired rows over the final columns of batch B, in column
 // chunks of <= chunk_nnz taken entries (ascending column order).
-void batch_masses(const Batch& B, const MassSpec& M, i64 n_ids, cudaStream_t s) {
+void batch_masses(const Batch& B, const MassSpec& M, cudaStream_t s) {
   const bool tr = trace_enabled();
-  double tms[5] = {0, 0, 0, 0, 0};
+  double tms[4] = {0, 0, 0, 0};
   auto tl = std::chrono::steady_clock::now();
   auto lap = [&](int k) {
     if (!tr) return;
@@ -761,32 +868,32 @@ void batch_masses(const Batch& B, const MassSpec& M, i64 n_ids, cudaStream_t s) 
   if (hp[B.N] == 0) return;
   const i64 chunk = std::max<i64>(256, std::min<i64>(M.chunk_nnz, i64{1} << 30));
   const i64 cap = std::min<i64>(hp[B.N], chunk);
-  const int kb = std::max(1, bits_for(std::max<i64>(n_ids - 1, 1)));
-  DBuf<int32_t> k1, k2, uk;
+  // buckets of 2^shift ranks: a 16-bit sort key (two radix passes)
+  const int rb = std::max(1, bits_for(std::max<i64>(M.n_retired - 1, 1)));
+  const int shift = std::max(0, rb - 16);
+  const int kbits = rb - shift;
+  const i64 nbuckets = ((M.n_retired - 1) >> shift) + 1;
+  DBuf<int32_t> k1, k2;
   DBuf<double> v1, v2;
-  DBuf<int> rl, ro, nr(1, s);
   DBuf<unsigned char> tmp;
   i64 have = 0;
   auto ensure = [&](i64 n) {
     if (n <= have) return;
     k1.alloc(n, s);
     k2.alloc(n, s);
-    uk.alloc(n, s);
     v1.alloc(n, s);
     v2.alloc(n, s);
-    rl.alloc(n, s);
-    ro.alloc(n, s);
-    size_t a = 0, b = 0, c = 0;
+    size_t a = 0;
     cub::DoubleBuffer<int32_t> kd(k1.get(), k2.get());
     cub::DoubleBuffer<double> vd(v1.get(), v2.get());
-    PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, a, kd, vd, static_cast<int64_t>(n), 0, kb, s));
-    PMMF_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b, k1.get(), uk.get(), rl.get(), nr.get(), static_cast<int>(n), s));
-    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, c, rl.get(), ro.get(), static_cast<int>(n), s));
-    tmp.alloc(static_cast<i64>(std::max({a, b, c})) + 1, s);
+    PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, a, kd, vd, static_cast<int64_t>(n), shift, shift + kbits, s));
+    tmp.alloc(static_cast<i64>(a) + 1, s);
     have = n;
   };
   ensure(cap);
   lap(0);
+  constexpr int kWarpsPerBlock = 8;
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * (size_t{1} << shift) * sizeof(double);
   int nchunks = 0;
   i64 w0 = 0;
   while (w0 < B.N) {
@@ -802,24 +909,17 @@ void batch_masses(const Batch& B, const MassSpec& M, i64 n_ids, cudaStream_t s) 
       cub::DoubleBuffer<int32_t> kd(k1.get(), k2.get());
       cub::DoubleBuffer<double> vd(v1.get(), v2.get());
       size_t t = static_cast<size_t>(tmp.n);
-      PMMF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), t, kd, vd, static_cast<int64_t>(n), 0, kb, s));
+      PMMF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), t, kd, vd, static_cast<int64_t>(n), shift, shift + kbits, s));
       lap(2);
-      t = static_cast<size_t>(tmp.n);
-      PMMF_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.get(), t, kd.Current(), uk.get(), rl.get(), nr.get(),
-                                                   static_cast<int>(n), s));
-      t = static_cast<size_t>(tmp.n);
-      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(tmp.get(), t, rl.get(), ro.get(), static_cast<int>(n), s));
+      PMMF_LAUNCH(k_mass_buckets, blocks_for(nbuckets * 32, 32 * kWarpsPerBlock), 32 * kWarpsPerBlock, smem, s, n,
+                  nbuckets, shift, kd.Current(), vd.Current(), M);
       lap(3);
-      // runs <= n; the kernel reads the exact count on the device
-      PMMF_LAUNCH(k_mass_runs, blocks_for(n, kThreads), kThreads, 0, s, nr.get(), uk.get(), rl.get(), ro.get(),
-                  vd.Current(), M);
-      lap(4);
     }
     w0 = w1;
   }
   if (tr)
-    std::fprintf(stderr, "[pmmf]     masses: %lld taken in %d chunks: count %.1f gather %.1f sort %.1f rle %.1f runs %.1f ms\n",
-                 static_cast<long long>(hp[B.N]), nchunks, tms[0], tms[1], tms[2], tms[3], tms[4]);
+    std::fprintf(stderr, "[pmmf]     masses: %lld taken in %d chunks: count %.1f gather %.1f sort %.1f sums %.1f ms\n",
+                 static_cast<long long>(hp[B.N]), nchunks, tms[0], tms[1], tms[2], tms[3]);
 }
 }  // namespace
 
@@ -900,6 +1000,16 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));
     set_scalar(S.cursor, static_cast<unsigned long long>(ne));
     int Lstart = 1, repeat = 0, last_ovf = -1;
+    const bool tr = trace_enabled();
+    auto tb = std::chrono::steady_clock::now();
+    double t_levels = 0.0, t_compact = 0.0;
+    auto since = [&](std::chrono::steady_clock::time_point& t0) {
+      PMMF_CUDA(cudaStreamSynchronize(s));
+      const auto now = std::chrono::steady_clock::now();
+      const double ms = std::chrono::duration<double, std::milli>(now - t0).count();
+      t0 = now;
+      return ms;
+    };
     for (;;) {
       for (int L = Lstart; L <= plan.max_level; ++L) {
         const auto [lo, hi] = range[L];
@@ -919,6 +1029,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       int32_t ovf = 0;
       PMMF_CUDA(cudaMemcpyAsync(&ovf, S.ovf.get(), sizeof(ovf), cudaMemcpyDeviceToHost, s));
       PMMF_CUDA(cudaStreamSynchronize(s));
+      if (tr) t_levels += since(tb);
       if (ovf == INT_MAX) break;
       // Level `ovf` did not fit: nothing of it was committed.  Compact the
       // live columns into a larger arena and resume there.
@@ -934,6 +1045,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       set_scalar(S.cursor, static_cast<unsigned long long>(B.used));
       set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));
       Lstart = ovf;
+      if (tr) t_compact += since(tb);
     }
     if (prof_enabled() && !S.ev.empty()) {
       double ms = 0.0;
@@ -950,7 +1062,11 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       prof_add_n("rotate_write", static_cast<int64_t>(S.ev.size()), ms,
                  12.0 * static_cast<double>(io[0] + io[1]) + S.rot_bytes);
     }
-    if (ms) batch_masses(B, *ms, in.N, s);
+    double t_mass = 0.0;
+    if (ms) {
+      batch_masses(B, *ms, s);
+      if (tr) t_mass = since(tb);
+    }
     // finalize into a compact piece
     Piece P;
     P.c0 = B.col0;
@@ -965,6 +1081,10 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     P.val.alloc(std::max<i64>(P.nnz, 1), s);
     PMMF_LAUNCH(k_final_copy, blocks_for(B.N * 32, kThreads), kThreads, 0, s, B.N, B.col0, B.off.get(), B.len.get(),
                 B.row.get(), B.val.get(), keep_row, keep_all_col, P.ptr.get(), P.row.get(), P.val.get());
+    if (tr)
+      std::fprintf(stderr, "[pmmf]     batch cols %lld: levels %.1f compact %.1f masses %.1f final %.1f ms (nnz in %lld out %lld)\n",
+                   static_cast<long long>(B.N), t_levels, t_compact, t_mass, since(tb), static_cast<long long>(ne),
+                   static_cast<long long>(P.nnz));
     out.push_back(std::move(P));
     u0 = u1;
   }

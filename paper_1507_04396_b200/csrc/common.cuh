@@ -106,7 +106,7 @@ inline bool trace_enabled() {
 // stage.  A cached block serves a request of at most its size and at least
 // 2/3 of it; it is reused on any stream after the event recorded at its
 // release.  On allocation failure the cache is emptied and the pool trimmed.
-constexpr size_t kBigBytes = size_t{256} << 20;
+constexpr size_t kBigBytes = size_t{32} << 20;
 
 struct BigCache {
   struct Blk {
@@ -213,7 +213,8 @@ inline i64 available_bytes() {
   return static_cast<i64>(f) + static_cast<i64>(reserved - used) + static_cast<i64>(BigCache::get().cached_bytes());
 }
 
-// Stream-ordered allocation.  Large requests are rounded up to 64 MB and
+// Stream-ordered allocation.  Large requests are rounded up (64 MB above
+// 1 GB, 4 MB below) and
 // served from the block cache when possible.  A failed request drains the
 // cache, trims the pool and is retried once.  *bytes is updated to the size
 // actually held.
@@ -221,7 +222,8 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
   int dev = 0;
   PMMF_CUDA(cudaGetDevice(&dev));
   if (*bytes >= kBigBytes) {
-    *bytes = (*bytes + (size_t{64} << 20) - 1) / (size_t{64} << 20) * (size_t{64} << 20);
+    const size_t g = *bytes >= (size_t{1} << 30) ? (size_t{64} << 20) : (size_t{4} << 20);
+    *bytes = (*bytes + g - 1) / g * g;
     size_t got = 0;
     if (void* q = BigCache::get().take(*bytes, dev, st, &got)) {
       *p = q;
@@ -229,7 +231,7 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
       return;
     }
   }
-  const bool timed = *bytes >= (size_t{1} << 30) && trace_enabled();
+  const bool timed = *bytes >= (size_t{64} << 20) && trace_enabled();
   std::chrono::steady_clock::time_point t0;
   if (timed) {
     cudaStreamSynchronize(st);

@@ -143,6 +143,7 @@ struct MassSpec {
   double* mass = nullptr;             // by rank (zero-initialised by the caller)
   double* diag = nullptr;             // by rank
   i64 chunk_nnz = 0;                  // entries sorted at once
+  i64 n_retired = 0;                  // ranks are [0, n_retired)
 };
 
 // One pass of a stage's rotations over the columns of `in` (stage

@@ -475,6 +475,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           ms.mass = mass.get();
           ms.diag = diag.get();
           ms.chunk_nnz = chunk;
+          ms.n_retired = ne;
         }
         rotate_pass(pieces, T, cur.off, slot_base, plan, keep_row.get(), nullptr, batch, growth,
                     ne > 0 ? &ms : nullptr, s);
