@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <chrono>
 #include <cstdint>
@@ -143,7 +144,9 @@ struct BigCache {
   void give(void* p, size_t bytes, int dev, cudaStream_t st) {
     cudaEvent_t ev = nullptr;
     cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    cudaEventRecord(ev, st);
+    if (cudaEventRecord(ev, st) != cudaSuccess)
+      std::fprintf(stderr, "[pmmf] cache: event record failed on stream %p: %s\n", static_cast<void*>(st),
+                   cudaGetErrorString(cudaGetLastError()));
     std::lock_guard<std::mutex> g(mu);
     blocks.push_back({p, bytes, dev, ev});
     cached += bytes;
@@ -159,6 +162,8 @@ struct BigCache {
       }
       cudaEventSynchronize(b.ready);
       cudaEventDestroy(b.ready);
+      if (trace_enabled() || std::getenv("PMMF_B200_ALLOC_CHECK"))
+        std::fprintf(stderr, "[pmmf]   cache drain frees %p+%zu\n", b.p, b.bytes);
       cudaFreeAsync(b.p, st);
       cached -= b.bytes;
     }
@@ -167,6 +172,47 @@ struct BigCache {
   size_t cached_bytes() {
     std::lock_guard<std::mutex> g(mu);
     return cached;
+  }
+};
+
+// Debug registry of live large blocks (PMMF_B200_ALLOC_CHECK): reports a
+// block handed out twice or released while not live.
+struct AllocCheck {
+  std::mutex mu;
+  std::map<void*, size_t> live;
+  static AllocCheck& get() {
+    static AllocCheck a;
+    return a;
+  }
+  static bool on() {
+    static const bool f = std::getenv("PMMF_B200_ALLOC_CHECK") != nullptr;
+    return f;
+  }
+  static bool verbose() {
+    static const bool f = std::getenv("PMMF_B200_ALLOC_CHECK") && std::getenv("PMMF_B200_ALLOC_CHECK")[0] == '2';
+    return f;
+  }
+  void add(void* p, size_t b, const char* how) {
+    std::lock_guard<std::mutex> g(mu);
+    if (verbose()) std::fprintf(stderr, "[ac] +%s %p %zu\n", how, p, b);
+    auto it = live.lower_bound(p);
+    if (it != live.end() && static_cast<char*>(it->first) < static_cast<char*>(p) + b)
+      std::fprintf(stderr, "[pmmf] alloc-check: %s %p+%zu overlaps live %p+%zu\n", how, p, b, it->first, it->second);
+    if (it != live.begin()) {
+      --it;
+      if (static_cast<char*>(it->first) + it->second > static_cast<char*>(p))
+        std::fprintf(stderr, "[pmmf] alloc-check: %s %p+%zu overlaps live %p+%zu\n", how, p, b, it->first, it->second);
+    }
+    live[p] = b;
+  }
+  void remove(void* p, size_t b) {
+    std::lock_guard<std::mutex> g(mu);
+    if (verbose()) std::fprintf(stderr, "[ac] -free %p %zu\n", p, b);
+    auto it = live.find(p);
+    if (it == live.end())
+      std::fprintf(stderr, "[pmmf] alloc-check: release of non-live %p+%zu\n", p, b);
+    else
+      live.erase(it);
   }
 };
 
@@ -228,6 +274,7 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
     if (void* q = BigCache::get().take(*bytes, dev, st, &got)) {
       *p = q;
       *bytes = got;
+      if (AllocCheck::on()) AllocCheck::get().add(q, got, "cache");
       return;
     }
   }
@@ -250,6 +297,7 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
     e = cudaMallocAsync(p, *bytes, st);
   }
   PMMF_CUDA(e);
+  if (AllocCheck::on()) AllocCheck::get().add(*p, *bytes, "malloc");
   if (timed) {
     cudaStreamSynchronize(st);
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -257,6 +305,7 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
   }
 }
 inline void pool_free(void* p, size_t bytes, cudaStream_t st) {
+  if (AllocCheck::on()) AllocCheck::get().remove(p, bytes);
   if (bytes >= kBigBytes) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -308,8 +357,18 @@ struct DBuf {
     held = 0;
   }
   T* get() const { return p; }
-  void zero() const {
-    if (n) PMMF_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * static_cast<size_t>(n), s));
+  void zero(const char* file = __builtin_FILE(), int line = __builtin_LINE()) const {
+    if (n) {
+      const cudaError_t e = cudaMemsetAsync(p, 0, sizeof(T) * static_cast<size_t>(n), s);
+      if (e != cudaSuccess) {
+        cudaPointerAttributes at{};
+        const cudaError_t e2 = cudaPointerGetAttributes(&at, p);
+        std::fprintf(stderr, "[pmmf] memset failed at %s:%d: p=%p bytes=%zu held=%zu stream=%p attr=%d type=%d dev=%d\n",
+                     file, line, static_cast<void*>(p), sizeof(T) * static_cast<size_t>(n), held, static_cast<void*>(s),
+                     static_cast<int>(e2), static_cast<int>(at.type), at.device);
+      }
+      PMMF_CUDA(e);
+    }
   }
   void fill_bytes(int v) const {
     if (n) PMMF_CUDA(cudaMemsetAsync(p, v, sizeof(T) * static_cast<size_t>(n), s));

@@ -305,9 +305,9 @@ void sort_pairs(DBuf<uint64_t>& keys, DBuf<double>& vals, i64 m, int begin_bit, 
   PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int64_t>(m), begin_bit, end_bit, s));
   DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
   PMMF_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kb, vb, static_cast<int64_t>(m), begin_bit, end_bit, s));
-  if (kb.Current() != keys.get()) {
-    std::swap(keys.p, k2.p);
-    std::swap(vals.p, v2.p);
+  if (kb.Current() != keys.get()) {  // whole buffers: a cached block may be larger than requested
+    std::swap(keys, k2);
+    std::swap(vals, v2);
   }
 }
 
