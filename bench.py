@@ -49,7 +49,22 @@ def parse():
     ap.add_argument("--scale", type=int, default=20, help="R-MAT scale (20 = BASELINE config 4)")
     ap.add_argument("--cpu-scale", type=int, default=14, help="R-MAT scale of the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launch-list", action="store_true",
+                    help="run exactly one factorization step and exit (for the ncu launch list / traffic passes)")
     return ap.parse_args()
+
+
+def merge_traffic():
+    """DRAM bytes (read + write) per launch of the write pass, from the ncu
+    dram__bytes pass over every such launch of one factorization
+    (profiles/merge_traffic_r01.json, scripts/gpu_profile_r01.sh)."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r01.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def config_params():
@@ -240,6 +255,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    if args.launch_list:
+        run_device()
+        torch.cuda.synchronize()
+        return
     for _ in range(args.warmup):
         run_device()
     # ---- timed region: device-resident input
@@ -291,8 +310,8 @@ def main():
     if "rotate_write" in prof:
         c, ms, by = prof["rotate_write"]
         achieved = (by / 1e9) / (ms / 1e3) if ms > 0 else 0.0
-        roof = {"bound": "hbm", "kernel": "k_merge<2,true> (rotation stream, write pass)", "achieved": achieved,
-                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+        roof = {"bound": "hbm", "kernel": "k_merge_p<2,true> (rotation stream, write pass)", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": merge_traffic(),
                 "launches": c, "kernel_ms_total": ms, "algorithmic_bytes_total": by, "peak_source": peak_src,
                 "share_of_step": ms / sum(step_ms)}
         if "rotate_count" in prof:

@@ -48,6 +48,15 @@ def kernel_launches() -> int:
     return int(library().lib.pmmf_b200_kernel_launches())
 
 
+def cached_device_bytes(device: int = 0, release: bool = False) -> int:
+    """Bytes of large device blocks the library keeps for reuse between
+    factorizations; release=True hands them back to the device."""
+    f = library().lib.pmmf_b200_cached_bytes
+    f.restype = ctypes.c_int64
+    f.argtypes = [ctypes.c_int32, ctypes.c_int32]
+    return int(f(int(device), 1 if release else 0))
+
+
 # ------------------------------------------------------------------ params
 @dataclass
 class ClusterParams:

@@ -191,6 +191,35 @@ int pmmf_b200_profile_read(const char* name, int64_t* launches, double* ms, doub
   return PMMF_OK;
 }
 
+int64_t pmmf_b200_cached_bytes(int32_t device, int32_t release) {
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return 0;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  if (release) {
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+      BigCache::get().drain(device, s);
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    }
+    (void)cudaGetLastError();
+  }
+  int64_t n = 0;
+  {
+    BigCache& c = BigCache::get();
+    std::lock_guard<std::mutex> g(c.mu);
+    for (const auto& b : c.blocks)
+      if (b.dev == device) n += static_cast<int64_t>(b.bytes);
+  }
+  cudaSetDevice(prev);
+  return n;
+}
+
 const char* pmmf_b200_version(void) { return "pmmf_b200 0.1 (sm_100a)"; }
 
 }  // extern "C"

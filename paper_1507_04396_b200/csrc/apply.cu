@@ -426,62 +426,6 @@ __global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, cons
   }
 }
 
-template <int K, bool kWrite>
-__global__ void k_merge(PassArgs A) {
-  const i64 item = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
-  if (item >= A.nitems) return;
-  // rotation of this partition: last i with ioff[i] <= item
-  i64 lo = 0, hi = A.nrot;
-  while (hi - lo > 1) {
-    const i64 mid = (lo + hi) >> 1;
-    if (A.ioff[mid] <= item) lo = mid; else hi = mid;
-  }
-  const i64 ri = lo;
-  const i64 p = item - A.ioff[ri];
-  const i64 np = (ri + 1 < A.nrot ? A.ioff[ri + 1] : A.nitems) - A.ioff[ri];
-  const int t = A.rots[ri];
-  int id[K];
-  double q[K][K];
-#pragma unroll
-  for (int b = 0; b < K; ++b) {
-    id[b] = A.ids[static_cast<i64>(t) * K + b] - static_cast<int>(A.col0);
-#pragma unroll
-    for (int a = 0; a < K; ++a) q[b][a] = A.qs[(static_cast<i64>(t) * K + b) * K + a];
-  }
-  i64 beg[K], end[K];
-  partition_range<K>(A, t, p, np, id, beg, end);
-  int kept[K];
-  i64 dst[K];
-#pragma unroll
-  for (int a = 0; a < K; ++a) {
-    kept[a] = 0;
-    dst[a] = kWrite ? A.base + A.pos[K * A.ioff[ri] + a * np + p] : 0;
-  }
-  merge_partition<K, kWrite>(A, q, beg, end, kept, dst);
-  if (!kWrite && (threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int a = 0; a < K; ++a) A.cnt[K * A.ioff[ri] + a * np + p] = kept[a];
-  }
-}
-
-// New (off, len) of every output column of the level.
-template <int K>
-__global__ void k_commit(PassArgs A, i64* __restrict__ off, int32_t* __restrict__ len, i64 total) {
-  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (i >= A.nrot) return;
-  const int t = A.rots[i];
-  const i64 np = (i + 1 < A.nrot ? A.ioff[i + 1] : A.nitems) - A.ioff[i];
-#pragma unroll
-  for (int a = 0; a < K; ++a) {
-    const i64 f = K * A.ioff[i] + a * np;
-    const i64 b = A.pos[f];
-    const i64 e = (f + np < K * A.nitems) ? A.pos[f + np] : total;
-    const int id = A.ids[static_cast<i64>(t) * K + a] - static_cast<int>(A.col0);
-    off[id] = A.base + b;
-    len[id] = static_cast<int32_t>(e - b);
-  }
-}
-
 __global__ void k_len64(i64 N, const int32_t* __restrict__ len, i64* __restrict__ out) {
   const i64 j = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (j < N) out[j] = len[j];
@@ -577,15 +521,6 @@ i64 read_i64(const i64* p, cudaStream_t s) {
   PMMF_CUDA(cudaMemcpyAsync(&v, p, sizeof(v), cudaMemcpyDeviceToHost, s));
   PMMF_CUDA(cudaStreamSynchronize(s));
   return v;
-}
-
-// a[0] + b[0] with a single synchronisation
-i64 read_sum2(const i64* a, const i64* b, cudaStream_t s) {
-  i64 v[2] = {0, 0};
-  PMMF_CUDA(cudaMemcpyAsync(&v[0], a, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  PMMF_CUDA(cudaMemcpyAsync(&v[1], b, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  PMMF_CUDA(cudaStreamSynchronize(s));
-  return v[0] + v[1];
 }
 
 // Batch working set: paged view of columns [col0, col0+N) in an arena.

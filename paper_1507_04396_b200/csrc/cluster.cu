@@ -130,7 +130,7 @@ constexpr int kPrefetch = 8;  // anchor entries of a hit row staged in shared me
 // Per-warp state: block partial p[m], total t[m], last block seen last[m],
 // then the prefetch buffers (16-byte aligned).
 __host__ __device__ constexpr size_t score_pf_off(int m) { return (static_cast<size_t>(m) * 20 + 15) / 16 * 16; }
-__host__ __device__ constexpr size_t score_stride(int m) { return score_pf_off(m) + 32 * kPrefetch * 12; }
+__host__ __device__ constexpr size_t score_stride(int m) { return score_pf_off(m) + 32 * kPrefetch * 12 + 32; }
 
 // Warps loop over pool columns.  For every chunk of 32 entries of the
 // column, each lane stages the first kPrefetch (anchor, value) pairs of its
@@ -156,6 +156,7 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
   int32_t* last = reinterpret_cast<int32_t*>(t + m);
   double* pf_v = reinterpret_cast<double*>(base + score_pf_off(m));
   int32_t* pf_a = reinterpret_cast<int32_t*>(pf_v + 32 * kPrefetch);
+  uint8_t* slotmap = reinterpret_cast<uint8_t*>(pf_a + 32 * kPrefetch);  // window slot -> row lane
   for (int a = lane; a < m; a += 32) {
     p[a] = 0.0;
     t[a] = 0.0;
@@ -219,35 +220,43 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
           }
       }
       __syncwarp();
-      unsigned hits = __ballot_sync(0xffffffffu, cnt > 0);
+      // Update of anchor a by row (value vr, block br) with anchor value av:
+      // the block partial p restarts at 0.0 on a new block row and the
+      // finished partial is flushed into the total t (two-level order, P3).
+      auto update = [&](int32_t a, double vr, int32_t br, double av) {
+        const double prod = dmul(vr, av);
+        const int32_t la = last[a];
+        const double pa = p[a], ta = t[a];
+        const bool same = la == br;
+        t[a] = (same || la < 0) ? ta : dadd(ta, pa);
+        p[a] = dadd(same ? pa : 0.0, prod);
+        last[a] = br;
+      };
+      // Light rows (<= kPrefetch anchors, staged in shared memory) are packed
+      // into windows of <= 32 (row, anchor) slots in row order; an anchor
+      // shared by several rows of a window is updated one row per round,
+      // in row order.  Heavy rows are processed alone.
+      const unsigned hit_mask = __ballot_sync(0xffffffffu, cnt > 0);
+      const unsigned heavy_mask = __ballot_sync(0xffffffffu, cnt > kPrefetch);
+      const int c32 = cnt > 0 ? static_cast<int>(cnt < 32 ? cnt : 32) : 0;
+      int incl = c32;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      const int excl = incl - c32;
+      unsigned hits = hit_mask;
       while (hits) {
-        const int src = __ffs(hits) - 1;
-        hits &= hits - 1;
-        const double vs = __shfl_sync(0xffffffffu, v, src);
-        const int32_t bs = __shfl_sync(0xffffffffu, b, src);
-        const i64 bg = __shfl_sync(0xffffffffu, beg, src);
-        const i64 n = __shfl_sync(0xffffffffu, cnt, src);
-        st_rows += 1;
-        st_ent += static_cast<unsigned long long>(n);
-        // one update of anchor a with product prod (distinct a per lane)
-        // one update of anchor a (distinct a per lane within a row):
-        // block partial p restarts at 0.0 on a new block row, the finished
-        // partial is flushed into the total t (two-level order, P3); the
-        // three shared-memory slots are read together, no branches.
-        auto update = [&](bool on, int32_t a, double av) {
-          if (!on) return;
-          const double prod = dmul(vs, av);
-          const int32_t la = last[a];
-          const double pa = p[a], ta = t[a];
-          const bool same = la == bs;
-          t[a] = (same || la < 0) ? ta : dadd(ta, pa);
-          p[a] = dadd(same ? pa : 0.0, prod);
-          last[a] = bs;
-        };
-        if (n <= kPrefetch) {
-          const bool on = lane < n;
-          update(on, on ? pf_a[src * kPrefetch + lane] : 0, on ? pf_v[src * kPrefetch + lane] : 0.0);
-        } else {
+        const int s0 = __ffs(hits) - 1;
+        if ((heavy_mask >> s0) & 1u) {
+          hits &= hits - 1;
+          const double vs = __shfl_sync(0xffffffffu, v, s0);
+          const int32_t bs = __shfl_sync(0xffffffffu, b, s0);
+          const i64 bg = __shfl_sync(0xffffffffu, beg, s0);
+          const i64 n = __shfl_sync(0xffffffffu, cnt, s0);
+          st_rows += 1;
+          st_ent += static_cast<unsigned long long>(n);
           // hub row: issue all of a 256-entry batch's loads before any update
           constexpr int kB = 8;
           for (i64 q0 = 0; q0 < n; q0 += 32 * kB) {
@@ -261,10 +270,37 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
             }
 #pragma unroll
             for (int k = 0; k < kB; ++k)
-              if (q0 + k * 32 < n) update(q0 + k * 32 + lane < n, ra[k], rv[k]);
+              if (q0 + k * 32 + lane < n) update(ra[k], vs, bs, rv[k]);
           }
+          __syncwarp();
+          continue;
         }
+        const int base = __shfl_sync(0xffffffffu, excl, s0);
+        const unsigned later_heavy = heavy_mask & (0xffffffffu << s0);
+        const int stop = later_heavy ? __ffs(later_heavy) - 1 : 32;
+        const bool fits = ((hits >> lane) & 1u) && lane < stop && incl - base <= 32;
+        const unsigned win = __ballot_sync(0xffffffffu, fits);
+        const int total = __shfl_sync(0xffffffffu, incl, 31 - __clz(win)) - base;
+        if (fits)
+          for (int k = 0; k < c32; ++k) slotmap[excl - base + k] = static_cast<uint8_t>(lane);
         __syncwarp();
+        const bool on = lane < total;
+        const int src = on ? slotmap[lane] : lane;
+        const int k = lane - (__shfl_sync(0xffffffffu, excl, src) - base);
+        const double vs = __shfl_sync(0xffffffffu, v, src);
+        const int32_t bs = __shfl_sync(0xffffffffu, b, src);
+        const int32_t a = on ? pf_a[src * kPrefetch + k] : -1 - lane;
+        const double av = on ? pf_v[src * kPrefetch + k] : 0.0;
+        const unsigned grp = __match_any_sync(0xffffffffu, a);
+        const int rk = __popc(grp & ((1u << lane) - 1u));
+        const int rounds = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(__popc(grp))));
+        for (int r = 0; r < rounds; ++r) {
+          if (on && rk == r) update(a, vs, bs, av);
+          __syncwarp();
+        }
+        st_rows += static_cast<unsigned long long>(__popc(win));
+        st_ent += static_cast<unsigned long long>(total);
+        hits &= ~win;
       }
     }
     __syncwarp();
@@ -757,6 +793,7 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
     std::vector<i64> orphans = std::move(clusters[worst]);
     clusters[worst].clear();
     size_t orr = 0;
+    std::vector<size_t> grew;  // clusters that received orphans (the others stay sorted)
     for (i64 o : orphans) {
       const int64_t row = cand_row[pool_pos(o)];
       if (row < 0) fail(PMMF_INTERNAL, "clustering: orphan without a precomputed score row");
@@ -772,8 +809,11 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
       }
       const size_t a = bs > 0.0 ? best : (orr++) % alive.size();
       clusters[alive[a]].push_back(o);
+      grew.push_back(alive[a]);
     }
-    for (size_t a : alive) std::sort(clusters[a].begin(), clusters[a].end());
+    std::sort(grew.begin(), grew.end());
+    grew.erase(std::unique(grew.begin(), grew.end()), grew.end());
+    for (size_t a : grew) std::sort(clusters[a].begin(), clusters[a].end());
   }
   for (size_t a : alive) {  // oversize recursion (clustering.hpp:165-176)
     auto& mem = clusters[a];

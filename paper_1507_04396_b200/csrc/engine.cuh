@@ -165,13 +165,6 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
 // entries so the sort buffers stay bounded.
 void transpose_pieces(Csc& out, const std::vector<Piece>& in, i64 N, const uint8_t* keep_row, i64 chunk_nnz,
                       cudaStream_t s);
-// Residual accounting (factorizer.hpp:521-547) straight from the rotated
-// transpose: column g of A' (= row g of the pieces) for every retired stage
-// id g, reduced chunk by chunk without materialising it.  mass/diag are
-// indexed by elimination rank (zero-initialised by the caller).
-void retired_masses(const std::vector<Piece>& in, i64 N, const uint8_t* is_retired, const int32_t* s2g,
-                    const uint8_t* is_active, const int32_t* rank, double* mass, double* diag, i64 chunk_nnz,
-                    cudaStream_t s);
 // Builds the level plan from a search result: slot = out_base[u] + t for
 // t < nrot[u]; stage id = cluster_off[u] + local.
 void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_base,

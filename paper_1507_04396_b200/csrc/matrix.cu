@@ -546,60 +546,6 @@ void transpose_pieces(Csc& out, const std::vector<Piece>& in, i64 N, const uint8
   if (!hp.empty()) out.ptr.upload(hp);
 }
 
-namespace {
-// Residual accounting (factorizer.hpp:529-542) for retired rows g of the
-// rotated transpose, i.e. columns g of A': warp per g, entries in column
-// (stage) order, lane 0 sums v^2 sequentially over qualifying rows.
-__global__ void k_chunk_masses(i64 r0, i64 r1, const i64* __restrict__ ptr, const uint64_t* __restrict__ keys,
-                               const double* __restrict__ vals, int cb, const int32_t* __restrict__ s2g,
-                               const uint8_t* __restrict__ is_active, const int32_t* __restrict__ rank,
-                               double* __restrict__ mass, double* __restrict__ diag) {
-  const i64 g = r0 + ((blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (g >= r1) return;
-  const i64 b = ptr[g] - ptr[r0], e = ptr[g + 1] - ptr[r0];
-  if (e == b) return;
-  const int32_t rg = rank[s2g[g]];
-  if (rg < 0) return;
-  const uint64_t cmask = (uint64_t{1} << cb) - 1;
-  double m = 0.0, d = 0.0;
-  for (i64 x = b; x < e; x += 32) {
-    const i64 i = x + lane;
-    double sq = 0.0, v = 0.0;
-    bool take = false, isdiag = false;
-    if (i < e) {
-      const int32_t c = static_cast<int32_t>(keys[i] & cmask);
-      v = vals[i];
-      if (c == g) {
-        isdiag = true;
-      } else {
-        const int32_t l = s2g[c];
-        take = is_active[l] || rank[l] > rg;
-        sq = dmul(v, v);
-      }
-    }
-    const unsigned tk = __ballot_sync(0xffffffffu, take);
-    const unsigned dg = __ballot_sync(0xffffffffu, isdiag);
-    if (dg) d = __shfl_sync(0xffffffffu, v, __ffs(dg) - 1);
-    for (unsigned mm = tk; mm; mm &= mm - 1) m = dadd(m, __shfl_sync(0xffffffffu, sq, __ffs(mm) - 1));
-  }
-  if (lane == 0) {
-    mass[rg] = m;
-    diag[rg] = d;
-  }
-}
-}  // namespace
-
-void retired_masses(const std::vector<Piece>& in, i64 N, const uint8_t* is_retired, const int32_t* s2g,
-                    const uint8_t* is_active, const int32_t* rank, double* mass, double* diag, i64 chunk_nnz,
-                    cudaStream_t s) {
-  std::vector<i64> hp;
-  transpose_chunks(in, N, is_retired, chunk_nnz, hp, s,
-                   [&](i64 r0, i64 r1, i64, int cb, const uint64_t* keys, const double* vals, const i64* ptr) {
-                     PMMF_LAUNCH(k_chunk_masses, blocks_for((r1 - r0) * 32, kThreads), kThreads, 0, s, r0, r1, ptr,
-                                 keys, vals, cb, s2g, is_active, rank, mass, diag);
-                   });
-}
 
 void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_t>& new2old, i64 n_new,
              cudaStream_t s) {

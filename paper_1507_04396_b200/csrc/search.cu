@@ -82,6 +82,36 @@ __device__ int warp_select(const uint32_t* bits, int nwords, int idx) {
   return __shfl_sync(0xffffffffu, found, who ? __ffs(who) - 1 : 0);
 }
 
+// Same selection through per-group counts (group = 32 words = 1024 ids, at
+// most 32 groups): two warp scans instead of a scan over every word.
+__device__ int warp_select2(const uint32_t* bits, const int* gcnt, int nwords, int idx) {
+  const int lane = threadIdx.x & 31;
+  const int ngroups = (nwords + 31) >> 5;
+  const int gc = lane < ngroups ? gcnt[lane] : 0;
+  int incl = gc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int g = __ffs(__ballot_sync(0xffffffffu, idx < incl)) - 1;
+  const int rem = idx - __shfl_sync(0xffffffffu, incl - gc, g);
+  const int w = (g << 5) + lane;
+  const uint32_t word = w < nwords ? bits[w] : 0u;
+  const int pc = __popc(word);
+  int incl2 = pc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl2, o);
+    if (lane >= o) incl2 += v;
+  }
+  const int wl = __ffs(__ballot_sync(0xffffffffu, rem < incl2)) - 1;
+  int r2 = rem - __shfl_sync(0xffffffffu, incl2 - pc, wl);
+  uint32_t ww = __shfl_sync(0xffffffffu, word, wl);
+  for (; r2 > 0; --r2) ww &= ww - 1;
+  return ((g << 5) + wl) * 32 + (__ffs(ww) - 1);
+}
+
 __device__ __forceinline__ bool is_on(const uint32_t* bits, int l) { return (bits[l >> 5] >> (l & 31)) & 1u; }
 
 struct KArgs {
@@ -150,10 +180,13 @@ __global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
   int32_t* level = A.level_scratch + static_cast<i64>(u) * A.max_c;
   double* G = A.G + A.tile[u];
   double* D = A.D + A.tile[u];
+  __shared__ int gcnt[32];
+  const bool sel2 = nwords <= 1024;
   for (int w = tid; w < nwords; w += kSearchThreads) {
     const int hi = min(32, c - w * 32);
     bits[w] = hi == 32 ? 0xffffffffu : ((1u << hi) - 1u);
   }
+  if (tid < 32) gcnt[tid] = max(0, min(1024, c - tid * 1024));
   for (int l = tid; l < c; l += kSearchThreads) {
     gd[l] = G[static_cast<i64>(l) * c + l];
     dd[l] = D[static_cast<i64>(l) * c + l];
@@ -174,12 +207,13 @@ __global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
   for (i64 s = 0; s < budget; ++s) {
     if (count <= K - 1) break;
     const int idx = static_cast<int>(rng.uniform_below(static_cast<uint64_t>(count)));
-    const int draw = warp_select(bits, nwords, idx);
+    const int draw = sel2 ? warp_select2(bits, gcnt, nwords, idx) : warp_select(bits, nwords, idx);
     TMARK(0)
     if (gd[draw] <= 0.0) {  // vanished column: retire without a rotation (:234-238)
       __syncthreads();      // everyone has read bits for this draw
       if (tid == 0) {
         bits[draw >> 5] &= ~(1u << (draw & 31));
+        gcnt[(draw >> 10) & 31] -= 1;
         A.elim_loc[base + nelim] = draw;
       }
       --count;
@@ -251,7 +285,7 @@ __global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
       // every warp computes the same answer.
       int have = npart;
       for (int i = 0; have < K - 1; ++i) {
-        const int l = warp_select(bits, nwords, i);
+        const int l = sel2 ? warp_select2(bits, gcnt, nwords, i) : warp_select(bits, nwords, i);
         bool taken = l == draw;
 #pragma unroll
         for (int t = 1; t < K; ++t) taken |= (t <= have) && loc[t] == l;
@@ -343,7 +377,10 @@ __global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
     TMARK(2)
     // Other warps may still have been reading the bitmask (partner fill)
     // before barrier 2; retire the victim only now.
-    if (tid == 0) bits[sh_victim >> 5] &= ~(1u << (sh_victim & 31));
+    if (tid == 0) {
+      bits[sh_victim >> 5] &= ~(1u << (sh_victim & 31));
+      gcnt[(sh_victim >> 10) & 31] -= 1;
+    }
     // ---- off-corner rows of G and D (sparse.hpp:398-439)
     {
       double q[K][K];
@@ -461,10 +498,13 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
   int32_t* level = A.level_scratch + static_cast<i64>(u) * A.max_c;
   double* G = A.G + A.tile[u];
   double* D = A.D + A.tile[u];
+  __shared__ int gcnt[32];
+  const bool sel2 = nwords <= 1024;
   for (int w = tid; w < nwords; w += kSearchThreads) {
     const int h = min(32, c - w * 32);
     bits[w] = h == 32 ? 0xffffffffu : ((1u << h) - 1u);
   }
+  if (tid < 32) gcnt[tid] = max(0, min(1024, c - tid * 1024));
   for (int l = tid; l < c; l += kSearchThreads) {
     gd[l] = __ldcg(G + static_cast<i64>(l) * c + l);
     dd[l] = __ldcg(D + static_cast<i64>(l) * c + l);
@@ -473,16 +513,26 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
   }
   Xoshiro rng(A.seed[u]);
   int count = c, nrot = 0, nelim = 0, par = 0, cpar = 0;
+  unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0}, tprev = clock64();
+  const bool timed = A.timing && crank == 0 && tid == 0;
+#define CMARK(i)                               \
+  if (timed) {                                 \
+    const unsigned long long now_ = clock64(); \
+    tacc[i] += now_ - tprev;                   \
+    tprev = now_;                              \
+  }
   cl.sync();
 
   for (i64 s = 0; s < budget; ++s) {
     if (count <= K - 1) break;
     const int idx = static_cast<int>(rng.uniform_below(static_cast<uint64_t>(count)));
-    const int draw = warp_select(bits, nwords, idx);
+    const int draw = sel2 ? warp_select2(bits, gcnt, nwords, idx) : warp_select(bits, nwords, idx);
+    CMARK(0)
     if (gd[draw] <= 0.0) {  // vanished column (:234-238)
       __syncthreads();
       if (tid == 0) {
         bits[draw >> 5] &= ~(1u << (draw & 31));
+        gcnt[(draw >> 10) & 31] -= 1;
         if (crank == 0) A.elim_loc[base + nelim] = draw;
       }
       --count;
@@ -547,7 +597,9 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
         }
       }
       par ^= 1;
+      CMARK(1)
       cl.sync();
+      CMARK(2)
       Best b = cand[cpar][0];
       for (int r = 1; r < csize; ++r)
         if (better(cand[cpar][r].s, cand[cpar][r].l, b.s, b.l)) b = cand[cpar][r];
@@ -561,7 +613,7 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
     if (npart < K - 1) {
       int have = npart;
       for (int i = 0; have < K - 1; ++i) {
-        const int l = warp_select(bits, nwords, i);
+        const int l = sel2 ? warp_select2(bits, gcnt, nwords, i) : warp_select(bits, nwords, i);
         bool taken = l == draw;
 #pragma unroll
         for (int t = 1; t < K; ++t) taken |= (t <= have) && loc[t] == l;
@@ -646,7 +698,11 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
       }
     }
     __syncthreads();
-    if (tid == 0) bits[sh_victim >> 5] &= ~(1u << (sh_victim & 31));
+    CMARK(3)
+    if (tid == 0) {
+      bits[sh_victim >> 5] &= ~(1u << (sh_victim & 31));
+      gcnt[(sh_victim >> 10) & 31] -= 1;
+    }
     {
       double q[K][K];
 #pragma unroll
@@ -685,9 +741,14 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
     --count;
     ++nrot;
     ++nelim;
+    CMARK(4)
     __threadfence();
     cl.sync();
+    CMARK(5)
   }
+  if (timed)
+    for (int i = 0; i < 6; ++i) A.timing[static_cast<i64>(u) * 8 + i] = tacc[i];
+#undef CMARK
   if (crank == 0 && tid == 0) {
     A.nrot[u] = nrot;
     A.nelim[u] = nelim;
@@ -905,10 +966,23 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
     double sum = 0.0;
     for (i64 u = 0; u < nclusters; ++u)
       for (int i = 0; i < 6; ++i) sum += static_cast<double>(h[u * 8 + i]);
-    std::fprintf(stderr, "[pmmf] search timing (slowest cluster %lld of %lld, c=%lld, max_c=%lld): select %llu partner %llu rot %llu offcorner %llu barrier %llu cycles; all clusters %.3g cycles\n",
-                 static_cast<long long>(arg), static_cast<long long>(nclusters), static_cast<long long>(hc[arg]),
-                 static_cast<long long>(max_c), h[arg * 8 + 0], h[arg * 8 + 1],
-                 h[arg * 8 + 2], h[arg * 8 + 3], h[arg * 8 + 4], sum);
+    std::vector<i64> ord(static_cast<size_t>(nclusters));
+    std::iota(ord.begin(), ord.end(), i64{0});
+    auto tot_of = [&](i64 u) {
+      unsigned long long t = 0;
+      for (int i = 0; i < 6; ++i) t += h[u * 8 + i];
+      return t;
+    };
+    std::sort(ord.begin(), ord.end(), [&](i64 x, i64 y) { return tot_of(x) > tot_of(y); });
+    std::fprintf(stderr, "[pmmf] search timing: %lld clusters, all %.3g cycles; slowest:\n", static_cast<long long>(nclusters), sum);
+    for (size_t i = 0; i < std::min<size_t>(5, ord.size()); ++i) {
+      const i64 u = ord[i];
+      std::fprintf(stderr, "[pmmf]     c=%lld total %llu: %llu %llu %llu %llu %llu %llu\n", static_cast<long long>(hc[u]),
+                   tot_of(u), h[u * 8 + 0], h[u * 8 + 1], h[u * 8 + 2], h[u * 8 + 3], h[u * 8 + 4], h[u * 8 + 5]);
+    }
+    (void)arg;
+    (void)mx;
+    (void)tot;
   }
 }
 

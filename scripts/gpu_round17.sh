@@ -3,4 +3,4 @@ timeout 900 python -m pytest -x -q test_gpu_parity.py test_golden.py -m gpu 2>&1
 cd ..
 timeout 600 python scripts/three_runs.py 3 > gpurun_out/three_m.log 2>&1
 grep -E "^run |rror" gpurun_out/three_m.log
-sed -n '/^run 1/,$p' gpurun_out/three_m.log | grep -E "batch cols|masses|apply\.(col|row)" | head -12
+sed -n '/^run 1/,$p' gpurun_out/three_m.log | grep -E "gram" | head -6

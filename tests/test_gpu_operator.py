@@ -46,3 +46,21 @@ def test_cg_traces(precondition):
     # the first 20 residuals agree to 1e-9 relative
     k = 20
     assert np.allclose(gt[:, :k], ot[:, :k], rtol=1e-9, atol=0)
+
+
+def test_cached_blocks_reused_and_released():
+    """Large device blocks stay cached between factorizations (reuse, no
+    fresh mapping) and pmmf_b200_cached_bytes(release=1) hands them back."""
+    from paper_1507_04396_b200 import api
+    from paper_1507_04396_b200.api import BlockedSparseMatrix, ClusterParams, FactorizeParams
+
+    inp = api.workload_rmat(16, 32, 7)
+    m = BlockedSparseMatrix.from_triplets(*inp)
+    p = FactorizeParams(seed=3, cluster=ClusterParams(m_target=64))
+    a = api.factorize(m, p)
+    cached = api.cached_device_bytes(0)
+    assert cached > 0
+    b = api.factorize(m, p)
+    assert np.array_equal(a.core, b.core) and a.residual_sq == b.residual_sq
+    assert api.cached_device_bytes(0, release=True) == 0
+    assert api.cached_device_bytes(0) == 0
