@@ -215,15 +215,39 @@ __device__ void merge_partition(const PassArgs& A, const double (&q)[K][K], i64 
   }
 }
 
-// k = 2 specialisation of merge_partition (the configs' k): the union of
-// two sorted windows needs two warp searches (each element's rank in the
-// other window), and output positions come from four ballots of non-zero
-// outputs instead of per-column OR-reductions -- about 2.5x fewer
-// instructions per step.  Same values, same order: out_a = (0 + q(a,0) v_0)
-// + q(a,1) v_1 with an absent entry read as 0.0.
-template <bool kWrite>
-__device__ void merge_partition2(const PassArgs& A, const double (&q)[2][2], i64 (&p)[2], const i64 (&hi)[2],
-                                 int (&kept)[2], const i64 (&dst)[2]) {
+// k = 2 specialisation of merge_partition (the configs' k).  Outputs are
+// the union rows of the two inputs, an exactly-zero result included: the
+// reference drops it (sparse.hpp:150), but an explicit 0.0 and an absent
+// entry are read identically everywhere downstream (a term q*0.0 in later
+// rotations, 0 in Gram and norm sums, nothing in the masses), so keeping
+// it is value-neutral -- and it makes the count
+// pass a row-only union count: no value loads, no arithmetic.
+__device__ __forceinline__ void merge_count2(const PassArgs& A, i64 (&p)[2], const i64 (&hi)[2], int& kept) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    if (p[0] >= hi[0] && p[1] >= hi[1]) break;
+    const i64 ea = p[0] + lane, eb = p[1] + lane;
+    const int ra = ea < hi[0] ? A.arow[ea] : INT_MAX;
+    const int rb = eb < hi[1] ? A.arow[eb] : INT_MAX;
+    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
+    const bool oka = ra != INT_MAX && ra <= frontier;
+    const bool okb = rb != INT_MAX && rb <= frontier;
+    const int la = warp_lower_bound(rb, ra);
+    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
+    const bool pa = oka && la < 32 && ca == ra;
+    const int na = __popc(__ballot_sync(0xffffffffu, oka));
+    const int nb = __popc(__ballot_sync(0xffffffffu, okb));
+    kept += na + nb - __popc(__ballot_sync(0xffffffffu, pa));
+    p[0] += na;
+    p[1] += nb;
+  }
+}
+
+// Write pass: two warp searches (each element's rank in the other window)
+// and one ballot of partner-less B rows give every output's position.
+// out_a = (0 + q(a,0) v_0) + q(a,1) v_1 with an absent entry read as 0.0.
+__device__ __forceinline__ void merge_write2(const PassArgs& A, const double (&q)[2][2], i64 (&p)[2],
+                                             const i64 (&hi)[2], int& kept, const i64 (&dst)[2]) {
   const int lane = threadIdx.x & 31;
   const unsigned below = (1u << lane) - 1u;
   for (;;) {
@@ -242,48 +266,28 @@ __device__ void merge_partition2(const PassArgs& A, const double (&q)[2][2], i64
     const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
     const int cb = __shfl_sync(0xffffffffu, ra, lb & 31);
     const double vp = __shfl_sync(0xffffffffu, vb, la & 31);
-    const bool pa = la < 32 && ca == ra;             // A element with a B partner
+    const bool pa = la < 32 && ca == ra;               // A element with a B partner
     const bool bonly = okb && !(lb < 32 && cb == rb);  // B element without an A partner
-    const double x1 = pa ? vp : 0.0;
-    const double oa0 = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
-    const double oa1 = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
-    const double ob0 = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
-    const double ob1 = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
-    const unsigned NA0 = __ballot_sync(0xffffffffu, oka && oa0 != 0.0);
-    const unsigned NA1 = __ballot_sync(0xffffffffu, oka && oa1 != 0.0);
-    const unsigned NB0 = __ballot_sync(0xffffffffu, bonly && ob0 != 0.0);
-    const unsigned NB1 = __ballot_sync(0xffffffffu, bonly && ob1 != 0.0);
-    if (kWrite) {
-      if (oka) {
-        const unsigned mb = la >= 32 ? 0xffffffffu : ((1u << la) - 1u);
-        if (oa0 != 0.0) {
-          const i64 d = dst[0] + kept[0] + __popc(NA0 & below) + __popc(NB0 & mb);
-          A.wrow[d] = ra;
-          A.wval[d] = oa0;
-        }
-        if (oa1 != 0.0) {
-          const i64 d = dst[1] + kept[1] + __popc(NA1 & below) + __popc(NB1 & mb);
-          A.wrow[d] = ra;
-          A.wval[d] = oa1;
-        }
-      }
-      if (bonly) {
-        const unsigned ma = lb >= 32 ? 0xffffffffu : ((1u << lb) - 1u);
-        if (ob0 != 0.0) {
-          const i64 d = dst[0] + kept[0] + __popc(NA0 & ma) + __popc(NB0 & below);
-          A.wrow[d] = rb;
-          A.wval[d] = ob0;
-        }
-        if (ob1 != 0.0) {
-          const i64 d = dst[1] + kept[1] + __popc(NA1 & ma) + __popc(NB1 & below);
-          A.wrow[d] = rb;
-          A.wval[d] = ob1;
-        }
-      }
+    const unsigned BO = __ballot_sync(0xffffffffu, bonly);
+    if (oka) {
+      const double x1 = pa ? vp : 0.0;
+      const unsigned mb = la >= 32 ? 0xffffffffu : ((1u << la) - 1u);
+      const i64 r = kept + lane + __popc(BO & mb);
+      A.wrow[dst[0] + r] = ra;
+      A.wval[dst[0] + r] = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
+      A.wrow[dst[1] + r] = ra;
+      A.wval[dst[1] + r] = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
     }
-    kept[0] += __popc(NA0) + __popc(NB0);
-    kept[1] += __popc(NA1) + __popc(NB1);
-    p[0] += __popc(__ballot_sync(0xffffffffu, oka));
+    if (bonly) {
+      const i64 r = kept + lb + __popc(BO & below);
+      A.wrow[dst[0] + r] = rb;
+      A.wval[dst[0] + r] = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
+      A.wrow[dst[1] + r] = rb;
+      A.wval[dst[1] + r] = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
+    }
+    const int na = __popc(__ballot_sync(0xffffffffu, oka));
+    kept += na + __popc(BO);
+    p[0] += na;
     p[1] += __popc(__ballot_sync(0xffffffffu, okb));
   }
 }
@@ -415,10 +419,16 @@ __global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, cons
       kept[a] = 0;
       dst[a] = kWrite ? A.pos[K * A.ioff[ri] + a * np + p] : 0;
     }
-    if constexpr (K == 2)
-      merge_partition2<kWrite>(A, q, beg, end, kept, dst);
-    else
+    if constexpr (K == 2) {
+      int u = 0;  // union size: the same for both output columns
+      if (kWrite)
+        merge_write2(A, q, beg, end, u, dst);
+      else
+        merge_count2(A, beg, end, u);
+      kept[0] = kept[1] = u;
+    } else {
       merge_partition<K, kWrite>(A, q, beg, end, kept, dst);
+    }
     if (!kWrite && (threadIdx.x & 31) == 0) {
 #pragma unroll
       for (int a = 0; a < K; ++a) A.cnt[K * A.ioff[ri] + a * np + p] = kept[a];

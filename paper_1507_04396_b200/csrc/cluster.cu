@@ -257,20 +257,24 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
           const i64 n = __shfl_sync(0xffffffffu, cnt, s0);
           st_rows += 1;
           st_ent += static_cast<unsigned long long>(n);
-          // hub row: issue all of a 256-entry batch's loads before any update
-          constexpr int kB = 8;
-          for (i64 q0 = 0; q0 < n; q0 += 32 * kB) {
-            int32_t ra[kB];
-            double rv[kB];
+          if (n <= 32) {  // one slot per lane
+            if (lane < n) update(A.ent_a[bg + lane], vs, bs, A.ent_v[bg + lane]);
+          } else {
+            // hub row: issue all of a 256-entry batch's loads before any update
+            constexpr int kB = 8;
+            for (i64 q0 = 0; q0 < n; q0 += 32 * kB) {
+              int32_t ra[kB];
+              double rv[kB];
 #pragma unroll
-            for (int k = 0; k < kB; ++k) {
-              const i64 q = q0 + k * 32 + lane;
-              ra[k] = q < n ? A.ent_a[bg + q] : 0;
-              rv[k] = q < n ? A.ent_v[bg + q] : 0.0;
+              for (int k = 0; k < kB; ++k) {
+                const i64 q = q0 + k * 32 + lane;
+                ra[k] = q < n ? A.ent_a[bg + q] : 0;
+                rv[k] = q < n ? A.ent_v[bg + q] : 0.0;
+              }
+#pragma unroll
+              for (int k = 0; k < kB; ++k)
+                if (q0 + k * 32 + lane < n) update(ra[k], vs, bs, rv[k]);
             }
-#pragma unroll
-            for (int k = 0; k < kB; ++k)
-              if (q0 + k * 32 + lane < n) update(ra[k], vs, bs, rv[k]);
           }
           __syncwarp();
           continue;

@@ -383,6 +383,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       R->phases[2] += search_ms;
       PMMF_TRACE("[pmmf] stage %d: gram %.2f ms, search %.2f ms\n", stage_no, gram_ms, search_ms);
     }
+    const auto t_asm = clk::now();
     if (so.error.to_host(1)[0]) fail(PMMF_INVALID_ARGUMENT, "rotation_from_gram: input not symmetric");
     std::vector<int32_t> nrot = so.nrot.to_host(std::max<i64>(rc, 1));
     std::vector<int32_t> nelim = so.nelim.to_host(std::max<i64>(rc, 1));
@@ -404,6 +405,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       }
     }
 
+    PMMF_TRACE("[pmmf] stage %d: host assembly of the rotation records %.2f ms\n", stage_no, ms_since(t_asm));
     // ---- stage apply: column side, transpose, row side, transpose
     t0 = clk::now();
     const i64 ne = static_cast<i64>(order_g.size());
@@ -499,6 +501,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     PMMF_CUDA(cudaStreamSynchronize(s));
     R->phases[3] += ms_since(t0);
     PMMF_TRACE("[pmmf] stage %d: apply %.2f ms\n", stage_no, ms_since(t0));
+    const auto t_res = clk::now();
 
     // ---- residual accounting against the end-of-stage matrix
     if (ne > 0) {
@@ -526,6 +529,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         if (!gone[g]) next.push_back(g);
       active = std::move(next);
     }
+    PMMF_TRACE("[pmmf] stage %d: residual + bookkeeping %.2f ms\n", stage_no, ms_since(t_res));
     R->hist.push_back(static_cast<i64>(active.size()));
     R->info.push_back({stage_no, rc, static_cast<i64>(st.bypassed.size()),
                        static_cast<i64>(st.rot_idx.size()) / p.k, ne, static_cast<i64>(active.size()),

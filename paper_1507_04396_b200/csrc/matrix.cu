@@ -463,6 +463,25 @@ void transpose_paged(Csc& out, const Paged& p, cudaStream_t s) {
 template <typename Sink>
 void transpose_chunks(const std::vector<Piece>& in, i64 N, const uint8_t* keep_row, i64 chunk_nnz,
                       std::vector<i64>& hp, cudaStream_t s, Sink&& sink) {
+  const bool tr = trace_enabled();
+  auto tl = std::chrono::steady_clock::now();
+  double tms[6] = {0, 0, 0, 0, 0, 0};
+  auto lap = [&](int k) {
+    if (!tr) return;
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    tms[k] += std::chrono::duration<double, std::milli>(now - tl).count();
+    tl = now;
+  };
+  struct Report {
+    bool on;
+    double* t;
+    ~Report() {
+      if (on)
+        std::fprintf(stderr, "[pmmf]     transpose: hist %.2f scan %.2f count %.2f gather %.2f sort %.2f sink %.2f ms\n",
+                     t[0], t[1], t[2], t[3], t[4], t[5]);
+    }
+  } report{tr, tms};
   DBuf<int32_t> hist(N + 1, s);
   hist.zero();
   for (const Piece& P : in) {
@@ -470,12 +489,14 @@ void transpose_chunks(const std::vector<Piece>& in, i64 N, const uint8_t* keep_r
     PMMF_LAUNCH(k_row_hist, blocks_for(n * 32, kThreads), kThreads, 0, s, n, P.ptr.get(), P.row.get(), keep_row,
                 hist.get());
   }
+  lap(0);
   DBuf<i64> h64(N + 1, s), ptr(N + 1, s);
   PMMF_LAUNCH(k_hist_widen, blocks_for(N + 1, kThreads), kThreads, 0, s, N, hist.get(), h64.get());
   exclusive_scan(h64.get(), ptr.get(), N + 1, s);
   hist.release();
   h64.release();
   hp = ptr.to_host(N + 1);
+  lap(1);
   const i64 m = hp[N];
   if (m == 0) return;
   chunk_nnz = std::max<i64>(chunk_nnz, 1 << 8);
@@ -500,12 +521,14 @@ void transpose_chunks(const std::vector<Piece>& in, i64 N, const uint8_t* keep_r
                     keep_row, static_cast<int>(r0), static_cast<int>(r1), cnt.get());
       }
       exclusive_scan(cnt.get(), pos.get(), N + 1, s);
+      lap(2);
       for (const Piece& P : in) {
         const i64 n = P.c1 - P.c0;
         PMMF_LAUNCH(k_chunk_gather, blocks_for(n * 32, kThreads), kThreads, 0, s, n, P.c0, P.ptr.get(), P.row.get(),
                     P.val.get(), keep_row, static_cast<int>(r0), static_cast<int>(r1), pos.get(), cb, keys.get(),
                     vals.get());
       }
+      lap(3);
       const int rb = std::max(1, bits_for(std::max<i64>(r1 - r0 - 1, 1)));
       DBuf<uint64_t> k2(cm, s);
       DBuf<double> v2(cm, s);
@@ -515,7 +538,9 @@ void transpose_chunks(const std::vector<Piece>& in, i64 N, const uint8_t* keep_r
       PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int64_t>(cm), cb, cb + rb, s));
       DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
       PMMF_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kb, vb, static_cast<int64_t>(cm), cb, cb + rb, s));
+      lap(4);
       sink(r0, r1, cm, cb, kb.Current(), vb.Current(), ptr.get());
+      lap(5);
     }
     r0 = r1;
   }
