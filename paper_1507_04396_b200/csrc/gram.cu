@@ -13,6 +13,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "engine.cuh"
 
@@ -104,6 +105,14 @@ __global__ void k_gram_owner(i64 col0, i64 ncols, i64 e0, const i64* __restrict_
   }
 }
 
+__global__ void k_run_total(i64 ne, const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
+                            unsigned long long* __restrict__ tot) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  unsigned long long v = i < ne ? static_cast<unsigned long long>(hi[i] - lo[i]) : 0ull;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0 && v) atomicAdd(tot, v);
+}
+
 // D[r][a] = D[a][r] = A[r][a] for the upper triangle r <= a of block (u,u).
 __global__ void k_diag_block(i64 col0, i64 ncols, const i64* __restrict__ ptr, const int32_t* __restrict__ row,
                              const double* __restrict__ val, const int32_t* __restrict__ col_cluster_off,
@@ -187,6 +196,13 @@ void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const
               dseg.get() + 1, a.val.get() + e0, run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get());
   PMMF_LAUNCH(k_gram_owner, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, e0, a.ptr.get(),
               a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco.get(), dct.get(), dcc.get(), G);
+  if (trace_enabled()) {  // products = sum over entries of their row-run length (the reference's count)
+    DBuf<unsigned long long> tot(1, s);
+    tot.zero();
+    PMMF_LAUNCH(k_run_total, blocks_for(ne, kThreads), kThreads, 0, s, ne, run_lo.get(), run_hi.get(), tot.get());
+    std::fprintf(stderr, "[pmmf]   gram: %lld columns, %lld entries, %llu products\n", static_cast<long long>(ncols),
+                 static_cast<long long>(ne), tot.to_host(1)[0]);
+  }
 }
 
 }  // namespace pmmf_b200
