@@ -216,6 +216,31 @@ struct AllocCheck {
   }
 };
 
+// Grow-only pinned host staging (device->host copies of the rotation records
+// run at full PCIe/C2C speed; pinned memory is never freed, so no implicit
+// device synchronisation).  A slot is held under its lock while in use.
+struct PinnedSlot {
+  std::mutex mu;
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* reserve(size_t n) {  // caller holds mu
+    if (n > bytes) {
+      void* q = nullptr;
+      if (cudaHostAlloc(&q, n, cudaHostAllocDefault) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return nullptr;
+      }
+      p = q;  // the previous block is kept (never freed): no implicit sync
+      bytes = n;
+    }
+    return p;
+  }
+  static PinnedSlot& get(int i) {
+    static PinnedSlot slots[4];
+    return slots[i & 3];
+  }
+};
+
 // Reusable timing events for the profiled passes (creating and destroying
 // two events per dependency level would itself cost ~10 us a level).
 struct EventPool {

@@ -12,6 +12,7 @@
 // active list, the partitions, the RNG stream of the clustering, and the
 // materialised outputs (rotations, eliminations).
 #include <algorithm>
+#include <future>
 #include <array>
 #include <chrono>
 #include <cmath>
@@ -387,22 +388,66 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     if (so.error.to_host(1)[0]) fail(PMMF_INVALID_ARGUMENT, "rotation_from_gram: input not symmetric");
     std::vector<int32_t> nrot = so.nrot.to_host(std::max<i64>(rc, 1));
     std::vector<int32_t> nelim = so.nelim.to_host(std::max<i64>(rc, 1));
-    std::vector<int32_t> rot_loc = so.rot_loc.to_host(std::max<i64>(slots * p.k, 1));
-    std::vector<double> rot_q = so.rot_q.to_host(std::max<i64>(slots * p.k * p.k, 1));
     std::vector<int32_t> elim_loc = so.elim_loc.to_host(std::max<i64>(slots, 1));
     std::vector<int32_t> order_sid;  // eliminated stage ids, stage elimination order
     std::vector<int32_t> order_g;
-    for (i64 u = 0; u < rc; ++u) {
-      for (i64 t = 0; t < nrot[u]; ++t) {
-        const i64 sl = out_base[u] + t;
-        for (int a = 0; a < p.k; ++a) st.rot_idx.push_back(cur.s2g[cur.off[u] + rot_loc[sl * p.k + a]]);
-        st.rot_q.insert(st.rot_q.end(), rot_q.begin() + sl * p.k * p.k, rot_q.begin() + (sl + 1) * p.k * p.k);
-      }
+    for (i64 u = 0; u < rc; ++u)
       for (i64 e = 0; e < nelim[u]; ++e) {
         const i64 sid = cur.off[u] + elim_loc[out_base[u] + e];
         order_sid.push_back(static_cast<int32_t>(sid));
         order_g.push_back(static_cast<int32_t>(cur.s2g[sid]));
       }
+    // The rotation records (global ids, k x k blocks) are only reported:
+    // a worker thread copies them through pinned staging on a side stream and
+    // assembles them while the device runs the stage apply (which reads the
+    // same device arrays, never writes them).
+    std::future<void> records;
+    {
+      int dev = 0;
+      PMMF_CUDA(cudaGetDevice(&dev));
+      cudaEvent_t ready = nullptr;
+      PMMF_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+      PMMF_CUDA(cudaEventRecord(ready, s));
+      const int32_t* d_loc = so.rot_loc.get();
+      const double* d_q = so.rot_q.get();
+      const int k = p.k;
+      records = std::async(std::launch::async, [&st, &nrot, &out_base, &cur, rc, slots, k, d_loc, d_q, ready, dev]() {
+        PMMF_CUDA(cudaSetDevice(dev));
+        cudaStream_t side = nullptr;
+        PMMF_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        PMMF_CUDA(cudaStreamWaitEvent(side, ready, 0));
+        const size_t nl = static_cast<size_t>(std::max<i64>(slots * k, 1));
+        const size_t nq = static_cast<size_t>(std::max<i64>(slots * k * k, 1));
+        PinnedSlot& pl = PinnedSlot::get(0);
+        PinnedSlot& pq = PinnedSlot::get(1);
+        std::lock_guard<std::mutex> gl(pl.mu), gq(pq.mu);
+        auto* hl = static_cast<int32_t*>(pl.reserve(nl * sizeof(int32_t)));
+        auto* hq = static_cast<double*>(pq.reserve(nq * sizeof(double)));
+        std::vector<int32_t> vl;
+        std::vector<double> vq;
+        if (!hl || !hq) {  // no pinned memory: pageable copies
+          vl.resize(nl);
+          vq.resize(nq);
+          hl = vl.data();
+          hq = vq.data();
+        }
+        PMMF_CUDA(cudaMemcpyAsync(hl, d_loc, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, side));
+        PMMF_CUDA(cudaMemcpyAsync(hq, d_q, nq * sizeof(double), cudaMemcpyDeviceToHost, side));
+        PMMF_CUDA(cudaStreamSynchronize(side));
+        cudaStreamDestroy(side);
+        cudaEventDestroy(ready);
+        i64 total = 0;
+        for (i64 u = 0; u < rc; ++u) total += nrot[u];
+        st.rot_idx.resize(static_cast<size_t>(total * k));
+        st.rot_q.resize(static_cast<size_t>(total * k * k));
+        i64 w = 0;
+        for (i64 u = 0; u < rc; ++u)
+          for (i64 t = 0; t < nrot[u]; ++t, ++w) {
+            const i64 sl = out_base[u] + t;
+            for (int a = 0; a < k; ++a) st.rot_idx[w * k + a] = cur.s2g[cur.off[u] + hl[sl * k + a]];
+            std::copy(hq + sl * k * k, hq + (sl + 1) * k * k, st.rot_q.begin() + w * k * k);
+          }
+      });
     }
 
     PMMF_TRACE("[pmmf] stage %d: host assembly of the rotation records %.2f ms\n", stage_no, ms_since(t_asm));
@@ -511,11 +556,24 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
                     A.val.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(), diag.get());
         PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
       }
-      std::vector<double> hm = mass.to_host(ne), hd = diag.to_host(ne);
+      PinnedSlot& ps = PinnedSlot::get(2);
+      std::lock_guard<std::mutex> lk(ps.mu);
+      auto* hmd = static_cast<double*>(ps.reserve(sizeof(double) * 2 * static_cast<size_t>(ne)));
+      std::vector<double> fallback;
+      if (!hmd) {
+        fallback.resize(2 * static_cast<size_t>(ne));
+        hmd = fallback.data();
+      }
+      PMMF_CUDA(cudaMemcpyAsync(hmd, mass.get(), sizeof(double) * ne, cudaMemcpyDeviceToHost, s));
+      PMMF_CUDA(cudaMemcpyAsync(hmd + ne, diag.get(), sizeof(double) * ne, cudaMemcpyDeviceToHost, s));
+      PMMF_CUDA(cudaStreamSynchronize(s));
+      const double* hm = hmd;
+      const double* hd = hmd + ne;
+      st.elim_idx.assign(order_g.begin(), order_g.end());
+      st.elim_diag.assign(hd, hd + ne);
+      st.elim_mass.assign(hm, hm + ne);
+      R->diag.reserve(R->diag.size() + static_cast<size_t>(ne));
       for (i64 r = 0; r < ne; ++r) {
-        st.elim_idx.push_back(order_g[r]);
-        st.elim_diag.push_back(hd[r]);
-        st.elim_mass.push_back(hm[r]);
         R->residual_sq += 2.0 * hm[r];
         R->diag.push_back({order_g[r], hd[r]});
       }
@@ -529,6 +587,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         if (!gone[g]) next.push_back(g);
       active = std::move(next);
     }
+    records.get();  // rotation records assembled (rethrows a copy failure)
     PMMF_TRACE("[pmmf] stage %d: residual + bookkeeping %.2f ms\n", stage_no, ms_since(t_res));
     R->hist.push_back(static_cast<i64>(active.size()));
     R->info.push_back({stage_no, rc, static_cast<i64>(st.bypassed.size()),
