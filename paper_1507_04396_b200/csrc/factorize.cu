@@ -172,6 +172,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       thr = static_cast<uint64_t>(std::atof(e) * 1073741824.0);
     PMMF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
   }
+  const auto fn_start = clk::now();
   StreamGuard sg;
   cudaStream_t s = sg.s;
   const i64 n = in->n;
@@ -223,6 +224,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   }
 
   const auto run_start = clk::now();
+  PMMF_TRACE("[pmmf] prologue (input numbering, from_triplets, symmetry) %.2f ms\n", ms_since(fn_start));
   std::vector<i64> active;
   for (i64 g = 0; g < n; ++g)
     if (cur.g2s[g] >= 0) active.push_back(g);
@@ -239,6 +241,9 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
 
   for (int stage_no = 1; stage_no <= p.n_stages && !R->trivial; ++stage_no) {
     if (static_cast<i64>(active.size()) <= p.core_min) break;
+    const auto t_stage = clk::now();
+    double ph0[5];
+    std::copy(R->phases, R->phases + 5, ph0);
     // ---- clustering on the pre-reblock matrix
     auto t0 = clk::now();
     const uint64_t cpath[2] = {0xC1u, static_cast<uint64_t>(stage_no)};
@@ -589,6 +594,12 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     }
     records.get();  // rotation records assembled (rethrows a copy failure)
     PMMF_TRACE("[pmmf] stage %d: residual + bookkeeping %.2f ms\n", stage_no, ms_since(t_res));
+    if (trace_on()) {
+      double in_phases = 0.0;
+      for (int i = 0; i < 5; ++i) in_phases += R->phases[i] - ph0[i];
+      PMMF_TRACE("[pmmf] stage %d: wall %.2f ms, outside the five phases %.2f ms\n", stage_no, ms_since(t_stage),
+                 ms_since(t_stage) - in_phases);
+    }
     R->hist.push_back(static_cast<i64>(active.size()));
     R->info.push_back({stage_no, rc, static_cast<i64>(st.bypassed.size()),
                        static_cast<i64>(st.rot_idx.size()) / p.k, ne, static_cast<i64>(active.size()),
@@ -617,9 +628,23 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
                 dpos.get(), dcore.get());
     R->core = dcore.to_host(g * g);
   }
-  std::sort(R->diag.begin(), R->diag.end());
+  {
+    // order by global index (each retired index appears once): a counting
+    // placement instead of an O(n log n) sort of ~10^6 pairs
+    std::vector<double> dv(static_cast<size_t>(n), 0.0);
+    std::vector<uint8_t> has(static_cast<size_t>(n), 0);
+    for (const auto& [idx, v] : R->diag) {
+      dv[idx] = v;
+      has[idx] = 1;
+    }
+    size_t w = 0;
+    for (i64 idx = 0; idx < n; ++idx)
+      if (has[idx]) R->diag[w++] = {idx, dv[idx]};
+    if (w != R->diag.size()) fail(PMMF_INTERNAL, "factorize: an index was retired twice");
+  }
   PMMF_CUDA(cudaStreamSynchronize(s));
   R->phases[5] = ms_since(run_start);
+  PMMF_TRACE("[pmmf] factorize total %.2f ms (stage loop + core %.2f ms)\n", ms_since(fn_start), R->phases[5]);
   return R;
 }
 
