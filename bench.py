@@ -212,7 +212,10 @@ def main():
     d_vals = torch.from_numpy(vals).cuda()
     torch.cuda.synchronize()
     coo_dev, keep_dev = abi.make_coo(n, d_rows, d_cols, d_vals, on_device=True, device=local)
-    coo_host, keep_host = abi.make_coo(n, rows, cols, vals, device=local)
+    # e2e input: host buffers in pinned memory (the contract's "copy of that
+    # step's inputs from pinned host memory"), copied by the library each step
+    pinned = [torch.from_numpy(x).pin_memory() for x in (rows, cols, vals)]
+    coo_host, keep_host = abi.make_coo(n, *(t.numpy() for t in pinned), device=local)
     err = lib.errbuf()
 
     last_phases = np.zeros(6)
