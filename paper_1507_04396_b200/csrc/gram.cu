@@ -123,45 +123,153 @@ __global__ void k_diag_block(i64 col0, i64 ncols, const i64* __restrict__ ptr, c
   }
 }
 
-}  // namespace
+// ------------------------------------------------------------ dense path
+// A cluster whose columns are well filled is summed as a dense SYRK: its
+// columns are scattered into a zero-filled column-major panel (ld = N, rows
+// in stage order) and every output G[a][b] is accumulated by one thread
+// over the rows strictly in ascending order with separately rounded
+// products and sums -- the reference's sequence with exact-zero products
+// inserted for rows where one side is absent.  0 + p = p, s + (+-0) = s for
+// s != 0, so the value is the reference's up to the sign of an exact zero,
+// which nothing downstream observes.
 
-void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const std::vector<i64>& tile_off,
-                double* G, double* D, cudaStream_t s) {
-  const i64 col0 = off[u0], ncols = off[u1] - off[u0];
-  if (ncols <= 0) return;
-  std::vector<i64> hptr(2);
-  PMMF_CUDA(cudaMemcpyAsync(&hptr[0], a.ptr.get() + col0, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  PMMF_CUDA(cudaMemcpyAsync(&hptr[1], a.ptr.get() + col0 + ncols, sizeof(i64), cudaMemcpyDeviceToHost, s));
-  // per-column cluster info
-  std::vector<int32_t> cco(static_cast<size_t>(ncols)), cc(static_cast<size_t>(ncols));
-  std::vector<int64_t> ct(static_cast<size_t>(ncols));
-  for (i64 u = u0; u < u1; ++u)
-    for (i64 J = off[u]; J < off[u + 1]; ++J) {
-      cco[J - col0] = static_cast<int32_t>(off[u]);
-      cc[J - col0] = static_cast<int32_t>(off[u + 1] - off[u]);
-      ct[J - col0] = tile_off[u] - tile_off[u0];
+__global__ void k_panel_scatter(i64 col0, i64 ncols, i64 N, const i64* __restrict__ ptr,
+                                const int32_t* __restrict__ row, const double* __restrict__ val,
+                                double* __restrict__ panel) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= ncols) return;
+  double* P = panel + w * N;
+  const i64 J = col0 + w;
+  for (i64 e = ptr[J] + lane; e < ptr[J + 1]; e += 32) P[row[e]] = val[e];
+}
+
+struct DenseTile {
+  int64_t pcol;   // panel column of the cluster's first member
+  int64_t gtile;  // tile offset of the cluster in G
+  int32_t c;      // cluster size
+  int32_t bi, bj; // output tile (bi <= bj)
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool pred) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const int n = pred ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// 256 threads, tile BM = 16*TM outputs square, KC rows per smem stage,
+// two-stage cp.async pipeline.  Thread (ty, tx) owns rows a in
+// {ty*4 + 64*h + i} and columns b in {tx*4 + 64*h + j} (TM = 8) or
+// {ty*4 + i} x {tx*4 + j} (TM = 4).
+template <int TM>
+__global__ void __launch_bounds__(256) k_syrk_seq(const DenseTile* __restrict__ tiles, i64 N,
+                                                  const double* __restrict__ panel, double* __restrict__ G) {
+  constexpr int BM = 16 * TM;
+  constexpr int KC = 16;
+  constexpr int LD = BM + 4;  // 32-byte aligned rows
+  constexpr int PER = KC * BM / 256;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                 // [2][KC][LD]
+  double* Bs = smem + 2 * KC * LD;   // [2][KC][LD]
+  const DenseTile t = tiles[blockIdx.x];
+  const int c = t.c;
+  const int a0 = t.bi * BM, b0 = t.bj * BM;
+  const double* Pa = panel + (t.pcol + a0) * N;
+  const double* Pb = panel + (t.pcol + b0) * N;
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;
+
+  auto load = [&](int st, i64 r0) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int idx = tid + 256 * i;
+      const int k = idx & (KC - 1), x = idx / KC;
+      const bool rk = r0 + k < N;
+      const bool pa = rk && a0 + x < c, pb = rk && b0 + x < c;
+      cp_async8(As + (st * KC + k) * LD + x, pa ? Pa + static_cast<i64>(x) * N + r0 + k : Pa, pa);
+      cp_async8(Bs + (st * KC + k) * LD + x, pb ? Pb + static_cast<i64>(x) * N + r0 + k : Pb, pb);
     }
-  DBuf<int32_t> dcco(ncols, s), dcc(ncols, s);
-  DBuf<int64_t> dct(ncols, s);
-  dcco.upload(cco);
-  dcc.upload(cc);
-  dct.upload(ct);
-  PMMF_CUDA(cudaStreamSynchronize(s));
-  const i64 e0 = hptr[0], ne = hptr[1] - hptr[0];
-  PMMF_LAUNCH(k_diag_block, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, a.ptr.get(), a.row.get(),
-              a.val.get(), dcco.get(), dct.get(), dcc.get(), D);
-  if (ne <= 0) return;
+    cp_async_commit();
+  };
+
+  double acc[TM][TM];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TM; ++j) acc[i][j] = 0.0;
+
+  const i64 nchunks = (N + KC - 1) / KC;
+  load(0, 0);
+  for (i64 ch = 0; ch < nchunks; ++ch) {
+    const int st = static_cast<int>(ch & 1);
+    if (ch + 1 < nchunks) {
+      load(st ^ 1, (ch + 1) * KC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* Ak = As + st * KC * LD;
+    const double* Bk = Bs + st * KC * LD;
+#pragma unroll 4
+    for (int k = 0; k < KC; ++k) {
+      double av[TM], bv[TM];
+#pragma unroll
+      for (int h = 0; h < TM / 4; ++h) {
+        const double2 x0 = *reinterpret_cast<const double2*>(Ak + k * LD + ty * 4 + 64 * h);
+        const double2 x1 = *reinterpret_cast<const double2*>(Ak + k * LD + ty * 4 + 64 * h + 2);
+        const double2 y0 = *reinterpret_cast<const double2*>(Bk + k * LD + tx * 4 + 64 * h);
+        const double2 y1 = *reinterpret_cast<const double2*>(Bk + k * LD + tx * 4 + 64 * h + 2);
+        av[4 * h] = x0.x; av[4 * h + 1] = x0.y; av[4 * h + 2] = x1.x; av[4 * h + 3] = x1.y;
+        bv[4 * h] = y0.x; bv[4 * h + 1] = y0.y; bv[4 * h + 2] = y1.x; bv[4 * h + 3] = y1.y;
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TM; ++j) acc[i][j] = dadd(acc[i][j], dmul(av[i], bv[j]));
+    }
+    __syncthreads();
+  }
+  double* Gt = G + t.gtile;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int a = a0 + ty * 4 + 64 * (i / 4) + (i & 3);
+    if (a >= c) continue;
+#pragma unroll
+    for (int j = 0; j < TM; ++j) {
+      const int b = b0 + tx * 4 + 64 * (j / 4) + (j & 3);
+      if (b >= c) continue;
+      Gt[static_cast<i64>(b) * c + a] = acc[i][j];
+      if (t.bi != t.bj) Gt[static_cast<i64>(a) * c + b] = acc[i][j];
+    }
+  }
+}
+
+__global__ void k_ptr_at(i64 n, const i64* __restrict__ ptr, const i64* __restrict__ cols, i64* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = ptr[cols[i]];
+}
+
+// Sparse path over the contiguous clusters [v0, v1) (column arrays indexed
+// from the batch's first column, offset by cbase).
+void gram_sparse(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 e0, i64 ne, const int32_t* dcco,
+                 const int64_t* dct, const int32_t* dcc, double* G, cudaStream_t s) {
+  const i64 col0 = off[v0], ncols = off[v1] - off[v0];
+  if (ncols <= 0 || ne <= 0) return;
   if (ne >= (i64{1} << 31)) fail(PMMF_INTERNAL, "gram: cluster batch exceeds 2^31 entries");
-  // One stable radix sort on (cluster index in the batch, row) keeps the
+  // One stable radix sort on (cluster index in the run, row) keeps the
   // columns ascending inside a run; a run is a row's entries inside the
   // owner column's own cluster.
   const i64 N = a.N;
-  const i64 nseg = u1 - u0;
+  const i64 nseg = v1 - v0;
   const int rb = std::max(1, bits_for(std::max<i64>(N - 1, 1)));
   const int sb = std::max(1, bits_for(std::max<i64>(nseg - 1, 1)));
   std::vector<int32_t> seg(static_cast<size_t>(ncols));
-  for (i64 u = u0; u < u1; ++u)
-    for (i64 J = off[u]; J < off[u + 1]; ++J) seg[J - col0] = static_cast<int32_t>(u - u0);
+  for (i64 u = v0; u < v1; ++u)
+    for (i64 J = off[u]; J < off[u + 1]; ++J) seg[J - col0] = static_cast<int32_t>(u - v0);
   DBuf<int32_t> dseg(ncols, s);
   dseg.upload(seg);
   DBuf<int32_t> idx(ne, s), idx2(ne, s), ecol(ne, s), run_lo(ne, s), run_hi(ne, s);
@@ -191,13 +299,152 @@ void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const
   idx2.release();
   ecol.release();
   PMMF_LAUNCH(k_gram_owner, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, e0, a.ptr.get(),
-              a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco.get(), dct.get(), dcc.get(), G);
+              a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco, dct, dcc, G);
   if (trace_enabled()) {  // products = sum over entries of their row-run length (the reference's count)
     DBuf<unsigned long long> tot(1, s);
     tot.zero();
     PMMF_LAUNCH(k_run_total, blocks_for(ne, kThreads), kThreads, 0, s, ne, run_lo.get(), run_hi.get(), tot.get());
-    std::fprintf(stderr, "[pmmf]   gram: %lld columns, %lld entries, %llu products\n", static_cast<long long>(ncols),
-                 static_cast<long long>(ne), tot.to_host(1)[0]);
+    std::fprintf(stderr, "[pmmf]   gram sparse: %lld columns, %lld entries, %llu products\n",
+                 static_cast<long long>(ncols), static_cast<long long>(ne), tot.to_host(1)[0]);
+  }
+}
+
+// Dense path over clusters [v0, v1): one panel, one SYRK launch.
+void gram_dense(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 u0, const std::vector<i64>& tile_off,
+                double* G, cudaStream_t s) {
+  const i64 col0 = off[v0], ncols = off[v1] - off[v0], N = a.N;
+  if (ncols <= 0) return;
+  i64 max_c = 0;
+  for (i64 u = v0; u < v1; ++u) max_c = std::max(max_c, off[u + 1] - off[u]);
+  // TM = 8 (128-wide tiles) unless that leaves the SMs short of work.
+  auto count_tiles = [&](int bm) {
+    i64 n = 0;
+    for (i64 u = v0; u < v1; ++u) {
+      const i64 nt = (off[u + 1] - off[u] + bm - 1) / bm;
+      n += nt * (nt + 1) / 2;
+    }
+    return n;
+  };
+  const int tm = count_tiles(128) >= 2 * 148 ? 8 : 4;
+  const int bm = 16 * tm;
+  std::vector<DenseTile> tl;
+  for (i64 u = v0; u < v1; ++u) {
+    const i64 c = off[u + 1] - off[u];
+    const i64 nt = (c + bm - 1) / bm;
+    for (i64 bj = 0; bj < nt; ++bj)
+      for (i64 bi = 0; bi <= bj; ++bi)
+        tl.push_back({off[u] - col0, tile_off[u] - tile_off[u0], static_cast<int32_t>(c), static_cast<int32_t>(bi),
+                      static_cast<int32_t>(bj)});
+  }
+  if (tl.empty()) return;
+  DBuf<double> panel(ncols * N, s);
+  panel.zero();
+  PMMF_LAUNCH(k_panel_scatter, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, N, a.ptr.get(),
+              a.row.get(), a.val.get(), panel.get());
+  DBuf<DenseTile> dtl(static_cast<i64>(tl.size()), s);
+  PMMF_CUDA(cudaMemcpyAsync(dtl.get(), tl.data(), sizeof(DenseTile) * tl.size(), cudaMemcpyHostToDevice, s));
+  const size_t smem = sizeof(double) * 2 * 2 * 16 * (bm + 4);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof_enabled()) {
+    e0 = EventPool::get().take();
+    e1 = EventPool::get().take();
+    cudaEventRecord(e0, s);
+  }
+  if (tm == 8) {
+    PMMF_CUDA(cudaFuncSetAttribute(k_syrk_seq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    PMMF_LAUNCH(k_syrk_seq<8>, static_cast<unsigned>(tl.size()), 256, smem, s, dtl.get(), N, panel.get(), G);
+  } else {
+    PMMF_CUDA(cudaFuncSetAttribute(k_syrk_seq<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    PMMF_LAUNCH(k_syrk_seq<4>, static_cast<unsigned>(tl.size()), 256, smem, s, dtl.get(), N, panel.get(), G);
+  }
+  double flops = 0.0;  // R_u * c_u * (c_u + 1) per cluster
+  for (i64 u = v0; u < v1; ++u) {
+    const double c = static_cast<double>(off[u + 1] - off[u]);
+    flops += static_cast<double>(N) * c * (c + 1.0);
+  }
+  if (e0) {
+    cudaEventRecord(e1, s);
+    PMMF_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    EventPool::get().give(e0);
+    EventPool::get().give(e1);
+    prof_add_n("gram_dense", 1, ms, flops);
+  }
+  if (trace_enabled()) {
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    std::fprintf(stderr, "[pmmf]   gram dense: %lld clusters, %lld columns x %lld rows, %zu tiles of %d, %.3g flop\n",
+                 static_cast<long long>(v1 - v0), static_cast<long long>(ncols), static_cast<long long>(N), tl.size(),
+                 bm, flops);
+  }
+}
+
+// Dense-vs-sparse choice: the sparse path costs ~ sum_r deg_u(r)^2 >= nnz_u^2 / N
+// scattered read-modify-writes, the dense one N c (c+1) / 2 register MACs.
+double dense_ratio() {
+  if (const char* e = std::getenv("PMMF_B200_GRAM_DENSE_RATIO")) return std::atof(e);  // test hook / tuning
+  return 32.0;
+}
+
+}  // namespace
+
+void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const std::vector<i64>& tile_off,
+                double* G, double* D, cudaStream_t s) {
+  const i64 col0 = off[u0], ncols = off[u1] - off[u0];
+  if (ncols <= 0) return;
+  const i64 nb = u1 - u0;
+  // per-column cluster info
+  std::vector<int32_t> cco(static_cast<size_t>(ncols)), cc(static_cast<size_t>(ncols));
+  std::vector<int64_t> ct(static_cast<size_t>(ncols));
+  for (i64 u = u0; u < u1; ++u)
+    for (i64 J = off[u]; J < off[u + 1]; ++J) {
+      cco[J - col0] = static_cast<int32_t>(off[u]);
+      cc[J - col0] = static_cast<int32_t>(off[u + 1] - off[u]);
+      ct[J - col0] = tile_off[u] - tile_off[u0];
+    }
+  DBuf<int32_t> dcco(ncols, s), dcc(ncols, s);
+  DBuf<int64_t> dct(ncols, s);
+  dcco.upload(cco);
+  dcc.upload(cc);
+  dct.upload(ct);
+  // entry offsets at the cluster boundaries
+  std::vector<i64> eptr;
+  {
+    DBuf<i64> cols(nb + 1, s), at(nb + 1, s);
+    cols.upload(off.data() + u0, nb + 1);
+    PMMF_LAUNCH(k_ptr_at, blocks_for(nb + 1, kThreads), kThreads, 0, s, nb + 1, a.ptr.get(), cols.get(), at.get());
+    eptr = at.to_host(nb + 1);
+  }
+  PMMF_LAUNCH(k_diag_block, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, a.ptr.get(), a.row.get(),
+              a.val.get(), dcco.get(), dct.get(), dcc.get(), D);
+  const double ratio = dense_ratio();
+  const double N = static_cast<double>(a.N);
+  // dense panels are bounded by a share of free memory
+  const i64 panel_cap = std::max<i64>(i64{1} << 24, available_bytes() / 4 / 8);
+  auto is_dense = [&](i64 u) {
+    const double c = static_cast<double>(off[u + 1] - off[u]);
+    const double nz = static_cast<double>(eptr[u + 1 - u0] - eptr[u - u0]);
+    return ratio > 0.0 && nz > 0.0 && N * c * (c + 1.0) * 0.5 <= ratio * nz * nz / N &&
+           static_cast<i64>(c) * a.N <= panel_cap;
+  };
+  i64 v0 = u0;
+  while (v0 < u1) {
+    const bool dense = is_dense(v0);
+    i64 v1 = v0 + 1;
+    if (dense) {
+      i64 cols = off[v0 + 1] - off[v0];
+      while (v1 < u1 && is_dense(v1) && (cols + off[v1 + 1] - off[v1]) * a.N <= panel_cap) {
+        cols += off[v1 + 1] - off[v1];
+        ++v1;
+      }
+      gram_dense(a, off, v0, v1, u0, tile_off, G, s);
+    } else {
+      while (v1 < u1 && !is_dense(v1)) ++v1;
+      const i64 w = off[v0] - col0;
+      gram_sparse(a, off, v0, v1, eptr[v0 - u0], eptr[v1 - u0] - eptr[v0 - u0], dcco.get() + w, dct.get() + w,
+                  dcc.get() + w, G, s);
+    }
+    v0 = v1;
   }
 }
 

@@ -38,6 +38,7 @@ int guarded(char* err, size_t errlen, F&& f) {
 
 constexpr int kThreads = 256;
 constexpr size_t kSmemBudget = 200 * 1024;
+constexpr size_t kSmemTwoPerSm = 112 * 1024;
 
 // ------------------------------------------------------------- host Jacobi
 // jacobi_eigensystem (dense.hpp:144-199) for the g x g core, row-major.
@@ -165,6 +166,92 @@ __global__ void k_stage_apply(int k, int nrhs, int rc, const int64_t* __restrict
       const int64_t li = i / nr, r = i % nr;
       V[static_cast<int64_t>(members[off + li]) * nrhs + r0 + r] = sm[li * rc + r];
     }
+  }
+}
+
+// Fast path for k = 2, 3 (configs 1-5): same arithmetic as k_stage_apply,
+// but the rotation record (local positions + q) of a thread's first item in
+// the NEXT level is loaded into registers before the current level's work,
+// so the dependent global loads overlap the level instead of following its
+// barrier.  The slice always lives in shared memory (run_stage sizes rc).
+template <int K, bool kTransposed>
+__global__ void __launch_bounds__(256) k_stage_apply_k(int nrhs, int rc, const int64_t* __restrict__ coff,
+                                                       const int32_t* __restrict__ members,
+                                                       const int64_t* __restrict__ rot_ptr,
+                                                       const int64_t* __restrict__ lvl_ptr,
+                                                       const int64_t* __restrict__ lvl_base,
+                                                       const int32_t* __restrict__ nlev,
+                                                       const int32_t* __restrict__ loc,
+                                                       const double* __restrict__ qs, double* __restrict__ V) {
+  extern __shared__ double sm[];
+  const int u = blockIdx.x;
+  const int r0 = blockIdx.y * rc;
+  const int nr = min(rc, nrhs - r0);
+  if (rot_ptr[u + 1] == rot_ptr[u] || nr <= 0) return;
+  const int64_t off = coff[u];
+  const int c = static_cast<int>(coff[u + 1] - off);
+  const int L = nlev[u];
+  const int64_t* lp = lvl_ptr + lvl_base[u];
+  for (int i = threadIdx.x; i < c * nr; i += blockDim.x) {
+    const int li = i / nr, r = i - li * nr;
+    sm[li * rc + r] = V[static_cast<int64_t>(members[off + li]) * nrhs + r0 + r];
+  }
+  struct Rec {
+    int a[K];
+    double q[K * K];
+  };
+  auto fetch = [&](int64_t t, Rec& x) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) x.a[j] = loc[t * K + j];
+#pragma unroll
+    for (int j = 0; j < K * K; ++j) x.q[j] = qs[t * K * K + j];
+  };
+  auto rotate = [&](const Rec& x, int r) {
+    double v[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) v[j] = sm[x.a[j] * rc + r];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc = dadd(acc, dmul(kTransposed ? x.q[j * K + a] : x.q[a * K + j], v[j]));
+      sm[x.a[a] * rc + r] = acc;
+    }
+  };
+  auto level_range = [&](int lv, int64_t& b, int64_t& e) {
+    const int l = kTransposed ? (L - 1 - lv) : lv;
+    b = lp[l];
+    e = lp[l + 1];
+  };
+  Rec cur, nxt;
+  int64_t b, e;
+  level_range(0, b, e);
+  bool have = threadIdx.x < (e - b) * nr;
+  if (have) fetch(b + threadIdx.x / nr, cur);
+  __syncthreads();
+  for (int lv = 0; lv < L; ++lv) {
+    int64_t nb = 0, ne = 0;
+    bool nhave = false;
+    if (lv + 1 < L) {
+      level_range(lv + 1, nb, ne);
+      nhave = threadIdx.x < (ne - nb) * nr;
+      if (nhave) fetch(nb + threadIdx.x / nr, nxt);
+    }
+    if (have) rotate(cur, threadIdx.x % nr);
+    for (int64_t i = threadIdx.x + blockDim.x; i < (e - b) * nr; i += blockDim.x) {  // wide levels
+      Rec x;
+      fetch(b + i / nr, x);
+      rotate(x, static_cast<int>(i % nr));
+    }
+    __syncthreads();
+    cur = nxt;
+    have = nhave;
+    b = nb;
+    e = ne;
+  }
+  for (int i = threadIdx.x; i < c * nr; i += blockDim.x) {
+    const int li = i / nr, r = i - li * nr;
+    V[static_cast<int64_t>(members[off + li]) * nrhs + r0 + r] = sm[li * rc + r];
   }
 }
 
@@ -368,6 +455,27 @@ struct Operator {
 
   void run_stage(const StageDev& sd, bool transposed, int nrhs, double* V, cudaStream_t st) const {
     if (sd.nclusters == 0) return;
+    if (k == 2 || k == 3) {
+      // rhs per CTA: as many as fit two CTAs per SM (<= 8), else one CTA
+      // per SM with the largest slice that fits.
+      const size_t row = static_cast<size_t>(sd.max_c) * 8;
+      int rc = std::min(nrhs, 8);
+      while (rc > 1 && row * rc > kSmemTwoPerSm) --rc;
+      if (row * rc <= kSmemBudget) {
+        const size_t smem = row * rc;
+        dim3 grid(static_cast<unsigned>(sd.nclusters), static_cast<unsigned>((nrhs + rc - 1) / rc));
+        auto kern = k == 2 ? (transposed ? k_stage_apply_k<2, true> : k_stage_apply_k<2, false>)
+                           : (transposed ? k_stage_apply_k<3, true> : k_stage_apply_k<3, false>);
+        if (smem > 48 * 1024)
+          PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<grid, kThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
+                                           sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
+                                           sd.q.get(), V);
+        launch_counter().fetch_add(1, std::memory_order_relaxed);
+        PMMF_CUDA(cudaGetLastError());
+        return;
+      }
+    }
     int rc = std::min(nrhs, 8);
     while (rc > 1 && static_cast<size_t>(sd.max_c) * rc * 8 > kSmemBudget) rc >>= 1;
     const bool smem_ok = static_cast<size_t>(sd.max_c) * rc * 8 <= kSmemBudget;

@@ -53,3 +53,16 @@ def test_cluster_search_path(name, csize, monkeypatch):
     monkeypatch.setenv("PMMF_B200_SEARCH_FORCE_W", csize)
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf256_k3", "rbf512_k4",
+                                  "zero_cols_bypass", "partitioned_input", "k3_sparse", "dups_and_zeros",
+                                  "undersize_repair", "c1_dense1024"])
+@pytest.mark.parametrize("ratio", ["1e30", "0"])
+def test_gram_paths(name, ratio, monkeypatch):
+    """Every cluster's Gram through the dense sequential SYRK (ratio=1e30:
+    zero-filled panels, exact-zero products inserted) or through the sparse
+    row-run path (ratio=0) — both bit-exact against the oracle."""
+    monkeypatch.setenv("PMMF_B200_GRAM_DENSE_RATIO", ratio)
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
