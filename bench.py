@@ -39,6 +39,18 @@ sys.path.insert(0, ROOT)
 METRIC = "pMMF factorization throughput, R-MAT n=1M (config 4)"
 UNIT = "rotations/s"
 
+# --workload: config 4 is the headline; the other BASELINE configs print the
+# same line shape (their own parity-test cases, timed on request).
+WORKLOADS = {
+    "c1": {"metric": "pMMF factorization throughput, dense SPD n=1024 (config 1)",
+           "desc": "config 1: dense SPD n=1024, X X^T/256 + 1e-3 I", "cpu": "c1"},
+    "c3": {"metric": "pMMF factorization throughput, RBF kernel n=16384 k=3 (config 3)",
+           "desc": "config 3: RBF kernel n=16384 in 10-D, bandwidth 0.5, + 1e-4 I", "cpu": "c3s"},
+    "c4": {"metric": METRIC, "desc": "config 4: R-MAT scale 20 epv 32, normalized Laplacian + 1e-2 I", "cpu": "c4s"},
+    "c5": {"metric": "pMMF factorization throughput, anisotropic Poisson 1024^2 (config 5)",
+           "desc": "config 5: 5-point anisotropic Poisson 1024x1024 (a_x=100, a_y=1)", "cpu": "c5s"},
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -46,6 +58,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--scale", type=int, default=20, help="R-MAT scale (20 = BASELINE config 4)")
     ap.add_argument("--cpu-scale", type=int, default=14, help="R-MAT scale of the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -67,17 +80,61 @@ def merge_traffic():
         return None
 
 
-def config_params():
+def config_params(wl="c4"):
     from paper_1507_04396_b200.abi import make_params
 
+    if wl == "c1":
+        return make_params(k=2, n_stages=8, eta=0.5, m_target=2, c_min=10, c_max=5000, d_max=500, seed=42)
+    if wl in ("c3", "c3s"):
+        return make_params(k=3, n_stages=10, eta=0.5, m_target=16, c_min=10, c_max=10000, d_max=500, seed=42)
+    if wl in ("c5", "c5s"):
+        return make_params(k=2, n_stages=15, eta=0.5, m_target=256, seed=42)
     return make_params(k=2, n_stages=15, eta=0.5, m_target=512, c_min=10, c_max=10000, d_max=500,
                        bypass_enabled=True, core_min=10, core_cap=4096, seed=42)
 
 
-def workload(scale):
+def workload(scale, wl="c4"):
     from paper_1507_04396_b200 import api
 
+    if wl == "c1":
+        return api.workload_dense_spd(1024, 256, 42)
+    if wl == "c3":
+        return api.workload_rbf(16384, seed=42)
+    if wl == "c3s":  # the CPU reference's feasible size
+        return api.workload_rbf(2048, seed=42)
+    if wl == "c5":
+        return api.workload_aniso_grid(1024)
+    if wl == "c5s":
+        return api.workload_aniso_grid(256)
     return api.workload_rmat(scale, 32, 42, 1e-2)
+
+
+def cpu_sample_desc(wl, scale):
+    return {"c1": "dense SPD n=1024 (full config 1)",
+            "c3s": "RBF n=2048 (config-3 recipe; n=16384 needs ~275 GB per Gram buffer on the CPU path)",
+            "c5s": "anisotropic Poisson 256x256, m=256 (config-5 recipe at 1/16 of the grid)",
+            "c4s": f"R-MAT scale {scale}, epv 32, m=512 (config-4 recipe at n=2^{scale}); the reference cannot "
+                   f"hold n=2^20 (OOM, SURVEY.md §6)"}[wl]
+
+
+def fp64_peak():
+    """cuBLAS DGEMM (torch.matmul fp64, 8192^3, best of 5) on this GPU, TFLOP/s."""
+    import torch
+
+    a = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    b = torch.randn(8192, 8192, dtype=torch.float64, device="cuda")
+    torch.matmul(a, b)
+    best = 1e30
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * 8192 ** 3 / (best / 1e3) / 1e12
 
 
 class Clocks:
@@ -140,15 +197,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def cpu_reference_run(scale, threads, steps=1, warmup=0):
-    """The reference compiled in place (oracle/_ref) on a bounded R-MAT sample."""
+def cpu_reference_run(scale, threads, steps=1, warmup=0, wl="c4"):
+    """The reference compiled in place (oracle/_ref) on a bounded sample."""
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import oracles
 
     ref = oracles.load("ref")
     ref.lib.pmmf_ref_set_threads(threads)
-    inp = workload(scale)
-    params = config_params()
+    cw = WORKLOADS[wl]["cpu"]
+    inp = workload(scale, cw)
+    params = config_params(cw)
     times, rots = [], 0
     for i in range(warmup + steps):
         t = time.perf_counter()
@@ -173,24 +231,68 @@ def dist_init(args):
     return world, rank, local, dist
 
 
+def time_mmf_apply(lib, coo_dev, params, err, n):
+    """MmfOperator inv_sqrt apply (the CG preconditioner, transform_ops.hpp:51-67)
+    on device-resident vectors: 1 and 20 rhs, CUDA events, best of 10.
+    Algorithmic bytes: 2 R_nid (8k^2+4k) + 2*2*8 n b + 8 g^2."""
+    import torch
+    from paper_1507_04396_b200 import abi
+
+    h = ctypes.c_void_p()
+    abi.raise_for(lib.factorize(ctypes.byref(coo_dev), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+    f = lib.read_result(h)
+    op = ctypes.c_void_p()
+    abi.raise_for(lib.operator_create(h, 1e-12, ctypes.byref(op), err, len(err)), err)
+    lib.result_free(h)
+    k = int(params.k)
+    ident = np.eye(k).reshape(-1)
+    r_nid = 0
+    for st in f.stages:
+        q = st.rot_matrices.reshape(len(st.rot_matrices), -1)
+        r_nid += int(np.sum(~np.all(q == ident, axis=1)))
+    g = len(f.core_indices)
+    out = {"rotations_non_identity": r_nid, "core": g}
+    peak, _ = peaks()
+    for b in (1, 20):
+        v = torch.randn(b, n, dtype=torch.float64, device="cuda")
+        o = torch.empty_like(v)
+        best = 1e30
+        for i in range(12):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            abi.raise_for(lib.operator_apply(op, 2, b, v.data_ptr(), o.data_ptr(), 1, err, len(err)), err)
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                best = min(best, e0.elapsed_time(e1))
+        by = 2 * r_nid * (8 * k * k + 4 * k) + 2 * 2 * 8 * n * b + 8 * g * g
+        out[f"rhs{b}"] = {"ms": best, "algorithmic_bytes": by, "achieved_GBs": by / 1e9 / (best / 1e3),
+                          "frac_hbm": by / 1e9 / (best / 1e3) / peak,
+                          "note": "includes the rhs-major <-> index-major transposes of the public call"}
+    lib.operator_free(op)
+    return out
+
+
 def main():
     args = parse()
+    W = WORKLOADS[args.workload]
     world, rank, local, dist = dist_init(args)
     if args.impl == "reference":
         if rank != 0:
             return
         threads = os.cpu_count() or 1
-        rots, times, inp = cpu_reference_run(args.cpu_scale, threads, steps=args.steps, warmup=args.warmup)
+        rots, times, inp = cpu_reference_run(args.cpu_scale, threads, steps=args.steps, warmup=args.warmup,
+                                             wl=args.workload)
         best = max(times)
         v = rots / best
-        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        line = {"metric": W["metric"], "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT recipe, SURVEY.md §8(d))",
                 "impl": "reference",
-                "config": {"workload": f"R-MAT scale {args.cpu_scale} (bounded sample of config 4), m=512, k=2, P=15",
+                "config": {"workload": "bounded CPU sample of " + W["desc"] + ": " + cpu_sample_desc(W["cpu"], args.cpu_scale),
                            "n": int(inp[0]), "nnz": int(len(inp[1]))},
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
-                                 "sample": f"R-MAT scale {args.cpu_scale}, epv 32, m=512 (config-4 recipe at n=2^{args.cpu_scale}); the reference cannot hold n=2^20 (OOM, SURVEY.md §6)"},
+                                 "sample": cpu_sample_desc(W["cpu"], args.cpu_scale)},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -205,8 +307,8 @@ def main():
     L.pmmf_b200_profile_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
                                          ctypes.POINTER(ctypes.c_double)]
     L.pmmf_b200_profile_enable.argtypes = [ctypes.c_int32]
-    params = config_params()
-    n, rows, cols, vals = workload(args.scale)
+    params = config_params(args.workload)
+    n, rows, cols, vals = workload(args.scale, args.workload)
     d_rows = torch.from_numpy(rows).cuda()
     d_cols = torch.from_numpy(cols).cuda()
     d_vals = torch.from_numpy(vals).cuda()
@@ -287,7 +389,7 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     prof = {}
-    for name in ("rotate_write", "rotate_count"):
+    for name in ("rotate_write", "rotate_count", "gram_dense"):
         c, ms, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
         if L.pmmf_b200_profile_read(name.encode(), ctypes.byref(c), ctypes.byref(ms), ctypes.byref(by)) == 0:
             prof[name] = (c.value, ms.value, by.value)
@@ -324,27 +426,45 @@ def main():
             c2, ms2, by2 = prof["rotate_count"]
             roof["count_pass"] = {"launches": c2, "ms": ms2, "achieved_GBs": (by2 / 1e9) / (ms2 / 1e3) if ms2 else 0.0}
 
+    if args.workload == "c3" and "gram_dense" in prof:
+        # dense Gram (bitwise sequential SYRK on the FP64 pipe) against cuBLAS DGEMM
+        c, ms, fl = prof["gram_dense"]
+        tf = (fl / 1e12) / (ms / 1e3) if ms > 0 else 0.0
+        pk = fp64_peak()
+        roof = {"bound": "fp64", "kernel": "k_syrk_seq (dense Gram, sequential row order, unfused mul/add)",
+                "achieved": tf, "peak": pk, "unit": "TFLOP/s", "frac": tf / pk, "traffic": None, "launches": c,
+                "kernel_ms_total": ms, "algorithmic_flops_total": fl,
+                "peak_source": "measured live: cuBLAS DGEMM (torch.matmul fp64 8192^3, best of 5)",
+                "share_of_step": ms / sum(step_ms), "write_pass": roof}
+
+    apply = None
+    if args.workload == "c5":
+        apply = time_mmf_apply(lib, coo_dev, params, err, n)
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            crots, ctimes, cinp = cpu_reference_run(args.cpu_scale, threads)
+            crots, ctimes, cinp = cpu_reference_run(args.cpu_scale, threads, wl=args.workload)
             cpu = {"value": crots / ctimes[0], "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"reference (oracle/_ref) on R-MAT scale {args.cpu_scale} epv 32 m=512 (n={cinp[0]}, "
+                   "sample": f"reference (oracle/_ref) on {cpu_sample_desc(W['cpu'], args.cpu_scale)} (n={cinp[0]}, "
                              f"nnz={len(cinp[1])}), {ctimes[0]:.1f} s, {threads} threads"}
         except Exception as e:  # the checker is optional on the box
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        line = {"metric": W["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded R-MAT recipe, SURVEY.md §8(d)); inputs > L2 (no flush needed)",
-                "config": {"workload": f"config 4: R-MAT scale {args.scale} epv 32, normalized Laplacian + 1e-2 I",
-                           "n": int(n), "nnz": int(len(vals)), "k": 2, "P": 15, "m": 512, "c_max": 10000,
+                "config": {"workload": W["desc"] if args.workload != "c4" else
+                           f"config 4: R-MAT scale {args.scale} epv 32, normalized Laplacian + 1e-2 I",
+                           "n": int(n), "nnz": int(len(vals)), "k": int(params.k), "P": int(params.n_stages),
+                           "m": int(params.m_target), "c_max": int(params.c_max),
                            "rotations_per_step": int(rots), "parallelism": f"replicas x{world}",
                            "l2": "working set >> 126 MB L2"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "mmf_apply": apply,
                 "clocks": clk, "step_ms": step_ms,
                 "phases_ms_last_step": dict(zip(["clustering", "gram", "search", "apply", "reblock", "total"],
                                                 [round(float(x), 1) for x in last_phases]))}

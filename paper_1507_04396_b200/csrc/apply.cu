@@ -72,6 +72,14 @@ struct PassArgs {
   int32_t* wrow;
   double* wval;
   unsigned long long* out_entries;  // profiling: outputs allocated
+  // k = 2 single-partition rotations allocate their own arena space in the
+  // write pass (count merge, atomicAdd, write merge back to back)
+  unsigned long long* cursor;
+  i64 cap;
+  int32_t* ovf;
+  int level;
+  i64* rbase;
+  int32_t* rlen;
 };
 
 // Row range of partition p of rotation t: split points are rows of the
@@ -328,6 +336,7 @@ __global__ void k_rot_alloc(PassArgs A, const int64_t* __restrict__ nitems_d, un
   if (i >= A.nrot || *reinterpret_cast<volatile int32_t*>(ovf) != INT_MAX) return;
   const i64 nitems = *nitems_d;
   const i64 np = (i + 1 < A.nrot ? A.ioff[i + 1] : nitems) - A.ioff[i];
+  if (K == 2 && np == 1) return;  // allocated by its write pass
   i64 tot[K];
 #pragma unroll
   for (int a = 0; a < K; ++a) {
@@ -401,6 +410,7 @@ __global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, cons
     const i64 ri = lo;
     const i64 p = item - A.ioff[ri];
     const i64 np = (ri + 1 < A.nrot ? A.ioff[ri + 1] : nitems) - A.ioff[ri];
+    if (K == 2 && np == 1 && !kWrite) continue;  // counted by its own write pass
     const int t = A.rots[ri];
     int id[K];
     double q[K][K];
@@ -417,9 +427,36 @@ __global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, cons
 #pragma unroll
     for (int a = 0; a < K; ++a) {
       kept[a] = 0;
-      dst[a] = kWrite ? A.pos[K * A.ioff[ri] + a * np + p] : 0;
+      dst[a] = (kWrite && !(K == 2 && np == 1)) ? A.pos[K * A.ioff[ri] + a * np + p] : 0;
     }
     if constexpr (K == 2) {
+      if (np == 1) {
+        // Single partition: no separate count pass.  Count the union (rows
+        // only, the columns are then hot in L1/L2), allocate 2u arena
+        // entries, write.  Overflow marks the level uncommitted exactly like
+        // k_rot_alloc does; the commit kernel then skips it.
+        i64 cb[2] = {beg[0], beg[1]};
+        int u = 0;
+        merge_count2(A, cb, end, u);
+        unsigned long long b0 = 0;
+        if ((threadIdx.x & 31) == 0) b0 = atomicAdd(A.cursor, 2ull * static_cast<unsigned long long>(u));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (static_cast<i64>(b0) + 2 * u > A.cap) {
+          if ((threadIdx.x & 31) == 0) atomicMin(A.ovf, A.level);
+          continue;
+        }
+        const i64 d2[2] = {static_cast<i64>(b0), static_cast<i64>(b0) + u};
+        int w = 0;
+        merge_write2(A, q, beg, end, w, d2);
+        if ((threadIdx.x & 31) == 0) {
+          A.rbase[2 * ri] = d2[0];
+          A.rbase[2 * ri + 1] = d2[1];
+          A.rlen[2 * ri] = u;
+          A.rlen[2 * ri + 1] = u;
+          atomicAdd(A.out_entries, 2ull * static_cast<unsigned long long>(u));
+        }
+        continue;
+      }
       int u = 0;  // union size: the same for both output columns
       if (kWrite)
         merge_write2(A, q, beg, end, u, dst);
@@ -676,7 +713,8 @@ struct LevelScratch {
   DBuf<unsigned long long> cursor, in_entries;
   DBuf<unsigned char> scan_tmp;
   size_t scan_bytes = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;  // profiled write passes
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // profiled write passes
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> cev;  // profiled count passes
   double rot_bytes = 0.0;
 };
 
@@ -703,13 +741,29 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.pos = S.pos.get();
   A.nitems = S.max_items;  // bound; kernels read the exact count from S.nitems
   A.out_entries = S.in_entries.get() + 1;
+  A.cursor = S.cursor.get();
+  A.cap = B.cap;
+  A.ovf = S.ovf.get();
+  A.level = level;
+  A.rbase = S.rbase.get();
+  A.rlen = S.rlen.get();
   PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
   {
     size_t tmp = S.scan_bytes;
     PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
   }
   PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
+  cudaEvent_t c0 = nullptr, c1 = nullptr;
+  if (prof_enabled()) {
+    c0 = EventPool::get().take();
+    c1 = EventPool::get().take();
+    cudaEventRecord(c0, s);
+  }
   PMMF_LAUNCH((k_merge_p<K, false>), kPersistentBlocks, kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  if (c0) {
+    cudaEventRecord(c1, s);
+    S.cev.push_back({c0, c1});
+  }
   PMMF_LAUNCH(k_rot_alloc<K>, blocks_for(nrot * 32, kThreads), kThreads, 0, s, A, S.nitems.get(), S.cursor.get(), B.cap,
               S.ovf.get(), level, S.pos.get(), S.rbase.get(), S.rlen.get());
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1006,6 +1060,17 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       // once (12 B per entry), rotation blocks (8k^2 + 4k per rotation)
       prof_add_n("rotate_write", static_cast<int64_t>(S.ev.size()), ms,
                  12.0 * static_cast<double>(io[0] + io[1]) + S.rot_bytes);
+      double cms = 0.0;
+      for (auto& [e0, e1] : S.cev) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, e0, e1);
+        cms += t;
+        EventPool::get().give(e0);
+        EventPool::get().give(e1);
+      }
+      // count pass bytes: the row indices of the multi-partition inputs (not
+      // counted separately; reported as 4 B per input entry, an upper bound)
+      prof_add_n("rotate_count", static_cast<int64_t>(S.cev.size()), cms, 4.0 * static_cast<double>(io[0]));
     }
     double t_mass = 0.0;
     if (ms) {

@@ -103,6 +103,7 @@ double scalar_factor(int mode, double d, double thr) {  // transform_ops.hpp:76-
 struct StageDev {
   int64_t nclusters = 0;
   int64_t max_c = 0;
+  size_t max_rec_bytes = 0;  // largest cluster's staged records (k_stage_apply_s)
   DBuf<int32_t> members;   // stage partition, global ids
   DBuf<int64_t> coff;      // cluster offsets
   DBuf<int64_t> rot_ptr;   // per cluster [rot_ptr[u], rot_ptr[u+1]) in level order
@@ -169,6 +170,74 @@ __global__ void k_stage_apply(int k, int nrhs, int rc, const int64_t* __restrict
   }
 }
 
+// Slice staging: 8 independent loads in flight per thread (the member
+// index and the vector element are two dependent global loads).
+constexpr int kGatherUnroll = 8;
+__device__ __forceinline__ void gather_slice(double* sm, const double* __restrict__ V,
+                                             const int32_t* __restrict__ members, int64_t off, int c, int nr, int rc,
+                                             int nrhs, int r0) {
+  const int n = c * nr;
+  for (int base = threadIdx.x; base < n; base += kGatherUnroll * blockDim.x) {
+    int64_t src[kGatherUnroll];
+#pragma unroll
+    for (int j = 0; j < kGatherUnroll; ++j) {
+      const int i = base + j * blockDim.x;
+      if (i < n) {
+        const int li = i / nr;
+        src[j] = static_cast<int64_t>(members[off + li]) * nrhs + r0 + (i - li * nr);
+      }
+    }
+    double x[kGatherUnroll];
+#pragma unroll
+    for (int j = 0; j < kGatherUnroll; ++j)
+      if (base + j * blockDim.x < n) x[j] = V[src[j]];
+#pragma unroll
+    for (int j = 0; j < kGatherUnroll; ++j) {
+      const int i = base + j * blockDim.x;
+      if (i < n) {
+        const int li = i / nr;
+        sm[li * rc + (i - li * nr)] = x[j];
+      }
+    }
+  }
+}
+template <typename T>
+__device__ __forceinline__ void copy_unrolled(T* dst, const T* __restrict__ src, int n) {
+  for (int base = threadIdx.x; base < n; base += kGatherUnroll * blockDim.x) {
+    T x[kGatherUnroll];
+#pragma unroll
+    for (int j = 0; j < kGatherUnroll; ++j)
+      if (base + j * blockDim.x < n) x[j] = src[base + j * blockDim.x];
+#pragma unroll
+    for (int j = 0; j < kGatherUnroll; ++j)
+      if (base + j * blockDim.x < n) dst[base + j * blockDim.x] = x[j];
+  }
+}
+__device__ __forceinline__ void scatter_slice(const double* sm, double* __restrict__ V,
+                                              const int32_t* __restrict__ members, int64_t off, int c, int nr, int rc,
+                                              int nrhs, int r0) {
+  const int n = c * nr;
+  for (int base = threadIdx.x; base < n; base += kGatherUnroll * blockDim.x) {
+    int64_t dst[kGatherUnroll];
+#pragma unroll
+    for (int j = 0; j < kGatherUnroll; ++j) {
+      const int i = base + j * blockDim.x;
+      if (i < n) {
+        const int li = i / nr;
+        dst[j] = static_cast<int64_t>(members[off + li]) * nrhs + r0 + (i - li * nr);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kGatherUnroll; ++j) {
+      const int i = base + j * blockDim.x;
+      if (i < n) {
+        const int li = i / nr;
+        V[dst[j]] = sm[li * rc + (i - li * nr)];
+      }
+    }
+  }
+}
+
 // Fast path for k = 2, 3 (configs 1-5): same arithmetic as k_stage_apply,
 // but the rotation record (local positions + q) of a thread's first item in
 // the NEXT level is loaded into registers before the current level's work,
@@ -192,10 +261,7 @@ __global__ void __launch_bounds__(256) k_stage_apply_k(int nrhs, int rc, const i
   const int c = static_cast<int>(coff[u + 1] - off);
   const int L = nlev[u];
   const int64_t* lp = lvl_ptr + lvl_base[u];
-  for (int i = threadIdx.x; i < c * nr; i += blockDim.x) {
-    const int li = i / nr, r = i - li * nr;
-    sm[li * rc + r] = V[static_cast<int64_t>(members[off + li]) * nrhs + r0 + r];
-  }
+  gather_slice(sm, V, members, off, c, nr, rc, nrhs, r0);
   struct Rec {
     int a[K];
     double q[K * K];
@@ -249,10 +315,65 @@ __global__ void __launch_bounds__(256) k_stage_apply_k(int nrhs, int rc, const i
     b = nb;
     e = ne;
   }
-  for (int i = threadIdx.x; i < c * nr; i += blockDim.x) {
-    const int li = i / nr, r = i - li * nr;
-    V[static_cast<int64_t>(members[off + li]) * nrhs + r0 + r] = sm[li * rc + r];
+  scatter_slice(sm, V, members, off, c, nr, rc, nrhs, r0);
+}
+
+// Fully staged variant: the cluster's rotation records (local positions,
+// q) and level boundaries are copied into shared memory next to the slice,
+// so a level is shared-memory work plus one barrier -- no global load on the
+// level chain.  Used when slice + records fit (run_stage).
+template <int K, bool kTransposed>
+__global__ void __launch_bounds__(256) k_stage_apply_s(int nrhs, int rc, const int64_t* __restrict__ coff,
+                                                       const int32_t* __restrict__ members,
+                                                       const int64_t* __restrict__ rot_ptr,
+                                                       const int64_t* __restrict__ lvl_ptr,
+                                                       const int64_t* __restrict__ lvl_base,
+                                                       const int32_t* __restrict__ nlev,
+                                                       const int32_t* __restrict__ loc,
+                                                       const double* __restrict__ qs, double* __restrict__ V) {
+  extern __shared__ double sm[];
+  const int u = blockIdx.x;
+  const int r0 = blockIdx.y * rc;
+  const int nr = min(rc, nrhs - r0);
+  const int64_t t0 = rot_ptr[u];
+  const int R = static_cast<int>(rot_ptr[u + 1] - t0);
+  if (R == 0 || nr <= 0) return;
+  const int64_t off = coff[u];
+  const int c = static_cast<int>(coff[u + 1] - off);
+  const int L = nlev[u];
+  const int64_t* lp = lvl_ptr + lvl_base[u];
+  double* sq = sm + static_cast<int64_t>(c) * rc;                        // R x K x K
+  int* sl = reinterpret_cast<int*>(sq + static_cast<int64_t>(R) * K * K);  // R x K
+  int* slp = sl + R * K;                                                   // L + 1
+  gather_slice(sm, V, members, off, c, nr, rc, nrhs, r0);
+  copy_unrolled(sq, qs + t0 * K * K, R * K * K);
+  copy_unrolled(sl, loc + t0 * K, R * K);
+  for (int i = threadIdx.x; i <= L; i += blockDim.x) slp[i] = static_cast<int>(lp[i] - t0);
+  __syncthreads();
+  for (int lv = 0; lv < L; ++lv) {
+    const int l = kTransposed ? (L - 1 - lv) : lv;
+    const int b = slp[l], n = (slp[l + 1] - b) * nr;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const int t = b + i / nr, r = i % nr;
+      int a[K];
+      double v[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        a[j] = sl[t * K + j] * rc + r;
+        v[j] = sm[a[j]];
+      }
+      const double* q = sq + t * K * K;
+#pragma unroll
+      for (int x = 0; x < K; ++x) {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc = dadd(acc, dmul(kTransposed ? q[j * K + x] : q[x * K + j], v[j]));
+        sm[a[x]] = acc;
+      }
+    }
+    __syncthreads();
   }
+  scatter_slice(sm, V, members, off, c, nr, rc, nrhs, r0);
 }
 
 // Core: y = E f(lambda) E^T x on the core indices (transform_ops.hpp:88-106),
@@ -372,14 +493,22 @@ struct Operator {
         for (int a = 0; a < k; ++a) lastlvl[st.rot_idx[t * k + a]] = lv;
         per[u].push_back({lv, t});
       }
-      std::vector<int64_t> rot_ptr(1, 0), lvl_ptr, lvl_base, coff(st.off.begin(), st.off.end());
-      std::vector<int32_t> nlev, loc, mem(st.members.begin(), st.members.end());
+      // Apply groups: the clusters with at least one non-identity rotation,
+      // each reduced to the indices those rotations touch (identity
+      // rotations are 51% of config 5's stage 1 and 98% of its stage 2; an
+      // untouched index keeps its value, so it is neither read nor written).
+      std::vector<int64_t> rot_ptr(1, 0), lvl_ptr, lvl_base, coff(1, 0);
+      std::vector<int32_t> nlev, loc, mem;
       std::vector<double> qv;
+      std::vector<int32_t> slot(static_cast<size_t>(sd.max_c), -1);
+      sd.max_c = 0;
       for (int64_t u = 0; u < m; ++u) {
         auto& v = per[u];
+        if (v.empty()) continue;
         std::stable_sort(v.begin(), v.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        const size_t mem0 = mem.size();
         lvl_base.push_back(static_cast<int64_t>(lvl_ptr.size()));
-        const int32_t L = v.empty() ? 0 : v.back().first;
+        const int32_t L = v.back().first;
         nlev.push_back(L);
         int64_t cur = rot_ptr.back();
         size_t i = 0;
@@ -387,15 +516,29 @@ struct Operator {
           lvl_ptr.push_back(cur);
           while (i < v.size() && v[i].first == lv) {
             const int64_t t = v[i].second;
-            for (int a = 0; a < k; ++a) loc.push_back(static_cast<int32_t>(pos_of[st.rot_idx[t * k + a]]));
+            for (int a = 0; a < k; ++a) {
+              const int64_t gidx = st.rot_idx[t * k + a];
+              int32_t& sl = slot[static_cast<size_t>(pos_of[gidx])];
+              if (sl < 0) {
+                sl = static_cast<int32_t>(mem.size() - mem0);
+                mem.push_back(static_cast<int32_t>(gidx));
+              }
+              loc.push_back(sl);
+            }
             qv.insert(qv.end(), st.rot_q.begin() + t * k * k, st.rot_q.begin() + (t + 1) * k * k);
             ++cur;
             ++i;
           }
         }
+        for (size_t j = mem0; j < mem.size(); ++j) slot[static_cast<size_t>(pos_of[mem[j]])] = -1;
         lvl_ptr.push_back(cur);
         rot_ptr.push_back(cur);
+        coff.push_back(static_cast<int64_t>(mem.size()));
+        sd.max_c = std::max<int64_t>(sd.max_c, static_cast<int64_t>(mem.size() - mem0));
+        const size_t rb = v.size() * static_cast<size_t>(k * k * 8 + k * 4) + static_cast<size_t>(L + 1) * 4;
+        sd.max_rec_bytes = std::max(sd.max_rec_bytes, (rb + 15) / 16 * 16);
       }
+      sd.nclusters = static_cast<int64_t>(coff.size()) - 1;
       auto up64 = [&](DBuf<int64_t>& d, const std::vector<int64_t>& h) {
         d.alloc(std::max<int64_t>(1, static_cast<int64_t>(h.size())), s);
         d.upload(h);
@@ -455,6 +598,28 @@ struct Operator {
 
   void run_stage(const StageDev& sd, bool transposed, int nrhs, double* V, cudaStream_t st) const {
     if (sd.nclusters == 0) return;
+    if ((k == 2 || k == 3) && sd.max_rec_bytes > 0) {
+      // Records staged in shared memory: the widest rhs chunk (<= 8) whose
+      // slice fits next to the largest cluster's records.
+      const size_t row = static_cast<size_t>(sd.max_c) * 8;
+      int rc = std::min(nrhs, 8);
+      const size_t cap = row + sd.max_rec_bytes <= kSmemTwoPerSm ? kSmemTwoPerSm : kSmemBudget;
+      while (rc > 1 && row * rc + sd.max_rec_bytes > cap) --rc;
+      const size_t smem = row * rc + sd.max_rec_bytes;
+      if (smem <= kSmemBudget) {
+        dim3 grid(static_cast<unsigned>(sd.nclusters), static_cast<unsigned>((nrhs + rc - 1) / rc));
+        auto kern = k == 2 ? (transposed ? k_stage_apply_s<2, true> : k_stage_apply_s<2, false>)
+                           : (transposed ? k_stage_apply_s<3, true> : k_stage_apply_s<3, false>);
+        if (smem > 48 * 1024)
+          PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        kern<<<grid, kThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
+                                           sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
+                                           sd.q.get(), V);
+        launch_counter().fetch_add(1, std::memory_order_relaxed);
+        PMMF_CUDA(cudaGetLastError());
+        return;
+      }
+    }
     if (k == 2 || k == 3) {
       // rhs per CTA: as many as fit two CTAs per SM (<= 8), else one CTA
       // per SM with the largest slice that fits.

@@ -868,17 +868,67 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
       }
     }
     cmax = std::min(cmax, dev_max);
-    for (int32_t u : h_order) {
+    auto need_of = [](i64 c) {
+      return ((static_cast<size_t>((c + 31) / 32) * 4 + 15) / 16) * 16 + static_cast<size_t>(c) * 20;
+    };
+    std::vector<int> width(static_cast<size_t>(nclusters), 1);
+    for (size_t i = 0; i < h_order.size(); ++i) {
+      const int32_t u = h_order[i];
       const i64 c = b.h_c[u];
-      const size_t need = ((static_cast<size_t>((c + 31) / 32) * 4 + 15) / 16) * 16 + static_cast<size_t>(c) * 20;
       int w = 1;
       while (w * 2 <= cmax && static_cast<i64>(w) * 2 * 1024 <= c) w *= 2;
-      if (c >= big_c && need <= 200 * 1024 && cmax >= 2) {
+      if (c >= big_c && need_of(c) <= 200 * 1024 && cmax >= 2) {
         w = std::max(w, 2);
         if (force_w >= 2) w = std::min(force_w, cmax);
+      } else {
+        w = 1;
+      }
+      width[i] = w;
+    }
+    // Capacity: the cluster kernel holds one CTA per SM, the single-CTA
+    // kernel two.  When the widths ask for more SMs than the device has,
+    // the launch runs in waves and wide slices stop paying: narrow the
+    // cheapest clusters first (model: c/2 iterations of alpha + beta c/w,
+    // measured on config 4: 34 us at c = 8192 on 1 CTA, ~7 us on 8 CTAs)
+    // until the summed SM-time fits under the longest cluster's time.
+    if (force_w < 2) {
+      int nsm = 148;
+      {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) (void)cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      }
+      auto t_of = [](i64 c, int w) { return 0.5 * static_cast<double>(c) * (3.0 + 0.0035 * static_cast<double>(c) / w); };
+      auto sm_time = [&](i64 c, int w) { return (w >= 2 ? w : 0.5) * t_of(c, w); };
+      for (;;) {
+        double work = 0.0, longest = 0.0;
+        for (size_t i = 0; i < h_order.size(); ++i) {
+          const i64 c = b.h_c[h_order[i]];
+          work += sm_time(c, width[i]);
+          longest = std::max(longest, t_of(c, width[i]));
+        }
+        if (work / nsm <= longest) break;
+        // narrow the cluster whose halved time stays smallest
+        size_t best = h_order.size();
+        double bt = 0.0;
+        for (size_t i = 0; i < h_order.size(); ++i) {
+          if (width[i] < 2) continue;
+          const double t = t_of(b.h_c[h_order[i]], width[i] / 2);
+          if (best == h_order.size() || t < bt) {
+            best = i;
+            bt = t;
+          }
+        }
+        if (best == h_order.size()) break;
+        width[best] /= 2;
+      }
+    }
+    for (size_t i = 0; i < h_order.size(); ++i) {
+      const int32_t u = h_order[i];
+      const int w = width[i];
+      if (w >= 2) {
         const int g = w >= 16 ? 4 : w >= 8 ? 3 : w >= 4 ? 2 : 1;
         group[g].push_back(u);
-        gsmem[g] = std::max(gsmem[g], need);
+        gsmem[g] = std::max(gsmem[g], need_of(b.h_c[u]));
       } else {
         small.push_back(u);
       }

@@ -37,6 +37,8 @@ def main():
     ap.add_argument("cfgs", nargs="*", default=["c1", "c3", "c5"])
     ap.add_argument("--rhs", type=int, default=20)
     ap.add_argument("--max-iter", type=int, default=20000)
+    ap.add_argument("--no-pcg", action="store_true")
+    ap.add_argument("--apply-only", action="store_true", help="c5: skip the factorization timing runs")
     args = ap.parse_args()
     for c in args.cfgs:
         if c == "c1":
@@ -51,7 +53,8 @@ def main():
         elif c == "c5":
             inp = api.workload_aniso_grid(1024)
             p = FactorizeParams(seed=42, cluster=ClusterParams(m_target=256))
-            run_factorize("c5", inp, p, reps=1)
+            if not args.apply_only:
+                run_factorize("c5", inp, p, reps=2)
             lib = api.library()
             n = inp[0]
             h = api.factorize_handle(BlockedSparseMatrix.from_triplets(*inp), p)
@@ -68,6 +71,20 @@ def main():
                                   err)
                     dt = time.time() - t
                 print(f"c5 apply inv_sqrt nrhs={nrhs}: {dt * 1e3:.2f} ms (host buffers)", flush=True)
+            import torch  # device buffers for the device-resident apply timing
+            for nrhs in (1, 20):
+                dv = torch.randn(nrhs, n, dtype=torch.float64, device="cuda")
+                do = torch.empty_like(dv)
+                for rep in range(6):
+                    torch.cuda.synchronize()
+                    t = time.time()
+                    abi.raise_for(lib.operator_apply(op, 2, nrhs, dv.data_ptr(), do.data_ptr(), 1, err, len(err)), err)
+                    torch.cuda.synchronize()
+                    dt = time.time() - t
+                print(f"c5 apply inv_sqrt nrhs={nrhs}: {dt * 1e3:.3f} ms (device buffers)", flush=True)
+            if args.no_pcg:
+                lib.operator_free(op)
+                continue
             coo, keep = abi.make_coo(*inp)
             cfg = abi.SolveConfig(1e-8, args.max_iter, args.rhs, 42)
             it = np.zeros(args.rhs, np.int32)
