@@ -64,6 +64,7 @@ struct PassArgs {
   const int32_t* arow;
   const double* aval;
   const int64_t* ioff;   // per level-rotation: first partition index (exclusive scan of nparts)
+  int32_t* item_rot;     // partition -> level-rotation index (k_item_rot)
   i64 nrot;              // rotations in level
   i64 nitems;            // total partitions
   int64_t* cnt;          // K * nitems kept counts, layout [K*ioff_t + a*np_t + p]
@@ -317,6 +318,17 @@ __global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long
   atomicAdd(in_entries, S);
 }
 
+// item_rot[ioff[i] + p] = i for the np_i partitions of level-rotation i, so a
+// merge warp finds its rotation with one load instead of a binary search
+// over ioff (17 dependent L2 round trips at 10^5 rotations per level).
+__global__ void k_item_rot(i64 nrot, const int64_t* __restrict__ ioff, const int64_t* __restrict__ np,
+                           int32_t* __restrict__ item_rot) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= nrot) return;
+  const i64 b = ioff[i], n = np[i];
+  for (i64 p = 0; p < n; ++p) item_rot[b + p] = static_cast<int32_t>(i);
+}
+
 // nitems = ioff[nrot-1] + nparts[nrot-1], on the device (no host sync).
 __global__ void k_items(i64 nrot, const int64_t* __restrict__ ioff, const int64_t* __restrict__ np,
                         int64_t* __restrict__ nitems) {
@@ -402,12 +414,7 @@ __global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, cons
   const i64 nitems = *nitems_d;
   const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
   for (i64 item = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5; item < nitems; item += nw) {
-    i64 lo = 0, hi = A.nrot;
-    while (hi - lo > 1) {
-      const i64 mid = (lo + hi) >> 1;
-      if (A.ioff[mid] <= item) lo = mid; else hi = mid;
-    }
-    const i64 ri = lo;
+    const i64 ri = A.item_rot[item];
     const i64 p = item - A.ioff[ri];
     const i64 np = (ri + 1 < A.nrot ? A.ioff[ri + 1] : nitems) - A.ioff[ri];
     if (K == 2 && np == 1 && !kWrite) continue;  // counted by its own write pass
@@ -708,6 +715,7 @@ __global__ void k_mass_buckets(i64 n, i64 nbuckets, int shift, const int32_t* __
 struct LevelScratch {
   i64 max_rot = 0, max_items = 0;
   DBuf<int64_t> np, ioff, nitems, cnt, pos;
+  DBuf<int32_t> item_rot;
   DBuf<i64> rbase;
   DBuf<int32_t> rlen, ovf;
   DBuf<unsigned long long> cursor, in_entries;
@@ -737,6 +745,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.wrow = B.row.get();
   A.wval = B.val.get();
   A.ioff = S.ioff.get();
+  A.item_rot = S.item_rot.get();
   A.cnt = S.cnt.get();
   A.pos = S.pos.get();
   A.nitems = S.max_items;  // bound; kernels read the exact count from S.nitems
@@ -753,6 +762,8 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
   }
   PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
+  PMMF_LAUNCH(k_item_rot, blocks_for(nrot, kThreads), kThreads, 0, s, nrot, S.ioff.get(), S.np.get(),
+              S.item_rot.get());
   cudaEvent_t c0 = nullptr, c1 = nullptr;
   if (prof_enabled()) {
     c0 = EventPool::get().take();
@@ -975,6 +986,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       S.max_items = max_rot + B.cap / kChunk + 1;
       S.cnt.alloc(K * S.max_items, s);
       S.pos.alloc(K * S.max_items, s);
+      S.item_rot.alloc(S.max_items, s);
     };
     S.max_rot = max_rot;
     S.np.alloc(max_rot, s);
