@@ -129,7 +129,9 @@ constexpr int kPrefetch = 8;  // anchor entries of a hit row staged in shared me
 
 // Per-warp state: block partial p[m], total t[m], last block seen last[m],
 // then the prefetch buffers (16-byte aligned).
-__host__ __device__ constexpr size_t score_pf_off(int m) { return (static_cast<size_t>(m) * 20 + 15) / 16 * 16; }
+// ... plus the list of anchors the current column touched (m int32) and its
+// length, so a column's epilogue costs its touched anchors, not m.
+__host__ __device__ constexpr size_t score_pf_off(int m) { return (static_cast<size_t>(m) * 24 + 4 + 15) / 16 * 16; }
 __host__ __device__ constexpr size_t score_stride(int m) { return score_pf_off(m) + 32 * kPrefetch * 12 + 32; }
 
 // Warps loop over pool columns.  For every chunk of 32 entries of the
@@ -154,6 +156,8 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
   double* p = reinterpret_cast<double*>(base);
   double* t = p + m;
   int32_t* last = reinterpret_cast<int32_t*>(t + m);
+  int32_t* touched = last + m;
+  int32_t* ntouched = touched + m;
   double* pf_v = reinterpret_cast<double*>(base + score_pf_off(m));
   int32_t* pf_a = reinterpret_cast<int32_t*>(pf_v + 32 * kPrefetch);
   uint8_t* slotmap = reinterpret_cast<uint8_t*>(pf_a + 32 * kPrefetch);  // window slot -> row lane
@@ -162,6 +166,7 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
     t[a] = 0.0;
     last[a] = -1;
   }
+  if (lane == 0) *ntouched = 0;
   __syncwarp();
   long long busy = 0;
   unsigned long long st_rows = 0, st_ent = 0;  // trace counters, flushed once per warp
@@ -228,6 +233,7 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
         const int32_t la = last[a];
         const double pa = p[a], ta = t[a];
         const bool same = la == br;
+        if (la < 0) touched[atomicAdd(ntouched, 1)] = a;
         t[a] = (same || la < 0) ? ta : dadd(ta, pa);
         p[a] = dadd(same ? pa : 0.0, prod);
         last[a] = br;
@@ -311,8 +317,9 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
     const double nj = A.cnorm[w];
     double best = 0.0;
     int ba = 0x7fffffff;
-    for (int a = lane; a < m; a += 32) {
-      if (last[a] < 0) continue;  // untouched: dot 0, score 0
+    const int nt = *ntouched;  // untouched anchors: dot 0, score 0
+    for (int i = lane; i < nt; i += 32) {
+      const int a = touched[i];
       const double dot = dadd(t[a], p[a]);
       const double na = A.anorm[a];
       double sc = 0.0;
@@ -326,6 +333,8 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
       t[a] = 0.0;
       last[a] = -1;
     }
+    __syncwarp();
+    if (lane == 0) *ntouched = 0;
     for (int o = 16; o; o >>= 1) {
       const double os = __shfl_xor_sync(0xffffffffu, best, o);
       const int oa = __shfl_xor_sync(0xffffffffu, ba, o);
@@ -473,6 +482,115 @@ __global__ void k_dense_argmax(ScoreArgs A, const int32_t* __restrict__ dcols, i
   if (lane == 0) A.assign[dcols[d]] = best > 0.0 ? ba : -1;
 }
 
+// ------------------------------------------------------------ GEMM path
+// Dense problems (configs 1 and 3: every column full): the pool and anchor
+// columns are scattered into zero-filled column-major panels (ld = N) and
+// the P x m dot products are computed as a tiled SIMT GEMM.  Each thread
+// keeps, per anchor, the reference's two-level sum (column_dot,
+// blocked_matrix.hpp:193-201): a block partial summed over the rows of one
+// pre-reblock block in ascending order, folded into the total when the
+// block changes (the row chunk's blocks are CTA-uniform).  Inserted rows
+// contribute exact-zero products: only the sign of a zero dot can differ,
+// which |dot| removes, so the scores are the sparse path's bit for bit.
+constexpr int kGemmKC = 32, kGemmTJ = 64, kGemmTA = 32;
+
+__global__ void k_panel_cols(i64 n, const int32_t* __restrict__ cols, const i64* __restrict__ ptr,
+                             const int32_t* __restrict__ row, const double* __restrict__ val, i64 N,
+                             double* __restrict__ X) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const int32_t j = cols[w];
+  double* x = X + w * N;
+  for (i64 e = ptr[j] + lane; e < ptr[j + 1]; e += 32) x[row[e]] = val[e];
+}
+
+__global__ void __launch_bounds__(256) k_score_gemm(i64 N, int Pc, int m, const double* __restrict__ Xp,
+                                                    const double* __restrict__ Xa, const int32_t* __restrict__ blk,
+                                                    const double* __restrict__ pnorm,
+                                                    const double* __restrict__ anorm, double* __restrict__ S) {
+  constexpr int KC = kGemmKC, TJ = kGemmTJ, TA = kGemmTA, AT = TA / 4;
+  __shared__ double ps[KC][TJ + 1];
+  __shared__ double as[KC][TA + 1];
+  __shared__ int32_t bs[KC];
+  const int j0 = blockIdx.x * TJ, a0 = blockIdx.y * TA;
+  const int tid = threadIdx.x, tj = tid % TJ, ag = tid / TJ;
+  double inner[AT], tot[AT];
+#pragma unroll
+  for (int i = 0; i < AT; ++i) inner[i] = tot[i] = 0.0;
+  int32_t cur = -1;
+  for (i64 r0 = 0; r0 < N; r0 += KC) {
+#pragma unroll
+    for (int i = 0; i < KC * TJ / 256; ++i) {
+      const int idx = tid + 256 * i, k = idx % KC, j = idx / KC;
+      ps[k][j] = (j0 + j < Pc && r0 + k < N) ? Xp[static_cast<i64>(j0 + j) * N + r0 + k] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < KC * TA / 256; ++i) {
+      const int idx = tid + 256 * i, k = idx % KC, a = idx / KC;
+      as[k][a] = (a0 + a < m && r0 + k < N) ? Xa[static_cast<i64>(a0 + a) * N + r0 + k] : 0.0;
+    }
+    if (tid < KC) bs[tid] = r0 + tid < N ? blk[r0 + tid] : -1;
+    __syncthreads();
+    const int kn = N - r0 < KC ? static_cast<int>(N - r0) : KC;
+    for (int k = 0; k < kn; ++k) {
+      const int32_t b = bs[k];
+      if (b != cur) {  // CTA-uniform
+        if (cur >= 0) {
+#pragma unroll
+          for (int i = 0; i < AT; ++i) tot[i] = dadd(tot[i], inner[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < AT; ++i) inner[i] = 0.0;
+        cur = b;
+      }
+      const double x = ps[k][tj];
+#pragma unroll
+      for (int i = 0; i < AT; ++i) inner[i] = dadd(inner[i], dmul(x, as[k][ag * AT + i]));
+    }
+    __syncthreads();
+  }
+  const int j = j0 + tj;
+  if (j >= Pc) return;
+  const double nj = pnorm[j];
+#pragma unroll
+  for (int i = 0; i < AT; ++i) {
+    const int a = a0 + ag * AT + i;
+    if (a >= m) continue;
+    const double dot = cur >= 0 ? dadd(tot[i], inner[i]) : 0.0;
+    const double na = anorm[a];
+    S[static_cast<i64>(j) * m + a] = (nj > 0.0 && na > 0.0) ? fabs(dot) / dmul(nj, na) : 0.0;
+  }
+}
+
+// Assignment from a P x m score table: self-assigned anchors keep their own
+// position (clustering.hpp:118-122); else the strict argmax (ties: lowest).
+__global__ void k_gemm_argmax(i64 Pc, int m, const int32_t* __restrict__ cols, const int32_t* __restrict__ self,
+                              const double* __restrict__ S, int32_t* __restrict__ assign) {
+  const i64 d = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (d >= Pc) return;
+  const int32_t sf = self[cols[d]];
+  double best = 0.0;
+  int ba = 0x7fffffff;
+  for (int a = lane; a < m; a += 32) {
+    const double sc = S[d * m + a];
+    if (sc > 0.0 && better(sc, a, best, ba)) {
+      best = sc;
+      ba = a;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double os = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oa = __shfl_xor_sync(0xffffffffu, ba, o);
+    if (better(os, oa, best, ba)) {
+      best = os;
+      ba = oa;
+    }
+  }
+  if (lane == 0) assign[d] = sf >= 0 ? sf : (best > 0.0 ? ba : -1);
+}
+
 __global__ void k_anchor_nnz(int m, const int32_t* __restrict__ anchors, const i64* __restrict__ ptr,
                              int32_t* __restrict__ nnz, int32_t* __restrict__ idx) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
@@ -509,6 +627,10 @@ struct Scorer {
     dpn.upload(pool_norm);
     danch.upload(anchors);
     dan.upload(anchor_norm);
+    if (gemm_mode()) {
+      run_gemm(P, m, dpool, dpn, danch, dan, rows_mode, assign, rows, t_start);
+      return;
+    }
     // row -> anchor index
     DBuf<int32_t> cnt(a.N + 1, s), cursor(a.N + 1, s);
     cnt.zero();
@@ -704,6 +826,68 @@ struct Scorer {
   }
 
   void set_self(const DBuf<int32_t>& anchors, const DBuf<int32_t>& pos, int m, bool on);
+
+  // Dense problems go through the GEMM path: at least a quarter of all
+  // entries stored (PMMF_B200_SCORE_GEMM=1/0 forces it on/off for tests).
+  bool gemm_mode() const {
+    if (const char* e = std::getenv("PMMF_B200_SCORE_GEMM")) return std::atoi(e) != 0;
+    const double N = static_cast<double>(a.N);
+    return a.N > 0 && static_cast<double>(a.nnz) >= 0.25 * N * N;
+  }
+
+  void run_gemm(i64 P, int m, const DBuf<int32_t>& dpool, const DBuf<double>& dpn, const DBuf<int32_t>& danch,
+                const DBuf<double>& dan, bool rows_mode, std::vector<int32_t>* assign, std::vector<double>* rows,
+                std::chrono::steady_clock::time_point t_start) {
+    const i64 N = a.N;
+    if (!rows_mode) {  // mark anchors (self-assignment, clustering.hpp:118-122)
+      std::vector<int32_t> pos(static_cast<size_t>(m));
+      std::iota(pos.begin(), pos.end(), 0);
+      DBuf<int32_t> dpos(m, s);
+      dpos.upload(pos);
+      set_self(danch, dpos, m, true);
+    }
+    DBuf<double> Xa(static_cast<i64>(m) * N, s);
+    Xa.zero();
+    PMMF_LAUNCH(k_panel_cols, blocks_for(static_cast<i64>(m) * 32, kThreads), kThreads, 0, s, static_cast<i64>(m),
+                danch.get(), a.ptr.get(), a.row.get(), a.val.get(), N, Xa.get());
+    // pool chunk: panel within a fifth of free memory
+    const i64 budget = std::max<i64>(i64{1} << 28, available_bytes() / 5);
+    const i64 pc = std::max<i64>(kGemmTJ, std::min<i64>(P, budget / (8 * std::max<i64>(N, 1)) / kGemmTJ * kGemmTJ));
+    DBuf<double> Xp(pc * N, s), S(pc * m, s);
+    DBuf<int32_t> dassign(rows_mode ? 1 : P, s);
+    std::vector<double> hrows;
+    if (rows_mode) hrows.resize(static_cast<size_t>(P * m));
+    for (i64 p0 = 0; p0 < P; p0 += pc) {
+      const i64 n = std::min<i64>(pc, P - p0);
+      Xp.zero();
+      PMMF_LAUNCH(k_panel_cols, blocks_for(n * 32, kThreads), kThreads, 0, s, n, dpool.get() + p0, a.ptr.get(),
+                  a.row.get(), a.val.get(), N, Xp.get());
+      dim3 grid(static_cast<unsigned>((n + kGemmTJ - 1) / kGemmTJ), static_cast<unsigned>((m + kGemmTA - 1) / kGemmTA));
+      k_score_gemm<<<grid, 256, 0, s>>>(N, static_cast<int>(n), m, Xp.get(), Xa.get(), nb.d_blk.get(), dpn.get() + p0,
+                                        dan.get(), S.get());
+      launch_counter().fetch_add(1, std::memory_order_relaxed);
+      PMMF_CUDA(cudaGetLastError());
+      if (rows_mode) {
+        S.download(hrows.data() + p0 * m, n * m);
+        PMMF_CUDA(cudaStreamSynchronize(s));
+      } else {
+        PMMF_LAUNCH(k_gemm_argmax, blocks_for(n * 32, kThreads), kThreads, 0, s, n, m, dpool.get() + p0, self.get(),
+                    S.get(), dassign.get() + p0);
+      }
+    }
+    if (trace_enabled()) {
+      PMMF_CUDA(cudaStreamSynchronize(s));
+      const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+      std::fprintf(stderr, "[pmmf]   score (gemm): pool=%lld anchors=%d rows=%lld chunk=%lld %.2f ms\n",
+                   static_cast<long long>(P), m, static_cast<long long>(N), static_cast<long long>(pc), ms);
+    }
+    if (rows_mode) {
+      *rows = std::move(hrows);
+    } else {
+      set_self(danch, danch, m, false);
+      *assign = dassign.to_host(P);
+    }
+  }
 };
 
 __global__ void k_set_self(int m, const int32_t* __restrict__ anchors, const int32_t* __restrict__ pos, bool on,

@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+cd tests && timeout 900 python -m pytest -x -q test_gpu_parity.py -m gpu -k "score_gemm or factorize_matches or dense_scoring" 2>&1 | tail -2; cd ..
+for w in c4 c3; do
+timeout 900 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err; echo "$w rc=$?"
+python -c "
+import json
+d=json.loads(open('gpurun_out/bench_$w.json').read().strip().splitlines()[-1])
+print(round(d['value']), 'ms/step', round(d['ms_per_step'],1), 'e2e', round(d['e2e']['value']), 'phases', d['phases_ms_last_step'])
+r=d['roofline']; print(' roofline', {k:r[k] for k in ('achieved','frac','kernel_ms_total','launches')})
+"
+done

@@ -66,3 +66,17 @@ def test_gram_paths(name, ratio, monkeypatch):
     monkeypatch.setenv("PMMF_B200_GRAM_DENSE_RATIO", ratio)
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf256_k3", "rbf512_k4",
+                                  "zero_cols_bypass", "partitioned_input", "oversize_recursion",
+                                  "undersize_repair", "c1_dense1024"])
+@pytest.mark.parametrize("gemm", ["1", "0"])
+def test_score_gemm_path(name, gemm, monkeypatch):
+    """Clustering scores through the dense GEMM scorer (gemm=1: zero-filled
+    panels, two-level block sums per thread) or never through it (gemm=0,
+    the sparse row-inverted scorer on dense inputs) — bit-exact either way,
+    including the orphan re-scoring table (rows mode) of undersize repair."""
+    monkeypatch.setenv("PMMF_B200_SCORE_GEMM", gemm)
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
