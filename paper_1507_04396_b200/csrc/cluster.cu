@@ -913,6 +913,7 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
              std::vector<std::vector<i64>>& out) {  // clustering.hpp:85-177
   ctx.max_depth = std::max(ctx.max_depth, depth);
   if (pool.empty()) return;
+  const auto t_rec = std::chrono::steady_clock::now();
   const auto& norm = *ctx.norm;
   std::vector<i64> shuffled;
   shuffled.reserve(pool.size());
@@ -939,7 +940,12 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
     an[a] = norm[anchors[a]];
   }
   std::vector<int32_t> assign;
+  const auto t_host0 = std::chrono::steady_clock::now();
   ctx.sc->run(dpool, pn, danch, an, false, &assign, nullptr);
+  if (trace_enabled() && depth == 0)
+    std::fprintf(stderr, "[pmmf]     pool setup %.2f ms, scorer %.2f ms\n",
+                 std::chrono::duration<double, std::milli>(t_host0 - t_rec).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count());
 
   std::vector<std::vector<i64>> clusters(m);
   std::vector<size_t> owner(pool.size());
@@ -972,6 +978,12 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
   auto pool_pos = [&](i64 g) {
     return static_cast<size_t>(std::lower_bound(pool.begin(), pool.end(), g) - pool.begin());
   };
+  // The reference re-sorts every alive cluster after each dissolution; a
+  // cluster's order is only observed when it is dissolved (its orphans are
+  // visited in ascending order) and at the end, so grown clusters are marked
+  // and sorted lazily at those two points.
+  const auto t_repair = std::chrono::steady_clock::now();
+  std::vector<uint8_t> dirty(m, 0);
   while (alive.size() > 1) {
     size_t worst = alive[0];
     for (size_t a : alive)
@@ -980,8 +992,8 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
     alive.erase(std::find(alive.begin(), alive.end(), worst));
     std::vector<i64> orphans = std::move(clusters[worst]);
     clusters[worst].clear();
+    if (dirty[worst]) std::sort(orphans.begin(), orphans.end());
     size_t orr = 0;
-    std::vector<size_t> grew;  // clusters that received orphans (the others stay sorted)
     for (i64 o : orphans) {
       const int64_t row = cand_row[pool_pos(o)];
       if (row < 0) fail(PMMF_INTERNAL, "clustering: orphan without a precomputed score row");
@@ -997,15 +1009,16 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
       }
       const size_t a = bs > 0.0 ? best : (orr++) % alive.size();
       clusters[alive[a]].push_back(o);
-      grew.push_back(alive[a]);
+      dirty[alive[a]] = 1;
     }
-    std::sort(grew.begin(), grew.end());
-    grew.erase(std::unique(grew.begin(), grew.end()), grew.end());
-    for (size_t a : grew) std::sort(clusters[a].begin(), clusters[a].end());
   }
+  if (trace_enabled() && depth == 0)
+    std::fprintf(stderr, "[pmmf]     undersize repair: %zu of %zu clusters alive, %.2f ms\n", alive.size(), m,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_repair).count());
   for (size_t a : alive) {  // oversize recursion (clustering.hpp:165-176)
     auto& mem = clusters[a];
     if (mem.empty()) continue;
+    if (dirty[a]) std::sort(mem.begin(), mem.end());
     if (static_cast<i64>(mem.size()) > ctx.c_max && depth < ctx.d_max) {
       const i64 sub = (static_cast<i64>(mem.size()) + ctx.c_max - 1) / ctx.c_max;
       recurse(ctx, std::move(mem), sub, depth + 1, rng, out);
