@@ -10,7 +10,7 @@
 //
 // Scheduling.  Rotations are grouped in dependency levels (search.cu); a
 // level's rotations touch disjoint ids.  Every rotation of a level is cut
-// into row-range partitions of <= kChunk rows of its longest input, so a
+// into row-range partitions of <= merge_chunk() rows of its longest input, so a
 // hub column with 10^6 entries is spread over hundreds of warps instead of
 // one.  Each partition is merged twice by one warp: a count pass (kept
 // outputs per column), an exclusive scan that yields exact arena offsets,
@@ -32,7 +32,14 @@ namespace pmmf_b200 {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunk = 1024;  // rows of the longest input per partition
+// rows of the longest input per partition (PMMF_B200_MERGE_CHUNK, default
+// 512; measured on config 4, write + count pass per step: 4096 -> 544 ms,
+// 1024 -> 285 ms, 512 -> 257 ms, 256 -> 267 ms)
+inline int merge_chunk() {
+  const char* e = std::getenv("PMMF_B200_MERGE_CHUNK");
+  const int v = e ? std::atoi(e) : 512;
+  return v >= 32 ? v : 512;
+}
 
 __device__ __forceinline__ int warp_lower_bound(int w, int r) {
   int lo = 0;
@@ -65,6 +72,7 @@ struct PassArgs {
   const double* aval;
   const int64_t* ioff;   // per level-rotation: first partition index (exclusive scan of nparts)
   int32_t* item_rot;     // partition -> level-rotation index (k_item_rot)
+  int chunk;             // partition size (rows of the longest input)
   i64 nrot;              // rotations in level
   i64 nitems;            // total partitions
   int64_t* cnt;          // K * nitems kept counts, layout [K*ioff_t + a*np_t + p]
@@ -84,7 +92,7 @@ struct PassArgs {
 };
 
 // Row range of partition p of rotation t: split points are rows of the
-// longest input at multiples of kChunk.
+// longest input at multiples of the chunk.
 template <int K>
 __device__ void partition_range(const PassArgs& A, int t, i64 p, i64 np, const int* id, i64 (&lo)[K], i64 (&hi)[K]) {
   int longest = 0;
@@ -98,8 +106,8 @@ __device__ void partition_range(const PassArgs& A, int t, i64 p, i64 np, const i
     }
   }
   const i64 lsrc = A.off[id[longest]];
-  const int r_lo = p == 0 ? INT_MIN : A.arow[lsrc + p * kChunk];
-  const int r_hi = p == np - 1 ? INT_MAX : A.arow[lsrc + (p + 1) * kChunk];
+  const int r_lo = p == 0 ? INT_MIN : A.arow[lsrc + p * A.chunk];
+  const int r_hi = p == np - 1 ? INT_MAX : A.arow[lsrc + (p + 1) * A.chunk];
 #pragma unroll
   for (int b = 0; b < K; ++b) {
     const i64 s = A.off[id[b]], e = s + A.len[id[b]];
@@ -314,7 +322,7 @@ __global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long
     Lmax = max(Lmax, L);
     S += static_cast<unsigned long long>(L);
   }
-  nparts[i] = max(1, (Lmax + kChunk - 1) / kChunk);
+  nparts[i] = max(1, (Lmax + A.chunk - 1) / A.chunk);
   atomicAdd(in_entries, S);
 }
 
@@ -723,12 +731,81 @@ struct LevelScratch {
   size_t scan_bytes = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // profiled write passes
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> cev;  // profiled count passes
+  PassArgs prev{};  // level whose commit is deferred to the next plan (nrot 0: none)
   double rot_bytes = 0.0;
 };
+
+// Single-CTA level plan for levels of <= kPlanMax rotations (most levels):
+// the previous level's deferred commit, then nparts, their exclusive scan,
+// nitems and the item -> rotation map in one launch instead of six.
+constexpr int kPlanThreads = 1024, kPlanPer = 8, kPlanMax = kPlanThreads * kPlanPer;
+template <int K>
+__global__ void __launch_bounds__(kPlanThreads, 1) k_level_plan(PassArgs A, PassArgs prev, const i64* __restrict__ rbase,
+                                                             const int32_t* __restrict__ rlen, i64* __restrict__ off,
+                                                             int32_t* __restrict__ len, int64_t* __restrict__ np,
+                                                             int64_t* __restrict__ ioff, int64_t* __restrict__ nitems,
+                                                             int32_t* __restrict__ item_rot,
+                                                             unsigned long long* __restrict__ in_entries) {
+  using Scan = cub::BlockScan<long long, kPlanThreads>;
+  using Red = cub::BlockReduce<unsigned long long, kPlanThreads>;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Red::TempStorage red;
+  } tmp;
+  const bool ok = *reinterpret_cast<volatile const int32_t*>(A.ovf) == INT_MAX;
+  if (ok && prev.nrot > 0) {  // k_commit_level of the previous level
+    for (i64 i = threadIdx.x; i < prev.nrot; i += kPlanThreads) {
+      const int t = prev.rots[i];
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        const int id = prev.ids[static_cast<i64>(t) * K + a] - static_cast<int>(prev.col0);
+        off[id] = rbase[K * i + a];
+        len[id] = rlen[K * i + a];
+      }
+    }
+  }
+  __syncthreads();
+  __shared__ int mine[kPlanMax];
+  const i64 i0 = static_cast<i64>(threadIdx.x) * kPlanPer;
+  long long sum = 0;
+  unsigned long long S = 0;
+  for (int j = 0; j < kPlanPer; ++j) {
+    const i64 i = i0 + j;
+    if (i >= A.nrot) break;
+    const int t = A.rots[i];
+    int Lmax = 0;
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      const int L = len[A.ids[static_cast<i64>(t) * K + b] - A.col0];
+      Lmax = max(Lmax, L);
+      S += static_cast<unsigned long long>(L);
+    }
+    mine[i0 + j] = max(1, (Lmax + A.chunk - 1) / A.chunk);
+    sum += mine[i0 + j];
+  }
+  long long excl = 0, total = 0;
+  Scan(tmp.scan).ExclusiveSum(sum, excl, total);
+  for (int j = 0; j < kPlanPer; ++j) {
+    const i64 i = i0 + j;
+    if (i >= A.nrot) break;
+    const int n = mine[i0 + j];
+    np[i] = n;
+    ioff[i] = excl;
+    for (int p = 0; p < n; ++p) item_rot[excl + p] = static_cast<int32_t>(i);
+    excl += n;
+  }
+  if (threadIdx.x == 0) *nitems = total;
+  __syncthreads();
+  const unsigned long long St = Red(tmp.red).Sum(S);
+  if (threadIdx.x == 0) atomicAdd(in_entries, St);
+}
 
 constexpr int kPersistentBlocks = 148 * 8;
 
 // One dependency level of a batch, entirely on the device (no host sync).
+template <int K>
+void flush_commit(Batch& B, LevelScratch& S, cudaStream_t s);
+
 template <int K>
 void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* rots, i64 nrot, int level,
                cudaStream_t s) {
@@ -746,6 +823,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.wval = B.val.get();
   A.ioff = S.ioff.get();
   A.item_rot = S.item_rot.get();
+  A.chunk = merge_chunk();
   A.cnt = S.cnt.get();
   A.pos = S.pos.get();
   A.nitems = S.max_items;  // bound; kernels read the exact count from S.nitems
@@ -756,14 +834,22 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.level = level;
   A.rbase = S.rbase.get();
   A.rlen = S.rlen.get();
-  PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
-  {
-    size_t tmp = S.scan_bytes;
-    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
+  if (nrot <= kPlanMax) {
+    PassArgs P = S.prev;  // deferred commit of the previous level (nrot 0: none)
+    PMMF_LAUNCH(k_level_plan<K>, 1, kPlanThreads, 0, s, A, P, S.rbase.get(), S.rlen.get(), B.off.get(), B.len.get(),
+                S.np.get(), S.ioff.get(), S.nitems.get(), S.item_rot.get(), S.in_entries.get());
+  } else {
+    flush_commit<K>(B, S, s);
+    PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
+    {
+      size_t tmp = S.scan_bytes;
+      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
+    }
+    PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
+    PMMF_LAUNCH(k_item_rot, blocks_for(nrot, kThreads), kThreads, 0, s, nrot, S.ioff.get(), S.np.get(),
+                S.item_rot.get());
   }
-  PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
-  PMMF_LAUNCH(k_item_rot, blocks_for(nrot, kThreads), kThreads, 0, s, nrot, S.ioff.get(), S.np.get(),
-              S.item_rot.get());
+  S.prev = PassArgs{};
   cudaEvent_t c0 = nullptr, c1 = nullptr;
   if (prof_enabled()) {
     c0 = EventPool::get().take();
@@ -789,8 +875,16 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     S.ev.push_back({e0, e1});
     S.rot_bytes += static_cast<double>(nrot) * (8.0 * K * K + 4.0 * K);
   }
-  PMMF_LAUNCH(k_commit_level<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.rbase.get(), S.rlen.get(), S.ovf.get(),
-              B.off.get(), B.len.get());
+  S.prev = A;  // committed by the next level's plan or by flush_commit
+}
+
+// Commit a deferred level (before anything else reads off/len).
+template <int K>
+void flush_commit(Batch& B, LevelScratch& S, cudaStream_t s) {
+  if (S.prev.nrot <= 0) return;
+  PMMF_LAUNCH(k_commit_level<K>, blocks_for(S.prev.nrot, kThreads), kThreads, 0, s, S.prev, S.rbase.get(),
+              S.rlen.get(), S.ovf.get(), B.off.get(), B.len.get());
+  S.prev = PassArgs{};
 }
 
 __global__ void k_plan(const int32_t* __restrict__ nrot, const int64_t* __restrict__ base,
@@ -983,7 +1077,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     LevelScratch S;
     const int K = plan.k;
     auto size_items = [&] {
-      S.max_items = max_rot + B.cap / kChunk + 1;
+      S.max_items = max_rot + B.cap / merge_chunk() + 1;
       S.cnt.alloc(K * S.max_items, s);
       S.pos.alloc(K * S.max_items, s);
       S.item_rot.alloc(S.max_items, s);
@@ -1036,6 +1130,15 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
           case 8: run_level<8>(B, S, plan, rots, hi - lo, L, s); break;
           default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
         }
+      }
+      switch (K) {  // the last level's deferred commit
+        case 2: flush_commit<2>(B, S, s); break;
+        case 3: flush_commit<3>(B, S, s); break;
+        case 4: flush_commit<4>(B, S, s); break;
+        case 5: flush_commit<5>(B, S, s); break;
+        case 6: flush_commit<6>(B, S, s); break;
+        case 7: flush_commit<7>(B, S, s); break;
+        default: flush_commit<8>(B, S, s); break;
       }
       int32_t ovf = 0;
       PMMF_CUDA(cudaMemcpyAsync(&ovf, S.ovf.get(), sizeof(ovf), cudaMemcpyDeviceToHost, s));
