@@ -497,42 +497,79 @@ __global__ void k_len64(i64 N, const int32_t* __restrict__ len, i64* __restrict_
 // Count / copy the live columns of a batch, optionally keeping only rows
 // flagged in keep_row (lean mode: rows the next stage reads) unless the
 // column itself is flagged in keep_all_col.
-__global__ void k_final_count(i64 N, i64 col0, const i64* __restrict__ off, const int32_t* __restrict__ len,
+// Column segments of <= kSeg entries: per-column kernels over the batch
+// arena (final copy, mass count/gather) run warp per segment, so a hub
+// column of 10^5-10^6 entries is spread over many warps instead of being
+// the tail of the launch.
+constexpr int kSeg = 2048;
+__global__ void k_seg_n(i64 N, const int32_t* __restrict__ len, i64* __restrict__ nseg) {
+  const i64 w = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (w > N) return;
+  nseg[w] = w == N ? 0 : max(1, (len[w] + kSeg - 1) / kSeg);
+}
+__global__ void k_seg_fill(i64 N, const i64* __restrict__ sfirst, int32_t* __restrict__ seg_col) {
+  const i64 w = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (w >= N) return;
+  for (i64 q = sfirst[w]; q < sfirst[w + 1]; ++q) seg_col[q] = static_cast<int32_t>(w);
+}
+struct Segs {
+  i64 n = 0;
+  DBuf<i64> first;      // N + 1: first segment of column w
+  DBuf<int32_t> col;    // segment -> column
+};
+// Entry range of segment q inside its column.
+__device__ __forceinline__ void seg_range(const Segs* /*unused*/, i64 q, const int32_t* __restrict__ seg_col,
+                                          const i64* __restrict__ sfirst, const int32_t* __restrict__ len, i64& w,
+                                          int& b, int& e) {
+  w = seg_col[q];
+  b = static_cast<int>((q - sfirst[w]) * kSeg);
+  e = min(len[w], b + kSeg);
+}
+
+__global__ void k_final_count(i64 S, i64 col0, const int32_t* __restrict__ seg_col, const i64* __restrict__ sfirst,
+                              const i64* __restrict__ off, const int32_t* __restrict__ len,
                               const int32_t* __restrict__ arow, const uint8_t* __restrict__ keep_row,
                               const uint8_t* __restrict__ keep_all_col, i64* __restrict__ cnt) {
-  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const i64 q = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w > N) return;
-  if (w == N) {
-    if (lane == 0) cnt[N] = 0;
+  if (q > S) return;
+  if (q == S) {
+    if (lane == 0) cnt[S] = 0;
     return;
   }
+  i64 w;
+  int b, e;
+  seg_range(nullptr, q, seg_col, sfirst, len, w, b, e);
   const bool all = keep_row == nullptr || (keep_all_col != nullptr && keep_all_col[col0 + w]);
   if (all) {
-    if (lane == 0) cnt[w] = len[w];
+    if (lane == 0) cnt[q] = e - b;
     return;
   }
   int c = 0;
-  for (int i = lane; i < len[w]; i += 32) c += keep_row[arow[off[w] + i]];
+  for (int i = b + lane; i < e; i += 32) c += keep_row[arow[off[w] + i]];
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0) cnt[w] = c;
+  if (lane == 0) cnt[q] = c;
 }
-__global__ void k_final_copy(i64 N, i64 col0, const i64* __restrict__ off, const int32_t* __restrict__ len,
+__global__ void k_final_copy(i64 S, i64 col0, const int32_t* __restrict__ seg_col, const i64* __restrict__ sfirst,
+                             const i64* __restrict__ off, const int32_t* __restrict__ len,
                              const int32_t* __restrict__ arow, const double* __restrict__ aval,
                              const uint8_t* __restrict__ keep_row, const uint8_t* __restrict__ keep_all_col,
                              const i64* __restrict__ pos, int32_t* __restrict__ orow, double* __restrict__ oval) {
-  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const i64 q = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= N) return;
+  if (q >= S) return;
+  i64 w;
+  int b, e;
+  seg_range(nullptr, q, seg_col, sfirst, len, w, b, e);
   const bool all = keep_row == nullptr || (keep_all_col != nullptr && keep_all_col[col0 + w]);
-  i64 o = pos[w];
+  i64 o = pos[q];
   const i64 s = off[w];
-  for (int base = 0; base < len[w]; base += 32) {
+  for (int base = b; base < e; base += 32) {
     const int i = base + lane;
     int r = 0;
     double v = 0.0;
     bool k = false;
-    if (i < len[w]) {
+    if (i < e) {
       r = arow[s + i];
       v = aval[s + i];
       k = all || keep_row[r];
@@ -545,6 +582,11 @@ __global__ void k_final_copy(i64 N, i64 col0, const i64* __restrict__ off, const
     }
     o += __popc(m);
   }
+}
+// Column pointers of a piece from its segment offsets.
+__global__ void k_seg_ptr(i64 N, const i64* __restrict__ sfirst, const i64* __restrict__ spos, i64* __restrict__ ptr) {
+  const i64 w = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (w <= N) ptr[w] = spos[sfirst[w]];
 }
 
 __global__ void k_paged_init_local(i64 N, const i64* __restrict__ ptr, i64 col0, i64 e0, i64* __restrict__ off,
@@ -617,21 +659,25 @@ struct Batch {
 // Per column c: the entries of retired rows g that it contributes to the
 // mass of g (c taken when it survives or retires after g); the diagonal
 // entry (g == c) goes to diag.
-__global__ void k_mass_count(i64 N, i64 col0, const i64* __restrict__ off, const int32_t* __restrict__ len,
+__global__ void k_mass_count(i64 S, i64 col0, const int32_t* __restrict__ seg_col, const i64* __restrict__ sfirst,
+                             const i64* __restrict__ off, const int32_t* __restrict__ len,
                              const int32_t* __restrict__ arow, const double* __restrict__ aval, MassSpec M,
                              i64* __restrict__ cnt) {
-  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const i64 q = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w > N) return;
-  if (w == N) {
-    if (lane == 0) cnt[N] = 0;
+  if (q > S) return;
+  if (q == S) {
+    if (lane == 0) cnt[S] = 0;
     return;
   }
+  i64 w;
+  int b, e;
+  seg_range(nullptr, q, seg_col, sfirst, len, w, b, e);
   const int32_t c = static_cast<int32_t>(col0 + w);
   const int32_t key = M.col_key[c];
   const i64 s0 = off[w];
   int n = 0;
-  for (int i = lane; i < len[w]; i += 32) {
+  for (int i = b + lane; i < e; i += 32) {
     const int32_t g = arow[s0 + i];
     const int32_t rg = M.row_rank[g];
     if (rg < 0) continue;
@@ -641,35 +687,39 @@ __global__ void k_mass_count(i64 N, i64 col0, const i64* __restrict__ off, const
       n += key > rg;
   }
   for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-  if (lane == 0) cnt[w] = n;
+  if (lane == 0) cnt[q] = n;
 }
-// Columns [w0, w1) of the batch: (rank of g, v^2) of the taken entries,
-// column-major.
-__global__ void k_mass_gather(i64 w0, i64 w1, i64 col0, const i64* __restrict__ off,
+// Segments [q0, q1) of the batch: (rank of g, v^2) of the taken entries,
+// in column order.
+__global__ void k_mass_gather(i64 q0, i64 q1, i64 col0, const int32_t* __restrict__ seg_col,
+                              const i64* __restrict__ sfirst, const i64* __restrict__ off,
                               const int32_t* __restrict__ len, const int32_t* __restrict__ arow,
                               const double* __restrict__ aval, MassSpec M, const i64* __restrict__ pos,
                               int32_t* __restrict__ okey, double* __restrict__ osq) {
-  const i64 w = w0 + ((blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5);
+  const i64 q = q0 + ((blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
-  if (w >= w1) return;
+  if (q >= q1) return;
+  i64 w;
+  int b, e;
+  seg_range(nullptr, q, seg_col, sfirst, len, w, b, e);
   const int32_t c = static_cast<int32_t>(col0 + w);
   const int32_t key = M.col_key[c];
   const i64 s0 = off[w];
-  i64 o = pos[w] - pos[w0];
-  for (int b = 0; b < len[w]; b += 32) {
-    const int i = b + lane;
-    int32_t g = 0;
+  i64 o = pos[q] - pos[q0];
+  for (int base = b; base < e; base += 32) {
+    const int i = base + lane;
+    int32_t rg = -1;
     bool take = false;
-    if (i < len[w]) {
-      g = arow[s0 + i];
-      const int32_t rg = M.row_rank[g];
+    if (i < e) {
+      const int32_t g = arow[s0 + i];
+      rg = M.row_rank[g];
       take = rg >= 0 && g != c && key > rg;
     }
     const unsigned m = __ballot_sync(0xffffffffu, take);
     if (take) {
       const i64 d = o + __popc(m & ((1u << lane) - 1u));
       const double v = aval[s0 + i];
-      okey[d] = M.row_rank[g];
+      okey[d] = rg;
       osq[d] = dmul(v, v);
     }
     o += __popc(m);
@@ -731,81 +781,12 @@ struct LevelScratch {
   size_t scan_bytes = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // profiled write passes
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> cev;  // profiled count passes
-  PassArgs prev{};  // level whose commit is deferred to the next plan (nrot 0: none)
   double rot_bytes = 0.0;
 };
-
-// Single-CTA level plan for levels of <= kPlanMax rotations (most levels):
-// the previous level's deferred commit, then nparts, their exclusive scan,
-// nitems and the item -> rotation map in one launch instead of six.
-constexpr int kPlanThreads = 1024, kPlanPer = 8, kPlanMax = kPlanThreads * kPlanPer;
-template <int K>
-__global__ void __launch_bounds__(kPlanThreads, 1) k_level_plan(PassArgs A, PassArgs prev, const i64* __restrict__ rbase,
-                                                             const int32_t* __restrict__ rlen, i64* __restrict__ off,
-                                                             int32_t* __restrict__ len, int64_t* __restrict__ np,
-                                                             int64_t* __restrict__ ioff, int64_t* __restrict__ nitems,
-                                                             int32_t* __restrict__ item_rot,
-                                                             unsigned long long* __restrict__ in_entries) {
-  using Scan = cub::BlockScan<long long, kPlanThreads>;
-  using Red = cub::BlockReduce<unsigned long long, kPlanThreads>;
-  __shared__ union {
-    typename Scan::TempStorage scan;
-    typename Red::TempStorage red;
-  } tmp;
-  const bool ok = *reinterpret_cast<volatile const int32_t*>(A.ovf) == INT_MAX;
-  if (ok && prev.nrot > 0) {  // k_commit_level of the previous level
-    for (i64 i = threadIdx.x; i < prev.nrot; i += kPlanThreads) {
-      const int t = prev.rots[i];
-#pragma unroll
-      for (int a = 0; a < K; ++a) {
-        const int id = prev.ids[static_cast<i64>(t) * K + a] - static_cast<int>(prev.col0);
-        off[id] = rbase[K * i + a];
-        len[id] = rlen[K * i + a];
-      }
-    }
-  }
-  __syncthreads();
-  __shared__ int mine[kPlanMax];
-  const i64 i0 = static_cast<i64>(threadIdx.x) * kPlanPer;
-  long long sum = 0;
-  unsigned long long S = 0;
-  for (int j = 0; j < kPlanPer; ++j) {
-    const i64 i = i0 + j;
-    if (i >= A.nrot) break;
-    const int t = A.rots[i];
-    int Lmax = 0;
-#pragma unroll
-    for (int b = 0; b < K; ++b) {
-      const int L = len[A.ids[static_cast<i64>(t) * K + b] - A.col0];
-      Lmax = max(Lmax, L);
-      S += static_cast<unsigned long long>(L);
-    }
-    mine[i0 + j] = max(1, (Lmax + A.chunk - 1) / A.chunk);
-    sum += mine[i0 + j];
-  }
-  long long excl = 0, total = 0;
-  Scan(tmp.scan).ExclusiveSum(sum, excl, total);
-  for (int j = 0; j < kPlanPer; ++j) {
-    const i64 i = i0 + j;
-    if (i >= A.nrot) break;
-    const int n = mine[i0 + j];
-    np[i] = n;
-    ioff[i] = excl;
-    for (int p = 0; p < n; ++p) item_rot[excl + p] = static_cast<int32_t>(i);
-    excl += n;
-  }
-  if (threadIdx.x == 0) *nitems = total;
-  __syncthreads();
-  const unsigned long long St = Red(tmp.red).Sum(S);
-  if (threadIdx.x == 0) atomicAdd(in_entries, St);
-}
 
 constexpr int kPersistentBlocks = 148 * 8;
 
 // One dependency level of a batch, entirely on the device (no host sync).
-template <int K>
-void flush_commit(Batch& B, LevelScratch& S, cudaStream_t s);
-
 template <int K>
 void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* rots, i64 nrot, int level,
                cudaStream_t s) {
@@ -834,22 +815,14 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.level = level;
   A.rbase = S.rbase.get();
   A.rlen = S.rlen.get();
-  if (nrot <= kPlanMax) {
-    PassArgs P = S.prev;  // deferred commit of the previous level (nrot 0: none)
-    PMMF_LAUNCH(k_level_plan<K>, 1, kPlanThreads, 0, s, A, P, S.rbase.get(), S.rlen.get(), B.off.get(), B.len.get(),
-                S.np.get(), S.ioff.get(), S.nitems.get(), S.item_rot.get(), S.in_entries.get());
-  } else {
-    flush_commit<K>(B, S, s);
-    PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
-    {
-      size_t tmp = S.scan_bytes;
-      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
-    }
-    PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
-    PMMF_LAUNCH(k_item_rot, blocks_for(nrot, kThreads), kThreads, 0, s, nrot, S.ioff.get(), S.np.get(),
-                S.item_rot.get());
+  PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
+  {
+    size_t tmp = S.scan_bytes;
+    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
   }
-  S.prev = PassArgs{};
+  PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
+  PMMF_LAUNCH(k_item_rot, blocks_for(nrot, kThreads), kThreads, 0, s, nrot, S.ioff.get(), S.np.get(),
+              S.item_rot.get());
   cudaEvent_t c0 = nullptr, c1 = nullptr;
   if (prof_enabled()) {
     c0 = EventPool::get().take();
@@ -875,16 +848,8 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     S.ev.push_back({e0, e1});
     S.rot_bytes += static_cast<double>(nrot) * (8.0 * K * K + 4.0 * K);
   }
-  S.prev = A;  // committed by the next level's plan or by flush_commit
-}
-
-// Commit a deferred level (before anything else reads off/len).
-template <int K>
-void flush_commit(Batch& B, LevelScratch& S, cudaStream_t s) {
-  if (S.prev.nrot <= 0) return;
-  PMMF_LAUNCH(k_commit_level<K>, blocks_for(S.prev.nrot, kThreads), kThreads, 0, s, S.prev, S.rbase.get(),
-              S.rlen.get(), S.ovf.get(), B.off.get(), B.len.get());
-  S.prev = PassArgs{};
+  PMMF_LAUNCH(k_commit_level<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.rbase.get(), S.rlen.get(), S.ovf.get(),
+              B.off.get(), B.len.get());
 }
 
 __global__ void k_plan(const int32_t* __restrict__ nrot, const int64_t* __restrict__ base,
@@ -953,7 +918,17 @@ void build_plan(LevelPlan& plan, const SearchOut& so, const DBuf<int64_t>& out_b
 namespace {
 // Masses of the retired rows over the final columns of batch B, in column
 // chunks of <= chunk_nnz taken entries (ascending column order).
-void batch_masses(const Batch& B, const MassSpec& M, cudaStream_t s) {
+void build_segs(const Batch& B, Segs& G, cudaStream_t s) {
+  DBuf<i64> nseg(B.N + 1, s);
+  G.first.alloc(B.N + 1, s);
+  PMMF_LAUNCH(k_seg_n, blocks_for(B.N + 1, kThreads), kThreads, 0, s, B.N, B.len.get(), nseg.get());
+  exscan(nseg.get(), G.first.get(), B.N + 1, s);
+  G.n = read_i64(G.first.get() + B.N, s);
+  G.col.alloc(std::max<i64>(G.n, 1), s);
+  PMMF_LAUNCH(k_seg_fill, blocks_for(B.N, kThreads), kThreads, 0, s, B.N, G.first.get(), G.col.get());
+}
+
+void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, cudaStream_t s) {
   const bool tr = trace_enabled();
   double tms[4] = {0, 0, 0, 0};
   auto tl = std::chrono::steady_clock::now();
@@ -964,14 +939,15 @@ void batch_masses(const Batch& B, const MassSpec& M, cudaStream_t s) {
     tms[k] += std::chrono::duration<double, std::milli>(now - tl).count();
     tl = now;
   };
-  DBuf<i64> cnt(B.N + 1, s), pos(B.N + 1, s);
-  PMMF_LAUNCH(k_mass_count, blocks_for((B.N + 1) * 32, kThreads), kThreads, 0, s, B.N, B.col0, B.off.get(),
-              B.len.get(), B.row.get(), B.val.get(), M, cnt.get());
-  exscan(cnt.get(), pos.get(), B.N + 1, s);
-  const std::vector<i64> hp = pos.to_host(B.N + 1);
-  if (hp[B.N] == 0) return;
-  const i64 chunk = std::max<i64>(256, std::min<i64>(M.chunk_nnz, i64{1} << 30));
-  const i64 cap = std::min<i64>(hp[B.N], chunk);
+  const i64 S = G.n;
+  DBuf<i64> cnt(S + 1, s), pos(S + 1, s);
+  PMMF_LAUNCH(k_mass_count, blocks_for((S + 1) * 32, kThreads), kThreads, 0, s, S, B.col0, G.col.get(), G.first.get(),
+              B.off.get(), B.len.get(), B.row.get(), B.val.get(), M, cnt.get());
+  exscan(cnt.get(), pos.get(), S + 1, s);
+  const std::vector<i64> hp = pos.to_host(S + 1);
+  if (hp[S] == 0) return;
+  const i64 chunk = std::max<i64>(kSeg, std::min<i64>(M.chunk_nnz, i64{1} << 30));
+  const i64 cap = std::min<i64>(hp[S], chunk);
   // buckets of 2^shift ranks: a 16-bit sort key (two radix passes)
   const int rb = std::max(1, bits_for(std::max<i64>(M.n_retired - 1, 1)));
   const int shift = std::max(0, rb - 16);
@@ -999,16 +975,16 @@ void batch_masses(const Batch& B, const MassSpec& M, cudaStream_t s) {
   constexpr int kWarpsPerBlock = 8;
   const size_t smem = static_cast<size_t>(kWarpsPerBlock) * (size_t{1} << shift) * sizeof(double);
   int nchunks = 0;
-  i64 w0 = 0;
-  while (w0 < B.N) {
+  i64 w0 = 0;  // segments [w0, w1) per chunk (a segment holds <= kSeg <= chunk entries)
+  while (w0 < S) {
     i64 w1 = w0 + 1;
-    while (w1 < B.N && hp[w1 + 1] - hp[w0] <= chunk) ++w1;
+    while (w1 < S && hp[w1 + 1] - hp[w0] <= chunk) ++w1;
     const i64 n = hp[w1] - hp[w0];
     if (n > 0) {
-      ensure(n);  // a single column above the chunk size
+      ensure(n);
       ++nchunks;
-      PMMF_LAUNCH(k_mass_gather, blocks_for((w1 - w0) * 32, kThreads), kThreads, 0, s, w0, w1, B.col0, B.off.get(),
-                  B.len.get(), B.row.get(), B.val.get(), M, pos.get(), k1.get(), v1.get());
+      PMMF_LAUNCH(k_mass_gather, blocks_for((w1 - w0) * 32, kThreads), kThreads, 0, s, w0, w1, B.col0, G.col.get(),
+                  G.first.get(), B.off.get(), B.len.get(), B.row.get(), B.val.get(), M, pos.get(), k1.get(), v1.get());
       lap(1);
       cub::DoubleBuffer<int32_t> kd(k1.get(), k2.get());
       cub::DoubleBuffer<double> vd(v1.get(), v2.get());
@@ -1023,7 +999,7 @@ void batch_masses(const Batch& B, const MassSpec& M, cudaStream_t s) {
   }
   if (tr)
     std::fprintf(stderr, "[pmmf]     masses: %lld taken in %d chunks: count %.1f gather %.1f sort %.1f sums %.1f ms\n",
-                 static_cast<long long>(hp[B.N]), nchunks, tms[0], tms[1], tms[2], tms[3]);
+                 static_cast<long long>(hp[S]), nchunks, tms[0], tms[1], tms[2], tms[3]);
 }
 }  // namespace
 
@@ -1131,15 +1107,6 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
           default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
         }
       }
-      switch (K) {  // the last level's deferred commit
-        case 2: flush_commit<2>(B, S, s); break;
-        case 3: flush_commit<3>(B, S, s); break;
-        case 4: flush_commit<4>(B, S, s); break;
-        case 5: flush_commit<5>(B, S, s); break;
-        case 6: flush_commit<6>(B, S, s); break;
-        case 7: flush_commit<7>(B, S, s); break;
-        default: flush_commit<8>(B, S, s); break;
-      }
       int32_t ovf = 0;
       PMMF_CUDA(cudaMemcpyAsync(&ovf, S.ovf.get(), sizeof(ovf), cudaMemcpyDeviceToHost, s));
       PMMF_CUDA(cudaStreamSynchronize(s));
@@ -1188,24 +1155,28 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       prof_add_n("rotate_count", static_cast<int64_t>(S.cev.size()), cms, 4.0 * static_cast<double>(io[0]));
     }
     double t_mass = 0.0;
+    Segs G;
+    build_segs(B, G, s);
     if (ms) {
-      batch_masses(B, *ms, s);
+      batch_masses(B, G, *ms, s);
       if (tr) t_mass = since(tb);
     }
     // finalize into a compact piece
     Piece P;
     P.c0 = B.col0;
     P.c1 = B.col0 + B.N;
-    DBuf<i64> cnt(B.N + 1, s);
+    DBuf<i64> cnt(G.n + 1, s), spos(G.n + 1, s);
     P.ptr.alloc(B.N + 1, s);
-    PMMF_LAUNCH(k_final_count, blocks_for((B.N + 1) * 32, kThreads), kThreads, 0, s, B.N, B.col0, B.off.get(),
-                B.len.get(), B.row.get(), keep_row, keep_all_col, cnt.get());
-    exscan(cnt.get(), P.ptr.get(), B.N + 1, s);
-    P.nnz = read_i64(P.ptr.get() + B.N, s);
+    PMMF_LAUNCH(k_final_count, blocks_for((G.n + 1) * 32, kThreads), kThreads, 0, s, G.n, B.col0, G.col.get(),
+                G.first.get(), B.off.get(), B.len.get(), B.row.get(), keep_row, keep_all_col, cnt.get());
+    exscan(cnt.get(), spos.get(), G.n + 1, s);
+    PMMF_LAUNCH(k_seg_ptr, blocks_for(B.N + 1, kThreads), kThreads, 0, s, B.N, G.first.get(), spos.get(), P.ptr.get());
+    P.nnz = read_i64(spos.get() + G.n, s);
     P.row.alloc(std::max<i64>(P.nnz, 1), s);
     P.val.alloc(std::max<i64>(P.nnz, 1), s);
-    PMMF_LAUNCH(k_final_copy, blocks_for(B.N * 32, kThreads), kThreads, 0, s, B.N, B.col0, B.off.get(), B.len.get(),
-                B.row.get(), B.val.get(), keep_row, keep_all_col, P.ptr.get(), P.row.get(), P.val.get());
+    PMMF_LAUNCH(k_final_copy, blocks_for(G.n * 32, kThreads), kThreads, 0, s, G.n, B.col0, G.col.get(), G.first.get(),
+                B.off.get(), B.len.get(), B.row.get(), B.val.get(), keep_row, keep_all_col, spos.get(), P.row.get(),
+                P.val.get());
     if (tr)
       std::fprintf(stderr, "[pmmf]     batch cols %lld: levels %.1f compact %.1f masses %.1f final %.1f ms (nnz in %lld out %lld)\n",
                    static_cast<long long>(B.N), t_levels, t_compact, t_mass, since(tb), static_cast<long long>(ne),
