@@ -419,7 +419,8 @@ def main():
         c, ms, by = prof["rotate_write"]
         achieved = (by / 1e9) / (ms / 1e3) if ms > 0 else 0.0
         roof = {"bound": "hbm", "kernel": "k_merge_p<2,true> (rotation stream, write pass)", "achieved": achieved,
-                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": merge_traffic(),
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": merge_traffic() if args.workload == "c4" else None,
                 "launches": c, "kernel_ms_total": ms, "algorithmic_bytes_total": by, "peak_source": peak_src,
                 "share_of_step": ms / sum(step_ms)}
         if "rotate_count" in prof:

@@ -309,6 +309,44 @@ __device__ __forceinline__ void merge_write2(const PassArgs& A, const double (&q
   }
 }
 
+// Dense partitions: when every input holds exactly the same contiguous rows
+// r0..r0+L-1 (dense clusters: configs 1 and 3), the union merge is the
+// identity on the structure and the rotation is elementwise -- a pure
+// stream.  Same arithmetic per entry ((0 + q(a,0) v_0) + q(a,1) v_1) + ...;
+// outputs keep exact zeros (value-neutral, as on the k = 2 path).
+template <int K>
+__device__ __forceinline__ int identical_rows(const PassArgs& A, const i64 (&b)[K], const i64 (&e)[K], int& r0) {
+  const i64 L = e[0] - b[0];
+  if (L <= 0) return -1;
+#pragma unroll
+  for (int k = 1; k < K; ++k)
+    if (e[k] - b[k] != L) return -1;
+  r0 = A.arow[b[0]];
+  const int r1 = A.arow[e[0] - 1];
+  if (static_cast<i64>(r1) - r0 != L - 1) return -1;
+#pragma unroll
+  for (int k = 1; k < K; ++k)
+    if (A.arow[b[k]] != r0 || A.arow[e[k] - 1] != r1) return -1;
+  return static_cast<int>(L);
+}
+template <int K>
+__device__ __forceinline__ void write_dense(const PassArgs& A, const double (&q)[K][K], const i64 (&b)[K], int L,
+                                            int r0, const i64 (&dst)[K]) {
+  for (int i = threadIdx.x & 31; i < L; i += 32) {
+    double v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = A.aval[b[k] + i];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) acc = dadd(acc, dmul(q[a][k], v[k]));
+      A.wrow[dst[a] + i] = r0 + i;
+      A.wval[dst[a] + i] = acc;
+    }
+  }
+}
+
 template <int K>
 __global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long long* __restrict__ in_entries) {
   const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
@@ -417,7 +455,7 @@ __global__ void k_commit_level(PassArgs A, const i64* __restrict__ rbase, const 
 // Persistent variant: warps stride over the level's partitions; the
 // partition count is read from the device.
 template <int K, bool kWrite>
-__global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, const int32_t* __restrict__ ovf) {
+__global__ void __launch_bounds__(256, K == 2 ? 6 : 2) k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, const int32_t* __restrict__ ovf) {
   if (*reinterpret_cast<volatile const int32_t*>(ovf) != INT_MAX) return;
   const i64 nitems = *nitems_d;
   const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
@@ -444,7 +482,35 @@ __global__ void k_merge_p(PassArgs A, const int64_t* __restrict__ nitems_d, cons
       kept[a] = 0;
       dst[a] = (kWrite && !(K == 2 && np == 1)) ? A.pos[K * A.ioff[ri] + a * np + p] : 0;
     }
-    if constexpr (K == 2) {
+    int r0 = 0;
+    const int dl = identical_rows<K>(A, beg, end, r0);
+    if (dl >= 0) {
+      if (K == 2 && np == 1) {  // self-allocating single partition (below), dense
+        unsigned long long b0 = 0;
+        if ((threadIdx.x & 31) == 0) b0 = atomicAdd(A.cursor, static_cast<unsigned long long>(K) * dl);
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (static_cast<i64>(b0) + static_cast<i64>(K) * dl > A.cap) {
+          if ((threadIdx.x & 31) == 0) atomicMin(A.ovf, A.level);
+          continue;
+        }
+        i64 d2[K];
+#pragma unroll
+        for (int a = 0; a < K; ++a) d2[a] = static_cast<i64>(b0) + static_cast<i64>(a) * dl;
+        write_dense<K>(A, q, beg, dl, r0, d2);
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+          for (int a = 0; a < K; ++a) {
+            A.rbase[K * ri + a] = d2[a];
+            A.rlen[K * ri + a] = dl;
+          }
+          atomicAdd(A.out_entries, static_cast<unsigned long long>(K) * dl);
+        }
+        continue;
+      }
+      if (kWrite) write_dense<K>(A, q, beg, dl, r0, dst);
+#pragma unroll
+      for (int a = 0; a < K; ++a) kept[a] = dl;
+    } else if constexpr (K == 2) {
       if (np == 1) {
         // Single partition: no separate count pass.  Count the union (rows
         // only, the columns are then hot in L1/L2), allocate 2u arena
