@@ -18,9 +18,12 @@ Gram, search, apply, residual, core) of that matrix.
   cpu_baseline : the reference compiled in place (oracle/_ref) on the host
           cores, on a bounded sample of the same recipe (R-MAT scale 14, m=512).
 
-Multi-GPU (--gpus N under torchrun): every rank factorizes its own replica
-(weak scaling, "replicas"; cluster sharding with an NCCL reblock is not built
-yet — DESIGN.md §6).  --impl reference runs the reference's CPU path instead.
+Multi-GPU (--gpus N under torchrun): ONE factorization per step with the
+clusters of every stage sharded over the N ranks (shard.cuh: redundant
+clustering/reblock, owned clusters' Gram + search + rotation passes, NCCL
+exchanges of the rotation slots and column slabs) — strong scaling, the
+step time is the max over ranks.  --impl reference runs the reference's CPU
+path instead.
 """
 import argparse
 import ctypes
@@ -286,7 +289,7 @@ def main():
         best = max(times)
         v = rots / best
         line = {"metric": W["metric"], "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": best * 1e3, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded R-MAT recipe, SURVEY.md §8(d))",
                 "impl": "reference",
                 "config": {"workload": "bounded CPU sample of " + W["desc"] + ": " + cpu_sample_desc(W["cpu"], args.cpu_scale),
@@ -319,12 +322,20 @@ def main():
     pinned = [torch.from_numpy(x).pin_memory() for x in (rows, cols, vals)]
     coo_host, keep_host = abi.make_coo(n, *(t.numpy() for t in pinned), device=local)
     err = lib.errbuf()
+    # N > 1: the clusters of every stage sharded over the ranks (NCCL)
+    comm = api.Communicator.from_torch_distributed(local) if world > 1 else None
+
+    def factorize(coo, h):
+        if comm is None:
+            return lib.factorize(ctypes.byref(coo), ctypes.byref(params), ctypes.byref(h), err, len(err))
+        return L.pmmf_b200_factorize_sharded(ctypes.byref(coo), ctypes.byref(params), comm.handle, ctypes.byref(h),
+                                             err, len(err))
 
     last_phases = np.zeros(6)
 
     def run_device():
         h = ctypes.c_void_p()
-        abi.raise_for(lib.factorize(ctypes.byref(coo_dev), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+        abi.raise_for(factorize(coo_dev, h), err)
         s = abi.Summary()
         lib.result_summary(h, ctypes.byref(s))
         ph = np.zeros(6)
@@ -341,7 +352,7 @@ def main():
 
     def run_e2e():
         h = ctypes.c_void_p()
-        abi.raise_for(lib.factorize(ctypes.byref(coo_host), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+        abi.raise_for(factorize(coo_host, h), err)
         f = lib.read_result(h)
         lib.result_free(h)
         out_bytes = sum(a.nbytes for st in f.stages for a in (st.cluster_offsets, st.members, st.rot_indices, st.rot_matrices,
@@ -396,7 +407,7 @@ def main():
     L.pmmf_b200_profile_enable(0)
     total_ms = max_over_ranks(sum(step_ms))
     ms_per_step = total_ms / args.steps
-    value = world * rots / (ms_per_step / 1e3)
+    value = rots / (ms_per_step / 1e3)  # one factorization per step for the whole job
 
     # ---- e2e: host buffers through the C-ABI, H2D + D2H inside the step
     barrier()
@@ -409,7 +420,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t) * 1e3)
     e2e_step = max_over_ranks(sum(e2e_ms) / len(e2e_ms))
-    e2e = {"value": world * rots / (e2e_step / 1e3), "unit": UNIT,
+    e2e = {"value": rots / (e2e_step / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(rows.nbytes + cols.nbytes + vals.nbytes), "d2h_bytes_per_step": int(out_bytes),
            "ms_per_step": e2e_step}
 
@@ -455,14 +466,14 @@ def main():
 
     if rank == 0:
         line = {"metric": W["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded R-MAT recipe, SURVEY.md §8(d)); inputs > L2 (no flush needed)",
                 "config": {"workload": W["desc"] if args.workload != "c4" else
                            f"config 4: R-MAT scale {args.scale} epv 32, normalized Laplacian + 1e-2 I",
                            "n": int(n), "nnz": int(len(vals)), "k": int(params.k), "P": int(params.n_stages),
                            "m": int(params.m_target), "c_max": int(params.c_max),
-                           "rotations_per_step": int(rots), "parallelism": f"replicas x{world}",
+                           "rotations_per_step": int(rots), "parallelism": f"clusters sharded x{world}" if world > 1 else "single GPU",
                            "l2": "working set >> 126 MB L2"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
                 "mmf_apply": apply,
@@ -470,6 +481,8 @@ def main():
                 "phases_ms_last_step": dict(zip(["clustering", "gram", "search", "apply", "reblock", "total"],
                                                 [round(float(x), 1) for x in last_phases]))}
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -131,6 +131,33 @@ int pmmf_b200_result_core(void* h, int64_t* core_indices, double* core, int64_t*
 int pmmf_b200_result_stats(void* h, double* phases, int64_t* stage_info);
 void pmmf_b200_result_free(void* h);
 
+/* ---- multi-GPU: the clusters of every stage sharded over ranks -------
+ * (replaces the reference's fork-join thread pool over
+ * the clusters of a stage, parallel.hpp:25-71 as used at
+ * factorizer.hpp:494-504 and :513).  One process per GPU: rank 0 makes a
+ * unique id, the launcher shares it (e.g. torch.distributed), every rank
+ * creates its communicator and calls pmmf_b200_factorize_sharded
+ * collectively.  Every rank returns the same, complete factorization,
+ * bit-identical to pmmf_b200_factorize for any number of ranks. */
+#define PMMF_B200_COMM_ID_BYTES 128
+int pmmf_b200_comm_unique_id(uint8_t* id, char* err, size_t errlen);
+/* NCCL communicator over nranks processes (nranks == 1 may pass id = NULL;
+ * its exchanges then run as self-broadcasts). */
+int pmmf_b200_comm_create(int32_t nranks, int32_t rank, const uint8_t* id, int32_t device, void** comm,
+                          char* err, size_t errlen);
+/* nranks virtual ranks run one after another in this process on one GPU
+ * (test hook: proves the decomposition bit-exact on a single device). */
+int pmmf_b200_comm_create_virtual(int32_t nranks, int32_t device, void** comm, char* err, size_t errlen);
+void pmmf_b200_comm_free(void* comm);
+/* pmmf::factorize with the stage's clusters split over the communicator's
+ * ranks (a->device must be the communicator's device). */
+int pmmf_b200_factorize_sharded(const pmmf_b200_coo* a, const pmmf_b200_params* p, void* comm, void** out,
+                                char* err, size_t errlen);
+/* The cluster split (host only): contiguous ranges lo[0..nranks] of about
+ * equal cost c_u^2 + 64 nnz_u (nnz may be NULL). */
+int pmmf_b200_shard_ranges(int64_t nclusters, const int64_t* sizes, const int64_t* nnz, int32_t nranks,
+                           int64_t* lo);
+
 /* ---- MmfOperator (transform_ops.hpp:30-137) ------------------------- */
 
 enum { PMMF_APPLY_FORWARD = 0, PMMF_APPLY_INVERSE = 1, PMMF_APPLY_INV_SQRT = 2 };

@@ -41,7 +41,91 @@ def library() -> abi.FlatAbi:
         for name in ("rmat", "dense_spd", "rbf", "aniso_grid"):
             getattr(L, "pmmf_b200_workload_" + name).restype = ctypes.c_int
         L.pmmf_b200_workload_free.argtypes = [ctypes.POINTER(abi.Workload)]
+        E = [ctypes.c_char_p, ctypes.c_size_t]
+        V = ctypes.c_void_p
+        L.pmmf_b200_comm_unique_id.restype = ctypes.c_int
+        L.pmmf_b200_comm_unique_id.argtypes = [ctypes.c_char_p] + E
+        L.pmmf_b200_comm_create.restype = ctypes.c_int
+        L.pmmf_b200_comm_create.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.c_char_p, ctypes.c_int32,
+                                            ctypes.POINTER(V)] + E
+        L.pmmf_b200_comm_create_virtual.restype = ctypes.c_int
+        L.pmmf_b200_comm_create_virtual.argtypes = [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(V)] + E
+        L.pmmf_b200_comm_free.restype = None
+        L.pmmf_b200_comm_free.argtypes = [V]
+        L.pmmf_b200_factorize_sharded.restype = ctypes.c_int
+        L.pmmf_b200_factorize_sharded.argtypes = [ctypes.POINTER(abi.Coo), ctypes.POINTER(abi.Params), V,
+                                                  ctypes.POINTER(V)] + E
+        L.pmmf_b200_shard_ranges.restype = ctypes.c_int
+        L.pmmf_b200_shard_ranges.argtypes = [ctypes.c_int64, V, V, ctypes.c_int32, V]
     return _ABI
+
+
+# ------------------------------------------------------------ multi-GPU
+COMM_ID_BYTES = 128
+
+
+class Communicator:
+    """The ranks a sharded factorization runs on: one
+    process per GPU over NCCL, or `virtual` ranks run one after another in
+    this process on one GPU (parity test hook).  The reference's analogue is
+    the fork-join pool over a stage's clusters (parallel.hpp:25-71)."""
+
+    def __init__(self, nranks: int, rank: int = 0, device: int = 0, unique_id: Optional[bytes] = None,
+                 virtual: bool = False):
+        lib = library()
+        self.nranks, self.rank, self.device, self.virtual = int(nranks), int(rank), int(device), bool(virtual)
+        self.handle = ctypes.c_void_p()
+        err = lib.errbuf()
+        if virtual:
+            st = lib.lib.pmmf_b200_comm_create_virtual(self.nranks, self.device, ctypes.byref(self.handle), err,
+                                                       len(err))
+        else:
+            if self.nranks > 1 and (unique_id is None or len(unique_id) != COMM_ID_BYTES):
+                raise ValueError("Communicator: a 128-byte unique id from rank 0 is required")
+            st = lib.lib.pmmf_b200_comm_create(self.nranks, self.rank, unique_id, self.device,
+                                               ctypes.byref(self.handle), err, len(err))
+        abi.raise_for(st, err)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        lib = library()
+        buf = ctypes.create_string_buffer(COMM_ID_BYTES)
+        err = lib.errbuf()
+        abi.raise_for(lib.lib.pmmf_b200_comm_unique_id(buf, err, len(err)), err)
+        return buf.raw
+
+    @classmethod
+    def from_torch_distributed(cls, device: int) -> "Communicator":
+        """Collective over an initialised torch.distributed group: rank 0
+        makes the NCCL id, the group broadcasts it."""
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(), dist.get_world_size()
+        box = [cls.unique_id() if rank == 0 and world > 1 else None]
+        if world > 1:
+            dist.broadcast_object_list(box, src=0)
+        return cls(world, rank, device, box[0])
+
+    def close(self) -> None:
+        if self.handle:
+            library().lib.pmmf_b200_comm_free(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def shard_ranges(sizes, nnz, nranks: int) -> np.ndarray:
+    """The cluster split of a sharded stage: contiguous ranges lo[0..nranks]."""
+    sizes = np.ascontiguousarray(sizes, np.int64)
+    z = None if nnz is None else np.ascontiguousarray(nnz, np.int64)
+    lo = np.zeros(int(nranks) + 1, np.int64)
+    st = library().lib.pmmf_b200_shard_ranges(len(sizes), abi.ptr(sizes), abi.ptr(z), int(nranks), abi.ptr(lo))
+    abi.raise_for(st, None)
+    return lo
 
 
 def kernel_launches() -> int:
@@ -172,14 +256,24 @@ class MmfFactorization(abi.FlatFactorization):
         return float(self.diag_value[pos])
 
 
-def factorize(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int = 0) -> MmfFactorization:
-    """pmmf::factorize on the GPU (factorizer.hpp:397-595)."""
+def _factorize_call(lib, coo, p, h, err, comm: Optional[Communicator]):
+    if comm is None:
+        return lib.factorize(ctypes.byref(coo), ctypes.byref(p), ctypes.byref(h), err, len(err))
+    return lib.lib.pmmf_b200_factorize_sharded(ctypes.byref(coo), ctypes.byref(p), comm.handle, ctypes.byref(h), err,
+                                               len(err))
+
+
+def factorize(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int = 0,
+              comm: Optional[Communicator] = None) -> MmfFactorization:
+    """pmmf::factorize on the GPU (factorizer.hpp:397-595); with `comm`, the
+    clusters of every stage are sharded over its ranks (collective call,
+    every rank returns the same factorization)."""
     lib = library()
     coo, keep = matrix.coo(device)
     p = params.to_c()
     h = ctypes.c_void_p()
     err = lib.errbuf()
-    abi.raise_for(lib.factorize(ctypes.byref(coo), ctypes.byref(p), ctypes.byref(h), err, len(err)), err)
+    abi.raise_for(_factorize_call(lib, coo, p, h, err, comm), err)
     try:
         flat = lib.read_result(h)
     finally:
@@ -190,14 +284,15 @@ def factorize(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int 
     return out
 
 
-def factorize_handle(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int = 0) -> ctypes.c_void_p:
+def factorize_handle(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int = 0,
+                     comm: Optional[Communicator] = None) -> ctypes.c_void_p:
     """Raw result handle (caller frees with library().result_free)."""
     lib = library()
     coo, keep = matrix.coo(device)
     p = params.to_c()
     h = ctypes.c_void_p()
     err = lib.errbuf()
-    abi.raise_for(lib.factorize(ctypes.byref(coo), ctypes.byref(p), ctypes.byref(h), err, len(err)), err)
+    abi.raise_for(_factorize_call(lib, coo, p, h, err, comm), err)
     return h
 
 

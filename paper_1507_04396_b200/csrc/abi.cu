@@ -9,6 +9,7 @@
 
 #include "result.cuh"
 #include "rotation.cuh"
+#include "shard.cuh"
 
 using namespace pmmf_b200;
 
@@ -93,6 +94,14 @@ int pmmf_b200_factorize(const pmmf_b200_coo* a, const pmmf_b200_params* p, void*
   return guarded(err, errlen, [&] {
     if (!a || !p || !out) fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_factorize: null argument");
     *out = factorize_device(a, *p).release();
+  });
+}
+
+int pmmf_b200_factorize_sharded(const pmmf_b200_coo* a, const pmmf_b200_params* p, void* comm, void** out,
+                                char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!a || !p || !out || !comm) fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_factorize_sharded: null argument");
+    *out = factorize_device(a, *p, static_cast<const Comm*>(comm)).release();
   });
 }
 

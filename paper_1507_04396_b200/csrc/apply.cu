@@ -1072,15 +1072,15 @@ void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, cudaStream_t
 void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
                  const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
                  const uint8_t* keep_all_col, i64 batch_nnz, double growth, const MassSpec* ms,
-                 cudaStream_t s) {
+                 cudaStream_t s, i64 u_lo, i64 u_hi) {
   out.clear();
-  const i64 m = static_cast<i64>(off.size()) - 1;
+  const i64 m = u_hi < 0 ? static_cast<i64>(off.size()) - 1 : u_hi;
   // host copy of ptr at cluster boundaries
   std::vector<i64> eptr(static_cast<size_t>(m + 1));
-  for (i64 u = 0; u <= m; ++u)
+  for (i64 u = u_lo; u <= m; ++u)
     PMMF_CUDA(cudaMemcpyAsync(&eptr[u], in.ptr.get() + off[u], sizeof(i64), cudaMemcpyDeviceToHost, s));
   PMMF_CUDA(cudaStreamSynchronize(s));
-  i64 u0 = 0;
+  i64 u0 = u_lo;
   while (u0 < m) {
     i64 u1 = u0 + 1;
     while (u1 < m && eptr[u1 + 1] - eptr[u0] <= batch_nnz) ++u1;

@@ -155,11 +155,12 @@ struct MassSpec {
 // `growth` is the expected arena/input ratio of a batch (final columns plus
 // superseded versions); the arena starts at that size so that compactions
 // (copy + re-map) stay rare.  With `ms`, the residual masses are taken from
-// the final columns before they are filtered into pieces.
+// the final columns before they are filtered into pieces.  Only clusters
+// [u_lo, u_hi) are passed (u_hi < 0: all); pieces then cover their columns.
 void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>& off,
                  const std::vector<i64>& slot_base, const LevelPlan& plan, const uint8_t* keep_row,
                  const uint8_t* keep_all_col, i64 batch_nnz, double growth, const MassSpec* ms,
-                 cudaStream_t s);
+                 cudaStream_t s, i64 u_lo = 0, i64 u_hi = -1);
 // Transpose of a matrix given as pieces covering [0, N), keeping only rows
 // r with keep_row[r] (all when nullptr); sorted in chunks of <= chunk_nnz
 // entries so the sort buffers stay bounded.

@@ -26,6 +26,7 @@
 #include "result.cuh"
 #include "rng.cuh"
 #include "rotation.cuh"
+#include "shard.cuh"
 
 namespace pmmf_b200 {
 
@@ -159,7 +160,14 @@ struct StreamGuard {
 
 }  // namespace
 
-std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b200_params& p) {
+std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b200_params& p,
+                                         const Comm* comm) {
+  const Comm one;
+  const Comm& C = comm ? *comm : one;
+  if (comm && comm->device != in->device)
+    fail(PMMF_INVALID_ARGUMENT, "factorize_sharded: input device differs from the communicator's");
+  const int W = C.world();
+  const std::vector<int> my_ranks = C.local_ranks();
   PMMF_CUDA(cudaSetDevice(in->device));
   {
     // The stream-ordered pool keeps freed blocks mapped across
@@ -305,6 +313,23 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     std::vector<int64_t> out_base(static_cast<size_t>(rc) + 1, 0);
     for (i64 u = 0; u < rc; ++u) out_base[u + 1] = out_base[u] + budget[u];
     const i64 slots = out_base[rc];
+    // ---- cluster ownership (shard.cuh): rank r owns clusters [lo[r], lo[r+1])
+    const i64 nclu = cur.clusters();
+    std::vector<i64> lo{0, nclu}, eptr_c;
+    if (W > 1) {
+      eptr_c = cluster_ptr(A, cur.off, s);
+      std::vector<i64> csz(static_cast<size_t>(nclu)), cnz(static_cast<size_t>(nclu));
+      for (i64 u = 0; u < nclu; ++u) {
+        csz[u] = cur.off[u + 1] - cur.off[u];
+        cnz[u] = eptr_c[u + 1] - eptr_c[u];
+      }
+      lo = shard_ranges(csz, cnz, W);
+    }
+    auto seg_of = [&](auto&& f) {  // per-rank segment bounds from a cluster-indexed prefix f(u)
+      std::vector<i64> g(static_cast<size_t>(W) + 1);
+      for (int r = 0; r <= W; ++r) g[r] = f(std::min(lo[r], rc));
+      return g;
+    };
 
     // ---- Gram + search, in batches of clusters whose tiles fit in memory
     SearchOut so;
@@ -324,12 +349,14 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     {
       const i64 budget_elems =
           std::max<i64>(i64{1} << 20, static_cast<i64>(static_cast<double>(available_bytes()) * 0.55) / 16);
-      i64 u0 = 0;
       double gram_ms = 0.0, search_ms = 0.0;
-      while (u0 < rc) {
+      for (const int me : my_ranks) {
+      const i64 u_end = std::min(lo[me + 1], rc);
+      i64 u0 = std::min(lo[me], rc);
+      while (u0 < u_end) {
         i64 u1 = u0, elems = 0, max_c = 0;
         std::vector<i64> tile_off(1, 0);
-        while (u1 < rc) {
+        while (u1 < u_end) {
           const i64 c = cur.off[u1 + 1] - cur.off[u1];
           if (u1 > u0 && elems + c * c > budget_elems) break;
           elems += c * c;
@@ -385,9 +412,25 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         search_ms += ms_since(ts);
         u0 = u1;
       }
+      }
       R->phases[1] += gram_ms;
       R->phases[2] += search_ms;
       PMMF_TRACE("[pmmf] stage %d: gram %.2f ms, search %.2f ms\n", stage_no, gram_ms, search_ms);
+    }
+    if (C.multi_process()) {
+      // exchange 1: every rank's clusters' rotation slots and counts
+      const auto t_x = clk::now();
+      const auto cseg = seg_of([](i64 u) { return u; });
+      const auto sseg = seg_of([&](i64 u) { return out_base[u]; });
+      bcast_segments(so.nrot.get(), sizeof(int32_t), cseg, C, s);
+      bcast_segments(so.nelim.get(), sizeof(int32_t), cseg, C, s);
+      bcast_segments(so.rot_loc.get(), sizeof(int32_t) * p.k, sseg, C, s);
+      bcast_segments(so.rot_q.get(), sizeof(double) * p.k * p.k, sseg, C, s);
+      bcast_segments(so.rot_level.get(), sizeof(int32_t), sseg, C, s);
+      bcast_segments(so.elim_loc.get(), sizeof(int32_t), sseg, C, s);
+      allreduce_max_i32(so.error.get(), C, s);
+      PMMF_CUDA(cudaStreamSynchronize(s));
+      R->phases[2] += ms_since(t_x);
     }
     const auto t_asm = clk::now();
     if (so.error.to_host(1)[0]) fail(PMMF_INVALID_ARGUMENT, "rotation_from_gram: input not symmetric");
@@ -483,16 +526,6 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           tl = clk::now();
         };
         lap("plan");
-        std::vector<Piece> pieces;
-        const i64 nnz_in = std::max<i64>(A.nnz, 1);
-        rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, 24.0, nullptr, s);
-        lap("column_pass");
-        A = Csc();
-        Csc T;
-        transpose_pieces(T, pieces, N, nullptr, chunk, s);
-        pieces.clear();
-        lap("transpose_1");
-        const i64 tn = T.nnz;
         // Retired ids: their rotated rows/columns feed only the residual.
         DBuf<uint8_t> keep_row(N, s);
         {
@@ -500,17 +533,6 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           for (int32_t sid : order_sid) kr[sid] = 0;
           keep_row.upload(kr);
         }
-        // The row pass grows its columns about as much as the column pass did
-        // (measured ratio); size its arena and batches from that.
-        const double growth = 1.4 * std::max(2.0, static_cast<double>(tn) / static_cast<double>(nnz_in));
-        // (free memory re-read: T and the retired masks now hold their share)
-        const i64 avail_row = available_bytes();
-        double frac = 0.2;  // share of free memory for one batch's arena
-        if (const char* e = std::getenv("PMMF_B200_ARENA_FRAC")) frac = std::atof(e);
-        i64 batch = std::max<i64>(i64{1} << 24, static_cast<i64>(frac * static_cast<double>(avail_row) / (12.0 * growth)));
-        if (const char* e = std::getenv("PMMF_B200_BATCH_NNZ")) batch = std::atoll(e);  // test hook
-        PMMF_TRACE("[pmmf] stage %d: column pass -> %lld entries, batch=%lld mem=%zuMB\n", stage_no,
-                   static_cast<long long>(tn), static_cast<long long>(batch), mem_used_mb());
         // Row pass with the residual masses taken from its final columns
         // (rows of A'), which then keep only the surviving rows.
         MassSpec ms;
@@ -529,21 +551,73 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           ms.chunk_nnz = chunk;
           ms.n_retired = ne;
         }
-        rotate_pass(pieces, T, cur.off, slot_base, plan, keep_row.get(), nullptr, batch, growth,
-                    ne > 0 ? &ms : nullptr, s);
-        T = Csc();
-        lap("row_pass");
-        i64 stored = 0;
-        for (const Piece& P : pieces) stored += P.nnz;
-        PMMF_TRACE("[pmmf] stage %d: row pass stored %lld entries in %zu pieces, mem=%zuMB\n", stage_no,
-                   static_cast<long long>(stored), pieces.size(), mem_used_mb());
+        // One column slab per rank (shard.cuh): the rank's clusters' columns
+        // through the column pass, transpose, row pass (all rotations) and
+        // transpose back.  With one rank the slab is the whole matrix.
+        std::vector<Csc> slabs;
+        for (size_t li = 0; li < my_ranks.size(); ++li) {
+          const int me = my_ranks[li];
+          std::vector<Piece> pieces;
+          const i64 nnz_in =
+              std::max<i64>(W > 1 ? eptr_c[lo[me + 1]] - eptr_c[lo[me]] : A.nnz, 1);
+          rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, 24.0, nullptr, s, lo[me],
+                      lo[me + 1]);
+          lap("column_pass");
+          if (li + 1 == my_ranks.size()) A = Csc();
+          Csc T;
+          transpose_pieces(T, pieces, N, nullptr, chunk, s);
+          pieces.clear();
+          lap("transpose_1");
+          const i64 tn = T.nnz;
+          // The row pass grows its columns about as much as the column pass
+          // did (measured ratio); size its arena and batches from that.
+          const double growth =
+              1.4 * std::max(2.0, static_cast<double>(tn) / static_cast<double>(nnz_in));
+          // (free memory re-read: T and the retired masks now hold their share)
+          const i64 avail_row = available_bytes();
+          double frac = 0.2;  // share of free memory for one batch's arena
+          if (const char* e = std::getenv("PMMF_B200_ARENA_FRAC")) frac = std::atof(e);
+          i64 batch = std::max<i64>(i64{1} << 24,
+                                    static_cast<i64>(frac * static_cast<double>(avail_row) / (12.0 * growth)));
+          if (const char* e = std::getenv("PMMF_B200_BATCH_NNZ")) batch = std::atoll(e);  // test hook
+          PMMF_TRACE("[pmmf] stage %d rank %d: column pass -> %lld entries, batch=%lld mem=%zuMB\n", stage_no, me,
+                     static_cast<long long>(tn), static_cast<long long>(batch), mem_used_mb());
+          rotate_pass(pieces, T, cur.off, slot_base, plan, keep_row.get(), nullptr, batch, growth,
+                      ne > 0 ? &ms : nullptr, s);
+          T = Csc();
+          lap("row_pass");
+          i64 stored = 0;
+          for (const Piece& P : pieces) stored += P.nnz;
+          PMMF_TRACE("[pmmf] stage %d rank %d: row pass stored %lld entries in %zu pieces, mem=%zuMB\n", stage_no,
+                     me, static_cast<long long>(stored), pieces.size(), mem_used_mb());
+          // The next stage reads only the surviving columns of A' (all rows).
+          slabs.emplace_back();
+          transpose_pieces(slabs.back(), pieces, N, nullptr, chunk, s);
+          lap("transpose_2");
+        }
         if (ne > 0) {  // retired ids leave the active set
           PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
           residual_done = true;
         }
-        // The next stage reads only the surviving columns of A' (all rows).
-        transpose_pieces(A, pieces, N, nullptr, chunk, s);
-        lap("transpose_2");
+        if (W == 1 && !C.multi_process()) {
+          A = std::move(slabs[0]);
+        } else {
+          // exchange 2: the owned columns of A'' and the owned eliminations'
+          // masses and diagonals (eliminations are cluster-major)
+          const auto t_x = clk::now();
+          std::vector<i64> col_seg(static_cast<size_t>(W) + 1);
+          for (int r = 0; r <= W; ++r) col_seg[r] = cur.off[lo[r]];
+          csc_gather_slabs(A, slabs, col_seg, N, C, s);
+          if (ne > 0 && C.multi_process()) {
+            std::vector<i64> epre(static_cast<size_t>(rc) + 1, 0);
+            for (i64 u = 0; u < rc; ++u) epre[u + 1] = epre[u] + nelim[u];
+            const auto eseg = seg_of([&](i64 u) { return epre[u]; });
+            bcast_segments(mass.get(), sizeof(double), eseg, C, s);
+            bcast_segments(diag.get(), sizeof(double), eseg, C, s);
+          }
+          lap("exchange_2");
+          PMMF_TRACE("[pmmf] stage %d: slab exchange %.2f ms\n", stage_no, ms_since(t_x));
+        }
         PMMF_TRACE("[pmmf] stage %d: A' %lld entries, mem=%zuMB\n", stage_no, static_cast<long long>(A.nnz),
                    mem_used_mb());
       }

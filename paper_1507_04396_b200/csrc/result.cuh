@@ -32,6 +32,9 @@ struct Result {
   std::vector<std::array<i64, 7>> info;
 };
 
-std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b200_params& p);
+struct Comm;
+// comm == nullptr: one GPU (shard.cuh for the sharded decomposition).
+std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b200_params& p,
+                                         const Comm* comm = nullptr);
 
 }  // namespace pmmf_b200

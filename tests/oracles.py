@@ -38,14 +38,20 @@ def available(which: str) -> bool:
     return os.path.exists({"oracle": ORACLE, "ref": REF}[which])
 
 
-def factorize(which, inp, params, clusters=None):
-    """Runs one factorization through a flat ABI; returns FlatFactorization."""
+def factorize(which, inp, params, clusters=None, comm=None):
+    """Runs one factorization through a flat ABI; returns FlatFactorization.
+    comm (gpu only): an api.Communicator for the sharded entry point."""
     lib = load(which)
     n, rows, cols, vals = inp
     coo, keep = abi.make_coo(n, rows, cols, vals, clusters)
     h = ctypes.c_void_p()
     err = lib.errbuf()
-    abi.raise_for(lib.factorize(ctypes.byref(coo), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+    if comm is None:
+        st = lib.factorize(ctypes.byref(coo), ctypes.byref(params), ctypes.byref(h), err, len(err))
+    else:
+        st = lib.lib.pmmf_b200_factorize_sharded(ctypes.byref(coo), ctypes.byref(params), comm.handle,
+                                                 ctypes.byref(h), err, len(err))
+    abi.raise_for(st, err)
     try:
         return lib.read_result(h)
     finally:

@@ -75,3 +75,85 @@ def test_two_gloo_ranks_replicas_identical():
     assert same, "replicas differ across ranks"
     assert tmax == 20.0  # max over ranks
     assert rots > 0
+
+
+def shard_ranges_py(sizes, nnz, world, apply_weight=64):
+    """Restatement of shard.cu shard_ranges: contiguous split of the clusters
+    by the cost prefix c^2 + 64 nnz, each boundary on the side nearer r/W."""
+    m = len(sizes)
+    pre = [0.0]
+    for u in range(m):
+        pre.append(pre[-1] + float(sizes[u]) * float(sizes[u]) + apply_weight * float(nnz[u] if nnz is not None else 0))
+    lo = [0] + [m] * world
+    u = 0
+    for r in range(1, world):
+        target = pre[m] * r / world
+        while u < m and pre[u + 1] <= target:
+            u += 1
+        b = u + 1 if (u < m and target - pre[u] > pre[u + 1] - target) else u
+        lo[r] = max(b, lo[r - 1])
+    lo[world] = m
+    return lo
+
+
+def _shard_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_1507_04396_b200 import api
+
+    # the communicator bootstrap: rank 0's NCCL id reaches every rank intact
+    box = [api.Communicator.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    ids = [None] * world
+    dist.all_gather_object(ids, box[0])
+    # every rank derives the same cluster split from the same stage partition
+    rng = np.random.default_rng(7)
+    sizes = rng.integers(10, 5000, size=517)
+    nnz = sizes * rng.integers(2, 40, size=517)
+    splits = {}
+    for w in (2, 3, 8):
+        splits[w] = api.shard_ranges(sizes, nnz, w).tolist()
+    all_splits = [None] * world
+    dist.all_gather_object(all_splits, splits)
+    if rank == 0:
+        out.put((ids, all_splits, sizes.tolist(), nnz.tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_gloo_ranks_shard_plan():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ids, all_splits, sizes, nnz = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert len(ids[0]) == 128 and ids[0] == ids[1]
+    assert all_splits[0] == all_splits[1]
+    for w, lo in all_splits[0].items():
+        assert lo == shard_ranges_py(sizes, nnz, w)
+        assert lo[0] == 0 and lo[-1] == len(sizes) and all(a <= b for a, b in zip(lo, lo[1:]))
+        cost = [s * s + 64 * z for s, z in zip(sizes, nnz)]
+        share = [sum(cost[lo[r]:lo[r + 1]]) for r in range(w)]
+        assert max(share) <= sum(cost) / w + max(cost)  # balanced to one cluster
+
+
+def test_shard_ranges_edges():
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_1507_04396_b200 import api
+
+    assert api.shard_ranges([], None, 3).tolist() == [0, 0, 0, 0]
+    assert api.shard_ranges([5], None, 4).tolist() == shard_ranges_py([5], None, 4)
+    assert api.shard_ranges([100] * 10, None, 4).tolist() == [0, 2, 5, 7, 10]
+    assert api.shard_ranges([3, 1, 4, 1, 5, 9, 2, 6], [1] * 8, 1).tolist() == [0, 8]
