@@ -351,6 +351,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           std::max<i64>(i64{1} << 20, static_cast<i64>(static_cast<double>(available_bytes()) * 0.55) / 16);
       double gram_ms = 0.0, search_ms = 0.0;
       for (const int me : my_ranks) {
+      const auto t_rank = clk::now();
+      const double gs0 = gram_ms + search_ms;
       const i64 u_end = std::min(lo[me + 1], rc);
       i64 u0 = std::min(lo[me], rc);
       while (u0 < u_end) {
@@ -412,6 +414,10 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         search_ms += ms_since(ts);
         u0 = u1;
       }
+      if (W > 1)  // per-rank cost of the sharded part (scripts/shard_model.py)
+        PMMF_TRACE("[pmmf] shard stage %d rank %d: gram+search %.3f ms (%.3f wall) clusters [%lld,%lld)\n", stage_no,
+                   me, gram_ms + search_ms - gs0, ms_since(t_rank), static_cast<long long>(lo[me]),
+                   static_cast<long long>(lo[me + 1]));
       }
       R->phases[1] += gram_ms;
       R->phases[2] += search_ms;
@@ -557,6 +563,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         std::vector<Csc> slabs;
         for (size_t li = 0; li < my_ranks.size(); ++li) {
           const int me = my_ranks[li];
+          if (W > 1 && trace_on()) PMMF_CUDA(cudaStreamSynchronize(s));
+          const auto t_rank = clk::now();
           std::vector<Piece> pieces;
           const i64 nnz_in =
               std::max<i64>(W > 1 ? eptr_c[lo[me + 1]] - eptr_c[lo[me]] : A.nnz, 1);
@@ -594,6 +602,11 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           slabs.emplace_back();
           transpose_pieces(slabs.back(), pieces, N, nullptr, chunk, s);
           lap("transpose_2");
+          if (W > 1 && trace_on()) {
+            PMMF_CUDA(cudaStreamSynchronize(s));
+            PMMF_TRACE("[pmmf] shard stage %d rank %d: apply %.3f ms, slab %lld entries\n", stage_no, me,
+                       ms_since(t_rank), static_cast<long long>(slabs.back().nnz));
+          }
         }
         if (ne > 0) {  // retired ids leave the active set
           PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
