@@ -123,6 +123,12 @@ __global__ void k_core(i64 g, const int32_t* __restrict__ col_sid, const i64* __
 using clk = std::chrono::steady_clock;
 
 bool trace_on() { return trace_enabled(); }
+// per-rank timings of the sharded part only (scripts/shard_model.py): one
+// synchronisation per rank and phase, unlike the full trace
+bool shard_timing() {
+  static const bool on = std::getenv("PMMF_B200_SHARD_TIMING") != nullptr;
+  return on || trace_enabled();
+}
 size_t mem_used_mb() {
   size_t f = 0, t = 0;
   cudaMemGetInfo(&f, &t);
@@ -414,8 +420,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         search_ms += ms_since(ts);
         u0 = u1;
       }
-      if (W > 1)  // per-rank cost of the sharded part (scripts/shard_model.py)
-        PMMF_TRACE("[pmmf] shard stage %d rank %d: gram+search %.3f ms (%.3f wall) clusters [%lld,%lld)\n", stage_no,
+      if (W > 1 && shard_timing())  // per-rank cost of the sharded part (scripts/shard_model.py)
+        std::fprintf(stderr, "[pmmf] shard stage %d rank %d: gram+search %.3f ms (%.3f wall) clusters [%lld,%lld)\n", stage_no,
                    me, gram_ms + search_ms - gs0, ms_since(t_rank), static_cast<long long>(lo[me]),
                    static_cast<long long>(lo[me + 1]));
       }
@@ -563,7 +569,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         std::vector<Csc> slabs;
         for (size_t li = 0; li < my_ranks.size(); ++li) {
           const int me = my_ranks[li];
-          if (W > 1 && trace_on()) PMMF_CUDA(cudaStreamSynchronize(s));
+          if (W > 1 && shard_timing()) PMMF_CUDA(cudaStreamSynchronize(s));
           const auto t_rank = clk::now();
           std::vector<Piece> pieces;
           const i64 nnz_in =
@@ -602,9 +608,9 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           slabs.emplace_back();
           transpose_pieces(slabs.back(), pieces, N, nullptr, chunk, s);
           lap("transpose_2");
-          if (W > 1 && trace_on()) {
+          if (W > 1 && shard_timing()) {
             PMMF_CUDA(cudaStreamSynchronize(s));
-            PMMF_TRACE("[pmmf] shard stage %d rank %d: apply %.3f ms, slab %lld entries\n", stage_no, me,
+            std::fprintf(stderr, "[pmmf] shard stage %d rank %d: apply %.3f ms, slab %lld entries\n", stage_no, me,
                        ms_since(t_rank), static_cast<long long>(slabs.back().nnz));
           }
         }

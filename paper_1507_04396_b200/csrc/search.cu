@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(kSearchThreads, 2) k_search(KArgs A) {
         }
       }
       if (off_diag_norm_sq(ng[0][0], nd[0][0]) < vn) victim = draw;
+      __syncwarp();  // every lane has read the corner before lane 0 rewrites it
       if (lane == 0) {
         if (!ok) atomicExch(A.error, 1);
 #pragma unroll
@@ -625,8 +626,8 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
         }
       }
     }
+    double gs[K][K], cd[K][K];
     if (wid == 0) {
-      double gs[K][K], cd[K][K], q[K][K], ng[K][K], nd[K][K];
 #pragma unroll
       for (int a = 0; a < K; ++a)
 #pragma unroll
@@ -636,6 +637,14 @@ __global__ void __launch_bounds__(kSearchThreads, 1) k_search_cl(KArgs A, const 
           gs[a][b] = __ldcg(G + at);
           cd[a][b] = __ldcg(D + at);
         }
+    }
+    // every CTA has read the corner before rank 0 overwrites it below (a
+    // late CTA would otherwise read the NEW corner, derive another rotation
+    // for its row slice and leave G asymmetric: the rare "input not
+    // symmetric" failures of full-size runs)
+    cl.sync();
+    if (wid == 0) {
+      double q[K][K], ng[K][K], nd[K][K];
       const bool ok = rotation_from_gram_k<K>(gs, q);
       conjugate_corner_k<K>(q, gs, ng);
       conjugate_corner_k<K>(q, cd, nd);

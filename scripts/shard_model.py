@@ -3,7 +3,7 @@
 Only one B200 is reachable this round, so the N-GPU step is assembled from
 measured parts: a config-N factorization with W virtual ranks
 (api.Communicator(W, virtual=True)) runs every rank's sharded work one after
-another on this GPU, and PMMF_B200_TRACE reports each rank's Gram+search and
+another on this GPU, and PMMF_B200_SHARD_TIMING reports each rank's Gram+search and
 slab apply time per stage.  Then
 
   T_W = T_virtual - sum_s sum_r (gs_rs + ap_rs) + sum_s (max_r gs_rs + max_r ap_rs) + X_W
@@ -58,7 +58,8 @@ def child(wl, world, out):
         lib.result_free(h)
         res = {"wall_ms": wall, "rotations": int(sum(len(s.rot_indices) for s in f.stages)),
                "digest": digest(f)}
-        sys.stderr.write("[model] run-end\n")
+        sys.stderr.flush()
+        os.write(2, b"[model] run-end\n")
     with open(out, "w") as fh:
         json.dump(res, fh)
 
@@ -82,7 +83,7 @@ def run(wl, world, trace):
     out = f"/tmp/shard_model_{wl}_{world}.json"
     env = dict(os.environ)
     if trace:
-        env["PMMF_B200_TRACE"] = "1"
+        env["PMMF_B200_SHARD_TIMING"] = "1"
     p = subprocess.run([sys.executable, __file__, "--child", wl, str(world), out], env=env, capture_output=True,
                        text=True, cwd=ROOT)
     if p.returncode != 0:
@@ -136,7 +137,7 @@ def main():
     base = run(a.workload, 0, trace=False)
     out = {"workload": a.workload, "rotations": base["rotations"], "one_gpu_wall_ms": base["wall_ms"],
            "one_gpu_rotations_per_s": base["rotations"] / base["wall_ms"] * 1e3, "nvlink_gbs_assumed": a.nvlink_gbs,
-           "note": "modelled from single-GPU virtual-rank runs (trace mode syncs between sub-phases); "
+           "note": "modelled from single-GPU virtual-rank runs (one sync per rank and phase); "
                    "exchange time = slab bytes / assumed NCCL broadcast ingress", "worlds": {}}
     for w in a.worlds:
         res = run(a.workload, w, trace=True)
