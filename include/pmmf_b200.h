@@ -131,6 +131,19 @@ int pmmf_b200_result_core(void* h, int64_t* core_indices, double* core, int64_t*
 int pmmf_b200_result_stats(void* h, double* phases, int64_t* stage_info);
 void pmmf_b200_result_free(void* h);
 
+/* ---- factorization container: save_factorization / load_factorization
+ * (serialize.hpp:167-183), the reference's versioned JSON schema
+ * ("pmmf-factorization", version 1, serialize.hpp:61-165) written and read
+ * without a JSON library.  Doubles round-trip exactly.  A loaded handle
+ * serves every pmmf_b200_result_* accessor and pmmf_b200_operator_create
+ * (MmfOperator without refactorizing); its stats are empty.  Errors:
+ * PMMF_DATA (DataError: unreadable file, unknown format or version, size
+ * mismatches). */
+int pmmf_b200_result_save(void* h, const char* path, char* err, size_t errlen);
+int pmmf_b200_result_load(const char* path, void** out, char* err, size_t errlen);
+/* MmfFactorization::params (factorizer.hpp:117). */
+int pmmf_b200_result_params(void* h, pmmf_b200_params* out);
+
 /* ---- multi-GPU: the clusters of every stage sharded over ranks -------
  * (replaces the reference's fork-join thread pool over
  * the clusters of a stage, parallel.hpp:25-71 as used at

@@ -55,6 +55,12 @@ def library() -> abi.FlatAbi:
         L.pmmf_b200_factorize_sharded.restype = ctypes.c_int
         L.pmmf_b200_factorize_sharded.argtypes = [ctypes.POINTER(abi.Coo), ctypes.POINTER(abi.Params), V,
                                                   ctypes.POINTER(V)] + E
+        L.pmmf_b200_result_save.restype = ctypes.c_int
+        L.pmmf_b200_result_save.argtypes = [V, ctypes.c_char_p] + E
+        L.pmmf_b200_result_load.restype = ctypes.c_int
+        L.pmmf_b200_result_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(V)] + E
+        L.pmmf_b200_result_params.restype = ctypes.c_int
+        L.pmmf_b200_result_params.argtypes = [V, ctypes.POINTER(abi.Params)]
         L.pmmf_b200_shard_ranges.restype = ctypes.c_int
         L.pmmf_b200_shard_ranges.argtypes = [ctypes.c_int64, V, V, ctypes.c_int32, V]
     return _ABI
@@ -294,6 +300,45 @@ def factorize_handle(matrix: BlockedSparseMatrix, params: FactorizeParams, devic
     err = lib.errbuf()
     abi.raise_for(_factorize_call(lib, coo, p, h, err, comm), err)
     return h
+
+
+# -------------------------------------------------- factorization container
+def save_factorization(handle: ctypes.c_void_p, path: str) -> None:
+    """save_factorization (serialize.hpp:167-171): the reference's JSON
+    container for a result handle (factorize_handle / load_factorization_handle)."""
+    lib = library()
+    err = lib.errbuf()
+    abi.raise_for(lib.lib.pmmf_b200_result_save(handle, os.fsencode(path), err, len(err)), err)
+
+
+def load_factorization_handle(path: str) -> ctypes.c_void_p:
+    """load_factorization (serialize.hpp:173-183) as a result handle: feeds
+    the accessors and MmfOperator (pmmf_b200_operator_create) without
+    refactorizing.  The caller frees it with library().result_free."""
+    lib = library()
+    h = ctypes.c_void_p()
+    err = lib.errbuf()
+    abi.raise_for(lib.lib.pmmf_b200_result_load(os.fsencode(path), ctypes.byref(h), err, len(err)), err)
+    return h
+
+
+def load_factorization(path: str) -> MmfFactorization:
+    lib = library()
+    h = load_factorization_handle(path)
+    try:
+        flat = lib.read_result(h)
+        p = abi.Params()
+        abi.raise_for(lib.lib.pmmf_b200_result_params(h, ctypes.byref(p)), None)
+    finally:
+        lib.result_free(h)
+    out = MmfFactorization.__new__(MmfFactorization)
+    out.__dict__.update(flat.__dict__)
+    out.params = FactorizeParams(k=p.k, n_stages=p.n_stages, eta=p.eta, core_min=p.core_min, core_cap=p.core_cap,
+                                 seed=p.seed,
+                                 cluster=ClusterParams(m_target=p.m_target, c_min=p.c_min, c_max=p.c_max,
+                                                       d_max=p.d_max, bypass_enabled=bool(p.bypass_enabled),
+                                                       seed=p.cluster_seed))
+    return out
 
 
 # -------------------------------------------------------------- workloads

@@ -105,6 +105,26 @@ int pmmf_b200_factorize_sharded(const pmmf_b200_coo* a, const pmmf_b200_params* 
   });
 }
 
+int pmmf_b200_result_save(void* h, const char* path, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !path) fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_result_save: null argument");
+    save_factorization(*static_cast<Result*>(h), path);
+  });
+}
+
+int pmmf_b200_result_load(const char* path, void** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!path || !out) fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_result_load: null argument");
+    *out = load_factorization(path).release();
+  });
+}
+
+int pmmf_b200_result_params(void* h, pmmf_b200_params* out) {
+  if (!h || !out) return PMMF_INVALID_ARGUMENT;
+  *out = static_cast<Result*>(h)->params;
+  return PMMF_OK;
+}
+
 int pmmf_b200_result_summary(void* h, pmmf_b200_summary* o) {
   auto* r = static_cast<Result*>(h);
   o->n = r->n;

@@ -194,6 +194,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   auto R = std::make_unique<Result>();
   R->n = n;
   R->k = p.k;
+  R->params = p;
 
   // ---- input partition and from_triplets
   Numbering cur;

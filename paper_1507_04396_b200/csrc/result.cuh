@@ -4,6 +4,7 @@
 
 #include <array>
 #include <memory>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -29,8 +30,15 @@ struct Result {
   std::vector<double> core;  // g x g row-major
   std::vector<std::pair<i64, double>> diag;
   double phases[6] = {0, 0, 0, 0, 0, 0};
+  pmmf_b200_params params{};  // MmfFactorization::params (factorizer.hpp:117)
   std::vector<std::array<i64, 7>> info;
 };
+
+// container.cpp: save_factorization / load_factorization (serialize.hpp)
+std::string factorization_to_json(const Result& r);
+std::unique_ptr<Result> factorization_from_json(const char* text, size_t len);
+void save_factorization(const Result& r, const std::string& path);
+std::unique_ptr<Result> load_factorization(const std::string& path);
 
 struct Comm;
 // comm == nullptr: one GPU (shard.cuh for the sharded decomposition).
