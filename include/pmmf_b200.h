@@ -199,6 +199,48 @@ int pmmf_b200_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_conf
                     int32_t* iterations, int32_t* converged, int32_t* breakdown, double* residuals,
                     double* wall_ms, char* err, size_t errlen);
 
+/* ---- input path (io.hpp:27-250) -------------------------------------- */
+
+/* TripletMatrix (io.hpp:27-33) / EdgeList (io.hpp:150-154), owned by the
+ * library (free with pmmf_b200_triplets_free).  For an edge list rows =
+ * cols = the compacted node count and original_ids[new] = id in the file;
+ * for Matrix Market original_ids is NULL. */
+typedef struct pmmf_b200_triplets {
+  int64_t rows;
+  int64_t cols;
+  int64_t nnz;
+  int64_t* row;
+  int64_t* col;
+  double* val;
+  int64_t n_ids;
+  int64_t* original_ids;
+} pmmf_b200_triplets;
+/* read_matrix_market (io.hpp:68-129): coordinate real/integer/pattern,
+ * general/symmetric; symmetric files mirror off-diagonal entries, pattern
+ * entries get 1, indices become 0-based.  PMMF_DATA on malformed input. */
+int pmmf_b200_read_matrix_market(const char* path, pmmf_b200_triplets** out, char* err, size_t errlen);
+/* read_edge_list (io.hpp:158-208): "u v [w]" lines, '#' comments, weight 1
+ * when absent, self-loops kept once, ids compacted in ascending order. */
+int pmmf_b200_read_edge_list(const char* path, pmmf_b200_triplets** out, char* err, size_t errlen);
+void pmmf_b200_triplets_free(pmmf_b200_triplets* t);
+/* write_matrix_market (io.hpp:131-147): general real, %.17g values. */
+int pmmf_b200_write_matrix_market(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* r,
+                                  const int64_t* c, const double* v, char* err, size_t errlen);
+/* laplacian (io.hpp:212-228) on the GPU: out = the adjacency negated in
+ * input order, then (i, i, degree_i + shift) for i < n; out arrays hold
+ * nnz + n entries.  Degrees are the reference's sequential sums (input
+ * order), bit for bit.  Pointers are device pointers when on_device. */
+int pmmf_b200_laplacian(int64_t n, int64_t nnz, const int64_t* r, const int64_t* c, const double* v, double shift,
+                        int32_t on_device, int32_t device, int64_t* out_r, int64_t* out_c, double* out_v, char* err,
+                        size_t errlen);
+/* symmetrize (io.hpp:231-250) on the GPU: A + A^T, each unordered pair
+ * summed once in input order, emitted in (min, max) order as (i,j),(j,i),
+ * diagonal doubled.  Out arrays need room for 2 nnz entries; *out_nnz
+ * receives the count. */
+int pmmf_b200_symmetrize(int64_t nnz, const int64_t* r, const int64_t* c, const double* v, int32_t on_device,
+                         int32_t device, int64_t* out_nnz, int64_t* out_r, int64_t* out_c, double* out_v, char* err,
+                         size_t errlen);
+
 /* ---- misc ----------------------------------------------------------- */
 
 /* rotation_from_gram (factorizer.hpp:150-171) on one k x k row-major

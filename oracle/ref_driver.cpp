@@ -9,15 +9,20 @@
 //
 // Nothing here re-implements the algorithm: every call forwards to the
 // reference (pmmf::factorize, pmmf::MmfOperator, pmmf::run_solve_experiment,
-// pmmf::rotation_from_gram, pmmf::residual_frobenius).
+// pmmf::rotation_from_gram, pmmf::residual_frobenius, and the input path
+// pmmf::read_matrix_market / read_edge_list / write_matrix_market /
+// laplacian / symmetrize of io.hpp).
 
 #include <pmmf/blocked_matrix.hpp>
 #include <pmmf/factorizer.hpp>
+#include <pmmf/io.hpp>
 #include <pmmf/parallel.hpp>
 #include <pmmf/solver.hpp>
 #include <pmmf/transform_ops.hpp>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -300,6 +305,93 @@ int pmmf_ref_residual_frobenius(void* result, const pmmf_b200_coo* a, double* ac
     const auto& f = *static_cast<RefResult*>(result)->f;
     *accumulated = pmmf::residual_frobenius(f, m, pmmf::ResidualMethod::accumulated);
     *dense = pmmf::residual_frobenius(f, m, pmmf::ResidualMethod::dense);
+  });
+}
+
+static pmmf_b200_triplets* ref_triplets(pmmf::index_t rows, pmmf::index_t cols, const std::vector<pmmf::Triplet>& t,
+                                        const std::vector<pmmf::index_t>* ids) {
+  auto* o = static_cast<pmmf_b200_triplets*>(std::calloc(1, sizeof(pmmf_b200_triplets)));
+  o->rows = rows;
+  o->cols = cols;
+  o->nnz = static_cast<int64_t>(t.size());
+  const size_t n = std::max<size_t>(t.size(), 1);
+  o->row = static_cast<int64_t*>(std::malloc(n * sizeof(int64_t)));
+  o->col = static_cast<int64_t*>(std::malloc(n * sizeof(int64_t)));
+  o->val = static_cast<double*>(std::malloc(n * sizeof(double)));
+  for (size_t i = 0; i < t.size(); ++i) {
+    o->row[i] = t[i].row;
+    o->col[i] = t[i].col;
+    o->val[i] = t[i].value;
+  }
+  if (ids) {
+    o->n_ids = static_cast<int64_t>(ids->size());
+    o->original_ids = static_cast<int64_t*>(std::malloc(std::max<size_t>(ids->size(), 1) * sizeof(int64_t)));
+    for (size_t i = 0; i < ids->size(); ++i) o->original_ids[i] = (*ids)[i];
+  }
+  return o;
+}
+
+void pmmf_ref_triplets_free(pmmf_b200_triplets* t) {
+  if (!t) return;
+  std::free(t->row);
+  std::free(t->col);
+  std::free(t->val);
+  std::free(t->original_ids);
+  std::free(t);
+}
+
+int pmmf_ref_read_matrix_market(const char* path, pmmf_b200_triplets** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const pmmf::TripletMatrix m = pmmf::read_matrix_market(std::string(path));
+    *out = ref_triplets(m.rows, m.cols, m.entries, nullptr);
+  });
+}
+
+int pmmf_ref_read_edge_list(const char* path, pmmf_b200_triplets** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const pmmf::EdgeList e = pmmf::read_edge_list(std::string(path));
+    *out = ref_triplets(e.n, e.n, e.entries, &e.original_ids);
+  });
+}
+
+static std::vector<pmmf::Triplet> ref_in(int64_t nnz, const int64_t* r, const int64_t* c, const double* v) {
+  std::vector<pmmf::Triplet> t(static_cast<size_t>(nnz));
+  for (int64_t i = 0; i < nnz; ++i) t[i] = {r[i], c[i], v[i]};
+  return t;
+}
+
+int pmmf_ref_write_matrix_market(const char* path, int64_t rows, int64_t cols, int64_t nnz, const int64_t* r,
+                                 const int64_t* c, const double* v, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const auto t = ref_in(nnz, r, c, v);
+    pmmf::write_matrix_market(std::string(path), rows, cols, t);
+  });
+}
+
+int pmmf_ref_laplacian(int64_t n, int64_t nnz, const int64_t* r, const int64_t* c, const double* v, double shift,
+                       int64_t* out_r, int64_t* out_c, double* out_v, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const auto t = ref_in(nnz, r, c, v);
+    const auto o = pmmf::laplacian(t, n, shift);
+    for (size_t i = 0; i < o.size(); ++i) {
+      out_r[i] = o[i].row;
+      out_c[i] = o[i].col;
+      out_v[i] = o[i].value;
+    }
+  });
+}
+
+int pmmf_ref_symmetrize(int64_t nnz, const int64_t* r, const int64_t* c, const double* v, int64_t* out_nnz,
+                        int64_t* out_r, int64_t* out_c, double* out_v, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const auto t = ref_in(nnz, r, c, v);
+    const auto o = pmmf::symmetrize(t);
+    *out_nnz = static_cast<int64_t>(o.size());
+    for (size_t i = 0; i < o.size(); ++i) {
+      out_r[i] = o[i].row;
+      out_c[i] = o[i].col;
+      out_v[i] = o[i].value;
+    }
   });
 }
 

@@ -349,3 +349,89 @@ def make_params(k=2, n_stages=15, eta=0.5, m_target=2, c_min=10, c_max=5000, d_m
     p.cluster_seed = cluster_seed
     p.core_min, p.core_cap, p.seed = core_min, core_cap, seed
     return p
+
+
+# ------------------------------------------------------------- input path
+class Triplets(ctypes.Structure):
+    """pmmf_b200_triplets: TripletMatrix / EdgeList (io.hpp:27-33, :150-154)."""
+
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("row", c_i64p), ("col", c_i64p), ("val", c_f64p), ("n_ids", ctypes.c_int64),
+                ("original_ids", c_i64p)]
+
+
+class IoAbi:
+    """The io.hpp entry points of one library (pmmf_b200_ or the reference's pmmf_ref_)."""
+
+    def __init__(self, lib: ctypes.CDLL, prefix: str, device_args: bool):
+        E = [ctypes.c_char_p, ctypes.c_size_t]
+        V = ctypes.c_void_p
+        self.prefix, self.device_args = prefix, device_args
+
+        def fn(name, argtypes):
+            f = getattr(lib, prefix + name)
+            f.restype = ctypes.c_int
+            f.argtypes = argtypes
+            return f
+
+        TP = ctypes.POINTER(ctypes.POINTER(Triplets))
+        self.read_mm = fn("read_matrix_market", [ctypes.c_char_p, TP] + E)
+        self.read_el = fn("read_edge_list", [ctypes.c_char_p, TP] + E)
+        self.free = getattr(lib, prefix + "triplets_free")
+        self.free.restype = None
+        self.free.argtypes = [ctypes.POINTER(Triplets)]
+        self.write_mm = fn("write_matrix_market", [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                                    V, V, V] + E)
+        dev = [ctypes.c_int32, ctypes.c_int32] if device_args else []
+        self.lap = fn("laplacian", [ctypes.c_int64, ctypes.c_int64, V, V, V, ctypes.c_double] + dev + [V, V, V] + E)
+        self.sym = fn("symmetrize", [ctypes.c_int64, V, V, V] + dev + [ctypes.POINTER(ctypes.c_int64), V, V, V] + E)
+
+    @staticmethod
+    def _take(t):
+        c = t.contents
+        n = c.nnz
+        r = np.ctypeslib.as_array(c.row, (max(n, 1),))[:n].copy()
+        cc = np.ctypeslib.as_array(c.col, (max(n, 1),))[:n].copy()
+        v = np.ctypeslib.as_array(c.val, (max(n, 1),))[:n].copy()
+        ids = None
+        if c.original_ids:
+            ids = np.ctypeslib.as_array(c.original_ids, (max(c.n_ids, 1),))[:c.n_ids].copy()
+        return c.rows, c.cols, r, cc, v, ids
+
+    def read(self, kind: str, path: str):
+        t = ctypes.POINTER(Triplets)()
+        err = ctypes.create_string_buffer(4096)
+        f = self.read_mm if kind == "mm" else self.read_el
+        raise_for(f(os.fsencode(path), ctypes.byref(t), err, len(err)), err)
+        try:
+            return self._take(t)
+        finally:
+            self.free(t)
+
+    def write_matrix_market(self, path, rows, cols, r, c, v):
+        r, c, v = (np.ascontiguousarray(x, t) for x, t in ((r, np.int64), (c, np.int64), (v, np.float64)))
+        err = ctypes.create_string_buffer(4096)
+        raise_for(self.write_mm(os.fsencode(path), int(rows), int(cols), len(v), ptr(r), ptr(c), ptr(v), err,
+                                len(err)), err)
+
+    def laplacian(self, r, c, v, n, shift=0.0, device=0):
+        r, c, v = (np.ascontiguousarray(x, t) for x, t in ((r, np.int64), (c, np.int64), (v, np.float64)))
+        m = len(v) + int(n)
+        o = (np.zeros(m, np.int64), np.zeros(m, np.int64), np.zeros(m, np.float64))
+        err = ctypes.create_string_buffer(4096)
+        dev = [0, int(device)] if self.device_args else []
+        raise_for(self.lap(int(n), len(v), ptr(r), ptr(c), ptr(v), float(shift), *dev, ptr(o[0]), ptr(o[1]),
+                           ptr(o[2]), err, len(err)), err)
+        return o
+
+    def symmetrize(self, r, c, v, device=0):
+        r, c, v = (np.ascontiguousarray(x, t) for x, t in ((r, np.int64), (c, np.int64), (v, np.float64)))
+        m = 2 * len(v)
+        o = (np.zeros(max(m, 1), np.int64), np.zeros(max(m, 1), np.int64), np.zeros(max(m, 1), np.float64))
+        cnt = ctypes.c_int64()
+        err = ctypes.create_string_buffer(4096)
+        dev = [0, int(device)] if self.device_args else []
+        raise_for(self.sym(len(v), ptr(r), ptr(c), ptr(v), *dev, ctypes.byref(cnt), ptr(o[0]), ptr(o[1]), ptr(o[2]),
+                           err, len(err)), err)
+        k = cnt.value
+        return o[0][:k], o[1][:k], o[2][:k]

@@ -341,6 +341,44 @@ def load_factorization(path: str) -> MmfFactorization:
     return out
 
 
+# --------------------------------------------------------------- input path
+_IO: Optional[abi.IoAbi] = None
+
+
+def _io() -> abi.IoAbi:
+    global _IO
+    if _IO is None:
+        _IO = abi.IoAbi(library().lib, "pmmf_b200_", device_args=True)
+    return _IO
+
+
+def read_matrix_market(path: str):
+    """read_matrix_market (io.hpp:68-129) -> (rows, cols, row, col, val)."""
+    rows, cols, r, c, v, _ = _io().read("mm", path)
+    return rows, cols, r, c, v
+
+
+def read_edge_list(path: str):
+    """read_edge_list (io.hpp:158-208) -> (n, row, col, val, original_ids)."""
+    n, _, r, c, v, ids = _io().read("el", path)
+    return n, r, c, v, ids
+
+
+def write_matrix_market(path: str, rows: int, cols: int, r, c, v) -> None:
+    """write_matrix_market (io.hpp:131-147)."""
+    _io().write_matrix_market(path, rows, cols, r, c, v)
+
+
+def laplacian(r, c, v, n: int, shift: float = 0.0, device: int = 0):
+    """laplacian (io.hpp:212-228) on the GPU -> (row, col, val), nnz + n entries."""
+    return _io().laplacian(r, c, v, n, shift, device)
+
+
+def symmetrize(r, c, v, device: int = 0):
+    """symmetrize (io.hpp:231-250) on the GPU -> (row, col, val)."""
+    return _io().symmetrize(r, c, v, device)
+
+
 # -------------------------------------------------------------- workloads
 def _take(w: abi.Workload):
     m = w.nnz
