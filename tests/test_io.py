@@ -135,7 +135,7 @@ def _random_adjacency(n, m, seed, dups=True):
     r = rng.integers(0, n, m)
     c = rng.integers(0, n, m)
     v = rng.random(m) * 10.0 ** rng.integers(-8, 8, m)
-    if dups:  # repeated pairs in both orientations, zeros and negative zeros
+    if dups and m >= 16:  # repeated pairs in both orientations, zeros and negative zeros
         k = m // 4
         r[:k], c[:k] = c[k:2 * k], r[k:2 * k]
         v[5:9] = [0.0, -0.0, 0.0, -0.0]
