@@ -785,7 +785,7 @@ __global__ void k_mass_gather(i64 q0, i64 q1, i64 col0, const int32_t* __restric
     if (take) {
       const i64 d = o + __popc(m & ((1u << lane) - 1u));
       const double v = aval[s0 + i];
-      okey[d] = rg;
+      okey[d] = static_cast<int32_t>(rg - M.rank_base);
       osq[d] = dmul(v, v);
     }
     o += __popc(m);
@@ -816,7 +816,8 @@ __global__ void k_mass_buckets(i64 n, i64 nbuckets, int shift, const int32_t* __
   };
   const i64 b = lb(bkt), e = lb(bkt + 1);
   if (b == e) return;
-  for (int i = lane; i < width; i += 32) m[i] = r0 + i < M.n_retired ? M.mass[r0 + i] : 0.0;
+  double* mass = M.mass + M.rank_base;
+  for (int i = lane; i < width; i += 32) m[i] = r0 + i < M.n_retired ? mass[r0 + i] : 0.0;
   __syncwarp();
   for (i64 x = b; x < e; x += 32) {
     const i64 i = x + lane;
@@ -832,7 +833,7 @@ __global__ void k_mass_buckets(i64 n, i64 nbuckets, int shift, const int32_t* __
     }
   }
   for (int i = lane; i < width; i += 32)
-    if (r0 + i < M.n_retired) M.mass[r0 + i] = m[i];
+    if (r0 + i < M.n_retired) mass[r0 + i] = m[i];
 }
 
 // Per-batch device scratch for the asynchronous level pipeline.

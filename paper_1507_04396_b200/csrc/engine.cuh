@@ -143,7 +143,8 @@ struct MassSpec {
   double* mass = nullptr;             // by rank (zero-initialised by the caller)
   double* diag = nullptr;             // by rank
   i64 chunk_nnz = 0;                  // entries sorted at once
-  i64 n_retired = 0;                  // ranks are [0, n_retired)
+  i64 n_retired = 0;                  // ranks of the retired rows present: [rank_base, rank_base + n_retired)
+  i64 rank_base = 0;                  // (a sharded slab holds only its own clusters' eliminations)
 };
 
 // One pass of a stage's rotations over the columns of `in` (stage

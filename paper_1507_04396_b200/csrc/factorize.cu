@@ -597,8 +597,14 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           if (const char* e = std::getenv("PMMF_B200_BATCH_NNZ")) batch = std::atoll(e);  // test hook
           PMMF_TRACE("[pmmf] stage %d rank %d: column pass -> %lld entries, batch=%lld mem=%zuMB\n", stage_no, me,
                      static_cast<long long>(tn), static_cast<long long>(batch), mem_used_mb());
+          if (ne > 0) {  // this slab's retired rows: its own clusters' eliminations (cluster-major ranks)
+            i64 e0 = 0, e1 = 0;
+            for (i64 u = 0; u < std::min(lo[me + 1], rc); ++u) (u < lo[me] ? e0 : e1) += nelim[u];
+            ms.rank_base = e0;
+            ms.n_retired = e1;
+          }
           rotate_pass(pieces, T, cur.off, slot_base, plan, keep_row.get(), nullptr, batch, growth,
-                      ne > 0 ? &ms : nullptr, s);
+                      ne > 0 && ms.n_retired > 0 ? &ms : nullptr, s);
           T = Csc();
           lap("row_pass");
           i64 stored = 0;
