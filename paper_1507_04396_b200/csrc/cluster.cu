@@ -22,6 +22,7 @@
 
 #include "engine.cuh"
 #include "rng.cuh"
+#include "shard.cuh"
 
 namespace pmmf_b200 {
 
@@ -600,10 +601,19 @@ __global__ void k_anchor_nnz(int m, const int32_t* __restrict__ anchors, const i
   idx[a] = a;
 }
 
+// Every W-th entry of a cost-sorted work list, from `first` (one rank's
+// share of the sparse scorer's columns when clustering is sharded).
+__global__ void k_stride_list(i64 n, const int32_t* __restrict__ in, int W, int first, int32_t* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  const i64 j = first + i * W;
+  if (j < n) out[i] = in[j];
+}
+
 struct Scorer {
   const Csc& a;
   const Numbering& nb;
   cudaStream_t s;
+  const Comm* comm = nullptr;  // sharded scoring (shard.cuh) when it spans several ranks
   DBuf<int32_t> self;  // stage id -> anchor pos (assignment mode)
 
   Scorer(const Csc& mat, const Numbering& numbering, cudaStream_t st) : a(mat), nb(numbering), s(st) {
@@ -678,6 +688,12 @@ struct Scorer {
     if (!use_smem)  // one state slot per launched warp (persistent grid of 148 x 8 blocks)
       scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(148 * 8 * wpb) + 7) / 8), s);
     DBuf<int32_t> dassign(P, s);
+    // Sharded (assignment mode, sparse scorer): the hub columns are scored
+    // on every rank, the rest of the cost-sorted list round-robin over the
+    // ranks; positions a rank did not score keep a sentinel below any
+    // result (-1 = no anchor hit) and an allreduce(max) completes the table.
+    const bool shard = !rows_mode && comm && comm->world() > 1;
+    if (shard) dassign.fill_bytes(0x80);
     DBuf<double> drows;
     if (rows_mode) {
       drows.alloc(P * m, s);
@@ -779,11 +795,28 @@ struct Scorer {
       }
     }
     if (timing) cudaEventRecord(ev[1], s);
-    if (args.nlist > 0) {
+    auto launch_sparse = [&] {
+      if (args.nlist <= 0) return;
       if (use_smem)
         PMMF_LAUNCH(k_score<true>, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb);
       else
         PMMF_LAUNCH(k_score<false>, static_cast<unsigned>(blocks), 32 * wpb, 0, s, args, wpb);
+    };
+    if (!shard) {
+      launch_sparse();
+    } else {
+      const int W = comm->world();
+      const i64 nl = P - nd;
+      DBuf<int32_t> sub(std::max<i64>((nl + W - 1) / W, 1), s);
+      for (const int r : comm->local_ranks()) {
+        const i64 cnt = nl > r ? (nl - r + W - 1) / W : 0;
+        PMMF_LAUNCH(k_stride_list, blocks_for(cnt, kThreads), kThreads, 0, s, nl, list.get() + nd, W, r, sub.get());
+        args.list = sub.get();
+        args.nlist = cnt;
+        next.zero();
+        launch_sparse();
+      }
+      allreduce_max_i32(dassign.get(), P, *comm, s);
     }
     if (timing) cudaEventRecord(ev[2], s);
     if (trace_enabled()) {
@@ -1032,7 +1065,7 @@ void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro&
 
 ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vector<i64>& active, i64 n,
                                i64 m_target, i64 c_min, i64 c_max, int d_max, bool bypass, uint64_t seed,
-                               cudaStream_t s) {
+                               cudaStream_t s, const Comm* comm) {
   if (active.empty()) fail(PMMF_INVALID_ARGUMENT, "cluster_columns: empty active set");
   ClusterOut res;
   // Norms of the active columns (clustering.hpp:189-195).
@@ -1056,6 +1089,7 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
   const auto t_norms = std::chrono::steady_clock::now();
   if (!pool.empty()) {
     Scorer sc(a, nb, s);
+    sc.comm = comm;
     Ctx ctx{&sc, &nb, &norm, c_min, c_max, d_max};
     Xoshiro rng(seed);
     recurse(ctx, std::move(pool), m_target, 0, rng, res.clusters);

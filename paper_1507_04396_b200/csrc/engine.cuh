@@ -73,9 +73,11 @@ struct ClusterOut {
 };
 // cluster_columns (clustering.hpp:183-225) over the pre-reblock matrix a
 // (numbering nb); active ascending global ids.
+struct Comm;
+// comm: score the sparse pool columns sharded over its ranks (shard.cuh).
 ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vector<i64>& active, i64 n,
                                i64 m_target, i64 c_min, i64 c_max, int d_max, bool bypass, uint64_t seed,
-                               cudaStream_t s);
+                               cudaStream_t s, const Comm* comm = nullptr);
 
 // ---- gram.cu
 // Dense c_u x c_u column-major tiles of G_u (blocked_matrix.hpp:238-254)

@@ -263,7 +263,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     auto t0 = clk::now();
     const uint64_t cpath[2] = {0xC1u, static_cast<uint64_t>(stage_no)};
     ClusterOut co = cluster_columns_dev(A, cur, active, n, p.m_target, p.c_min, p.c_max, p.d_max,
-                                        p.bypass_enabled != 0, derive(p.seed, cpath), s);
+                                        p.bypass_enabled != 0, derive(p.seed, cpath), s, comm);
     R->phases[0] += ms_since(t0);
     const i64 rc = static_cast<i64>(co.clusters.size());
     std::vector<std::vector<i64>> stage_clusters = std::move(co.clusters);

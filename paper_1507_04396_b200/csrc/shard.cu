@@ -92,9 +92,11 @@ void bcast_segments(void* dev, size_t elem, const std::vector<i64>& seg, const C
   PMMF_NCCL(ncclGroupEnd());
 }
 
-void allreduce_max_i32(int32_t* dev, const Comm& c, cudaStream_t s) {
-  if (!c.multi_process()) return;
-  PMMF_NCCL(ncclAllReduce(dev, dev, 1, ncclInt32, ncclMax, c.nccl, s));
+void allreduce_max_i32(int32_t* dev, const Comm& c, cudaStream_t s) { allreduce_max_i32(dev, 1, c, s); }
+
+void allreduce_max_i32(int32_t* dev, i64 n, const Comm& c, cudaStream_t s) {
+  if (!c.multi_process() || n <= 0) return;
+  PMMF_NCCL(ncclAllReduce(dev, dev, static_cast<size_t>(n), ncclInt32, ncclMax, c.nccl, s));
 }
 
 void csc_gather_slabs(Csc& out, std::vector<Csc>& parts, const std::vector<i64>& col_seg, i64 N, const Comm& c,

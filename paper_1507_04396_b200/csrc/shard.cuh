@@ -70,6 +70,7 @@ std::vector<i64> cluster_ptr(const Csc& a, const std::vector<i64>& off, cudaStre
 void bcast_segments(void* dev, size_t elem, const std::vector<i64>& seg, const Comm& c, cudaStream_t s);
 // max over ranks of one device int32 (no-op for one process).
 void allreduce_max_i32(int32_t* dev, const Comm& c, cudaStream_t s);
+void allreduce_max_i32(int32_t* dev, i64 n, const Comm& c, cudaStream_t s);
 
 // The full matrix from the per-rank column slabs: parts[i] holds (over all
 // N columns) only the columns [col_seg[r], col_seg[r+1]) of local rank
