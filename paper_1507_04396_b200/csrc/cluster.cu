@@ -808,14 +808,27 @@ struct Scorer {
       const int W = comm->world();
       const i64 nl = P - nd;
       DBuf<int32_t> sub(std::max<i64>((nl + W - 1) / W, 1), s);
+      static const bool st_timing = std::getenv("PMMF_B200_SHARD_TIMING") != nullptr || trace_enabled();
+      const bool per_rank = st_timing && comm->virt;  // scripts/shard_model.py
+      double tsum = 0.0, tmax = 0.0;
       for (const int r : comm->local_ranks()) {
+        if (per_rank) PMMF_CUDA(cudaStreamSynchronize(s));
+        const auto tr0 = std::chrono::steady_clock::now();
         const i64 cnt = nl > r ? (nl - r + W - 1) / W : 0;
         PMMF_LAUNCH(k_stride_list, blocks_for(cnt, kThreads), kThreads, 0, s, nl, list.get() + nd, W, r, sub.get());
         args.list = sub.get();
         args.nlist = cnt;
         next.zero();
         launch_sparse();
+        if (per_rank) {
+          PMMF_CUDA(cudaStreamSynchronize(s));
+          const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
+          tsum += ms;
+          tmax = std::max(tmax, ms);
+        }
       }
+      if (per_rank)
+        std::fprintf(stderr, "[pmmf] shard score: %d ranks, sum %.3f ms, max %.3f ms\n", W, tsum, tmax);
       allreduce_max_i32(dassign.get(), P, *comm, s);
     }
     if (timing) cudaEventRecord(ev[2], s);

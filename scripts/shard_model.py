@@ -8,6 +8,9 @@ slab apply time per stage.  Then
 
   T_W = T_virtual - sum_s sum_r (gs_rs + ap_rs) + sum_s (max_r gs_rs + max_r ap_rs) + X_W
 
+(the sharded clustering scorer's calls enter the same way: sum over ranks
+out, max over ranks in)
+
 where the clustering/reblock/bookkeeping remainder is replicated on every
 rank and X_W is the slab exchange: every rank receives the other ranks'
 slabs, 12 B x nnz(A'') x (W-1)/W per stage, at an assumed NCCL broadcast
@@ -106,6 +109,10 @@ def model(res, world, gbs):
     stages = sorted({s for s, _ in gs} | {s for s, _ in ap})
     serial = sum(gs.values()) + sum(ap.values())
     par = 0.0
+    # sharded clustering scorer: every call's ranks ran back to back
+    for m in re.finditer(r"shard score: (\d+) ranks, sum ([\d.]+) ms, max ([\d.]+) ms", res["trace"]):
+        serial += float(m[2])
+        par += float(m[3])
     xbytes = 0.0
     per_stage = []
     for s in stages:
