@@ -183,6 +183,13 @@ int pmmf_b200_operator_create(void* result, double zero_threshold, void** op, ch
  * in/out are host pointers unless on_device != 0. */
 int pmmf_b200_operator_apply(void* op, int32_t mode, int64_t nrhs, const double* in,
                              double* out, int32_t on_device, char* err, size_t errlen);
+/* residual_frobenius (transform_ops.hpp:225-237): method 0 = accumulated
+ * (sqrt(residual_sq)), 1 = dense ||A - Q^T H Q||_F with the reconstruction
+ * on the GPU (reconstruct_dense, :175-213; PMMF_NUMERIC when n > cap, as
+ * the reference).  The dense value equals the reference's up to rounding
+ * (it reconstructs by the apply's level order). */
+int pmmf_b200_residual_frobenius(void* result, const pmmf_b200_coo* a, int32_t method, int64_t cap, double* out,
+                                 char* err, size_t errlen);
 /* inv_sqrt_zeroed_negatives() (transform_ops.hpp:47-49). */
 int pmmf_b200_operator_zeroed_negatives(void* op, int64_t* out);
 void pmmf_b200_operator_free(void* op);

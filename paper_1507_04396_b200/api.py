@@ -61,6 +61,9 @@ def library() -> abi.FlatAbi:
         L.pmmf_b200_result_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(V)] + E
         L.pmmf_b200_result_params.restype = ctypes.c_int
         L.pmmf_b200_result_params.argtypes = [V, ctypes.POINTER(abi.Params)]
+        L.pmmf_b200_residual_frobenius.restype = ctypes.c_int
+        L.pmmf_b200_residual_frobenius.argtypes = [V, ctypes.POINTER(abi.Coo), ctypes.c_int32, ctypes.c_int64,
+                                                   ctypes.POINTER(ctypes.c_double)] + E
         L.pmmf_b200_shard_ranges.restype = ctypes.c_int
         L.pmmf_b200_shard_ranges.argtypes = [ctypes.c_int64, V, V, ctypes.c_int32, V]
     return _ABI
@@ -339,6 +342,20 @@ def load_factorization(path: str) -> MmfFactorization:
                                                        d_max=p.d_max, bypass_enabled=bool(p.bypass_enabled),
                                                        seed=p.cluster_seed))
     return out
+
+
+def residual_frobenius(handle: ctypes.c_void_p, matrix: "BlockedSparseMatrix", method: str = "dense",
+                       cap: int = 4096, device: int = 0) -> float:
+    """residual_frobenius (transform_ops.hpp:225-237): "accumulated" =
+    sqrt(residual_sq); "dense" = ||A - Q^T H Q||_F reconstructed on the GPU."""
+    lib = library()
+    coo, keep = matrix.coo(device)
+    out = ctypes.c_double()
+    err = lib.errbuf()
+    st = lib.lib.pmmf_b200_residual_frobenius(handle, ctypes.byref(coo), 0 if method == "accumulated" else 1,
+                                              int(cap), ctypes.byref(out), err, len(err))
+    abi.raise_for(st, err)
+    return out.value
 
 
 # --------------------------------------------------------------- input path

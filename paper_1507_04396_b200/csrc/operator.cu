@@ -426,6 +426,46 @@ __global__ void k_from_imaj(int64_t n, int nrhs, const double* __restrict__ in, 
 }  // namespace
 
 // ============================================================== Operator
+__global__ void k_dense_scatter_coo(int64_t nnz, int64_t n, const int64_t* __restrict__ r,
+                                    const int64_t* __restrict__ c, const double* __restrict__ v,
+                                    double* __restrict__ A, int* __restrict__ bad) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= nnz) return;
+  if (r[t] < 0 || r[t] >= n || c[t] < 0 || c[t] >= n) {
+    atomicExch(bad, 1);
+    return;
+  }
+  atomicAdd(A + r[t] * n + c[t], v[t]);
+}
+
+// index-major n x cnt block of unit vectors e_{j0 + r}
+__global__ void k_unit_block(int64_t n, int cnt, int64_t j0, double* __restrict__ V) {
+  const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= n * cnt) return;
+  const int64_t i = t / cnt, r = t % cnt;
+  V[t] = i == j0 + r ? 1.0 : 0.0;
+}
+
+// per-block partial sums of (A[i][j0+r] - V[i][r])^2 over the batch
+__global__ void k_diff_sq(int64_t n, int cnt, int64_t j0, const double* __restrict__ A, const double* __restrict__ V,
+                          double* __restrict__ part) {
+  extern __shared__ double red[];
+  double acc = 0.0;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < n * cnt;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = t / cnt, r = t % cnt;
+    const double d = A[i * n + j0 + r] - V[t];
+    acc += d * d;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
 struct Operator {
   int device = 0;
   int64_t n = 0;
@@ -829,6 +869,71 @@ int pmmf_b200_operator_apply(void* opv, int32_t mode, int64_t nrhs, const double
     else
       a.download(out, m);
     PMMF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// ||A - Q^T H Q||_F, dense (residual_frobenius with ResidualMethod::dense,
+// transform_ops.hpp:225-237): Q^T H Q e_j for batches of unit vectors
+// through the operator's forward apply (reconstruct_dense,
+// transform_ops.hpp:175-213, by the apply's level order instead of the
+// reference's rotation-by-rotation order: equal up to rounding), minus the
+// dense input, squared and summed per batch by a fixed-shape reduction.
+int pmmf_b200_residual_frobenius(void* result, const pmmf_b200_coo* a, int32_t method, int64_t cap, double* out,
+                                 char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!result || !a || !out) fail(PMMF_INVALID_ARGUMENT, "residual_frobenius: null argument");
+    const Result& f = *static_cast<Result*>(result);
+    if (method == 0) {  // ResidualMethod::accumulated
+      *out = std::sqrt(f.residual_sq);
+      return;
+    }
+    if (method != 1) fail(PMMF_INVALID_ARGUMENT, "residual_frobenius: bad method");
+    const int64_t n = f.n;
+    if (n > cap) fail(PMMF_NUMERIC, "reconstruct_dense: dimension exceeds cap");
+    if (a->n != n) fail(PMMF_INVALID_ARGUMENT, "residual_frobenius: matrix dimension differs");
+    PMMF_CUDA(cudaSetDevice(a->device));
+    Operator o;
+    o.thr = 0.0;
+    o.build(f);
+    cudaStream_t s = o.s;
+    // dense A, row-major (duplicates summed)
+    DBuf<double> A(std::max<int64_t>(n * n, 1), s);
+    A.zero();
+    if (a->nnz > 0) {
+      DBuf<int64_t> r, c;
+      DBuf<double> v;
+      const int64_t* pr = a->rows;
+      const int64_t* pc = a->cols;
+      const double* pv = a->vals;
+      if (!a->on_device) {
+        r.alloc(a->nnz, s);
+        c.alloc(a->nnz, s);
+        v.alloc(a->nnz, s);
+        r.upload(a->rows, a->nnz);
+        c.upload(a->cols, a->nnz);
+        v.upload(a->vals, a->nnz);
+        pr = r.get();
+        pc = c.get();
+        pv = v.get();
+      }
+      DBuf<int> bad(1, s);
+      bad.zero();
+      PMMF_LAUNCH(k_dense_scatter_coo, blocks_for(a->nnz, kThreads), kThreads, 0, s, a->nnz, n, pr, pc, pv, A.get(),
+                  bad.get());
+      if (bad.to_host(1)[0]) fail(PMMF_OUT_OF_RANGE, "residual_frobenius: index out of range");
+    }
+    const int nb = static_cast<int>(std::min<int64_t>(n, 256));
+    DBuf<double> V(n * nb, s), part(1024, s);
+    double total = 0.0;
+    for (int64_t j0 = 0; j0 < n; j0 += nb) {
+      const int cnt = static_cast<int>(std::min<int64_t>(nb, n - j0));
+      PMMF_LAUNCH(k_unit_block, blocks_for(n * cnt, kThreads), kThreads, 0, s, n, cnt, j0, V.get());
+      o.apply_dev(PMMF_APPLY_FORWARD, cnt, V.get(), s);
+      PMMF_LAUNCH(k_diff_sq, 1024, kThreads, kThreads * sizeof(double), s, n, cnt, j0, A.get(), V.get(), part.get());
+      const std::vector<double> h = part.to_host(1024);
+      for (double x : h) total += x;
+    }
+    *out = std::sqrt(total);
   });
 }
 
