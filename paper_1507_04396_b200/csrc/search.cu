@@ -906,7 +906,15 @@ void search_clusters(const SearchBatch& b, i64 u0, i64 nclusters, int k, double 
         int dev = 0;
         if (cudaGetDevice(&dev) == cudaSuccess) (void)cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       }
-      auto t_of = [](i64 c, int w) { return 0.5 * static_cast<double>(c) * (3.0 + 0.0035 * static_cast<double>(c) / w); };
+      // per-iteration cost alpha + beta c / w (us); tunable for the sweep in
+      // scripts/search_sweep.sh
+      double a1 = 3.0, acl = 3.0, beta = 0.0035;
+      if (const char* e = std::getenv("PMMF_B200_SEARCH_A1")) a1 = std::atof(e);
+      if (const char* e = std::getenv("PMMF_B200_SEARCH_ACL")) acl = std::atof(e);
+      if (const char* e = std::getenv("PMMF_B200_SEARCH_BETA")) beta = std::atof(e);
+      auto t_of = [=](i64 c, int w) {
+        return 0.5 * static_cast<double>(c) * ((w >= 2 ? acl : a1) + beta * static_cast<double>(c) / w);
+      };
       auto sm_time = [&](i64 c, int w) { return (w >= 2 ? w : 0.5) * t_of(c, w); };
       for (;;) {
         double work = 0.0, longest = 0.0;
