@@ -64,3 +64,37 @@ def test_sharded_rmat16_full():
     finally:
         comm.close()
     oracles.assert_same(sharded, oracles.factorize("gpu", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat14_m32", "c1_dense1024"])
+@pytest.mark.parametrize("world", [5, 16])
+def test_virtual_ranks_larger(name, world):
+    """More ranks than most stages have large clusters, uneven splits."""
+    inp, params, part = cases.build(name)
+    comm = api.Communicator(world, virtual=True)
+    try:
+        gpu = oracles.factorize("gpu", inp, params, part, comm=comm)
+    finally:
+        comm.close()
+    oracles.assert_same(gpu, oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "k3_sparse", "grid64_m16"])
+@pytest.mark.parametrize("env", [
+    {"PMMF_B200_SEARCH_BIG_C": "2", "PMMF_B200_SEARCH_CSIZE": "16", "PMMF_B200_SEARCH_FORCE_W": "4"},
+    {"PMMF_B200_DENSE_DIV": "3"},
+    {"PMMF_B200_GRAM_DENSE_RATIO": "1e30"},
+    {"PMMF_B200_SCORE_GEMM": "1"},
+], ids=["cluster_search", "dense_scoring", "dense_gram", "gemm_scorer"])
+def test_virtual_ranks_alternative_paths(name, env, monkeypatch):
+    """The sharded stage loop over every alternative kernel path (the sharded
+    scorer only splits the sparse scorer; the GEMM scorer stays whole)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    inp, params, part = cases.build(name)
+    comm = api.Communicator(3, virtual=True)
+    try:
+        gpu = oracles.factorize("gpu", inp, params, part, comm=comm)
+    finally:
+        comm.close()
+    oracles.assert_same(gpu, oracles.factorize("oracle", inp, params, part))
