@@ -209,6 +209,13 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     }
     cur.build(init, std::max<i64>(n, 0), s);
   }
+  auto plap = [&, tp = clk::now()](const char* what) mutable {  // trace-mode prologue laps
+    if (!trace_on()) return;
+    PMMF_CUDA(cudaStreamSynchronize(s));
+    PMMF_TRACE("[pmmf]   prologue.%s %.2f ms\n", what, ms_since(tp));
+    tp = clk::now();
+  };
+  plap("numbering");
   Csc A;
   {
     const int64_t* rows = in->rows;
@@ -227,13 +234,16 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       cols = dcol.get();
       vals = dval.get();
     }
+    plap("upload");
     csc_from_coo(A, cur, std::max<i64>(n, 0), in->nnz, rows, cols, vals, s);
+    plap("from_triplets");
   }
   validate(p);
   if (n < 1) fail(PMMF_INVALID_ARGUMENT, "factorize: empty matrix");
   {
     double asym = 0.0, fro = 0.0;
     csc_symmetry(A, cur, &asym, &fro, s);
+    plap("symmetry");
     if (asym > 1e-9 * std::max(std::sqrt(fro), 1e-300))
       fail(PMMF_INVALID_ARGUMENT, "factorize: input matrix is not symmetric");
   }
