@@ -851,7 +851,22 @@ struct LevelScratch {
   double rot_bytes = 0.0;
 };
 
-constexpr int kPersistentBlocks = 148 * 8;
+// Persistent grid of the merge kernels: exactly the resident capacity
+// (blocks per SM at this kernel's register use x SMs).  A larger grid runs
+// its surplus blocks as a second, thin wave whose statically strided items
+// finish last.
+template <int K, bool kWrite>
+int persistent_blocks() {
+  static const int nb = [] {
+    int per_sm = 0, dev = 0, sms = 148;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0) != cudaSuccess)
+      per_sm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    (void)cudaGetLastError();
+    return std::max(1, per_sm) * sms;
+  }();
+  return nb;
+}
 
 // One dependency level of a batch, entirely on the device (no host sync).
 template <int K>
@@ -896,7 +911,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     c1 = EventPool::get().take();
     cudaEventRecord(c0, s);
   }
-  PMMF_LAUNCH((k_merge_p<K, false>), kPersistentBlocks, kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  PMMF_LAUNCH((k_merge_p<K, false>), (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (c0) {
     cudaEventRecord(c1, s);
     S.cev.push_back({c0, c1});
@@ -909,7 +924,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     e1 = EventPool::get().take();
     cudaEventRecord(e0, s);
   }
-  PMMF_LAUNCH((k_merge_p<K, true>), kPersistentBlocks, kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  PMMF_LAUNCH((k_merge_p<K, true>), (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (e0) {
     cudaEventRecord(e1, s);
     S.ev.push_back({e0, e1});
