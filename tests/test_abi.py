@@ -69,3 +69,22 @@ def test_error_mapping_types():
     assert issubclass(abi.OutOfRange, IndexError)
     with pytest.raises(abi.NumericError):
         abi.raise_for(3, ctypes.create_string_buffer(b"x"))
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/pmmf_b200.h is the drop-in boundary for cgo/ctypes/C callers:
+    it must compile as strict C99 with no C++ types."""
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        import pytest
+
+        pytest.skip("no C compiler")
+    src = tmp_path / "h.c"
+    src.write_text('#include "pmmf_b200.h"\nint main(void) { return (int)sizeof(pmmf_b200_triplets) == 0; }\n')
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", inc, "-c", str(src), "-o",
+                        str(tmp_path / "h.o")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
