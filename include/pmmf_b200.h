@@ -59,7 +59,14 @@ typedef struct pmmf_b200_params {
 /* Input matrix in coordinate form plus its block partition: the data of
  * BlockedSparseMatrix::from_triplets(n, entries, partition)
  * (blocked_matrix.hpp:133-156).  n_clusters == 0 means Partition::trivial(n)
- * (partition.hpp:57-61).  Duplicates are summed in input order. */
+ * (partition.hpp:57-61).  Duplicates are summed in input order.
+ *
+ * Device input (on_device != 0): rows/cols/vals must be CUDA pointers on
+ * `device`.  The library reads them on its own non-blocking stream, so the
+ * caller must have COMPLETED the work that produced them before the call
+ * (e.g. cudaStreamSynchronize on the producing stream); the Python layer
+ * does this for torch tensors.  Every entry point that takes device
+ * buffers returns only after its device outputs are complete. */
 typedef struct pmmf_b200_coo {
   int64_t n;
   int64_t nnz;

@@ -30,6 +30,8 @@
 #include <vector>
 
 #include "../include/pmmf_b200.h"
+#include "../include/pmmf_b200_workloads.h"
+#include "../paper_1507_04396_b200/csrc/recipes.hpp"
 
 namespace {
 
@@ -393,6 +395,59 @@ int pmmf_ref_symmetrize(int64_t nnz, const int64_t* r, const int64_t* c, const d
       out_v[i] = o[i].value;
     }
   });
+}
+
+// ---- seeded inputs on the reference's own generator (pmmf::Rng, rng.hpp) ----
+// The recipes of SURVEY.md §8(d) (paper_1507_04396_b200/csrc/recipes.hpp,
+// templates over the draw interface) instantiated on pmmf::Rng, so the
+// --impl reference arm of bench.py never loads libpmmf_b200.so.
+
+static int ref_emit(const pmmf_recipes::Coo& coo, pmmf_b200_workload* out) {
+  const size_t m = coo.v.size();
+  out->n = coo.n;
+  out->nnz = static_cast<int64_t>(m);
+  out->rows = static_cast<int64_t*>(std::malloc(std::max<size_t>(1, m) * sizeof(int64_t)));
+  out->cols = static_cast<int64_t*>(std::malloc(std::max<size_t>(1, m) * sizeof(int64_t)));
+  out->vals = static_cast<double*>(std::malloc(std::max<size_t>(1, m) * sizeof(double)));
+  if (!out->rows || !out->cols || !out->vals) return 1;
+  if (m) {
+    std::memcpy(out->rows, coo.r.data(), m * sizeof(int64_t));
+    std::memcpy(out->cols, coo.c.data(), m * sizeof(int64_t));
+    std::memcpy(out->vals, coo.v.data(), m * sizeof(double));
+  }
+  return 0;
+}
+
+int pmmf_ref_workload_rmat(int32_t scale, int32_t epv, uint64_t seed, double shift, pmmf_b200_workload* out) {
+  pmmf::Rng rng(seed);
+  pmmf_recipes::Coo coo;
+  return pmmf_recipes::rmat(scale, epv, rng, shift, coo) ? ref_emit(coo, out) : 1;
+}
+
+int pmmf_ref_workload_dense_spd(int64_t n, int64_t d, uint64_t seed, double shift, pmmf_b200_workload* out) {
+  pmmf::Rng rng(seed);
+  pmmf_recipes::Coo coo;
+  return pmmf_recipes::dense_spd(n, d, rng, shift, coo) ? ref_emit(coo, out) : 1;
+}
+
+int pmmf_ref_workload_rbf(int64_t n, int32_t dim, double bw, uint64_t seed, double shift, pmmf_b200_workload* out) {
+  pmmf::Rng rng(seed);
+  pmmf_recipes::Coo coo;
+  return pmmf_recipes::rbf(n, dim, bw, rng, shift, coo) ? ref_emit(coo, out) : 1;
+}
+
+int pmmf_ref_workload_aniso_grid(int64_t side, double ax, double ay, pmmf_b200_workload* out) {
+  pmmf_recipes::Coo coo;
+  return pmmf_recipes::aniso_grid(side, ax, ay, coo) ? ref_emit(coo, out) : 1;
+}
+
+void pmmf_ref_workload_free(pmmf_b200_workload* w) {
+  if (!w) return;
+  std::free(w->rows);
+  std::free(w->cols);
+  std::free(w->vals);
+  w->rows = w->cols = nullptr;
+  w->vals = nullptr;
 }
 
 }  // extern "C"

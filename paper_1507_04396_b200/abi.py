@@ -308,16 +308,39 @@ class FlatAbi:
         )
 
 
+def _check_device_triplets(rows, cols, vals, device):
+    """Device triplets must be CUDA tensors on `device`, contiguous, int64 /
+    int64 / float64 and of equal length (the C-ABI reads them as raw
+    pointers, include/pmmf_b200.h)."""
+    import torch
+
+    want = (torch.int64, torch.int64, torch.float64)
+    for name, x, dt in zip(("rows", "cols", "vals"), (rows, cols, vals), want):
+        if not getattr(x, "is_cuda", False):
+            raise ValueError(f"device input: {name} is not a CUDA tensor")
+        if x.dtype != dt:
+            raise ValueError(f"device input: {name} has dtype {x.dtype}, expected {dt}")
+        if not x.is_contiguous():
+            raise ValueError(f"device input: {name} is not contiguous")
+        if x.device.index != int(device):
+            raise ValueError(f"device input: {name} lives on cuda:{x.device.index}, the call targets cuda:{device}")
+    if not (rows.numel() == cols.numel() == vals.numel()):
+        raise ValueError(f"device input: lengths differ ({rows.numel()}, {cols.numel()}, {vals.numel()})")
+
+
 def make_coo(n, rows, cols, vals, clusters=None, on_device=False, device=0, keep=None):
     """Builds a Coo struct; ``keep`` collects the arrays that must outlive it."""
     keep = [] if keep is None else keep
     c = Coo()
     c.n = int(n)
     if on_device:
+        _check_device_triplets(rows, cols, vals, device)
         c.nnz = int(rows.numel())
         c.rows, c.cols, c.vals = rows.data_ptr(), cols.data_ptr(), vals.data_ptr()
         keep += [rows, cols, vals]
     else:
+        if hasattr(rows, "is_cuda"):  # CPU torch tensors: host buffers
+            rows, cols, vals = (x.numpy() for x in (rows, cols, vals))
         rows = np.ascontiguousarray(rows, np.int64)
         cols = np.ascontiguousarray(cols, np.int64)
         vals = np.ascontiguousarray(vals, np.float64)

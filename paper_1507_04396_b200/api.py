@@ -233,7 +233,7 @@ class BlockedSparseMatrix:
 
     @property
     def on_device(self) -> bool:
-        return hasattr(self.rows, "data_ptr")
+        return bool(getattr(self.rows, "is_cuda", False))
 
     def coo(self, device: int = 0):
         clusters = None
@@ -279,6 +279,12 @@ def factorize(matrix: BlockedSparseMatrix, params: FactorizeParams, device: int 
     every rank returns the same factorization)."""
     lib = library()
     coo, keep = matrix.coo(device)
+    if matrix.on_device:
+        # the library reads the triplets on its own stream: order it after
+        # the work that produced them (include/pmmf_b200.h, "Device input")
+        import torch
+
+        torch.cuda.current_stream(device).synchronize()
     p = params.to_c()
     h = ctypes.c_void_p()
     err = lib.errbuf()
@@ -298,6 +304,12 @@ def factorize_handle(matrix: BlockedSparseMatrix, params: FactorizeParams, devic
     """Raw result handle (caller frees with library().result_free)."""
     lib = library()
     coo, keep = matrix.coo(device)
+    if matrix.on_device:
+        # the library reads the triplets on its own stream: order it after
+        # the work that produced them (include/pmmf_b200.h, "Device input")
+        import torch
+
+        torch.cuda.current_stream(device).synchronize()
     p = params.to_c()
     h = ctypes.c_void_p()
     err = lib.errbuf()

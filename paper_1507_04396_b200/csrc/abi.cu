@@ -126,6 +126,7 @@ int pmmf_b200_result_params(void* h, pmmf_b200_params* out) {
 }
 
 int pmmf_b200_result_summary(void* h, pmmf_b200_summary* o) {
+  if (!h || !o) return PMMF_INVALID_ARGUMENT;
   auto* r = static_cast<Result*>(h);
   o->n = r->n;
   o->n_stages = static_cast<int64_t>(r->stages.size());
@@ -138,12 +139,14 @@ int pmmf_b200_result_summary(void* h, pmmf_b200_summary* o) {
 }
 
 int pmmf_b200_result_active_history(void* h, int64_t* o) {
+  if (!h || (!o && !static_cast<Result*>(h)->hist.empty())) return PMMF_INVALID_ARGUMENT;
   auto* r = static_cast<Result*>(h);
   std::copy(r->hist.begin(), r->hist.end(), o);
   return PMMF_OK;
 }
 
 int pmmf_b200_result_stage_sizes(void* h, int64_t s, pmmf_b200_stage_sizes* o) {
+  if (!h || !o) return PMMF_INVALID_ARGUMENT;
   auto* r = static_cast<Result*>(h);
   if (s < 0 || s >= static_cast<int64_t>(r->stages.size())) return PMMF_OUT_OF_RANGE;
   const auto& st = r->stages[s];
@@ -157,6 +160,7 @@ int pmmf_b200_result_stage_sizes(void* h, int64_t s, pmmf_b200_stage_sizes* o) {
 
 int pmmf_b200_result_stage(void* h, int64_t s, int64_t* offs, int64_t* mem, int64_t* ri, double* rq, int64_t* ei,
                            double* ed, double* em, int64_t* by) {
+  if (!h || !offs || !mem || !ri || !rq || !ei || !ed || !em || !by) return PMMF_INVALID_ARGUMENT;
   auto* r = static_cast<Result*>(h);
   if (s < 0 || s >= static_cast<int64_t>(r->stages.size())) return PMMF_OUT_OF_RANGE;
   const auto& st = r->stages[s];
@@ -172,6 +176,7 @@ int pmmf_b200_result_stage(void* h, int64_t s, int64_t* offs, int64_t* mem, int6
 }
 
 int pmmf_b200_result_core(void* h, int64_t* ci, double* core, int64_t* di, double* dv) {
+  if (!h || !ci || !core || !di || !dv) return PMMF_INVALID_ARGUMENT;
   auto* r = static_cast<Result*>(h);
   std::copy(r->core_idx.begin(), r->core_idx.end(), ci);
   std::copy(r->core.begin(), r->core.end(), core);
@@ -183,6 +188,7 @@ int pmmf_b200_result_core(void* h, int64_t* ci, double* core, int64_t* di, doubl
 }
 
 int pmmf_b200_result_stats(void* h, double* phases, int64_t* info) {
+  if (!h || !phases || (!info && !static_cast<Result*>(h)->info.empty())) return PMMF_INVALID_ARGUMENT;
   auto* r = static_cast<Result*>(h);
   std::copy(r->phases, r->phases + 6, phases);
   for (size_t s = 0; s < r->info.size(); ++s) std::copy(r->info[s].begin(), r->info[s].end(), info + 7 * s);

@@ -391,6 +391,39 @@ std::string factorization_to_json(const Result& r) {  // serialize.hpp:61-110
   return std::move(o.b);
 }
 
+// A loaded factorization drives device kernels that index arrays by these
+// values (operator.cu): reject anything out of range as PMMF_DATA instead
+// of corrupting memory.  k bounds the operator's per-rotation registers
+// (kMaxK = 8, factorizer.hpp:44-46 allows k >= 2).
+static void validate(const Result& r) {
+  auto bad = [](const char* what) { fail(PMMF_DATA, std::string("factorization file: ") + what); };
+  if (r.n < 0) bad("negative n");
+  if (r.k < 2 || r.k > 8) bad("params.k outside [2, 8]");
+  auto in_range = [&](int64_t i) { return i >= 0 && i < r.n; };
+  for (const Result::Stage& st : r.stages) {
+    if (st.off.empty() || st.off.front() != 0 || st.off.back() != static_cast<int64_t>(st.members.size()))
+      bad("inconsistent partition offsets");
+    for (size_t u = 0; u + 1 < st.off.size(); ++u)
+      if (st.off[u + 1] < st.off[u]) bad("inconsistent partition offsets");
+    for (int64_t m : st.members)
+      if (!in_range(m)) bad("partition member out of range");
+    for (int64_t b : st.bypassed)
+      if (!in_range(b)) bad("bypassed index out of range");
+    for (int64_t i : st.rot_idx)
+      if (!in_range(i)) bad("rotation index out of range");
+    for (int64_t i : st.elim_idx)
+      if (!in_range(i)) bad("eliminated index out of range");
+    if (st.rot_q.size() != st.rot_idx.size() * static_cast<size_t>(r.k)) bad("rotation matrix size mismatch");
+  }
+  for (int64_t i : r.core_idx)
+    if (!in_range(i)) bad("core index out of range");
+  for (const auto& d : r.diag)
+    if (!in_range(d.first)) bad("diagonal index out of range");
+  if (r.hist.size() > 0)
+    for (int64_t h : r.hist)
+      if (h < 0 || h > r.n) bad("active history out of range");
+}
+
 std::unique_ptr<Result> factorization_from_json(const char* text, size_t len) {  // serialize.hpp:112-165
   JVal j;
   Parser ps{text, text + len, text};
@@ -423,6 +456,8 @@ std::unique_ptr<Result> factorization_from_json(const char* text, size_t len) { 
     p.bypass_enabled = c.at("bypass").as_bool() ? 1 : 0;
     p.cluster_seed = c.at("seed").as_u64();
     r->k = p.k;
+    if (r->k < 2 || r->k > 8) fail(PMMF_DATA, "factorization file: params.k outside [2, 8]");
+    if (r->n < 0) fail(PMMF_DATA, "factorization file: negative n");
   }
   int k = r->k;
   for (const JVal& js : j.at("stages").arr()) {
@@ -462,6 +497,7 @@ std::unique_ptr<Result> factorization_from_json(const char* text, size_t len) { 
   }
   for (const JVal& jd : j.at("diagonal").arr()) r->diag.emplace_back(jd.at("i").as_int(), jd.at("d").as_double());
   r->trivial = r->stages.empty();
+  validate(*r);
   return r;
 }
 

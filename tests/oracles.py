@@ -34,6 +34,33 @@ def load(which: str) -> abi.FlatAbi:
     return _cache[which]
 
 
+def ref_workload(kind: str, *args):
+    """Seeded SURVEY.md §8(d) inputs generated on the reference's own pmmf::Rng
+    (oracle/ref_driver.cpp), without loading libpmmf_b200.so.
+    kind: rmat(scale, epv, seed, shift) | dense_spd(n, d, seed, shift) |
+          rbf(n, dim, bw, seed, shift) | aniso_grid(side, ax, ay)."""
+    lib = load("ref").lib
+    fn = getattr(lib, "pmmf_ref_workload_" + kind)
+    sig = {"rmat": [ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double],
+           "dense_spd": [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double],
+           "rbf": [ctypes.c_int64, ctypes.c_int32, ctypes.c_double, ctypes.c_uint64, ctypes.c_double],
+           "aniso_grid": [ctypes.c_int64, ctypes.c_double, ctypes.c_double]}[kind]
+    fn.argtypes = sig + [ctypes.POINTER(abi.Workload)]
+    fn.restype = ctypes.c_int
+    lib.pmmf_ref_workload_free.argtypes = [ctypes.POINTER(abi.Workload)]
+    w = abi.Workload()
+    if fn(*args, ctypes.byref(w)):
+        raise ValueError(f"ref workload {kind}{args}: bad arguments")
+    try:
+        m = w.nnz
+        rows = np.ctypeslib.as_array(w.rows, (m,)).copy() if m else np.zeros(0, np.int64)
+        cols = np.ctypeslib.as_array(w.cols, (m,)).copy() if m else np.zeros(0, np.int64)
+        vals = np.ctypeslib.as_array(w.vals, (m,)).copy() if m else np.zeros(0)
+        return int(w.n), rows, cols, vals
+    finally:
+        lib.pmmf_ref_workload_free(ctypes.byref(w))
+
+
 def available(which: str) -> bool:
     return os.path.exists({"oracle": ORACLE, "ref": REF}[which])
 

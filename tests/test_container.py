@@ -112,6 +112,15 @@ def test_bad_files(tmp_path):
         (lambda d: d["core"]["dense"].pop(), "core size mismatch"),
         (lambda d: d["stages"][0]["rotations"][0]["q"].pop(), "rotation matrix size mismatch"),
         (lambda d: d.pop("n"), "missing key"),
+        (lambda d: d["params"].update(k=0), "params.k outside"),
+        (lambda d: d["params"].update(k=9), "params.k outside"),
+        (lambda d: d.update(n=-1), "negative n"),
+        (lambda d: d["stages"][0]["rotations"][0]["i"].__setitem__(0, 10 ** 9), "rotation index out of range"),
+        (lambda d: d["stages"][0]["rotations"][0]["i"].__setitem__(1, -3), "rotation index out of range"),
+        (lambda d: d["stages"][0]["partition"][0].__setitem__(0, 1 << 40), "partition member out of range"),
+        (lambda d: d["stages"][0]["eliminated"][0].update(i=-1), "eliminated index out of range"),
+        (lambda d: d["core"]["indices"].__setitem__(0, 1 << 30), "core index out of range"),
+        (lambda d: d["diagonal"][0].update(i=1 << 30), "diagonal index out of range"),
     ]:
         d = json.loads(json.dumps(doc))
         mutate(d)

@@ -24,7 +24,7 @@ def test_restatement_matches_reference(name):
 
 @needs_ref
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["rmat14_m32", "c1_dense1024"])
+@pytest.mark.parametrize("name", ["rmat14_m32", "c1_dense1024", "c2_rmat16"])
 def test_restatement_matches_reference_large(name):
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("ref", inp, params, part), oracles.factorize("oracle", inp, params, part))
