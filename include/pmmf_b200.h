@@ -151,6 +151,26 @@ int pmmf_b200_result_load(const char* path, void** out, char* err, size_t errlen
 /* MmfFactorization::params (factorizer.hpp:117). */
 int pmmf_b200_result_params(void* h, pmmf_b200_params* out);
 
+/* ---- building a result handle from an existing MmfFactorization ------
+ * (the data of factorizer.hpp:56-118 in the accessors' flat layout), so
+ * that a factorization made elsewhere (the reference's pmmf::factorize, a
+ * file) can drive pmmf_b200_operator_create: the counterpart of
+ * MmfOperator(shared_ptr<const MmfFactorization>, zero_threshold)
+ * (transform_ops.hpp:32-41).  Create, add every stage in order, set the
+ * core; the handle is validated (PMMF_DATA on an index outside [0, n), a
+ * rotation order other than params->k, k outside [2, 8], inconsistent
+ * offsets) when the core is set.  Free with pmmf_b200_result_free. */
+int pmmf_b200_result_create(int64_t n, const pmmf_b200_params* params, double residual_sq, void** out, char* err,
+                            size_t errlen);
+int pmmf_b200_result_add_stage(void* h, int64_t n_clusters, const int64_t* cluster_offsets, const int64_t* members,
+                               int64_t n_rotations, const int64_t* rot_indices, const double* rot_matrices,
+                               int64_t n_eliminated, const int64_t* elim_index, const double* elim_diagonal,
+                               const double* elim_off_mass_sq, int64_t n_bypassed, const int64_t* bypassed,
+                               char* err, size_t errlen);
+int pmmf_b200_result_set_core(void* h, int64_t g, const int64_t* core_indices, const double* core,
+                              int64_t n_diagonal, const int64_t* diag_index, const double* diag_value,
+                              const int64_t* active_history, int64_t n_history, char* err, size_t errlen);
+
 /* ---- multi-GPU: the clusters of every stage sharded over ranks -------
  * (replaces the reference's fork-join thread pool over
  * the clusters of a stage, parallel.hpp:25-71 as used at

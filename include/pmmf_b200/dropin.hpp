@@ -8,8 +8,14 @@
 //
 //   pmmf::MmfFactorization f = pmmf_b200::factorize(a, params, &stats);
 //       // replaces pmmf::factorize (factorizer.hpp:397-398)
-//   pmmf_b200::GpuOperator op(f);      // replaces pmmf::MmfOperator (transform_ops.hpp:30-41)
+//   auto fp = std::make_shared<const pmmf::MmfFactorization>(std::move(f));
+//   pmmf_b200::GpuOperator op(fp);     // replaces pmmf::MmfOperator (transform_ops.hpp:30-41)
 //   op.apply(pmmf::MmfOperator::Mode::inv_sqrt, in, out);
+//
+// GpuOperator wraps any MmfFactorization (from pmmf_b200::factorize, the
+// reference's pmmf::factorize or pmmf::load_factorization) without
+// refactorizing, exactly as MmfOperator(shared_ptr<const MmfFactorization>,
+// zero_threshold) does.
 //
 // Errors are rethrown as the reference's exception types.
 #pragma once
@@ -176,17 +182,90 @@ inline pmmf::MmfFactorization factorize(const pmmf::BlockedSparseMatrix& input, 
   return materialize(r.h, params, stats_out);
 }
 
+// The reverse of materialize: a result handle holding an existing
+// MmfFactorization (pmmf_b200_result_create / _add_stage / _set_core).
+// Throws DataError when the factorization mixes rotation orders (the device
+// operator keeps one k per factorization) or holds out-of-range indices.
+inline void* result_from(const pmmf::MmfFactorization& f) {
+  char err[4096] = {0};
+  const int64_t k = f.params.k;
+  for (const pmmf::Stage& st : f.stages)
+    for (const pmmf::Rotation& rot : st.rotations)
+      if (static_cast<int64_t>(rot.indices.size()) != k)
+        throw pmmf::DataError("GpuOperator: rotation order differs from params.k");
+  const pmmf_b200_params p = to_params(f.params);
+  ResultHandle r;
+  rethrow(pmmf_b200_result_create(f.n, &p, f.residual_sq, &r.h, err, sizeof(err)), err);
+  for (const pmmf::Stage& st : f.stages) {
+    std::vector<int64_t> off(1, 0), mem, ri, ei, by(st.bypassed.begin(), st.bypassed.end());
+    std::vector<double> rq, ed, em;
+    const pmmf::Partition& part = *st.partition;
+    for (pmmf::index_t u = 0; u < part.num_clusters(); ++u) {
+      auto cl = part.cluster(u);
+      mem.insert(mem.end(), cl.begin(), cl.end());
+      off.push_back(static_cast<int64_t>(mem.size()));
+    }
+    for (const pmmf::Rotation& rot : st.rotations) {
+      ri.insert(ri.end(), rot.indices.begin(), rot.indices.end());
+      for (int64_t a = 0; a < k; ++a)
+        for (int64_t b = 0; b < k; ++b) rq.push_back(rot.matrix(a, b));
+    }
+    for (const pmmf::Elimination& e : st.eliminated) {
+      ei.push_back(e.index);
+      ed.push_back(e.diagonal);
+      em.push_back(e.off_mass_sq);
+    }
+    rethrow(pmmf_b200_result_add_stage(r.h, static_cast<int64_t>(off.size()) - 1, off.data(), mem.data(),
+                                       static_cast<int64_t>(st.rotations.size()), ri.data(), rq.data(),
+                                       static_cast<int64_t>(ei.size()), ei.data(), ed.data(), em.data(),
+                                       static_cast<int64_t>(by.size()), by.data(), err, sizeof(err)),
+            err);
+  }
+  const int64_t g = static_cast<int64_t>(f.h.core_indices.size());
+  std::vector<int64_t> ci(f.h.core_indices.begin(), f.h.core_indices.end()), di;
+  std::vector<double> core, dv;
+  for (int64_t a = 0; a < g; ++a)
+    for (int64_t b = 0; b < g; ++b) core.push_back(f.h.core(a, b));
+  for (const auto& [i, d] : f.h.diagonal) {
+    di.push_back(i);
+    dv.push_back(d);
+  }
+  std::vector<int64_t> hist(f.active_history.begin(), f.active_history.end());
+  rethrow(pmmf_b200_result_set_core(r.h, g, ci.data(), core.data(), static_cast<int64_t>(di.size()), di.data(),
+                                    dv.data(), hist.data(), static_cast<int64_t>(hist.size()), err, sizeof(err)),
+          err);
+  void* h = r.h;
+  r.h = nullptr;
+  return h;
+}
+
 // Drop-in for pmmf::MmfOperator (transform_ops.hpp:30-137) on the GPU.
 class GpuOperator {
  public:
+  // MmfOperator(shared_ptr<const MmfFactorization>, zero_threshold)
+  // (transform_ops.hpp:34-41): the core eigensystem and the rotation stream
+  // go to the calling thread's current CUDA device; the factorization is
+  // kept for factorization().
+  explicit GpuOperator(std::shared_ptr<const pmmf::MmfFactorization> f, double zero_threshold = 1e-12)
+      : f_(std::move(f)) {
+    if (!f_) throw std::invalid_argument("GpuOperator: null factorization");
+    ResultHandle r;
+    r.h = result_from(*f_);
+    n_ = f_->n;
+    char err[4096] = {0};
+    rethrow(pmmf_b200_operator_create(r.h, zero_threshold, &op_, err, sizeof(err)), err);
+  }
+  // Convenience: factorize on the GPU, then wrap (one factorization).
   explicit GpuOperator(const pmmf::BlockedSparseMatrix& input, const pmmf::FactorizeParams& params,
                        double zero_threshold = 1e-12, int device = 0) {
     ResultHandle r;
     r.h = factorize_handle(input, params, device);
+    f_ = std::make_shared<const pmmf::MmfFactorization>(materialize(r.h, params, nullptr));
     n_ = input.dim();
     char err[4096] = {0};
     rethrow(pmmf_b200_operator_create(r.h, zero_threshold, &op_, err, sizeof(err)), err);
   }
+  const pmmf::MmfFactorization& factorization() const { return *f_; }
   GpuOperator(const GpuOperator&) = delete;
   GpuOperator& operator=(const GpuOperator&) = delete;
   ~GpuOperator() {
@@ -207,6 +286,7 @@ class GpuOperator {
   }
 
  private:
+  std::shared_ptr<const pmmf::MmfFactorization> f_;
   void* op_ = nullptr;
   pmmf::index_t n_ = 0;
 };

@@ -51,15 +51,37 @@ int main(int argc, char** argv) {
   check(ref.active_history == gpu.active_history, "active_history");
   check(s_ref.stages.size() == s_gpu.stages.size(), "stats stages");
   // operator
-  pmmf::MmfOperator op_ref(std::make_shared<const pmmf::MmfFactorization>(ref));
+  auto ref_ptr = std::make_shared<const pmmf::MmfFactorization>(ref);
+  pmmf::MmfOperator op_ref(ref_ptr);
   pmmf_b200::GpuOperator op_gpu(a, p);
-  std::vector<double> v(static_cast<size_t>(a.dim())), o1(v.size()), o2(v.size());
+  // the reference's own factorization wrapped on the GPU (no refactorization)
+  pmmf_b200::GpuOperator op_wrap(ref_ptr);
+  check(&op_wrap.factorization() == ref_ptr.get(), "factorization() identity");
+  check(op_gpu.factorization().residual_sq == ref.residual_sq, "factorization() of the GPU operator");
+  check(op_wrap.inv_sqrt_zeroed_negatives() == op_ref.inv_sqrt_zeroed_negatives(), "zeroed negatives");
+  std::vector<double> v(static_cast<size_t>(a.dim())), o1(v.size()), o2(v.size()), o3(v.size());
   for (size_t i = 0; i < v.size(); ++i) v[i] = std::sin(0.37 * static_cast<double>(i) + 1.0);
   for (auto mode : {pmmf::MmfOperator::Mode::forward, pmmf::MmfOperator::Mode::inverse,
                     pmmf::MmfOperator::Mode::inv_sqrt}) {
     op_ref.apply(mode, v, o1);
     op_gpu.apply(mode, v, o2);
+    op_wrap.apply(mode, v, o3);
     check(o1 == o2, "operator apply");
+    check(o1 == o3, "wrapped operator apply");
+  }
+  // a corrupt factorization is rejected as DataError, not a device fault
+  {
+    pmmf::MmfFactorization corrupt = ref;
+    if (!corrupt.stages.empty() && !corrupt.stages[0].rotations.empty()) {
+      corrupt.stages[0].rotations[0].indices[0] = corrupt.n + 5;
+      bool threw = false;
+      try {
+        pmmf_b200::GpuOperator op_bad(std::make_shared<const pmmf::MmfFactorization>(corrupt));
+      } catch (const pmmf::DataError&) {
+        threw = true;
+      }
+      check(threw, "out-of-range rotation index rejected");
+    }
   }
   std::printf("%s: %zu stages, %zu rotations in stage 1\n", bad ? "FAIL" : "PASS", gpu.stages.size(),
               gpu.stages.empty() ? size_t{0} : gpu.stages[0].rotations.size());

@@ -5,10 +5,12 @@ from .api import (  # noqa: F401
     ClusterParams,
     FactorizeParams,
     MmfFactorization,
+    MmfOperator,
     Partition,
     factorize,
     kernel_launches,
     library,
+    result_handle_from,
     workload_aniso_grid,
     workload_dense_spd,
     workload_rbf,

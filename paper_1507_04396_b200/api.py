@@ -66,6 +66,14 @@ def library() -> abi.FlatAbi:
                                                    ctypes.POINTER(ctypes.c_double)] + E
         L.pmmf_b200_shard_ranges.restype = ctypes.c_int
         L.pmmf_b200_shard_ranges.argtypes = [ctypes.c_int64, V, V, ctypes.c_int32, V]
+        L.pmmf_b200_result_create.restype = ctypes.c_int
+        L.pmmf_b200_result_create.argtypes = [ctypes.c_int64, ctypes.POINTER(abi.Params), ctypes.c_double,
+                                              ctypes.POINTER(V)] + E
+        L.pmmf_b200_result_add_stage.restype = ctypes.c_int
+        L.pmmf_b200_result_add_stage.argtypes = [V, ctypes.c_int64, V, V, ctypes.c_int64, V, V, ctypes.c_int64, V, V, V,
+                                                 ctypes.c_int64, V] + E
+        L.pmmf_b200_result_set_core.restype = ctypes.c_int
+        L.pmmf_b200_result_set_core.argtypes = [V, ctypes.c_int64, V, V, ctypes.c_int64, V, V, V, ctypes.c_int64] + E
     return _ABI
 
 
@@ -354,6 +362,122 @@ def load_factorization(path: str) -> MmfFactorization:
                                                        d_max=p.d_max, bypass_enabled=bool(p.bypass_enabled),
                                                        seed=p.cluster_seed))
     return out
+
+
+def result_handle_from(f: abi.FlatFactorization, params: Optional[FactorizeParams] = None) -> ctypes.c_void_p:
+    """A result handle holding an existing factorization (this library's, the
+    reference's or a loaded one), for MmfOperator without refactorizing
+    (pmmf_b200_result_create / _add_stage / _set_core; PMMF_DATA on
+    out-of-range indices).  The caller frees it with library().result_free."""
+    lib = library()
+    L = lib.lib
+    err = lib.errbuf()
+    p = params or getattr(f, "params", None) or FactorizeParams(k=int(f.k))
+    p = p.to_c() if hasattr(p, "to_c") else p
+    p.k = int(f.k)
+    h = ctypes.c_void_p()
+    abi.raise_for(L.pmmf_b200_result_create(int(f.n), ctypes.byref(p), float(f.residual_sq), ctypes.byref(h), err,
+                                            len(err)), err)
+    keep = []
+
+    def arr(x, dt):
+        a = np.ascontiguousarray(x, dt)
+        if a.size == 0:
+            a = np.zeros(1, dt)
+        keep.append(a)
+        return a.ctypes.data
+
+    try:
+        for st in f.stages:
+            nc = len(st.cluster_offsets) - 1
+            abi.raise_for(L.pmmf_b200_result_add_stage(
+                h, nc, arr(st.cluster_offsets, np.int64), arr(st.members, np.int64), len(st.rot_indices),
+                arr(st.rot_indices, np.int64), arr(st.rot_matrices, np.float64), len(st.elim_index),
+                arr(st.elim_index, np.int64), arr(st.elim_diagonal, np.float64), arr(st.elim_off_mass_sq, np.float64),
+                len(st.bypassed), arr(st.bypassed, np.int64), err, len(err)), err)
+        g = len(f.core_indices)
+        abi.raise_for(L.pmmf_b200_result_set_core(
+            h, g, arr(f.core_indices, np.int64), arr(f.core, np.float64), len(f.diag_index),
+            arr(f.diag_index, np.int64), arr(f.diag_value, np.float64), arr(f.active_history, np.int64),
+            len(f.active_history), err, len(err)), err)
+    except Exception:
+        lib.result_free(h)
+        raise
+    return h
+
+
+class MmfOperator:
+    """pmmf::MmfOperator (transform_ops.hpp:30-137) on the GPU: wraps a
+    factorization (an MmfFactorization / FlatFactorization, or a raw result
+    handle) without refactorizing; apply(mode, x) computes Q^T H^(mode) Q x.
+    x: one vector (n,) or a batch (b, n), as numpy (host) or a contiguous
+    float64 CUDA tensor (device); the result has x's type and shape."""
+
+    class Mode:
+        forward, inverse, inv_sqrt = 0, 1, 2
+
+    def __init__(self, f, zero_threshold: float = 1e-12):
+        lib = library()
+        self._f = f if isinstance(f, abi.FlatFactorization) else None
+        own = not isinstance(f, ctypes.c_void_p)
+        h = result_handle_from(f) if own else f
+        self._op = ctypes.c_void_p()
+        err = lib.errbuf()
+        try:
+            abi.raise_for(lib.operator_create(h, float(zero_threshold), ctypes.byref(self._op), err, len(err)), err)
+            s = abi.Summary()
+            lib.result_summary(h, ctypes.byref(s))
+            self._n = int(s.n)
+        finally:
+            if own:
+                lib.result_free(h)
+
+    def dim(self) -> int:
+        return self._n
+
+    def factorization(self):
+        if self._f is None:
+            raise RuntimeError("MmfOperator was built from a raw handle")
+        return self._f
+
+    def inv_sqrt_zeroed_negatives(self) -> int:
+        v = ctypes.c_int64()
+        library().operator_zeroed_negatives(self._op, ctypes.byref(v))
+        return int(v.value)
+
+    def apply(self, mode: int, x):
+        lib = library()
+        err = lib.errbuf()
+        if getattr(x, "is_cuda", False):
+            import torch
+
+            if x.dtype != torch.float64 or not x.is_contiguous() or x.shape[-1] != self._n:
+                raise ValueError("MmfOperator.apply: expected a contiguous float64 (.., n) CUDA tensor")
+            out = torch.empty_like(x)
+            torch.cuda.current_stream(x.device).synchronize()
+            nrhs = 1 if x.dim() == 1 else int(x.shape[0])
+            abi.raise_for(lib.operator_apply(self._op, int(mode), nrhs, x.data_ptr(), out.data_ptr(), 1, err,
+                                             len(err)), err)
+            return out
+        a = np.ascontiguousarray(x, np.float64)
+        if a.shape[-1] != self._n or a.ndim > 2:
+            raise ValueError("MmfOperator::apply: dimension mismatch")
+        out = np.zeros_like(a)
+        nrhs = 1 if a.ndim == 1 else a.shape[0]
+        abi.raise_for(lib.operator_apply(self._op, int(mode), nrhs, a.ctypes.data, out.ctypes.data, 0, err,
+                                         len(err)), err)
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_op", None):
+            library().operator_free(self._op)
+            self._op = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def residual_frobenius(handle: ctypes.c_void_p, matrix: "BlockedSparseMatrix", method: str = "dense",

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -123,6 +124,64 @@ int pmmf_b200_result_params(void* h, pmmf_b200_params* out) {
   if (!h || !out) return PMMF_INVALID_ARGUMENT;
   *out = static_cast<Result*>(h)->params;
   return PMMF_OK;
+}
+
+int pmmf_b200_result_create(int64_t n, const pmmf_b200_params* p, double residual_sq, void** out, char* err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!p || !out) fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_result_create: null argument");
+    if (n < 0) fail(PMMF_DATA, "factorization: negative n");
+    if (p->k < 2 || p->k > kMaxK) fail(PMMF_DATA, "factorization: params.k outside [2, 8]");
+    auto r = std::make_unique<Result>();
+    r->n = n;
+    r->k = p->k;
+    r->params = *p;
+    r->residual_sq = residual_sq;
+    r->trivial = true;
+    *out = r.release();
+  });
+}
+
+int pmmf_b200_result_add_stage(void* h, int64_t n_clusters, const int64_t* offs, const int64_t* mem, int64_t nr,
+                               const int64_t* ri, const double* rq, int64_t ne, const int64_t* ei, const double* ed,
+                               const double* em, int64_t nb, const int64_t* by, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || !offs || n_clusters < 0 || nr < 0 || ne < 0 || nb < 0)
+      fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_result_add_stage: bad argument");
+    auto* r = static_cast<Result*>(h);
+    const int64_t k = r->k;
+    const int64_t np = offs[n_clusters];
+    if ((np && !mem) || (nr && (!ri || !rq)) || (ne && (!ei || !ed || !em)) || (nb && !by))
+      fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_result_add_stage: null array");
+    Result::Stage st;
+    st.off.assign(offs, offs + n_clusters + 1);
+    if (np < 0) fail(PMMF_DATA, "factorization: inconsistent partition offsets");
+    st.members.assign(mem, mem + np);
+    st.rot_idx.assign(ri, ri + nr * k);
+    st.rot_q.assign(rq, rq + nr * k * k);
+    st.elim_idx.assign(ei, ei + ne);
+    st.elim_diag.assign(ed, ed + ne);
+    st.elim_mass.assign(em, em + ne);
+    st.bypassed.assign(by, by + nb);
+    r->stages.push_back(std::move(st));
+    r->trivial = false;
+  });
+}
+
+int pmmf_b200_result_set_core(void* h, int64_t g, const int64_t* ci, const double* core, int64_t nd,
+                              const int64_t* di, const double* dv, const int64_t* hist, int64_t nh, char* err,
+                              size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!h || g < 0 || nd < 0 || nh < 0 || (g && (!ci || !core)) || (nd && (!di || !dv)) || (nh && !hist))
+      fail(PMMF_INVALID_ARGUMENT, "pmmf_b200_result_set_core: bad argument");
+    auto* r = static_cast<Result*>(h);
+    r->core_idx.assign(ci, ci + g);
+    r->core.assign(core, core + g * g);
+    r->diag.clear();
+    for (int64_t i = 0; i < nd; ++i) r->diag.emplace_back(di[i], dv[i]);
+    r->hist.assign(hist, hist + nh);
+    validate_result(*r);
+  });
 }
 
 int pmmf_b200_result_summary(void* h, pmmf_b200_summary* o) {

@@ -395,7 +395,7 @@ std::string factorization_to_json(const Result& r) {  // serialize.hpp:61-110
 // values (operator.cu): reject anything out of range as PMMF_DATA instead
 // of corrupting memory.  k bounds the operator's per-rotation registers
 // (kMaxK = 8, factorizer.hpp:44-46 allows k >= 2).
-static void validate(const Result& r) {
+void validate_result(const Result& r) {
   auto bad = [](const char* what) { fail(PMMF_DATA, std::string("factorization file: ") + what); };
   if (r.n < 0) bad("negative n");
   if (r.k < 2 || r.k > 8) bad("params.k outside [2, 8]");
@@ -497,7 +497,7 @@ std::unique_ptr<Result> factorization_from_json(const char* text, size_t len) { 
   }
   for (const JVal& jd : j.at("diagonal").arr()) r->diag.emplace_back(jd.at("i").as_int(), jd.at("d").as_double());
   r->trivial = r->stages.empty();
-  validate(*r);
+  validate_result(*r);
   return r;
 }
 

@@ -39,6 +39,8 @@ std::string factorization_to_json(const Result& r);
 std::unique_ptr<Result> factorization_from_json(const char* text, size_t len);
 void save_factorization(const Result& r, const std::string& path);
 std::unique_ptr<Result> load_factorization(const std::string& path);
+// Range checks on a result built outside factorize (PMMF_DATA on failure).
+void validate_result(const Result& r);
 
 struct Comm;
 // comm == nullptr: one GPU (shard.cuh for the sharded decomposition).
