@@ -40,57 +40,50 @@ constexpr int kThreads = 256;
 constexpr size_t kSmemBudget = 200 * 1024;
 constexpr size_t kSmemTwoPerSm = 112 * 1024;
 
-// ------------------------------------------------------------- host Jacobi
-// jacobi_eigensystem (dense.hpp:144-199) for the g x g core, row-major.
-void jacobi_eig(std::vector<double> a, int64_t n, std::vector<double>& values, std::vector<double>& vectors) {
-  std::vector<double> q(static_cast<size_t>(n * n), 0.0);
-  for (int64_t i = 0; i < n; ++i) q[i * n + i] = 1.0;
-  double fro = 0.0;
-  for (double v : a) fro += v * v;
-  const double scale = std::sqrt(fro);
-  if (!(scale == 0.0 || n < 2)) {
-    const double stop = 1e-15 * scale;
-    for (int sweep = 0; sweep < 64; ++sweep) {
-      double off = 0.0;
-      for (int64_t i = 0; i < n; ++i)
-        for (int64_t j = i + 1; j < n; ++j) off += 2.0 * a[i * n + j] * a[i * n + j];
-      if (std::sqrt(off) <= stop) break;
-      for (int64_t p = 0; p < n; ++p)
-        for (int64_t r = p + 1; r < n; ++r) {
-          if (a[p * n + r] == 0.0) continue;
-          double c = 1.0, s = 0.0;
-          {
-            const double gpp = a[p * n + p], grr = a[r * n + r], gpr = a[p * n + r];
-            const double tau = (grr - gpp) / (2.0 * gpr);
-            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (std::abs(tau) + std::sqrt(1.0 + tau * tau));
-            c = 1.0 / std::sqrt(1.0 + t * t);
-            s = t * c;
-          }
-          for (int64_t t = 0; t < n; ++t) {
-            const double ap = a[p * n + t], ar = a[r * n + t];
-            a[p * n + t] = c * ap - s * ar;
-            a[r * n + t] = s * ap + c * ar;
-          }
-          for (int64_t t = 0; t < n; ++t) {
-            const double ap = a[t * n + p], ar = a[t * n + r];
-            a[t * n + p] = c * ap - s * ar;
-            a[t * n + r] = s * ap + c * ar;
-          }
-          a[p * n + r] = 0.0;
-          a[r * n + p] = 0.0;
-          for (int64_t t = 0; t < n; ++t) {
-            const double qp = q[p * n + t], qr = q[r * n + t];
-            q[p * n + t] = c * qp - s * qr;
-            q[r * n + t] = s * qp + c * qr;
-          }
-        }
-    }
+// ------------------------------------------------- core eigensystem (device)
+// jacobi_eigensystem (dense.hpp:191-199, called by MmfOperator's constructor,
+// transform_ops.hpp:34-41) on the g x g core: one CTA runs the cyclic
+// Jacobi of rotation.cuh with the per-pair row / column updates strided over
+// its threads (CtaLoop); the Frobenius and off-diagonal sums run on thread 0
+// in the reference's order, so values and vectors are bit-identical to the
+// reference's sequential sweeps.  Matrices live in shared memory up to
+// g = 48, else in global scratch.
+struct CtaLoop {
+  double* slot;  // one shared double for broadcasts
+  template <class F>
+  __device__ void each(int n, F&& f) const {
+    for (int t = threadIdx.x; t < n; t += blockDim.x) f(t);
   }
-  values.resize(static_cast<size_t>(n));
-  for (int64_t i = 0; i < n; ++i) values[i] = a[i * n + i];
-  vectors.assign(static_cast<size_t>(n * n), 0.0);  // eigenvectors as columns: vectors(a,e) = q(e,a)
-  for (int64_t i = 0; i < n; ++i)
-    for (int64_t j = 0; j < n; ++j) vectors[i * n + j] = q[j * n + i];
+  __device__ void sync() const { __syncthreads(); }
+  __device__ bool leader() const { return threadIdx.x == 0; }
+  __device__ double bcast(double v) const {
+    if (threadIdx.x == 0) *slot = v;
+    __syncthreads();
+    const double r = *slot;
+    __syncthreads();
+    return r;
+  }
+};
+
+constexpr int kEigSmemMax = 48;  // two 48 x 48 fp64 tiles = 36 KB of static shared memory
+
+__global__ void k_core_eig(int g, const double* __restrict__ core, double* __restrict__ work_a,
+                           double* __restrict__ work_q, double* __restrict__ values, double* __restrict__ vectors) {
+  __shared__ double slot;
+  __shared__ double sa[kEigSmemMax * kEigSmemMax], sq[kEigSmemMax * kEigSmemMax];
+  const bool small = g <= kEigSmemMax;
+  double* a = small ? sa : work_a;
+  double* q = small ? sq : work_q;
+  for (int x = threadIdx.x; x < g * g; x += blockDim.x) a[x] = core[x];
+  __syncthreads();
+  jacobi_diagonalize_g(RowMajor{a, g}, RowMajor{q, g}, g, CtaLoop{&slot});
+  __syncthreads();
+  for (int i = threadIdx.x; i < g; i += blockDim.x) values[i] = a[static_cast<long long>(i) * g + i];
+  // eigenvectors as columns: vectors(a, e) = q(e, a)
+  for (long long x = threadIdx.x; x < static_cast<long long>(g) * g; x += blockDim.x) {
+    const long long i = x / g, j = x % g;
+    vectors[x] = q[j * g + i];
+  }
 }
 
 double scalar_factor(int mode, double d, double thr) {  // transform_ops.hpp:76-86
@@ -599,10 +592,23 @@ struct Operator {
       PMMF_CUDA(cudaStreamSynchronize(s));
       stages.push_back(std::move(sd));
     }
-    // core eigensystem (transform_ops.hpp:34-41)
+    // core eigensystem (transform_ops.hpp:34-41) on the device
     g = static_cast<int64_t>(f.core_idx.size());
-    std::vector<double> vals, vecs;
-    jacobi_eig(f.core, g, vals, vecs);
+    std::vector<double> vals;
+    if (g > 0) {
+      DBuf<double> dcore(g * g, s), dval(g, s);
+      E.alloc(g * g, s);
+      dcore.upload(f.core);
+      DBuf<double> wa, wq;
+      if (g > kEigSmemMax) {
+        wa.alloc(g * g, s);
+        wq.alloc(g * g, s);
+      }
+      const int threads = g <= 32 ? 32 : (g <= kEigSmemMax ? 64 : 256);
+      PMMF_LAUNCH(k_core_eig, 1, threads, 0, s, static_cast<int>(g), dcore.get(), wa.get(), wq.get(), dval.get(),
+                  E.get());
+      vals = dval.to_host(g);
+    }
     for (double l : vals)
       if (l < -thr) ++neg;
     for (const auto& d : f.diag)
@@ -611,8 +617,6 @@ struct Operator {
       std::vector<int32_t> ci(f.core_idx.begin(), f.core_idx.end());
       core_idx.alloc(g, s);
       core_idx.upload(ci);
-      E.alloc(g * g, s);
-      E.upload(vecs);
       for (int mode = 0; mode < 3; ++mode) {
         std::vector<double> fv(static_cast<size_t>(g));
         for (int64_t e = 0; e < g; ++e) fv[e] = scalar_factor(mode, vals[e], thr);

@@ -31,45 +31,82 @@ PMMF_HDI void jacobi_angle(double gpp, double grr, double gpr, double& c, double
   s = t * c;
 }
 
-// a (n x n, row-major stride kMaxK) is diagonalized in place; q returned.
-PMMF_HDI void jacobi_diagonalize(double (*a)[kMaxK], int n, double (*q)[kMaxK]) {
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) q[i][j] = i == j ? 1.0 : 0.0;
+// Loop policies for the cyclic Jacobi below.  SeqLoop: the calling thread
+// runs every loop (the search kernel's scalar lane, the host).  CtaLoop (see
+// operator.cu): the per-pair row / column updates are independent over t and
+// run strided over a CTA, with barriers between dependent steps; sums whose
+// order matters run on the leader thread and are broadcast.  Every matrix
+// element sees the same operation sequence under both policies.
+struct SeqLoop {
+  template <class F>
+  PMMF_HDI void each(int n, F&& f) const {
+    for (int t = 0; t < n; ++t) f(t);
+  }
+  PMMF_HDI void sync() const {}
+  PMMF_HDI bool leader() const { return true; }
+  PMMF_HDI double bcast(double v) const { return v; }
+};
+
+// Cyclic Jacobi (jacobi_diagonalize, dense.hpp:144-183; rel_tol 1e-15, 64
+// sweeps) on accessors a(i, j), q(i, j): a is diagonalized in place, q
+// receives the rotation (q a q^T diagonal).
+template <class MA, class MQ, class Par>
+PMMF_HDI void jacobi_diagonalize_g(MA a, MQ q, int n, const Par& par) {
+  par.each(n * n, [&](int x) { q(x / n, x % n) = (x / n == x % n) ? 1.0 : 0.0; });
   double fro = 0.0;
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) fro += a[i][j] * a[i][j];
-  const double scale = sqrt(fro);
+  if (par.leader())
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) fro += a(i, j) * a(i, j);
+  const double scale = sqrt(par.bcast(fro));
   if (scale == 0.0 || n < 2) return;
   const double stop = 1e-15 * scale;
   for (int sweep = 0; sweep < 64; ++sweep) {
     double off = 0.0;
-    for (int i = 0; i < n; ++i)
-      for (int j = i + 1; j < n; ++j) off += 2.0 * a[i][j] * a[i][j];
-    if (sqrt(off) <= stop) break;
+    if (par.leader())
+      for (int i = 0; i < n; ++i)
+        for (int j = i + 1; j < n; ++j) off += 2.0 * a(i, j) * a(i, j);
+    if (sqrt(par.bcast(off)) <= stop) break;
     for (int p = 0; p < n; ++p)
       for (int r = p + 1; r < n; ++r) {
-        if (a[p][r] == 0.0) continue;
+        const double apr = a(p, r);
+        if (apr == 0.0) continue;
         double c, s;
-        jacobi_angle(a[p][p], a[r][r], a[p][r], c, s);
-        for (int t = 0; t < n; ++t) {
-          const double ap = a[p][t], ar = a[r][t];
-          a[p][t] = c * ap - s * ar;
-          a[r][t] = s * ap + c * ar;
+        jacobi_angle(a(p, p), a(r, r), apr, c, s);
+        par.sync();  // every thread has read the pivot entries
+        par.each(n, [&](int t) {
+          const double ap = a(p, t), ar = a(r, t);
+          a(p, t) = c * ap - s * ar;
+          a(r, t) = s * ap + c * ar;
+        });
+        par.sync();
+        par.each(n, [&](int t) {
+          const double ap = a(t, p), ar = a(t, r);
+          a(t, p) = c * ap - s * ar;
+          a(t, r) = s * ap + c * ar;
+          const double qp = q(p, t), qr = q(r, t);
+          q(p, t) = c * qp - s * qr;
+          q(r, t) = s * qp + c * qr;
+        });
+        par.sync();
+        if (par.leader()) {
+          a(p, r) = 0.0;
+          a(r, p) = 0.0;
         }
-        for (int t = 0; t < n; ++t) {
-          const double ap = a[t][p], ar = a[t][r];
-          a[t][p] = c * ap - s * ar;
-          a[t][r] = s * ap + c * ar;
-        }
-        a[p][r] = 0.0;
-        a[r][p] = 0.0;
-        for (int t = 0; t < n; ++t) {
-          const double qp = q[p][t], qr = q[r][t];
-          q[p][t] = c * qp - s * qr;
-          q[r][t] = s * qp + c * qr;
-        }
+        par.sync();
       }
   }
+}
+
+// Row-major view with a fixed stride.
+struct RowMajor {
+  double* p;
+  int ld;
+  PMMF_HDI double& operator()(int i, int j) const { return p[static_cast<long long>(i) * ld + j]; }
+};
+
+// a (n x n, row-major stride kMaxK) is diagonalized in place; q returned.
+PMMF_HDI void jacobi_diagonalize(double (*a)[kMaxK], int n, double (*q)[kMaxK]) {
+  jacobi_diagonalize_g(RowMajor{&a[0][0], kMaxK}, RowMajor{&q[0][0], kMaxK}, n, SeqLoop{});
 }
 
 // Returns false when g is not symmetric within 1e-9 * max(1, max|g|)

@@ -92,3 +92,23 @@ def test_operator_device_tensors():
     assert np.array_equal(dev.cpu().numpy(), host)
     with pytest.raises(ValueError):
         op.apply(op.Mode.forward, torch.zeros(3, inp[0], dtype=torch.float32, device="cuda"))
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("core_min", [10, 40, 100, 300])
+def test_core_eigensystem_on_device(core_min):
+    """The core's jacobi_eigensystem (dense.hpp:191-199) runs on the device:
+    shared-memory tiles up to g = 48, global scratch above; the inverse and
+    inv_sqrt applies (which go through the eigenvectors and f(lambda)) equal
+    the reference's bit for bit."""
+    inp, params, part = cases.build("rmat12_m16")
+    params = abi.make_params(m_target=16, seed=42, core_min=core_min)
+    f = oracles.factorize("ref", inp, params, part)
+    assert len(f.core_indices) >= min(core_min, inp[0])
+    op = api.MmfOperator(f)
+    vecs = np.random.default_rng(13).standard_normal((2, inp[0]))
+    for mode in (1, 2):
+        r, rneg = oracles.operator_apply("ref", inp, params, mode, vecs, clusters=part)
+        assert np.array_equal(op.apply(mode, vecs), r), mode
+        assert op.inv_sqrt_zeroed_negatives() == rneg
