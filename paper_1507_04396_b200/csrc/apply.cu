@@ -18,6 +18,7 @@
 // works in its own arena (superseded versions are garbage), and its final
 // columns are copied into a compact Piece, optionally dropping rows that no
 // later consumer reads (lean mode).
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -554,6 +555,358 @@ __global__ void __launch_bounds__(256, K == 2 ? 6 : 2) k_merge_p(PassArgs A, con
   }
 }
 
+// ---- persistent level loop ---------------------------------------------
+// All dependency levels of a batch in ONE cooperative kernel (the per-level
+// chain nparts -> scan -> item map -> count pass -> allocation -> write pass
+// -> commit was ~7 launches per level, ~26 k per factorization on config 4).
+// Per level, three phases separated by grid barriers:
+//   1. partitions per rotation (np) and a block-level scan;
+//   2. global offsets of every rotation's partitions, partition -> rotation
+//      map, per-item chain state reset;
+//   3. merges, one warp per partition (static stride over the items):
+//      * single-partition rotations count, allocate (atomicAdd on the arena
+//        cursor), write and commit their columns back to back;
+//      * multi-partition rotations count their partition, publish it
+//        (decoupled look-back over the rotation's partitions: aggregate, then
+//        inclusive prefix), write at base + prefix, and the last partition to
+//        finish commits.  Partition 0 reserves the rotation's upper bound
+//        (K outputs x sum of input lengths), so no separate count pass or
+//        allocation kernel is needed; the unused tail of a reservation is
+//        garbage that the next compaction drops.
+// A look-back only waits on lower items; items are visited in increasing
+// order by every warp and all warps are co-resident (cooperative launch), so
+// the lowest unfinished item can always proceed.
+// Overflow: an allocation that does not fit marks the level (atomicMin);
+// rotations that committed are flagged `done` and skipped when the host
+// resumes the level after compacting the arena.
+struct LoopArgs {
+  const int32_t* order;  // plan order (level-sorted slots)
+  const i64* lv_lo;      // per level: [lo, hi) into order
+  const i64* lv_hi;
+  int L0, L1;            // levels [L0, L1]
+  const int32_t* ids;
+  const double* qs;
+  i64 col0;
+  i64* off;
+  int32_t* len;
+  int32_t* arow;
+  double* aval;
+  int chunk;
+  unsigned long long* cursor;
+  i64 cap;
+  int32_t* ovf;
+  uint8_t* done;         // per order position
+  int32_t* np;           // per level-rotation
+  int64_t* ioff;         // per level-rotation
+  int32_t* item_rot;     // per item
+  int64_t* bsum;         // per block (+ total)
+  int32_t* status;       // per item: 0 none, 1 aggregate, 2 inclusive, 3 failed
+  int32_t* agg;          // per item x K
+  int32_t* incl;         // per item x K
+  i64* rbase;            // per level-rotation: arena base of a multi-partition rotation
+  int32_t* ndone;        // per level-rotation: finished partitions
+  unsigned long long* in_entries;   // [0] inputs read, [1] outputs written
+  i64 max_rot;
+};
+
+__device__ __forceinline__ int ld_volatile(const int32_t* p) { return *reinterpret_cast<const volatile int32_t*>(p); }
+
+template <int K>
+__device__ void loop_count(const LoopArgs& A, const PassArgs& P, const double (&q)[K][K], const i64 (&beg)[K],
+                           const i64 (&end)[K], int (&kept)[K], bool& dense, int& r0) {
+  const int dl = identical_rows<K>(P, beg, end, r0);
+  dense = dl >= 0;
+  if (dense) {
+#pragma unroll
+    for (int a = 0; a < K; ++a) kept[a] = dl;
+    return;
+  }
+  if constexpr (K == 2) {
+    i64 cb[2] = {beg[0], beg[1]};
+    int u = 0;
+    merge_count2(P, cb, end, u);
+    kept[0] = kept[1] = u;
+  } else {
+    i64 cb[K];
+    i64 dst[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      cb[a] = beg[a];
+      kept[a] = 0;
+      dst[a] = 0;
+    }
+    merge_partition<K, false>(P, q, cb, end, kept, dst);
+  }
+}
+
+template <int K>
+__device__ void loop_write(const PassArgs& P, const double (&q)[K][K], const i64 (&beg)[K], const i64 (&end)[K],
+                           bool dense, int r0, const i64 (&dst)[K]) {
+  if (dense) {
+    write_dense<K>(P, q, beg, static_cast<int>(end[0] - beg[0]), r0, dst);
+    return;
+  }
+  i64 cb[K];
+#pragma unroll
+  for (int a = 0; a < K; ++a) cb[a] = beg[a];
+  if constexpr (K == 2) {
+    int u = 0;
+    merge_write2(P, q, cb, end, u, dst);
+  } else {
+    int kept[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) kept[a] = 0;
+    merge_partition<K, true>(P, q, cb, end, kept, dst);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, K == 2 ? 4 : 1) k_level_loop(LoopArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int64_t s_scan[256 / 32 + 1];
+  __shared__ int64_t s_base;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const i64 gwarp = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const i64 nwarps = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+  PassArgs P{};  // the merge helpers' view of the batch
+  P.ids = A.ids;
+  P.qs = A.qs;
+  P.col0 = A.col0;
+  P.off = A.off;
+  P.len = A.len;
+  P.arow = A.arow;
+  P.aval = A.aval;
+  P.wrow = A.arow;
+  P.wval = A.aval;
+  P.chunk = A.chunk;
+  for (int L = A.L0; L <= A.L1; ++L) {
+    const i64 lo = A.lv_lo[L], nrot = A.lv_hi[L] - lo;
+    if (nrot <= 0) continue;
+    // ---- phase 1: partitions per rotation, block sums over contiguous ranges
+    const i64 per = (nrot + gridDim.x - 1) / gridDim.x;
+    const i64 b0 = blockIdx.x * per, b1 = min(nrot, b0 + per);
+    int64_t mine = 0;
+    unsigned long long ins = 0;
+    for (i64 i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      int npi = 0;
+      if (!A.done[lo + i]) {
+        const int t = A.order[lo + i];
+        int Lmax = 0;
+#pragma unroll
+        for (int b = 0; b < K; ++b) {
+          const int l = A.len[A.ids[static_cast<i64>(t) * K + b] - A.col0];
+          Lmax = max(Lmax, l);
+          ins += static_cast<unsigned long long>(l);
+        }
+        npi = max(1, (Lmax + A.chunk - 1) / A.chunk);
+      }
+      A.np[i] = npi;
+      mine += npi;
+    }
+    for (int o = 16; o; o >>= 1) {
+      mine += __shfl_xor_sync(0xffffffffu, mine, o);
+      ins += __shfl_xor_sync(0xffffffffu, ins, o);
+    }
+    if (lane == 0 && ins) atomicAdd(A.in_entries, ins);
+    if (lane == 0) s_scan[wib] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s_scan[w];
+      A.bsum[blockIdx.x] = t;
+    }
+    grid.sync();
+    // ---- phase 2: offsets, item map, chain-state reset
+    if (threadIdx.x == 0) {
+      int64_t base = 0, all = 0;
+      for (unsigned b = 0; b < gridDim.x; ++b) {
+        const int64_t v = A.bsum[b];
+        if (b < blockIdx.x) base += v;
+        all += v;
+      }
+      s_base = base;
+      if (blockIdx.x == 0) A.bsum[gridDim.x] = all;
+    }
+    __syncthreads();
+    {
+      // sequential exclusive scan of this block's range, tile by tile
+      int64_t run = s_base;
+      for (i64 t0 = b0; t0 < b1; t0 += blockDim.x) {
+        const i64 i = t0 + threadIdx.x;
+        const int v = i < b1 ? A.np[i] : 0;
+        // block-wide exclusive scan of v
+        int64_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        __syncthreads();
+        if (lane == 31) s_scan[wib] = x;
+        __syncthreads();
+        int64_t wpre = 0, tile = 0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+          if (w < wib) wpre += s_scan[w];
+          tile += s_scan[w];
+        }
+        if (i < b1) {
+          const int64_t o = run + wpre + x - v;
+          A.ioff[i] = o;
+          for (int p = 0; p < v; ++p) {
+            A.item_rot[o + p] = static_cast<int32_t>(i);
+            A.status[o + p] = 0;
+          }
+          A.ndone[i] = 0;
+        }
+        run += tile;
+      }
+    }
+    grid.sync();
+    // ---- phase 3: merges
+    const i64 nitems = A.bsum[gridDim.x];
+    for (i64 item = gwarp; item < nitems; item += nwarps) {
+      const i64 ri = A.item_rot[item];
+      const i64 i0 = A.ioff[ri];
+      const i64 p = item - i0;
+      const int np = A.np[ri];
+      const int t = A.order[lo + ri];
+      int id[K];
+      double q[K][K];
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        id[b] = A.ids[static_cast<i64>(t) * K + b] - static_cast<int>(A.col0);
+#pragma unroll
+        for (int a = 0; a < K; ++a) q[b][a] = A.qs[(static_cast<i64>(t) * K + b) * K + a];
+      }
+      i64 beg[K], end[K];
+      partition_range<K>(P, t, p, np, id, beg, end);
+      int kept[K];
+      bool dense = false;
+      int r0 = 0;
+      loop_count<K>(A, P, q, beg, end, kept, dense, r0);
+      if (np == 1) {
+        int tot = 0;
+#pragma unroll
+        for (int a = 0; a < K; ++a) tot += kept[a];
+        unsigned long long bb = 0;
+        if (lane == 0) bb = atomicAdd(A.cursor, static_cast<unsigned long long>(tot));
+        bb = __shfl_sync(0xffffffffu, bb, 0);
+        if (static_cast<i64>(bb) + tot > A.cap) {
+          if (lane == 0) atomicMin(A.ovf, L);
+          continue;
+        }
+        i64 dst[K];
+        i64 c = static_cast<i64>(bb);
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+          dst[a] = c;
+          c += kept[a];
+        }
+        loop_write<K>(P, q, beg, end, dense, r0, dst);
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int a = 0; a < K; ++a) {
+            A.off[id[a]] = dst[a];
+            A.len[id[a]] = kept[a];
+          }
+          A.done[lo + ri] = 1;
+          atomicAdd(A.in_entries + 1, static_cast<unsigned long long>(tot));
+        }
+        continue;
+      }
+      // multi-partition: decoupled look-back over the rotation's partitions
+      i64 ub = 0;  // per-output upper bound: sum of the full input lengths
+#pragma unroll
+      for (int b = 0; b < K; ++b) ub += A.len[id[b]];
+      int prefix[K];
+#pragma unroll
+      for (int a = 0; a < K; ++a) prefix[a] = 0;
+      bool failed = false;
+      if (lane == 0) {
+        if (p == 0) {
+          const unsigned long long bb = atomicAdd(A.cursor, static_cast<unsigned long long>(K * ub));
+          if (static_cast<i64>(bb) + K * ub > A.cap) {
+            atomicMin(A.ovf, L);
+            failed = true;
+            __threadfence();
+            atomicExch(A.status + item, 3);
+          } else {
+            A.rbase[ri] = static_cast<i64>(bb);
+#pragma unroll
+            for (int a = 0; a < K; ++a) A.incl[item * K + a] = kept[a];
+            __threadfence();
+            atomicExch(A.status + item, 2);
+          }
+        } else {
+#pragma unroll
+          for (int a = 0; a < K; ++a) A.agg[item * K + a] = kept[a];
+          __threadfence();
+          atomicExch(A.status + item, 1);
+          i64 j = item - 1;
+          for (;;) {
+            int st = ld_volatile(A.status + j);
+            while (st == 0) {
+              __nanosleep(64);
+              st = ld_volatile(A.status + j);
+            }
+            __threadfence();
+            if (st == 3) {
+              failed = true;
+              break;
+            }
+            const int32_t* src = st == 2 ? A.incl : A.agg;
+#pragma unroll
+            for (int a = 0; a < K; ++a) prefix[a] += ld_volatile(src + j * K + a);
+            if (st == 2) break;
+            --j;
+          }
+          if (failed) {
+            atomicExch(A.status + item, 3);
+          } else {
+#pragma unroll
+            for (int a = 0; a < K; ++a) A.incl[item * K + a] = prefix[a] + kept[a];
+            __threadfence();
+            atomicExch(A.status + item, 2);
+          }
+        }
+      }
+      failed = __shfl_sync(0xffffffffu, failed, 0);
+      if (failed) continue;
+#pragma unroll
+      for (int a = 0; a < K; ++a) prefix[a] = __shfl_sync(0xffffffffu, prefix[a], 0);
+      __threadfence();
+      const i64 base = *reinterpret_cast<volatile const i64*>(A.rbase + ri);
+      i64 dst[K];
+#pragma unroll
+      for (int a = 0; a < K; ++a) dst[a] = base + a * ub + prefix[a];
+      loop_write<K>(P, q, beg, end, dense, r0, dst);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        const int fin = atomicAdd(A.ndone + ri, 1);
+        if (fin == np - 1) {  // every partition written: commit the rotation
+          __threadfence();
+          const i64 last = i0 + np - 1;
+          int total = 0;
+#pragma unroll
+          for (int a = 0; a < K; ++a) {
+            const int la = ld_volatile(A.incl + last * K + a);
+            A.off[id[a]] = base + a * ub;
+            A.len[id[a]] = la;
+            total += la;
+          }
+          A.done[lo + ri] = 1;
+          atomicAdd(A.in_entries + 1, static_cast<unsigned long long>(total));
+        }
+      }
+    }
+    grid.sync();
+    if (ld_volatile(A.ovf) != INT_MAX) return;  // the host compacts and resumes
+  }
+}
+
 __global__ void k_len64(i64 N, const int32_t* __restrict__ len, i64* __restrict__ out) {
   const i64 j = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (j < N) out[j] = len[j];
@@ -868,6 +1221,41 @@ int persistent_blocks() {
   return nb;
 }
 
+inline bool level_loop_enabled() {
+  const char* e = std::getenv("PMMF_B200_LEVEL_LOOP");
+  return !(e && e[0] == '0');
+}
+
+// Co-resident grid of the level loop (cooperative launch).
+template <int K>
+int loop_blocks() {
+  static const int nb = [] {
+    int per_sm = 0, dev = 0, sms = 148;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_level_loop<K>, kThreads, 0) != cudaSuccess)
+      per_sm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    (void)cudaGetLastError();
+    return std::max(1, per_sm) * sms;
+  }();
+  return nb;
+}
+
+struct LoopScratch {
+  i64 max_rot = 0, max_items = 0;
+  DBuf<i64> lv_lo, lv_hi, rbase;
+  DBuf<int32_t> np, item_rot, status, agg, incl, ndone;
+  DBuf<int64_t> ioff, bsum;
+  DBuf<uint8_t> done;
+};
+
+template <int K>
+void launch_level_loop(LoopArgs A, cudaStream_t s) {
+  void* args[] = {&A};
+  PMMF_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_level_loop<K>), dim3(loop_blocks<K>()),
+                                        dim3(kThreads), args, 0, s));
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+}
+
 // One dependency level of a batch, entirely on the device (no host sync).
 template <int K>
 void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* rots, i64 nrot, int level,
@@ -1155,7 +1543,8 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
                                               static_cast<int64_t>(max_rot), s));
       S.scan_tmp.alloc(static_cast<i64>(S.scan_bytes) + 1, s);
     }
-    size_items();
+    const bool loop = level_loop_enabled();
+    if (!loop) size_items();
     auto set_scalar = [&](auto& buf, auto v) {
       PMMF_CUDA(cudaMemcpyAsync(buf.get(), &v, sizeof(v), cudaMemcpyHostToDevice, s));
       PMMF_CUDA(cudaStreamSynchronize(s));
@@ -1173,20 +1562,113 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       t0 = now;
       return ms;
     };
+    // persistent level loop (default) or the per-level launch chain
+    LoopScratch X;
+    int loop_grid = 0;
+    if (loop) {
+      switch (K) {
+        case 2: loop_grid = loop_blocks<2>(); break;
+        case 3: loop_grid = loop_blocks<3>(); break;
+        case 4: loop_grid = loop_blocks<4>(); break;
+        case 5: loop_grid = loop_blocks<5>(); break;
+        case 6: loop_grid = loop_blocks<6>(); break;
+        case 7: loop_grid = loop_blocks<7>(); break;
+        case 8: loop_grid = loop_blocks<8>(); break;
+        default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
+      }
+      std::vector<i64> hlo(static_cast<size_t>(plan.max_level) + 1, 0), hhi(hlo.size(), 0);
+      for (int L = 1; L <= plan.max_level; ++L) {
+        hlo[L] = range[L].first;
+        hhi[L] = range[L].second;
+        S.rot_bytes += static_cast<double>(range[L].second - range[L].first) * (8.0 * K * K + 4.0 * K);
+      }
+      X.lv_lo.alloc(static_cast<i64>(hlo.size()), s);
+      X.lv_hi.alloc(static_cast<i64>(hhi.size()), s);
+      X.lv_lo.upload(hlo);
+      X.lv_hi.upload(hhi);
+      X.max_rot = max_rot;
+      X.np.alloc(max_rot, s);
+      X.ioff.alloc(max_rot, s);
+      X.rbase.alloc(max_rot, s);
+      X.ndone.alloc(max_rot, s);
+      X.bsum.alloc(loop_grid + 1, s);
+      X.done.alloc(std::max<i64>(plan.R, 1), s);
+      X.done.zero();
+    }
+    auto size_loop_items = [&] {
+      X.max_items = max_rot + B.cap / merge_chunk() + 1;
+      X.item_rot.alloc(X.max_items, s);
+      X.status.alloc(X.max_items, s);
+      X.agg.alloc(K * X.max_items, s);
+      X.incl.alloc(K * X.max_items, s);
+    };
+    if (loop) size_loop_items();
     for (;;) {
-      for (int L = Lstart; L <= plan.max_level; ++L) {
-        const auto [lo, hi] = range[L];
-        if (hi <= lo) continue;
-        const int32_t* rots = plan.order.get() + lo;
+      if (loop) {
+        LoopArgs LA{};
+        LA.order = plan.order.get();
+        LA.lv_lo = X.lv_lo.get();
+        LA.lv_hi = X.lv_hi.get();
+        LA.L0 = Lstart;
+        LA.L1 = plan.max_level;
+        LA.ids = plan.ids.get();
+        LA.qs = plan.q;
+        LA.col0 = B.col0;
+        LA.off = B.off.get();
+        LA.len = B.len.get();
+        LA.arow = B.row.get();
+        LA.aval = B.val.get();
+        LA.chunk = merge_chunk();
+        LA.cursor = S.cursor.get();
+        LA.cap = B.cap;
+        LA.ovf = S.ovf.get();
+        LA.done = X.done.get();
+        LA.np = X.np.get();
+        LA.ioff = X.ioff.get();
+        LA.item_rot = X.item_rot.get();
+        LA.bsum = X.bsum.get();
+        LA.status = X.status.get();
+        LA.agg = X.agg.get();
+        LA.incl = X.incl.get();
+        LA.rbase = X.rbase.get();
+        LA.ndone = X.ndone.get();
+        LA.in_entries = S.in_entries.get();
+        LA.max_rot = max_rot;
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (prof_enabled()) {
+          e0 = EventPool::get().take();
+          e1 = EventPool::get().take();
+          cudaEventRecord(e0, s);
+        }
         switch (K) {
-          case 2: run_level<2>(B, S, plan, rots, hi - lo, L, s); break;
-          case 3: run_level<3>(B, S, plan, rots, hi - lo, L, s); break;
-          case 4: run_level<4>(B, S, plan, rots, hi - lo, L, s); break;
-          case 5: run_level<5>(B, S, plan, rots, hi - lo, L, s); break;
-          case 6: run_level<6>(B, S, plan, rots, hi - lo, L, s); break;
-          case 7: run_level<7>(B, S, plan, rots, hi - lo, L, s); break;
-          case 8: run_level<8>(B, S, plan, rots, hi - lo, L, s); break;
+          case 2: launch_level_loop<2>(LA, s); break;
+          case 3: launch_level_loop<3>(LA, s); break;
+          case 4: launch_level_loop<4>(LA, s); break;
+          case 5: launch_level_loop<5>(LA, s); break;
+          case 6: launch_level_loop<6>(LA, s); break;
+          case 7: launch_level_loop<7>(LA, s); break;
+          case 8: launch_level_loop<8>(LA, s); break;
           default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
+        }
+        if (e0) {
+          cudaEventRecord(e1, s);
+          S.ev.push_back({e0, e1});
+        }
+      } else {
+        for (int L = Lstart; L <= plan.max_level; ++L) {
+          const auto [lo, hi] = range[L];
+          if (hi <= lo) continue;
+          const int32_t* rots = plan.order.get() + lo;
+          switch (K) {
+            case 2: run_level<2>(B, S, plan, rots, hi - lo, L, s); break;
+            case 3: run_level<3>(B, S, plan, rots, hi - lo, L, s); break;
+            case 4: run_level<4>(B, S, plan, rots, hi - lo, L, s); break;
+            case 5: run_level<5>(B, S, plan, rots, hi - lo, L, s); break;
+            case 6: run_level<6>(B, S, plan, rots, hi - lo, L, s); break;
+            case 7: run_level<7>(B, S, plan, rots, hi - lo, L, s); break;
+            case 8: run_level<8>(B, S, plan, rots, hi - lo, L, s); break;
+            default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
+          }
         }
       }
       int32_t ovf = 0;
@@ -1204,7 +1686,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       if (trace_enabled())
         std::fprintf(stderr, "[pmmf]   arena overflow at level %d: compacted to %lld live, cap %lld\n", ovf,
                      static_cast<long long>(B.used), static_cast<long long>(B.cap));
-      size_items();
+      if (loop) size_loop_items(); else size_items();
       set_scalar(S.cursor, static_cast<unsigned long long>(B.used));
       set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));
       Lstart = ovf;
@@ -1222,7 +1704,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       std::vector<unsigned long long> io = S.in_entries.to_host(2);
       // algorithmic bytes: inputs read once, outputs written
       // once (12 B per entry), rotation blocks (8k^2 + 4k per rotation)
-      prof_add_n("rotate_write", static_cast<int64_t>(S.ev.size()), ms,
+      prof_add_n(loop ? "rotate_loop" : "rotate_write", static_cast<int64_t>(S.ev.size()), ms,
                  12.0 * static_cast<double>(io[0] + io[1]) + S.rot_bytes);
       double cms = 0.0;
       for (auto& [e0, e1] : S.cev) {
