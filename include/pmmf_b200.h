@@ -233,6 +233,56 @@ int pmmf_b200_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_conf
                     int32_t* iterations, int32_t* converged, int32_t* breakdown, double* residuals,
                     double* wall_ms, char* err, size_t errlen);
 
+/* ---- comparison preconditioners (solver.hpp:46-56, :224-349) -------- */
+
+/* PreconditionerKind (solver.hpp:60).  A preconditioner handle is a split
+ * pair M = K K^T given by the actions of K^-1 (side 0, "left") and K^-T
+ * (side 1, "right"), built on the GPU of a->device from the same triplets
+ * (and input partition) a factorization takes:
+ *   JACOBI  jacobi_preconditioner (solver.hpp:222-233): 1/sqrt(a_ii), 0 for
+ *           a_ii <= 0;
+ *   SSOR    ssor_preconditioner (:237-267), omega in (0, 2), else
+ *           PMMF_INVALID_ARGUMENT; a zero diagonal entry is PMMF_NUMERIC;
+ *   IC      ic_preconditioner (:278-340): IC(0) on the pattern of the lower
+ *           triangle (stored zeros included), restarted once on
+ *           A + alpha diag(A) after a breakdown; PMMF_NUMERIC when that is
+ *           impossible or breaks down again.
+ * The triangular solves and the IC(0) factorization are bit-identical to
+ * the reference's sequential loops (same operation order per entry). */
+enum { PMMF_PRECOND_NONE = 0, PMMF_PRECOND_JACOBI = 1, PMMF_PRECOND_SSOR = 2, PMMF_PRECOND_IC = 3,
+       PMMF_PRECOND_PMMF = 4 };
+int pmmf_b200_precond_create(const pmmf_b200_coo* a, int32_t kind, double omega, void** out, char* err,
+                             size_t errlen);
+/* pmmf_preconditioner (solver.hpp:343-349): K^-1 = K^-T = op->apply(inv_sqrt).
+ * The operator handle must outlive the preconditioner. */
+int pmmf_b200_precond_from_operator(void* op, void** out, char* err, size_t errlen);
+/* out = K^-1 in (side 0) or K^-T in (side 1) for nrhs rhs-major vectors;
+ * host pointers unless on_device != 0 (then device pointers on the
+ * preconditioner's GPU, ordered after the caller's prior work by a device
+ * synchronisation). */
+int pmmf_b200_precond_apply(void* pc, int32_t side, int64_t nrhs, const double* in, double* out,
+                            int32_t on_device, char* err, size_t errlen);
+/* IncompleteCholesky::{compensated, alpha} (solver.hpp:270-274); 0 / 0.0
+ * for the other kinds. */
+int pmmf_b200_precond_info(void* pc, int32_t* kind, int32_t* compensated, double* alpha);
+void pmmf_b200_precond_free(void* pc);
+/* run_solve_experiment with any split preconditioner (pc == NULL: plain CG,
+ * solver.hpp:170-172); outputs as pmmf_b200_solve. */
+int pmmf_b200_solve_precond(const pmmf_b200_coo* a, void* pc, const pmmf_b200_solve_config* cfg,
+                            int32_t* iterations, int32_t* converged, int32_t* breakdown, double* residuals,
+                            double* wall_ms, char* err, size_t errlen);
+
+/* ---- Nystrom sketch: nystrom_uniform (transform_ops.hpp:252-307) ----- */
+
+/* m distinct columns drawn uniformly by Rng(seed) (partial Fisher-Yates),
+ * A ~= C W^+ C^T with W^+ from the Jacobi eigensystem of W (eigenvalues
+ * |l| <= 1e-10 max|l| dropped), evaluated densely on the GPU.  Writes
+ * ||A - C W^+ C^T||_F and the m sampled columns (ascending).  m outside
+ * [1, n] is PMMF_INVALID_ARGUMENT, n > cap PMMF_NUMERIC (as the reference).
+ * Every entry and the final sum follow the reference's operation order. */
+int pmmf_b200_nystrom_uniform(const pmmf_b200_coo* a, int64_t m, uint64_t seed, int64_t cap,
+                              double* frobenius_error, int64_t* columns, char* err, size_t errlen);
+
 /* ---- input path (io.hpp:27-250) -------------------------------------- */
 
 /* TripletMatrix (io.hpp:27-33) / EdgeList (io.hpp:150-154), owned by the

@@ -17,10 +17,21 @@
 // refactorizing, exactly as MmfOperator(shared_ptr<const MmfFactorization>,
 // zero_threshold) does.
 //
+// The solver study (solver.hpp:222-416) swaps the same way:
+//
+//   pmmf_b200::GpuPreconditioner ic = pmmf_b200::ic_preconditioner(a);
+//       // replaces pmmf::ic_preconditioner (solver.hpp:278); also jacobi_ /
+//       // ssor_ / pmmf_preconditioner
+//   pmmf::SolveReport rep = pmmf_b200::run_solve_experiment(a, &ic, cfg, "ic");
+//       // replaces pmmf::run_solve_experiment (solver.hpp:368) with CG on the GPU
+//   pmmf::SplitPreconditioner k = ic.split();   // or feed the reference's own pcg
+//   pmmf::NystromResult ny = pmmf_b200::nystrom_uniform(a, m, seed);
+//
 // Errors are rethrown as the reference's exception types.
 #pragma once
 
 #include <pmmf/factorizer.hpp>
+#include <pmmf/solver.hpp>
 #include <pmmf/transform_ops.hpp>
 
 #include <memory>
@@ -272,6 +283,7 @@ class GpuOperator {
     if (op_) pmmf_b200_operator_free(op_);
   }
   pmmf::index_t dim() const { return n_; }
+  void* handle() const { return op_; }
   void apply(pmmf::MmfOperator::Mode mode, std::span<const double> in, std::span<double> out) const {
     if (static_cast<pmmf::index_t>(in.size()) != n_ || static_cast<pmmf::index_t>(out.size()) != n_)
       throw std::invalid_argument("MmfOperator::apply: dimension mismatch");
@@ -290,5 +302,164 @@ class GpuOperator {
   void* op_ = nullptr;
   pmmf::index_t n_ = 0;
 };
+
+// ---- solver study (solver.hpp:222-416) --------------------------------
+
+// A split preconditioner on the GPU (K^-1 = left, K^-T = right).
+class GpuPreconditioner {
+ public:
+  GpuPreconditioner(void* h, pmmf::index_t n) : h_(h, [](void* p) { pmmf_b200_precond_free(p); }), n_(n) {}
+  void* handle() const { return h_.get(); }
+  pmmf::index_t dim() const { return n_; }
+  bool compensated() const {
+    int32_t k = 0, c = 0;
+    double a = 0.0;
+    pmmf_b200_precond_info(h_.get(), &k, &c, &a);
+    return c != 0;
+  }
+  double alpha() const {
+    int32_t k = 0, c = 0;
+    double a = 0.0;
+    pmmf_b200_precond_info(h_.get(), &k, &c, &a);
+    return a;
+  }
+  void apply(int side, std::span<const double> in, std::span<double> out) const {
+    if (static_cast<pmmf::index_t>(in.size()) != n_ || static_cast<pmmf::index_t>(out.size()) != n_)
+      throw std::invalid_argument("SplitPreconditioner: length mismatch");
+    char err[4096] = {0};
+    rethrow(pmmf_b200_precond_apply(h_.get(), side, 1, in.data(), out.data(), 0, err, sizeof(err)), err);
+  }
+  // The reference's own SplitPreconditioner (solver.hpp:49-52) over this handle.
+  pmmf::SplitPreconditioner split() const {
+    auto h = h_;
+    const pmmf::index_t n = n_;
+    auto side = [h, n](int s) {
+      return [h, n, s](std::span<const double> in, std::span<double> out) {
+        char err[4096] = {0};
+        rethrow(pmmf_b200_precond_apply(h.get(), s, 1, in.data(), out.data(), 0, err, sizeof(err)), err);
+      };
+    };
+    return {{n, side(0)}, {n, side(1)}};
+  }
+
+ private:
+  std::shared_ptr<void> h_;
+  pmmf::index_t n_;
+};
+
+struct CooView {  // owns the triplet arrays behind a pmmf_b200_coo
+  std::vector<int64_t> r, c, off, mem;
+  std::vector<double> v;
+  pmmf_b200_coo coo{};
+  CooView(const pmmf::BlockedSparseMatrix& a, int device) {
+    to_coo(a, r, c, v, off, mem);
+    coo.n = a.dim();
+    coo.nnz = static_cast<int64_t>(v.size());
+    coo.rows = r.data();
+    coo.cols = c.data();
+    coo.vals = v.data();
+    coo.n_clusters = static_cast<int64_t>(off.size()) - 1;
+    coo.cluster_offsets = off.data();
+    coo.cluster_members = mem.data();
+    coo.device = device;
+  }
+};
+
+inline GpuPreconditioner make_preconditioner(const pmmf::BlockedSparseMatrix& a, int kind, double omega, int device) {
+  CooView cv(a, device);
+  char err[4096] = {0};
+  void* h = nullptr;
+  rethrow(pmmf_b200_precond_create(&cv.coo, kind, omega, &h, err, sizeof(err)), err);
+  return GpuPreconditioner(h, a.dim());
+}
+// jacobi_preconditioner (solver.hpp:222-233)
+inline GpuPreconditioner jacobi_preconditioner(const pmmf::BlockedSparseMatrix& a, int device = 0) {
+  return make_preconditioner(a, PMMF_PRECOND_JACOBI, 1.0, device);
+}
+// ssor_preconditioner (solver.hpp:237-267)
+inline GpuPreconditioner ssor_preconditioner(const pmmf::BlockedSparseMatrix& a, double omega = 1.0, int device = 0) {
+  return make_preconditioner(a, PMMF_PRECOND_SSOR, omega, device);
+}
+// ic_preconditioner (solver.hpp:278-340); compensated() / alpha() as
+// IncompleteCholesky's fields.
+inline GpuPreconditioner ic_preconditioner(const pmmf::BlockedSparseMatrix& a, int device = 0) {
+  return make_preconditioner(a, PMMF_PRECOND_IC, 1.0, device);
+}
+// pmmf_preconditioner (solver.hpp:343-349); `op` must outlive the result.
+inline GpuPreconditioner pmmf_preconditioner(const GpuOperator& op) {
+  char err[4096] = {0};
+  void* h = nullptr;
+  rethrow(pmmf_b200_precond_from_operator(op.handle(), &h, err, sizeof(err)), err);
+  return GpuPreconditioner(h, op.dim());
+}
+
+// run_solve_experiment (solver.hpp:368-416) with the CG on the GPU; the
+// report is aggregated exactly as the reference aggregates its runs.
+inline pmmf::SolveReport run_solve_experiment(const pmmf::BlockedSparseMatrix& a, const GpuPreconditioner* m,
+                                              const pmmf::SolveConfig& cfg, const std::string& method_name,
+                                              int device = 0) {
+  cfg.validate();
+  CooView cv(a, device);
+  const pmmf_b200_solve_config c{cfg.tol, cfg.max_iter, cfg.rhs_count, cfg.seed};
+  const size_t nr = static_cast<size_t>(cfg.rhs_count), stride = static_cast<size_t>(cfg.max_iter) + 1;
+  std::vector<int32_t> it(nr), conv(nr), brk(nr);
+  std::vector<double> res(nr * stride);
+  double wall = 0.0;
+  char err[4096] = {0};
+  rethrow(pmmf_b200_solve_precond(&cv.coo, m ? m->handle() : nullptr, &c, it.data(), conv.data(), brk.data(),
+                                  res.data(), &wall, err, sizeof(err)),
+          err);
+  pmmf::SolveReport report;
+  report.method = method_name;
+  report.runs.resize(nr);
+  for (size_t r = 0; r < nr; ++r) {
+    auto& run = report.runs[r];
+    run.iterations = it[r];
+    run.converged = conv[r] != 0;
+    run.breakdown = brk[r] != 0;
+    run.residuals.assign(res.begin() + static_cast<std::ptrdiff_t>(r * stride),
+                         res.begin() + static_cast<std::ptrdiff_t>(r * stride + static_cast<size_t>(it[r]) + 1));
+  }
+  report.wall_ms_total = wall;
+  size_t longest = 0;
+  long total = 0;
+  for (const auto& run : report.runs) {
+    longest = std::max(longest, run.residuals.size());
+    total += run.iterations;
+    report.max_iterations_used = std::max(report.max_iterations_used, run.iterations);
+    report.all_converged = report.all_converged && run.converged;
+    report.any_breakdown = report.any_breakdown || run.breakdown;
+  }
+  report.mean_iterations = static_cast<double>(total) / cfg.rhs_count;
+  report.per_iteration_ms = total > 0 ? wall / static_cast<double>(total) : 0.0;
+  report.mean_residual.assign(longest, 0.0);
+  report.std_residual.assign(longest, 0.0);
+  for (size_t k = 0; k < longest; ++k) {
+    double mean = 0.0;
+    for (const auto& run : report.runs) mean += k < run.residuals.size() ? run.residuals[k] : run.residuals.back();
+    mean /= cfg.rhs_count;
+    double var = 0.0;
+    for (const auto& run : report.runs) {
+      const double d = (k < run.residuals.size() ? run.residuals[k] : run.residuals.back()) - mean;
+      var += d * d;
+    }
+    report.mean_residual[k] = mean;
+    report.std_residual[k] = std::sqrt(var / cfg.rhs_count);
+  }
+  return report;
+}
+
+// nystrom_uniform (transform_ops.hpp:259-307), evaluated on the GPU.
+inline pmmf::NystromResult nystrom_uniform(const pmmf::BlockedSparseMatrix& a, pmmf::index_t m, std::uint64_t seed,
+                                           pmmf::index_t cap = 4096, int device = 0) {
+  CooView cv(a, device);
+  pmmf::NystromResult out;
+  out.columns.assign(static_cast<size_t>(std::max<pmmf::index_t>(m, 1)), 0);
+  char err[4096] = {0};
+  rethrow(pmmf_b200_nystrom_uniform(&cv.coo, m, seed, cap, &out.frobenius_error, out.columns.data(), err, sizeof(err)),
+          err);
+  out.columns.resize(static_cast<size_t>(m));
+  return out;
+}
 
 }  // namespace pmmf_b200

@@ -8,6 +8,7 @@
 #include <pmmf/factorizer.hpp>
 #include <pmmf/transform_ops.hpp>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -82,6 +83,38 @@ int main(int argc, char** argv) {
       }
       check(threw, "out-of-range rotation index rejected");
     }
+  }
+  // solver study: the GPU preconditioners equal the reference's, side by side
+  {
+    std::vector<double> x(v.size()), r1(v.size()), r2(v.size());
+    for (size_t i = 0; i < x.size(); ++i) x[i] = std::cos(0.11 * static_cast<double>(i));
+    const pmmf::SplitPreconditioner jr = pmmf::jacobi_preconditioner(a), sr = pmmf::ssor_preconditioner(a, 1.2);
+    const pmmf::IncompleteCholesky icr = pmmf::ic_preconditioner(a);
+    const pmmf_b200::GpuPreconditioner jg = pmmf_b200::jacobi_preconditioner(a), sg = pmmf_b200::ssor_preconditioner(a, 1.2),
+                                       ig = pmmf_b200::ic_preconditioner(a);
+    check(ig.compensated() == icr.compensated && ig.alpha() == icr.alpha, "ic compensation");
+    const std::pair<const pmmf::SplitPreconditioner*, const pmmf_b200::GpuPreconditioner*> pairs[] = {
+        {&jr, &jg}, {&sr, &sg}, {&icr.precond, &ig}};
+    for (const auto& [pr, pg] : pairs) {
+      const pmmf::SplitPreconditioner k = pg->split();
+      pr->left.apply(x, r1);
+      k.left.apply(x, r2);
+      check(r1 == r2, "preconditioner K^-1");
+      pr->right.apply(x, r1);
+      pg->apply(1, x, r2);
+      check(r1 == r2, "preconditioner K^-T");
+    }
+    pmmf::SolveConfig sc;
+    sc.tol = 1e-8;
+    sc.max_iter = 500;
+    sc.rhs_count = 2;
+    const pmmf::LinearOperator lin = pmmf::make_operator(a);
+    const pmmf::SolveReport rr = pmmf::run_solve_experiment(lin, &icr.precond, sc, "ic");
+    const pmmf::SolveReport rg = pmmf_b200::run_solve_experiment(a, &ig, sc, "ic");
+    check(rr.all_converged == rg.all_converged && std::abs(rr.mean_iterations - rg.mean_iterations) <= 2.0,
+          "run_solve_experiment (ic)");
+    const pmmf::NystromResult nr = pmmf::nystrom_uniform(a, 64, 9), ng = pmmf_b200::nystrom_uniform(a, 64, 9);
+    check(nr.columns == ng.columns && nr.frobenius_error == ng.frobenius_error, "nystrom_uniform");
   }
   std::printf("%s: %zu stages, %zu rotations in stage 1\n", bad ? "FAIL" : "PASS", gpu.stages.size(),
               gpu.stages.empty() ? size_t{0} : gpu.stages[0].rotations.size());

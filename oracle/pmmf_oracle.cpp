@@ -929,6 +929,204 @@ double vdot(const std::vector<double>& a, const std::vector<double>& b) {  // so
   return s;
 }
 
+// ---- comparison preconditioners (solver.hpp:174-340), restated
+// Entries of A after from_triplets in to_triplets order (blocked_matrix.hpp:
+// 422-436): row clusters, then column clusters, then the block's columns,
+// then rows; duplicates summed in input order, stored zeros KEPT.
+struct Trip {
+  i64 r, c;
+  double v;
+};
+std::vector<Trip> to_triplets_kept(const pmmf_b200_coo* in) {
+  Numbering nb;
+  std::vector<std::vector<i64>> init;
+  if (in->n_clusters == 0) {
+    init.emplace_back(static_cast<size_t>(in->n));
+    std::iota(init[0].begin(), init[0].end(), i64{0});
+  } else {
+    for (i64 u = 0; u < in->n_clusters; ++u)
+      init.emplace_back(in->cluster_members + in->cluster_offsets[u], in->cluster_members + in->cluster_offsets[u + 1]);
+  }
+  nb.build(init, in->n);
+  std::vector<Col> cols(static_cast<size_t>(nb.size()));
+  for (i64 t = 0; t < in->nnz; ++t) {
+    if (in->rows[t] < 0 || in->rows[t] >= in->n || in->cols[t] < 0 || in->cols[t] >= in->n)
+      fail(PMMF_OUT_OF_RANGE, "from_triplets: index out of range");
+    cols[nb.g2s[in->cols[t]]].push_back({nb.g2s[in->rows[t]], in->vals[t]});
+  }
+  // per stage column: stable sort by row, sum duplicates (sparse.hpp:66-79)
+  std::vector<std::vector<std::pair<i64, double>>> summed(cols.size());
+  for (size_t j = 0; j < cols.size(); ++j) {
+    Col& col = cols[j];
+    std::stable_sort(col.begin(), col.end(), [](const Ent& x, const Ent& y) { return x.r < y.r; });
+    for (size_t i = 0; i < col.size();) {
+      double s = col[i].v;
+      size_t k = i + 1;
+      while (k < col.size() && col[k].r == col[i].r) s += col[k++].v;
+      summed[j].push_back({col[i].r, s});
+      i = k;
+    }
+  }
+  std::vector<Trip> out;
+  const i64 m = nb.clusters();
+  for (i64 u = 0; u < m; ++u)
+    for (i64 v = 0; v < m; ++v)
+      for (i64 j = nb.off[v]; j < nb.off[v + 1]; ++j)
+        for (const auto& [r, val] : summed[j])
+          if (r >= nb.off[u] && r < nb.off[u + 1]) out.push_back({nb.s2g[r], nb.s2g[j], val});
+  return out;
+}
+
+struct LowerTri {  // detail::LowerTriangle (solver.hpp:174-202)
+  std::vector<double> diag;
+  std::vector<std::vector<std::pair<i64, double>>> cols;  // strictly lower, rows ascending
+  i64 n() const { return static_cast<i64>(diag.size()); }
+  void forward_solve(const double* b, double* x) const {  // solver.hpp:183-191
+    std::copy(b, b + n(), x);
+    for (i64 j = 0; j < n(); ++j) {
+      x[j] /= diag[j];
+      const double xj = x[j];
+      for (const auto& [r, v] : cols[j]) x[r] -= v * xj;
+    }
+  }
+  void backward_solve(const double* b, double* x) const {  // solver.hpp:193-201
+    for (i64 j = n() - 1; j >= 0; --j) {
+      double acc = b[j];
+      for (const auto& [r, v] : cols[j]) acc -= v * x[r];
+      x[j] = acc / diag[j];
+    }
+  }
+};
+
+LowerTri extract_lower(const std::vector<Trip>& t, i64 n) {  // solver.hpp:204-218
+  LowerTri l;
+  l.diag.assign(static_cast<size_t>(n), 0.0);
+  l.cols.resize(static_cast<size_t>(n));
+  for (const Trip& e : t) {
+    if (e.r == e.c)
+      l.diag[e.r] = e.v;
+    else if (e.r > e.c)
+      l.cols[e.c].push_back({e.r, e.v});
+  }
+  for (auto& c : l.cols) std::stable_sort(c.begin(), c.end(), [](auto& a, auto& b) { return a.first < b.first; });
+  return l;
+}
+
+struct Pre {
+  int kind = 0;
+  i64 n = 0;
+  std::vector<double> scale;  // jacobi
+  LowerTri lower;             // ssor / ic
+  std::vector<double> sqrt_d;  // ssor
+  int compensated = 0;
+  double alpha = 0.0;
+  const Operator* op = nullptr;  // pmmf
+  void apply(int side, const double* in, double* out) const {
+    if (kind == PMMF_PRECOND_JACOBI) {
+      for (i64 i = 0; i < n; ++i) out[i] = scale[i] * in[i];
+    } else if (kind == PMMF_PRECOND_SSOR) {
+      if (side == 0) {
+        lower.forward_solve(in, out);
+        for (i64 i = 0; i < n; ++i) out[i] *= sqrt_d[i];
+      } else {
+        std::vector<double> sc(static_cast<size_t>(n));
+        for (i64 i = 0; i < n; ++i) sc[i] = in[i] * sqrt_d[i];
+        lower.backward_solve(sc.data(), out);
+      }
+    } else if (kind == PMMF_PRECOND_IC) {
+      if (side == 0)
+        lower.forward_solve(in, out);
+      else
+        lower.backward_solve(in, out);
+    } else if (kind == PMMF_PRECOND_PMMF) {
+      op->apply(2, in, out);
+    } else {
+      std::copy(in, in + n, out);
+    }
+  }
+};
+
+bool ic_attempt(const LowerTri& pattern, double boost, LowerTri& l) {  // solver.hpp:284-313
+  const i64 n = pattern.n();
+  l = pattern;
+  for (i64 j = 0; j < n; ++j) l.diag[j] *= (1.0 + boost);
+  std::vector<std::vector<std::pair<i64, size_t>>> rows(static_cast<size_t>(n));
+  std::vector<double> work;
+  for (i64 j = 0; j < n; ++j) {
+    auto& col = l.cols[j];
+    double pivot = l.diag[j];
+    work.assign(col.size(), 0.0);
+    for (size_t t = 0; t < col.size(); ++t) work[t] = col[t].second;
+    for (const auto& [k, pos] : rows[j]) {
+      const auto& ck = l.cols[k];
+      const double ljk = ck[pos].second;
+      pivot -= ljk * ljk;
+      size_t t = 0;
+      for (size_t s = pos + 1; s < ck.size(); ++s) {
+        const i64 r = ck[s].first;
+        while (t < col.size() && col[t].first < r) ++t;
+        if (t == col.size()) break;
+        if (col[t].first == r) work[t] -= ck[s].second * ljk;
+      }
+    }
+    if (!(pivot > 0.0)) return false;
+    l.diag[j] = std::sqrt(pivot);
+    for (size_t t = 0; t < col.size(); ++t) {
+      col[t].second = work[t] / l.diag[j];
+      rows[col[t].first].emplace_back(j, t);
+    }
+  }
+  return true;
+}
+
+std::unique_ptr<Pre> make_pre(const pmmf_b200_coo* a, int kind, double omega) {
+  auto p = std::make_unique<Pre>();
+  p->kind = kind;
+  p->n = a->n;
+  const i64 n = a->n;
+  if (kind == PMMF_PRECOND_SSOR && !(omega > 0.0 && omega < 2.0))
+    fail(PMMF_INVALID_ARGUMENT, "ssor: omega must be in (0, 2)");
+  const std::vector<Trip> t = to_triplets_kept(a);
+  if (kind == PMMF_PRECOND_JACOBI) {  // solver.hpp:222-233
+    p->scale.assign(static_cast<size_t>(n), 0.0);
+    for (const Trip& e : t)
+      if (e.r == e.c && e.v > 0.0) p->scale[e.r] = 1.0 / std::sqrt(e.v);
+  } else if (kind == PMMF_PRECOND_SSOR) {  // solver.hpp:237-267
+    p->lower = extract_lower(t, n);
+    for (i64 i = 0; i < n; ++i)
+      if (p->lower.diag[i] == 0.0) fail(PMMF_NUMERIC, "ssor: zero diagonal entry at row " + std::to_string(i));
+    p->sqrt_d.resize(static_cast<size_t>(n));
+    const double front = std::sqrt((2.0 - omega) / omega);
+    for (i64 i = 0; i < n; ++i) {
+      const double d = p->lower.diag[i];
+      p->sqrt_d[i] = front * std::sqrt(std::abs(d));
+      p->lower.diag[i] = d / omega;
+    }
+  } else if (kind == PMMF_PRECOND_IC) {  // solver.hpp:278-340
+    const LowerTri pattern = extract_lower(t, n);
+    if (!ic_attempt(pattern, 0.0, p->lower)) {
+      std::vector<double> row_abs(static_cast<size_t>(n), 0.0), diag(static_cast<size_t>(n), 0.0);
+      for (const Trip& e : t) {
+        row_abs[e.r] += std::abs(e.v);
+        if (e.r == e.c) diag[e.r] = e.v;
+      }
+      double alpha = 0.0;
+      for (i64 i = 0; i < n; ++i) {
+        if (!(diag[i] > 0.0))
+          fail(PMMF_NUMERIC, "ic: non-positive diagonal, cannot compensate row " + std::to_string(i));
+        alpha = std::max(alpha, row_abs[i] / diag[i]);
+      }
+      p->compensated = 1;
+      p->alpha = alpha;
+      if (!ic_attempt(pattern, alpha, p->lower))
+        fail(PMMF_NUMERIC, "ic: breakdown persists after diagonal compensation");
+    }
+  } else {
+    fail(PMMF_INVALID_ARGUMENT, "preconditioner: unknown kind");
+  }
+  return p;
+}
+
 }  // namespace orc
 
 // =================================================================== C-ABI
@@ -1067,19 +1265,18 @@ int pmmf_oracle_operator_zeroed_negatives(void* op, int64_t* out) {
 void pmmf_oracle_operator_free(void* op) { delete static_cast<Operator*>(op); }
 
 // run_solve_experiment + pcg_symmetric (solver.hpp:112-167, :368-416).
-int pmmf_oracle_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_config* cfg, int32_t* iters,
-                      int32_t* conv, int32_t* brk, double* res, double* wall_ms, char* err, size_t errlen) {
-  return guarded(err, errlen, [&] {
+static void solve_with(const pmmf_b200_coo* a, const Pre* pc, const pmmf_b200_solve_config* cfg, int32_t* iters,
+                       int32_t* conv, int32_t* brk, double* res, double* wall_ms) {
+  {
     if (!(cfg->tol > 0.0)) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: tol must be positive");
     if (cfg->max_iter < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: max_iter < 1");
     if (cfg->rhs_count < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: rhs_count < 1");
     const auto start = clk::now();
     SpMat S = make_spmat(a);
     const i64 n = a->n;
-    auto* o = static_cast<Operator*>(op);
-    auto pre = [&](const std::vector<double>& x, std::vector<double>& y) {
-      if (o)
-        o->apply(2, x.data(), y.data());
+    auto pre = [&](int side, const std::vector<double>& x, std::vector<double>& y) {
+      if (pc)
+        pc->apply(side, x.data(), y.data());
       else
         y = x;
     };
@@ -1123,13 +1320,13 @@ int pmmf_oracle_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_co
         continue;
       }
       std::vector<double> y(n, 0.0), r(n), p(n), w(n), t1(n), t2(n), x(n), tr(n);
-      pre(b, r);
+      pre(0, b, r);
       p = r;
       double rr = vdot(r, r);
       for (int k = 1; k <= cfg->max_iter; ++k) {
-        pre(p, t1);
+        pre(1, p, t1);
         spmv(S, t1, t2);
-        pre(t2, w);
+        pre(0, t2, w);
         const double pap = vdot(p, w);
         if (!(pap > 0.0)) {
           brk[rhs] = 1;
@@ -1138,7 +1335,7 @@ int pmmf_oracle_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_co
         const double alpha = rr / pap;
         for (i64 i = 0; i < n; ++i) y[i] += alpha * p[i];
         for (i64 i = 0; i < n; ++i) r[i] -= alpha * w[i];
-        pre(y, x);
+        pre(1, y, x);
         spmv(S, x, t2);
         for (i64 i = 0; i < n; ++i) tr[i] = b[i] - t2[i];
         const double rs = std::sqrt(vdot(tr, tr));
@@ -1155,6 +1352,107 @@ int pmmf_oracle_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_co
       }
     }
     *wall_ms = ms_since(start);
+  }
+}
+
+int pmmf_oracle_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_config* cfg, int32_t* iters,
+                      int32_t* conv, int32_t* brk, double* res, double* wall_ms, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    std::unique_ptr<Pre> pc;
+    if (op) {
+      pc = std::make_unique<Pre>();
+      pc->kind = PMMF_PRECOND_PMMF;
+      pc->n = a->n;
+      pc->op = static_cast<Operator*>(op);
+    }
+    solve_with(a, pc.get(), cfg, iters, conv, brk, res, wall_ms);
+  });
+}
+
+int pmmf_oracle_solve_precond(const pmmf_b200_coo* a, void* pc, const pmmf_b200_solve_config* cfg, int32_t* iters,
+                              int32_t* conv, int32_t* brk, double* res, double* wall_ms, char* err, size_t errlen) {
+  return guarded(err, errlen,
+                 [&] { solve_with(a, static_cast<const Pre*>(pc), cfg, iters, conv, brk, res, wall_ms); });
+}
+
+int pmmf_oracle_precond_create(const pmmf_b200_coo* a, int32_t kind, double omega, void** out, char* err,
+                               size_t errlen) {
+  return guarded(err, errlen, [&] { *out = make_pre(a, kind, omega).release(); });
+}
+
+int pmmf_oracle_precond_from_operator(void* op, void** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto p = std::make_unique<Pre>();
+    p->kind = PMMF_PRECOND_PMMF;
+    p->op = static_cast<Operator*>(op);
+    p->n = p->op->f->n;
+    *out = p.release();
+  });
+}
+
+int pmmf_oracle_precond_apply(void* pc, int32_t side, int64_t nrhs, const double* in, double* out, int32_t on_device,
+                              char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (on_device) fail(PMMF_INVALID_ARGUMENT, "oracle takes host buffers only");
+    const auto* p = static_cast<const Pre*>(pc);
+    for (int64_t r = 0; r < nrhs; ++r) p->apply(side, in + r * p->n, out + r * p->n);
+  });
+}
+
+int pmmf_oracle_precond_info(void* pc, int32_t* kind, int32_t* compensated, double* alpha) {
+  const auto* p = static_cast<const Pre*>(pc);
+  *kind = p->kind;
+  *compensated = p->compensated;
+  *alpha = p->alpha;
+  return PMMF_OK;
+}
+
+void pmmf_oracle_precond_free(void* pc) { delete static_cast<Pre*>(pc); }
+
+// nystrom_uniform (transform_ops.hpp:252-307)
+int pmmf_oracle_nystrom_uniform(const pmmf_b200_coo* a, int64_t m, uint64_t seed, int64_t cap, double* fro,
+                                int64_t* columns, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const i64 n = a->n;
+    if (m < 1 || m > n) fail(PMMF_INVALID_ARGUMENT, "nystrom_uniform: m out of range");
+    if (n > cap) fail(PMMF_NUMERIC, "dense_from_blocked: dimension exceeds cap");
+    Mat dense(n, n);
+    for (const Trip& e : to_triplets_kept(a)) dense(e.r, e.c) = e.v;
+    std::vector<i64> ids(static_cast<size_t>(n));
+    std::iota(ids.begin(), ids.end(), i64{0});
+    Rng rng(seed);
+    for (i64 t = 0; t < m; ++t) {
+      const i64 pick = t + static_cast<i64>(rng.below(static_cast<uint64_t>(n - t)));
+      std::swap(ids[t], ids[pick]);
+    }
+    std::vector<i64> sel(ids.begin(), ids.begin() + m);
+    std::sort(sel.begin(), sel.end());
+    std::copy(sel.begin(), sel.end(), columns);
+    Mat c(n, m), w(m, m);
+    for (i64 j = 0; j < m; ++j) {
+      for (i64 i = 0; i < n; ++i) c(i, j) = dense(i, sel[j]);
+      for (i64 i = 0; i < m; ++i) w(i, j) = dense(sel[i], sel[j]);
+    }
+    Mat q = jacobi_diagonalize(w);  // jacobi_eigensystem: values = diag(w), vectors = q^T
+    double max_mag = 0.0;
+    for (i64 e = 0; e < m; ++e) max_mag = std::max(max_mag, std::abs(w(e, e)));
+    const double threshold = 1e-10 * max_mag;
+    Mat pinv(m, m);
+    for (i64 e = 0; e < m; ++e) {
+      const double lambda = w(e, e);
+      if (std::abs(lambda) <= threshold) continue;
+      const double inv = 1.0 / lambda;
+      for (i64 i = 0; i < m; ++i)
+        for (i64 j = 0; j < m; ++j) pinv(i, j) += inv * q(e, i) * q(e, j);
+    }
+    Mat approx = multiply(multiply(c, pinv), transposed(c));
+    double s = 0.0;
+    for (i64 i = 0; i < n; ++i)
+      for (i64 j = 0; j < n; ++j) {
+        const double d = dense(i, j) - approx(i, j);
+        s += d * d;
+      }
+    *fro = std::sqrt(s);
   });
 }
 

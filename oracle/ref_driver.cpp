@@ -287,6 +287,110 @@ int pmmf_ref_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_confi
   });
 }
 
+// ---- comparison preconditioners (solver.hpp:222-349), the reference's own
+struct RefPrecond {
+  pmmf::SplitPreconditioner pre;
+  int kind = 0;
+  int64_t n = 0;
+  int compensated = 0;
+  double alpha = 0.0;
+};
+
+int pmmf_ref_precond_create(const pmmf_b200_coo* a, int32_t kind, double omega, void** out, char* err,
+                            size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto m = make_matrix(a);
+    auto p = std::make_unique<RefPrecond>();
+    p->kind = kind;
+    p->n = a->n;
+    if (kind == PMMF_PRECOND_JACOBI) {
+      p->pre = pmmf::jacobi_preconditioner(m);
+    } else if (kind == PMMF_PRECOND_SSOR) {
+      p->pre = pmmf::ssor_preconditioner(m, omega);
+    } else if (kind == PMMF_PRECOND_IC) {
+      pmmf::IncompleteCholesky ic = pmmf::ic_preconditioner(m);
+      p->pre = ic.precond;
+      p->compensated = ic.compensated ? 1 : 0;
+      p->alpha = ic.alpha;
+    } else {
+      throw std::invalid_argument("preconditioner: unknown kind");
+    }
+    *out = p.release();
+  });
+}
+
+int pmmf_ref_precond_from_operator(void* op, void** out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto* o = static_cast<RefOperator*>(op);
+    auto f = std::shared_ptr<const pmmf::MmfFactorization>(&o->op->factorization(),
+                                                           [](const pmmf::MmfFactorization*) {});
+    auto p = std::make_unique<RefPrecond>();
+    p->kind = PMMF_PRECOND_PMMF;
+    p->n = o->op->dim();
+    p->pre = pmmf::pmmf_preconditioner(f);
+    *out = p.release();
+  });
+}
+
+int pmmf_ref_precond_apply(void* pc, int32_t side, int64_t nrhs, const double* in, double* out, int32_t on_device,
+                           char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (on_device) throw std::invalid_argument("reference path takes host buffers only");
+    auto* p = static_cast<RefPrecond*>(pc);
+    const auto n = static_cast<std::size_t>(p->n);
+    const pmmf::LinearOperator& op = side == 0 ? p->pre.left : p->pre.right;
+    for (int64_t r = 0; r < nrhs; ++r)
+      op.apply(std::span<const double>(in + r * n, n), std::span<double>(out + r * n, n));
+  });
+}
+
+int pmmf_ref_precond_info(void* pc, int32_t* kind, int32_t* compensated, double* alpha) {
+  auto* p = static_cast<RefPrecond*>(pc);
+  *kind = p->kind;
+  *compensated = p->compensated;
+  *alpha = p->alpha;
+  return PMMF_OK;
+}
+
+void pmmf_ref_precond_free(void* pc) { delete static_cast<RefPrecond*>(pc); }
+
+int pmmf_ref_solve_precond(const pmmf_b200_coo* a, void* pc, const pmmf_b200_solve_config* cfg,
+                           int32_t* iterations, int32_t* converged, int32_t* breakdown, double* residuals,
+                           double* wall_ms, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto m = make_matrix(a);
+    pmmf::LinearOperator lin = pmmf::make_operator(m);
+    pmmf::SolveConfig sc;
+    sc.tol = cfg->tol;
+    sc.max_iter = cfg->max_iter;
+    sc.rhs_count = cfg->rhs_count;
+    sc.seed = cfg->seed;
+    auto* p = static_cast<RefPrecond*>(pc);
+    pmmf::SolveReport rep = pmmf::run_solve_experiment(lin, p ? &p->pre : nullptr, sc, "precond");
+    const int64_t stride = cfg->max_iter + 1;
+    for (int r = 0; r < cfg->rhs_count; ++r) {
+      const auto& run = rep.runs[static_cast<std::size_t>(r)];
+      iterations[r] = run.iterations;
+      converged[r] = run.converged ? 1 : 0;
+      breakdown[r] = run.breakdown ? 1 : 0;
+      for (int64_t i = 0; i < stride; ++i)
+        residuals[r * stride + i] =
+            i < static_cast<int64_t>(run.residuals.size()) ? run.residuals[static_cast<std::size_t>(i)] : NAN;
+    }
+    *wall_ms = rep.wall_ms_total;
+  });
+}
+
+int pmmf_ref_nystrom_uniform(const pmmf_b200_coo* a, int64_t m, uint64_t seed, int64_t cap, double* fro,
+                             int64_t* columns, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto mat = make_matrix(a);
+    pmmf::NystromResult r = pmmf::nystrom_uniform(mat, m, seed, cap);
+    *fro = r.frobenius_error;
+    std::copy(r.columns.begin(), r.columns.end(), columns);
+  });
+}
+
 int pmmf_ref_rotation_from_gram(int32_t k, const double* g, double* q, char* err, size_t errlen) {
   return guarded(err, errlen, [&] {
     pmmf::DenseMatrix gs(k, k);

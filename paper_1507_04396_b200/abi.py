@@ -227,6 +227,22 @@ class FlatAbi:
             [ctypes.POINTER(Coo), V, ctypes.POINTER(SolveConfig), c_i32p, c_i32p, c_i32p, c_f64p, c_f64p] + E,
         )
         self.rotation_from_gram = fn("rotation_from_gram", ctypes.c_int, [ctypes.c_int32, c_f64p, c_f64p] + E)
+        # comparison preconditioners + Nystrom (solver.hpp:222-349, transform_ops.hpp:252-307)
+        self.precond_create = fn("precond_create", ctypes.c_int,
+                                 [ctypes.POINTER(Coo), ctypes.c_int32, ctypes.c_double, ctypes.POINTER(V)] + E)
+        self.precond_from_operator = fn("precond_from_operator", ctypes.c_int, [V, ctypes.POINTER(V)] + E)
+        self.precond_apply = fn("precond_apply", ctypes.c_int,
+                                [V, ctypes.c_int32, ctypes.c_int64, V, V, ctypes.c_int32] + E)
+        self.precond_info = fn("precond_info", ctypes.c_int, [V, c_i32p, c_i32p, c_f64p])
+        self.precond_free = fn("precond_free", None, [V])
+        self.solve_precond = fn(
+            "solve_precond",
+            ctypes.c_int,
+            [ctypes.POINTER(Coo), V, ctypes.POINTER(SolveConfig), c_i32p, c_i32p, c_i32p, c_f64p, c_f64p] + E,
+        )
+        self.nystrom_uniform = fn("nystrom_uniform", ctypes.c_int,
+                                  [ctypes.POINTER(Coo), ctypes.c_int64, ctypes.c_uint64, ctypes.c_int64, c_f64p,
+                                   c_i64p] + E)
 
     # ------------------------------------------------------------------
     @staticmethod

@@ -494,6 +494,185 @@ def residual_frobenius(handle: ctypes.c_void_p, matrix: "BlockedSparseMatrix", m
     return out.value
 
 
+# ------------------------------------------- solver study (solver.hpp)
+class PreconditionerKind:
+    """PreconditionerKind (solver.hpp:60)."""
+    none, jacobi, ssor, ic, pmmf = 0, 1, 2, 3, 4
+
+
+def preconditioner_name(kind: int) -> str:  # solver.hpp:62-71
+    return {0: "none", 1: "jacobi", 2: "ssor", 3: "ic", 4: "pmmf"}.get(int(kind), "?")
+
+
+class SplitPreconditioner:
+    """SplitPreconditioner (solver.hpp:49-52) on the GPU: left(x) = K^-1 x,
+    right(x) = K^-T x for one vector (n,) or a batch (b, n) of host vectors."""
+
+    def __init__(self, handle: ctypes.c_void_p, n: int, keep=None):
+        self._h = handle
+        self._n = int(n)
+        self._keep = keep  # e.g. the MmfOperator a pmmf preconditioner wraps
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def _apply(self, side: int, x):
+        lib = library()
+        a = np.ascontiguousarray(x, np.float64)
+        if a.shape[-1] != self._n or a.ndim > 2:
+            raise ValueError("SplitPreconditioner: length mismatch")
+        out = np.zeros_like(a)
+        err = lib.errbuf()
+        abi.raise_for(lib.precond_apply(self._h, side, 1 if a.ndim == 1 else a.shape[0], a.ctypes.data,
+                                        out.ctypes.data, 0, err, len(err)), err)
+        return out
+
+    def left(self, x):
+        return self._apply(0, x)
+
+    def right(self, x):
+        return self._apply(1, x)
+
+    def info(self):
+        k, c, a = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+        library().precond_info(self._h, ctypes.byref(k), ctypes.byref(c), ctypes.byref(a))
+        return int(k.value), bool(c.value), float(a.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            library().precond_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class IncompleteCholesky:
+    """IncompleteCholesky (solver.hpp:270-274)."""
+    precond: SplitPreconditioner
+    compensated: bool = False
+    alpha: float = 0.0
+
+
+def _make_precond(matrix: "BlockedSparseMatrix", kind: int, omega: float, device: int) -> SplitPreconditioner:
+    lib = library()
+    coo, keep = matrix.coo(device)
+    h = ctypes.c_void_p()
+    err = lib.errbuf()
+    abi.raise_for(lib.precond_create(ctypes.byref(coo), int(kind), float(omega), ctypes.byref(h), err, len(err)), err)
+    return SplitPreconditioner(h, matrix.n)
+
+
+def jacobi_preconditioner(matrix: "BlockedSparseMatrix", device: int = 0) -> SplitPreconditioner:
+    """jacobi_preconditioner (solver.hpp:222-233)."""
+    return _make_precond(matrix, PreconditionerKind.jacobi, 1.0, device)
+
+
+def ssor_preconditioner(matrix: "BlockedSparseMatrix", omega: float = 1.0, device: int = 0) -> SplitPreconditioner:
+    """ssor_preconditioner (solver.hpp:237-267); omega in (0, 2)."""
+    return _make_precond(matrix, PreconditionerKind.ssor, omega, device)
+
+
+def ic_preconditioner(matrix: "BlockedSparseMatrix", device: int = 0) -> IncompleteCholesky:
+    """ic_preconditioner (solver.hpp:278-340): IC(0), one compensated restart."""
+    p = _make_precond(matrix, PreconditionerKind.ic, 1.0, device)
+    _, comp, alpha = p.info()
+    return IncompleteCholesky(p, comp, alpha)
+
+
+def pmmf_preconditioner(op: "MmfOperator") -> SplitPreconditioner:
+    """pmmf_preconditioner (solver.hpp:343-349): K^-1 = K^-T = apply(inv_sqrt)."""
+    lib = library()
+    h = ctypes.c_void_p()
+    err = lib.errbuf()
+    abi.raise_for(lib.precond_from_operator(op._op, ctypes.byref(h), err, len(err)), err)
+    return SplitPreconditioner(h, op.dim(), keep=op)
+
+
+@dataclass
+class SolveConfig:
+    """SolveConfig (solver.hpp:73-86); the preconditioner is passed to
+    run_solve_experiment."""
+    tol: float = 1e-5
+    max_iter: int = 100
+    rhs_count: int = 20
+    seed: int = 0
+
+
+@dataclass
+class SolveReport:
+    """SolveReport (solver.hpp:352-365); runs[r] = (iterations, converged,
+    breakdown, residual trace)."""
+    method: str
+    mean_residual: np.ndarray
+    std_residual: np.ndarray
+    mean_iterations: float
+    max_iterations_used: int
+    all_converged: bool
+    any_breakdown: bool
+    wall_ms_total: float
+    per_iteration_ms: float
+    iterations: np.ndarray
+    converged: np.ndarray
+    breakdown: np.ndarray
+    residuals: List[np.ndarray]
+
+
+def run_solve_experiment(matrix: "BlockedSparseMatrix", m: Optional[SplitPreconditioner], cfg: SolveConfig,
+                         method_name: str, device: int = 0) -> SolveReport:
+    """run_solve_experiment (solver.hpp:368-416): CG / split-preconditioned CG
+    on cfg.rhs_count seeded unit-norm right-hand sides, all advanced together
+    on the GPU; residual traces aggregated as the reference does."""
+    lib = library()
+    coo, keep = matrix.coo(device)
+    c = abi.SolveConfig(float(cfg.tol), int(cfg.max_iter), int(cfg.rhs_count), int(cfg.seed))
+    nr = int(cfg.rhs_count)
+    it = np.zeros(nr, np.int32)
+    cv = np.zeros(nr, np.int32)
+    bk = np.zeros(nr, np.int32)
+    tr = np.zeros((nr, int(cfg.max_iter) + 1))
+    wall = ctypes.c_double()
+    err = lib.errbuf()
+    abi.raise_for(lib.solve_precond(ctypes.byref(coo), m.handle if m is not None else None, ctypes.byref(c),
+                                    it.ctypes.data_as(abi.c_i32p), cv.ctypes.data_as(abi.c_i32p),
+                                    bk.ctypes.data_as(abi.c_i32p), tr.ctypes.data_as(abi.c_f64p), ctypes.byref(wall),
+                                    err, len(err)), err)
+    runs = [tr[r, : it[r] + 1].copy() for r in range(nr)]
+    longest = max(len(x) for x in runs)
+    ext = np.array([np.concatenate([x, np.full(longest - len(x), x[-1])]) for x in runs])
+    total = int(it.sum())
+    return SolveReport(method=method_name, mean_residual=ext.mean(axis=0), std_residual=ext.std(axis=0),
+                       mean_iterations=total / nr, max_iterations_used=int(it.max()), all_converged=bool(cv.all()),
+                       any_breakdown=bool(bk.any()), wall_ms_total=wall.value,
+                       per_iteration_ms=wall.value / total if total else 0.0, iterations=it, converged=cv.astype(bool),
+                       breakdown=bk.astype(bool), residuals=runs)
+
+
+@dataclass
+class NystromResult:
+    """NystromResult (transform_ops.hpp:252-255)."""
+    frobenius_error: float
+    columns: np.ndarray
+
+
+def nystrom_uniform(matrix: "BlockedSparseMatrix", m: int, seed: int, cap: int = 4096,
+                    device: int = 0) -> NystromResult:
+    """nystrom_uniform (transform_ops.hpp:259-307) evaluated densely on the GPU."""
+    lib = library()
+    coo, keep = matrix.coo(device)
+    fro = ctypes.c_double()
+    cols = np.zeros(max(int(m), 1), np.int64)
+    err = lib.errbuf()
+    abi.raise_for(lib.nystrom_uniform(ctypes.byref(coo), int(m), int(seed), int(cap), ctypes.byref(fro),
+                                      cols.ctypes.data_as(abi.c_i64p), err, len(err)), err)
+    return NystromResult(fro.value, cols[: int(m)])
+
+
 # --------------------------------------------------------------- input path
 _IO: Optional[abi.IoAbi] = None
 

@@ -1221,9 +1221,15 @@ int persistent_blocks() {
   return nb;
 }
 
+// Opt-in (PMMF_B200_LEVEL_LOOP=1).  Measured on config 4 (gpurun_out r02b,
+// DESIGN.md §9): the loop wins only on the small late stages (launch-bound
+// levels, stages 11-15: 16.6 -> 10.8 ms) and loses 2x on the large ones
+// (stage 1 row-pass levels 142 -> 333 ms): with a static item stride the
+// partitions' look-back chains tie the warps' rounds together, so one heavy
+// rotation stalls every later item.
 inline bool level_loop_enabled() {
   const char* e = std::getenv("PMMF_B200_LEVEL_LOOP");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 // Co-resident grid of the level loop (cooperative launch).

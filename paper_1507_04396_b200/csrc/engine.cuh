@@ -51,9 +51,11 @@ struct Numbering {
 // ---- matrix.cu
 // from_triplets (blocked_matrix.hpp:138-156) on the device: validates in
 // input order, stable-sorts by (col,row), sums duplicates in input order,
-// drops exact zeros.  rows/cols/vals are device pointers.
+// drops exact zeros unless keep_zeros (the reference stores them; only the
+// preconditioners' patterns see the difference).  rows/cols/vals are device
+// pointers.
 void csc_from_coo(Csc& out, const Numbering& nb, i64 n, i64 nnz, const int64_t* rows, const int64_t* cols,
-                  const double* vals, cudaStream_t s);
+                  const double* vals, cudaStream_t s, bool keep_zeros = false);
 // max_asymmetry (blocked_matrix.hpp:447-463) and frobenius_norm_sq.
 void csc_symmetry(const Csc& a, const Numbering& nb, double* max_asym, double* fro_sq, cudaStream_t s);
 // Paged view of a contiguous matrix (takes ownership of its arrays).

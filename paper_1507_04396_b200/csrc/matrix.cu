@@ -61,7 +61,7 @@ __global__ void k_coo_keys(i64 n, i64 nnz, const int64_t* __restrict__ rows, con
 
 // Sum runs of equal keys in their (stable) order; flag the kept heads.
 __global__ void k_sum_dups(i64 m, const uint64_t* __restrict__ keys, const double* __restrict__ vals,
-                           double* __restrict__ sums, int32_t* __restrict__ keep) {
+                           double* __restrict__ sums, int32_t* __restrict__ keep, bool keep_zeros) {
   const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (i >= m) return;
   if (i > 0 && keys[i - 1] == keys[i]) {
@@ -71,7 +71,7 @@ __global__ void k_sum_dups(i64 m, const uint64_t* __restrict__ keys, const doubl
   double s = vals[i];
   for (i64 j = i + 1; j < m && keys[j] == keys[i]; ++j) s = dadd(s, vals[j]);
   sums[i] = s;
-  keep[i] = s != 0.0 ? 1 : 0;
+  keep[i] = (keep_zeros || s != 0.0) ? 1 : 0;
 }
 
 __global__ void k_scatter_kept(i64 m, const uint64_t* __restrict__ keys, const double* __restrict__ sums,
@@ -343,7 +343,7 @@ void Numbering::build(const std::vector<std::vector<i64>>& cls, i64 n, cudaStrea
 }
 
 void csc_from_coo(Csc& out, const Numbering& nb, i64 n, i64 nnz, const int64_t* rows, const int64_t* cols,
-                  const double* vals, cudaStream_t s) {
+                  const double* vals, cudaStream_t s, bool keep_zeros) {
   const i64 N = nb.size();
   out.N = N;
   DBuf<int32_t> g2s(std::max<i64>(n, 1), s);
@@ -373,7 +373,8 @@ void csc_from_coo(Csc& out, const Numbering& nb, i64 n, i64 nnz, const int64_t* 
   DBuf<int32_t> keep(nnz + 1, s);
   DBuf<i64> keep64(nnz + 1, s), pos(nnz + 1, s);
   keep.zero();
-  PMMF_LAUNCH(k_sum_dups, blocks_for(nnz, kThreads), kThreads, 0, s, nnz, keys.get(), v.get(), sums.get(), keep.get());
+  PMMF_LAUNCH(k_sum_dups, blocks_for(nnz, kThreads), kThreads, 0, s, nnz, keys.get(), v.get(), sums.get(), keep.get(),
+              keep_zeros);
   // widen flags to int64 and scan
   PMMF_LAUNCH(k_len64, blocks_for(nnz + 1, kThreads), kThreads, 0, s, nnz, keep.get(), keep64.get());
   exclusive_scan(keep64.get(), pos.get(), nnz + 1, s);

@@ -21,6 +21,7 @@
 #include <string>
 
 #include "engine.cuh"
+#include "precond.cuh"
 #include "result.cuh"
 #include "rng.cuh"
 #include "rotation.cuh"
@@ -835,6 +836,208 @@ __global__ void k_cg_rr(int nrhs, const int32_t* __restrict__ active, const doub
 }
 
 }  // namespace
+
+void eigensystem_dev(int g, const double* a, double* values, double* vectors, cudaStream_t s) {
+  if (g <= 0) return;
+  DBuf<double> wa, wq;
+  if (g > kEigSmemMax) {
+    wa.alloc(static_cast<int64_t>(g) * g, s);
+    wq.alloc(static_cast<int64_t>(g) * g, s);
+  }
+  const int threads = g <= 32 ? 32 : (g <= kEigSmemMax ? 64 : 256);
+  PMMF_LAUNCH(k_core_eig, 1, threads, 0, s, g, a, wa.get(), wq.get(), values, vectors);
+  PMMF_CUDA(cudaStreamSynchronize(s));
+}
+
+namespace {
+// pmmf_preconditioner (solver.hpp:343-349): both sides are apply(inv_sqrt).
+struct OpPrecond : SplitPrecond {
+  const Operator* op = nullptr;
+  void apply(int, int nr, const double* in, double* out, cudaStream_t s) override {
+    PMMF_CUDA(cudaMemcpyAsync(out, in, sizeof(double) * n * nr, cudaMemcpyDeviceToDevice, s));
+    op->apply_dev(PMMF_APPLY_INV_SQRT, nr, out, s);
+  }
+};
+}  // namespace
+
+std::unique_ptr<SplitPrecond> precond_from_operator(void* opv) {
+  const auto* o = static_cast<const Operator*>(opv);
+  PMMF_CUDA(cudaSetDevice(o->device));
+  auto p = std::make_unique<OpPrecond>();
+  p->kind = PMMF_PRECOND_PMMF;
+  p->op = o;
+  p->n = o->n;
+  p->device = o->device;
+  return p;
+}
+
+// run_solve_experiment (solver.hpp:368-416) over pcg_symmetric
+// (solver.hpp:112-167): all rhs_count right-hand sides advance together.
+void run_cg(const pmmf_b200_coo* a, SplitPrecond* pc, const pmmf_b200_solve_config* cfg, int32_t* iterations,
+            int32_t* converged, int32_t* breakdown, double* residuals, double* wall_ms) {
+    if (!(cfg->tol > 0.0)) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: tol must be positive");
+    if (cfg->max_iter < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: max_iter < 1");
+    if (cfg->rhs_count < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: rhs_count < 1");
+    if (cfg->rhs_count > 1024) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: rhs_count > 1024 unsupported");
+    PMMF_CUDA(cudaSetDevice(a->device));
+    cudaStream_t s;
+    PMMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    struct SG {
+      cudaStream_t s;
+      ~SG() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    } sg{s};
+    const auto start = std::chrono::steady_clock::now();
+    const int64_t n = a->n;
+    const int nr = cfg->rhs_count;
+    if (pc && pc->n != n) fail(PMMF_INVALID_ARGUMENT, "pcg_symmetric: operator dimension mismatch");
+    if (pc && pc->device != a->device) fail(PMMF_INVALID_ARGUMENT, "pcg_symmetric: preconditioner on another device");
+    // Matrix rows in input-partition order for y = A x.
+    Numbering nb;
+    {
+      std::vector<std::vector<int64_t>> init;
+      if (a->n_clusters == 0) {
+        init.emplace_back(static_cast<size_t>(n));
+        std::iota(init[0].begin(), init[0].end(), int64_t{0});
+      } else {
+        for (int64_t u = 0; u < a->n_clusters; ++u)
+          init.emplace_back(a->cluster_members + a->cluster_offsets[u], a->cluster_members + a->cluster_offsets[u + 1]);
+      }
+      nb.build(init, n, s);
+    }
+    Csc A;
+    {
+      const int64_t* rows = a->rows;
+      const int64_t* cols = a->cols;
+      const double* vals = a->vals;
+      DBuf<int64_t> dr, dc;
+      DBuf<double> dv;
+      if (!a->on_device && a->nnz > 0) {
+        dr.alloc(a->nnz, s);
+        dc.alloc(a->nnz, s);
+        dv.alloc(a->nnz, s);
+        dr.upload(a->rows, a->nnz);
+        dc.upload(a->cols, a->nnz);
+        dv.upload(a->vals, a->nnz);
+        rows = dr.get();
+        cols = dc.get();
+        vals = dv.get();
+      }
+      csc_from_coo(A, nb, n, a->nnz, rows, cols, vals, s);
+    }
+    Csc Arow;  // transpose: per row (stage id), columns ascending in stage order
+    {
+      Paged P;
+      const int64_t nz = A.nnz;
+      paged_from_csc(P, std::move(A), 1, s);
+      (void)nz;
+      transpose_paged(Arow, P, s);
+    }
+    // right-hand sides (solver.hpp:375-381), bnorm on the host in order
+    std::vector<double> hb(static_cast<size_t>(n * nr)), bimaj(static_cast<size_t>(n * nr)), bn(static_cast<size_t>(nr));
+    for (int r = 0; r < nr; ++r) {
+      const uint64_t path[2] = {0xB0u, static_cast<uint64_t>(r)};
+      Xoshiro rng(derive(cfg->seed, path));
+      double* b = hb.data() + static_cast<int64_t>(r) * n;
+      for (int64_t i = 0; i < n; ++i) b[i] = normal_draw(rng);
+      double sq = 0.0;
+      for (int64_t i = 0; i < n; ++i) sq += b[i] * b[i];
+      const double norm = std::sqrt(sq);
+      if (norm > 0.0)
+        for (int64_t i = 0; i < n; ++i) b[i] /= norm;
+      double s2 = 0.0;
+      for (int64_t i = 0; i < n; ++i) s2 += b[i] * b[i];
+      bn[r] = std::sqrt(s2);
+      for (int64_t i = 0; i < n; ++i) bimaj[i * nr + r] = b[i];
+    }
+    const int stride = cfg->max_iter + 1;
+    for (int64_t i = 0; i < static_cast<int64_t>(nr) * stride; ++i) residuals[i] = NAN;
+    std::vector<int32_t> act(static_cast<size_t>(nr), 1), zero(static_cast<size_t>(nr), 0);
+    for (int r = 0; r < nr; ++r) {
+      residuals[static_cast<int64_t>(r) * stride] = bn[r];
+      iterations[r] = 0;
+      converged[r] = 0;
+      breakdown[r] = 0;
+      if (bn[r] == 0.0) {
+        converged[r] = 1;
+        act[r] = 0;
+      }
+    }
+    const int64_t m = n * nr;
+    DBuf<double> B(m, s), Y(m, s), Rv(m, s), Pv(m, s), W(m, s), T1(m, s), T2(m, s), X(m, s);
+    B.upload(bimaj);
+    Y.zero();
+    DBuf<double> part(static_cast<int64_t>(kDotBlocks) * nr, s);
+    DBuf<double> rr(nr, s), pap(nr, s), res(nr, s), rrn(nr, s), alpha(nr, s), dbn(nr, s);
+    DBuf<int32_t> dact(nr, s), diters(nr, s), dconv(nr, s), dbrk(nr, s);
+    DBuf<double> trace(static_cast<int64_t>(nr) * stride, s);
+    dbn.upload(bn);
+    dact.upload(act);
+    diters.upload(zero);
+    dconv.upload(zero);
+    dbrk.upload(zero);
+    trace.fill_bytes(0xff);  // NaN pattern
+    // side 0: K^-1, side 1: K^-T (identity_preconditioner when pc is null)
+    auto pre = [&](int side, const DBuf<double>& in, DBuf<double>& out) {
+      if (pc)
+        pc->apply(side, nr, in.get(), out.get(), s);
+      else
+        PMMF_CUDA(cudaMemcpyAsync(out.get(), in.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    };
+    auto spmv = [&](const DBuf<double>& x, DBuf<double>& y) {
+      y.zero();
+      PMMF_LAUNCH(k_spmv, blocks_for(Arow.N * 32, kThreads), kThreads, 0, s, Arow.N, nr, Arow.ptr.get(), Arow.row.get(),
+                  Arow.val.get(), nb.d_s2g.get(), x.get(), y.get());
+    };
+    auto dot = [&](const DBuf<double>& x, const DBuf<double>& y, DBuf<double>& out) {
+      PMMF_LAUNCH(k_dot_partial, kDotBlocks, kThreads, 0, s, n, nr, x.get(), y.get(), part.get());
+      PMMF_LAUNCH(k_dot_final, 1, std::max(32, ((nr + 31) / 32) * 32), 0, s, nr, kDotBlocks, part.get(), out.get());
+    };
+    CgState S{rr.get(), pap.get(), res.get(), rrn.get(), alpha.get(), dbn.get(), dact.get(), diters.get(),
+              dconv.get(), dbrk.get(), trace.get(), stride, cfg->tol};
+    const int th = std::max(32, ((nr + 31) / 32) * 32);
+    pre(0, B, Rv);  // r = K^-1 b
+    PMMF_CUDA(cudaMemcpyAsync(Pv.get(), Rv.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    dot(Rv, Rv, rr);
+    for (int it = 1; it <= cfg->max_iter; ++it) {
+      pre(1, Pv, T1);
+      spmv(T1, T2);
+      pre(0, T2, W);
+      dot(Pv, W, pap);
+      PMMF_LAUNCH(k_cg_alpha, 1, th, 0, s, nr, S);
+      PMMF_LAUNCH(k_cg_update, blocks_for(m, kThreads), kThreads, 0, s, n, nr, dact.get(), alpha.get(), Pv.get(),
+                  W.get(), Y.get(), Rv.get());
+      pre(1, Y, X);
+      spmv(X, T2);
+      PMMF_LAUNCH(k_sub, blocks_for(m, kThreads), kThreads, 0, s, m, B.get(), T2.get(), T1.get());
+      dot(T1, T1, res);
+      PMMF_LAUNCH(k_cg_check, 1, th, 0, s, nr, it, S);
+      dot(Rv, Rv, rrn);
+      PMMF_LAUNCH(k_cg_beta, blocks_for(m, kThreads), kThreads, 0, s, n, nr, dact.get(), rrn.get(), rr.get(), Rv.get(),
+                  Pv.get());
+      PMMF_LAUNCH(k_cg_rr, 1, th, 0, s, nr, dact.get(), rrn.get(), rr.get());
+      if (it % 8 == 0 || it == cfg->max_iter) {
+        std::vector<int32_t> h = dact.to_host(nr);
+        bool any = false;
+        for (int r = 0; r < nr; ++r) any |= h[r] != 0;
+        if (!any) break;
+      }
+    }
+    std::vector<int32_t> hi = diters.to_host(nr), hc = dconv.to_host(nr), hbk = dbrk.to_host(nr);
+    std::vector<double> ht = trace.to_host(static_cast<int64_t>(nr) * stride);
+    for (int r = 0; r < nr; ++r) {
+      if (bn[r] == 0.0) continue;
+      iterations[r] = hi[r];
+      converged[r] = hc[r];
+      breakdown[r] = hbk[r];
+      for (int i = 1; i < stride; ++i) residuals[static_cast<int64_t>(r) * stride + i] = ht[static_cast<int64_t>(r) * stride + i];
+    }
+    *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+
+}
+
 }  // namespace pmmf_b200
 
 using namespace pmmf_b200;
@@ -952,163 +1155,10 @@ int pmmf_b200_solve(const pmmf_b200_coo* a, void* opv, const pmmf_b200_solve_con
                     int32_t* converged, int32_t* breakdown, double* residuals, double* wall_ms, char* err,
                     size_t errlen) {
   return guarded(err, errlen, [&] {
-    if (!(cfg->tol > 0.0)) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: tol must be positive");
-    if (cfg->max_iter < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: max_iter < 1");
-    if (cfg->rhs_count < 1) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: rhs_count < 1");
-    if (cfg->rhs_count > 1024) fail(PMMF_INVALID_ARGUMENT, "SolveConfig: rhs_count > 1024 unsupported");
-    auto* o = static_cast<Operator*>(opv);
-    PMMF_CUDA(cudaSetDevice(a->device));
-    cudaStream_t s;
-    PMMF_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    struct SG {
-      cudaStream_t s;
-      ~SG() {
-        cudaStreamSynchronize(s);
-        cudaStreamDestroy(s);
-      }
-    } sg{s};
-    const auto start = std::chrono::steady_clock::now();
-    const int64_t n = a->n;
-    const int nr = cfg->rhs_count;
-    if (o && o->n != n) fail(PMMF_INVALID_ARGUMENT, "pcg_symmetric: operator dimension mismatch");
-    // Matrix rows in input-partition order for y = A x.
-    Numbering nb;
-    {
-      std::vector<std::vector<int64_t>> init;
-      if (a->n_clusters == 0) {
-        init.emplace_back(static_cast<size_t>(n));
-        std::iota(init[0].begin(), init[0].end(), int64_t{0});
-      } else {
-        for (int64_t u = 0; u < a->n_clusters; ++u)
-          init.emplace_back(a->cluster_members + a->cluster_offsets[u], a->cluster_members + a->cluster_offsets[u + 1]);
-      }
-      nb.build(init, n, s);
-    }
-    Csc A;
-    {
-      const int64_t* rows = a->rows;
-      const int64_t* cols = a->cols;
-      const double* vals = a->vals;
-      DBuf<int64_t> dr, dc;
-      DBuf<double> dv;
-      if (!a->on_device && a->nnz > 0) {
-        dr.alloc(a->nnz, s);
-        dc.alloc(a->nnz, s);
-        dv.alloc(a->nnz, s);
-        dr.upload(a->rows, a->nnz);
-        dc.upload(a->cols, a->nnz);
-        dv.upload(a->vals, a->nnz);
-        rows = dr.get();
-        cols = dc.get();
-        vals = dv.get();
-      }
-      csc_from_coo(A, nb, n, a->nnz, rows, cols, vals, s);
-    }
-    Csc Arow;  // transpose: per row (stage id), columns ascending in stage order
-    {
-      Paged P;
-      const int64_t nz = A.nnz;
-      paged_from_csc(P, std::move(A), 1, s);
-      (void)nz;
-      transpose_paged(Arow, P, s);
-    }
-    // right-hand sides (solver.hpp:375-381), bnorm on the host in order
-    std::vector<double> hb(static_cast<size_t>(n * nr)), bimaj(static_cast<size_t>(n * nr)), bn(static_cast<size_t>(nr));
-    for (int r = 0; r < nr; ++r) {
-      const uint64_t path[2] = {0xB0u, static_cast<uint64_t>(r)};
-      Xoshiro rng(derive(cfg->seed, path));
-      double* b = hb.data() + static_cast<int64_t>(r) * n;
-      for (int64_t i = 0; i < n; ++i) b[i] = normal_draw(rng);
-      double sq = 0.0;
-      for (int64_t i = 0; i < n; ++i) sq += b[i] * b[i];
-      const double norm = std::sqrt(sq);
-      if (norm > 0.0)
-        for (int64_t i = 0; i < n; ++i) b[i] /= norm;
-      double s2 = 0.0;
-      for (int64_t i = 0; i < n; ++i) s2 += b[i] * b[i];
-      bn[r] = std::sqrt(s2);
-      for (int64_t i = 0; i < n; ++i) bimaj[i * nr + r] = b[i];
-    }
-    const int stride = cfg->max_iter + 1;
-    for (int64_t i = 0; i < static_cast<int64_t>(nr) * stride; ++i) residuals[i] = NAN;
-    std::vector<int32_t> act(static_cast<size_t>(nr), 1), zero(static_cast<size_t>(nr), 0);
-    for (int r = 0; r < nr; ++r) {
-      residuals[static_cast<int64_t>(r) * stride] = bn[r];
-      iterations[r] = 0;
-      converged[r] = 0;
-      breakdown[r] = 0;
-      if (bn[r] == 0.0) {
-        converged[r] = 1;
-        act[r] = 0;
-      }
-    }
-    const int64_t m = n * nr;
-    DBuf<double> B(m, s), Y(m, s), Rv(m, s), Pv(m, s), W(m, s), T1(m, s), T2(m, s), X(m, s);
-    B.upload(bimaj);
-    Y.zero();
-    DBuf<double> part(static_cast<int64_t>(kDotBlocks) * nr, s);
-    DBuf<double> rr(nr, s), pap(nr, s), res(nr, s), rrn(nr, s), alpha(nr, s), dbn(nr, s);
-    DBuf<int32_t> dact(nr, s), diters(nr, s), dconv(nr, s), dbrk(nr, s);
-    DBuf<double> trace(static_cast<int64_t>(nr) * stride, s);
-    dbn.upload(bn);
-    dact.upload(act);
-    diters.upload(zero);
-    dconv.upload(zero);
-    dbrk.upload(zero);
-    trace.fill_bytes(0xff);  // NaN pattern
-    auto pre = [&](const DBuf<double>& in, DBuf<double>& out) {
-      PMMF_CUDA(cudaMemcpyAsync(out.get(), in.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
-      if (o) o->apply_dev(PMMF_APPLY_INV_SQRT, nr, out.get(), s);
-    };
-    auto spmv = [&](const DBuf<double>& x, DBuf<double>& y) {
-      y.zero();
-      PMMF_LAUNCH(k_spmv, blocks_for(Arow.N * 32, kThreads), kThreads, 0, s, Arow.N, nr, Arow.ptr.get(), Arow.row.get(),
-                  Arow.val.get(), nb.d_s2g.get(), x.get(), y.get());
-    };
-    auto dot = [&](const DBuf<double>& x, const DBuf<double>& y, DBuf<double>& out) {
-      PMMF_LAUNCH(k_dot_partial, kDotBlocks, kThreads, 0, s, n, nr, x.get(), y.get(), part.get());
-      PMMF_LAUNCH(k_dot_final, 1, std::max(32, ((nr + 31) / 32) * 32), 0, s, nr, kDotBlocks, part.get(), out.get());
-    };
-    CgState S{rr.get(), pap.get(), res.get(), rrn.get(), alpha.get(), dbn.get(), dact.get(), diters.get(),
-              dconv.get(), dbrk.get(), trace.get(), stride, cfg->tol};
-    const int th = std::max(32, ((nr + 31) / 32) * 32);
-    pre(B, Rv);  // r = K^-1 b
-    PMMF_CUDA(cudaMemcpyAsync(Pv.get(), Rv.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
-    dot(Rv, Rv, rr);
-    for (int it = 1; it <= cfg->max_iter; ++it) {
-      pre(Pv, T1);
-      spmv(T1, T2);
-      pre(T2, W);
-      dot(Pv, W, pap);
-      PMMF_LAUNCH(k_cg_alpha, 1, th, 0, s, nr, S);
-      PMMF_LAUNCH(k_cg_update, blocks_for(m, kThreads), kThreads, 0, s, n, nr, dact.get(), alpha.get(), Pv.get(),
-                  W.get(), Y.get(), Rv.get());
-      pre(Y, X);
-      spmv(X, T2);
-      PMMF_LAUNCH(k_sub, blocks_for(m, kThreads), kThreads, 0, s, m, B.get(), T2.get(), T1.get());
-      dot(T1, T1, res);
-      PMMF_LAUNCH(k_cg_check, 1, th, 0, s, nr, it, S);
-      dot(Rv, Rv, rrn);
-      PMMF_LAUNCH(k_cg_beta, blocks_for(m, kThreads), kThreads, 0, s, n, nr, dact.get(), rrn.get(), rr.get(), Rv.get(),
-                  Pv.get());
-      PMMF_LAUNCH(k_cg_rr, 1, th, 0, s, nr, dact.get(), rrn.get(), rr.get());
-      if (it % 8 == 0 || it == cfg->max_iter) {
-        std::vector<int32_t> h = dact.to_host(nr);
-        bool any = false;
-        for (int r = 0; r < nr; ++r) any |= h[r] != 0;
-        if (!any) break;
-      }
-    }
-    std::vector<int32_t> hi = diters.to_host(nr), hc = dconv.to_host(nr), hbk = dbrk.to_host(nr);
-    std::vector<double> ht = trace.to_host(static_cast<int64_t>(nr) * stride);
-    for (int r = 0; r < nr; ++r) {
-      if (bn[r] == 0.0) continue;
-      iterations[r] = hi[r];
-      converged[r] = hc[r];
-      breakdown[r] = hbk[r];
-      for (int i = 1; i < stride; ++i) residuals[static_cast<int64_t>(r) * stride + i] = ht[static_cast<int64_t>(r) * stride + i];
-    }
-    *wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - start).count();
+    if (!a || !cfg) fail(PMMF_INVALID_ARGUMENT, "solve: null argument");
+    std::unique_ptr<SplitPrecond> pc;
+    if (opv) pc = precond_from_operator(opv);
+    run_cg(a, pc.get(), cfg, iterations, converged, breakdown, residuals, wall_ms);
   });
 }
 

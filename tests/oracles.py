@@ -163,3 +163,70 @@ def solve(which, inp, params, tol, max_iter, rhs_count, seed, precondition=True)
         if precondition:
             lib.operator_free(op)
     return it, cv, bk, tr, wall.value
+
+
+# ---- comparison preconditioners and Nystrom (solver.hpp:222-349, transform_ops.hpp:252-307)
+PRECOND = {"none": 0, "jacobi": 1, "ssor": 2, "ic": 3, "pmmf": 4}
+
+
+def precond_apply(which, inp, kind, vecs, side, omega=1.0, part=None):
+    """K^-1 (side 0) or K^-T (side 1) of a comparison preconditioner on the
+    rows of `vecs`; returns (out, (kind, compensated, alpha))."""
+    lib = load(which)
+    n, rows, cols, vals = inp
+    coo, keep = abi.make_coo(n, rows, cols, vals, clusters=part)
+    err = lib.errbuf()
+    pc = ctypes.c_void_p()
+    abi.raise_for(lib.precond_create(ctypes.byref(coo), PRECOND[kind], omega, ctypes.byref(pc), err, len(err)), err)
+    try:
+        vecs = np.ascontiguousarray(vecs, dtype=np.float64)
+        out = np.zeros_like(vecs)
+        abi.raise_for(lib.precond_apply(pc, side, vecs.shape[0], vecs.ctypes.data, out.ctypes.data, 0, err, len(err)),
+                      err)
+        k, c, a = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+        lib.precond_info(pc, ctypes.byref(k), ctypes.byref(c), ctypes.byref(a))
+        return out, (k.value, c.value, a.value)
+    finally:
+        lib.precond_free(pc)
+
+
+def solve_precond(which, inp, kind, tol, max_iter, rhs_count, seed, omega=1.0):
+    """run_solve_experiment with a comparison preconditioner (kind "none" =
+    plain CG): returns (iters, conv, brk, traces, wall_ms)."""
+    lib = load(which)
+    n, rows, cols, vals = inp
+    coo, keep = abi.make_coo(n, rows, cols, vals)
+    err = lib.errbuf()
+    pc = ctypes.c_void_p()
+    if kind != "none":
+        abi.raise_for(lib.precond_create(ctypes.byref(coo), PRECOND[kind], omega, ctypes.byref(pc), err, len(err)),
+                      err)
+    cfg = abi.SolveConfig(tol, max_iter, rhs_count, seed)
+    it = np.zeros(rhs_count, np.int32)
+    cv = np.zeros(rhs_count, np.int32)
+    bk = np.zeros(rhs_count, np.int32)
+    tr = np.zeros((rhs_count, max_iter + 1))
+    wall = ctypes.c_double()
+    try:
+        abi.raise_for(
+            lib.solve_precond(ctypes.byref(coo), pc if kind != "none" else None, ctypes.byref(cfg),
+                              it.ctypes.data_as(abi.c_i32p), cv.ctypes.data_as(abi.c_i32p),
+                              bk.ctypes.data_as(abi.c_i32p), tr.ctypes.data_as(abi.c_f64p), ctypes.byref(wall), err,
+                              len(err)), err)
+    finally:
+        if kind != "none":
+            lib.precond_free(pc)
+    return it, cv, bk, tr, wall.value
+
+
+def nystrom(which, inp, m, seed, cap=4096, part=None):
+    """nystrom_uniform: returns (frobenius_error, columns)."""
+    lib = load(which)
+    n, rows, cols, vals = inp
+    coo, keep = abi.make_coo(n, rows, cols, vals, clusters=part)
+    err = lib.errbuf()
+    fro = ctypes.c_double()
+    sel = np.zeros(max(int(m), 1), np.int64)
+    abi.raise_for(lib.nystrom_uniform(ctypes.byref(coo), m, seed, cap, ctypes.byref(fro),
+                                      sel.ctypes.data_as(abi.c_i64p), err, len(err)), err)
+    return fro.value, sel[:m]

@@ -80,3 +80,18 @@ def test_score_gemm_path(name, gemm, monkeypatch):
     monkeypatch.setenv("PMMF_B200_SCORE_GEMM", gemm)
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf512_k4", "k3_sparse",
+                                  "partitioned_input"])
+@pytest.mark.parametrize("batch", ["0", "2000"])
+def test_level_loop_path(name, batch, monkeypatch):
+    """The opt-in persistent level loop (one cooperative launch per batch,
+    partitions ordered by a decoupled look-back) — bit-exact, also with many
+    batches and arena compactions."""
+    monkeypatch.setenv("PMMF_B200_LEVEL_LOOP", "1")
+    if batch != "0":
+        monkeypatch.setenv("PMMF_B200_BATCH_NNZ", batch)
+        monkeypatch.setenv("PMMF_B200_MERGE_CHUNK", "32")
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
