@@ -332,6 +332,70 @@ def time_mmf_apply(lib, coo_dev, params, err, n):
     return out
 
 
+def cg_block(lib, coo_dev, params, err, cpu_threads):
+    """Config 5's CG (run_solve_experiment + pmmf_preconditioner, solver.hpp:
+    343-416; SURVEY.md §8(d) "CG time per iteration on the same RHS set"):
+      * GPU at full size: 20 seeded rhs, tol 1e-8, a bounded 400 iterations
+        (convergence takes ~5,500; per-iteration time is the metric);
+      * the reference (oracle/_ref, all host threads, rhs in parallel as its
+        run_solve_experiment does) and the GPU on the 256^2 sample to
+        convergence: same input, same rhs set.
+    per_iteration_ms = wall / sum of iterations over the rhs (the reference's
+    SolveReport::per_iteration_ms), plus the batched GPU figure
+    wall / max iterations (all 20 rhs advance together)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import oracles
+    from paper_1507_04396_b200 import abi
+
+    def run(which, handle_lib, coo, op, nr, max_iter):
+        cfg = abi.SolveConfig(1e-8, max_iter, nr, 0)
+        it = np.zeros(nr, np.int32)
+        cv = np.zeros(nr, np.int32)
+        bk = np.zeros(nr, np.int32)
+        tr = np.zeros((nr, max_iter + 1))
+        wall = ctypes.c_double()
+        e = handle_lib.errbuf()
+        abi.raise_for(handle_lib.solve(ctypes.byref(coo), op, ctypes.byref(cfg), it.ctypes.data_as(abi.c_i32p),
+                                       cv.ctypes.data_as(abi.c_i32p), bk.ctypes.data_as(abi.c_i32p),
+                                       tr.ctypes.data_as(abi.c_f64p), ctypes.byref(wall), e, len(e)), e)
+        tot = int(it.sum())
+        return {"impl": which, "rhs": nr, "iterations_mean": float(it.mean()), "iterations_max": int(it.max()),
+                "converged": int(cv.sum()), "wall_ms": wall.value,
+                "per_iteration_ms": wall.value / tot if tot else None,
+                "batched_iteration_ms": wall.value / int(it.max()) if it.max() else None,
+                "final_rel_residual_mean": float(np.mean([tr[r, it[r]] / tr[r, 0] for r in range(nr)]))}
+
+    out = {}
+    h = ctypes.c_void_p()
+    abi.raise_for(lib.factorize(ctypes.byref(coo_dev), ctypes.byref(params), ctypes.byref(h), err, len(err)), err)
+    op = ctypes.c_void_p()
+    abi.raise_for(lib.operator_create(h, 1e-12, ctypes.byref(op), err, len(err)), err)
+    lib.result_free(h)
+    # full size: the triplets on the device (the solve builds its CSR there)
+    out["gpu_full_1024x1024"] = run("gpu", lib, coo_dev, op, 20, 400)
+    out["gpu_full_1024x1024"]["note"] = "bounded at 400 iterations (full convergence ~5,500)"
+    lib.operator_free(op)
+    # 256^2 sample, both arms, to convergence
+    inp = ref_workload(0, "c5s")
+    p = config_params("c5s")
+    for which in ("ref", "gpu"):
+        L = oracles.load(which)
+        if which == "ref":
+            L.lib.pmmf_ref_set_threads(cpu_threads)
+        _, hh = oracles.result_handle(which, inp, p)
+        o = ctypes.c_void_p()
+        e = L.errbuf()
+        abi.raise_for(L.operator_create(hh, 1e-12, ctypes.byref(o), e, len(e)), e)
+        L.result_free(hh)
+        coo, keep = abi.make_coo(*inp)
+        r = run(which, L, coo, o, 20, 5000)
+        L.operator_free(o)
+        out[f"{which}_256x256"] = r
+    out["cores"] = cpu_threads
+    out["cpu_model"] = cpu_model()
+    return out
+
+
 def like_for_like(lib, inp, cw, cpu_rots, cpu_s, err, steps=5):
     """The GPU on the reference's exact sample input (same triplets, same
     params): e2e through the C-ABI with host buffers (H2D of the triplets and
@@ -492,6 +556,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clk = clocks.stop()
+    timed_phases = last_phases.copy()
     # roofline pass: one untimed step with the per-launch CUDA events on
     L.pmmf_b200_profile_enable(1)
     prof_step_ms = time.perf_counter()
@@ -550,8 +615,15 @@ def main():
                 "share_of_step": ms / prof_step_ms, "write_pass": roof}
 
     apply = None
+    cg = None
     if args.workload == "c5":
         apply = time_mmf_apply(lib, coo_dev, params, err, n)
+        if rank == 0 and not args.no_cpu_baseline:
+            try:
+                cg = cg_block(lib, coo_dev, params, err, os.cpu_count() or 1)
+            except Exception as e:  # the checker is optional on the box
+                import traceback
+                cg = {"unavailable": f"{e!r}: {traceback.format_exc()[-600:]}"}
 
     cpu, like = None, None
     if rank == 0 and not args.no_cpu_baseline:
@@ -579,10 +651,10 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": DATA,
                 "config": config_dict(args, W, n, len(vals), params, world), "rotations_per_step": int(rots),
                 "roofline": roof, "cpu_baseline": cpu, "like_for_like": like, "e2e": e2e, "gpu_launches": int(launches),
-                "mmf_apply": apply,
+                "mmf_apply": apply, "cg": cg,
                 "clocks": clk, "step_ms": step_ms,
                 "phases_ms_last_step": dict(zip(["clustering", "gram", "search", "apply", "reblock", "total"],
-                                                [round(float(x), 1) for x in last_phases]))}
+                                                [round(float(x), 1) for x in timed_phases]))}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

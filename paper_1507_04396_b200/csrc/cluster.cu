@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdio>
 #include <numeric>
+#include <unordered_map>
 
 #include "engine.cuh"
 #include "rng.cuh"
@@ -36,11 +37,12 @@ constexpr int kThreads = 256;
 // flushed into the outer sum at block changes) through shuffles.
 __global__ void k_norms(i64 P, const int32_t* __restrict__ cols, const i64* __restrict__ ptr,
                         const int32_t* __restrict__ row, const double* __restrict__ val,
-                        const int32_t* __restrict__ blk, double* __restrict__ norm) {
+                        const int32_t* __restrict__ blk, double* __restrict__ norm, i64 long_len) {
   const i64 p = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= P) return;
   const int32_t j = cols[p];
+  if (ptr[j + 1] - ptr[j] > long_len) return;  // k_norms_long
   double s = 0.0, inner = 0.0;
   int32_t cur = -1;
   const i64 e1 = ptr[j + 1];
@@ -67,6 +69,56 @@ __global__ void k_norms(i64 P, const int32_t* __restrict__ cols, const i64* __re
   }
   if (cur >= 0) s = dadd(s, inner);
   if (lane == 0) norm[p] = sqrt(s);
+}
+
+// Long columns (hub columns after a stage's fill-in: up to ~n/2 entries,
+// which one warp would sum serially for milliseconds): a CTA per column,
+// thread per pre-reblock block.  Block u's part of the column is the row
+// range [off[u], off[u+1]) (blocks are contiguous stage-id ranges, rows are
+// ascending), summed sequentially by its thread; the column norm then adds
+// the block sums in block order, empty blocks included, exactly as
+// column_norm_sq does (blocked_matrix.hpp:203-209, sparse.hpp:99-103).
+constexpr int kNormLongThreads = 256;
+__global__ void __launch_bounds__(kNormLongThreads) k_norms_long(const int32_t* __restrict__ list,
+                                                                 const int32_t* __restrict__ cols,
+                                                                 const i64* __restrict__ ptr,
+                                                                 const int32_t* __restrict__ row,
+                                                                 const double* __restrict__ val, const i64* __restrict__ off,
+                                                                 i64 nblk, double* __restrict__ part,
+                                                                 double* __restrict__ norm) {
+  const i64 p = list[blockIdx.x];
+  const int32_t j = cols[p];
+  const i64 e0 = ptr[j], e1 = ptr[j + 1];
+  double* my = part + static_cast<i64>(blockIdx.x) * nblk;
+  auto lb = [&](i64 key) {
+    i64 lo = e0, hi = e1;
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (row[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  for (i64 u = threadIdx.x; u < nblk; u += blockDim.x) {
+    const i64 b = lb(off[u]), e = lb(off[u + 1]);
+    double s = 0.0;
+    for (i64 x = b; x < e; ++x) {
+      const double v = val[x];
+      s = dadd(s, dmul(v, v));
+    }
+    my[u] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (i64 u = 0; u < nblk; ++u) s = dadd(s, my[u]);
+    norm[p] = sqrt(s);
+  }
+}
+
+__global__ void k_long_flags(i64 P, const int32_t* __restrict__ cols, const i64* __restrict__ ptr, i64 long_len,
+                             uint8_t* __restrict__ flag) {
+  const i64 p = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (p < P) flag[p] = ptr[cols[p] + 1] - ptr[cols[p]] > long_len ? 1 : 0;
 }
 
 // Row -> anchor index: count, then scatter (order inside a row is free:
@@ -621,31 +673,23 @@ struct Scorer {
     self.fill_bytes(0xff);
   }
 
-  // Scores of `pool` (stage ids) against `anchors` (stage ids, ascending
-  // global).  Assignment mode returns best anchor or -1 per pool column;
-  // rows mode returns the full P x m score table.
-  void run(const std::vector<int32_t>& pool, const std::vector<double>& pool_norm,
-           const std::vector<int32_t>& anchors, const std::vector<double>& anchor_norm, bool rows_mode,
-           std::vector<int32_t>* assign, std::vector<double>* rows) {
-    const i64 P = static_cast<i64>(pool.size());
-    const int m = static_cast<int>(anchors.size());
+  // Scores of the P pool columns `dpool` (stage ids, device) against the m
+  // `danch` (stage ids, ascending global; device).  Assignment mode writes
+  // the best anchor or -1 per pool column to assign_out (device); rows mode
+  // writes the full P x m score table to rows_out (device).
+  void run(const int32_t* dpool, const double* dpn, i64 P, const int32_t* danch, const double* dan, int m,
+           bool rows_mode, int32_t* assign_out, double* rows_out) {
     if (P == 0) return;
     const auto t_start = std::chrono::steady_clock::now();
-    DBuf<int32_t> dpool(P, s), danch(m, s);
-    DBuf<double> dpn(P, s), dan(m, s);
-    dpool.upload(pool);
-    dpn.upload(pool_norm);
-    danch.upload(anchors);
-    dan.upload(anchor_norm);
     if (gemm_mode()) {
-      run_gemm(P, m, dpool, dpn, danch, dan, rows_mode, assign, rows, t_start);
+      run_gemm(P, m, dpool, dpn, danch, dan, rows_mode, assign_out, rows_out, t_start);
       return;
     }
     // row -> anchor index
     DBuf<int32_t> cnt(a.N + 1, s), cursor(a.N + 1, s);
     cnt.zero();
     cursor.zero();
-    PMMF_LAUNCH(k_anchor_count, static_cast<unsigned>(m), 128, 0, s, m, danch.get(), a.ptr.get(), a.row.get(), cnt.get());
+    PMMF_LAUNCH(k_anchor_count, static_cast<unsigned>(m), 128, 0, s, m, danch, a.ptr.get(), a.row.get(), cnt.get());
     DBuf<i64> cnt64(a.N + 1, s), rptr(a.N + 1, s);
     PMMF_LAUNCH(k_widen, blocks_for(a.N + 1, kThreads), kThreads, 0, s, a.N, cnt.get(), cnt64.get());
     {
@@ -659,7 +703,7 @@ struct Scorer {
     PMMF_CUDA(cudaStreamSynchronize(s));
     DBuf<int32_t> ent_a(std::max<i64>(total, 1), s);
     DBuf<double> ent_v(std::max<i64>(total, 1), s);
-    PMMF_LAUNCH(k_anchor_scatter, static_cast<unsigned>(m), 128, 0, s, m, danch.get(), a.ptr.get(), a.row.get(),
+    PMMF_LAUNCH(k_anchor_scatter, static_cast<unsigned>(m), 128, 0, s, m, danch, a.ptr.get(), a.row.get(),
                 a.val.get(), rptr.get(), cursor.get(), ent_a.get(), ent_v.get());
     if (!rows_mode) {
       std::vector<int32_t> pos(static_cast<size_t>(m));
@@ -667,7 +711,7 @@ struct Scorer {
       // mark anchors (self-assignment, clustering.hpp:118-122)
       DBuf<int32_t> dpos(m, s);
       dpos.upload(pos);
-      set_self(danch, dpos, m, true);
+      set_self(danch, dpos.get(), m, true);
     }
     // warps per block: most resident warps per SM under the shared-memory
     // limit (227 KB per SM, 1 KB reserved per block)
@@ -687,26 +731,22 @@ struct Scorer {
     DBuf<double> scratch;
     if (!use_smem)  // one state slot per launched warp (persistent grid of 148 x 8 blocks)
       scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(148 * 8 * wpb) + 7) / 8), s);
-    DBuf<int32_t> dassign(P, s);
+    int32_t* dassign = assign_out;
     // Sharded (assignment mode, sparse scorer): the hub columns are scored
     // on every rank, the rest of the cost-sorted list round-robin over the
     // ranks; positions a rank did not score keep a sentinel below any
     // result (-1 = no anchor hit) and an allreduce(max) completes the table.
     const bool shard = !rows_mode && comm && comm->world() > 1;
-    if (shard) dassign.fill_bytes(0x80);
-    DBuf<double> drows;
-    if (rows_mode) {
-      drows.alloc(P * m, s);
-      drows.zero();
-    }
-    ScoreArgs args{P,           dpool.get(), dpn.get(),        m,           dan.get(),   self.get(),
+    if (shard) PMMF_CUDA(cudaMemsetAsync(dassign, 0x80, sizeof(int32_t) * P, s));
+    if (rows_mode) PMMF_CUDA(cudaMemsetAsync(rows_out, 0, sizeof(double) * P * m, s));
+    ScoreArgs args{P,           dpool,       dpn,              m,           dan,         self.get(),
                    a.ptr.get(), a.row.get(), a.val.get(),      nb.d_blk.get(), rptr.get(), ent_a.get(),
-                   ent_v.get(), dassign.get(), rows_mode ? drows.get() : nullptr, scratch.get(), nullptr,
-                   nullptr, nullptr, danch.get(), nullptr, 0, nullptr};
+                   ent_v.get(), dassign, rows_mode ? rows_out : nullptr, scratch.get(), nullptr,
+                   nullptr, nullptr, danch, nullptr, 0, nullptr};
     // Work list: pool positions by decreasing serial cost (rows hit); the
     // heaviest, above a share of the anchors' total size, take the dense path.
     DBuf<int32_t> key(P, s), key2(P, s), idx(P, s), list(P, s), nd_d(1, s);
-    PMMF_LAUNCH(k_col_cost, blocks_for(P * 32, kThreads), kThreads, 0, s, P, dpool.get(), self.get(), rows_mode,
+    PMMF_LAUNCH(k_col_cost, blocks_for(P * 32, kThreads), kThreads, 0, s, P, dpool, self.get(), rows_mode,
                 a.ptr.get(), a.row.get(), cnt.get(), key.get(), idx.get());
     {
       size_t tmp = 0;
@@ -759,7 +799,7 @@ struct Scorer {
     if (nd > 0) {
       // anchors by decreasing size (longest walks start first)
       DBuf<int32_t> ann(m, s), ann2(m, s), aidx(m, s), aorder(m, s);
-      PMMF_LAUNCH(k_anchor_nnz, blocks_for(m, kThreads), kThreads, 0, s, m, danch.get(), a.ptr.get(), ann.get(),
+      PMMF_LAUNCH(k_anchor_nnz, blocks_for(m, kThreads), kThreads, 0, s, m, danch, a.ptr.get(), ann.get(),
                   aidx.get());
       {
         size_t tmp = 0;
@@ -783,14 +823,14 @@ struct Scorer {
       for (i64 d0 = 0; d0 < nd; d0 += D) {
         const int Dcur = static_cast<int>(std::min<i64>(D, nd - d0));
         const int32_t* dcols = list.get() + d0;
-        PMMF_LAUNCH(k_dense_scatter, static_cast<unsigned>(Dcur), 256, 0, s, dcols, dpool.get(), a.ptr.get(),
+        PMMF_LAUNCH(k_dense_scatter, static_cast<unsigned>(Dcur), 256, 0, s, dcols, dpool, a.ptr.get(),
                     a.row.get(), a.val.get(), D, false, X.get());
         PMMF_LAUNCH(k_score_spmm, blocks_for(static_cast<i64>(m) * G * 32, 256), 256, 0, s, args, aorder.get(), G,
                     dcols, Dcur, D, X.get(), S.get());
         if (!rows_mode)
           PMMF_LAUNCH(k_dense_argmax, blocks_for(static_cast<i64>(Dcur) * 32, kThreads), kThreads, 0, s, args, dcols,
                       Dcur, S.get());
-        PMMF_LAUNCH(k_dense_scatter, static_cast<unsigned>(Dcur), 256, 0, s, dcols, dpool.get(), a.ptr.get(),
+        PMMF_LAUNCH(k_dense_scatter, static_cast<unsigned>(Dcur), 256, 0, s, dcols, dpool, a.ptr.get(),
                     a.row.get(), a.val.get(), D, true, X.get());
       }
     }
@@ -829,7 +869,7 @@ struct Scorer {
       }
       if (per_rank)
         std::fprintf(stderr, "[pmmf] shard score: %d ranks, sum %.3f ms, max %.3f ms\n", W, tsum, tmax);
-      allreduce_max_i32(dassign.get(), P, *comm, s);
+      allreduce_max_i32(dassign, P, *comm, s);
     }
     if (timing) cudaEventRecord(ev[2], s);
     if (trace_enabled()) {
@@ -863,15 +903,10 @@ struct Scorer {
       for (auto& e : ev)
         if (e) cudaEventDestroy(e);
     }
-    if (!rows_mode) {
-      set_self(danch, danch, m, false);
-      *assign = dassign.to_host(P);
-    } else {
-      *rows = drows.to_host(P * m);
-    }
+    if (!rows_mode) set_self(danch, danch, m, false);
   }
 
-  void set_self(const DBuf<int32_t>& anchors, const DBuf<int32_t>& pos, int m, bool on);
+  void set_self(const int32_t* anchors, const int32_t* pos, int m, bool on);
 
   // Dense problems go through the GEMM path: at least a quarter of all
   // entries stored (PMMF_B200_SCORE_GEMM=1/0 forces it on/off for tests).
@@ -881,45 +916,37 @@ struct Scorer {
     return a.N > 0 && static_cast<double>(a.nnz) >= 0.25 * N * N;
   }
 
-  void run_gemm(i64 P, int m, const DBuf<int32_t>& dpool, const DBuf<double>& dpn, const DBuf<int32_t>& danch,
-                const DBuf<double>& dan, bool rows_mode, std::vector<int32_t>* assign, std::vector<double>* rows,
-                std::chrono::steady_clock::time_point t_start) {
+  void run_gemm(i64 P, int m, const int32_t* dpool, const double* dpn, const int32_t* danch, const double* dan,
+                bool rows_mode, int32_t* assign_out, double* rows_out, std::chrono::steady_clock::time_point t_start) {
     const i64 N = a.N;
     if (!rows_mode) {  // mark anchors (self-assignment, clustering.hpp:118-122)
       std::vector<int32_t> pos(static_cast<size_t>(m));
       std::iota(pos.begin(), pos.end(), 0);
       DBuf<int32_t> dpos(m, s);
       dpos.upload(pos);
-      set_self(danch, dpos, m, true);
+      set_self(danch, dpos.get(), m, true);
     }
     DBuf<double> Xa(static_cast<i64>(m) * N, s);
     Xa.zero();
     PMMF_LAUNCH(k_panel_cols, blocks_for(static_cast<i64>(m) * 32, kThreads), kThreads, 0, s, static_cast<i64>(m),
-                danch.get(), a.ptr.get(), a.row.get(), a.val.get(), N, Xa.get());
+                danch, a.ptr.get(), a.row.get(), a.val.get(), N, Xa.get());
     // pool chunk: panel within a fifth of free memory
     const i64 budget = std::max<i64>(i64{1} << 28, available_bytes() / 5);
     const i64 pc = std::max<i64>(kGemmTJ, std::min<i64>(P, budget / (8 * std::max<i64>(N, 1)) / kGemmTJ * kGemmTJ));
     DBuf<double> Xp(pc * N, s), S(pc * m, s);
-    DBuf<int32_t> dassign(rows_mode ? 1 : P, s);
-    std::vector<double> hrows;
-    if (rows_mode) hrows.resize(static_cast<size_t>(P * m));
     for (i64 p0 = 0; p0 < P; p0 += pc) {
       const i64 n = std::min<i64>(pc, P - p0);
       Xp.zero();
-      PMMF_LAUNCH(k_panel_cols, blocks_for(n * 32, kThreads), kThreads, 0, s, n, dpool.get() + p0, a.ptr.get(),
+      PMMF_LAUNCH(k_panel_cols, blocks_for(n * 32, kThreads), kThreads, 0, s, n, dpool + p0, a.ptr.get(),
                   a.row.get(), a.val.get(), N, Xp.get());
       dim3 grid(static_cast<unsigned>((n + kGemmTJ - 1) / kGemmTJ), static_cast<unsigned>((m + kGemmTA - 1) / kGemmTA));
-      k_score_gemm<<<grid, 256, 0, s>>>(N, static_cast<int>(n), m, Xp.get(), Xa.get(), nb.d_blk.get(), dpn.get() + p0,
-                                        dan.get(), S.get());
+      k_score_gemm<<<grid, 256, 0, s>>>(N, static_cast<int>(n), m, Xp.get(), Xa.get(), nb.d_blk.get(), dpn + p0,
+                                        dan, rows_mode ? rows_out + p0 * m : S.get());
       launch_counter().fetch_add(1, std::memory_order_relaxed);
       PMMF_CUDA(cudaGetLastError());
-      if (rows_mode) {
-        S.download(hrows.data() + p0 * m, n * m);
-        PMMF_CUDA(cudaStreamSynchronize(s));
-      } else {
-        PMMF_LAUNCH(k_gemm_argmax, blocks_for(n * 32, kThreads), kThreads, 0, s, n, m, dpool.get() + p0, self.get(),
-                    S.get(), dassign.get() + p0);
-      }
+      if (!rows_mode)
+        PMMF_LAUNCH(k_gemm_argmax, blocks_for(n * 32, kThreads), kThreads, 0, s, n, m, dpool + p0, self.get(),
+                    S.get(), assign_out + p0);
     }
     if (trace_enabled()) {
       PMMF_CUDA(cudaStreamSynchronize(s));
@@ -927,12 +954,7 @@ struct Scorer {
       std::fprintf(stderr, "[pmmf]   score (gemm): pool=%lld anchors=%d rows=%lld chunk=%lld %.2f ms\n",
                    static_cast<long long>(P), m, static_cast<long long>(N), static_cast<long long>(pc), ms);
     }
-    if (rows_mode) {
-      *rows = std::move(hrows);
-    } else {
-      set_self(danch, danch, m, false);
-      *assign = dassign.to_host(P);
-    }
+    if (!rows_mode) set_self(danch, danch, m, false);
   }
 };
 
@@ -942,136 +964,359 @@ __global__ void k_set_self(int m, const int32_t* __restrict__ anchors, const int
   if (a < m) self[anchors[a]] = on ? pos[a] : -1;
 }
 
-void Scorer::set_self(const DBuf<int32_t>& anchors, const DBuf<int32_t>& pos, int m, bool on) {
-  PMMF_LAUNCH(k_set_self, blocks_for(m, kThreads), kThreads, 0, s, m, anchors.get(), pos.get(), on, self.get());
+void Scorer::set_self(const int32_t* anchors, const int32_t* pos, int m, bool on) {
+  PMMF_LAUNCH(k_set_self, blocks_for(m, kThreads), kThreads, 0, s, m, anchors, pos, on, self.get());
 }
 
-struct Ctx {
+// ------------------------------------------------ device control path
+// cluster_recursive (clustering.hpp:85-177) with every O(pool) step on the
+// device: the pool's nonzero-norm filter and the final cluster lists are
+// stable compactions / a stable radix sort by assignment, unscored columns
+// take the round-robin anchor from a scan of the unscored flags, and the
+// undersize repair runs as one CTA (below).  The host keeps what the
+// reference's RNG stream and recursion order need: the m anchor draws
+// (positions only, they do not depend on the values), the m cluster sizes
+// and the DFS order of the oversize recursion.
+
+__global__ void k_pool_gather(i64 P, const int32_t* __restrict__ g, const int32_t* __restrict__ g2s,
+                              const double* __restrict__ norm_g, int32_t* __restrict__ sid, double* __restrict__ nrm,
+                              uint8_t* __restrict__ nz) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= P) return;
+  const int32_t x = g[i];
+  sid[i] = g2s[x];
+  const double v = norm_g[x];
+  nrm[i] = v;
+  if (nz) nz[i] = v > 0.0 ? 1 : 0;
+}
+
+__global__ void k_take(i64 m, const int32_t* __restrict__ src, const int64_t* __restrict__ pos,
+                       int32_t* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < m) out[i] = src[pos[i]];
+}
+
+// Unscored pool columns go round-robin over the anchors in pool order
+// (clustering.hpp:124-131): rank among the unscored (exclusive scan) mod m.
+__global__ void k_unscored(i64 P, const int32_t* __restrict__ assign, int32_t* __restrict__ flag) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < P) flag[i] = assign[i] < 0 ? 1 : 0;
+}
+__global__ void k_round_robin(i64 P, int m, const int32_t* __restrict__ rank, int32_t* __restrict__ assign,
+                              i64* __restrict__ sizes) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= P) return;
+  int32_t a = assign[i];
+  if (a < 0) {
+    a = rank[i] % m;
+    assign[i] = a;
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(sizes + a), 1ull);
+}
+
+__global__ void k_cand_flag(i64 P, const int32_t* __restrict__ assign, const i64* __restrict__ sizes, i64 c_min,
+                            uint8_t* __restrict__ flag) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < P) flag[i] = sizes[assign[i]] < c_min ? 1 : 0;
+}
+__global__ void k_cand_take(i64 C, const int64_t* __restrict__ pos, const int32_t* __restrict__ sid,
+                            const double* __restrict__ nrm, const int32_t* __restrict__ assign,
+                            int32_t* __restrict__ csid, double* __restrict__ cn, int32_t* __restrict__ cur) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= C) return;
+  const i64 p = pos[i];
+  csid[i] = sid[p];
+  cn[i] = nrm[p];
+  cur[i] = assign[p];
+}
+__global__ void k_cand_back(i64 C, const int64_t* __restrict__ pos, const int32_t* __restrict__ cur,
+                            int32_t* __restrict__ assign) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < C) assign[pos[i]] = cur[i];
+}
+
+// Undersize repair (clustering.hpp:138-163) in one CTA.  Candidates are the
+// members of clusters that started below c_min (clusters only grow, so no
+// other column can be orphaned), in pool (ascending global) order, with
+// their rows of the P_c x m score table.  Per dissolution: the first alive
+// cluster of minimal size (ascending index, the reference's alive vector),
+// its members = candidates currently in it, in candidate order (= the
+// sorted order the reference visits), each sent to the first strict-max
+// alive anchor with a positive score, else round-robin over the alive list.
+constexpr int kRepairThreads = 1024;
+__global__ void __launch_bounds__(kRepairThreads) k_repair(i64 C, int m, i64 c_min, const double* __restrict__ table,
+                                                           int32_t* __restrict__ cur, i64* __restrict__ sizes,
+                                                           int32_t* __restrict__ alive, int32_t* __restrict__ orphans) {
+  using BlockScan = cub::BlockScan<int, kRepairThreads>;
+  __shared__ typename BlockScan::TempStorage scan;
+  __shared__ i64 rv[32];
+  __shared__ int ri[32];
+  __shared__ double rs[32];
+  __shared__ int s_worst, s_wpos, s_norph, s_nalive;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  for (int a = tid; a < m; a += blockDim.x) alive[a] = a;
+  if (tid == 0) s_nalive = m;
+  __syncthreads();
+  for (;;) {
+    const int na = s_nalive;
+    if (na <= 1) break;
+    // first alive position of minimal size
+    i64 bv = 0x7fffffffffffffffll;
+    int bi = 0x7fffffff;
+    for (int i = tid; i < na; i += blockDim.x) {
+      const i64 v = sizes[alive[i]];
+      if (v < bv || (v == bv && i < bi)) {
+        bv = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const i64 ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov < bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      rv[wid] = bv;
+      ri[wid] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < nw; ++w)
+        if (rv[w] < bv || (rv[w] == bv && ri[w] < bi)) {
+          bv = rv[w];
+          bi = ri[w];
+        }
+      s_wpos = bi;
+      s_worst = alive[bi];
+    }
+    __syncthreads();
+    const int worst = s_worst;
+    if (sizes[worst] >= c_min) break;
+    // erase it from the alive list (order preserved; na <= m)
+    if (tid == 0) {
+      for (int i = s_wpos; i + 1 < na; ++i) alive[i] = alive[i + 1];
+      s_nalive = na - 1;
+    }
+    __syncthreads();
+    const int nal = s_nalive;
+    // orphans in candidate order: per-thread contiguous chunks + block scan
+    const i64 per = (C + blockDim.x - 1) / blockDim.x;
+    const i64 c0 = tid * per, c1 = min(C, c0 + per);
+    int cnt = 0;
+    for (i64 c = c0; c < c1; ++c) cnt += cur[c] == worst;
+    int off = 0, total = 0;
+    BlockScan(scan).ExclusiveSum(cnt, off, total);
+    for (i64 c = c0; c < c1; ++c)
+      if (cur[c] == worst) orphans[off++] = static_cast<int32_t>(c);
+    if (tid == 0) s_norph = total;
+    __syncthreads();
+    const int norph = s_norph;
+    int orr = 0;
+    for (int q = 0; q < norph; ++q) {
+      const i64 o = orphans[q];
+      const double* sr = table + o * m;
+      double bs = 0.0;
+      int bp = 0x7fffffff;
+      for (int i = tid; i < nal; i += blockDim.x) {
+        const double sc = sr[alive[i]];
+        if (sc > bs || (sc == bs && sc > 0.0 && i < bp)) {
+          bs = sc;
+          bp = i;
+        }
+      }
+      for (int o2 = 16; o2; o2 >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, bs, o2);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o2);
+        if (os > bs || (os == bs && os > 0.0 && op < bp)) {
+          bs = os;
+          bp = op;
+        }
+      }
+      if (lane == 0) {
+        rs[wid] = bs;
+        ri[wid] = bp;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        for (int w = 1; w < nw; ++w)
+          if (rs[w] > bs || (rs[w] == bs && rs[w] > 0.0 && ri[w] < bp)) {
+            bs = rs[w];
+            bp = ri[w];
+          }
+        const int a = bs > 0.0 ? alive[bp] : alive[(orr++) % nal];
+        cur[o] = a;
+        ++sizes[a];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) sizes[worst] = 0;
+    __syncthreads();
+  }
+}
+
+template <typename In, typename T>
+void stable_select(In in, const uint8_t* flags, i64 n, T* out, i64* count, cudaStream_t s) {
+  DBuf<i64> nsel(1, s);
+  size_t tmp = 0;
+  PMMF_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, in, flags, out, nsel.get(), static_cast<int64_t>(n), s));
+  DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+  PMMF_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, in, flags, out, nsel.get(), static_cast<int64_t>(n), s));
+  *count = nsel.to_host(1)[0];
+}
+
+struct DevCtx {
   Scorer* sc;
-  const Numbering* nb;
-  const std::vector<double>* norm;  // by global id
+  const int32_t* g2s;    // device: global -> stage id
+  const double* norm_g;  // device: norm by global id
   i64 c_min, c_max;
   int d_max;
   int max_depth = 0;
+  cudaStream_t s;
 };
 
-void recurse(Ctx& ctx, std::vector<i64> pool, i64 m_request, int depth, Xoshiro& rng,
-             std::vector<std::vector<i64>>& out) {  // clustering.hpp:85-177
+// seg: the pool (global ids ascending, device) of one recursion node; on
+// return it holds the node's clusters in DFS order and `sizes` has one entry
+// per emitted cluster.
+void recurse(DevCtx& ctx, int32_t* seg, i64 P, i64 m_request, int depth, Xoshiro& rng, std::vector<i64>& sizes_out) {
   ctx.max_depth = std::max(ctx.max_depth, depth);
-  if (pool.empty()) return;
+  if (P == 0) return;
+  cudaStream_t s = ctx.s;
   const auto t_rec = std::chrono::steady_clock::now();
-  const auto& norm = *ctx.norm;
-  std::vector<i64> shuffled;
-  shuffled.reserve(pool.size());
-  for (i64 g : pool)
-    if (norm[g] > 0.0) shuffled.push_back(g);
-  if (shuffled.empty()) {
-    out.push_back(std::move(pool));
+  DBuf<int32_t> sid(P, s), fil(P, s);
+  DBuf<double> nrm(P, s);
+  DBuf<uint8_t> nz(P, s);
+  PMMF_LAUNCH(k_pool_gather, blocks_for(P, kThreads), kThreads, 0, s, P, seg, ctx.g2s, ctx.norm_g, sid.get(), nrm.get(),
+              nz.get());
+  i64 F = 0;
+  stable_select(seg, nz.get(), P, fil.get(), &F, s);
+  if (F == 0) {
+    sizes_out.push_back(P);
     return;
   }
-  const size_t m = static_cast<size_t>(std::min<i64>(m_request, static_cast<i64>(shuffled.size())));
-  for (size_t t = 0; t < m; ++t) std::swap(shuffled[t], shuffled[t + rng.uniform_below(shuffled.size() - t)]);
-  std::vector<i64> anchors(shuffled.begin(), shuffled.begin() + static_cast<std::ptrdiff_t>(m));
-  std::sort(anchors.begin(), anchors.end());
-
-  const auto& g2s = ctx.nb->g2s;
-  std::vector<int32_t> dpool(pool.size()), danch(m);
-  std::vector<double> pn(pool.size()), an(m);
-  for (size_t i = 0; i < pool.size(); ++i) {
-    dpool[i] = static_cast<int32_t>(g2s[pool[i]]);
-    pn[i] = norm[pool[i]];
+  // anchors: the partial Fisher-Yates of the reference over the filtered pool
+  // (clustering.hpp:99-104) only needs positions
+  const i64 m = std::min(m_request, F);
+  std::vector<int64_t> slot(static_cast<size_t>(m));
+  {
+    std::unordered_map<i64, i64> moved;
+    auto at = [&](i64 x) {
+      auto it = moved.find(x);
+      return it == moved.end() ? x : it->second;
+    };
+    for (i64 t = 0; t < m; ++t) {
+      const i64 j = t + static_cast<i64>(rng.uniform_below(static_cast<uint64_t>(F - t)));
+      const i64 vt = at(t), vj = at(j);
+      moved[t] = vj;
+      moved[j] = vt;
+    }
+    for (i64 t = 0; t < m; ++t) slot[t] = at(t);
   }
-  for (size_t a = 0; a < m; ++a) {
-    danch[a] = static_cast<int32_t>(g2s[anchors[a]]);
-    an[a] = norm[anchors[a]];
+  std::vector<int32_t> anchors(static_cast<size_t>(m));
+  {
+    DBuf<int64_t> dslot(m, s);
+    DBuf<int32_t> dan(m, s);
+    dslot.upload(slot);
+    PMMF_LAUNCH(k_take, blocks_for(m, kThreads), kThreads, 0, s, m, fil.get(), dslot.get(), dan.get());
+    anchors = dan.to_host(m);
+    std::sort(anchors.begin(), anchors.end());
   }
-  std::vector<int32_t> assign;
+  DBuf<int32_t> ag(m, s), asid(m, s);
+  DBuf<double> anrm(m, s);
+  ag.upload(anchors);
+  PMMF_LAUNCH(k_pool_gather, blocks_for(m, kThreads), kThreads, 0, s, m, ag.get(), ctx.g2s, ctx.norm_g, asid.get(),
+              anrm.get(), static_cast<uint8_t*>(nullptr));
+  DBuf<int32_t> assign(P, s);
   const auto t_host0 = std::chrono::steady_clock::now();
-  ctx.sc->run(dpool, pn, danch, an, false, &assign, nullptr);
-  if (trace_enabled() && depth == 0)
+  ctx.sc->run(sid.get(), nrm.get(), P, asid.get(), anrm.get(), static_cast<int>(m), false, assign.get(), nullptr);
+  if (trace_enabled() && depth == 0) {
+    PMMF_CUDA(cudaStreamSynchronize(s));
     std::fprintf(stderr, "[pmmf]     pool setup %.2f ms, scorer %.2f ms\n",
                  std::chrono::duration<double, std::milli>(t_host0 - t_rec).count(),
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count());
-
-  std::vector<std::vector<i64>> clusters(m);
-  std::vector<size_t> owner(pool.size());
-  size_t rr = 0;
-  for (size_t p = 0; p < pool.size(); ++p) {
-    size_t a = assign[p] >= 0 ? static_cast<size_t>(assign[p]) : (rr++) % m;
-    clusters[a].push_back(pool[p]);
-    owner[p] = a;
   }
-
-  // Undersize repair (clustering.hpp:138-163).  Orphans are always members
-  // of clusters that started below c_min (clusters only grow), so their
-  // scores against every anchor are computed once, up front.
-  std::vector<size_t> alive(m);
-  std::iota(alive.begin(), alive.end(), size_t{0});
-  std::vector<int64_t> cand_row(pool.size(), -1);
-  std::vector<double> table;
+  // round-robin for the unscored, cluster sizes
+  DBuf<i64> dsz(m, s);
+  dsz.zero();
   {
-    std::vector<int32_t> cand;
-    std::vector<double> cn;
-    for (size_t p = 0; p < pool.size(); ++p)
-      if (static_cast<i64>(clusters[owner[p]].size()) < ctx.c_min && m > 1) {
-        cand_row[p] = static_cast<int64_t>(cand.size());
-        cand.push_back(dpool[p]);
-        cn.push_back(pn[p]);
-      }
-    if (!cand.empty()) ctx.sc->run(cand, cn, danch, an, true, nullptr, &table);
+    DBuf<int32_t> fl(P, s), rk(P, s);
+    PMMF_LAUNCH(k_unscored, blocks_for(P, kThreads), kThreads, 0, s, P, assign.get(), fl.get());
+    size_t tmp = 0;
+    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, fl.get(), rk.get(), static_cast<int64_t>(P), s));
+    DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, fl.get(), rk.get(), static_cast<int64_t>(P), s));
+    PMMF_LAUNCH(k_round_robin, blocks_for(P, kThreads), kThreads, 0, s, P, static_cast<int>(m), rk.get(), assign.get(),
+                dsz.get());
   }
-  std::vector<int64_t> pos_of;  // global -> pool position, for orphans
-  auto pool_pos = [&](i64 g) {
-    return static_cast<size_t>(std::lower_bound(pool.begin(), pool.end(), g) - pool.begin());
-  };
-  // The reference re-sorts every alive cluster after each dissolution; a
-  // cluster's order is only observed when it is dissolved (its orphans are
-  // visited in ascending order) and at the end, so grown clusters are marked
-  // and sorted lazily at those two points.
+  std::vector<i64> sz = dsz.to_host(m);
+  // undersize repair (clustering.hpp:138-163), on the device
   const auto t_repair = std::chrono::steady_clock::now();
-  std::vector<uint8_t> dirty(m, 0);
-  while (alive.size() > 1) {
-    size_t worst = alive[0];
-    for (size_t a : alive)
-      if (clusters[a].size() < clusters[worst].size()) worst = a;
-    if (static_cast<i64>(clusters[worst].size()) >= ctx.c_min) break;
-    alive.erase(std::find(alive.begin(), alive.end(), worst));
-    std::vector<i64> orphans = std::move(clusters[worst]);
-    clusters[worst].clear();
-    if (dirty[worst]) std::sort(orphans.begin(), orphans.end());
-    size_t orr = 0;
-    for (i64 o : orphans) {
-      const int64_t row = cand_row[pool_pos(o)];
-      if (row < 0) fail(PMMF_INTERNAL, "clustering: orphan without a precomputed score row");
-      const double* sr = table.data() + static_cast<size_t>(row) * m;
-      size_t best = 0;
-      double bs = 0.0;
-      for (size_t i = 0; i < alive.size(); ++i) {
-        const double s = sr[alive[i]];
-        if (s > bs) {
-          bs = s;
-          best = i;
-        }
-      }
-      const size_t a = bs > 0.0 ? best : (orr++) % alive.size();
-      clusters[alive[a]].push_back(o);
-      dirty[alive[a]] = 1;
-    }
+  i64 nalive = m;
+  if (m > 1 && *std::min_element(sz.begin(), sz.end()) < ctx.c_min) {
+    DBuf<uint8_t> cf(P, s);
+    PMMF_LAUNCH(k_cand_flag, blocks_for(P, kThreads), kThreads, 0, s, P, assign.get(), dsz.get(), ctx.c_min, cf.get());
+    DBuf<int64_t> cpos(P, s);
+    i64 C = 0;
+    stable_select(cub::CountingInputIterator<int64_t>(0), cf.get(), P, cpos.get(), &C, s);
+    DBuf<int32_t> csid(C, s), cur(C, s), orph(C, s), alive(m, s);
+    DBuf<double> cn(C, s), table(C * m, s);
+    PMMF_LAUNCH(k_cand_take, blocks_for(C, kThreads), kThreads, 0, s, C, cpos.get(), sid.get(), nrm.get(),
+                assign.get(), csid.get(), cn.get(), cur.get());
+    ctx.sc->run(csid.get(), cn.get(), C, asid.get(), anrm.get(), static_cast<int>(m), true, nullptr, table.get());
+    PMMF_LAUNCH(k_repair, 1, kRepairThreads, 0, s, C, static_cast<int>(m), ctx.c_min, table.get(), cur.get(),
+                dsz.get(), alive.get(), orph.get());
+    PMMF_LAUNCH(k_cand_back, blocks_for(C, kThreads), kThreads, 0, s, C, cpos.get(), cur.get(), assign.get());
+    sz = dsz.to_host(m);
+    nalive = 0;
+    for (i64 a = 0; a < m; ++a) nalive += sz[a] > 0;
   }
   if (trace_enabled() && depth == 0)
-    std::fprintf(stderr, "[pmmf]     undersize repair: %zu of %zu clusters alive, %.2f ms\n", alive.size(), m,
+    std::fprintf(stderr, "[pmmf]     undersize repair: %lld of %lld clusters alive, %.2f ms\n",
+                 static_cast<long long>(nalive), static_cast<long long>(m),
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_repair).count());
-  for (size_t a : alive) {  // oversize recursion (clustering.hpp:165-176)
-    auto& mem = clusters[a];
-    if (mem.empty()) continue;
-    if (dirty[a]) std::sort(mem.begin(), mem.end());
-    if (static_cast<i64>(mem.size()) > ctx.c_max && depth < ctx.d_max) {
-      const i64 sub = (static_cast<i64>(mem.size()) + ctx.c_max - 1) / ctx.c_max;
-      recurse(ctx, std::move(mem), sub, depth + 1, rng, out);
-    } else {
-      out.push_back(std::move(mem));
-    }
+  // clusters: a stable sort of the pool by assignment keeps each cluster's
+  // members ascending (the reference sorts its grown clusters)
+  {
+    DBuf<int32_t> k2(P, s), v2(P, s);
+    cub::DoubleBuffer<int32_t> kb(assign.get(), k2.get()), vb(seg, v2.get());
+    const int bits = std::max(1, bits_for(m));
+    size_t tmp = 0;
+    PMMF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int64_t>(P), 0, bits, s));
+    DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+    PMMF_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, kb, vb, static_cast<int64_t>(P), 0, bits, s));
+    if (vb.Current() != seg)
+      PMMF_CUDA(cudaMemcpyAsync(seg, vb.Current(), sizeof(int32_t) * P, cudaMemcpyDeviceToDevice, s));
   }
+  // oversize recursion (clustering.hpp:165-176) in the alive clusters' order
+  i64 off = 0;
+  for (i64 a = 0; a < m; ++a) {
+    const i64 c = sz[a];
+    if (c == 0) continue;
+    if (c > ctx.c_max && depth < ctx.d_max)
+      recurse(ctx, seg + off, c, (c + ctx.c_max - 1) / ctx.c_max, depth + 1, rng, sizes_out);
+    else
+      sizes_out.push_back(c);
+    off += c;
+  }
+}
+
+__global__ void k_scatter_norm(i64 P, const int32_t* __restrict__ g, const double* __restrict__ v,
+                               double* __restrict__ norm_g, uint8_t* __restrict__ in_pool, bool bypass) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= P) return;
+  norm_g[g[i]] = v[i];
+  in_pool[i] = (!bypass || v[i] > 0.0) ? 1 : 0;
+}
+__global__ void k_not(i64 n, const uint8_t* __restrict__ a, uint8_t* __restrict__ b) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < n) b[i] = !a[i];
+}
+__global__ void k_sid_of(i64 P, const int32_t* __restrict__ g, const int32_t* __restrict__ g2s,
+                         int32_t* __restrict__ sid) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < P) sid[i] = g2s[g[i]];
 }
 
 }  // namespace
@@ -1083,36 +1328,65 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
   ClusterOut res;
   // Norms of the active columns (clustering.hpp:189-195).
   const i64 P = static_cast<i64>(active.size());
-  std::vector<int32_t> ids(static_cast<size_t>(P));
-  for (i64 i = 0; i < P; ++i) ids[i] = static_cast<int32_t>(nb.g2s[active[i]]);
-  DBuf<int32_t> dids(P, s);
-  dids.upload(ids);
-  DBuf<double> dnorm(P, s);
-  PMMF_LAUNCH(k_norms, blocks_for(P * 32, kThreads), kThreads, 0, s, P, dids.get(), a.ptr.get(), a.row.get(), a.val.get(),
-              nb.d_blk.get(), dnorm.get());
-  std::vector<double> hn = dnorm.to_host(P);
-  std::vector<double> norm(static_cast<size_t>(n), 0.0);
-  std::vector<i64> pool;
-  pool.reserve(active.size());
-  for (i64 i = 0; i < P; ++i) {
-    norm[active[i]] = hn[i];
-    if (!bypass || hn[i] > 0.0) pool.push_back(active[i]);
-    else res.bypassed.push_back(active[i]);
+  DBuf<int32_t> act(P, s), ids(P, s);
+  {
+    std::vector<int32_t> a32(active.begin(), active.end());
+    act.upload(a32);
+  }
+  PMMF_LAUNCH(k_sid_of, blocks_for(P, kThreads), kThreads, 0, s, P, act.get(), nb.d_g2s.get(), ids.get());
+  DBuf<double> dnorm(P, s), norm_g(std::max<i64>(n, 1), s);
+  {
+    // columns longer than kLong entries: k_norms_long, a CTA per column
+    i64 kLong = 4096;
+    if (const char* e = std::getenv("PMMF_B200_NORM_LONG")) kLong = std::atoll(e);  // test hook
+    const i64 nblk = nb.clusters();
+    const i64 long_len = nblk > 1 ? kLong : (i64{1} << 62);
+    PMMF_LAUNCH(k_norms, blocks_for(P * 32, kThreads), kThreads, 0, s, P, ids.get(), a.ptr.get(), a.row.get(),
+                a.val.get(), nb.d_blk.get(), dnorm.get(), long_len);
+    if (nblk > 1) {
+      DBuf<uint8_t> fl(P, s);
+      PMMF_LAUNCH(k_long_flags, blocks_for(P, kThreads), kThreads, 0, s, P, ids.get(), a.ptr.get(), long_len, fl.get());
+      DBuf<int32_t> lst(P, s);
+      i64 nl = 0;
+      stable_select(cub::CountingInputIterator<int32_t>(0), fl.get(), P, lst.get(), &nl, s);
+      if (nl > 0) {
+        DBuf<int64_t> doff(nblk + 1, s);
+        doff.upload(nb.off);
+        DBuf<double> part(nl * nblk, s);
+        PMMF_LAUNCH(k_norms_long, static_cast<unsigned>(nl), kNormLongThreads, 0, s, lst.get(), ids.get(), a.ptr.get(),
+                    a.row.get(), a.val.get(), doff.get(), nblk, part.get(), dnorm.get());
+      }
+    }
+  }
+  norm_g.zero();
+  DBuf<uint8_t> in_pool(P, s), byp(P, s);
+  PMMF_LAUNCH(k_scatter_norm, blocks_for(P, kThreads), kThreads, 0, s, P, act.get(), dnorm.get(), norm_g.get(),
+              in_pool.get(), bypass);
+  res.members.alloc(P, s);
+  i64 np = 0, nbyp = 0;
+  stable_select(act.get(), in_pool.get(), P, res.members.get(), &np, s);
+  if (np < P) {  // zero-norm columns bypass (clustering.hpp:207-214), appended by the caller
+    PMMF_LAUNCH(k_not, blocks_for(P, kThreads), kThreads, 0, s, P, in_pool.get(), byp.get());
+    DBuf<int32_t> bl(P - np, s);
+    stable_select(act.get(), byp.get(), P, bl.get(), &nbyp, s);
+    std::vector<int32_t> h = bl.to_host(nbyp);
+    res.bypassed.assign(h.begin(), h.end());
+    PMMF_CUDA(cudaMemcpyAsync(res.members.get() + np, bl.get(), sizeof(int32_t) * nbyp, cudaMemcpyDeviceToDevice, s));
   }
   const auto t_norms = std::chrono::steady_clock::now();
-  if (!pool.empty()) {
+  if (np > 0) {
     Scorer sc(a, nb, s);
     sc.comm = comm;
-    Ctx ctx{&sc, &nb, &norm, c_min, c_max, d_max};
+    DevCtx ctx{&sc, nb.d_g2s.get(), norm_g.get(), c_min, c_max, d_max, 0, s};
     Xoshiro rng(seed);
-    recurse(ctx, std::move(pool), m_target, 0, rng, res.clusters);
+    recurse(ctx, res.members.get(), np, m_target, 0, rng, res.sizes);
     res.max_depth = ctx.max_depth;
   }
+  PMMF_CUDA(cudaStreamSynchronize(s));
   if (trace_enabled())
     std::fprintf(stderr, "[pmmf]   clustering: %.2f ms after norms (pool %lld, nnz %lld)\n",
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_norms).count(),
                  static_cast<long long>(P), static_cast<long long>(a.nnz));
-  std::sort(res.bypassed.begin(), res.bypassed.end());
   return res;
 }
 

@@ -43,9 +43,14 @@ struct Numbering {
   std::vector<i64> s2g, off, g2s;  // host: stage->global, cluster offsets, global->stage (-1)
   DBuf<int32_t> d_blk;             // stage id -> cluster (row block)
   DBuf<int32_t> d_s2g;             // stage id -> global
+  DBuf<int32_t> d_g2s;             // global -> stage id (-1 when absent)
   i64 size() const { return static_cast<i64>(s2g.size()); }
   i64 clusters() const { return static_cast<i64>(off.size()) - 1; }
+  // from host cluster lists (validated: the input partition)
   void build(const std::vector<std::vector<i64>>& clusters, i64 n, cudaStream_t s);
+  // from a device member list (a stage partition built on the device) and
+  // the cluster offsets; host mirrors are copied back
+  void build_device(DBuf<int32_t>&& members, std::vector<i64> offsets, i64 n, cudaStream_t s);
 };
 
 // ---- matrix.cu
@@ -69,8 +74,11 @@ void reblock(Csc& out, const Csc& a, const DBuf<int32_t>& map, const DBuf<int32_
 
 // ---- cluster.cu
 struct ClusterOut {
-  std::vector<std::vector<i64>> clusters;  // DFS order, members ascending global
-  std::vector<i64> bypassed;
+  // device: the clusters' members (global ids) in DFS order, each cluster
+  // ascending, followed by the bypassed columns; sizes[u] per cluster
+  DBuf<int32_t> members;
+  std::vector<i64> sizes;
+  std::vector<i64> bypassed;  // ascending global ids
   int max_depth = 0;
 };
 // cluster_columns (clustering.hpp:183-225) over the pre-reblock matrix a

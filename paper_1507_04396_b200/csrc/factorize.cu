@@ -164,7 +164,16 @@ struct StreamGuard {
   }
 };
 
+// out[i] = b[a[i]] (relabel maps between two stage numberings: stage id ->
+// global -> stage id)
+__global__ void k_compose(i64 N, const int32_t* __restrict__ a, const int32_t* __restrict__ b,
+                          int32_t* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < N) out[i] = b[a[i]];
+}
+
 }  // namespace
+
 
 std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b200_params& p,
                                          const Comm* comm) {
@@ -275,25 +284,21 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     ClusterOut co = cluster_columns_dev(A, cur, active, n, p.m_target, p.c_min, p.c_max, p.d_max,
                                         p.bypass_enabled != 0, derive(p.seed, cpath), s, comm);
     R->phases[0] += ms_since(t0);
-    const i64 rc = static_cast<i64>(co.clusters.size());
-    std::vector<std::vector<i64>> stage_clusters = std::move(co.clusters);
-    if (!co.bypassed.empty()) stage_clusters.push_back(co.bypassed);
+    const i64 rc = static_cast<i64>(co.sizes.size());
+    std::vector<i64> stage_off(1, 0);
+    for (i64 c : co.sizes) stage_off.push_back(stage_off.back() + c);
+    if (!co.bypassed.empty()) stage_off.push_back(stage_off.back() + static_cast<i64>(co.bypassed.size()));
 
-    // ---- reblock to the stage numbering
+    // ---- reblock to the stage numbering (relabel maps composed on the device)
     t0 = clk::now();
     Numbering nxt;
-    nxt.build(stage_clusters, n, s);
+    nxt.build_device(std::move(co.members), std::move(stage_off), n, s);
     {
-      std::vector<int32_t> map(static_cast<size_t>(cur.size())), new2old(static_cast<size_t>(nxt.size()));
-      for (i64 r = 0; r < cur.size(); ++r) map[r] = static_cast<int32_t>(nxt.g2s[cur.s2g[r]]);
-      for (i64 J = 0; J < nxt.size(); ++J) {
-        const i64 old = cur.g2s[nxt.s2g[J]];
-        if (old < 0) fail(PMMF_INVALID_ARGUMENT, "reblock: new partition references an absent index");
-        new2old[J] = static_cast<int32_t>(old);
-      }
       DBuf<int32_t> dmap(std::max<i64>(cur.size(), 1), s), dn2o(std::max<i64>(nxt.size(), 1), s);
-      dmap.upload(map);
-      dn2o.upload(new2old);
+      PMMF_LAUNCH(k_compose, blocks_for(cur.size(), kThreads), kThreads, 0, s, cur.size(), cur.d_s2g.get(),
+                  nxt.d_g2s.get(), dmap.get());
+      PMMF_LAUNCH(k_compose, blocks_for(nxt.size(), kThreads), kThreads, 0, s, nxt.size(), nxt.d_s2g.get(),
+                  cur.d_g2s.get(), dn2o.get());
       Csc B;
       reblock(B, A, dmap, dn2o, nxt.size(), s);
       A = std::move(B);

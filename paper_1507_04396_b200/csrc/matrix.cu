@@ -33,6 +33,11 @@ __global__ void k_fill_blk(const int64_t* off, i64 m, int32_t* blk) {
 }
 
 // ------------------------------------------------------------ from_coo
+__global__ void k_g2s(i64 N, const int32_t* __restrict__ s2g, int32_t* __restrict__ g2s) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < N) g2s[s2g[i]] = static_cast<int32_t>(i);
+}
+
 __global__ void k_coo_keys(i64 n, i64 nnz, const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
                            const double* __restrict__ vals, const int32_t* __restrict__ g2s, uint64_t N,
                            uint64_t* __restrict__ keys, unsigned long long* __restrict__ first_err) {
@@ -340,6 +345,27 @@ void Numbering::build(const std::vector<std::vector<i64>>& cls, i64 n, cudaStrea
   DBuf<int64_t> doff(clusters() + 1, s);
   doff.upload(off);
   PMMF_LAUNCH(k_fill_blk, static_cast<unsigned>(clusters()), 256, 0, s, doff.get(), clusters(), d_blk.get());
+  d_g2s.alloc(std::max<i64>(n, 1), s);
+  d_g2s.fill_bytes(0xff);
+  PMMF_LAUNCH(k_g2s, blocks_for(N, 256), 256, 0, s, N, d_s2g.get(), d_g2s.get());
+}
+
+void Numbering::build_device(DBuf<int32_t>&& members, std::vector<i64> offsets, i64 n, cudaStream_t s) {
+  off = std::move(offsets);
+  const i64 N = off.back();
+  d_s2g = std::move(members);
+  d_blk.alloc(std::max<i64>(N, 1), s);
+  DBuf<int64_t> doff(clusters() + 1, s);
+  doff.upload(off);
+  PMMF_LAUNCH(k_fill_blk, static_cast<unsigned>(clusters()), 256, 0, s, doff.get(), clusters(), d_blk.get());
+  d_g2s.alloc(std::max<i64>(n, 1), s);
+  d_g2s.fill_bytes(0xff);
+  PMMF_LAUNCH(k_g2s, blocks_for(N, 256), 256, 0, s, N, d_s2g.get(), d_g2s.get());
+  // host mirrors
+  std::vector<int32_t> h = d_s2g.to_host(N);
+  s2g.assign(h.begin(), h.end());
+  std::vector<int32_t> hg = d_g2s.to_host(std::max<i64>(n, 1));
+  g2s.assign(hg.begin(), hg.begin() + std::max<i64>(n, 0));
 }
 
 void csc_from_coo(Csc& out, const Numbering& nb, i64 n, i64 nnz, const int64_t* rows, const int64_t* cols,

@@ -95,3 +95,13 @@ def test_level_loop_path(name, batch, monkeypatch):
         monkeypatch.setenv("PMMF_B200_MERGE_CHUNK", "32")
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf512_k4", "zero_cols_bypass",
+                                  "partitioned_input", "undersize_repair", "oversize_recursion"])
+def test_long_column_norms(name, monkeypatch):
+    """Every column longer than 8 entries through the CTA-per-column norm
+    kernel (hub columns on config 4) — still bit-exact."""
+    monkeypatch.setenv("PMMF_B200_NORM_LONG", "8")
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
