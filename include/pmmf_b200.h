@@ -233,6 +233,19 @@ int pmmf_b200_solve(const pmmf_b200_coo* a, void* op, const pmmf_b200_solve_conf
                     int32_t* iterations, int32_t* converged, int32_t* breakdown, double* residuals,
                     double* wall_ms, char* err, size_t errlen);
 
+/* ---- dense Gram mode (gram_of_cluster_sparse, blocked_matrix.hpp:238-254) */
+
+/* Process-wide choice of the dense-cluster Gram kernel.  0 (default): the
+ * bitwise SIMT SYRK, every G[a][b] summed over the rows in the reference's
+ * order with separately rounded products.  1: FP64 tensor cores (DMMA
+ * mma.sync m8n8k4, operands staged by TMA): G agrees to ~1e-15 relative,
+ * not bitwise, so a pivot whose score margin is within that distance can
+ * differ from the reference (the near-tie clause of the parity contract).
+ * Also PMMF_B200_GRAM_DMMA=1 at load time.  Returns PMMF_INVALID_ARGUMENT
+ * for another mode. */
+int pmmf_b200_set_dense_gram(int32_t mode);
+int32_t pmmf_b200_get_dense_gram(void);
+
 /* ---- comparison preconditioners (solver.hpp:46-56, :224-349) -------- */
 
 /* PreconditionerKind (solver.hpp:60).  A preconditioner handle is a split

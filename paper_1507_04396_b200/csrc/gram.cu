@@ -12,6 +12,8 @@
 // distinct b, rows strictly in order.  Work is sum_r deg_u(r)^2, the
 // reference's own product count.
 #include <cub/cub.cuh>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -248,6 +250,159 @@ __global__ void __launch_bounds__(256) k_syrk_seq(const DenseTile* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------- DMMA path
+// Opt-in (pmmf_b200_set_dense_gram(1)): the dense Gram on the FP64 tensor
+// cores.  mma.sync m8n8k4 f64 (DMMA) accumulates each 4-row k-step with its
+// own rounding, so G differs from the reference's sequential sum in the
+// last bits and a pivot whose score margin is that small can flip (the
+// near-tie clause of SURVEY.md §8(c)); the bitwise SIMT SYRK stays the
+// default.  Operands are staged by TMA (cp.async.bulk.tensor, 128-byte
+// swizzle, boxes of 16 rows x 128 panel columns) into a 3-stage mbarrier
+// pipeline; 128 x 128 output tile per CTA, 8 warps of 32 x 64, 32 DMMA per
+// warp per k-step.
+constexpr int kDmT = 128;          // output tile edge
+constexpr int kDmKC = 32;          // k rows per pipeline stage
+constexpr int kDmStages = 3;
+constexpr int kDmBox = 16 * kDmT * 8;              // bytes of one 16 x 128 box
+constexpr int kDmStageBytes = 4 * kDmBox;          // A (2 boxes) + B (2 boxes)
+constexpr int kDmSmem = kDmStages * kDmStageBytes + 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+// Element (panel column x in [0,128), row k in [0,16)) of a 128B-swizzled box.
+__device__ __forceinline__ const double* box_at(const char* box, int x, int k) {
+  return reinterpret_cast<const double*>(box + x * 128 + ((((k >> 1) ^ (x & 7))) << 4) + ((k & 1) << 3));
+}
+
+__global__ void __launch_bounds__(256, 1) k_syrk_dmma(const __grid_constant__ CUtensorMap map,
+                                                      const DenseTile* __restrict__ tiles, i64 N,
+                                                      double* __restrict__ G) {
+  extern __shared__ __align__(1024) char dm_smem[];
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(dm_smem) + 1023) & ~uintptr_t{1023});
+  __shared__ __align__(8) uint64_t full[kDmStages];
+  const DenseTile t = tiles[blockIdx.x];
+  const int c = t.c;
+  const int a0 = t.bi * kDmT, b0 = t.bj * kDmT;
+  const int ca = static_cast<int>(t.pcol) + a0, cb = static_cast<int>(t.pcol) + b0;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  const int wa = (w >> 1) * 32, wb = (w & 1) * 64;
+  const int nch = static_cast<int>((N + kDmKC - 1) / kDmKC);
+  if (tid == 0) {
+    for (int i = 0; i < kDmStages; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int ch) {
+    const int st = ch % kDmStages;
+    char* sb = base + st * kDmStageBytes;
+    mbar_expect(&full[st], kDmStageBytes);
+    const int k0 = ch * kDmKC;
+    tma_load_2d(sb, &map, k0, ca, &full[st]);
+    tma_load_2d(sb + kDmBox, &map, k0 + 16, ca, &full[st]);
+    tma_load_2d(sb + 2 * kDmBox, &map, k0, cb, &full[st]);
+    tma_load_2d(sb + 3 * kDmBox, &map, k0 + 16, cb, &full[st]);
+  };
+  if (tid == 0)
+    for (int ch = 0; ch < kDmStages - 1 && ch < nch; ++ch) issue(ch);
+  double acc[4][8][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int st = ch % kDmStages;
+    if (tid == 0 && ch + kDmStages - 1 < nch) issue(ch + kDmStages - 1);
+    mbar_wait(&full[st], static_cast<uint32_t>((ch / kDmStages) & 1));
+    const char* sb = base + st * kDmStageBytes;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const char* Ab = sb + h * kDmBox;
+      const char* Bb = sb + (2 + h) * kDmBox;
+#pragma unroll
+      for (int ks = 0; ks < 16; ks += 4) {
+        double av[4], bv[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = *box_at(Ab, wa + 8 * i + g, ks + tg);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) bv[j] = *box_at(Bb, wb + 8 * j + g, ks + tg);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+      }
+    }
+    __syncthreads();  // the stage is refilled next iteration
+  }
+  double* Gt = G + t.gtile;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int a = a0 + wa + 8 * i + g;
+    if (a >= c) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int b = b0 + wb + 8 * j + 2 * tg + q;
+        if (b >= c) continue;
+        Gt[static_cast<i64>(b) * c + a] = acc[i][j][q];
+        if (t.bi != t.bj) Gt[static_cast<i64>(a) * c + b] = acc[i][j][q];
+      }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    (void)cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  if (!fn) fail(PMMF_CUDA, "gram (DMMA): cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+std::atomic<int>& dense_gram_mode() {
+  static std::atomic<int> m{[] {
+    const char* e = std::getenv("PMMF_B200_GRAM_DMMA");
+    return e && e[0] == '1' ? 1 : 0;
+  }()};
+  return m;
+}
+
 __global__ void k_ptr_at(i64 n, const i64* __restrict__ ptr, const i64* __restrict__ cols, i64* __restrict__ out) {
   const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (i < n) out[i] = ptr[cols[i]];
@@ -325,8 +480,9 @@ void gram_dense(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 u
     }
     return n;
   };
-  const int tm = count_tiles(128) >= 2 * 148 ? 8 : 4;
-  const int bm = 16 * tm;
+  const bool dmma = dense_gram_mode().load() == 1;
+  const int tm = dmma ? 8 : (count_tiles(128) >= 2 * 148 ? 8 : 4);
+  const int bm = dmma ? kDmT : 16 * tm;
   std::vector<DenseTile> tl;
   for (i64 u = v0; u < v1; ++u) {
     const i64 c = off[u + 1] - off[u];
@@ -337,9 +493,11 @@ void gram_dense(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 u
                       static_cast<int32_t>(bj)});
   }
   if (tl.empty()) return;
-  DBuf<double> panel(ncols * N, s);
+  // panel leading dimension: even for TMA (16-byte global strides)
+  const i64 ld = dmma ? (N + 1) / 2 * 2 : N;
+  DBuf<double> panel(ncols * ld, s);
   panel.zero();
-  PMMF_LAUNCH(k_panel_scatter, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, N, a.ptr.get(),
+  PMMF_LAUNCH(k_panel_scatter, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, ld, a.ptr.get(),
               a.row.get(), a.val.get(), panel.get());
   DBuf<DenseTile> dtl(static_cast<i64>(tl.size()), s);
   PMMF_CUDA(cudaMemcpyAsync(dtl.get(), tl.data(), sizeof(DenseTile) * tl.size(), cudaMemcpyHostToDevice, s));
@@ -350,7 +508,19 @@ void gram_dense(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 u
     e1 = EventPool::get().take();
     cudaEventRecord(e0, s);
   }
-  if (tm == 8) {
+  if (dmma) {
+    CUtensorMap map{};
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(ncols)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(kDmT)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, panel.get(), dims, strides, box,
+                                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(PMMF_CUDA, "gram (DMMA): tensor map encode failed (" + std::to_string(r) + ")");
+    PMMF_CUDA(cudaFuncSetAttribute(k_syrk_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, kDmSmem));
+    PMMF_LAUNCH(k_syrk_dmma, static_cast<unsigned>(tl.size()), 256, kDmSmem, s, map, dtl.get(), N, G);
+  } else if (tm == 8) {
     PMMF_CUDA(cudaFuncSetAttribute(k_syrk_seq<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     PMMF_LAUNCH(k_syrk_seq<8>, static_cast<unsigned>(tl.size()), 256, smem, s, dtl.get(), N, panel.get(), G);
   } else {
@@ -369,13 +539,13 @@ void gram_dense(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 u
     cudaEventElapsedTime(&ms, e0, e1);
     EventPool::get().give(e0);
     EventPool::get().give(e1);
-    prof_add_n("gram_dense", 1, ms, flops);
+    prof_add_n(dmma ? "gram_dmma" : "gram_dense", 1, ms, flops);
   }
   if (trace_enabled()) {
     PMMF_CUDA(cudaStreamSynchronize(s));
-    std::fprintf(stderr, "[pmmf]   gram dense: %lld clusters, %lld columns x %lld rows, %zu tiles of %d, %.3g flop\n",
-                 static_cast<long long>(v1 - v0), static_cast<long long>(ncols), static_cast<long long>(N), tl.size(),
-                 bm, flops);
+    std::fprintf(stderr, "[pmmf]   gram dense%s: %lld clusters, %lld columns x %lld rows, %zu tiles of %d, %.3g flop\n",
+                 dmma ? " (DMMA)" : "", static_cast<long long>(v1 - v0), static_cast<long long>(ncols),
+                 static_cast<long long>(N), tl.size(), bm, flops);
   }
 }
 
@@ -449,3 +619,11 @@ void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const
 }
 
 }  // namespace pmmf_b200
+
+extern "C" int pmmf_b200_set_dense_gram(int32_t mode) {
+  if (mode != 0 && mode != 1) return PMMF_INVALID_ARGUMENT;
+  pmmf_b200::dense_gram_mode().store(mode);
+  return PMMF_OK;
+}
+extern "C" int32_t pmmf_b200_get_dense_gram(void) { return pmmf_b200::dense_gram_mode().load(); }
+
