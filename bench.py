@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--scale", type=int, default=20, help="R-MAT scale (20 = BASELINE config 4)")
     ap.add_argument("--cpu-scale", type=int, default=14, help="R-MAT scale of the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gram", default="seq", choices=["seq", "dmma"],
+                    help="dense Gram kernel: bitwise sequential SYRK (default) or FP64 tensor cores (DMMA)")
     ap.add_argument("--launch-list", action="store_true",
                     help="run exactly one factorization step and exit (for the ncu launch list / traffic passes)")
     return ap.parse_args()
@@ -269,7 +271,7 @@ DATA = "synthetic (seeded SURVEY.md §8(d) recipes, s_in = 42); inputs > L2 (no 
 def config_dict(args, W, n, nnz, params, world):
     """The workload both arms report (the reference arm times a bounded
     sample of it, described in its cpu_baseline.sample)."""
-    return {"workload": W["desc"] if args.workload != "c4" else
+    return {"dense_gram": getattr(args, "gram", "seq"),"workload": W["desc"] if args.workload != "c4" else
             f"config 4: R-MAT scale {args.scale} epv 32, normalized Laplacian + 1e-2 I",
             "n": int(n), "nnz": int(nnz), "k": int(params.k), "P": int(params.n_stages),
             "m": int(params.m_target), "c_max": int(params.c_max),
@@ -469,6 +471,7 @@ def main():
                                          ctypes.POINTER(ctypes.c_double)]
     L.pmmf_b200_profile_enable.argtypes = [ctypes.c_int32]
     params = config_params(args.workload)
+    api.set_dense_gram(1 if args.gram == "dmma" else 0)
     n, rows, cols, vals = workload(args.scale, args.workload)
     d_rows = torch.from_numpy(rows).cuda()
     d_cols = torch.from_numpy(cols).cuda()
@@ -564,7 +567,7 @@ def main():
     torch.cuda.synchronize()
     prof_step_ms = (time.perf_counter() - prof_step_ms) * 1e3
     prof = {}
-    for name in ("rotate_write", "rotate_count", "gram_dense"):
+    for name in ("rotate_write", "rotate_count", "gram_dense", "gram_dmma"):
         c, ms, by = ctypes.c_int64(), ctypes.c_double(), ctypes.c_double()
         if L.pmmf_b200_profile_read(name.encode(), ctypes.byref(c), ctypes.byref(ms), ctypes.byref(by)) == 0:
             prof[name] = (c.value, ms.value, by.value)
@@ -603,12 +606,16 @@ def main():
             c2, ms2, by2 = prof["rotate_count"]
             roof["count_pass"] = {"launches": c2, "ms": ms2, "achieved_GBs": (by2 / 1e9) / (ms2 / 1e3) if ms2 else 0.0}
 
-    if args.workload == "c3" and "gram_dense" in prof:
-        # dense Gram (bitwise sequential SYRK on the FP64 pipe) against cuBLAS DGEMM
-        c, ms, fl = prof["gram_dense"]
+    gname = "gram_dmma" if args.gram == "dmma" else "gram_dense"
+    if args.workload == "c3" and gname in prof:
+        # dense Gram against cuBLAS DGEMM: the bitwise sequential SYRK on the
+        # FP64 pipe, or the DMMA tensor-core SYRK (--gram dmma)
+        c, ms, fl = prof[gname]
         tf = (fl / 1e12) / (ms / 1e3) if ms > 0 else 0.0
         pk = fp64_peak()
-        roof = {"bound": "fp64", "kernel": "k_syrk_seq (dense Gram, sequential row order, unfused mul/add)",
+        kname = ("k_syrk_dmma (dense Gram, FP64 tensor cores: DMMA m8n8k4, TMA-staged)" if args.gram == "dmma" else
+                 "k_syrk_seq (dense Gram, sequential row order, unfused mul/add)")
+        roof = {"bound": "tensor" if args.gram == "dmma" else "fp64", "kernel": kname,
                 "achieved": tf, "peak": pk, "unit": "TFLOP/s", "frac": tf / pk, "traffic": None, "launches": c,
                 "kernel_ms_total": ms, "algorithmic_flops_total": fl,
                 "peak_source": "measured live: cuBLAS DGEMM (torch.matmul fp64 8192^3, best of 5)",

@@ -145,6 +145,22 @@ def shard_ranges(sizes, nnz, nranks: int) -> np.ndarray:
     return lo
 
 
+def set_dense_gram(mode: int) -> None:
+    """Dense-cluster Gram kernel (pmmf_b200_set_dense_gram): 0 = bitwise SIMT
+    SYRK (default), 1 = FP64 tensor cores (DMMA; the near-tie clause)."""
+    L = library().lib
+    L.pmmf_b200_set_dense_gram.argtypes = [ctypes.c_int32]
+    L.pmmf_b200_set_dense_gram.restype = ctypes.c_int
+    if L.pmmf_b200_set_dense_gram(int(mode)) != 0:
+        raise abi.InvalidArgument(1, "set_dense_gram: mode must be 0 or 1")
+
+
+def get_dense_gram() -> int:
+    L = library().lib
+    L.pmmf_b200_get_dense_gram.restype = ctypes.c_int32
+    return int(L.pmmf_b200_get_dense_gram())
+
+
 def kernel_launches() -> int:
     return int(library().lib.pmmf_b200_kernel_launches())
 
