@@ -355,9 +355,11 @@ int64_t pmmf_b200_kernel_launches(void);
 void pmmf_b200_profile_enable(int32_t on);
 int pmmf_b200_profile_read(const char* name, int64_t* launches, double* ms, double* bytes);
 
-/* Device memory kept between calls: the library caches whole large blocks
- * (>= 32 MB) for reuse by later factorizations (mapping fresh memory costs
- * ~80 ms per GB).  Returns the cached bytes on `device`; with release != 0
+/* Device memory kept between calls: the library allocates from its own
+ * stream-ordered memory pool per device (never the device's default pool,
+ * whose attributes stay the caller's), keeps freed pool memory mapped, and
+ * caches whole large blocks (>= 32 MB) for reuse by later factorizations
+ * (mapping fresh memory costs ~80 ms per GB).  Returns the cached bytes on `device`; with release != 0
  * the cache is returned to the device pool and the pool trimmed first
  * (returns 0 then).  Blocks in use are never affected. */
 int64_t pmmf_b200_cached_bytes(int32_t device, int32_t release);

@@ -298,8 +298,10 @@ int64_t pmmf_b200_cached_bytes(int32_t device, int32_t release) {
       BigCache::get().drain(device, s);
       cudaStreamSynchronize(s);
       cudaStreamDestroy(s);
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+      try {
+        cudaMemPoolTrimTo(lib_pool(device), 0);
+      } catch (...) {
+      }
     }
     (void)cudaGetLastError();
   }

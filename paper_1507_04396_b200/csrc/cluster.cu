@@ -1039,39 +1039,53 @@ __global__ void k_cand_back(i64 C, const int64_t* __restrict__ pos, const int32_
 // members of clusters that started below c_min (clusters only grow, so no
 // other column can be orphaned), in pool (ascending global) order, with
 // their rows of the P_c x m score table.  Per dissolution: the first alive
-// cluster of minimal size (ascending index, the reference's alive vector),
+// cluster of minimal size (ascending index, the reference's alive vector);
 // its members = candidates currently in it, in candidate order (= the
-// sorted order the reference visits), each sent to the first strict-max
-// alive anchor with a positive score, else round-robin over the alive list.
+// sorted order the reference visits).  An orphan's target does not depend
+// on the other orphans' (only the round-robin counter does), so every
+// orphan's first strict-max alive anchor with a positive score is found in
+// parallel, warp per orphan; thread 0 then assigns them in order, the
+// zero-score ones round-robin over the alive list.  State lives in shared
+// memory when it fits (sizes, alive list, candidate assignments, orphan
+// list, targets), else in the global scratch passed in.
 constexpr int kRepairThreads = 1024;
 __global__ void __launch_bounds__(kRepairThreads) k_repair(i64 C, int m, i64 c_min, const double* __restrict__ table,
-                                                           int32_t* __restrict__ cur, i64* __restrict__ sizes,
-                                                           int32_t* __restrict__ alive, int32_t* __restrict__ orphans) {
+                                                           int32_t* __restrict__ cur_g, i64* __restrict__ sizes_g,
+                                                           int32_t* __restrict__ scratch, bool in_smem) {
   using BlockScan = cub::BlockScan<int, kRepairThreads>;
   __shared__ typename BlockScan::TempStorage scan;
-  __shared__ i64 rv[32];
-  __shared__ int ri[32];
-  __shared__ double rs[32];
+  __shared__ int rv[32], ri[32];
   __shared__ int s_worst, s_wpos, s_norph, s_nalive;
+  extern __shared__ int32_t rep_smem[];
+  int32_t* base = in_smem ? rep_smem : scratch;
+  int32_t* sz = base;             // m
+  int32_t* alive = sz + m;        // m
+  int32_t* cur = alive + m;       // C
+  int32_t* orph = cur + C;        // C
+  int32_t* res = orph + C;        // C
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  for (int a = tid; a < m; a += blockDim.x) alive[a] = a;
+  for (int a = tid; a < m; a += blockDim.x) {
+    sz[a] = static_cast<int32_t>(sizes_g[a]);
+    alive[a] = a;
+  }
+  for (i64 c = tid; c < C; c += blockDim.x) cur[c] = cur_g[c];
   if (tid == 0) s_nalive = m;
   __syncthreads();
+  int orr = 0;  // thread 0's round-robin counter of the current dissolution
   for (;;) {
     const int na = s_nalive;
     if (na <= 1) break;
     // first alive position of minimal size
-    i64 bv = 0x7fffffffffffffffll;
-    int bi = 0x7fffffff;
+    int bv = 0x7fffffff, bi = 0x7fffffff;
     for (int i = tid; i < na; i += blockDim.x) {
-      const i64 v = sizes[alive[i]];
+      const int v = sz[alive[i]];
       if (v < bv || (v == bv && i < bi)) {
         bv = v;
         bi = i;
       }
     }
     for (int o = 16; o; o >>= 1) {
-      const i64 ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov < bv || (ov == bv && oi < bi)) {
         bv = ov;
@@ -1093,15 +1107,20 @@ __global__ void __launch_bounds__(kRepairThreads) k_repair(i64 C, int m, i64 c_m
       s_worst = alive[bi];
     }
     __syncthreads();
-    const int worst = s_worst;
-    if (sizes[worst] >= c_min) break;
-    // erase it from the alive list (order preserved; na <= m)
-    if (tid == 0) {
-      for (int i = s_wpos; i + 1 < na; ++i) alive[i] = alive[i + 1];
-      s_nalive = na - 1;
+    const int worst = s_worst, wpos = s_wpos;
+    if (sz[worst] >= c_min) break;
+    // erase it from the alive list (order preserved): read, sync, write
+    if (na - wpos <= 2 * kRepairThreads) {
+      int nxt[2];
+      int k = 0;
+      for (int i = wpos + tid; i + 1 < na; i += blockDim.x) nxt[k++] = alive[i + 1];
+      __syncthreads();
+      k = 0;
+      for (int i = wpos + tid; i + 1 < na; i += blockDim.x) alive[i] = nxt[k++];
+    } else {
+      if (tid == 0)
+        for (int i = wpos; i + 1 < na; ++i) alive[i] = alive[i + 1];
     }
-    __syncthreads();
-    const int nal = s_nalive;
     // orphans in candidate order: per-thread contiguous chunks + block scan
     const i64 per = (C + blockDim.x - 1) / blockDim.x;
     const i64 c0 = tid * per, c1 = min(C, c0 + per);
@@ -1110,51 +1129,49 @@ __global__ void __launch_bounds__(kRepairThreads) k_repair(i64 C, int m, i64 c_m
     int off = 0, total = 0;
     BlockScan(scan).ExclusiveSum(cnt, off, total);
     for (i64 c = c0; c < c1; ++c)
-      if (cur[c] == worst) orphans[off++] = static_cast<int32_t>(c);
-    if (tid == 0) s_norph = total;
+      if (cur[c] == worst) orph[off++] = static_cast<int32_t>(c);
+    if (tid == 0) {
+      s_norph = total;
+      s_nalive = na - 1;
+    }
     __syncthreads();
-    const int norph = s_norph;
-    int orr = 0;
-    for (int q = 0; q < norph; ++q) {
-      const i64 o = orphans[q];
-      const double* sr = table + o * m;
+    const int norph = s_norph, nal = na - 1;
+    // every orphan's target, warp per orphan
+    for (int q = wid; q < norph; q += nw) {
+      const double* sr = table + static_cast<i64>(orph[q]) * m;
       double bs = 0.0;
       int bp = 0x7fffffff;
-      for (int i = tid; i < nal; i += blockDim.x) {
+      for (int i = lane; i < nal; i += 32) {
         const double sc = sr[alive[i]];
-        if (sc > bs || (sc == bs && sc > 0.0 && i < bp)) {
+        if (sc > bs) {  // lanes visit increasing i: strict > keeps the first
           bs = sc;
           bp = i;
         }
       }
-      for (int o2 = 16; o2; o2 >>= 1) {
-        const double os = __shfl_xor_sync(0xffffffffu, bs, o2);
-        const int op = __shfl_xor_sync(0xffffffffu, bp, o2);
-        if (os > bs || (os == bs && os > 0.0 && op < bp)) {
+      for (int o = 16; o; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+        if (os > bs || (os == bs && op < bp)) {
           bs = os;
           bp = op;
         }
       }
-      if (lane == 0) {
-        rs[wid] = bs;
-        ri[wid] = bp;
-      }
-      __syncthreads();
-      if (tid == 0) {
-        for (int w = 1; w < nw; ++w)
-          if (rs[w] > bs || (rs[w] == bs && rs[w] > 0.0 && ri[w] < bp)) {
-            bs = rs[w];
-            bp = ri[w];
-          }
-        const int a = bs > 0.0 ? alive[bp] : alive[(orr++) % nal];
-        cur[o] = a;
-        ++sizes[a];
-      }
-      __syncthreads();
+      if (lane == 0) res[q] = bs > 0.0 ? bp : -1;
     }
-    if (tid == 0) sizes[worst] = 0;
+    __syncthreads();
+    if (tid == 0) {
+      orr = 0;
+      for (int q = 0; q < norph; ++q) {
+        const int a = res[q] >= 0 ? alive[res[q]] : alive[(orr++) % nal];
+        cur[orph[q]] = a;
+        ++sz[a];
+      }
+      sz[worst] = 0;
+    }
     __syncthreads();
   }
+  for (int a = tid; a < m; a += blockDim.x) sizes_g[a] = sz[a];
+  for (i64 c = tid; c < C; c += blockDim.x) cur_g[c] = cur[c];
 }
 
 template <typename In, typename T>
@@ -1260,13 +1277,18 @@ void recurse(DevCtx& ctx, int32_t* seg, i64 P, i64 m_request, int depth, Xoshiro
     DBuf<int64_t> cpos(P, s);
     i64 C = 0;
     stable_select(cub::CountingInputIterator<int64_t>(0), cf.get(), P, cpos.get(), &C, s);
-    DBuf<int32_t> csid(C, s), cur(C, s), orph(C, s), alive(m, s);
+    DBuf<int32_t> csid(C, s), cur(C, s);
     DBuf<double> cn(C, s), table(C * m, s);
+    const size_t rep_bytes = sizeof(int32_t) * static_cast<size_t>(2 * m + 3 * C);
+    const bool rep_smem = rep_bytes <= 160 * 1024;
+    DBuf<int32_t> rep_scratch(rep_smem ? 1 : 2 * m + 3 * C, s);
+    if (rep_smem && rep_bytes > 48 * 1024)
+      PMMF_CUDA(cudaFuncSetAttribute(k_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rep_bytes)));
     PMMF_LAUNCH(k_cand_take, blocks_for(C, kThreads), kThreads, 0, s, C, cpos.get(), sid.get(), nrm.get(),
                 assign.get(), csid.get(), cn.get(), cur.get());
     ctx.sc->run(csid.get(), cn.get(), C, asid.get(), anrm.get(), static_cast<int>(m), true, nullptr, table.get());
-    PMMF_LAUNCH(k_repair, 1, kRepairThreads, 0, s, C, static_cast<int>(m), ctx.c_min, table.get(), cur.get(),
-                dsz.get(), alive.get(), orph.get());
+    PMMF_LAUNCH(k_repair, 1, kRepairThreads, rep_smem ? rep_bytes : 0, s, C, static_cast<int>(m), ctx.c_min,
+                table.get(), cur.get(), dsz.get(), rep_scratch.get(), rep_smem);
     PMMF_LAUNCH(k_cand_back, blocks_for(C, kThreads), kThreads, 0, s, C, cpos.get(), cur.get(), assign.get());
     sz = dsz.to_host(m);
     nalive = 0;

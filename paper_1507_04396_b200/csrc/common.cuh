@@ -269,6 +269,32 @@ struct EventPool {
   }
 };
 
+// The library's own stream-ordered memory pool per device (not the device's
+// default pool, whose settings belong to the process: torch and other
+// cudaMallocAsync users).  Freed blocks stay mapped (release threshold =
+// max): re-mapping tens of GB per stage costs seconds; pool_alloc trims it
+// when fragmentation alone fails a request, pmmf_b200_cached_bytes(dev, 1)
+// hands everything back.
+inline cudaMemPool_t lib_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  PMMF_CUDA(cudaMemPoolCreate(&pool, &props));
+  uint64_t thr = ~uint64_t{0};
+  if (const char* e = std::getenv("PMMF_B200_POOL_KEEP_GB")) thr = static_cast<uint64_t>(std::atof(e) * 1073741824.0);
+  PMMF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  pools[dev] = pool;
+  return pool;
+}
+
 // Device memory a new allocation can still get: free memory, the pool's
 // reserved-but-unused blocks and the cached large blocks.
 inline i64 available_bytes() {
@@ -276,8 +302,7 @@ inline i64 available_bytes() {
   PMMF_CUDA(cudaMemGetInfo(&f, &t));
   int dev = 0;
   PMMF_CUDA(cudaGetDevice(&dev));
-  cudaMemPool_t pool;
-  PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  cudaMemPool_t pool = lib_pool(dev);
   uint64_t reserved = 0, used = 0;
   PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
   PMMF_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
@@ -309,17 +334,15 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
     cudaStreamSynchronize(st);
     t0 = std::chrono::steady_clock::now();
   }
-  cudaError_t e = cudaMallocAsync(p, *bytes, st);
+  cudaError_t e = cudaMallocFromPoolAsync(p, *bytes, lib_pool(dev), st);
   if (e == cudaErrorMemoryAllocation) {
     (void)cudaGetLastError();
     PMMF_CUDA(cudaStreamSynchronize(st));
     BigCache::get().drain(dev, st);
     PMMF_CUDA(cudaStreamSynchronize(st));
-    cudaMemPool_t pool;
-    PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    PMMF_CUDA(cudaMemPoolTrimTo(pool, 0));
+    PMMF_CUDA(cudaMemPoolTrimTo(lib_pool(dev), 0));
     if (trace_enabled()) std::fprintf(stderr, "[pmmf]   pool trimmed for a %zu MB request\n", *bytes >> 20);
-    e = cudaMallocAsync(p, *bytes, st);
+    e = cudaMallocFromPoolAsync(p, *bytes, lib_pool(dev), st);
   }
   PMMF_CUDA(e);
   if (AllocCheck::on()) AllocCheck::get().add(*p, *bytes, "malloc");
@@ -340,7 +363,7 @@ inline void pool_free(void* p, size_t bytes, cudaStream_t st) {
   }
 }
 
-// Stream-ordered device buffer (cudaMallocAsync from the device pool).
+// Stream-ordered device buffer (from the library's pool, lib_pool).
 template <typename T>
 struct DBuf {
   T* p = nullptr;

@@ -184,17 +184,6 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   const int W = C.world();
   const std::vector<int> my_ranks = C.local_ranks();
   PMMF_CUDA(cudaSetDevice(in->device));
-  {
-    // The stream-ordered pool keeps freed blocks mapped across
-    // synchronisations (re-mapping tens of GB per stage costs seconds);
-    // pool_alloc trims it when fragmentation alone fails a request.
-    cudaMemPool_t pool;
-    PMMF_CUDA(cudaDeviceGetDefaultMemPool(&pool, in->device));
-    uint64_t thr = ~uint64_t{0};
-    if (const char* e = std::getenv("PMMF_B200_POOL_KEEP_GB"))
-      thr = static_cast<uint64_t>(std::atof(e) * 1073741824.0);
-    PMMF_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  }
   const auto fn_start = clk::now();
   StreamGuard sg;
   cudaStream_t s = sg.s;

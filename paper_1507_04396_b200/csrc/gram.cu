@@ -453,7 +453,16 @@ void gram_sparse(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 
               csr_col.get(), csr_val.get());
   idx2.release();
   ecol.release();
-  PMMF_LAUNCH(k_gram_owner, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, e0, a.ptr.get(),
+  // Resident warps bound the live accumulator columns (c doubles each) that
+  // compete for L2; unused dynamic shared memory caps the warps per SM
+  // (PMMF_B200_GRAM_OWNER_SMEM bytes per 256-thread block, tuning hook).
+  static const int owner_smem = [] {
+    const char* e = std::getenv("PMMF_B200_GRAM_OWNER_SMEM");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (owner_smem > 48 * 1024)
+    PMMF_CUDA(cudaFuncSetAttribute(k_gram_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, owner_smem));
+  PMMF_LAUNCH(k_gram_owner, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, col0, ncols, e0, a.ptr.get(),
               a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco, dct, dcc, G);
   if (trace_enabled()) {  // products = sum over entries of their row-run length (the reference's count)
     DBuf<unsigned long long> tot(1, s);

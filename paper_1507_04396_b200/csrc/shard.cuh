@@ -26,6 +26,7 @@
 // decomposition bit-exact on a single device.
 #pragma once
 
+#include <utility>
 #include <vector>
 
 #include "engine.cuh"
@@ -71,6 +72,36 @@ void bcast_segments(void* dev, size_t elem, const std::vector<i64>& seg, const C
 // max over ranks of one device int32 (no-op for one process).
 void allreduce_max_i32(int32_t* dev, const Comm& c, cudaStream_t s);
 void allreduce_max_i32(int32_t* dev, i64 n, const Comm& c, cudaStream_t s);
+
+// ---- owned-column slabs -------------------------------
+// A slab is a full-width Csc (N columns, rows over all N ids) whose entries
+// lie in the column range its rank owns; the other columns are empty.
+
+// sum / max over ranks of device arrays (no-op for one process; virtual
+// ranks write disjoint parts of one buffer instead).
+void allreduce_sum_i64(int64_t* dev, i64 n, const Comm& c, cudaStream_t s);
+void allreduce_sum_f64(double* dev, i64 n, const Comm& c, cudaStream_t s);
+void allreduce_max_f64(double* dev, i64 n, const Comm& c, cudaStream_t s);
+
+// out = the columns [c0, c1) of a (full width).
+void slab_of(Csc& out, const Csc& a, i64 c0, i64 c1, cudaStream_t s);
+
+// Columns cols[0..m) (stage ids, device) gathered from their owners into
+// every rank: a full-width Csc holding exactly those columns.  slabs[i] is
+// local rank i's slab, owning [own[i], own[i+1]) ... given as pairs.
+void gather_columns(Csc& out, const std::vector<const Csc*>& slabs,
+                    const std::vector<std::pair<i64, i64>>& own, const int32_t* cols, int m, i64 N,
+                    const Comm& c, cudaStream_t s);
+
+// out = a with b's columns added where a's are empty (full width).
+void merge_columns(Csc& out, const Csc& a, const Csc& b, cudaStream_t s);
+
+// The all-to-all reblock exchange: slabs[i] (local rank i, any columns) are
+// replaced by the slabs of the new ownership, rank r holding exactly the
+// columns [dest[r], dest[r+1]) gathered from every rank (ncclSend/ncclRecv
+// across processes; buffer moves between virtual ranks).  Every column
+// comes from exactly one source, entries are copied unchanged.
+void redistribute(std::vector<Csc>& slabs, const std::vector<i64>& dest, i64 N, const Comm& c, cudaStream_t s);
 
 // The full matrix from the per-rank column slabs: parts[i] holds (over all
 // N columns) only the columns [col_seg[r], col_seg[r+1]) of local rank
