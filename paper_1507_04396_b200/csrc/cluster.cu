@@ -18,6 +18,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <memory>
 #include <numeric>
 #include <unordered_map>
 
@@ -37,11 +38,13 @@ constexpr int kThreads = 256;
 // flushed into the outer sum at block changes) through shuffles.
 __global__ void k_norms(i64 P, const int32_t* __restrict__ cols, const i64* __restrict__ ptr,
                         const int32_t* __restrict__ row, const double* __restrict__ val,
-                        const int32_t* __restrict__ blk, double* __restrict__ norm, i64 long_len) {
+                        const int32_t* __restrict__ blk, double* __restrict__ norm, i64 long_len, i64 c0,
+                        i64 c1) {
   const i64 p = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= P) return;
   const int32_t j = cols[p];
+  if (j < c0 || j >= c1) return;               // another rank's column
   if (ptr[j + 1] - ptr[j] > long_len) return;  // k_norms_long
   double s = 0.0, inner = 0.0;
   int32_t cur = -1;
@@ -665,7 +668,8 @@ struct Scorer {
   const Csc& a;
   const Numbering& nb;
   cudaStream_t s;
-  const Comm* comm = nullptr;  // sharded scoring (shard.cuh) when it spans several ranks
+  const Comm* comm = nullptr;  // (round-robin split of the sparse list; unused: owned-column scoring, score())
+  int force_gemm = -1;         // >= 0: the GEMM / sparse choice made for the whole matrix
   DBuf<int32_t> self;  // stage id -> anchor pos (assignment mode)
 
   Scorer(const Csc& mat, const Numbering& numbering, cudaStream_t st) : a(mat), nb(numbering), s(st) {
@@ -912,6 +916,7 @@ struct Scorer {
   // entries stored (PMMF_B200_SCORE_GEMM=1/0 forces it on/off for tests).
   bool gemm_mode() const {
     if (const char* e = std::getenv("PMMF_B200_SCORE_GEMM")) return std::atoi(e) != 0;
+    if (force_gemm >= 0) return force_gemm != 0;
     const double N = static_cast<double>(a.N);
     return a.N > 0 && static_cast<double>(a.nnz) >= 0.25 * N * N;
   }
@@ -1185,7 +1190,10 @@ void stable_select(In in, const uint8_t* flags, i64 n, T* out, i64* count, cudaS
 }
 
 struct DevCtx {
-  Scorer* sc;
+  Scorer* sc;            // one-GPU path
+  const SlabSet* ss;     // sharded path (sc == nullptr)
+  const Numbering* nb;
+  int gemm = -1;         // sharded: the scorer path chosen for the whole matrix
   const int32_t* g2s;    // device: global -> stage id
   const double* norm_g;  // device: norm by global id
   i64 c_min, c_max;
@@ -1193,6 +1201,101 @@ struct DevCtx {
   int max_depth = 0;
   cudaStream_t s;
 };
+
+__global__ void k_own_flags(i64 P, const int32_t* __restrict__ sid, i64 c0, i64 c1, uint8_t* __restrict__ f) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < P) f[i] = sid[i] >= c0 && sid[i] < c1 ? 1 : 0;
+}
+__global__ void k_take_pos(i64 n, const int64_t* __restrict__ pos, const int32_t* __restrict__ sid,
+                           const double* __restrict__ nrm, int32_t* __restrict__ osid, double* __restrict__ on) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  osid[i] = sid[pos[i]];
+  on[i] = nrm[pos[i]];
+}
+__global__ void k_put_assign(i64 n, const int64_t* __restrict__ pos, const int32_t* __restrict__ v,
+                             int32_t* __restrict__ out) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i < n) out[pos[i]] = v[i];
+}
+__global__ void k_put_rows(i64 n, int m, const int64_t* __restrict__ pos, const double* __restrict__ v,
+                           double* __restrict__ out) {
+  const i64 x = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (x >= n * m) return;
+  out[pos[x / m] * m + x % m] = v[x];
+}
+
+// Scores of a pool against anchors (Scorer::run's contract).  Sharded: the
+// anchor columns are gathered to every rank; each rank scores the pool
+// columns it owns on its slab plus those anchor columns, with exactly the
+// one-GPU kernels, and the results meet by a max over ranks (sentinel -2^31
+// for unscored positions, 0.0 in rows mode; scores are >= 0).
+void score(DevCtx& ctx, const int32_t* dpool, const double* dpn, i64 P, const int32_t* danch, const double* dan,
+           int m, bool rows_mode, int32_t* assign_out, double* rows_out) {
+  if (!ctx.ss) {
+    ctx.sc->run(dpool, dpn, P, danch, dan, m, rows_mode, assign_out, rows_out);
+    return;
+  }
+  cudaStream_t s = ctx.s;
+  const SlabSet& ss = *ctx.ss;
+  const Comm& comm = *ss.comm;
+  const i64 N = ctx.nb->size();
+  Csc anch;
+  gather_columns(anch, ss.slabs, ss.own, danch, m, N, comm, s);
+  if (rows_mode)
+    PMMF_CUDA(cudaMemsetAsync(rows_out, 0, sizeof(double) * P * m, s));
+  else
+    PMMF_CUDA(cudaMemsetAsync(assign_out, 0x80, sizeof(int32_t) * P, s));
+  static const bool st_timing = std::getenv("PMMF_B200_SHARD_TIMING") != nullptr || trace_enabled();
+  double tsum = 0.0, tmax = 0.0;
+  for (size_t i = 0; i < ss.slabs.size(); ++i) {
+    if (st_timing) PMMF_CUDA(cudaStreamSynchronize(s));
+    const auto tr0 = std::chrono::steady_clock::now();
+    struct Lap {  // per-rank time of this scoring call (scripts/shard_model.py)
+      bool on;
+      cudaStream_t s;
+      std::chrono::steady_clock::time_point t0;
+      double *sum, *mx;
+      ~Lap() {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        *sum += ms;
+        *mx = std::max(*mx, ms);
+      }
+    } lap{st_timing, s, tr0, &tsum, &tmax};
+    DBuf<uint8_t> f(P, s);
+    PMMF_LAUNCH(k_own_flags, blocks_for(P, kThreads), kThreads, 0, s, P, dpool, ss.own[i].first, ss.own[i].second,
+                f.get());
+    DBuf<int64_t> pos(P, s);
+    i64 Pi = 0;
+    stable_select(cub::CountingInputIterator<int64_t>(0), f.get(), P, pos.get(), &Pi, s);
+    if (Pi == 0) continue;
+    DBuf<int32_t> sub(Pi, s);
+    DBuf<double> subn(Pi, s);
+    PMMF_LAUNCH(k_take_pos, blocks_for(Pi, kThreads), kThreads, 0, s, Pi, pos.get(), dpool, dpn, sub.get(),
+                subn.get());
+    Csc M;
+    merge_columns(M, *ss.slabs[i], anch, s);
+    Scorer sc(M, *ctx.nb, s);
+    sc.force_gemm = ctx.gemm;
+    if (rows_mode) {
+      DBuf<double> r(Pi * m, s);
+      sc.run(sub.get(), subn.get(), Pi, danch, dan, m, true, nullptr, r.get());
+      PMMF_LAUNCH(k_put_rows, blocks_for(Pi * m, kThreads), kThreads, 0, s, Pi, m, pos.get(), r.get(), rows_out);
+    } else {
+      DBuf<int32_t> as(Pi, s);
+      sc.run(sub.get(), subn.get(), Pi, danch, dan, m, false, as.get(), nullptr);
+      PMMF_LAUNCH(k_put_assign, blocks_for(Pi, kThreads), kThreads, 0, s, Pi, pos.get(), as.get(), assign_out);
+    }
+  }
+  if (st_timing && comm.virt)
+    std::fprintf(stderr, "[pmmf] shard score: %d ranks, sum %.3f ms, max %.3f ms\n", comm.world(), tsum, tmax);
+  if (rows_mode)
+    allreduce_max_f64(rows_out, P * m, comm, s);
+  else
+    allreduce_max_i32(assign_out, P, comm, s);
+}
 
 // seg: the pool (global ids ascending, device) of one recursion node; on
 // return it holds the node's clusters in DFS order and `sizes` has one entry
@@ -1247,7 +1350,7 @@ void recurse(DevCtx& ctx, int32_t* seg, i64 P, i64 m_request, int depth, Xoshiro
               anrm.get(), static_cast<uint8_t*>(nullptr));
   DBuf<int32_t> assign(P, s);
   const auto t_host0 = std::chrono::steady_clock::now();
-  ctx.sc->run(sid.get(), nrm.get(), P, asid.get(), anrm.get(), static_cast<int>(m), false, assign.get(), nullptr);
+  score(ctx, sid.get(), nrm.get(), P, asid.get(), anrm.get(), static_cast<int>(m), false, assign.get(), nullptr);
   if (trace_enabled() && depth == 0) {
     PMMF_CUDA(cudaStreamSynchronize(s));
     std::fprintf(stderr, "[pmmf]     pool setup %.2f ms, scorer %.2f ms\n",
@@ -1286,7 +1389,7 @@ void recurse(DevCtx& ctx, int32_t* seg, i64 P, i64 m_request, int depth, Xoshiro
       PMMF_CUDA(cudaFuncSetAttribute(k_repair, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(rep_bytes)));
     PMMF_LAUNCH(k_cand_take, blocks_for(C, kThreads), kThreads, 0, s, C, cpos.get(), sid.get(), nrm.get(),
                 assign.get(), csid.get(), cn.get(), cur.get());
-    ctx.sc->run(csid.get(), cn.get(), C, asid.get(), anrm.get(), static_cast<int>(m), true, nullptr, table.get());
+    score(ctx, csid.get(), cn.get(), C, asid.get(), anrm.get(), static_cast<int>(m), true, nullptr, table.get());
     PMMF_LAUNCH(k_repair, 1, kRepairThreads, rep_smem ? rep_bytes : 0, s, C, static_cast<int>(m), ctx.c_min,
                 table.get(), cur.get(), dsz.get(), rep_scratch.get(), rep_smem);
     PMMF_LAUNCH(k_cand_back, blocks_for(C, kThreads), kThreads, 0, s, C, cpos.get(), cur.get(), assign.get());
@@ -1343,12 +1446,12 @@ __global__ void k_sid_of(i64 P, const int32_t* __restrict__ g, const int32_t* __
 
 }  // namespace
 
-ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vector<i64>& active, i64 n,
+ClusterOut cluster_columns_dev(const SlabSet& ss, const Numbering& nb, const std::vector<i64>& active, i64 n,
                                i64 m_target, i64 c_min, i64 c_max, int d_max, bool bypass, uint64_t seed,
-                               cudaStream_t s, const Comm* comm) {
+                               cudaStream_t s) {
   if (active.empty()) fail(PMMF_INVALID_ARGUMENT, "cluster_columns: empty active set");
   ClusterOut res;
-  // Norms of the active columns (clustering.hpp:189-195).
+  // Norms of the active columns (clustering.hpp:189-195), each by its owner.
   const i64 P = static_cast<i64>(active.size());
   DBuf<int32_t> act(P, s), ids(P, s);
   {
@@ -1357,14 +1460,17 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
   }
   PMMF_LAUNCH(k_sid_of, blocks_for(P, kThreads), kThreads, 0, s, P, act.get(), nb.d_g2s.get(), ids.get());
   DBuf<double> dnorm(P, s), norm_g(std::max<i64>(n, 1), s);
-  {
+  if (ss.sharded()) dnorm.zero();
+  for (size_t i = 0; i < ss.slabs.size(); ++i) {
+    const Csc& a = *ss.slabs[i];
+    const i64 c0 = ss.own[i].first, c1 = ss.own[i].second;
     // columns longer than kLong entries: k_norms_long, a CTA per column
     i64 kLong = 4096;
     if (const char* e = std::getenv("PMMF_B200_NORM_LONG")) kLong = std::atoll(e);  // test hook
     const i64 nblk = nb.clusters();
     const i64 long_len = nblk > 1 ? kLong : (i64{1} << 62);
     PMMF_LAUNCH(k_norms, blocks_for(P * 32, kThreads), kThreads, 0, s, P, ids.get(), a.ptr.get(), a.row.get(),
-                a.val.get(), nb.d_blk.get(), dnorm.get(), long_len);
+                a.val.get(), nb.d_blk.get(), dnorm.get(), long_len, c0, c1);
     if (nblk > 1) {
       DBuf<uint8_t> fl(P, s);
       PMMF_LAUNCH(k_long_flags, blocks_for(P, kThreads), kThreads, 0, s, P, ids.get(), a.ptr.get(), long_len, fl.get());
@@ -1380,6 +1486,7 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
       }
     }
   }
+  if (ss.sharded()) allreduce_max_f64(dnorm.get(), P, *ss.comm, s);
   norm_g.zero();
   DBuf<uint8_t> in_pool(P, s), byp(P, s);
   PMMF_LAUNCH(k_scatter_norm, blocks_for(P, kThreads), kThreads, 0, s, P, act.get(), dnorm.get(), norm_g.get(),
@@ -1397,9 +1504,22 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
   }
   const auto t_norms = std::chrono::steady_clock::now();
   if (np > 0) {
-    Scorer sc(a, nb, s);
-    sc.comm = comm;
-    DevCtx ctx{&sc, nb.d_g2s.get(), norm_g.get(), c_min, c_max, d_max, 0, s};
+    std::unique_ptr<Scorer> sc;
+    DevCtx ctx{nullptr, nullptr, &nb, -1, nb.d_g2s.get(), norm_g.get(), c_min, c_max, d_max, 0, s};
+    if (ss.sharded()) {
+      ctx.ss = &ss;
+      // the scorer path of the whole matrix (GEMM for dense problems)
+      DBuf<int64_t> tot(1, s);
+      int64_t mine = 0;
+      for (const Csc* a : ss.slabs) mine += a->nnz;
+      tot.upload(&mine, 1);
+      allreduce_sum_i64(tot.get(), 1, *ss.comm, s);
+      const double nnz = static_cast<double>(tot.to_host(1)[0]), N = static_cast<double>(nb.size());
+      ctx.gemm = nb.size() > 0 && nnz >= 0.25 * N * N ? 1 : 0;
+    } else {
+      sc = std::make_unique<Scorer>(*ss.slabs[0], nb, s);
+      ctx.sc = sc.get();
+    }
     Xoshiro rng(seed);
     recurse(ctx, res.members.get(), np, m_target, 0, rng, res.sizes);
     res.max_depth = ctx.max_depth;
@@ -1408,7 +1528,7 @@ ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vec
   if (trace_enabled())
     std::fprintf(stderr, "[pmmf]   clustering: %.2f ms after norms (pool %lld, nnz %lld)\n",
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_norms).count(),
-                 static_cast<long long>(P), static_cast<long long>(a.nnz));
+                 static_cast<long long>(P), static_cast<long long>(ss.slabs[0]->nnz));
   return res;
 }
 

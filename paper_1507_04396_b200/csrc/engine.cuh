@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -81,13 +82,23 @@ struct ClusterOut {
   std::vector<i64> bypassed;  // ascending global ids
   int max_depth = 0;
 };
-// cluster_columns (clustering.hpp:183-225) over the pre-reblock matrix a
+// cluster_columns (clustering.hpp:183-225) over the pre-reblock matrix
 // (numbering nb); active ascending global ids.
 struct Comm;
-// comm: score the sparse pool columns sharded over its ranks (shard.cuh).
-ClusterOut cluster_columns_dev(const Csc& a, const Numbering& nb, const std::vector<i64>& active, i64 n,
+// The owned-column slabs of this process's ranks (shard.cuh): slabs[i]
+// holds the columns [own[i].first, own[i].second) of the matrix.  With one
+// slab owning everything and no communicator the clustering is the one-GPU
+// path.  Sharded: the norms and scores of a column are computed by its
+// owner (the anchor columns gathered to every rank), combined by max.
+struct SlabSet {
+  std::vector<const Csc*> slabs;
+  std::vector<std::pair<i64, i64>> own;
+  const Comm* comm = nullptr;
+  bool sharded() const { return comm != nullptr; }
+};
+ClusterOut cluster_columns_dev(const SlabSet& ss, const Numbering& nb, const std::vector<i64>& active, i64 n,
                                i64 m_target, i64 c_min, i64 c_max, int d_max, bool bypass, uint64_t seed,
-                               cudaStream_t s, const Comm* comm = nullptr);
+                               cudaStream_t s);
 
 // ---- gram.cu
 // Dense c_u x c_u column-major tiles of G_u (blocked_matrix.hpp:238-254)

@@ -82,10 +82,12 @@ __device__ __forceinline__ void residual_column(i64 r, int32_t j, const int32_t*
 __global__ void k_residual(i64 R, const int32_t* __restrict__ elim_sid, const i64* __restrict__ ptr,
                            const int32_t* __restrict__ row, const double* __restrict__ val,
                            const int32_t* __restrict__ s2g, const uint8_t* __restrict__ is_active,
-                           const int32_t* __restrict__ rank, double* __restrict__ mass, double* __restrict__ diag) {
+                           const int32_t* __restrict__ rank, double* __restrict__ mass, double* __restrict__ diag,
+                           i64 c0, i64 c1) {
   const i64 r = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   if (r >= R) return;
   const int32_t j = elim_sid[r];
+  if (j < c0 || j >= c1) return;  // another rank's column
   residual_column(r, j, row, val, ptr[j], ptr[j + 1], s2g, is_active, rank, mass, diag);
 }
 
@@ -246,6 +248,38 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       fail(PMMF_INVALID_ARGUMENT, "factorize: input matrix is not symmetric");
   }
 
+  // ---- owned-column slabs (shard.cuh).  One GPU: one slab, the matrix.
+  // Sharded: rank r keeps the columns it owns (full row range); the stage's
+  // clustering, Gram, search and rotation passes run on them, and the
+  // reblock moves columns to their new owners (all-to-all).  Before the
+  // first stage: W contiguous column ranges of about equal nnz.
+  const bool sharded = W > 1 || C.multi_process();
+  std::vector<Csc> slab(my_ranks.size());
+  std::vector<std::pair<i64, i64>> own(my_ranks.size());
+  if (!sharded) {
+    own[0] = {0, A.N};
+    slab[0] = std::move(A);
+  } else {
+    const std::vector<i64> hp = A.ptr.to_host(A.N + 1);
+    std::vector<i64> cut(static_cast<size_t>(W) + 1, A.N);
+    cut[0] = 0;
+    for (int r = 1; r < W; ++r) {
+      const i64 target = A.nnz * r / W;
+      cut[r] = std::max(cut[r - 1], static_cast<i64>(std::lower_bound(hp.begin(), hp.end(), target) - hp.begin()));
+      cut[r] = std::min(cut[r], A.N);
+    }
+    for (size_t li = 0; li < my_ranks.size(); ++li) {
+      own[li] = {cut[my_ranks[li]], cut[my_ranks[li] + 1]};
+      slab_of(slab[li], A, own[li].first, own[li].second, s);
+    }
+    A = Csc();
+  }
+  auto slab_nnz = [&] {
+    i64 t = 0;
+    for (const Csc& x : slab) t += x.nnz;
+    return t;
+  };
+
   const auto run_start = clk::now();
   PMMF_TRACE("[pmmf] prologue (input numbering, from_triplets, symmetry) %.2f ms\n", ms_since(fn_start));
   std::vector<i64> active;
@@ -270,8 +304,12 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     // ---- clustering on the pre-reblock matrix
     auto t0 = clk::now();
     const uint64_t cpath[2] = {0xC1u, static_cast<uint64_t>(stage_no)};
-    ClusterOut co = cluster_columns_dev(A, cur, active, n, p.m_target, p.c_min, p.c_max, p.d_max,
-                                        p.bypass_enabled != 0, derive(p.seed, cpath), s, comm);
+    SlabSet ss;
+    for (const Csc& x : slab) ss.slabs.push_back(&x);
+    ss.own = own;
+    ss.comm = sharded ? &C : nullptr;
+    ClusterOut co = cluster_columns_dev(ss, cur, active, n, p.m_target, p.c_min, p.c_max, p.d_max,
+                                        p.bypass_enabled != 0, derive(p.seed, cpath), s);
     R->phases[0] += ms_since(t0);
     const i64 rc = static_cast<i64>(co.sizes.size());
     std::vector<i64> stage_off(1, 0);
@@ -288,15 +326,23 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
                   nxt.d_g2s.get(), dmap.get());
       PMMF_LAUNCH(k_compose, blocks_for(nxt.size(), kThreads), kThreads, 0, s, nxt.size(), nxt.d_s2g.get(),
                   cur.d_g2s.get(), dn2o.get());
-      Csc B;
-      reblock(B, A, dmap, dn2o, nxt.size(), s);
-      A = std::move(B);
+      for (size_t li = 0; li < slab.size(); ++li) {  // each slab relabelled in place (its columns stay)
+        const auto t_r = clk::now();
+        Csc B;
+        reblock(B, slab[li], dmap, dn2o, nxt.size(), s);
+        slab[li] = std::move(B);
+        if (sharded && shard_timing()) {
+          PMMF_CUDA(cudaStreamSynchronize(s));
+          std::fprintf(stderr, "[pmmf] shard stage %d rank %d: reblock %.3f ms\n", stage_no + 1, my_ranks[li],
+                       ms_since(t_r));
+        }
+      }
     }
     cur = std::move(nxt);
     PMMF_CUDA(cudaStreamSynchronize(s));
     R->phases[4] += ms_since(t0);
     PMMF_TRACE("[pmmf] stage %d: reblock %.2f ms (%lld entries)\n", stage_no + 1, ms_since(t0),
-               static_cast<long long>(A.nnz));
+               static_cast<long long>(slab_nnz()));
 
     Result::Stage st;
     st.off = cur.off;
@@ -326,15 +372,49 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     const i64 slots = out_base[rc];
     // ---- cluster ownership (shard.cuh): rank r owns clusters [lo[r], lo[r+1])
     const i64 nclu = cur.clusters();
-    std::vector<i64> lo{0, nclu}, eptr_c;
+    std::vector<i64> lo{0, nclu};
     if (W > 1) {
-      eptr_c = cluster_ptr(A, cur.off, s);
-      std::vector<i64> csz(static_cast<size_t>(nclu)), cnz(static_cast<size_t>(nclu));
-      for (i64 u = 0; u < nclu; ++u) {
-        csz[u] = cur.off[u + 1] - cur.off[u];
-        cnz[u] = eptr_c[u + 1] - eptr_c[u];
+      std::vector<i64> csz(static_cast<size_t>(nclu)), cnz(static_cast<size_t>(nclu), 0);
+      for (const Csc& x : slab) {  // this rank's entries per new cluster, summed over ranks
+        const std::vector<i64> e = cluster_ptr(x, cur.off, s);
+        for (i64 u = 0; u < nclu; ++u) cnz[u] += e[u + 1] - e[u];
       }
+      if (C.multi_process()) {
+        DBuf<int64_t> d(nclu, s);
+        d.upload(cnz);
+        allreduce_sum_i64(d.get(), nclu, C, s);
+        cnz = d.to_host(nclu);
+      }
+      for (i64 u = 0; u < nclu; ++u) csz[u] = cur.off[u + 1] - cur.off[u];
       lo = shard_ranges(csz, cnz, W);
+    }
+    if (sharded) {
+      // the all-to-all of the reblock: columns to the owners of their clusters
+      const auto t_x = clk::now();
+      std::vector<i64> dest(static_cast<size_t>(W) + 1);
+      for (int r = 0; r <= W; ++r) dest[r] = cur.off[std::min(lo[r], nclu)];
+      if (shard_timing() && C.virt) {  // ingress per rank of the all-to-all (scripts/shard_model.py)
+        std::vector<i64> in_bytes(static_cast<size_t>(W), 0);
+        DBuf<i64> idx(W + 1, s), v(W + 1, s);
+        idx.upload(dest);
+        for (size_t si = 0; si < slab.size(); ++si) {
+          const std::vector<i64> at = cluster_ptr(slab[si], dest, s);
+          for (int d = 0; d < W; ++d)
+            if (d != my_ranks[si]) in_bytes[d] += 12 * (at[d + 1] - at[d]) + 4 * (dest[d + 1] - dest[d]);
+        }
+        std::fprintf(stderr, "[pmmf] shard stage %d: all-to-all ingress max %lld bytes\n", stage_no,
+                     static_cast<long long>(*std::max_element(in_bytes.begin(), in_bytes.end())));
+        PMMF_CUDA(cudaStreamSynchronize(s));
+      }
+      const auto t_rd = clk::now();
+      redistribute(slab, dest, cur.size(), C, s);
+      if (shard_timing()) {
+        PMMF_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[pmmf] shard stage %d: exchange %.3f ms\n", stage_no, ms_since(t_rd));
+      }
+      for (size_t li = 0; li < my_ranks.size(); ++li) own[li] = {dest[my_ranks[li]], dest[my_ranks[li] + 1]};
+      PMMF_CUDA(cudaStreamSynchronize(s));
+      R->phases[4] += ms_since(t_x);
     }
     auto seg_of = [&](auto&& f) {  // per-rank segment bounds from a cluster-indexed prefix f(u)
       std::vector<i64> g(static_cast<size_t>(W) + 1);
@@ -361,7 +441,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       const i64 budget_elems =
           std::max<i64>(i64{1} << 20, static_cast<i64>(static_cast<double>(available_bytes()) * 0.55) / 16);
       double gram_ms = 0.0, search_ms = 0.0;
-      for (const int me : my_ranks) {
+      for (size_t li = 0; li < my_ranks.size(); ++li) {
+      const int me = my_ranks[li];
       const auto t_rank = clk::now();
       const double gs0 = gram_ms + search_ms;
       const i64 u_end = std::min(lo[me + 1], rc);
@@ -384,7 +465,7 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         // gram_tiles wants tile_off indexed by absolute u
         std::vector<i64> toff(static_cast<size_t>(u1) + 1, 0);
         for (i64 u = u0; u <= u1; ++u) toff[u] = tile_off[u - u0];
-        gram_tiles(A, cur.off, u0, u1, toff, G.get(), D.get(), s);
+        gram_tiles(slab[li], cur.off, u0, u1, toff, G.get(), D.get(), s);
         PMMF_CUDA(cudaStreamSynchronize(s));
         gram_ms += ms_since(tg);
         auto ts = clk::now();
@@ -577,12 +658,11 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           if (W > 1 && shard_timing()) PMMF_CUDA(cudaStreamSynchronize(s));
           const auto t_rank = clk::now();
           std::vector<Piece> pieces;
-          const i64 nnz_in =
-              std::max<i64>(W > 1 ? eptr_c[lo[me + 1]] - eptr_c[lo[me]] : A.nnz, 1);
-          rotate_pass(pieces, A, cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, 24.0, nullptr, s, lo[me],
+          const i64 nnz_in = std::max<i64>(slab[li].nnz, 1);
+          rotate_pass(pieces, slab[li], cur.off, slot_base, plan, nullptr, nullptr, i64{1} << 62, 24.0, nullptr, s, lo[me],
                       lo[me + 1]);
           lap("column_pass");
-          if (li + 1 == my_ranks.size()) A = Csc();
+          slab[li] = Csc();
           Csc T;
           transpose_pieces(T, pieces, N, nullptr, chunk, s);
           pieces.clear();
@@ -629,26 +709,18 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
           PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
           residual_done = true;
         }
-        if (W == 1 && !C.multi_process()) {
-          A = std::move(slabs[0]);
-        } else {
-          // exchange 2: the owned columns of A'' and the owned eliminations'
-          // masses and diagonals (eliminations are cluster-major)
-          const auto t_x = clk::now();
-          std::vector<i64> col_seg(static_cast<size_t>(W) + 1);
-          for (int r = 0; r <= W; ++r) col_seg[r] = cur.off[lo[r]];
-          csc_gather_slabs(A, slabs, col_seg, N, C, s);
-          if (ne > 0 && C.multi_process()) {
-            std::vector<i64> epre(static_cast<size_t>(rc) + 1, 0);
-            for (i64 u = 0; u < rc; ++u) epre[u + 1] = epre[u] + nelim[u];
-            const auto eseg = seg_of([&](i64 u) { return epre[u]; });
-            bcast_segments(mass.get(), sizeof(double), eseg, C, s);
-            bcast_segments(diag.get(), sizeof(double), eseg, C, s);
-          }
-          lap("exchange_2");
-          PMMF_TRACE("[pmmf] stage %d: slab exchange %.2f ms\n", stage_no, ms_since(t_x));
+        // the owned columns of A'' stay on their rank (the next reblock moves
+        // them); across processes the owned eliminations' masses and
+        // diagonals (cluster-major) are broadcast
+        slab = std::move(slabs);
+        if (ne > 0 && C.multi_process()) {
+          std::vector<i64> epre(static_cast<size_t>(rc) + 1, 0);
+          for (i64 u = 0; u < rc; ++u) epre[u + 1] = epre[u] + nelim[u];
+          const auto eseg = seg_of([&](i64 u) { return epre[u]; });
+          bcast_segments(mass.get(), sizeof(double), eseg, C, s);
+          bcast_segments(diag.get(), sizeof(double), eseg, C, s);
         }
-        PMMF_TRACE("[pmmf] stage %d: A' %lld entries, mem=%zuMB\n", stage_no, static_cast<long long>(A.nnz),
+        PMMF_TRACE("[pmmf] stage %d: A' %lld entries, mem=%zuMB\n", stage_no, static_cast<long long>(slab_nnz()),
                    mem_used_mb());
       }
     }
@@ -661,8 +733,14 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     if (ne > 0) {
       if (!residual_done) {
         PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 1);
-        PMMF_LAUNCH(k_residual, blocks_for(ne * 32, kThreads), kThreads, 0, s, ne, dsid.get(), A.ptr.get(), A.row.get(),
-                    A.val.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(), diag.get());
+        for (size_t li = 0; li < slab.size(); ++li)
+          PMMF_LAUNCH(k_residual, blocks_for(ne * 32, kThreads), kThreads, 0, s, ne, dsid.get(), slab[li].ptr.get(),
+                      slab[li].row.get(), slab[li].val.get(), cur.d_s2g.get(), d_active.get(), d_rank.get(), mass.get(),
+                      diag.get(), own[li].first, own[li].second);
+        if (C.multi_process()) {  // zeros elsewhere: the sums are the owners' values
+          allreduce_sum_f64(mass.get(), ne, C, s);
+          allreduce_sum_f64(diag.get(), ne, C, s);
+        }
         PMMF_LAUNCH(k_mark, blocks_for(ne, kThreads), kThreads, 0, s, ne, dg.get(), d_active.get(), d_rank.get(), 0);
       }
       PinnedSlot& ps = PinnedSlot::get(2);
@@ -728,8 +806,10 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     dpos.upload(pos);
     DBuf<double> dcore(g * g, s);
     dcore.zero();
-    PMMF_LAUNCH(k_core, static_cast<unsigned>(g), 128, 0, s, g, dcs.get(), A.ptr.get(), A.row.get(), A.val.get(),
-                dpos.get(), dcore.get());
+    for (const Csc& x : slab)  // other ranks' columns are empty in a slab
+      PMMF_LAUNCH(k_core, static_cast<unsigned>(g), 128, 0, s, g, dcs.get(), x.ptr.get(), x.row.get(), x.val.get(),
+                  dpos.get(), dcore.get());
+    allreduce_sum_f64(dcore.get(), g * g, C, s);
     R->core = dcore.to_host(g * g);
   }
   {

@@ -100,35 +100,43 @@ def run(wl, world, trace):
 
 
 def model(res, world, gbs):
-    gs, ap, slab = {}, {}, {}
-    for m in re.finditer(r"shard stage (\d+) rank (\d+): gram\+search ([\d.]+) ms \(([\d.]+) wall\)", res["trace"]):
+    """Owned-column design (shard.cuh): per stage, the max over ranks of
+    every sharded part (scoring calls, slab reblock, Gram+search, slab
+    apply) replaces their sum; the in-process slab exchange of the virtual
+    run is replaced by the all-to-all at `gbs` GB/s of per-rank ingress."""
+    tr = res["trace"]
+    gs, ap, rb = {}, {}, {}
+    for m in re.finditer(r"shard stage (\d+) rank (\d+): gram\+search ([\d.]+) ms \(([\d.]+) wall\)", tr):
         gs[(int(m[1]), int(m[2]))] = float(m[4])
-    for m in re.finditer(r"shard stage (\d+) rank (\d+): apply ([\d.]+) ms, slab (\d+) entries", res["trace"]):
+    for m in re.finditer(r"shard stage (\d+) rank (\d+): apply ([\d.]+) ms, slab (\d+) entries", tr):
         ap[(int(m[1]), int(m[2]))] = float(m[3])
-        slab[(int(m[1]), int(m[2]))] = int(m[4])
-    stages = sorted({s for s, _ in gs} | {s for s, _ in ap})
-    serial = sum(gs.values()) + sum(ap.values())
+    for m in re.finditer(r"shard stage (\d+) rank (\d+): reblock ([\d.]+) ms", tr):
+        rb[(int(m[1]), int(m[2]))] = float(m[3])
+    xv = sum(float(m[1]) for m in re.finditer(r"shard stage \d+: exchange ([\d.]+) ms", tr))
+    ingress = [int(m[1]) for m in re.finditer(r"shard stage \d+: all-to-all ingress max (\d+) bytes", tr)]
+    serial = sum(gs.values()) + sum(ap.values()) + sum(rb.values()) + xv
     par = 0.0
-    # sharded clustering scorer: every call's ranks ran back to back
-    for m in re.finditer(r"shard score: (\d+) ranks, sum ([\d.]+) ms, max ([\d.]+) ms", res["trace"]):
-        serial += float(m[2])
-        par += float(m[3])
-    xbytes = 0.0
+    sc_sum = sc_max = 0.0
+    for m in re.finditer(r"shard score: (\d+) ranks, sum ([\d.]+) ms, max ([\d.]+) ms", tr):
+        sc_sum += float(m[2])
+        sc_max += float(m[3])
+    serial += sc_sum
+    par += sc_max
+    stages = sorted({s for s, _ in gs} | {s for s, _ in ap} | {s for s, _ in rb})
     per_stage = []
     for s in stages:
         g = [gs.get((s, r), 0.0) for r in range(world)]
         a = [ap.get((s, r), 0.0) for r in range(world)]
-        nnz = sum(slab.get((s, r), 0) for r in range(world))
-        xb = 12.0 * nnz * (world - 1) / world
-        par += max(g) + max(a)
-        xbytes += xb
+        b = [rb.get((s, r), 0.0) for r in range(world)]
+        par += max(g) + max(a) + max(b)
         per_stage.append({"stage": s, "gram_search_ms": [round(x, 2) for x in g], "apply_ms": [round(x, 2) for x in a],
-                          "exchange_bytes_per_rank": int(xb)})
-    xms = xbytes / (gbs * 1e9) * 1e3
+                          "reblock_ms": [round(x, 2) for x in b]})
+    xms = sum(ingress) / (gbs * 1e9) * 1e3
     t = res["wall_ms"] - serial + par + xms
     return {"virtual_wall_ms": res["wall_ms"], "sharded_serial_ms": serial, "sharded_max_over_ranks_ms": par,
-            "replicated_ms": res["wall_ms"] - serial, "exchange_ms_modelled": xms, "modelled_step_ms": t,
-            "per_stage": per_stage}
+            "scoring_sum_ms": sc_sum, "scoring_max_ms": sc_max, "virtual_exchange_ms": xv,
+            "replicated_ms": res["wall_ms"] - serial, "all_to_all_bytes_max_rank": sum(ingress),
+            "exchange_ms_modelled": xms, "modelled_step_ms": t, "per_stage": per_stage}
 
 
 def main():
@@ -144,8 +152,9 @@ def main():
     base = run(a.workload, 0, trace=False)
     out = {"workload": a.workload, "rotations": base["rotations"], "one_gpu_wall_ms": base["wall_ms"],
            "one_gpu_rotations_per_s": base["rotations"] / base["wall_ms"] * 1e3, "nvlink_gbs_assumed": a.nvlink_gbs,
-           "note": "modelled from single-GPU virtual-rank runs (one sync per rank and phase); "
-                   "exchange time = slab bytes / assumed NCCL broadcast ingress", "worlds": {}}
+           "note": "owned-column slabs: modelled from single-GPU virtual-rank runs (one sync per rank and "
+                   "phase); all-to-all reblock time = max per-rank ingress bytes / assumed NCCL bandwidth",
+           "worlds": {}}
     for w in a.worlds:
         res = run(a.workload, w, trace=True)
         m = model(res, w, a.nvlink_gbs)
