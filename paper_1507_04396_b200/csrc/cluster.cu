@@ -656,19 +656,10 @@ __global__ void k_anchor_nnz(int m, const int32_t* __restrict__ anchors, const i
   idx[a] = a;
 }
 
-// Every W-th entry of a cost-sorted work list, from `first` (one rank's
-// share of the sparse scorer's columns when clustering is sharded).
-__global__ void k_stride_list(i64 n, const int32_t* __restrict__ in, int W, int first, int32_t* __restrict__ out) {
-  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  const i64 j = first + i * W;
-  if (j < n) out[i] = in[j];
-}
-
 struct Scorer {
   const Csc& a;
   const Numbering& nb;
   cudaStream_t s;
-  const Comm* comm = nullptr;  // (round-robin split of the sparse list; unused: owned-column scoring, score())
   int force_gemm = -1;         // >= 0: the GEMM / sparse choice made for the whole matrix
   DBuf<int32_t> self;  // stage id -> anchor pos (assignment mode)
 
@@ -736,12 +727,6 @@ struct Scorer {
     if (!use_smem)  // one state slot per launched warp (persistent grid of 148 x 8 blocks)
       scratch.alloc(static_cast<i64>((stride * static_cast<size_t>(148 * 8 * wpb) + 7) / 8), s);
     int32_t* dassign = assign_out;
-    // Sharded (assignment mode, sparse scorer): the hub columns are scored
-    // on every rank, the rest of the cost-sorted list round-robin over the
-    // ranks; positions a rank did not score keep a sentinel below any
-    // result (-1 = no anchor hit) and an allreduce(max) completes the table.
-    const bool shard = !rows_mode && comm && comm->world() > 1;
-    if (shard) PMMF_CUDA(cudaMemsetAsync(dassign, 0x80, sizeof(int32_t) * P, s));
     if (rows_mode) PMMF_CUDA(cudaMemsetAsync(rows_out, 0, sizeof(double) * P * m, s));
     ScoreArgs args{P,           dpool,       dpn,              m,           dan,         self.get(),
                    a.ptr.get(), a.row.get(), a.val.get(),      nb.d_blk.get(), rptr.get(), ent_a.get(),
@@ -846,35 +831,7 @@ struct Scorer {
       else
         PMMF_LAUNCH(k_score<false>, static_cast<unsigned>(blocks), 32 * wpb, 0, s, args, wpb);
     };
-    if (!shard) {
-      launch_sparse();
-    } else {
-      const int W = comm->world();
-      const i64 nl = P - nd;
-      DBuf<int32_t> sub(std::max<i64>((nl + W - 1) / W, 1), s);
-      static const bool st_timing = std::getenv("PMMF_B200_SHARD_TIMING") != nullptr || trace_enabled();
-      const bool per_rank = st_timing && comm->virt;  // scripts/shard_model.py
-      double tsum = 0.0, tmax = 0.0;
-      for (const int r : comm->local_ranks()) {
-        if (per_rank) PMMF_CUDA(cudaStreamSynchronize(s));
-        const auto tr0 = std::chrono::steady_clock::now();
-        const i64 cnt = nl > r ? (nl - r + W - 1) / W : 0;
-        PMMF_LAUNCH(k_stride_list, blocks_for(cnt, kThreads), kThreads, 0, s, nl, list.get() + nd, W, r, sub.get());
-        args.list = sub.get();
-        args.nlist = cnt;
-        next.zero();
-        launch_sparse();
-        if (per_rank) {
-          PMMF_CUDA(cudaStreamSynchronize(s));
-          const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count();
-          tsum += ms;
-          tmax = std::max(tmax, ms);
-        }
-      }
-      if (per_rank)
-        std::fprintf(stderr, "[pmmf] shard score: %d ranks, sum %.3f ms, max %.3f ms\n", W, tsum, tmax);
-      allreduce_max_i32(dassign, P, *comm, s);
-    }
+    launch_sparse();
     if (timing) cudaEventRecord(ev[2], s);
     if (trace_enabled()) {
       std::vector<unsigned long long> h = stats.to_host(2);

@@ -400,58 +400,6 @@ void allreduce_max_i32(int32_t* dev, i64 n, const Comm& c, cudaStream_t s) {
   PMMF_NCCL(ncclAllReduce(dev, dev, static_cast<size_t>(n), ncclInt32, ncclMax, c.nccl, s));
 }
 
-void csc_gather_slabs(Csc& out, std::vector<Csc>& parts, const std::vector<i64>& col_seg, i64 N, const Comm& c,
-                      cudaStream_t s) {
-  const std::vector<int> mine = c.local_ranks();
-  const int W = c.size;
-  // slab sizes of every rank
-  std::vector<i64> nnz(static_cast<size_t>(W), 0);
-  for (size_t i = 0; i < mine.size(); ++i) nnz[mine[i]] = parts[i].nnz;
-  if (c.multi_process()) {
-    DBuf<i64> d(W, s);
-    d.upload(nnz);
-    std::vector<i64> seg(static_cast<size_t>(W) + 1);
-    for (int r = 0; r <= W; ++r) seg[r] = r;
-    bcast_segments(d.get(), sizeof(i64), seg, c, s);
-    nnz = d.to_host(W);
-  }
-  std::vector<i64> base(static_cast<size_t>(W) + 1, 0);
-  for (int r = 0; r < W; ++r) base[r + 1] = base[r] + nnz[r];
-  const i64 total = base[W];
-  out = Csc();
-  out.N = N;
-  out.nnz = total;
-  out.ptr.alloc(N + 1, s);
-  out.row.alloc(std::max<i64>(total, 1), s);
-  out.val.alloc(std::max<i64>(total, 1), s);
-  for (size_t i = 0; i < mine.size(); ++i) {
-    const int r = mine[i];
-    Csc& P = parts[i];
-    const i64 c0 = col_seg[r], c1 = col_seg[r + 1];
-    // the slab's entries are contiguous: columns outside [c0, c1) are empty
-    if (c1 > c0) {
-      i64 p0 = 0;
-      PMMF_CUDA(cudaMemcpyAsync(&p0, P.ptr.get() + c0, sizeof(i64), cudaMemcpyDeviceToHost, s));
-      PMMF_CUDA(cudaStreamSynchronize(s));
-      if (p0 != 0) fail(PMMF_INTERNAL, "csc_gather_slabs: slab has entries before its column range");
-      PMMF_LAUNCH(k_ptr_shift, blocks_for(c1 - c0, kThreads), kThreads, 0, s, c1 - c0, P.ptr.get() + c0, i64{0},
-                  base[r], out.ptr.get() + c0);
-    }
-    if (nnz[r] > 0) {
-      PMMF_CUDA(cudaMemcpyAsync(out.row.get() + base[r], P.row.get(), sizeof(int32_t) * nnz[r],
-                                cudaMemcpyDeviceToDevice, s));
-      PMMF_CUDA(cudaMemcpyAsync(out.val.get() + base[r], P.val.get(), sizeof(double) * nnz[r],
-                                cudaMemcpyDeviceToDevice, s));
-    }
-    P = Csc();
-  }
-  PMMF_CUDA(cudaMemcpyAsync(out.ptr.get() + N, &total, sizeof(i64), cudaMemcpyHostToDevice, s));
-  bcast_segments(out.ptr.get(), sizeof(i64), col_seg, c, s);
-  bcast_segments(out.row.get(), sizeof(int32_t), base, c, s);
-  bcast_segments(out.val.get(), sizeof(double), base, c, s);
-  PMMF_CUDA(cudaStreamSynchronize(s));  // `total` is a host stack value
-}
-
 }  // namespace pmmf_b200
 
 // ---- C-ABI (include/pmmf_b200.h, multi-GPU section)

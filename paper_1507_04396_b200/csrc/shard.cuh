@@ -1,12 +1,22 @@
-// shard.cuh — clusters of a stage sharded over GPUs.
+// shard.cuh — clusters of a stage sharded over GPUs,
+// each rank holding only the columns it owns.
 //
-// One process per GPU.  Every rank holds the whole matrix at the start of a
-// stage (pre-reblock, all columns) and runs the clustering and the reblock
-// redundantly: they are deterministic, so every rank derives the same stage
-// partition.  The clusters of the stage are then split into W contiguous
-// ranges of about equal cost; rank r owns the clusters [lo_r, hi_r) and
-// therefore the contiguous stage-id range [off[lo_r], off[hi_r)) of columns.
-//   * Gram tiles and the pivot search of a cluster read only its own columns:
+// One process per GPU.  Rank r's matrix is a slab: a full-width Csc whose
+// entries are the columns r owns (all rows); nothing is replicated but the
+// O(n) metadata (stage numbering, active set, RNG stream).  Per stage:
+//   * Clustering: norms of a column by its owner; the m anchor columns are
+//     gathered to every rank (gather_columns); each rank scores the pool
+//     columns it owns on its slab plus the anchors with the one-GPU kernels,
+//     and the assignment (and the repair's score table) meet by an
+//     allreduce(max).  The device control path (round-robin, repair, cluster
+//     lists) then runs on every rank on identical data.
+//   * Reblock: every rank relabels its own slab (ids of the new partition,
+//     retired ids dropped); the new clusters are split into W contiguous
+//     ranges of about equal cost (shard_ranges, cost c_u^2 + 64 nnz_u with
+//     nnz summed over ranks), and redistribute() moves each column to the
+//     owner of its new cluster: an all-to-all of column lengths and entries
+//     (ncclSend/ncclRecv), ~12 B x nnz/W per rank and stage.
+//   * Gram tiles and the pivot search of a cluster read only its columns:
 //     each rank searches its clusters.  Exchange 1: the rotation slots and
 //     per-cluster counts, each rank's contiguous segment broadcast in place.
 //   * Column pass: a rotation mixes columns of its own cluster, so rank r
@@ -15,14 +25,13 @@
 //     rotations, now known to every rank) rotates those partial columns, and
 //     row g of it is column g of A'' for the owned retired ids g — the
 //     residual masses of rank r's eliminations are complete locally.  The
-//     second transpose gives the owned columns of A''.
-//   * Exchange 2: the owned columns of A'' and the owned eliminations'
-//     masses / diagonals, broadcast in place into the full arrays.
+//     second transpose gives the owned columns of A'': the next stage's slab.
+//     The owned eliminations' masses / diagonals are broadcast (small).
 // Every value is computed by exactly the kernels of the one-GPU path on the
 // same entries in the same order, so the result is bit-identical for any W.
 //
 // Comm::virt runs W ranks one after another inside one process on one GPU
-// (the exchanges become shared buffers): the parity tests use it to prove the
+// (the exchanges become buffer moves): the parity tests use it to prove the
 // decomposition bit-exact on a single device.
 #pragma once
 
@@ -102,12 +111,5 @@ void merge_columns(Csc& out, const Csc& a, const Csc& b, cudaStream_t s);
 // across processes; buffer moves between virtual ranks).  Every column
 // comes from exactly one source, entries are copied unchanged.
 void redistribute(std::vector<Csc>& slabs, const std::vector<i64>& dest, i64 N, const Comm& c, cudaStream_t s);
-
-// The full matrix from the per-rank column slabs: parts[i] holds (over all
-// N columns) only the columns [col_seg[r], col_seg[r+1]) of local rank
-// r = c.local_ranks()[i]; the slabs are concatenated (and, across
-// processes, broadcast) into `out`.
-void csc_gather_slabs(Csc& out, std::vector<Csc>& parts, const std::vector<i64>& col_seg, i64 N, const Comm& c,
-                      cudaStream_t s);
 
 }  // namespace pmmf_b200
