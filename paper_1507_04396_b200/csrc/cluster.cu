@@ -1213,19 +1213,25 @@ void score(DevCtx& ctx, const int32_t* dpool, const double* dpn, i64 P, const in
       cudaStream_t s;
       std::chrono::steady_clock::time_point t0;
       double *sum, *mx;
+      int rank;
+      i64* cols;
       ~Lap() {
         if (!on) return;
         cudaStreamSynchronize(s);
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         *sum += ms;
         *mx = std::max(*mx, ms);
+        if (std::getenv("PMMF_B200_SHARD_DETAIL"))
+          std::fprintf(stderr, "[pmmf]   shard score rank %d: %lld columns %.3f ms\n", rank, static_cast<long long>(*cols),
+                       ms);
       }
-    } lap{st_timing, s, tr0, &tsum, &tmax};
+    };
+    i64 Pi = 0;
+    Lap lap{st_timing, s, tr0, &tsum, &tmax, ss.comm->local_ranks()[i], &Pi};
     DBuf<uint8_t> f(P, s);
     PMMF_LAUNCH(k_own_flags, blocks_for(P, kThreads), kThreads, 0, s, P, dpool, ss.own[i].first, ss.own[i].second,
                 f.get());
     DBuf<int64_t> pos(P, s);
-    i64 Pi = 0;
     stable_select(cub::CountingInputIterator<int64_t>(0), f.get(), P, pos.get(), &Pi, s);
     if (Pi == 0) continue;
     DBuf<int32_t> sub(Pi, s);
