@@ -123,13 +123,16 @@ struct BigCache {
     static BigCache c;
     return c;
   }
-  // Best fit among cached blocks; nullptr if none qualifies.
+  // Best fit among cached blocks; nullptr if none qualifies.  Requests
+  // below 1 GB are power-of-two size classes (pool_alloc) and take a block
+  // of their class or the next; larger ones a block within 1.5x.
   void* take(size_t bytes, int dev, cudaStream_t st, size_t* got) {
     std::lock_guard<std::mutex> g(mu);
     size_t best = blocks.size();
+    const size_t lim = bytes < (size_t{1} << 30) ? 2 * bytes : bytes + bytes / 2;
     for (size_t i = 0; i < blocks.size(); ++i) {
       const Blk& b = blocks[i];
-      if (b.dev != dev || b.bytes < bytes || b.bytes > bytes + bytes / 2) continue;
+      if (b.dev != dev || b.bytes < bytes || b.bytes > lim) continue;
       if (best == blocks.size() || b.bytes < blocks[best].bytes) best = i;
     }
     if (best == blocks.size()) return nullptr;
@@ -318,8 +321,18 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
   int dev = 0;
   PMMF_CUDA(cudaGetDevice(&dev));
   if (*bytes >= kBigBytes) {
-    const size_t g = *bytes >= (size_t{1} << 30) ? (size_t{64} << 20) : (size_t{4} << 20);
-    *bytes = (*bytes + g - 1) / g * g;
+    // mid-size blocks (32 MB .. 1 GB) in power-of-two classes: the sizes a
+    // stage asks for vary from step to step and stage to stage, and a class
+    // that misses the cache maps fresh memory (~80 ms per GB, more when the
+    // device is nearly full); the largest blocks keep 64 MB granularity
+    if (*bytes < (size_t{1} << 30)) {
+      size_t c = kBigBytes;
+      while (c < *bytes) c <<= 1;
+      *bytes = c;
+    } else {
+      const size_t g = size_t{64} << 20;
+      *bytes = (*bytes + g - 1) / g * g;
+    }
     size_t got = 0;
     if (void* q = BigCache::get().take(*bytes, dev, st, &got)) {
       *p = q;

@@ -316,8 +316,12 @@ __global__ void __launch_bounds__(256) k_stage_apply_k(int nrhs, int rc, const i
 // q) and level boundaries are copied into shared memory next to the slice,
 // so a level is shared-memory work plus one barrier -- no global load on the
 // level chain.  Used when slice + records fit (run_stage).
+// 1024 threads: a level's (rotation, rhs) pairs are spread 4x finer than
+// over 256, and the level chain's barriers are the critical path (one CTA
+// per SM: the slice and records fill shared memory).
+constexpr int kApplyThreads = 1024;
 template <int K, bool kTransposed>
-__global__ void __launch_bounds__(256) k_stage_apply_s(int nrhs, int rc, const int64_t* __restrict__ coff,
+__global__ void __launch_bounds__(kApplyThreads, 1) k_stage_apply_s(int nrhs, int rc, const int64_t* __restrict__ coff,
                                                        const int32_t* __restrict__ members,
                                                        const int64_t* __restrict__ rot_ptr,
                                                        const int64_t* __restrict__ lvl_ptr,
@@ -657,9 +661,9 @@ struct Operator {
                            : (transposed ? k_stage_apply_s<3, true> : k_stage_apply_s<3, false>);
         if (smem > 48 * 1024)
           PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        kern<<<grid, kThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
-                                           sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
-                                           sd.q.get(), V);
+        kern<<<grid, kApplyThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
+                                                sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
+                                                sd.q.get(), V);
         launch_counter().fetch_add(1, std::memory_order_relaxed);
         PMMF_CUDA(cudaGetLastError());
         return;
@@ -740,23 +744,29 @@ __global__ void k_spmv(int64_t N, int nrhs, const int64_t* __restrict__ ptr, con
 }
 
 // Deterministic per-rhs dot products: fixed grid of partials, then a fixed
-// order final pass (no atomics).
+// order final pass (no atomics).  Vectors are index-major (v[i * nrhs + r]):
+// a warp reads one row's rhs lanes contiguously, block b owns a contiguous
+// row range, warp w its rows b0 + w + 8k, lane r the running sum of rhs r;
+// the 8 warps' sums are folded in warp order.
 constexpr int kDotBlocks = 296;
-__global__ void k_dot_partial(int64_t n, int nrhs, const double* __restrict__ a, const double* __restrict__ b,
-                              double* __restrict__ part) {
-  __shared__ double red[kThreads];
-  for (int r = 0; r < nrhs; ++r) {
+__global__ void __launch_bounds__(kThreads) k_dot_partial(int64_t n, int nrhs, const double* __restrict__ a,
+                                                          const double* __restrict__ b, double* __restrict__ part) {
+  __shared__ double red[kThreads / 32][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = kThreads / 32;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+  for (int r0 = 0; r0 < nrhs; r0 += 32) {
+    const int r = r0 + lane;
     double s = 0.0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-      s = dadd(s, dmul(a[i * nrhs + r], b[i * nrhs + r]));
-    red[threadIdx.x] = s;
+    if (r < nrhs)
+      for (int64_t i = i0 + w; i < i1; i += nw) s = dadd(s, dmul(a[i * nrhs + r], b[i * nrhs + r]));
+    red[w][lane] = s;
     __syncthreads();
-    for (int o = blockDim.x / 2; o; o >>= 1) {
-      if (threadIdx.x < o) red[threadIdx.x] = dadd(red[threadIdx.x], red[threadIdx.x + o]);
-      __syncthreads();
+    if (w == 0 && r < nrhs) {
+      double t = red[0][lane];
+      for (int q = 1; q < nw; ++q) t = dadd(t, red[q][lane]);
+      part[static_cast<int64_t>(r) * gridDim.x + blockIdx.x] = t;
     }
-    if (threadIdx.x == 0) part[static_cast<int64_t>(r) * gridDim.x + blockIdx.x] = red[0];
     __syncthreads();
   }
 }
