@@ -21,6 +21,7 @@
 #include <string>
 
 #include "engine.cuh"
+#include "layout.cuh"
 #include "precond.cuh"
 #include "result.cuh"
 #include "rng.cuh"
@@ -316,6 +317,18 @@ __global__ void __launch_bounds__(256) k_stage_apply_k(int nrhs, int rc, const i
 // q) and level boundaries are copied into shared memory next to the slice,
 // so a level is shared-memory work plus one barrier -- no global load on the
 // level chain.  Used when slice + records fit (run_stage).
+// Raises a kernel's dynamic shared memory limit only when it grows: a
+// captured CG iteration (CUDA graph) then makes no attribute calls.
+inline void set_max_smem(const void* kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void*, size_t> done;
+  std::lock_guard<std::mutex> g(mu);
+  size_t& cur = done[kern];
+  if (bytes <= cur) return;
+  PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  cur = bytes;
+}
+
 // 1024 threads: a level's (rotation, rhs) pairs are spread 4x finer than
 // over 256, and the level chain's barriers are the critical path (one CTA
 // per SM: the slice and records fill shared memory).
@@ -407,19 +420,6 @@ __global__ void k_diag_scale(int64_t nd, int nrhs, const int32_t* __restrict__ i
   v = dmul(v, f[d]);
 }
 
-// rhs-major <-> index-major
-__global__ void k_to_imaj(int64_t n, int nrhs, const double* __restrict__ in, double* __restrict__ out) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n * nrhs) return;
-  const int64_t idx = i / nrhs, r = i % nrhs;
-  out[i] = in[r * n + idx];
-}
-__global__ void k_from_imaj(int64_t n, int nrhs, const double* __restrict__ in, double* __restrict__ out) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n * nrhs) return;
-  const int64_t r = i / n, idx = i % n;
-  out[i] = in[idx * nrhs + r];
-}
 
 }  // namespace
 
@@ -660,7 +660,7 @@ struct Operator {
         auto kern = k == 2 ? (transposed ? k_stage_apply_s<2, true> : k_stage_apply_s<2, false>)
                            : (transposed ? k_stage_apply_s<3, true> : k_stage_apply_s<3, false>);
         if (smem > 48 * 1024)
-          PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          set_max_smem(reinterpret_cast<const void*>(kern), smem);
         kern<<<grid, kApplyThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
                                                 sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
                                                 sd.q.get(), V);
@@ -681,7 +681,7 @@ struct Operator {
         auto kern = k == 2 ? (transposed ? k_stage_apply_k<2, true> : k_stage_apply_k<2, false>)
                            : (transposed ? k_stage_apply_k<3, true> : k_stage_apply_k<3, false>);
         if (smem > 48 * 1024)
-          PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+          set_max_smem(reinterpret_cast<const void*>(kern), smem);
         kern<<<grid, kThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
                                            sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
                                            sd.q.get(), V);
@@ -696,7 +696,7 @@ struct Operator {
     const size_t smem = smem_ok ? static_cast<size_t>(sd.max_c) * rc * 8 : 0;
     dim3 grid(static_cast<unsigned>(sd.nclusters), static_cast<unsigned>((nrhs + rc - 1) / rc));
     auto kern = transposed ? k_stage_apply<true> : k_stage_apply<false>;
-    if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (smem > 48 * 1024) set_max_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<grid, kThreads, smem, st>>>(k, nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(), sd.lvl_ptr.get(),
                                        sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(), sd.q.get(), V, smem_ok);
     launch_counter().fetch_add(1, std::memory_order_relaxed);
@@ -708,7 +708,7 @@ struct Operator {
     for (const auto& sd : stages) run_stage(sd, false, nrhs, V, st);
     if (g > 0) {
       const size_t smem = static_cast<size_t>(2 * g) * 8;
-      if (smem > 48 * 1024) PMMF_CUDA(cudaFuncSetAttribute(k_core_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      if (smem > 48 * 1024) set_max_smem(reinterpret_cast<const void*>(k_core_apply), smem);
       PMMF_LAUNCH(k_core_apply, static_cast<unsigned>(nrhs), kThreads, smem, st, g, nrhs, core_idx.get(), E.get(),
                   core_f[mode].get(), V);
     }
@@ -748,7 +748,7 @@ __global__ void k_spmv(int64_t N, int nrhs, const int64_t* __restrict__ ptr, con
 // a warp reads one row's rhs lanes contiguously, block b owns a contiguous
 // row range, warp w its rows b0 + w + 8k, lane r the running sum of rhs r;
 // the 8 warps' sums are folded in warp order.
-constexpr int kDotBlocks = 296;
+constexpr int kDotBlocks = 1184;  // 8 per SM: enough loads in flight to stream both vectors
 __global__ void __launch_bounds__(kThreads) k_dot_partial(int64_t n, int nrhs, const double* __restrict__ a,
                                                           const double* __restrict__ b, double* __restrict__ part) {
   __shared__ double red[kThreads / 32][32];
@@ -758,8 +758,20 @@ __global__ void __launch_bounds__(kThreads) k_dot_partial(int64_t n, int nrhs, c
   for (int r0 = 0; r0 < nrhs; r0 += 32) {
     const int r = r0 + lane;
     double s = 0.0;
-    if (r < nrhs)
-      for (int64_t i = i0 + w; i < i1; i += nw) s = dadd(s, dmul(a[i * nrhs + r], b[i * nrhs + r]));
+    if (r < nrhs) {
+      int64_t i = i0 + w;
+      for (; i + 3 * nw < i1; i += 4 * nw) {  // four rows' loads in flight, the sum still in row order
+        const double a0 = a[i * nrhs + r], b0 = b[i * nrhs + r];
+        const double a1 = a[(i + nw) * nrhs + r], b1 = b[(i + nw) * nrhs + r];
+        const double a2 = a[(i + 2 * nw) * nrhs + r], b2 = b[(i + 2 * nw) * nrhs + r];
+        const double a3 = a[(i + 3 * nw) * nrhs + r], b3 = b[(i + 3 * nw) * nrhs + r];
+        s = dadd(s, dmul(a0, b0));
+        s = dadd(s, dmul(a1, b1));
+        s = dadd(s, dmul(a2, b2));
+        s = dadd(s, dmul(a3, b3));
+      }
+      for (; i < i1; i += nw) s = dadd(s, dmul(a[i * nrhs + r], b[i * nrhs + r]));
+    }
     red[w][lane] = s;
     __syncthreads();
     if (w == 0 && r < nrhs) {
@@ -820,7 +832,11 @@ __global__ void k_sub(int64_t m, const double* __restrict__ b, const double* __r
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < m) o[i] = dsub(b[i], t[i]);
 }
-__global__ void k_cg_check(int nrhs, int it, CgState S) {
+// The iteration number comes from a device counter (k_cg_tick), so one
+// captured iteration can be replayed as a CUDA graph.
+__global__ void k_cg_tick(int32_t* it) { ++*it; }
+__global__ void k_cg_check(int nrhs, const int32_t* __restrict__ itp, CgState S) {
+  const int it = *itp;
   const int r = threadIdx.x;
   if (r >= nrhs || !S.active[r]) return;
   const double res = sqrt(S.res[r]);
@@ -1011,7 +1027,10 @@ void run_cg(const pmmf_b200_coo* a, SplitPrecond* pc, const pmmf_b200_solve_conf
     pre(0, B, Rv);  // r = K^-1 b
     PMMF_CUDA(cudaMemcpyAsync(Pv.get(), Rv.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
     dot(Rv, Rv, rr);
-    for (int it = 1; it <= cfg->max_iter; ++it) {
+    DBuf<int32_t> dit(1, s);
+    dit.zero();
+    auto iteration = [&] {
+      PMMF_LAUNCH(k_cg_tick, 1, 1, 0, s, dit.get());
       pre(1, Pv, T1);
       spmv(T1, T2);
       pre(0, T2, W);
@@ -1023,16 +1042,59 @@ void run_cg(const pmmf_b200_coo* a, SplitPrecond* pc, const pmmf_b200_solve_conf
       spmv(X, T2);
       PMMF_LAUNCH(k_sub, blocks_for(m, kThreads), kThreads, 0, s, m, B.get(), T2.get(), T1.get());
       dot(T1, T1, res);
-      PMMF_LAUNCH(k_cg_check, 1, th, 0, s, nr, it, S);
+      PMMF_LAUNCH(k_cg_check, 1, th, 0, s, nr, dit.get(), S);
       dot(Rv, Rv, rrn);
       PMMF_LAUNCH(k_cg_beta, blocks_for(m, kThreads), kThreads, 0, s, n, nr, dact.get(), rrn.get(), rr.get(), Rv.get(),
                   Pv.get());
       PMMF_LAUNCH(k_cg_rr, 1, th, 0, s, nr, dact.get(), rrn.get(), rr.get());
-      if (it % 8 == 0 || it == cfg->max_iter) {
-        std::vector<int32_t> h = dact.to_host(nr);
-        bool any = false;
-        for (int r = 0; r < nr; ++r) any |= h[r] != 0;
-        if (!any) break;
+    };
+    auto all_done = [&] {
+      std::vector<int32_t> h = dact.to_host(nr);
+      for (int r = 0; r < nr; ++r)
+        if (h[r]) return false;
+      return true;
+    };
+    // The first iteration runs eagerly (it sizes every buffer and sets the
+    // kernels' attributes); with graphs on, the rest replay it as one CUDA
+    // graph (~130 launches per iteration), the host convergence check every 8.
+    // The sync-free triangular solves number their ready flags per solve on
+    // the host, so SSOR / IC(0) keep the eager loop.
+    // Opt-in (PMMF_B200_CG_GRAPH=1): measured on config 5, the replay gains
+    // ~2% per iteration at 1024^2 and loses at 256^2 (gpurun_out/r02t).
+    const char* ge = std::getenv("PMMF_B200_CG_GRAPH");
+    const bool graph_ok = (!pc || pc->kind == PMMF_PRECOND_PMMF || pc->kind == PMMF_PRECOND_JACOBI) && ge &&
+                          ge[0] == '1';
+    int it = 0;
+    if (cfg->max_iter >= 1) {
+      iteration();
+      it = 1;
+    }
+    cudaGraphExec_t exec = nullptr;
+    if (graph_ok && it < cfg->max_iter) {
+      cudaGraph_t graph = nullptr;
+      PMMF_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      const int64_t launches0 = launch_counter().load();
+      iteration();
+      const int64_t per_iter = launch_counter().load() - launches0;
+      PMMF_CUDA(cudaStreamEndCapture(s, &graph));
+      PMMF_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      launch_counter().fetch_sub(per_iter, std::memory_order_relaxed);  // counted per replay below
+      while (it < cfg->max_iter) {
+        const int k = std::min(8 - (it % 8 == 0 ? 0 : it % 8), cfg->max_iter - it);
+        for (int q = 0; q < k; ++q) {
+          PMMF_CUDA(cudaGraphLaunch(exec, s));
+          launch_counter().fetch_add(per_iter, std::memory_order_relaxed);
+        }
+        it += k;
+        if (all_done()) break;
+      }
+      cudaGraphExecDestroy(exec);
+    } else {
+      while (it < cfg->max_iter) {
+        if (it % 8 == 0 && all_done()) break;
+        iteration();
+        ++it;
       }
     }
     std::vector<int32_t> hi = diters.to_host(nr), hc = dconv.to_host(nr), hbk = dbrk.to_host(nr);
@@ -1078,9 +1140,9 @@ int pmmf_b200_operator_apply(void* opv, int32_t mode, int64_t nrhs, const double
       PMMF_CUDA(cudaMemcpyAsync(a.get(), in, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
     else
       a.upload(in, m);
-    PMMF_LAUNCH(k_to_imaj, blocks_for(m, kThreads), kThreads, 0, s, o->n, static_cast<int>(nrhs), a.get(), b.get());
+    to_index_major(a.get(), b.get(), o->n, static_cast<int>(nrhs), s);
     o->apply_dev(mode, static_cast<int>(nrhs), b.get(), s);
-    PMMF_LAUNCH(k_from_imaj, blocks_for(m, kThreads), kThreads, 0, s, o->n, static_cast<int>(nrhs), b.get(), a.get());
+    to_rhs_major(b.get(), a.get(), o->n, static_cast<int>(nrhs), s);
     if (on_device)
       PMMF_CUDA(cudaMemcpyAsync(out, a.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
     else

@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "engine.cuh"
+#include "layout.cuh"
 #include "precond.cuh"
 #include "rng.cuh"
 
@@ -173,19 +174,6 @@ __global__ void k_scale_rows_inplace(i64 n, int nr, const double* __restrict__ s
   const i64 x = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (x >= n * nr) return;
   v[x] = dmul(v[x], s[x / nr]);
-}
-
-__global__ void k_to_imaj(i64 n, int nr, const double* __restrict__ in, double* __restrict__ out) {
-  const i64 x = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (x >= n * nr) return;
-  const i64 r = x / n, i = x % n;
-  out[i * nr + r] = in[x];
-}
-__global__ void k_from_imaj(i64 n, int nr, const double* __restrict__ in, double* __restrict__ out) {
-  const i64 x = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-  if (x >= n * nr) return;
-  const i64 r = x / n, i = x % n;
-  out[x] = in[i * nr + r];
 }
 
 // ------------------------------------------------------------ sync-free solves
@@ -708,9 +696,9 @@ int pmmf_b200_precond_apply(void* pcv, int32_t side, int64_t nrhs, const double*
       PMMF_CUDA(cudaMemcpyAsync(a.get(), in, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
     else
       a.upload(in, m);
-    PMMF_LAUNCH(k_to_imaj, blocks_for(m, kThreads), kThreads, 0, s, n, static_cast<int>(nrhs), a.get(), b.get());
+    to_index_major(a.get(), b.get(), n, static_cast<int>(nrhs), s);
     pc->apply(side, static_cast<int>(nrhs), b.get(), c.get(), s);
-    PMMF_LAUNCH(k_from_imaj, blocks_for(m, kThreads), kThreads, 0, s, n, static_cast<int>(nrhs), c.get(), a.get());
+    to_rhs_major(c.get(), a.get(), n, static_cast<int>(nrhs), s);
     if (on_device)
       PMMF_CUDA(cudaMemcpyAsync(out, a.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
     else
