@@ -76,7 +76,9 @@ def merge_traffic():
     """DRAM bytes (read + write) per launch of the write pass, from the ncu
     dram__bytes pass over every such launch of one factorization
     (profiles/merge_traffic_r01e.json, scripts/gpu_evidence_r01e.sh)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r01e.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r02.json")
+    if not os.path.exists(path):
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r01e.json")
     try:
         with open(path) as f:
             d = json.load(f)
