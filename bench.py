@@ -172,9 +172,18 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
             self.first.set()
         self.first.set()
+
+    def mark(self, begin=True):
+        """Bounds of the timed region: only samples inside it are reported
+        (the sampler starts before the warm-up, so its start-up cost never
+        lands in a timed step)."""
+        if begin:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
 
     def stop(self):
         if not self.proc:
@@ -186,7 +195,9 @@ class Clocks:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        inside = [ln for t, ln in self.lines if (t0 is None or t >= t0) and (t1 is None or t <= t1 + 0.25)]
+        for ln in inside or [ln for _, ln in self.lines[-3:]]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
                 continue
@@ -543,15 +554,16 @@ def main():
         torch.cuda.synchronize()
         return
     L.pmmf_b200_profile_enable(0)
+    clocks = Clocks(local)
+    clocks.start()  # nvidia-smi's start-up overlaps the warm-up
     for _ in range(args.warmup):
         run_device()
     # ---- timed region: device-resident input, live kernel accounting OFF
     # (its per-level events would count toward the step); the roofline
     # counters come from one extra profiled step after the timed region.
-    clocks = Clocks(local)
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark(True)
     launches0 = api.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ms, rots = [], 0
@@ -564,6 +576,7 @@ def main():
     launches = api.kernel_launches() - launches0
     barrier()
     torch.cuda.synchronize()
+    clocks.mark(False)
     clk = clocks.stop()
     timed_phases = last_phases.copy()
     # roofline pass: one untimed step with the per-launch CUDA events on

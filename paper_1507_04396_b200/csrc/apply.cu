@@ -1231,6 +1231,14 @@ inline bool level_loop_enabled() {
   const char* e = std::getenv("PMMF_B200_LEVEL_LOOP");
   return e && e[0] == '1';
 }
+// Hybrid: the per-level launch chain for the large levels of a batch, then
+// one persistent level-loop launch for its tail of levels with fewer than
+// this many rotations each (where the chain's ~7 launches per level cost
+// more than the loop's three grid barriers).  0 disables.
+inline i64 loop_below() {
+  const char* e = std::getenv("PMMF_B200_LOOP_BELOW");
+  return e ? std::atoll(e) : 0;
+}
 
 // Co-resident grid of the level loop (cooperative launch).
 template <int K>
@@ -1550,6 +1558,11 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       S.scan_tmp.alloc(static_cast<i64>(S.scan_bytes) + 1, s);
     }
     const bool loop = level_loop_enabled();
+    const i64 below = loop ? 0 : loop_below();
+    int L_switch = plan.max_level + 1;  // hybrid: levels >= L_switch all below the threshold
+    if (below > 0)
+      while (L_switch > 1 && range[L_switch - 1].second - range[L_switch - 1].first < below) --L_switch;
+    const bool hybrid = below > 0 && L_switch <= plan.max_level;
     if (!loop) size_items();
     auto set_scalar = [&](auto& buf, auto v) {
       PMMF_CUDA(cudaMemcpyAsync(buf.get(), &v, sizeof(v), cudaMemcpyHostToDevice, s));
@@ -1571,7 +1584,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     // persistent level loop (default) or the per-level launch chain
     LoopScratch X;
     int loop_grid = 0;
-    if (loop) {
+    if (loop || hybrid) {
       switch (K) {
         case 2: loop_grid = loop_blocks<2>(); break;
         case 3: loop_grid = loop_blocks<3>(); break;
@@ -1586,7 +1599,8 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       for (int L = 1; L <= plan.max_level; ++L) {
         hlo[L] = range[L].first;
         hhi[L] = range[L].second;
-        S.rot_bytes += static_cast<double>(range[L].second - range[L].first) * (8.0 * K * K + 4.0 * K);
+        if (L >= (loop ? 1 : L_switch))  // the chain counts its own levels (run_level)
+          S.rot_bytes += static_cast<double>(range[L].second - range[L].first) * (8.0 * K * K + 4.0 * K);
       }
       X.lv_lo.alloc(static_cast<i64>(hlo.size()), s);
       X.lv_hi.alloc(static_cast<i64>(hhi.size()), s);
@@ -1608,14 +1622,13 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       X.agg.alloc(K * X.max_items, s);
       X.incl.alloc(K * X.max_items, s);
     };
-    if (loop) size_loop_items();
-    for (;;) {
-      if (loop) {
+    if (loop || hybrid) size_loop_items();
+    auto launch_loop = [&](int L0) {
         LoopArgs LA{};
         LA.order = plan.order.get();
         LA.lv_lo = X.lv_lo.get();
         LA.lv_hi = X.lv_hi.get();
-        LA.L0 = Lstart;
+        LA.L0 = L0;
         LA.L1 = plan.max_level;
         LA.ids = plan.ids.get();
         LA.qs = plan.q;
@@ -1660,8 +1673,16 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
           cudaEventRecord(e1, s);
           S.ev.push_back({e0, e1});
         }
+    };
+    for (;;) {
+      if (loop) {
+        launch_loop(Lstart);
       } else {
         for (int L = Lstart; L <= plan.max_level; ++L) {
+          if (hybrid && L >= L_switch) {
+            launch_loop(L);
+            break;
+          }
           const auto [lo, hi] = range[L];
           if (hi <= lo) continue;
           const int32_t* rots = plan.order.get() + lo;
@@ -1692,7 +1713,8 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       if (trace_enabled())
         std::fprintf(stderr, "[pmmf]   arena overflow at level %d: compacted to %lld live, cap %lld\n", ovf,
                      static_cast<long long>(B.used), static_cast<long long>(B.cap));
-      if (loop) size_loop_items(); else size_items();
+      if (loop || hybrid) size_loop_items();
+      if (!loop) size_items();
       set_scalar(S.cursor, static_cast<unsigned long long>(B.used));
       set_scalar(S.ovf, static_cast<int32_t>(INT_MAX));
       Lstart = ovf;

@@ -5,10 +5,11 @@ def summarize(path, top=16):
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     scale = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3, "second": 1e3}
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         v = float(r[vi].replace(",", "")) * scale[r[ui]]
         name = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")

@@ -105,3 +105,15 @@ def test_long_column_norms(name, monkeypatch):
     monkeypatch.setenv("PMMF_B200_NORM_LONG", "8")
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "rbf512_k4", "k3_sparse",
+                                  "partitioned_input"])
+@pytest.mark.parametrize("below", ["8", "64"])
+def test_level_loop_hybrid(name, below, monkeypatch):
+    """The per-level chain for a batch's large levels, then one level-loop
+    launch for its tail of small levels — bit-exact, with compactions."""
+    monkeypatch.setenv("PMMF_B200_LOOP_BELOW", below)
+    monkeypatch.setenv("PMMF_B200_BATCH_NNZ", "5000")
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
