@@ -460,7 +460,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         }
         auto tg = clk::now();
         DBuf<double> G(std::max<i64>(elems, 1), s), D(std::max<i64>(elems, 1), s);
-        D.zero();  // G: every entry is written by its Gram path (the sparse owner warps zero their column first)
+        G.zero();
+        D.zero();
         // gram_tiles wants tile_off indexed by absolute u
         std::vector<i64> toff(static_cast<size_t>(u1) + 1, 0);
         for (i64 u = u0; u <= u1; ++u) toff[u] = tile_off[u - u0];

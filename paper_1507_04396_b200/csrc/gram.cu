@@ -87,8 +87,6 @@ __global__ void k_gram_owner(i64 col0, i64 ncols, i64 e0, const i64* __restrict_
   const i64 a = J - cbase;
   const i64 c = col_c[w];
   double* Gcol = G + col_tile[w] + a * c;
-  for (i64 b = lane; b < c; b += 32) Gcol[b] = 0.0;  // this warp's column only: no tile memset needed
-  __syncwarp();
   for (i64 e = ptr[J]; e < ptr[J + 1]; ++e) {
     const double va = val[e];
     const int32_t lo = run_lo[e - e0], hi = run_hi[e - e0];
@@ -623,10 +621,6 @@ void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const
       while (v1 < u1 && !is_dense(v1)) ++v1;
       const i64 w = off[v0] - col0;
       const i64 ne = eptr[v1 - u0] - eptr[v0 - u0];
-      if (ne <= 0) {  // no entries: the owner kernel (which zeroes its columns) does not run
-        const i64 t0 = tile_off[v0] - tile_off[u0], t1 = tile_off[v1] - tile_off[u0];
-        if (t1 > t0) PMMF_CUDA(cudaMemsetAsync(G + t0, 0, sizeof(double) * (t1 - t0), s));
-      }
       gram_sparse(a, off, v0, v1, eptr[v0 - u0], ne, dcco.get() + w, dct.get() + w, dcc.get() + w, G, s);
     }
     v0 = v1;

@@ -782,12 +782,18 @@ __global__ void __launch_bounds__(kThreads) k_dot_partial(int64_t n, int nrhs, c
     __syncthreads();
   }
 }
+// Warp per rhs: lanes load 32 partials at a time (coalesced), lane 0 adds
+// them in partial order (the same fixed order as a sequential loop).
 __global__ void k_dot_final(int nrhs, int nparts, const double* __restrict__ part, double* __restrict__ out) {
-  const int r = threadIdx.x;
+  const int r = blockIdx.x, lane = threadIdx.x;
   if (r >= nrhs) return;
   double s = 0.0;
-  for (int p = 0; p < nparts; ++p) s = dadd(s, part[static_cast<int64_t>(r) * nparts + p]);
-  out[r] = s;
+  for (int p0 = 0; p0 < nparts; p0 += 32) {
+    const double v = p0 + lane < nparts ? part[static_cast<int64_t>(r) * nparts + p0 + lane] : 0.0;
+    const int cnt = nparts - p0 < 32 ? nparts - p0 : 32;
+    for (int q = 0; q < cnt; ++q) s = dadd(s, __shfl_sync(0xffffffffu, v, q));
+  }
+  if (lane == 0) out[r] = s;
 }
 
 struct CgState {
@@ -1019,7 +1025,7 @@ void run_cg(const pmmf_b200_coo* a, SplitPrecond* pc, const pmmf_b200_solve_conf
     };
     auto dot = [&](const DBuf<double>& x, const DBuf<double>& y, DBuf<double>& out) {
       PMMF_LAUNCH(k_dot_partial, kDotBlocks, kThreads, 0, s, n, nr, x.get(), y.get(), part.get());
-      PMMF_LAUNCH(k_dot_final, 1, std::max(32, ((nr + 31) / 32) * 32), 0, s, nr, kDotBlocks, part.get(), out.get());
+      PMMF_LAUNCH(k_dot_final, static_cast<unsigned>(nr), 32, 0, s, nr, kDotBlocks, part.get(), out.get());
     };
     CgState S{rr.get(), pap.get(), res.get(), rrn.get(), alpha.get(), dbn.get(), dact.get(), diters.get(),
               dconv.get(), dbrk.get(), trace.get(), stride, cfg->tol};
