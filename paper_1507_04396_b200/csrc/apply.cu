@@ -376,6 +376,54 @@ __global__ void k_item_rot(i64 nrot, const int64_t* __restrict__ ioff, const int
   for (i64 p = 0; p < n; ++p) item_rot[b + p] = static_cast<int32_t>(i);
 }
 
+// Small levels: k_nparts, the exclusive scan, k_items and k_item_rot in one
+// CTA (one launch instead of five; most of a factorization's ~3.7k levels
+// have a few hundred rotations).
+constexpr int kSetupThreads = 1024;
+constexpr i64 kSetupMax = 8 * kSetupThreads;
+template <int K>
+__global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64_t* __restrict__ np,
+                                                               int64_t* __restrict__ ioff, int64_t* __restrict__ nitems,
+                                                               int32_t* __restrict__ item_rot,
+                                                               unsigned long long* __restrict__ in_entries) {
+  using BlockScan = cub::BlockScan<int64_t, kSetupThreads>;
+  __shared__ typename BlockScan::TempStorage scan;
+  __shared__ int64_t s_run;
+  const i64 nrot = A.nrot;
+  if (threadIdx.x == 0) s_run = 0;
+  unsigned long long ins = 0;
+  __syncthreads();
+  for (i64 base = 0; base < nrot; base += kSetupThreads) {
+    const i64 i = base + threadIdx.x;
+    int64_t v = 0;
+    if (i < nrot) {
+      const int t = A.rots[i];
+      int Lmax = 0;
+#pragma unroll
+      for (int b = 0; b < K; ++b) {
+        const int L = A.len[A.ids[static_cast<i64>(t) * K + b] - A.col0];
+        Lmax = max(Lmax, L);
+        ins += static_cast<unsigned long long>(L);
+      }
+      v = max(1, (Lmax + A.chunk - 1) / A.chunk);
+      np[i] = v;
+    }
+    int64_t ex = 0, tot = 0;
+    BlockScan(scan).ExclusiveSum(v, ex, tot);
+    const int64_t run = s_run;
+    if (i < nrot) {
+      ioff[i] = run + ex;
+      for (int64_t q = 0; q < v; ++q) item_rot[run + ex + q] = static_cast<int32_t>(i);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_run = run + tot;
+    __syncthreads();
+  }
+  for (int o = 16; o; o >>= 1) ins += __shfl_xor_sync(0xffffffffu, ins, o);
+  if ((threadIdx.x & 31) == 0 && ins) atomicAdd(in_entries, ins);
+  if (threadIdx.x == 0) *nitems = s_run;
+}
+
 // nitems = ioff[nrot-1] + nparts[nrot-1], on the device (no host sync).
 __global__ void k_items(i64 nrot, const int64_t* __restrict__ ioff, const int64_t* __restrict__ np,
                         int64_t* __restrict__ nitems) {
@@ -1299,14 +1347,19 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.level = level;
   A.rbase = S.rbase.get();
   A.rlen = S.rlen.get();
-  PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
-  {
-    size_t tmp = S.scan_bytes;
-    PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
+  if (nrot <= kSetupMax && !std::getenv("PMMF_B200_NO_LEVEL_SETUP")) {
+    PMMF_LAUNCH(k_level_setup<K>, 1, kSetupThreads, 0, s, A, S.np.get(), S.ioff.get(), S.nitems.get(),
+                S.item_rot.get(), S.in_entries.get());
+  } else {
+    PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
+    {
+      size_t tmp = S.scan_bytes;
+      PMMF_CUDA(cub::DeviceScan::ExclusiveSum(S.scan_tmp.get(), tmp, S.np.get(), S.ioff.get(), static_cast<int64_t>(nrot), s));
+    }
+    PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
+    PMMF_LAUNCH(k_item_rot, blocks_for(nrot, kThreads), kThreads, 0, s, nrot, S.ioff.get(), S.np.get(),
+                S.item_rot.get());
   }
-  PMMF_LAUNCH(k_items, 1, 32, 0, s, nrot, S.ioff.get(), S.np.get(), S.nitems.get());
-  PMMF_LAUNCH(k_item_rot, blocks_for(nrot, kThreads), kThreads, 0, s, nrot, S.ioff.get(), S.np.get(),
-              S.item_rot.get());
   cudaEvent_t c0 = nullptr, c1 = nullptr;
   if (prof_enabled()) {
     c0 = EventPool::get().take();
