@@ -567,12 +567,14 @@ def main():
     launches0 = api.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ms, rots = [], 0
+    step_phases = []
     for _ in range(args.steps):
         ev0.record()
         rots = run_device()
         ev1.record()
         torch.cuda.synchronize()
         step_ms.append(ev0.elapsed_time(ev1))
+        step_phases.append([round(float(x), 1) for x in last_phases])
     launches = api.kernel_launches() - launches0
     barrier()
     torch.cuda.synchronize()
@@ -679,6 +681,7 @@ def main():
                 "roofline": roof, "cpu_baseline": cpu, "like_for_like": like, "e2e": e2e, "gpu_launches": int(launches),
                 "mmf_apply": apply, "cg": cg,
                 "clocks": clk, "step_ms": step_ms,
+                "phases_ms_steps": step_phases,  # [clustering, gram, search, apply, reblock, total] per timed step
                 "phases_ms_last_step": dict(zip(["clustering", "gram", "search", "apply", "reblock", "total"],
                                                 [round(float(x), 1) for x in timed_phases]))}
         print(json.dumps(line), flush=True)
