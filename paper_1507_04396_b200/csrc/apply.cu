@@ -385,10 +385,26 @@ template <int K>
 __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64_t* __restrict__ np,
                                                                int64_t* __restrict__ ioff, int64_t* __restrict__ nitems,
                                                                int32_t* __restrict__ item_rot,
-                                                               unsigned long long* __restrict__ in_entries) {
+                                                               unsigned long long* __restrict__ in_entries,
+                                                               PassArgs P, const i64* __restrict__ rbase,
+                                                               const int32_t* __restrict__ rlen, i64* __restrict__ off,
+                                                               int32_t* __restrict__ len) {
   using BlockScan = cub::BlockScan<int64_t, kSetupThreads>;
   __shared__ typename BlockScan::TempStorage scan;
   __shared__ int64_t s_run;
+  // the previous level's commit (k_commit_level), deferred into this launch:
+  // its outputs' (off, len) must be in place before this level reads len
+  if (P.nrot > 0 && *reinterpret_cast<volatile const int32_t*>(P.ovf) == INT_MAX)
+    for (i64 i = threadIdx.x; i < P.nrot; i += blockDim.x) {
+      const int t = P.rots[i];
+#pragma unroll
+      for (int a = 0; a < K; ++a) {
+        const int id = P.ids[static_cast<i64>(t) * K + a] - static_cast<int>(P.col0);
+        off[id] = rbase[K * i + a];
+        len[id] = rlen[K * i + a];
+      }
+    }
+  __syncthreads();
   const i64 nrot = A.nrot;
   if (threadIdx.x == 0) s_run = 0;
   unsigned long long ins = 0;
@@ -1318,10 +1334,19 @@ void launch_level_loop(LoopArgs A, cudaStream_t s) {
   launch_counter().fetch_add(1, std::memory_order_relaxed);
 }
 
+// The deferred commit of the last level run (run_level), as its own launch.
+template <int K>
+void flush_commit(Batch& B, LevelScratch& S, PassArgs& pending, cudaStream_t s) {
+  if (pending.nrot <= 0) return;
+  PMMF_LAUNCH(k_commit_level<K>, blocks_for(pending.nrot, kThreads), kThreads, 0, s, pending, S.rbase.get(),
+              S.rlen.get(), S.ovf.get(), B.off.get(), B.len.get());
+  pending.nrot = 0;
+}
+
 // One dependency level of a batch, entirely on the device (no host sync).
 template <int K>
 void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* rots, i64 nrot, int level,
-               cudaStream_t s) {
+               cudaStream_t s, PassArgs& pending) {
   PassArgs A{};
   A.rots = rots;
   A.ids = plan.ids.get();
@@ -1349,8 +1374,11 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.rlen = S.rlen.get();
   if (nrot <= kSetupMax && !std::getenv("PMMF_B200_NO_LEVEL_SETUP")) {
     PMMF_LAUNCH(k_level_setup<K>, 1, kSetupThreads, 0, s, A, S.np.get(), S.ioff.get(), S.nitems.get(),
-                S.item_rot.get(), S.in_entries.get());
+                S.item_rot.get(), S.in_entries.get(), pending, S.rbase.get(), S.rlen.get(), B.off.get(),
+                B.len.get());
+    pending.nrot = 0;
   } else {
+    flush_commit<K>(B, S, pending, s);
     PMMF_LAUNCH(k_nparts<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.np.get(), S.in_entries.get());
     {
       size_t tmp = S.scan_bytes;
@@ -1385,8 +1413,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     S.ev.push_back({e0, e1});
     S.rot_bytes += static_cast<double>(nrot) * (8.0 * K * K + 4.0 * K);
   }
-  PMMF_LAUNCH(k_commit_level<K>, blocks_for(nrot, kThreads), kThreads, 0, s, A, S.rbase.get(), S.rlen.get(), S.ovf.get(),
-              B.off.get(), B.len.get());
+  pending = A;  // committed by the next level's setup (or flush_commit)
 }
 
 __global__ void k_plan(const int32_t* __restrict__ nrot, const int64_t* __restrict__ base,
@@ -1731,8 +1758,22 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
       if (loop) {
         launch_loop(Lstart);
       } else {
+        PassArgs pending{};  // the last level's deferred commit
+        auto flush = [&] {
+          switch (K) {
+            case 2: flush_commit<2>(B, S, pending, s); break;
+            case 3: flush_commit<3>(B, S, pending, s); break;
+            case 4: flush_commit<4>(B, S, pending, s); break;
+            case 5: flush_commit<5>(B, S, pending, s); break;
+            case 6: flush_commit<6>(B, S, pending, s); break;
+            case 7: flush_commit<7>(B, S, pending, s); break;
+            case 8: flush_commit<8>(B, S, pending, s); break;
+            default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
+          }
+        };
         for (int L = Lstart; L <= plan.max_level; ++L) {
           if (hybrid && L >= L_switch) {
+            flush();
             launch_loop(L);
             break;
           }
@@ -1740,16 +1781,17 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
           if (hi <= lo) continue;
           const int32_t* rots = plan.order.get() + lo;
           switch (K) {
-            case 2: run_level<2>(B, S, plan, rots, hi - lo, L, s); break;
-            case 3: run_level<3>(B, S, plan, rots, hi - lo, L, s); break;
-            case 4: run_level<4>(B, S, plan, rots, hi - lo, L, s); break;
-            case 5: run_level<5>(B, S, plan, rots, hi - lo, L, s); break;
-            case 6: run_level<6>(B, S, plan, rots, hi - lo, L, s); break;
-            case 7: run_level<7>(B, S, plan, rots, hi - lo, L, s); break;
-            case 8: run_level<8>(B, S, plan, rots, hi - lo, L, s); break;
+            case 2: run_level<2>(B, S, plan, rots, hi - lo, L, s, pending); break;
+            case 3: run_level<3>(B, S, plan, rots, hi - lo, L, s, pending); break;
+            case 4: run_level<4>(B, S, plan, rots, hi - lo, L, s, pending); break;
+            case 5: run_level<5>(B, S, plan, rots, hi - lo, L, s, pending); break;
+            case 6: run_level<6>(B, S, plan, rots, hi - lo, L, s, pending); break;
+            case 7: run_level<7>(B, S, plan, rots, hi - lo, L, s, pending); break;
+            case 8: run_level<8>(B, S, plan, rots, hi - lo, L, s, pending); break;
             default: fail(PMMF_INVALID_ARGUMENT, "apply: unsupported k");
           }
         }
+        flush();
       }
       int32_t ovf = 0;
       PMMF_CUDA(cudaMemcpyAsync(&ovf, S.ovf.get(), sizeof(ovf), cudaMemcpyDeviceToHost, s));
