@@ -156,9 +156,13 @@ class Clocks:
         self.lines = []
 
     def start(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):  # experiments only: no sampler process
+            self.proc = None
+            return
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"],
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 os.environ.get("BENCH_CLOCK_MS", "200")],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.first = threading.Event()
             self.t = threading.Thread(target=self._read, daemon=True)
