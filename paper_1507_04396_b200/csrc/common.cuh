@@ -312,6 +312,13 @@ inline i64 available_bytes() {
   return static_cast<i64>(f) + static_cast<i64>(reserved - used) + static_cast<i64>(BigCache::get().cached_bytes());
 }
 
+// Bytes of large blocks that missed the cache (fresh pool allocations):
+// a steady-state factorization should add none (PMMF_B200_TRACE reports it).
+inline std::atomic<uint64_t>& fresh_big_bytes() {
+  static std::atomic<uint64_t> b{0};
+  return b;
+}
+
 // Stream-ordered allocation.  Large requests are rounded up (64 MB above
 // 1 GB, 4 MB below) and
 // served from the block cache when possible.  A failed request drains the
@@ -341,6 +348,7 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
       return;
     }
   }
+  if (*bytes >= kBigBytes) fresh_big_bytes().fetch_add(*bytes, std::memory_order_relaxed);  // cache missed
   const bool timed = *bytes >= (size_t{64} << 20) && trace_enabled();
   std::chrono::steady_clock::time_point t0;
   if (timed) {

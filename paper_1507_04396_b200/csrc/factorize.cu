@@ -187,6 +187,10 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   const std::vector<int> my_ranks = C.local_ranks();
   PMMF_CUDA(cudaSetDevice(in->device));
   const auto fn_start = clk::now();
+  const uint64_t fresh0 = fresh_big_bytes().load();
+  uint64_t reserved0 = 0;
+  if (trace_on())
+    (void)cudaMemPoolGetAttribute(lib_pool(in->device), cudaMemPoolAttrReservedMemCurrent, &reserved0);
   StreamGuard sg;
   cudaStream_t s = sg.s;
   const i64 n = in->n;
@@ -829,6 +833,13 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   PMMF_CUDA(cudaStreamSynchronize(s));
   R->phases[5] = ms_since(run_start);
   PMMF_TRACE("[pmmf] factorize total %.2f ms (stage loop + core %.2f ms)\n", ms_since(fn_start), R->phases[5]);
+  if (trace_on()) {
+    uint64_t reserved1 = 0;
+    (void)cudaMemPoolGetAttribute(lib_pool(in->device), cudaMemPoolAttrReservedMemCurrent, &reserved1);
+    PMMF_TRACE("[pmmf] memory: %llu MB of large blocks missed the cache, pool reserved %+lld MB\n",
+               static_cast<unsigned long long>((fresh_big_bytes().load() - fresh0) >> 20),
+               static_cast<long long>((static_cast<int64_t>(reserved1) - static_cast<int64_t>(reserved0)) >> 20));
+  }
   return R;
 }
 

@@ -410,14 +410,17 @@ __global__ void k_core_apply(int64_t g, int nrhs, const int32_t* __restrict__ ci
   }
 }
 
+// Retired diagonal powers: V[idx[d], r] *= f[d].  A warp row per retired
+// index, lanes over the rhs (contiguous in the index-major layout): no
+// 64-bit division per element (it made this scaling ALU-bound, 3.7x its
+// HBM time).
 __global__ void k_diag_scale(int64_t nd, int nrhs, const int32_t* __restrict__ idx, const double* __restrict__ f,
                              double* __restrict__ V) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= nd * nrhs) return;
-  const int64_t d = i / nrhs;
-  const int r = static_cast<int>(i % nrhs);
-  double& v = V[static_cast<int64_t>(idx[d]) * nrhs + r];
-  v = dmul(v, f[d]);
+  const int64_t d = blockIdx.x * static_cast<int64_t>(blockDim.y) + threadIdx.y;
+  if (d >= nd) return;
+  const double fd = f[d];
+  double* row = V + static_cast<int64_t>(idx[d]) * nrhs;
+  for (int r = threadIdx.x; r < nrhs; r += 32) row[r] = dmul(row[r], fd);
 }
 
 
@@ -713,7 +716,7 @@ struct Operator {
                   core_f[mode].get(), V);
     }
     if (nd > 0)
-      PMMF_LAUNCH(k_diag_scale, blocks_for(nd * nrhs, kThreads), kThreads, 0, st, nd, nrhs, diag_idx.get(),
+      PMMF_LAUNCH(k_diag_scale, static_cast<unsigned>((nd + 7) / 8), dim3(32, 8), 0, st, nd, nrhs, diag_idx.get(),
                   diag_f[mode].get(), V);
     for (auto it = stages.rbegin(); it != stages.rend(); ++it) run_stage(*it, true, nrhs, V, st);
   }
