@@ -210,6 +210,14 @@ int pmmf_b200_operator_create(void* result, double zero_threshold, void** op, ch
  * in/out are host pointers unless on_device != 0. */
 int pmmf_b200_operator_apply(void* op, int32_t mode, int64_t nrhs, const double* in,
                              double* out, int32_t on_device, char* err, size_t errlen);
+/* The same apply over the ranks of a communicator (pmmf_b200_comm_*,
+ * SURVEY.md §8(e) "MMF apply: shard by cluster per stage"): called
+ * collectively, every rank passes the same input vectors and receives the
+ * full result.  Per stage each rank applies the rotations of its range of
+ * apply groups; the updated rows are exchanged before the next stage.
+ * Bit-identical to pmmf_b200_operator_apply for any rank count. */
+int pmmf_b200_operator_apply_sharded(void* op, void* comm, int32_t mode, int64_t nrhs, const double* in,
+                                     double* out, int32_t on_device, char* err, size_t errlen);
 /* residual_frobenius (transform_ops.hpp:225-237): method 0 = accumulated
  * (sqrt(residual_sq)), 1 = dense ||A - Q^T H Q||_F with the reconstruction
  * on the GPU (reconstruct_dense, :175-213; PMMF_NUMERIC when n > cap, as

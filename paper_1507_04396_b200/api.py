@@ -461,6 +461,24 @@ class MmfOperator:
         library().operator_zeroed_negatives(self._op, ctypes.byref(v))
         return int(v.value)
 
+    def apply_sharded(self, mode: int, x, comm: "Communicator"):
+        """apply(mode, x) over the ranks of `comm` (host numpy vectors; every
+        rank passes the same x and gets the full result)."""
+        lib = library()
+        L = lib.lib
+        L.pmmf_b200_operator_apply_sharded.restype = ctypes.c_int
+        L.pmmf_b200_operator_apply_sharded.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32,
+                                                       ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                                                       ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t]
+        a = np.ascontiguousarray(x, np.float64)
+        if a.shape[-1] != self._n or a.ndim > 2:
+            raise ValueError("MmfOperator::apply: dimension mismatch")
+        out = np.zeros_like(a)
+        err = lib.errbuf()
+        abi.raise_for(L.pmmf_b200_operator_apply_sharded(self._op, comm.handle, int(mode), 1 if a.ndim == 1 else a.shape[0],
+                                                         a.ctypes.data, out.ctypes.data, 0, err, len(err)), err)
+        return out
+
     def apply(self, mode: int, x):
         lib = library()
         err = lib.errbuf()

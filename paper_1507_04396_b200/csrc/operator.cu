@@ -26,6 +26,7 @@
 #include "result.cuh"
 #include "rng.cuh"
 #include "rotation.cuh"
+#include "shard.cuh"
 
 namespace pmmf_b200 {
 
@@ -107,7 +108,26 @@ struct StageDev {
   DBuf<int32_t> nlev;      // per cluster
   DBuf<int32_t> loc;       // R x k local positions
   DBuf<double> q;          // R x k x k
+  std::vector<int64_t> h_coff, h_rot;  // host: cluster offsets, rotations per apply group (sharding)
 };
+
+// Sharded apply (SURVEY.md §8(e) "MMF apply: shard by cluster per stage"):
+// pack / unpack the vector rows of a contiguous run of a stage's members.
+__global__ void k_pack_rows(int64_t j0, int64_t j1, int nrhs, const int32_t* __restrict__ members,
+                            const double* __restrict__ V, double* __restrict__ buf) {
+  const int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t m = (j1 - j0) * nrhs;
+  if (x >= m) return;
+  const int64_t j = j0 + x / nrhs;
+  buf[j * nrhs + x % nrhs] = V[static_cast<int64_t>(members[j]) * nrhs + x % nrhs];
+}
+__global__ void k_unpack_rows(int64_t nj, int nrhs, const int32_t* __restrict__ members,
+                              const double* __restrict__ buf, double* __restrict__ V) {
+  const int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (x >= nj * nrhs) return;
+  const int64_t j = x / nrhs;
+  V[static_cast<int64_t>(members[j]) * nrhs + x % nrhs] = buf[x];
+}
 
 template <bool kTransposed>
 __global__ void k_stage_apply(int k, int nrhs, int rc, const int64_t* __restrict__ coff,
@@ -595,6 +615,9 @@ struct Operator {
       up64(sd.lvl_base, lvl_base);
       up32(sd.nlev, nlev);
       up32(sd.loc, loc);
+      sd.h_coff = coff;
+      sd.h_rot.resize(static_cast<size_t>(sd.nclusters));
+      for (int64_t u = 0; u < sd.nclusters; ++u) sd.h_rot[u] = rot_ptr[u + 1] - rot_ptr[u];
       sd.q.alloc(std::max<int64_t>(1, static_cast<int64_t>(qv.size())), s);
       sd.q.upload(qv);
       PMMF_CUDA(cudaStreamSynchronize(s));
@@ -648,8 +671,17 @@ struct Operator {
     PMMF_CUDA(cudaStreamSynchronize(s));
   }
 
-  void run_stage(const StageDev& sd, bool transposed, int nrhs, double* V, cudaStream_t st) const {
-    if (sd.nclusters == 0) return;
+  // Apply groups [u0, u1) of a stage (default all): the kernels index their
+  // group by blockIdx.x, so the range is passed as offset per-group arrays.
+  void run_stage(const StageDev& sd, bool transposed, int nrhs, double* V, cudaStream_t st, int64_t u0 = 0,
+                 int64_t u1 = -1) const {
+    if (u1 < 0) u1 = sd.nclusters;
+    const int64_t ng = u1 - u0;
+    if (ng <= 0) return;
+    const int64_t* coff = sd.coff.get() + u0;
+    const int64_t* rotp = sd.rot_ptr.get() + u0;
+    const int64_t* lbase = sd.lvl_base.get() + u0;
+    const int32_t* nlev = sd.nlev.get() + u0;
     if ((k == 2 || k == 3) && sd.max_rec_bytes > 0) {
       // Records staged in shared memory: the widest rhs chunk (<= 8) whose
       // slice fits next to the largest cluster's records.
@@ -659,14 +691,13 @@ struct Operator {
       while (rc > 1 && row * rc + sd.max_rec_bytes > cap) --rc;
       const size_t smem = row * rc + sd.max_rec_bytes;
       if (smem <= kSmemBudget) {
-        dim3 grid(static_cast<unsigned>(sd.nclusters), static_cast<unsigned>((nrhs + rc - 1) / rc));
+        dim3 grid(static_cast<unsigned>(ng), static_cast<unsigned>((nrhs + rc - 1) / rc));
         auto kern = k == 2 ? (transposed ? k_stage_apply_s<2, true> : k_stage_apply_s<2, false>)
                            : (transposed ? k_stage_apply_s<3, true> : k_stage_apply_s<3, false>);
         if (smem > 48 * 1024)
           set_max_smem(reinterpret_cast<const void*>(kern), smem);
-        kern<<<grid, kApplyThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
-                                                sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
-                                                sd.q.get(), V);
+        kern<<<grid, kApplyThreads, smem, st>>>(nrhs, rc, coff, sd.members.get(), rotp, sd.lvl_ptr.get(), lbase,
+                                                nlev, sd.loc.get(), sd.q.get(), V);
         launch_counter().fetch_add(1, std::memory_order_relaxed);
         PMMF_CUDA(cudaGetLastError());
         return;
@@ -680,14 +711,13 @@ struct Operator {
       while (rc > 1 && row * rc > kSmemTwoPerSm) --rc;
       if (row * rc <= kSmemBudget) {
         const size_t smem = row * rc;
-        dim3 grid(static_cast<unsigned>(sd.nclusters), static_cast<unsigned>((nrhs + rc - 1) / rc));
+        dim3 grid(static_cast<unsigned>(ng), static_cast<unsigned>((nrhs + rc - 1) / rc));
         auto kern = k == 2 ? (transposed ? k_stage_apply_k<2, true> : k_stage_apply_k<2, false>)
                            : (transposed ? k_stage_apply_k<3, true> : k_stage_apply_k<3, false>);
         if (smem > 48 * 1024)
           set_max_smem(reinterpret_cast<const void*>(kern), smem);
-        kern<<<grid, kThreads, smem, st>>>(nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(),
-                                           sd.lvl_ptr.get(), sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(),
-                                           sd.q.get(), V);
+        kern<<<grid, kThreads, smem, st>>>(nrhs, rc, coff, sd.members.get(), rotp, sd.lvl_ptr.get(), lbase,
+                                           nlev, sd.loc.get(), sd.q.get(), V);
         launch_counter().fetch_add(1, std::memory_order_relaxed);
         PMMF_CUDA(cudaGetLastError());
         return;
@@ -697,11 +727,11 @@ struct Operator {
     while (rc > 1 && static_cast<size_t>(sd.max_c) * rc * 8 > kSmemBudget) rc >>= 1;
     const bool smem_ok = static_cast<size_t>(sd.max_c) * rc * 8 <= kSmemBudget;
     const size_t smem = smem_ok ? static_cast<size_t>(sd.max_c) * rc * 8 : 0;
-    dim3 grid(static_cast<unsigned>(sd.nclusters), static_cast<unsigned>((nrhs + rc - 1) / rc));
+    dim3 grid(static_cast<unsigned>(ng), static_cast<unsigned>((nrhs + rc - 1) / rc));
     auto kern = transposed ? k_stage_apply<true> : k_stage_apply<false>;
     if (smem > 48 * 1024) set_max_smem(reinterpret_cast<const void*>(kern), smem);
-    kern<<<grid, kThreads, smem, st>>>(k, nrhs, rc, sd.coff.get(), sd.members.get(), sd.rot_ptr.get(), sd.lvl_ptr.get(),
-                                       sd.lvl_base.get(), sd.nlev.get(), sd.loc.get(), sd.q.get(), V, smem_ok);
+    kern<<<grid, kThreads, smem, st>>>(k, nrhs, rc, coff, sd.members.get(), rotp, sd.lvl_ptr.get(), lbase, nlev,
+                                       sd.loc.get(), sd.q.get(), V, smem_ok);
     launch_counter().fetch_add(1, std::memory_order_relaxed);
     PMMF_CUDA(cudaGetLastError());
   }
@@ -719,6 +749,49 @@ struct Operator {
       PMMF_LAUNCH(k_diag_scale, static_cast<unsigned>((nd + 7) / 8), dim3(32, 8), 0, st, nd, nrhs, diag_idx.get(),
                   diag_f[mode].get(), V);
     for (auto it = stages.rbegin(); it != stages.rend(); ++it) run_stage(*it, true, nrhs, V, st);
+  }
+
+  // apply over W ranks (shard.cuh): stage by stage, rank r applies the
+  // rotations of its contiguous range of apply groups (shard_ranges, cost
+  // from rotations and group sizes) to the rows it then owns, and the
+  // updated rows are exchanged before the next stage (grouped broadcasts of
+  // each rank's packed segment; virtual ranks share V).  Core and retired
+  // diagonals are applied by every rank.  Same kernels, same order per row:
+  // bit-identical to apply_dev for any W.
+  void apply_dev_sharded(int mode, int nrhs, double* V, cudaStream_t st, const Comm& C) const {
+    const int W = C.world();
+    auto split = [&](const StageDev& sd) {
+      std::vector<i64> sz(sd.h_rot.begin(), sd.h_rot.end()), c(static_cast<size_t>(sd.nclusters));
+      for (int64_t u = 0; u < sd.nclusters; ++u) c[u] = sd.h_coff[u + 1] - sd.h_coff[u];
+      return shard_ranges(sz, c, W);
+    };
+    DBuf<double> buf;
+    auto stage = [&](const StageDev& sd, bool transposed) {
+      const std::vector<i64> lo = split(sd);
+      for (const int r : C.local_ranks()) run_stage(sd, transposed, nrhs, V, st, lo[r], lo[r + 1]);
+      if (!C.multi_process()) return;
+      const int64_t total = sd.h_coff.back();
+      if (buf.n < total * nrhs) buf.alloc(std::max<int64_t>(total * nrhs, 1), st);
+      const int64_t j0 = sd.h_coff[lo[C.rank]], j1 = sd.h_coff[lo[C.rank + 1]];
+      PMMF_LAUNCH(k_pack_rows, blocks_for((j1 - j0) * nrhs, kThreads), kThreads, 0, st, j0, j1, nrhs,
+                  sd.members.get(), V, buf.get());
+      std::vector<i64> seg(static_cast<size_t>(W) + 1);
+      for (int q = 0; q <= W; ++q) seg[q] = sd.h_coff[lo[q]];
+      bcast_segments(buf.get(), sizeof(double) * nrhs, seg, C, st);
+      PMMF_LAUNCH(k_unpack_rows, blocks_for(total * nrhs, kThreads), kThreads, 0, st, total, nrhs, sd.members.get(),
+                  buf.get(), V);
+    };
+    for (const auto& sd : stages) stage(sd, false);
+    if (g > 0) {
+      const size_t smem = static_cast<size_t>(2 * g) * 8;
+      if (smem > 48 * 1024) set_max_smem(reinterpret_cast<const void*>(k_core_apply), smem);
+      PMMF_LAUNCH(k_core_apply, static_cast<unsigned>(nrhs), kThreads, smem, st, g, nrhs, core_idx.get(), E.get(),
+                  core_f[mode].get(), V);
+    }
+    if (nd > 0)
+      PMMF_LAUNCH(k_diag_scale, static_cast<unsigned>((nd + 7) / 8), dim3(32, 8), 0, st, nd, nrhs, diag_idx.get(),
+                  diag_f[mode].get(), V);
+    for (auto it = stages.rbegin(); it != stages.rend(); ++it) stage(*it, true);
   }
 };
 
@@ -1151,6 +1224,34 @@ int pmmf_b200_operator_apply(void* opv, int32_t mode, int64_t nrhs, const double
       a.upload(in, m);
     to_index_major(a.get(), b.get(), o->n, static_cast<int>(nrhs), s);
     o->apply_dev(mode, static_cast<int>(nrhs), b.get(), s);
+    to_rhs_major(b.get(), a.get(), o->n, static_cast<int>(nrhs), s);
+    if (on_device)
+      PMMF_CUDA(cudaMemcpyAsync(out, a.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    else
+      a.download(out, m);
+    PMMF_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int pmmf_b200_operator_apply_sharded(void* opv, void* commv, int32_t mode, int64_t nrhs, const double* in,
+                                     double* out, int32_t on_device, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    auto* o = static_cast<Operator*>(opv);
+    const auto* C = static_cast<const Comm*>(commv);
+    if (!o || !C) fail(PMMF_INVALID_ARGUMENT, "MmfOperator::apply (sharded): null argument");
+    if (mode < 0 || mode > 2) fail(PMMF_INVALID_ARGUMENT, "MmfOperator::apply: bad mode");
+    if (C->device != o->device) fail(PMMF_INVALID_ARGUMENT, "MmfOperator::apply (sharded): communicator on another device");
+    if (nrhs < 1) return;
+    PMMF_CUDA(cudaSetDevice(o->device));
+    cudaStream_t s = o->s;
+    const int64_t m = o->n * nrhs;
+    DBuf<double> a(m, s), b(m, s);
+    if (on_device)
+      PMMF_CUDA(cudaMemcpyAsync(a.get(), in, sizeof(double) * m, cudaMemcpyDeviceToDevice, s));
+    else
+      a.upload(in, m);
+    to_index_major(a.get(), b.get(), o->n, static_cast<int>(nrhs), s);
+    o->apply_dev_sharded(mode, static_cast<int>(nrhs), b.get(), s, *C);
     to_rhs_major(b.get(), a.get(), o->n, static_cast<int>(nrhs), s);
     if (on_device)
       PMMF_CUDA(cudaMemcpyAsync(out, a.get(), sizeof(double) * m, cudaMemcpyDeviceToDevice, s));

@@ -4,6 +4,7 @@ after another in this process, with the exchanges as shared buffers; the
 result must equal the CPU oracle bit-for-bit for every W — the decomposition
 changes which GPU computes an entry, never how.  A one-rank NCCL
 communicator runs the NCCL exchange code itself (self-broadcasts)."""
+import numpy as np
 import pytest
 
 import cases
@@ -98,3 +99,34 @@ def test_virtual_ranks_alternative_paths(name, env, monkeypatch):
     finally:
         comm.close()
     oracles.assert_same(gpu, oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["grid64_m16", "rmat12_m16", "rbf256_k3", "partitioned_input"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_operator_apply(name, world):
+    """MmfOperator apply sharded by apply group per stage (virtual ranks):
+    bit-identical to the one-GPU apply in every mode."""
+    inp, params, part = cases.build(name)
+    f = oracles.factorize("gpu", inp, params, part)
+    op = api.MmfOperator(f)
+    comm = api.Communicator(world, virtual=True)
+    try:
+        x = np.random.default_rng(4).standard_normal((5, inp[0]))
+        for mode in (0, 1, 2):
+            assert np.array_equal(op.apply_sharded(mode, x, comm), op.apply(mode, x))
+    finally:
+        comm.close()
+        op.close()
+
+
+def test_sharded_operator_apply_nccl_one_rank():
+    inp, params, part = cases.build("grid64_m16")
+    f = oracles.factorize("gpu", inp, params, part)
+    op = api.MmfOperator(f)
+    comm = api.Communicator(1, 0, 0)
+    try:
+        x = np.random.default_rng(5).standard_normal((3, inp[0]))
+        assert np.array_equal(op.apply_sharded(2, x, comm), op.apply(2, x))
+    finally:
+        comm.close()
+        op.close()
