@@ -619,6 +619,257 @@ __global__ void __launch_bounds__(256, K == 2 ? 6 : 2) k_merge_p(PassArgs A, con
   }
 }
 
+// ---- k = 2 merge kernel with latency hiding ------------------------------
+// Same results as k_merge_p<2, kWrite> (every output entry, offset and
+// count identical), scheduled to keep loads in flight:
+//  * item prologue in batches: lane l of a warp resolves the l-th of the
+//    warp's next 32 items (item -> rotation -> ids -> column (off, len) ->
+//    output offsets, rotation block) into shared memory, so the chain of
+//    ~6 dependent global loads is paid once per 32 items, not per item;
+//  * partition bounds by a warp-wide search (32 probes per round: 4 rounds
+//    for 10^6 entries instead of 20 dependent binary-search loads);
+//  * one-window-ahead prefetch in the merge loops: a window's advance
+//    (frontier, ballots) is known before its rank searches and stores, so
+//    the next window's rows and values are requested first.
+struct ItemRec {
+  i64 off[2];
+  i64 dst[2];
+  double q[2][2];
+  int32_t ri, p, np, len[2], pad;
+};
+constexpr int kMerge2Warps = kThreads / 32;
+
+// First index i in [lo, hi) with a[i] >= key (hi if none), warp-wide.
+__device__ __forceinline__ i64 warp_search_g(const int32_t* __restrict__ a, i64 lo, i64 hi, int key) {
+  const int lane = threadIdx.x & 31;
+  while (hi - lo > 32) {
+    const i64 step = (hi - lo + 31) >> 5;
+    const i64 idx = min(lo + (lane + 1) * step, hi) - 1;
+    const int c = __popc(__ballot_sync(0xffffffffu, __ldg(a + idx) < key));
+    const i64 nlo = lo + c * step;
+    hi = min(hi, nlo + step);
+    lo = nlo;
+    if (c == 32) return hi;
+  }
+  const i64 e = lo + lane;
+  const bool lt = e < hi && __ldg(a + e) < key;
+  return lo + __popc(__ballot_sync(0xffffffffu, lt));
+}
+
+__device__ __forceinline__ int merge_count2_pf(const int32_t* __restrict__ arow, i64 p0, i64 p1, const i64 h0,
+                                               const i64 h1) {
+  const int lane = threadIdx.x & 31;
+  int kept = 0;
+  int ra = p0 + lane < h0 ? __ldg(arow + p0 + lane) : INT_MAX;
+  int rb = p1 + lane < h1 ? __ldg(arow + p1 + lane) : INT_MAX;
+  while (p0 < h0 || p1 < h1) {
+    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
+    const bool oka = ra != INT_MAX && ra <= frontier;
+    const bool okb = rb != INT_MAX && rb <= frontier;
+    const int na = __popc(__ballot_sync(0xffffffffu, oka));
+    const int nb = __popc(__ballot_sync(0xffffffffu, okb));
+    p0 += na;
+    p1 += nb;
+    const int nra = p0 + lane < h0 ? __ldg(arow + p0 + lane) : INT_MAX;
+    const int nrb = p1 + lane < h1 ? __ldg(arow + p1 + lane) : INT_MAX;
+    const int la = warp_lower_bound(rb, ra);
+    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
+    const bool pa = oka && la < 32 && ca == ra;
+    kept += na + nb - __popc(__ballot_sync(0xffffffffu, pa));
+    ra = nra;
+    rb = nrb;
+  }
+  return kept;
+}
+
+__device__ __forceinline__ int merge_write2_pf(const PassArgs& A, const double (&q)[2][2], i64 p0, i64 p1,
+                                               const i64 h0, const i64 h1, const i64 d0, const i64 d1) {
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const int32_t* __restrict__ arow = A.arow;
+  const double* __restrict__ aval = A.aval;
+  int kept = 0;
+  bool ina = p0 + lane < h0, inb = p1 + lane < h1;
+  int ra = ina ? __ldg(arow + p0 + lane) : INT_MAX;
+  int rb = inb ? __ldg(arow + p1 + lane) : INT_MAX;
+  double va = ina ? __ldg(aval + p0 + lane) : 0.0;
+  double vb = inb ? __ldg(aval + p1 + lane) : 0.0;
+  while (p0 < h0 || p1 < h1) {
+    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
+    const bool oka = ra != INT_MAX && ra <= frontier;
+    const bool okb = rb != INT_MAX && rb <= frontier;
+    const int na = __popc(__ballot_sync(0xffffffffu, oka));
+    const int nb = __popc(__ballot_sync(0xffffffffu, okb));
+    p0 += na;
+    p1 += nb;
+    ina = p0 + lane < h0;
+    inb = p1 + lane < h1;
+    const int nra = ina ? __ldg(arow + p0 + lane) : INT_MAX;
+    const int nrb = inb ? __ldg(arow + p1 + lane) : INT_MAX;
+    const double nva = ina ? __ldg(aval + p0 + lane) : 0.0;
+    const double nvb = inb ? __ldg(aval + p1 + lane) : 0.0;
+    const int la = warp_lower_bound(rb, ra);  // B-window rows < ra
+    const int lb = warp_lower_bound(ra, rb);  // A-window rows < rb
+    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
+    const int cb = __shfl_sync(0xffffffffu, ra, lb & 31);
+    const double vp = __shfl_sync(0xffffffffu, vb, la & 31);
+    const bool pa = la < 32 && ca == ra;
+    const bool bonly = okb && !(lb < 32 && cb == rb);
+    const unsigned BO = __ballot_sync(0xffffffffu, bonly);
+    if (oka) {
+      const double x1 = pa ? vp : 0.0;
+      const unsigned mb = la >= 32 ? 0xffffffffu : ((1u << la) - 1u);
+      const i64 r = kept + lane + __popc(BO & mb);
+      A.wrow[d0 + r] = ra;
+      A.wval[d0 + r] = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
+      A.wrow[d1 + r] = ra;
+      A.wval[d1 + r] = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
+    }
+    if (bonly) {
+      const i64 r = kept + lb + __popc(BO & below);
+      A.wrow[d0 + r] = rb;
+      A.wval[d0 + r] = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
+      A.wrow[d1 + r] = rb;
+      A.wval[d1 + r] = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
+    }
+    kept += na + __popc(BO);
+    ra = nra;
+    rb = nrb;
+    va = nva;
+    vb = nvb;
+  }
+  return kept;
+}
+
+template <bool kWrite>
+__global__ void __launch_bounds__(kThreads, 4) k_merge2(PassArgs A, const int64_t* __restrict__ nitems_d,
+                                                        const int32_t* __restrict__ ovf) {
+  __shared__ ItemRec recs[kMerge2Warps][32];
+  if (*reinterpret_cast<volatile const int32_t*>(ovf) != INT_MAX) return;
+  const i64 nitems = *nitems_d;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  ItemRec* rec = recs[wib];
+  unsigned long long produced = 0;  // profiling counter, one atomic per warp
+  for (i64 first = w; first < nitems; first += 32 * nw) {
+    {
+      const i64 item = first + lane * nw;
+      if (item < nitems) {
+        ItemRec r;
+        const int ri = A.item_rot[item];
+        const i64 io = A.ioff[ri];
+        const i64 io1 = ri + 1 < A.nrot ? A.ioff[ri + 1] : nitems;
+        r.ri = ri;
+        r.np = static_cast<int32_t>(io1 - io);
+        r.p = static_cast<int32_t>(item - io);
+        if (kWrite || r.np > 1) {
+          const int t = A.rots[ri];
+#pragma unroll
+          for (int b = 0; b < 2; ++b) {
+            const int id = A.ids[2 * static_cast<i64>(t) + b] - static_cast<int>(A.col0);
+            r.off[b] = A.off[id];
+            r.len[b] = A.len[id];
+#pragma unroll
+            for (int a = 0; a < 2; ++a) r.q[b][a] = A.qs[(2 * static_cast<i64>(t) + b) * 2 + a];
+            r.dst[b] = (kWrite && r.np > 1) ? A.pos[2 * io + b * r.np + r.p] : 0;
+          }
+          if (!kWrite) r.dst[0] = 2 * io;  // count slots of this rotation
+        }
+        rec[lane] = r;
+      }
+    }
+    __syncwarp();
+    const i64 left = (nitems - first + nw - 1) / nw;
+    const int cnt = left < 32 ? static_cast<int>(left) : 32;
+    for (int j = 0; j < cnt; ++j) {
+      const ItemRec& r = rec[j];
+      const int np = r.np, p = r.p, ri = r.ri;
+      if (!kWrite && np == 1) continue;  // counted by its own write pass
+      const double q[2][2] = {{r.q[0][0], r.q[0][1]}, {r.q[1][0], r.q[1][1]}};
+      i64 beg[2], end[2];
+      const i64 s0 = r.off[0], s1 = r.off[1];
+      const int L0 = r.len[0], L1 = r.len[1];
+      if (np == 1) {
+        beg[0] = s0;
+        end[0] = s0 + L0;
+        beg[1] = s1;
+        end[1] = s1 + L1;
+      } else {
+        // partition_range<2>: split rows are rows of the longest input (the
+        // first on a tie) at multiples of the chunk
+        const int lg = L1 > L0 ? 1 : 0;
+        const i64 ls = lg ? s1 : s0;
+        const i64 os = lg ? s0 : s1, oe = os + (lg ? L0 : L1);
+        const i64 lo_l = ls + static_cast<i64>(p) * A.chunk;
+        const i64 hi_l = p == np - 1 ? ls + (lg ? L1 : L0) : ls + static_cast<i64>(p + 1) * A.chunk;
+        const i64 lo_o = p == 0 ? os : warp_search_g(A.arow, os, oe, __ldg(A.arow + lo_l));
+        const i64 hi_o = p == np - 1 ? oe : warp_search_g(A.arow, os, oe, __ldg(A.arow + hi_l));
+        beg[0] = lg ? lo_o : lo_l;
+        end[0] = lg ? hi_o : hi_l;
+        beg[1] = lg ? lo_l : lo_o;
+        end[1] = lg ? hi_l : hi_o;
+      }
+      int r0 = 0;
+      const int dl = identical_rows<2>(A, beg, end, r0);
+      int u = 0;
+      if (dl >= 0) {
+        if (np == 1) {  // self-allocating single partition, dense
+          unsigned long long b0 = 0;
+          if (lane == 0) b0 = atomicAdd(A.cursor, 2ull * static_cast<unsigned long long>(dl));
+          b0 = __shfl_sync(0xffffffffu, b0, 0);
+          if (static_cast<i64>(b0) + 2 * static_cast<i64>(dl) > A.cap) {
+            if (lane == 0) atomicMin(A.ovf, A.level);
+            continue;
+          }
+          const i64 d2[2] = {static_cast<i64>(b0), static_cast<i64>(b0) + dl};
+          write_dense<2>(A, q, beg, dl, r0, d2);
+          if (lane == 0) {
+            A.rbase[2 * ri] = d2[0];
+            A.rbase[2 * ri + 1] = d2[1];
+            A.rlen[2 * ri] = dl;
+            A.rlen[2 * ri + 1] = dl;
+          }
+          produced += 2ull * static_cast<unsigned long long>(dl);
+          continue;
+        }
+        if (kWrite) write_dense<2>(A, q, beg, dl, r0, r.dst);
+        u = dl;
+      } else if (np == 1) {
+        // single partition: count the union, allocate 2u, write
+        u = merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
+        unsigned long long b0 = 0;
+        if (lane == 0) b0 = atomicAdd(A.cursor, 2ull * static_cast<unsigned long long>(u));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (static_cast<i64>(b0) + 2 * static_cast<i64>(u) > A.cap) {
+          if (lane == 0) atomicMin(A.ovf, A.level);
+          continue;
+        }
+        const i64 d0 = static_cast<i64>(b0), d1 = d0 + u;
+        merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], d0, d1);
+        if (lane == 0) {
+          A.rbase[2 * ri] = d0;
+          A.rbase[2 * ri + 1] = d1;
+          A.rlen[2 * ri] = u;
+          A.rlen[2 * ri + 1] = u;
+        }
+        produced += 2ull * static_cast<unsigned long long>(u);
+        continue;
+      } else if (kWrite) {
+        u = merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], r.dst[0], r.dst[1]);
+      } else {
+        u = merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
+      }
+      if (!kWrite && lane == 0) {
+        A.cnt[r.dst[0] + p] = u;
+        A.cnt[r.dst[0] + np + p] = u;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0 && produced) atomicAdd(A.out_entries, produced);
+}
+
 // ---- persistent level loop ---------------------------------------------
 // All dependency levels of a batch in ONE cooperative kernel (the per-level
 // chain nparts -> scan -> item map -> count pass -> allocation -> write pass
@@ -1272,11 +1523,27 @@ struct LevelScratch {
 // (blocks per SM at this kernel's register use x SMs).  A larger grid runs
 // its surplus blocks as a second, thin wave whose statically strided items
 // finish last.
+inline bool merge2_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PMMF_B200_MERGE2");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 template <int K, bool kWrite>
 int persistent_blocks() {
   static const int nb = [] {
     int per_sm = 0, dev = 0, sms = 148;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0) != cudaSuccess)
+    cudaError_t e = cudaSuccess;
+    if constexpr (K == 2) {
+      if (merge2_enabled())
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite>, kThreads, 0);
+      else
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0);
+    } else {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0);
+    }
+    if (e != cudaSuccess)
       per_sm = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     (void)cudaGetLastError();
@@ -1394,7 +1661,10 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     c1 = EventPool::get().take();
     cudaEventRecord(c0, s);
   }
-  PMMF_LAUNCH((k_merge_p<K, false>), (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  if (K == 2 && merge2_enabled())
+    PMMF_LAUNCH(k_merge2<false>, (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  else
+    PMMF_LAUNCH((k_merge_p<K, false>), (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (c0) {
     cudaEventRecord(c1, s);
     S.cev.push_back({c0, c1});
@@ -1407,7 +1677,10 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     e1 = EventPool::get().take();
     cudaEventRecord(e0, s);
   }
-  PMMF_LAUNCH((k_merge_p<K, true>), (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  if (K == 2 && merge2_enabled())
+    PMMF_LAUNCH(k_merge2<true>, (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  else
+    PMMF_LAUNCH((k_merge_p<K, true>), (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (e0) {
     cudaEventRecord(e1, s);
     S.ev.push_back({e0, e1});
