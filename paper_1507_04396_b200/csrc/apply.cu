@@ -90,6 +90,8 @@ struct PassArgs {
   int level;
   i64* rbase;
   int32_t* rlen;
+  bool prefetch;  // k_merge2: L2 prefetch of the items' inputs (PMMF_B200_MERGE_PF=1, default off)
+  bool ring;      // k_merge2: windows from the cp.async shared-memory ring (PMMF_B200_MERGE_RING, default on)
 };
 
 // Row range of partition p of rotation t: split points are rows of the
@@ -656,12 +658,30 @@ __device__ __forceinline__ i64 warp_search_g(const int32_t* __restrict__ a, i64 
   return lo + __popc(__ballot_sync(0xffffffffu, lt));
 }
 
-__device__ __forceinline__ int merge_count2_pf(const int32_t* __restrict__ arow, i64 p0, i64 p1, const i64 h0,
-                                               const i64 h1) {
+// L2 prefetch of entries [b, e) of the arena (one 128-byte line per lane and
+// round): the merge loops below then find their windows in L2 instead of
+// paying the DRAM latency inside the window-to-window dependency chain.
+template <bool kVals>
+__device__ __forceinline__ void prefetch_range(const int32_t* __restrict__ arow, const double* __restrict__ aval,
+                                               i64 b, i64 e) {
   const int lane = threadIdx.x & 31;
-  int kept = 0;
-  int ra = p0 + lane < h0 ? __ldg(arow + p0 + lane) : INT_MAX;
-  int rb = p1 + lane < h1 ? __ldg(arow + p1 + lane) : INT_MAX;
+  for (i64 o = b + lane * 32; o < e; o += 1024) asm volatile("prefetch.global.L2 [%0];" ::"l"(arow + o));
+  if (kVals)
+    for (i64 o = b + lane * 16; o < e; o += 512) asm volatile("prefetch.global.L2 [%0];" ::"l"(aval + o));
+}
+
+// Both loops index their inputs and outputs with 32-bit offsets from the
+// partition's base pointers (a column holds < 2^31 entries): one IMAD.WIDE per
+// access instead of 64-bit adds and compares.
+__device__ __forceinline__ int merge_count2_pf(const int32_t* __restrict__ arow, const i64 b0, const i64 b1,
+                                               const i64 e0, const i64 e1) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* __restrict__ rap = arow + b0;
+  const int32_t* __restrict__ rbp = arow + b1;
+  const int h0 = static_cast<int>(e0 - b0), h1 = static_cast<int>(e1 - b1);
+  int p0 = 0, p1 = 0, kept = 0;
+  int ra = lane < h0 ? __ldg(rap + lane) : INT_MAX;
+  int rb = lane < h1 ? __ldg(rbp + lane) : INT_MAX;
   while (p0 < h0 || p1 < h1) {
     const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
     const bool oka = ra != INT_MAX && ra <= frontier;
@@ -670,8 +690,8 @@ __device__ __forceinline__ int merge_count2_pf(const int32_t* __restrict__ arow,
     const int nb = __popc(__ballot_sync(0xffffffffu, okb));
     p0 += na;
     p1 += nb;
-    const int nra = p0 + lane < h0 ? __ldg(arow + p0 + lane) : INT_MAX;
-    const int nrb = p1 + lane < h1 ? __ldg(arow + p1 + lane) : INT_MAX;
+    const int nra = p0 + lane < h0 ? __ldg(rap + p0 + lane) : INT_MAX;
+    const int nrb = p1 + lane < h1 ? __ldg(rbp + p1 + lane) : INT_MAX;
     const int la = warp_lower_bound(rb, ra);
     const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
     const bool pa = oka && la < 32 && ca == ra;
@@ -682,18 +702,25 @@ __device__ __forceinline__ int merge_count2_pf(const int32_t* __restrict__ arow,
   return kept;
 }
 
-__device__ __forceinline__ int merge_write2_pf(const PassArgs& A, const double (&q)[2][2], i64 p0, i64 p1,
-                                               const i64 h0, const i64 h1, const i64 d0, const i64 d1) {
+__device__ __forceinline__ int merge_write2_pf(const PassArgs& A, const double (&q)[2][2], const i64 b0, const i64 b1,
+                                               const i64 e0, const i64 e1, const i64 d0, const i64 d1) {
   const int lane = threadIdx.x & 31;
   const unsigned below = (1u << lane) - 1u;
-  const int32_t* __restrict__ arow = A.arow;
-  const double* __restrict__ aval = A.aval;
-  int kept = 0;
-  bool ina = p0 + lane < h0, inb = p1 + lane < h1;
-  int ra = ina ? __ldg(arow + p0 + lane) : INT_MAX;
-  int rb = inb ? __ldg(arow + p1 + lane) : INT_MAX;
-  double va = ina ? __ldg(aval + p0 + lane) : 0.0;
-  double vb = inb ? __ldg(aval + p1 + lane) : 0.0;
+  const int32_t* __restrict__ rap = A.arow + b0;
+  const int32_t* __restrict__ rbp = A.arow + b1;
+  const double* __restrict__ vap = A.aval + b0;
+  const double* __restrict__ vbp = A.aval + b1;
+  int32_t* __restrict__ wr0 = A.wrow + d0;
+  int32_t* __restrict__ wr1 = A.wrow + d1;
+  double* __restrict__ wv0 = A.wval + d0;
+  double* __restrict__ wv1 = A.wval + d1;
+  const int h0 = static_cast<int>(e0 - b0), h1 = static_cast<int>(e1 - b1);
+  int p0 = 0, p1 = 0, kept = 0;
+  bool ina = lane < h0, inb = lane < h1;
+  int ra = ina ? __ldg(rap + lane) : INT_MAX;
+  int rb = inb ? __ldg(rbp + lane) : INT_MAX;
+  double va = ina ? __ldg(vap + lane) : 0.0;
+  double vb = inb ? __ldg(vbp + lane) : 0.0;
   while (p0 < h0 || p1 < h1) {
     const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
     const bool oka = ra != INT_MAX && ra <= frontier;
@@ -704,10 +731,10 @@ __device__ __forceinline__ int merge_write2_pf(const PassArgs& A, const double (
     p1 += nb;
     ina = p0 + lane < h0;
     inb = p1 + lane < h1;
-    const int nra = ina ? __ldg(arow + p0 + lane) : INT_MAX;
-    const int nrb = inb ? __ldg(arow + p1 + lane) : INT_MAX;
-    const double nva = ina ? __ldg(aval + p0 + lane) : 0.0;
-    const double nvb = inb ? __ldg(aval + p1 + lane) : 0.0;
+    const int nra = ina ? __ldg(rap + p0 + lane) : INT_MAX;
+    const int nrb = inb ? __ldg(rbp + p1 + lane) : INT_MAX;
+    const double nva = ina ? __ldg(vap + p0 + lane) : 0.0;
+    const double nvb = inb ? __ldg(vbp + p1 + lane) : 0.0;
     const int la = warp_lower_bound(rb, ra);  // B-window rows < ra
     const int lb = warp_lower_bound(ra, rb);  // A-window rows < rb
     const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
@@ -719,18 +746,18 @@ __device__ __forceinline__ int merge_write2_pf(const PassArgs& A, const double (
     if (oka) {
       const double x1 = pa ? vp : 0.0;
       const unsigned mb = la >= 32 ? 0xffffffffu : ((1u << la) - 1u);
-      const i64 r = kept + lane + __popc(BO & mb);
-      A.wrow[d0 + r] = ra;
-      A.wval[d0 + r] = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
-      A.wrow[d1 + r] = ra;
-      A.wval[d1 + r] = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
+      const int r = kept + lane + __popc(BO & mb);
+      wr0[r] = ra;
+      wv0[r] = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
+      wr1[r] = ra;
+      wv1[r] = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
     }
     if (bonly) {
-      const i64 r = kept + lb + __popc(BO & below);
-      A.wrow[d0 + r] = rb;
-      A.wval[d0 + r] = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
-      A.wrow[d1 + r] = rb;
-      A.wval[d1 + r] = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
+      const int r = kept + lb + __popc(BO & below);
+      wr0[r] = rb;
+      wv0[r] = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
+      wr1[r] = rb;
+      wv1[r] = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
     }
     kept += na + __popc(BO);
     ra = nra;
@@ -741,10 +768,187 @@ __device__ __forceinline__ int merge_write2_pf(const PassArgs& A, const double (
   return kept;
 }
 
-template <bool kWrite>
-__global__ void __launch_bounds__(kThreads, 4) k_merge2(PassArgs A, const int64_t* __restrict__ nitems_d,
+// ---- merge loops fed from a per-warp shared-memory ring -----------------
+// The loops above load a window after the previous window's advance is known,
+// so at most one window per input is in flight per warp and the loads' DRAM
+// latency sits inside the window-to-window chain (ncu: 66% of the stall
+// samples are long-scoreboard waits on exactly those loads, 3.5 TB/s).  Here
+// each input streams through a ring of four 32-entry chunks filled by
+// cp.async (LDGSTS, no registers): chunk c+4 is requested when the window
+// leaves chunk c, three or more iterations before its first use, and a window
+// is read from shared memory at any alignment.  One commit group per
+// iteration; `cp.async.wait_group 2` at the top of an iteration covers every
+// chunk the window can touch (an iteration advances an input by <= 32).
+constexpr int kRing = 128;  // entries per input: 4 chunks of 32
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// Requests chunk `c` (entries [32c, 32c+32) of the slice) into its ring slot.
+template <bool kVals>
+__device__ __forceinline__ void ring_issue(uint32_t rs, uint32_t vs, const int32_t* __restrict__ rp,
+                                           const double* __restrict__ vp, int c, int h) {
+  const int idx = c * 32 + (threadIdx.x & 31);
+  if (idx < h) {
+    cp_async4(rs + static_cast<uint32_t>(idx & (kRing - 1)) * 4u, rp + idx);
+    if (kVals) cp_async8(vs + static_cast<uint32_t>(idx & (kRing - 1)) * 8u, vp + idx);
+  }
+}
+
+__device__ __forceinline__ int merge_count2_ring(const int32_t* __restrict__ arow, const i64 b0, const i64 b1,
+                                                 const i64 e0, const i64 e1, int32_t (*ring_r)[kRing]) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* __restrict__ rap = arow + b0;
+  const int32_t* __restrict__ rbp = arow + b1;
+  const int h0 = static_cast<int>(e0 - b0), h1 = static_cast<int>(e1 - b1);
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(ring_r[0]));
+  const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(ring_r[1]));
+  __syncwarp();  // the previous item's window reads are done
+  ring_issue<false>(sa, 0, rap, nullptr, 0, h0);
+  ring_issue<false>(sa, 0, rap, nullptr, 1, h0);
+  ring_issue<false>(sb, 0, rbp, nullptr, 0, h1);
+  ring_issue<false>(sb, 0, rbp, nullptr, 1, h1);
+  cp_async_commit();
+  ring_issue<false>(sa, 0, rap, nullptr, 2, h0);
+  ring_issue<false>(sb, 0, rbp, nullptr, 2, h1);
+  cp_async_commit();
+  ring_issue<false>(sa, 0, rap, nullptr, 3, h0);
+  ring_issue<false>(sb, 0, rbp, nullptr, 3, h1);
+  cp_async_commit();
+  int p0 = 0, p1 = 0, c0 = 0, c1 = 0, kept = 0;
+  while (p0 < h0 || p1 < h1) {
+    cp_async_wait<2>();
+    __syncwarp();
+    const int ra = p0 + lane < h0 ? ring_r[0][(p0 + lane) & (kRing - 1)] : INT_MAX;
+    const int rb = p1 + lane < h1 ? ring_r[1][(p1 + lane) & (kRing - 1)] : INT_MAX;
+    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
+    const bool oka = ra != INT_MAX && ra <= frontier;
+    const bool okb = rb != INT_MAX && rb <= frontier;
+    const int na = __popc(__ballot_sync(0xffffffffu, oka));
+    const int nb = __popc(__ballot_sync(0xffffffffu, okb));
+    p0 += na;
+    p1 += nb;
+    __syncwarp();  // every lane has read its window before a slot is refilled
+    if ((p0 >> 5) > c0) {
+      ring_issue<false>(sa, 0, rap, nullptr, c0 + 4, h0);
+      ++c0;
+    }
+    if ((p1 >> 5) > c1) {
+      ring_issue<false>(sb, 0, rbp, nullptr, c1 + 4, h1);
+      ++c1;
+    }
+    cp_async_commit();
+    const int la = warp_lower_bound(rb, ra);
+    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
+    const bool pa = oka && la < 32 && ca == ra;
+    kept += na + nb - __popc(__ballot_sync(0xffffffffu, pa));
+  }
+  cp_async_wait<0>();
+  return kept;
+}
+
+__device__ __forceinline__ int merge_write2_ring(const PassArgs& A, const double (&q)[2][2], const i64 b0,
+                                                 const i64 b1, const i64 e0, const i64 e1, const i64 d0,
+                                                 const i64 d1, int32_t (*ring_r)[kRing], double (*ring_v)[kRing]) {
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  const int32_t* __restrict__ rap = A.arow + b0;
+  const int32_t* __restrict__ rbp = A.arow + b1;
+  const double* __restrict__ vap = A.aval + b0;
+  const double* __restrict__ vbp = A.aval + b1;
+  int32_t* __restrict__ wr0 = A.wrow + d0;
+  int32_t* __restrict__ wr1 = A.wrow + d1;
+  double* __restrict__ wv0 = A.wval + d0;
+  double* __restrict__ wv1 = A.wval + d1;
+  const int h0 = static_cast<int>(e0 - b0), h1 = static_cast<int>(e1 - b1);
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(ring_r[0]));
+  const uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(ring_r[1]));
+  const uint32_t ta = static_cast<uint32_t>(__cvta_generic_to_shared(ring_v[0]));
+  const uint32_t tb = static_cast<uint32_t>(__cvta_generic_to_shared(ring_v[1]));
+  __syncwarp();  // the previous item's window reads are done
+  ring_issue<true>(sa, ta, rap, vap, 0, h0);
+  ring_issue<true>(sa, ta, rap, vap, 1, h0);
+  ring_issue<true>(sb, tb, rbp, vbp, 0, h1);
+  ring_issue<true>(sb, tb, rbp, vbp, 1, h1);
+  cp_async_commit();
+  ring_issue<true>(sa, ta, rap, vap, 2, h0);
+  ring_issue<true>(sb, tb, rbp, vbp, 2, h1);
+  cp_async_commit();
+  ring_issue<true>(sa, ta, rap, vap, 3, h0);
+  ring_issue<true>(sb, tb, rbp, vbp, 3, h1);
+  cp_async_commit();
+  int p0 = 0, p1 = 0, c0 = 0, c1 = 0, kept = 0;
+  while (p0 < h0 || p1 < h1) {
+    cp_async_wait<2>();
+    __syncwarp();
+    const bool ina = p0 + lane < h0, inb = p1 + lane < h1;
+    const int ia = (p0 + lane) & (kRing - 1), ib = (p1 + lane) & (kRing - 1);
+    const int ra = ina ? ring_r[0][ia] : INT_MAX;
+    const int rb = inb ? ring_r[1][ib] : INT_MAX;
+    const double va = ina ? ring_v[0][ia] : 0.0;
+    const double vb = inb ? ring_v[1][ib] : 0.0;
+    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
+    const bool oka = ra != INT_MAX && ra <= frontier;
+    const bool okb = rb != INT_MAX && rb <= frontier;
+    const int na = __popc(__ballot_sync(0xffffffffu, oka));
+    const int nb = __popc(__ballot_sync(0xffffffffu, okb));
+    p0 += na;
+    p1 += nb;
+    __syncwarp();  // every lane has read its window before a slot is refilled
+    if ((p0 >> 5) > c0) {
+      ring_issue<true>(sa, ta, rap, vap, c0 + 4, h0);
+      ++c0;
+    }
+    if ((p1 >> 5) > c1) {
+      ring_issue<true>(sb, tb, rbp, vbp, c1 + 4, h1);
+      ++c1;
+    }
+    cp_async_commit();
+    const int la = warp_lower_bound(rb, ra);  // B-window rows < ra
+    const int lb = warp_lower_bound(ra, rb);  // A-window rows < rb
+    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
+    const int cb = __shfl_sync(0xffffffffu, ra, lb & 31);
+    const double vp = __shfl_sync(0xffffffffu, vb, la & 31);
+    const bool pa = la < 32 && ca == ra;
+    const bool bonly = okb && !(lb < 32 && cb == rb);
+    const unsigned BO = __ballot_sync(0xffffffffu, bonly);
+    if (oka) {
+      const double x1 = pa ? vp : 0.0;
+      const unsigned mb = la >= 32 ? 0xffffffffu : ((1u << la) - 1u);
+      const int r = kept + lane + __popc(BO & mb);
+      wr0[r] = ra;
+      wv0[r] = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
+      wr1[r] = ra;
+      wv1[r] = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
+    }
+    if (bonly) {
+      const int r = kept + lb + __popc(BO & below);
+      wr0[r] = rb;
+      wv0[r] = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
+      wr1[r] = rb;
+      wv1[r] = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
+    }
+    kept += na + __popc(BO);
+  }
+  cp_async_wait<0>();
+  return kept;
+}
+
+template <bool kWrite, int kOcc>
+__global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int64_t* __restrict__ nitems_d,
                                                         const int32_t* __restrict__ ovf) {
   __shared__ ItemRec recs[kMerge2Warps][32];
+  __shared__ int32_t ring_r[kMerge2Warps][2][kRing];
+  __shared__ double ring_v[kMerge2Warps][2][kWrite ? kRing : 1];
+  const bool merge_prefetch = A.prefetch;
+  const bool use_ring = A.ring;
   if (*reinterpret_cast<volatile const int32_t*>(ovf) != INT_MAX) return;
   const i64 nitems = *nitems_d;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -785,6 +989,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_merge2(PassArgs A, const int64_
     for (int j = 0; j < cnt; ++j) {
       const ItemRec& r = rec[j];
       const int np = r.np, p = r.p, ri = r.ri;
+      // next item's inputs into L2 while this one is merged: both columns of a
+      // single-partition rotation, the longest input's slice of a partition
+      // (the other input's slice needs the search below)
+      if (merge_prefetch && j + 1 < cnt) {
+        const ItemRec& x = rec[j + 1];
+        if (x.np == 1) {
+          if (kWrite) {
+            prefetch_range<true>(A.arow, A.aval, x.off[0], x.off[0] + x.len[0]);
+            prefetch_range<true>(A.arow, A.aval, x.off[1], x.off[1] + x.len[1]);
+          }
+        } else {
+          const int lg = x.len[1] > x.len[0] ? 1 : 0;
+          const i64 b = x.off[lg] + static_cast<i64>(x.p) * A.chunk;
+          prefetch_range<kWrite>(A.arow, A.aval, b, min(b + A.chunk, x.off[lg] + x.len[lg]));
+        }
+      }
       if (!kWrite && np == 1) continue;  // counted by its own write pass
       const double q[2][2] = {{r.q[0][0], r.q[0][1]}, {r.q[1][0], r.q[1][1]}};
       i64 beg[2], end[2];
@@ -809,6 +1029,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_merge2(PassArgs A, const int64_
         end[0] = lg ? hi_o : hi_l;
         beg[1] = lg ? lo_l : lo_o;
         end[1] = lg ? hi_l : hi_o;
+        if (merge_prefetch) prefetch_range<kWrite>(A.arow, A.aval, lo_o, hi_o);
+      }
+      if (merge_prefetch && j == 0) {  // a batch's first item had no predecessor
+        prefetch_range<kWrite>(A.arow, A.aval, beg[0], end[0]);
+        prefetch_range<kWrite>(A.arow, A.aval, beg[1], end[1]);
       }
       int r0 = 0;
       const int dl = identical_rows<2>(A, beg, end, r0);
@@ -837,7 +1062,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_merge2(PassArgs A, const int64_
         u = dl;
       } else if (np == 1) {
         // single partition: count the union, allocate 2u, write
-        u = merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
+        u = use_ring ? merge_count2_ring(A.arow, beg[0], beg[1], end[0], end[1], ring_r[wib])
+                     : merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
         unsigned long long b0 = 0;
         if (lane == 0) b0 = atomicAdd(A.cursor, 2ull * static_cast<unsigned long long>(u));
         b0 = __shfl_sync(0xffffffffu, b0, 0);
@@ -846,7 +1072,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_merge2(PassArgs A, const int64_
           continue;
         }
         const i64 d0 = static_cast<i64>(b0), d1 = d0 + u;
-        merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], d0, d1);
+        if constexpr (kWrite) {
+          if (use_ring)
+            merge_write2_ring(A, q, beg[0], beg[1], end[0], end[1], d0, d1, ring_r[wib], ring_v[wib]);
+          else
+            merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], d0, d1);
+        }
         if (lane == 0) {
           A.rbase[2 * ri] = d0;
           A.rbase[2 * ri + 1] = d1;
@@ -855,10 +1086,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_merge2(PassArgs A, const int64_
         }
         produced += 2ull * static_cast<unsigned long long>(u);
         continue;
-      } else if (kWrite) {
-        u = merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], r.dst[0], r.dst[1]);
+      } else if constexpr (kWrite) {
+        u = use_ring ? merge_write2_ring(A, q, beg[0], beg[1], end[0], end[1], r.dst[0], r.dst[1], ring_r[wib],
+                                         ring_v[wib])
+                     : merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], r.dst[0], r.dst[1]);
       } else {
-        u = merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
+        u = use_ring ? merge_count2_ring(A.arow, beg[0], beg[1], end[0], end[1], ring_r[wib])
+                     : merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
       }
       if (!kWrite && lane == 0) {
         A.cnt[r.dst[0] + p] = u;
@@ -1355,6 +1589,7 @@ void exscan(const T* in, T* out, i64 n, cudaStream_t s) {
 }
 
 i64 read_i64(const i64* p, cudaStream_t s) {
+  SlowCall slow_("read_i64");
   i64 v = 0;
   PMMF_CUDA(cudaMemcpyAsync(&v, p, sizeof(v), cudaMemcpyDeviceToHost, s));
   PMMF_CUDA(cudaStreamSynchronize(s));
@@ -1393,26 +1628,35 @@ struct Batch {
 // Per column c: the entries of retired rows g that it contributes to the
 // mass of g (c taken when it survives or retires after g); the diagonal
 // entry (g == c) goes to diag.
-__global__ void k_mass_count(i64 S, i64 col0, const int32_t* __restrict__ seg_col, const i64* __restrict__ sfirst,
-                             const i64* __restrict__ off, const int32_t* __restrict__ len,
-                             const int32_t* __restrict__ arow, const double* __restrict__ aval, MassSpec M,
-                             i64* __restrict__ cnt) {
+// Kept entries (k_final_count) and taken mass entries per segment in one pass
+// over the segment's rows; the diagonal entry (g == c) goes to diag.
+__global__ void k_final_mass_count(i64 S, i64 col0, const int32_t* __restrict__ seg_col,
+                                   const i64* __restrict__ sfirst, const i64* __restrict__ off,
+                                   const int32_t* __restrict__ len, const int32_t* __restrict__ arow,
+                                   const double* __restrict__ aval, const uint8_t* __restrict__ keep_row,
+                                   const uint8_t* __restrict__ keep_all_col, MassSpec M, i64* __restrict__ kcnt,
+                                   i64* __restrict__ mcnt) {
   const i64 q = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (q > S) return;
   if (q == S) {
-    if (lane == 0) cnt[S] = 0;
+    if (lane == 0) {
+      kcnt[S] = 0;
+      mcnt[S] = 0;
+    }
     return;
   }
   i64 w;
   int b, e;
   seg_range(nullptr, q, seg_col, sfirst, len, w, b, e);
+  const bool all = keep_row == nullptr || (keep_all_col != nullptr && keep_all_col[col0 + w]);
   const int32_t c = static_cast<int32_t>(col0 + w);
   const int32_t key = M.col_key[c];
   const i64 s0 = off[w];
-  int n = 0;
+  int n = 0, kc = 0;
   for (int i = b + lane; i < e; i += 32) {
     const int32_t g = arow[s0 + i];
+    if (!all) kc += keep_row[g];
     const int32_t rg = M.row_rank[g];
     if (rg < 0) continue;
     if (g == c)
@@ -1420,8 +1664,14 @@ __global__ void k_mass_count(i64 S, i64 col0, const int32_t* __restrict__ seg_co
     else
       n += key > rg;
   }
-  for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-  if (lane == 0) cnt[q] = n;
+  for (int o = 16; o; o >>= 1) {
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+    kc += __shfl_xor_sync(0xffffffffu, kc, o);
+  }
+  if (lane == 0) {
+    mcnt[q] = n;
+    kcnt[q] = all ? e - b : kc;
+  }
 }
 // Segments [q0, q1) of the batch: (rank of g, v^2) of the taken entries,
 // in column order.
@@ -1504,6 +1754,18 @@ __global__ void k_mass_buckets(i64 n, i64 nbuckets, int shift, const int32_t* __
     if (r0 + i < M.n_retired) mass[r0 + i] = m[i];
 }
 
+// Sort-key bits of the mass buckets (PMMF_B200_MASS_KBITS, tuning): fewer
+// bits = wider buckets = fewer equal-rank conflicts per 32-entry window, but
+// fewer bucket warps.
+inline int mass_key_bits() {
+  static const int v = [] {
+    const char* e = std::getenv("PMMF_B200_MASS_KBITS");
+    const int b = e ? std::atoi(e) : 16;
+    return b >= 4 && b <= 16 ? b : 16;
+  }();
+  return v;
+}
+
 // Per-batch device scratch for the asynchronous level pipeline.
 struct LevelScratch {
   i64 max_rot = 0, max_items = 0;
@@ -1530,6 +1792,38 @@ inline bool merge2_enabled() {
   }();
   return on;
 }
+inline bool merge_ring_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PMMF_B200_MERGE_RING");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+inline bool merge_prefetch_enabled() {  // measured: no gain with the ring (write pass 113.7 vs 106.7 ms)
+  static const bool on = [] {
+    const char* e = std::getenv("PMMF_B200_MERGE_PF");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+// Resident blocks per SM the k = 2 merge kernel is compiled for
+// (PMMF_B200_MERGE2_OCC = 4 | 5 | 6: registers per thread 64 | 48 | 40).
+inline int merge2_occ() {
+  static const int v = [] {
+    const char* e = std::getenv("PMMF_B200_MERGE2_OCC");
+    const int o = e ? std::atoi(e) : 4;
+    return o == 5 || o == 6 ? o : 4;
+  }();
+  return v;
+}
+template <bool kWrite>
+void launch_merge2(const PassArgs& A, int blocks, const int64_t* nitems, const int32_t* ovf, cudaStream_t s) {
+  switch (merge2_occ()) {
+    case 6: PMMF_LAUNCH((k_merge2<kWrite, 6>), blocks, kThreads, 0, s, A, nitems, ovf); break;
+    case 5: PMMF_LAUNCH((k_merge2<kWrite, 5>), blocks, kThreads, 0, s, A, nitems, ovf); break;
+    default: PMMF_LAUNCH((k_merge2<kWrite, 4>), blocks, kThreads, 0, s, A, nitems, ovf); break;
+  }
+}
 template <int K, bool kWrite>
 int persistent_blocks() {
   static const int nb = [] {
@@ -1537,7 +1831,9 @@ int persistent_blocks() {
     cudaError_t e = cudaSuccess;
     if constexpr (K == 2) {
       if (merge2_enabled())
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite>, kThreads, 0);
+        e = merge2_occ() == 6   ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite, 6>, kThreads, 0)
+            : merge2_occ() == 5 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite, 5>, kThreads, 0)
+                                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite, 4>, kThreads, 0);
       else
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0);
     } else {
@@ -1639,6 +1935,8 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.level = level;
   A.rbase = S.rbase.get();
   A.rlen = S.rlen.get();
+  A.prefetch = merge_prefetch_enabled();
+  A.ring = merge_ring_enabled();
   if (nrot <= kSetupMax && !std::getenv("PMMF_B200_NO_LEVEL_SETUP")) {
     PMMF_LAUNCH(k_level_setup<K>, 1, kSetupThreads, 0, s, A, S.np.get(), S.ioff.get(), S.nitems.get(),
                 S.item_rot.get(), S.in_entries.get(), pending, S.rbase.get(), S.rlen.get(), B.off.get(),
@@ -1662,7 +1960,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     cudaEventRecord(c0, s);
   }
   if (K == 2 && merge2_enabled())
-    PMMF_LAUNCH(k_merge2<false>, (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+    launch_merge2<false>(A, persistent_blocks<K, false>(), S.nitems.get(), S.ovf.get(), s);
   else
     PMMF_LAUNCH((k_merge_p<K, false>), (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (c0) {
@@ -1678,7 +1976,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     cudaEventRecord(e0, s);
   }
   if (K == 2 && merge2_enabled())
-    PMMF_LAUNCH(k_merge2<true>, (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+    launch_merge2<true>(A, persistent_blocks<K, true>(), S.nitems.get(), S.ovf.get(), s);
   else
     PMMF_LAUNCH((k_merge_p<K, true>), (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (e0) {
@@ -1765,7 +2063,7 @@ void build_segs(const Batch& B, Segs& G, cudaStream_t s) {
   PMMF_LAUNCH(k_seg_fill, blocks_for(B.N, kThreads), kThreads, 0, s, B.N, G.first.get(), G.col.get());
 }
 
-void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, cudaStream_t s) {
+void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, const DBuf<i64>& cnt, cudaStream_t s) {
   const bool tr = trace_enabled();
   double tms[4] = {0, 0, 0, 0};
   auto tl = std::chrono::steady_clock::now();
@@ -1777,9 +2075,7 @@ void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, cudaStream_t
     tl = now;
   };
   const i64 S = G.n;
-  DBuf<i64> cnt(S + 1, s), pos(S + 1, s);
-  PMMF_LAUNCH(k_mass_count, blocks_for((S + 1) * 32, kThreads), kThreads, 0, s, S, B.col0, G.col.get(), G.first.get(),
-              B.off.get(), B.len.get(), B.row.get(), B.val.get(), M, cnt.get());
+  DBuf<i64> pos(S + 1, s);  // cnt: taken entries per segment (k_final_mass_count)
   exscan(cnt.get(), pos.get(), S + 1, s);
   const std::vector<i64> hp = pos.to_host(S + 1);
   if (hp[S] == 0) return;
@@ -1787,7 +2083,7 @@ void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, cudaStream_t
   const i64 cap = std::min<i64>(hp[S], chunk);
   // buckets of 2^shift ranks: a 16-bit sort key (two radix passes)
   const int rb = std::max(1, bits_for(std::max<i64>(M.n_retired - 1, 1)));
-  const int shift = std::max(0, rb - 16);
+  const int shift = std::max(0, rb - mass_key_bits());
   const int kbits = rb - shift;
   const i64 nbuckets = ((M.n_retired - 1) >> shift) + 1;
   DBuf<int32_t> k1, k2;
@@ -2117,18 +2413,24 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     double t_mass = 0.0;
     Segs G;
     build_segs(B, G, s);
+    DBuf<i64> cnt(G.n + 1, s), spos(G.n + 1, s);
     if (ms) {
-      batch_masses(B, G, *ms, s);
+      // kept-entry and taken-entry counts per segment in one pass over the rows
+      DBuf<i64> mcnt(G.n + 1, s);
+      PMMF_LAUNCH(k_final_mass_count, blocks_for((G.n + 1) * 32, kThreads), kThreads, 0, s, G.n, B.col0, G.col.get(),
+                  G.first.get(), B.off.get(), B.len.get(), B.row.get(), B.val.get(), keep_row, keep_all_col, *ms,
+                  cnt.get(), mcnt.get());
+      batch_masses(B, G, *ms, mcnt, s);
       if (tr) t_mass = since(tb);
+    } else {
+      PMMF_LAUNCH(k_final_count, blocks_for((G.n + 1) * 32, kThreads), kThreads, 0, s, G.n, B.col0, G.col.get(),
+                  G.first.get(), B.off.get(), B.len.get(), B.row.get(), keep_row, keep_all_col, cnt.get());
     }
     // finalize into a compact piece
     Piece P;
     P.c0 = B.col0;
     P.c1 = B.col0 + B.N;
-    DBuf<i64> cnt(G.n + 1, s), spos(G.n + 1, s);
     P.ptr.alloc(B.N + 1, s);
-    PMMF_LAUNCH(k_final_count, blocks_for((G.n + 1) * 32, kThreads), kThreads, 0, s, G.n, B.col0, G.col.get(),
-                G.first.get(), B.off.get(), B.len.get(), B.row.get(), keep_row, keep_all_col, cnt.get());
     exscan(cnt.get(), spos.get(), G.n + 1, s);
     PMMF_LAUNCH(k_seg_ptr, blocks_for(B.N + 1, kThreads), kThreads, 0, s, B.N, G.first.get(), spos.get(), P.ptr.get());
     P.nnz = read_i64(spos.get() + G.n, s);

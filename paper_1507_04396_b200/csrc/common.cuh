@@ -38,12 +38,38 @@ struct Error {
                                        " (" + __FILE__ + ":" + std::to_string(__LINE__) + ")"); \
   } while (0)
 
+// Diagnostic (PMMF_B200_SLOWCALL=<ms>): reports any instrumented host call
+// (allocation, copy, launch, memset) that blocks longer than the threshold --
+// host-side stalls inside the launch-bound late stages show up here.
+inline double slowcall_ms() {
+  static const double v = [] {
+    const char* e = std::getenv("PMMF_B200_SLOWCALL");
+    return e ? std::atof(e) : 0.0;
+  }();
+  return v;
+}
+struct SlowCall {
+  const char* what;
+  size_t arg;
+  std::chrono::steady_clock::time_point t0;
+  bool on;
+  explicit SlowCall(const char* w, size_t a = 0) : what(w), arg(a), on(slowcall_ms() > 0.0) {
+    if (on) t0 = std::chrono::steady_clock::now();
+  }
+  ~SlowCall() {
+    if (!on) return;
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (ms > slowcall_ms()) std::fprintf(stderr, "[pmmf] slow call: %s (%zu) %.2f ms\n", what, arg, ms);
+  }
+};
+
 // Every kernel launch in csrc/ goes through PMMF_LAUNCH so the library can
 // report how many of its own kernels ran (bench.py "gpu_launches").
 std::atomic<int64_t>& launch_counter();
 #define PMMF_LAUNCH(kernel, grid, block, smem, stream, ...)                  \
   do {                                                                       \
     if ((grid) > 0) {                                                        \
+      ::pmmf_b200::SlowCall slow_(#kernel);                                  \
       kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);            \
       ::pmmf_b200::launch_counter().fetch_add(1, std::memory_order_relaxed); \
       PMMF_CUDA(cudaGetLastError());                                         \
@@ -325,6 +351,7 @@ inline std::atomic<uint64_t>& fresh_big_bytes() {
 // cache, trims the pool and is retried once.  *bytes is updated to the size
 // actually held.
 inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
+  SlowCall slow_("pool_alloc", *bytes);
   int dev = 0;
   PMMF_CUDA(cudaGetDevice(&dev));
   if (*bytes >= kBigBytes) {
@@ -374,6 +401,7 @@ inline void pool_alloc(void** p, size_t* bytes, cudaStream_t st) {
   }
 }
 inline void pool_free(void* p, size_t bytes, cudaStream_t st) {
+  SlowCall slow_("pool_free", bytes);
   if (AllocCheck::on()) AllocCheck::get().remove(p, bytes);
   if (bytes >= kBigBytes) {
     int dev = 0;
@@ -443,13 +471,16 @@ struct DBuf {
     if (n) PMMF_CUDA(cudaMemsetAsync(p, v, sizeof(T) * static_cast<size_t>(n), s));
   }
   void upload(const T* h, i64 count) const {
+    SlowCall slow_("upload", sizeof(T) * static_cast<size_t>(count));
     if (count) PMMF_CUDA(cudaMemcpyAsync(p, h, sizeof(T) * static_cast<size_t>(count), cudaMemcpyHostToDevice, s));
   }
   void upload(const std::vector<T>& h) const { upload(h.data(), static_cast<i64>(h.size())); }
   void download(T* h, i64 count) const {
+    SlowCall slow_("download", sizeof(T) * static_cast<size_t>(count));
     if (count) PMMF_CUDA(cudaMemcpyAsync(h, p, sizeof(T) * static_cast<size_t>(count), cudaMemcpyDeviceToHost, s));
   }
   std::vector<T> to_host(i64 count) const {
+    SlowCall slow_("to_host", sizeof(T) * static_cast<size_t>(count));
     std::vector<T> h(static_cast<size_t>(count));
     download(h.data(), count);
     PMMF_CUDA(cudaStreamSynchronize(s));
