@@ -605,7 +605,7 @@ def main():
     barrier()
     e2e_ms = []
     out_bytes = 0
-    for _ in range(max(1, min(args.steps, 2))):
+    for _ in range(max(1, min(args.steps, 10))):
         torch.cuda.synchronize()
         t = time.perf_counter()
         _, out_bytes = run_e2e()

@@ -90,8 +90,10 @@ struct PassArgs {
   int level;
   i64* rbase;
   int32_t* rlen;
-  bool prefetch;  // k_merge2: L2 prefetch of the items' inputs (PMMF_B200_MERGE_PF=1, default off)
-  bool ring;      // k_merge2: windows from the cp.async shared-memory ring (PMMF_B200_MERGE_RING, default on)
+  // k = 2 count pass: counted partitions per level-rotation; the warp that
+  // counts a rotation's last partition allocates it (rot_alloc_warp), so the
+  // level needs no separate allocation launch (nullptr: k_rot_alloc runs)
+  int32_t* ndone;
 };
 
 // Row range of partition p of rotation t: split points are rows of the
@@ -364,6 +366,7 @@ __global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long
     S += static_cast<unsigned long long>(L);
   }
   nparts[i] = max(1, (Lmax + A.chunk - 1) / A.chunk);
+  if (A.ndone) A.ndone[i] = 0;
   atomicAdd(in_entries, S);
 }
 
@@ -425,6 +428,7 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
       }
       v = max(1, (Lmax + A.chunk - 1) / A.chunk);
       np[i] = v;
+      if (A.ndone) A.ndone[i] = 0;
     }
     int64_t ex = 0, tot = 0;
     BlockScan(scan).ExclusiveSum(v, ex, tot);
@@ -446,6 +450,54 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
 __global__ void k_items(i64 nrot, const int64_t* __restrict__ ioff, const int64_t* __restrict__ np,
                         int64_t* __restrict__ nitems) {
   if (threadIdx.x == 0 && blockIdx.x == 0) *nitems = ioff[nrot - 1] + np[nrot - 1];
+}
+
+// One warp, k = 2: exclusive scan of rotation i's partition counts (the union
+// size, the same for both output columns), one arena allocation of twice the
+// total; a partition writes at rbase[2i + b] + pos[2 io + p].  Counts come
+// from L2 (ld.cg: other SMs wrote them in this launch), four chunks of 32 in
+// flight (a hub rotation has ~2,000 partitions, and this warp is the tail of
+// the count pass).
+__device__ __forceinline__ void rot_alloc_warp2(const PassArgs& A, i64 i, i64 io, i64 np) {
+  const int lane = threadIdx.x & 31;
+  const i64 f = 2 * io;
+  int64_t* pos = const_cast<int64_t*>(A.pos);
+  i64 run = 0;
+  for (i64 p0 = 0; p0 < np; p0 += 128) {
+    i64 c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const i64 p = p0 + 32 * j + lane;
+      c[j] = p < np ? __ldcg(A.cnt + f + p) : 0;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const i64 p = p0 + 32 * j + lane;
+      i64 incl = c[j];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const i64 v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (p < np) pos[f + p] = run + incl - c[j];
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  const i64 all = 2 * run;
+  unsigned long long b = 0;
+  if (lane == 0) b = atomicAdd(A.cursor, static_cast<unsigned long long>(all));
+  b = __shfl_sync(0xffffffffu, b, 0);
+  if (static_cast<i64>(b) + all > A.cap) {
+    if (lane == 0) atomicMin(A.ovf, A.level);
+    return;
+  }
+  if (lane == 0) {
+    atomicAdd(A.out_entries, static_cast<unsigned long long>(all));
+    A.rbase[2 * i] = static_cast<i64>(b);
+    A.rbase[2 * i + 1] = static_cast<i64>(b) + run;
+    A.rlen[2 * i] = static_cast<int32_t>(run);
+    A.rlen[2 * i + 1] = static_cast<int32_t>(run);
+  }
 }
 
 // Per rotation: exclusive scan of its partitions' kept counts per output
@@ -630,9 +682,8 @@ __global__ void __launch_bounds__(256, K == 2 ? 6 : 2) k_merge_p(PassArgs A, con
 //    ~6 dependent global loads is paid once per 32 items, not per item;
 //  * partition bounds by a warp-wide search (32 probes per round: 4 rounds
 //    for 10^6 entries instead of 20 dependent binary-search loads);
-//  * one-window-ahead prefetch in the merge loops: a window's advance
-//    (frontier, ballots) is known before its rank searches and stores, so
-//    the next window's rows and values are requested first.
+//  * merge windows read from a per-warp shared-memory ring that cp.async
+//    fills three or more windows ahead (below).
 struct ItemRec {
   i64 off[2];
   i64 dst[2];
@@ -640,6 +691,13 @@ struct ItemRec {
   int32_t ri, p, np, len[2], pad;
 };
 constexpr int kMerge2Warps = kThreads / 32;
+// Resident blocks per SM the kernel is compiled for (64 registers).  Measured
+// with the ring, write pass per config-4 step: 2: 115.6, 3: 107.1, 4: 106.9,
+// 5 (48 registers): 125.5, 6 (40 registers): 159.1 ms.  A two-level window
+// search (8 independent pivot probes + 3, a chain of two shuffles instead of
+// six) measured 114.5 against 111.1 ms: rejected.
+constexpr int kMerge2Occ = 4;
+constexpr int kItemBatch = 16;  // items resolved per prologue (<= 32); 11 KB of records per block
 
 // First index i in [lo, hi) with a[i] >= key (hi if none), warp-wide.
 __device__ __forceinline__ i64 warp_search_g(const int32_t* __restrict__ a, i64 lo, i64 hi, int key) {
@@ -658,121 +716,13 @@ __device__ __forceinline__ i64 warp_search_g(const int32_t* __restrict__ a, i64 
   return lo + __popc(__ballot_sync(0xffffffffu, lt));
 }
 
-// L2 prefetch of entries [b, e) of the arena (one 128-byte line per lane and
-// round): the merge loops below then find their windows in L2 instead of
-// paying the DRAM latency inside the window-to-window dependency chain.
-template <bool kVals>
-__device__ __forceinline__ void prefetch_range(const int32_t* __restrict__ arow, const double* __restrict__ aval,
-                                               i64 b, i64 e) {
-  const int lane = threadIdx.x & 31;
-  for (i64 o = b + lane * 32; o < e; o += 1024) asm volatile("prefetch.global.L2 [%0];" ::"l"(arow + o));
-  if (kVals)
-    for (i64 o = b + lane * 16; o < e; o += 512) asm volatile("prefetch.global.L2 [%0];" ::"l"(aval + o));
-}
-
-// Both loops index their inputs and outputs with 32-bit offsets from the
-// partition's base pointers (a column holds < 2^31 entries): one IMAD.WIDE per
-// access instead of 64-bit adds and compares.
-__device__ __forceinline__ int merge_count2_pf(const int32_t* __restrict__ arow, const i64 b0, const i64 b1,
-                                               const i64 e0, const i64 e1) {
-  const int lane = threadIdx.x & 31;
-  const int32_t* __restrict__ rap = arow + b0;
-  const int32_t* __restrict__ rbp = arow + b1;
-  const int h0 = static_cast<int>(e0 - b0), h1 = static_cast<int>(e1 - b1);
-  int p0 = 0, p1 = 0, kept = 0;
-  int ra = lane < h0 ? __ldg(rap + lane) : INT_MAX;
-  int rb = lane < h1 ? __ldg(rbp + lane) : INT_MAX;
-  while (p0 < h0 || p1 < h1) {
-    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
-    const bool oka = ra != INT_MAX && ra <= frontier;
-    const bool okb = rb != INT_MAX && rb <= frontier;
-    const int na = __popc(__ballot_sync(0xffffffffu, oka));
-    const int nb = __popc(__ballot_sync(0xffffffffu, okb));
-    p0 += na;
-    p1 += nb;
-    const int nra = p0 + lane < h0 ? __ldg(rap + p0 + lane) : INT_MAX;
-    const int nrb = p1 + lane < h1 ? __ldg(rbp + p1 + lane) : INT_MAX;
-    const int la = warp_lower_bound(rb, ra);
-    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
-    const bool pa = oka && la < 32 && ca == ra;
-    kept += na + nb - __popc(__ballot_sync(0xffffffffu, pa));
-    ra = nra;
-    rb = nrb;
-  }
-  return kept;
-}
-
-__device__ __forceinline__ int merge_write2_pf(const PassArgs& A, const double (&q)[2][2], const i64 b0, const i64 b1,
-                                               const i64 e0, const i64 e1, const i64 d0, const i64 d1) {
-  const int lane = threadIdx.x & 31;
-  const unsigned below = (1u << lane) - 1u;
-  const int32_t* __restrict__ rap = A.arow + b0;
-  const int32_t* __restrict__ rbp = A.arow + b1;
-  const double* __restrict__ vap = A.aval + b0;
-  const double* __restrict__ vbp = A.aval + b1;
-  int32_t* __restrict__ wr0 = A.wrow + d0;
-  int32_t* __restrict__ wr1 = A.wrow + d1;
-  double* __restrict__ wv0 = A.wval + d0;
-  double* __restrict__ wv1 = A.wval + d1;
-  const int h0 = static_cast<int>(e0 - b0), h1 = static_cast<int>(e1 - b1);
-  int p0 = 0, p1 = 0, kept = 0;
-  bool ina = lane < h0, inb = lane < h1;
-  int ra = ina ? __ldg(rap + lane) : INT_MAX;
-  int rb = inb ? __ldg(rbp + lane) : INT_MAX;
-  double va = ina ? __ldg(vap + lane) : 0.0;
-  double vb = inb ? __ldg(vbp + lane) : 0.0;
-  while (p0 < h0 || p1 < h1) {
-    const int frontier = min(__shfl_sync(0xffffffffu, ra, 31), __shfl_sync(0xffffffffu, rb, 31));
-    const bool oka = ra != INT_MAX && ra <= frontier;
-    const bool okb = rb != INT_MAX && rb <= frontier;
-    const int na = __popc(__ballot_sync(0xffffffffu, oka));
-    const int nb = __popc(__ballot_sync(0xffffffffu, okb));
-    p0 += na;
-    p1 += nb;
-    ina = p0 + lane < h0;
-    inb = p1 + lane < h1;
-    const int nra = ina ? __ldg(rap + p0 + lane) : INT_MAX;
-    const int nrb = inb ? __ldg(rbp + p1 + lane) : INT_MAX;
-    const double nva = ina ? __ldg(vap + p0 + lane) : 0.0;
-    const double nvb = inb ? __ldg(vbp + p1 + lane) : 0.0;
-    const int la = warp_lower_bound(rb, ra);  // B-window rows < ra
-    const int lb = warp_lower_bound(ra, rb);  // A-window rows < rb
-    const int ca = __shfl_sync(0xffffffffu, rb, la & 31);
-    const int cb = __shfl_sync(0xffffffffu, ra, lb & 31);
-    const double vp = __shfl_sync(0xffffffffu, vb, la & 31);
-    const bool pa = la < 32 && ca == ra;
-    const bool bonly = okb && !(lb < 32 && cb == rb);
-    const unsigned BO = __ballot_sync(0xffffffffu, bonly);
-    if (oka) {
-      const double x1 = pa ? vp : 0.0;
-      const unsigned mb = la >= 32 ? 0xffffffffu : ((1u << la) - 1u);
-      const int r = kept + lane + __popc(BO & mb);
-      wr0[r] = ra;
-      wv0[r] = dadd(dadd(0.0, dmul(q[0][0], va)), dmul(q[0][1], x1));
-      wr1[r] = ra;
-      wv1[r] = dadd(dadd(0.0, dmul(q[1][0], va)), dmul(q[1][1], x1));
-    }
-    if (bonly) {
-      const int r = kept + lb + __popc(BO & below);
-      wr0[r] = rb;
-      wv0[r] = dadd(dadd(0.0, dmul(q[0][0], 0.0)), dmul(q[0][1], vb));
-      wr1[r] = rb;
-      wv1[r] = dadd(dadd(0.0, dmul(q[1][0], 0.0)), dmul(q[1][1], vb));
-    }
-    kept += na + __popc(BO);
-    ra = nra;
-    rb = nrb;
-    va = nva;
-    vb = nvb;
-  }
-  return kept;
-}
-
 // ---- merge loops fed from a per-warp shared-memory ring -----------------
-// The loops above load a window after the previous window's advance is known,
-// so at most one window per input is in flight per warp and the loads' DRAM
-// latency sits inside the window-to-window chain (ncu: 66% of the stall
-// samples are long-scoreboard waits on exactly those loads, 3.5 TB/s).  Here
+// A loop that loads a window once the previous window's advance is known has
+// at most one window per input in flight per warp, and the loads' DRAM
+// latency sits inside the window-to-window chain (ncu of that variant: 66% of
+// the stall samples were long-scoreboard waits on exactly those loads; an L2
+// prefetch of the items' inputs did not help: write pass 120.6 ms either way,
+// 106.7 ms with the ring).  Here
 // each input streams through a ring of four 32-entry chunks filled by
 // cp.async (LDGSTS, no registers): chunk c+4 is requested when the window
 // leaves chunk c, three or more iterations before its first use, and a window
@@ -941,14 +891,12 @@ __device__ __forceinline__ int merge_write2_ring(const PassArgs& A, const double
   return kept;
 }
 
-template <bool kWrite, int kOcc>
-__global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int64_t* __restrict__ nitems_d,
+template <bool kWrite>
+__global__ void __launch_bounds__(kThreads, kMerge2Occ) k_merge2(PassArgs A, const int64_t* __restrict__ nitems_d,
                                                         const int32_t* __restrict__ ovf) {
-  __shared__ ItemRec recs[kMerge2Warps][32];
+  __shared__ ItemRec recs[kMerge2Warps][kItemBatch];
   __shared__ int32_t ring_r[kMerge2Warps][2][kRing];
   __shared__ double ring_v[kMerge2Warps][2][kWrite ? kRing : 1];
-  const bool merge_prefetch = A.prefetch;
-  const bool use_ring = A.ring;
   if (*reinterpret_cast<volatile const int32_t*>(ovf) != INT_MAX) return;
   const i64 nitems = *nitems_d;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -956,10 +904,10 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int
   const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   ItemRec* rec = recs[wib];
   unsigned long long produced = 0;  // profiling counter, one atomic per warp
-  for (i64 first = w; first < nitems; first += 32 * nw) {
+  for (i64 first = w; first < nitems; first += kItemBatch * nw) {
     {
       const i64 item = first + lane * nw;
-      if (item < nitems) {
+      if (lane < kItemBatch && item < nitems) {
         ItemRec r;
         const int ri = A.item_rot[item];
         const i64 io = A.ioff[ri];
@@ -976,7 +924,10 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int
             r.len[b] = A.len[id];
 #pragma unroll
             for (int a = 0; a < 2; ++a) r.q[b][a] = A.qs[(2 * static_cast<i64>(t) + b) * 2 + a];
-            r.dst[b] = (kWrite && r.np > 1) ? A.pos[2 * io + b * r.np + r.p] : 0;
+            // fused allocation (A.ndone): one within-column offset per partition + the column's base
+            r.dst[b] = !(kWrite && r.np > 1) ? 0
+                       : A.ndone            ? A.pos[2 * io + r.p] + A.rbase[2 * static_cast<i64>(ri) + b]
+                                            : A.pos[2 * io + b * r.np + r.p];
           }
           if (!kWrite) r.dst[0] = 2 * io;  // count slots of this rotation
         }
@@ -985,26 +936,10 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int
     }
     __syncwarp();
     const i64 left = (nitems - first + nw - 1) / nw;
-    const int cnt = left < 32 ? static_cast<int>(left) : 32;
+    const int cnt = left < kItemBatch ? static_cast<int>(left) : kItemBatch;
     for (int j = 0; j < cnt; ++j) {
       const ItemRec& r = rec[j];
       const int np = r.np, p = r.p, ri = r.ri;
-      // next item's inputs into L2 while this one is merged: both columns of a
-      // single-partition rotation, the longest input's slice of a partition
-      // (the other input's slice needs the search below)
-      if (merge_prefetch && j + 1 < cnt) {
-        const ItemRec& x = rec[j + 1];
-        if (x.np == 1) {
-          if (kWrite) {
-            prefetch_range<true>(A.arow, A.aval, x.off[0], x.off[0] + x.len[0]);
-            prefetch_range<true>(A.arow, A.aval, x.off[1], x.off[1] + x.len[1]);
-          }
-        } else {
-          const int lg = x.len[1] > x.len[0] ? 1 : 0;
-          const i64 b = x.off[lg] + static_cast<i64>(x.p) * A.chunk;
-          prefetch_range<kWrite>(A.arow, A.aval, b, min(b + A.chunk, x.off[lg] + x.len[lg]));
-        }
-      }
       if (!kWrite && np == 1) continue;  // counted by its own write pass
       const double q[2][2] = {{r.q[0][0], r.q[0][1]}, {r.q[1][0], r.q[1][1]}};
       i64 beg[2], end[2];
@@ -1029,11 +964,6 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int
         end[0] = lg ? hi_o : hi_l;
         beg[1] = lg ? lo_l : lo_o;
         end[1] = lg ? hi_l : hi_o;
-        if (merge_prefetch) prefetch_range<kWrite>(A.arow, A.aval, lo_o, hi_o);
-      }
-      if (merge_prefetch && j == 0) {  // a batch's first item had no predecessor
-        prefetch_range<kWrite>(A.arow, A.aval, beg[0], end[0]);
-        prefetch_range<kWrite>(A.arow, A.aval, beg[1], end[1]);
       }
       int r0 = 0;
       const int dl = identical_rows<2>(A, beg, end, r0);
@@ -1062,8 +992,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int
         u = dl;
       } else if (np == 1) {
         // single partition: count the union, allocate 2u, write
-        u = use_ring ? merge_count2_ring(A.arow, beg[0], beg[1], end[0], end[1], ring_r[wib])
-                     : merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
+        u = merge_count2_ring(A.arow, beg[0], beg[1], end[0], end[1], ring_r[wib]);
         unsigned long long b0 = 0;
         if (lane == 0) b0 = atomicAdd(A.cursor, 2ull * static_cast<unsigned long long>(u));
         b0 = __shfl_sync(0xffffffffu, b0, 0);
@@ -1072,12 +1001,7 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int
           continue;
         }
         const i64 d0 = static_cast<i64>(b0), d1 = d0 + u;
-        if constexpr (kWrite) {
-          if (use_ring)
-            merge_write2_ring(A, q, beg[0], beg[1], end[0], end[1], d0, d1, ring_r[wib], ring_v[wib]);
-          else
-            merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], d0, d1);
-        }
+        if constexpr (kWrite) merge_write2_ring(A, q, beg[0], beg[1], end[0], end[1], d0, d1, ring_r[wib], ring_v[wib]);
         if (lane == 0) {
           A.rbase[2 * ri] = d0;
           A.rbase[2 * ri + 1] = d1;
@@ -1087,16 +1011,25 @@ __global__ void __launch_bounds__(kThreads, kOcc) k_merge2(PassArgs A, const int
         produced += 2ull * static_cast<unsigned long long>(u);
         continue;
       } else if constexpr (kWrite) {
-        u = use_ring ? merge_write2_ring(A, q, beg[0], beg[1], end[0], end[1], r.dst[0], r.dst[1], ring_r[wib],
-                                         ring_v[wib])
-                     : merge_write2_pf(A, q, beg[0], beg[1], end[0], end[1], r.dst[0], r.dst[1]);
+        u = merge_write2_ring(A, q, beg[0], beg[1], end[0], end[1], r.dst[0], r.dst[1], ring_r[wib], ring_v[wib]);
       } else {
-        u = use_ring ? merge_count2_ring(A.arow, beg[0], beg[1], end[0], end[1], ring_r[wib])
-                     : merge_count2_pf(A.arow, beg[0], beg[1], end[0], end[1]);
+        u = merge_count2_ring(A.arow, beg[0], beg[1], end[0], end[1], ring_r[wib]);
       }
-      if (!kWrite && lane == 0) {
-        A.cnt[r.dst[0] + p] = u;
-        A.cnt[r.dst[0] + np + p] = u;
+      if constexpr (!kWrite) {
+        int fin = 0;
+        if (lane == 0) {
+          A.cnt[r.dst[0] + p] = u;
+          if (!A.ndone) A.cnt[r.dst[0] + np + p] = u;
+          if (A.ndone) {
+            __threadfence();
+            fin = atomicAdd(A.ndone + ri, 1) + 1;
+          }
+        }
+        // the warp that counted the rotation's last partition allocates it
+        if (__shfl_sync(0xffffffffu, fin, 0) == np) {
+          __threadfence();
+          if (*reinterpret_cast<volatile const int32_t*>(A.ovf) == INT_MAX) rot_alloc_warp2(A, ri, r.dst[0] >> 1, np);
+        }
       }
     }
     __syncwarp();
@@ -1772,7 +1705,7 @@ struct LevelScratch {
   DBuf<int64_t> np, ioff, nitems, cnt, pos;
   DBuf<int32_t> item_rot;
   DBuf<i64> rbase;
-  DBuf<int32_t> rlen, ovf;
+  DBuf<int32_t> rlen, ovf, ndone;
   DBuf<unsigned long long> cursor, in_entries;
   DBuf<unsigned char> scan_tmp;
   size_t scan_bytes = 0;
@@ -1792,37 +1725,14 @@ inline bool merge2_enabled() {
   }();
   return on;
 }
-inline bool merge_ring_enabled() {
+// k = 2: a rotation's arena allocation runs inside the count pass
+// (PMMF_B200_FUSED_ALLOC=0: separate k_rot_alloc launch per level).
+inline bool fused_alloc_enabled() {
   static const bool on = [] {
-    const char* e = std::getenv("PMMF_B200_MERGE_RING");
+    const char* e = std::getenv("PMMF_B200_FUSED_ALLOC");
     return !(e && e[0] == '0');
   }();
   return on;
-}
-inline bool merge_prefetch_enabled() {  // measured: no gain with the ring (write pass 113.7 vs 106.7 ms)
-  static const bool on = [] {
-    const char* e = std::getenv("PMMF_B200_MERGE_PF");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-// Resident blocks per SM the k = 2 merge kernel is compiled for
-// (PMMF_B200_MERGE2_OCC = 4 | 5 | 6: registers per thread 64 | 48 | 40).
-inline int merge2_occ() {
-  static const int v = [] {
-    const char* e = std::getenv("PMMF_B200_MERGE2_OCC");
-    const int o = e ? std::atoi(e) : 4;
-    return o == 5 || o == 6 ? o : 4;
-  }();
-  return v;
-}
-template <bool kWrite>
-void launch_merge2(const PassArgs& A, int blocks, const int64_t* nitems, const int32_t* ovf, cudaStream_t s) {
-  switch (merge2_occ()) {
-    case 6: PMMF_LAUNCH((k_merge2<kWrite, 6>), blocks, kThreads, 0, s, A, nitems, ovf); break;
-    case 5: PMMF_LAUNCH((k_merge2<kWrite, 5>), blocks, kThreads, 0, s, A, nitems, ovf); break;
-    default: PMMF_LAUNCH((k_merge2<kWrite, 4>), blocks, kThreads, 0, s, A, nitems, ovf); break;
-  }
 }
 template <int K, bool kWrite>
 int persistent_blocks() {
@@ -1831,9 +1741,7 @@ int persistent_blocks() {
     cudaError_t e = cudaSuccess;
     if constexpr (K == 2) {
       if (merge2_enabled())
-        e = merge2_occ() == 6   ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite, 6>, kThreads, 0)
-            : merge2_occ() == 5 ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite, 5>, kThreads, 0)
-                                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite, 4>, kThreads, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite>, kThreads, 0);
       else
         e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0);
     } else {
@@ -1935,8 +1843,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.level = level;
   A.rbase = S.rbase.get();
   A.rlen = S.rlen.get();
-  A.prefetch = merge_prefetch_enabled();
-  A.ring = merge_ring_enabled();
+  A.ndone = (K == 2 && merge2_enabled() && fused_alloc_enabled()) ? S.ndone.get() : nullptr;
   if (nrot <= kSetupMax && !std::getenv("PMMF_B200_NO_LEVEL_SETUP")) {
     PMMF_LAUNCH(k_level_setup<K>, 1, kSetupThreads, 0, s, A, S.np.get(), S.ioff.get(), S.nitems.get(),
                 S.item_rot.get(), S.in_entries.get(), pending, S.rbase.get(), S.rlen.get(), B.off.get(),
@@ -1960,15 +1867,16 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     cudaEventRecord(c0, s);
   }
   if (K == 2 && merge2_enabled())
-    launch_merge2<false>(A, persistent_blocks<K, false>(), S.nitems.get(), S.ovf.get(), s);
+    PMMF_LAUNCH(k_merge2<false>, (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   else
     PMMF_LAUNCH((k_merge_p<K, false>), (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (c0) {
     cudaEventRecord(c1, s);
     S.cev.push_back({c0, c1});
   }
-  PMMF_LAUNCH(k_rot_alloc<K>, blocks_for(nrot * 32, kThreads), kThreads, 0, s, A, S.nitems.get(), S.cursor.get(), B.cap,
-              S.ovf.get(), level, S.pos.get(), S.rbase.get(), S.rlen.get());
+  if (!A.ndone)  // else allocated inside the count pass (rot_alloc_warp)
+    PMMF_LAUNCH(k_rot_alloc<K>, blocks_for(nrot * 32, kThreads), kThreads, 0, s, A, S.nitems.get(), S.cursor.get(), B.cap,
+                S.ovf.get(), level, S.pos.get(), S.rbase.get(), S.rlen.get());
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (prof_enabled()) {
     e0 = EventPool::get().take();
@@ -1976,7 +1884,7 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     cudaEventRecord(e0, s);
   }
   if (K == 2 && merge2_enabled())
-    launch_merge2<true>(A, persistent_blocks<K, true>(), S.nitems.get(), S.ovf.get(), s);
+    PMMF_LAUNCH(k_merge2<true>, (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   else
     PMMF_LAUNCH((k_merge_p<K, true>), (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   if (e0) {
@@ -2197,6 +2105,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     S.nitems.alloc(1, s);
     S.rbase.alloc(K * max_rot, s);
     S.rlen.alloc(K * max_rot, s);
+    S.ndone.alloc(max_rot, s);
     S.ovf.alloc(1, s);
     S.cursor.alloc(1, s);
     S.in_entries.alloc(2, s);

@@ -300,6 +300,17 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   }
   R->trivial = static_cast<i64>(active.size()) <= p.core_min;
 
+  // one side stream for the rotation-record copies of every stage, one
+  // retired-id scratch mask (both were per stage: ~1 ms of fixed host cost each)
+  struct SideStream {
+    cudaStream_t st = nullptr;
+    ~SideStream() {
+      if (st) cudaStreamDestroy(st);
+    }
+  } side_holder;
+  PMMF_CUDA(cudaStreamCreateWithFlags(&side_holder.st, cudaStreamNonBlocking));
+  const cudaStream_t side = side_holder.st;
+  std::vector<uint8_t> gone(static_cast<size_t>(std::max<i64>(n, 1)), 0);
   for (int stage_no = 1; stage_no <= p.n_stages && !R->trivial; ++stage_no) {
     if (static_cast<i64>(active.size()) <= p.core_min) break;
     const auto t_stage = clk::now();
@@ -561,10 +572,8 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       const int32_t* d_loc = so.rot_loc.get();
       const double* d_q = so.rot_q.get();
       const int k = p.k;
-      records = std::async(std::launch::async, [&st, &nrot, &out_base, &cur, rc, slots, k, d_loc, d_q, ready, dev]() {
+      records = std::async(std::launch::async, [&st, &nrot, &out_base, &cur, rc, slots, k, d_loc, d_q, ready, dev, side]() {
         PMMF_CUDA(cudaSetDevice(dev));
-        cudaStream_t side = nullptr;
-        PMMF_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         PMMF_CUDA(cudaStreamWaitEvent(side, ready, 0));
         const size_t nl = static_cast<size_t>(std::max<i64>(slots * k, 1));
         const size_t nq = static_cast<size_t>(std::max<i64>(slots * k * k, 1));
@@ -584,7 +593,6 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
         PMMF_CUDA(cudaMemcpyAsync(hl, d_loc, nl * sizeof(int32_t), cudaMemcpyDeviceToHost, side));
         PMMF_CUDA(cudaMemcpyAsync(hq, d_q, nq * sizeof(double), cudaMemcpyDeviceToHost, side));
         PMMF_CUDA(cudaStreamSynchronize(side));
-        cudaStreamDestroy(side);
         cudaEventDestroy(ready);
         i64 total = 0;
         for (i64 u = 0; u < rc; ++u) total += nrot[u];
@@ -770,13 +778,13 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       }
     }
     {
-      std::vector<uint8_t> gone(static_cast<size_t>(n), 0);
       for (int32_t g : order_g) gone[g] = 1;
       std::vector<i64> next;
       next.reserve(active.size() - order_g.size());
       for (i64 g : active)
         if (!gone[g]) next.push_back(g);
       active = std::move(next);
+      for (int32_t g : order_g) gone[g] = 0;
     }
     records.get();  // rotation records assembled (rethrows a copy failure)
     PMMF_TRACE("[pmmf] stage %d: residual + bookkeeping %.2f ms\n", stage_no, ms_since(t_res));

@@ -98,6 +98,81 @@ __global__ void k_gram_owner(i64 col0, i64 ncols, i64 e0, const i64* __restrict_
   }
 }
 
+// Software-pipelined k_gram_owner (same sums in the same order).  The plain
+// kernel pays three dependent global round trips per row of the owner column
+// (run bounds -> run entries -> accumulator), ~31 rows in a row on config 4.
+// Here a warp loads the (value, run) records of 32 rows at once, and while row
+// t is accumulated the run entries of row t+2 are being loaded and the
+// accumulator sectors of row t+1 are being prefetched (kPf = 1: into L1,
+// 2: into L2), so a row costs one cache-hit read-modify-write.
+template <int kPf>
+__global__ void k_gram_owner_pipe(i64 col0, i64 ncols, i64 e0, const i64* __restrict__ ptr,
+                                  const double* __restrict__ val, const int32_t* __restrict__ run_lo,
+                                  const int32_t* __restrict__ run_hi, const int32_t* __restrict__ csr_col,
+                                  const double* __restrict__ csr_val, const int32_t* __restrict__ col_cluster_off,
+                                  const int64_t* __restrict__ col_tile, const int32_t* __restrict__ col_c,
+                                  double* __restrict__ G) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= ncols) return;
+  const i64 J = col0 + w;
+  const int32_t cbase = col_cluster_off[w];
+  const i64 a = J - cbase;
+  const i64 c = col_c[w];
+  double* Gcol = G + col_tile[w] + a * c;
+  const i64 end = ptr[J + 1];
+  for (i64 base = ptr[J]; base < end; base += 32) {
+    const int n = static_cast<int>(end - base < 32 ? end - base : 32);
+    double va_l = 0.0;
+    int32_t lo_l = 0, hi_l = 0;
+    if (lane < n) {
+      va_l = val[base + lane];
+      lo_l = run_lo[base + lane - e0];
+      hi_l = run_hi[base + lane - e0];
+    }
+    // stage A: the first 32 run entries of row x (b < 0: none for this lane)
+    auto load_run = [&](int x, int32_t& b, double& pv, int32_t& lo, int32_t& hi) {
+      lo = __shfl_sync(0xffffffffu, lo_l, x & 31);
+      hi = __shfl_sync(0xffffffffu, hi_l, x & 31);
+      b = -1;
+      pv = 0.0;
+      if (x < n && lo + lane < hi) {
+        b = csr_col[lo + lane] - cbase;
+        pv = csr_val[lo + lane];
+      }
+    };
+    auto prefetch = [&](int32_t b) {
+      if (kPf == 1 && b >= 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(Gcol + b));
+      if (kPf == 2 && b >= 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(Gcol + b));
+    };
+    int32_t b0, b1, b2 = -1, lo0, hi0, lo1, hi1, lo2 = 0, hi2 = 0;
+    double pv0, pv1, pv2 = 0.0;
+    load_run(0, b0, pv0, lo0, hi0);
+    load_run(1, b1, pv1, lo1, hi1);
+    prefetch(b0);
+    for (int t = 0; t < n; ++t) {
+      if (t + 2 < n) load_run(t + 2, b2, pv2, lo2, hi2);
+      prefetch(b1);
+      const double va = __shfl_sync(0xffffffffu, va_l, t);
+      if (b0 >= 0) Gcol[b0] = dadd(Gcol[b0], dmul(va, pv0));
+      for (int32_t q = lo0 + 32 + lane; q < hi0; q += 32) {  // rows shared by more than 32 columns
+        const int32_t b = csr_col[q] - cbase;
+        Gcol[b] = dadd(Gcol[b], dmul(va, csr_val[q]));
+      }
+      __syncwarp();
+      b0 = b1;
+      pv0 = pv1;
+      lo0 = lo1;
+      hi0 = hi1;
+      b1 = b2;
+      pv1 = pv2;
+      lo1 = lo2;
+      hi1 = hi2;
+      b2 = -1;
+    }
+  }
+}
+
 __global__ void k_run_total(i64 ne, const int32_t* __restrict__ lo, const int32_t* __restrict__ hi,
                             unsigned long long* __restrict__ tot) {
   const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
@@ -462,8 +537,22 @@ void gram_sparse(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 
   }();
   if (owner_smem > 48 * 1024)
     PMMF_CUDA(cudaFuncSetAttribute(k_gram_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, owner_smem));
-  PMMF_LAUNCH(k_gram_owner, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, col0, ncols, e0, a.ptr.get(),
-              a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco, dct, dcc, G);
+  // PMMF_B200_GRAM_PIPE: 0 = plain kernel, 1 / 2 = pipelined with L1 / L2 accumulator prefetch, 3 = pipelined, none
+  static const int pipe = [] {
+    const char* e = std::getenv("PMMF_B200_GRAM_PIPE");
+    return e ? std::atoi(e) : 3;  // measured, config 4 gram phase: 0: 150, 1: 143.8, 2: 146.1, 3: 142.9 ms
+  }();
+#define PMMF_OWNER_ARGS                                                                                              \
+  col0, ncols, e0, a.ptr.get(), a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco, dct, dcc, G
+  if (pipe == 1)
+    PMMF_LAUNCH(k_gram_owner_pipe<1>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
+  else if (pipe == 2)
+    PMMF_LAUNCH(k_gram_owner_pipe<2>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
+  else if (pipe == 3)
+    PMMF_LAUNCH(k_gram_owner_pipe<0>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
+  else
+    PMMF_LAUNCH(k_gram_owner, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
+#undef PMMF_OWNER_ARGS
   if (trace_enabled()) {  // products = sum over entries of their row-run length (the reference's count)
     DBuf<unsigned long long> tot(1, s);
     tot.zero();
