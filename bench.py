@@ -76,7 +76,9 @@ def merge_traffic():
     """DRAM bytes (read + write) per launch of the write pass, from the ncu
     dram__bytes pass over every such launch of one factorization
     (profiles/merge_traffic_r01e.json, scripts/gpu_evidence_r01e.sh)."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r02.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r03.json")
+    if not os.path.exists(path):
+        path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r02.json")
     if not os.path.exists(path):
         path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "merge_traffic_r01e.json")
     try:
@@ -85,6 +87,28 @@ def merge_traffic():
         return d["dram_bytes_per_launch"]
     except (OSError, KeyError, ValueError):
         return None
+
+
+def reference_full_size(wl):
+    """The reference's own full-size run of this config, RECORDED (not timed
+    here: 753 s and 183 GB of host RAM on config 4): GPU vs compiled reference
+    on the GPU box's 16 host cores, bitwise identical
+    (scripts/gpu_parity_fullsize_r03.sh -> profiles/parity_fullsize_r03.jsonl)."""
+    want = {"c4": "rmat:20", "c5": "grid:1024"}.get(wl)
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "parity_fullsize_r03.jsonl")
+    if want is None or not os.path.exists(path):
+        return None
+    try:
+        for ln in open(path):
+            d = json.loads(ln)
+            if d.get("workload") == want:
+                return {"recorded": True, "source": "profiles/parity_fullsize_r03.jsonl", "workload": want,
+                        "n": d["n"], "nnz": d["nnz"], "threads": d["threads"], "reference_s": d["ref_s"],
+                        "reference_value": d["ref_rot_per_s"], "unit": UNIT, "peak_rss_gb": d["peak_rss_gb"],
+                        "gpu_e2e_s_cold_first_call": d["gpu_s"], "bitwise_identical": d["bitwise_identical"]}
+    except (OSError, ValueError, KeyError):
+        return None
+    return None
 
 
 def config_params(wl="c4"):
@@ -621,7 +645,7 @@ def main():
     if "rotate_write" in prof:
         c, ms, by = prof["rotate_write"]
         achieved = (by / 1e9) / (ms / 1e3) if ms > 0 else 0.0
-        roof = {"bound": "hbm", "kernel": "k_merge_p<2,true> (rotation stream, write pass)", "achieved": achieved,
+        roof = {"bound": "hbm", "kernel": "k_merge2<true> (k = 2 rotation stream, write pass)", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": merge_traffic() if args.workload == "c4" else None,
                 "launches": c, "kernel_ms_total": ms, "algorithmic_bytes_total": by, "peak_source": peak_src,
@@ -682,7 +706,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": DATA,
                 "config": config_dict(args, W, n, len(vals), params, world), "rotations_per_step": int(rots),
-                "roofline": roof, "cpu_baseline": cpu, "like_for_like": like, "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roof, "cpu_baseline": cpu, "like_for_like": like,
+                "reference_full_size": reference_full_size(args.workload), "e2e": e2e, "gpu_launches": int(launches),
                 "mmf_apply": apply, "cg": cg,
                 "clocks": clk, "step_ms": step_ms,
                 "phases_ms_steps": step_phases,  # [clustering, gram, search, apply, reblock, total] per timed step

@@ -397,6 +397,9 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
   using BlockScan = cub::BlockScan<int64_t, kSetupThreads>;
   __shared__ typename BlockScan::TempStorage scan;
   __shared__ int64_t s_run;
+  __shared__ int s_nq;
+  __shared__ int64_t q_start[kSetupThreads];
+  __shared__ int32_t q_len[kSetupThreads], q_rot[kSetupThreads];
   // the previous level's commit (k_commit_level), deferred into this launch:
   // its outputs' (off, len) must be in place before this level reads len
   if (P.nrot > 0 && *reinterpret_cast<volatile const int32_t*>(P.ovf) == INT_MAX)
@@ -411,7 +414,10 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
     }
   __syncthreads();
   const i64 nrot = A.nrot;
-  if (threadIdx.x == 0) s_run = 0;
+  if (threadIdx.x == 0) {
+    s_run = 0;
+    s_nq = 0;
+  }
   unsigned long long ins = 0;
   __syncthreads();
   for (i64 base = 0; base < nrot; base += kSetupThreads) {
@@ -435,10 +441,27 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
     const int64_t run = s_run;
     if (i < nrot) {
       ioff[i] = run + ex;
-      for (int64_t q = 0; q < v; ++q) item_rot[run + ex + q] = static_cast<int32_t>(i);
+      if (v <= 8) {
+        for (int64_t q = 0; q < v; ++q) item_rot[run + ex + q] = static_cast<int32_t>(i);
+      } else {  // a hub rotation has ~2,000 partitions: filled by a warp below
+        const int e = atomicAdd(&s_nq, 1);
+        q_start[e] = run + ex;
+        q_len[e] = static_cast<int32_t>(v);
+        q_rot[e] = static_cast<int32_t>(i);
+      }
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_run = run + tot;
+    const int nq = s_nq;
+    for (int e = threadIdx.x >> 5; e < nq; e += kSetupThreads / 32) {
+      const int64_t b = q_start[e];
+      const int32_t r = q_rot[e];
+      for (int q = threadIdx.x & 31; q < q_len[e]; q += 32) item_rot[b + q] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_run = run + tot;
+      s_nq = 0;
+    }
     __syncthreads();
   }
   for (int o = 16; o; o >>= 1) ins += __shfl_xor_sync(0xffffffffu, ins, o);
@@ -1447,6 +1470,7 @@ __global__ void k_final_count(i64 S, i64 col0, const int32_t* __restrict__ seg_c
     return;
   }
   int c = 0;
+#pragma unroll 4
   for (int i = b + lane; i < e; i += 32) c += keep_row[arow[off[w] + i]];
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) cnt[q] = c;
@@ -1465,23 +1489,31 @@ __global__ void k_final_copy(i64 S, i64 col0, const int32_t* __restrict__ seg_co
   const bool all = keep_row == nullptr || (keep_all_col != nullptr && keep_all_col[col0 + w]);
   i64 o = pos[q];
   const i64 s = off[w];
-  for (int base = b; base < e; base += 32) {
-    const int i = base + lane;
-    int r = 0;
-    double v = 0.0;
-    bool k = false;
-    if (i < e) {
-      r = arow[s + i];
-      v = aval[s + i];
-      k = all || keep_row[r];
+  for (int base = b; base < e; base += 128) {  // four windows per round, loads of all four in flight
+    int r[4];
+    bool k[4];
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = base + 32 * j + lane;
+      r[j] = i < e ? arow[s + i] : -1;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, k);
-    if (k) {
-      const i64 d = o + __popc(m & ((1u << lane) - 1u));
-      orow[d] = r;
-      oval[d] = v;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      k[j] = r[j] >= 0 && (all || keep_row[r[j]]);
+      // dropped rows (most of a row pass's entries): value never read
+      v[j] = k[j] ? aval[s + base + 32 * j + lane] : 0.0;
     }
-    o += __popc(m);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, k[j]);
+      if (k[j]) {
+        const i64 d = o + __popc(m & ((1u << lane) - 1u));
+        orow[d] = r[j];
+        oval[d] = v[j];
+      }
+      o += __popc(m);
+    }
   }
 }
 // Column pointers of a piece from its segment offsets.
@@ -1587,6 +1619,7 @@ __global__ void k_final_mass_count(i64 S, i64 col0, const int32_t* __restrict__ 
   const int32_t key = M.col_key[c];
   const i64 s0 = off[w];
   int n = 0, kc = 0;
+#pragma unroll 4
   for (int i = b + lane; i < e; i += 32) {
     const int32_t g = arow[s0 + i];
     if (!all) kc += keep_row[g];
@@ -1623,23 +1656,34 @@ __global__ void k_mass_gather(i64 q0, i64 q1, i64 col0, const int32_t* __restric
   const int32_t key = M.col_key[c];
   const i64 s0 = off[w];
   i64 o = pos[q] - pos[q0];
-  for (int base = b; base < e; base += 32) {
-    const int i = base + lane;
-    int32_t rg = -1;
-    bool take = false;
-    if (i < e) {
-      const int32_t g = arow[s0 + i];
-      rg = M.row_rank[g];
-      take = rg >= 0 && g != c && key > rg;
+  // four windows per round: rows, rank gathers and values of all four are in
+  // flight together (the chain row -> rank -> value was ~3 round trips per window)
+  for (int base = b; base < e; base += 128) {
+    int32_t g[4], rg[4];
+    bool take[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = base + 32 * j + lane;
+      g[j] = i < e ? arow[s0 + i] : -1;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (take) {
-      const i64 d = o + __popc(m & ((1u << lane) - 1u));
-      const double v = aval[s0 + i];
-      okey[d] = static_cast<int32_t>(rg - M.rank_base);
-      osq[d] = dmul(v, v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) rg[j] = g[j] >= 0 ? M.row_rank[g[j]] : -1;
+    double v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      take[j] = rg[j] >= 0 && g[j] != c && key > rg[j];
+      v[j] = take[j] ? aval[s0 + base + 32 * j + lane] : 0.0;
     }
-    o += __popc(m);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, take[j]);
+      if (take[j]) {
+        const i64 d = o + __popc(m & ((1u << lane) - 1u));
+        okey[d] = static_cast<int32_t>(rg[j] - M.rank_base);
+        osq[d] = dmul(v[j], v[j]);
+      }
+      o += __popc(m);
+    }
   }
 }
 // The chunk is stably sorted by bucket = rank >> shift (so column order is
@@ -1647,8 +1691,18 @@ __global__ void k_mass_gather(i64 q0, i64 q1, i64 col0, const int32_t* __restric
 // its (1 << shift) ranks in shared memory.  Inside a 32-entry window, equal
 // ranks (one per column) are added in lane = column order, one member per
 // round (factorizer.hpp:529-542 sequential order).
-__global__ void k_mass_buckets(i64 n, i64 nbuckets, int shift, const int32_t* __restrict__ key,
-                               const double* __restrict__ sq, MassSpec M) {
+// start[b] = first sorted position of bucket b (start[nbuckets] = n): one
+// streaming pass instead of two 30-step binary searches per bucket warp.
+__global__ void k_bucket_bounds(i64 n, i64 nbuckets, int shift, const int32_t* __restrict__ key,
+                                i64* __restrict__ start) {
+  const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+  if (i > n) return;
+  const i64 prev = i == 0 ? -1 : static_cast<i64>(key[i - 1]) >> shift;
+  const i64 cur = i == n ? nbuckets : static_cast<i64>(key[i]) >> shift;
+  for (i64 b = prev + 1; b <= cur; ++b) start[b] = i;
+}
+__global__ void k_mass_buckets(i64 nbuckets, int shift, const int32_t* __restrict__ key,
+                               const double* __restrict__ sq, const i64* __restrict__ start, MassSpec M) {
   extern __shared__ double slots[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const i64 bkt = blockIdx.x * static_cast<i64>(blockDim.x >> 5) + wib;
@@ -1656,25 +1710,22 @@ __global__ void k_mass_buckets(i64 n, i64 nbuckets, int shift, const int32_t* __
   const int width = 1 << shift;
   double* m = slots + static_cast<i64>(wib) * width;
   const i64 r0 = bkt << shift;
-  // bounds of the bucket in the sorted keys
-  auto lb = [&](i64 v) {
-    i64 lo = 0, hi = n;
-    while (lo < hi) {
-      const i64 mid = (lo + hi) >> 1;
-      if ((static_cast<i64>(key[mid]) >> shift) < v) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-  };
-  const i64 b = lb(bkt), e = lb(bkt + 1);
+  const i64 b = start[bkt], e = start[bkt + 1];
   if (b == e) return;
   double* mass = M.mass + M.rank_base;
   for (int i = lane; i < width; i += 32) m[i] = r0 + i < M.n_retired ? mass[r0 + i] : 0.0;
   __syncwarp();
+  int32_t nr = b + lane < e ? key[b + lane] : 0;  // windows loaded one ahead
+  double nv = b + lane < e ? sq[b + lane] : 0.0;
   for (i64 x = b; x < e; x += 32) {
     const i64 i = x + lane;
     const bool on = i < e;
-    const int32_t r = on ? key[i] : -1 - lane;  // distinct dummies
-    const double v = on ? sq[i] : 0.0;
+    const int32_t r = on ? nr : -1 - lane;  // distinct dummies
+    const double v = on ? nv : 0.0;
+    if (i + 32 < e) {
+      nr = key[i + 32];
+      nv = sq[i + 32];
+    }
     const unsigned grp = __match_any_sync(0xffffffffu, r);
     const int rk = __popc(grp & ((1u << lane) - 1u));
     const int rounds = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(__popc(grp)));
@@ -1997,6 +2048,7 @@ void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, const DBuf<i
   DBuf<int32_t> k1, k2;
   DBuf<double> v1, v2;
   DBuf<unsigned char> tmp;
+  DBuf<i64> bstart(nbuckets + 1, s);
   i64 have = 0;
   auto ensure = [&](i64 n) {
     if (n <= have) return;
@@ -2032,8 +2084,10 @@ void batch_masses(const Batch& B, const Segs& G, const MassSpec& M, const DBuf<i
       size_t t = static_cast<size_t>(tmp.n);
       PMMF_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), t, kd, vd, static_cast<int64_t>(n), shift, shift + kbits, s));
       lap(2);
-      PMMF_LAUNCH(k_mass_buckets, blocks_for(nbuckets * 32, 32 * kWarpsPerBlock), 32 * kWarpsPerBlock, smem, s, n,
-                  nbuckets, shift, kd.Current(), vd.Current(), M);
+      PMMF_LAUNCH(k_bucket_bounds, blocks_for(n + 1, kThreads), kThreads, 0, s, n, nbuckets, shift, kd.Current(),
+                  bstart.get());
+      PMMF_LAUNCH(k_mass_buckets, blocks_for(nbuckets * 32, 32 * kWarpsPerBlock), 32 * kWarpsPerBlock, smem, s,
+                  nbuckets, shift, kd.Current(), vd.Current(), bstart.get(), M);
       lap(3);
     }
     w0 = w1;

@@ -186,6 +186,7 @@ __global__ void k_reblock_count(i64 Nn, const int32_t* __restrict__ new2old, con
   }
   const int32_t j = new2old[warp];
   int c = 0;
+#pragma unroll 4
   for (i64 e = ptr[j] + lane; e < ptr[j + 1]; e += 32) c += map[row[e]] >= 0;
   for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
   if (lane == 0) cnt[warp] = c;
@@ -200,21 +201,30 @@ __global__ void k_reblock_fill(i64 Nn, const int32_t* __restrict__ new2old, cons
   if (warp >= Nn) return;
   const int32_t j = new2old[warp];
   i64 out = nptr[warp];
-  for (i64 base = ptr[j]; base < ptr[j + 1]; base += 32) {
-    const i64 e = base + lane;
-    int32_t nr = -1;
-    double v = 0.0;
-    if (e < ptr[j + 1]) {
-      nr = map[row[e]];
-      v = val[e];
+  const i64 e1 = ptr[j + 1];
+  // four windows per round: the rows, the relabel gathers and the values of all
+  // four are in flight together (a hub column is one warp's sequential loop)
+  for (i64 base = ptr[j]; base < e1; base += 128) {
+    int32_t r[4], nr[4];
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const i64 e = base + 32 * q + lane;
+      r[q] = e < e1 ? row[e] : -1;
+      v[q] = e < e1 ? val[e] : 0.0;
     }
-    const unsigned keep = __ballot_sync(0xffffffffu, nr >= 0);
-    if (nr >= 0) {
-      const int p = __popc(keep & ((1u << lane) - 1));
-      nrow[out + p] = nr;
-      nval[out + p] = v;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) nr[q] = r[q] >= 0 ? map[r[q]] : -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned keep = __ballot_sync(0xffffffffu, nr[q] >= 0);
+      if (nr[q] >= 0) {
+        const int p = __popc(keep & ((1u << lane) - 1));
+        nrow[out + p] = nr[q];
+        nval[out + p] = v[q];
+      }
+      out += __popc(keep);
     }
-    out += __popc(keep);
   }
 }
 
@@ -262,21 +272,30 @@ __global__ void k_chunk_gather(i64 N, i64 c0, const i64* __restrict__ ptr, const
   const i64 lo = lb_rows(row, ptr[w], ptr[w + 1], r0), hi = lb_rows(row, lo, ptr[w + 1], r1);
   i64 o = pos[c0 + w];
   const uint64_t col = static_cast<uint64_t>(c0 + w);
-  for (i64 b = lo; b < hi; b += 32) {
-    const i64 e = b + lane;
-    int32_t r = 0;
-    bool k = false;
-    if (e < hi) {
-      r = row[e];
-      k = keep_row == nullptr || keep_row[r];
+  for (i64 b = lo; b < hi; b += 128) {  // four windows per round, loads of all four in flight
+    int32_t r[4];
+    bool k[4];
+    double v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const i64 e = b + 32 * q + lane;
+      r[q] = e < hi ? row[e] : -1;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, k);
-    if (k) {
-      const i64 d = o + __popc(m & ((1u << lane) - 1u));
-      keys[d] = (static_cast<uint64_t>(r - r0) << cb) | col;
-      vals[d] = val[e];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      k[q] = r[q] >= 0 && (keep_row == nullptr || keep_row[r[q]]);
+      v[q] = k[q] ? val[b + 32 * q + lane] : 0.0;
     }
-    o += __popc(m);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned m = __ballot_sync(0xffffffffu, k[q]);
+      if (k[q]) {
+        const i64 d = o + __popc(m & ((1u << lane) - 1u));
+        keys[d] = (static_cast<uint64_t>(r[q] - r0) << cb) | col;
+        vals[d] = v[q];
+      }
+      o += __popc(m);
+    }
   }
 }
 __global__ void k_chunk_emit(i64 m, const uint64_t* __restrict__ keys, const double* __restrict__ vals, int cb,

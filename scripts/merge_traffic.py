@@ -8,6 +8,8 @@ UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1
 
 
 def is_write(name):
+    if "k_merge2" in name:
+        return any(t in name for t in ("k_merge2<1", "k_merge2<(bool)1", "k_merge2<true"))
     return "k_merge_p" in name and any(t in name for t in ("(bool)1", ", 1>", ", true>"))
 
 
@@ -26,10 +28,10 @@ def main(path, out):
     w = [per[i] for i in per if is_write(names[i])]
     tot = sum(d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0) for d in w)
     ms = sum(d.get("gpu__time_duration.sum", 0) for d in w)
-    res = {"kernel": "k_merge_p<2,true> (rotation stream, write pass)", "launches": len(w),
+    res = {"kernel": "k_merge2<true> (k = 2 rotation stream, write pass)", "launches": len(w),
            "dram_bytes_total": tot, "dram_bytes_per_launch": tot / max(len(w), 1), "kernel_ms_total_ncu": ms,
            "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                     f"--clock-control none over every k_merge_p launch of one config-4 factorization ({path})"}
+                     f"--clock-control none over every write-pass launch of one config-4 factorization ({path})"}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res))
 
