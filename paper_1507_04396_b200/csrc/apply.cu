@@ -1619,16 +1619,26 @@ __global__ void k_final_mass_count(i64 S, i64 col0, const int32_t* __restrict__ 
   const int32_t key = M.col_key[c];
   const i64 s0 = off[w];
   int n = 0, kc = 0;
-#pragma unroll 4
-  for (int i = b + lane; i < e; i += 32) {
-    const int32_t g = arow[s0 + i];
-    if (!all) kc += keep_row[g];
-    const int32_t rg = M.row_rank[g];
-    if (rg < 0) continue;
-    if (g == c)
-      M.diag[rg] = aval[s0 + i];
-    else
-      n += key > rg;
+  for (int base = b; base < e; base += 128) {  // four windows per round: rows, then both table gathers
+    int32_t g[4], rg[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = base + 32 * j + lane;
+      g[j] = i < e ? arow[s0 + i] : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      rg[j] = g[j] >= 0 ? M.row_rank[g[j]] : -1;
+      if (!all && g[j] >= 0) kc += keep_row[g[j]];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (rg[j] < 0) continue;
+      if (g[j] == c)
+        M.diag[rg[j]] = aval[s0 + base + 32 * j + lane];
+      else
+        n += key > rg[j];
+    }
   }
   for (int o = 16; o; o >>= 1) {
     n += __shfl_xor_sync(0xffffffffu, n, o);

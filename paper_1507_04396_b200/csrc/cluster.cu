@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <memory>
 #include <numeric>
+#include <type_traits>
 #include <unordered_map>
 
 #include "engine.cuh"
@@ -187,8 +188,17 @@ constexpr int kPrefetch = 8;  // anchor entries of a hit row staged in shared me
 // then the prefetch buffers (16-byte aligned).
 // ... plus the list of anchors the current column touched (m int32) and its
 // length, so a column's epilogue costs its touched anchors, not m.
-__host__ __device__ constexpr size_t score_pf_off(int m) { return (static_cast<size_t>(m) * 24 + 4 + 15) / 16 * 16; }
-__host__ __device__ constexpr size_t score_stride(int m) { return score_pf_off(m) + 32 * kPrefetch * 12 + 32; }
+// Narrow layout (anchors and pre-reblock blocks < 32768, every BASELINE
+// config): 16-bit last-block, touched-list and staged anchor indices, 12.5 KB
+// instead of 15.0 KB per warp at m = 512 -> 17 instead of 14 resident warps per
+// SM for a kernel whose issue rate is set by its resident warps (ncu: 3.5
+// active and 0.32 eligible warps per scheduler).
+__host__ __device__ constexpr size_t score_pf_off(int m, bool narrow) {
+  return (static_cast<size_t>(m) * (narrow ? 20 : 24) + 4 + 15) / 16 * 16;
+}
+__host__ __device__ constexpr size_t score_stride(int m, bool narrow) {
+  return score_pf_off(m, narrow) + 32 * kPrefetch * (narrow ? 10 : 12) + 32;
+}
 
 // Warps loop over pool columns.  For every chunk of 32 entries of the
 // column, each lane stages the first kPrefetch (anchor, value) pairs of its
@@ -197,13 +207,15 @@ __host__ __device__ constexpr size_t score_stride(int m) { return score_pf_off(m
 // row's anchors, updating the two-level accumulators of distinct anchors.
 // kSmem: per-warp state in shared memory (else in a global scratch slot,
 // for anchor counts whose state exceeds shared memory).
-template <bool kSmem>
+template <bool kSmem, bool kNarrow>
 __global__ void k_score(ScoreArgs A, int warps_per_block) {
+  using last_t = std::conditional_t<kNarrow, int16_t, int32_t>;
+  using idx_t = std::conditional_t<kNarrow, uint16_t, int32_t>;
   extern __shared__ __align__(16) unsigned char smem[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const i64 gwarp = blockIdx.x * static_cast<i64>(warps_per_block) + wib;
   const int m = A.m;
-  const size_t stride = score_stride(m);
+  const size_t stride = score_stride(m, kNarrow);
   unsigned char* base;
   if constexpr (kSmem)
     base = smem + stride * wib;
@@ -211,16 +223,16 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
     base = reinterpret_cast<unsigned char*>(A.g_scratch) + stride * static_cast<size_t>(gwarp);
   double* p = reinterpret_cast<double*>(base);
   double* t = p + m;
-  int32_t* last = reinterpret_cast<int32_t*>(t + m);
-  int32_t* touched = last + m;
-  int32_t* ntouched = touched + m;
-  double* pf_v = reinterpret_cast<double*>(base + score_pf_off(m));
-  int32_t* pf_a = reinterpret_cast<int32_t*>(pf_v + 32 * kPrefetch);
+  last_t* last = reinterpret_cast<last_t*>(t + m);
+  idx_t* touched = reinterpret_cast<idx_t*>(last + m);
+  int32_t* ntouched = reinterpret_cast<int32_t*>(touched + m);
+  double* pf_v = reinterpret_cast<double*>(base + score_pf_off(m, kNarrow));
+  idx_t* pf_a = reinterpret_cast<idx_t*>(pf_v + 32 * kPrefetch);
   uint8_t* slotmap = reinterpret_cast<uint8_t*>(pf_a + 32 * kPrefetch);  // window slot -> row lane
   for (int a = lane; a < m; a += 32) {
     p[a] = 0.0;
     t[a] = 0.0;
-    last[a] = -1;
+    last[a] = static_cast<last_t>(-1);
   }
   if (lane == 0) *ntouched = 0;
   __syncwarp();
@@ -276,7 +288,7 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
 #pragma unroll
         for (int k = 0; k < kPrefetch; ++k)
           if (k < cnt) {
-            pf_a[lane * kPrefetch + k] = A.ent_a[beg + k];
+            pf_a[lane * kPrefetch + k] = static_cast<idx_t>(A.ent_a[beg + k]);
             pf_v[lane * kPrefetch + k] = A.ent_v[beg + k];
           }
       }
@@ -289,10 +301,10 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
         const int32_t la = last[a];
         const double pa = p[a], ta = t[a];
         const bool same = la == br;
-        if (la < 0) touched[atomicAdd(ntouched, 1)] = a;
+        if (la < 0) touched[atomicAdd(ntouched, 1)] = static_cast<idx_t>(a);
         t[a] = (same || la < 0) ? ta : dadd(ta, pa);
         p[a] = dadd(same ? pa : 0.0, prod);
-        last[a] = br;
+        last[a] = static_cast<last_t>(br);
       };
       // Light rows (<= kPrefetch anchors, staged in shared memory) are packed
       // into windows of <= 32 (row, anchor) slots in row order; an anchor
@@ -355,7 +367,7 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
         const int k = lane - (__shfl_sync(0xffffffffu, excl, src) - base);
         const double vs = __shfl_sync(0xffffffffu, v, src);
         const int32_t bs = __shfl_sync(0xffffffffu, b, src);
-        const int32_t a = on ? pf_a[src * kPrefetch + k] : -1 - lane;
+        const int32_t a = on ? static_cast<int32_t>(pf_a[src * kPrefetch + k]) : -1 - lane;
         const double av = on ? pf_v[src * kPrefetch + k] : 0.0;
         const unsigned grp = __match_any_sync(0xffffffffu, a);
         const int rk = __popc(grp & ((1u << lane) - 1u));
@@ -387,7 +399,7 @@ __global__ void k_score(ScoreArgs A, int warps_per_block) {
       }
       p[a] = 0.0;  // reset for the next column
       t[a] = 0.0;
-      last[a] = -1;
+      last[a] = static_cast<last_t>(-1);
     }
     __syncwarp();
     if (lane == 0) *ntouched = 0;
@@ -710,11 +722,12 @@ struct Scorer {
     }
     // warps per block: most resident warps per SM under the shared-memory
     // limit (227 KB per SM, 1 KB reserved per block)
-    const size_t stride = score_stride(m);
+    const bool narrow = m <= 32767 && nb.clusters() <= 32767;
+    const size_t stride = score_stride(m, narrow);
     int wpb = 0, best_w = 0;
-    for (int w : {1, 2, 4, 8}) {
+    for (int w = 1; w <= 18; ++w) {  // 18 warps x 104 registers fit the register file of one block
       const size_t per_block = stride * static_cast<size_t>(w);
-      if (per_block > 200 * 1024) break;
+      if (per_block + 1024 > 227 * 1024) break;
       const int bps = std::min<int>(32, static_cast<int>((227 * 1024) / (per_block + 1024)));
       if (w * bps > best_w) {
         best_w = w * bps;
@@ -761,7 +774,8 @@ struct Scorer {
     args.next = next.get();
     const size_t smem = use_smem ? stride * static_cast<size_t>(wpb) : 0;
     if (smem > 48 * 1024)
-      PMMF_CUDA(cudaFuncSetAttribute(k_score<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      PMMF_CUDA(cudaFuncSetAttribute(narrow ? k_score<true, true> : k_score<true, false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     // persistent grid: resident warps loop over the work list
     const i64 blocks = std::min<i64>((P + wpb - 1) / wpb, use_smem ? 148 * std::max(1, best_w / wpb) : 148 * 8);
     DBuf<unsigned long long> stats;
@@ -826,10 +840,14 @@ struct Scorer {
     if (timing) cudaEventRecord(ev[1], s);
     auto launch_sparse = [&] {
       if (args.nlist <= 0) return;
-      if (use_smem)
-        PMMF_LAUNCH(k_score<true>, static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb);
+      if (use_smem && narrow)
+        PMMF_LAUNCH((k_score<true, true>), static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb);
+      else if (use_smem)
+        PMMF_LAUNCH((k_score<true, false>), static_cast<unsigned>(blocks), 32 * wpb, smem, s, args, wpb);
+      else if (narrow)
+        PMMF_LAUNCH((k_score<false, true>), static_cast<unsigned>(blocks), 32 * wpb, 0, s, args, wpb);
       else
-        PMMF_LAUNCH(k_score<false>, static_cast<unsigned>(blocks), 32 * wpb, 0, s, args, wpb);
+        PMMF_LAUNCH((k_score<false, false>), static_cast<unsigned>(blocks), 32 * wpb, 0, s, args, wpb);
     };
     launch_sparse();
     if (timing) cudaEventRecord(ev[2], s);
