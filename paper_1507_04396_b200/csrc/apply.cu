@@ -1779,41 +1779,35 @@ struct LevelScratch {
 // (blocks per SM at this kernel's register use x SMs).  A larger grid runs
 // its surplus blocks as a second, thin wave whose statically strided items
 // finish last.
+// Test hooks, read per call: PMMF_B200_MERGE2=0 sends k = 2 through the
+// generic merge kernel, PMMF_B200_FUSED_ALLOC=0 restores the separate
+// allocation launch per level.
 inline bool merge2_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PMMF_B200_MERGE2");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+  const char* e = std::getenv("PMMF_B200_MERGE2");
+  return !(e && e[0] == '0');
 }
-// k = 2: a rotation's arena allocation runs inside the count pass
-// (PMMF_B200_FUSED_ALLOC=0: separate k_rot_alloc launch per level).
+// k = 2: a rotation's arena allocation runs inside the count pass.
 inline bool fused_alloc_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("PMMF_B200_FUSED_ALLOC");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+  const char* e = std::getenv("PMMF_B200_FUSED_ALLOC");
+  return !(e && e[0] == '0');
+}
+template <typename Kernel>
+int resident_blocks(Kernel kernel) {
+  int per_sm = 0, dev = 0, sms = 148;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0) != cudaSuccess) per_sm = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  (void)cudaGetLastError();
+  return std::max(1, per_sm) * sms;
 }
 template <int K, bool kWrite>
-int persistent_blocks() {
-  static const int nb = [] {
-    int per_sm = 0, dev = 0, sms = 148;
-    cudaError_t e = cudaSuccess;
-    if constexpr (K == 2) {
-      if (merge2_enabled())
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge2<kWrite>, kThreads, 0);
-      else
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0);
-    } else {
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_merge_p<K, kWrite>, kThreads, 0);
+int persistent_blocks(bool merge2) {
+  if constexpr (K == 2) {
+    if (merge2) {
+      static const int nb2 = resident_blocks(k_merge2<kWrite>);
+      return nb2;
     }
-    if (e != cudaSuccess)
-      per_sm = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) (void)cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    (void)cudaGetLastError();
-    return std::max(1, per_sm) * sms;
-  }();
+  }
+  static const int nb = resident_blocks(k_merge_p<K, kWrite>);
   return nb;
 }
 
@@ -1904,7 +1898,8 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.level = level;
   A.rbase = S.rbase.get();
   A.rlen = S.rlen.get();
-  A.ndone = (K == 2 && merge2_enabled() && fused_alloc_enabled()) ? S.ndone.get() : nullptr;
+  const bool merge2 = K == 2 && merge2_enabled();
+  A.ndone = (merge2 && fused_alloc_enabled()) ? S.ndone.get() : nullptr;
   if (nrot <= kSetupMax && !std::getenv("PMMF_B200_NO_LEVEL_SETUP")) {
     PMMF_LAUNCH(k_level_setup<K>, 1, kSetupThreads, 0, s, A, S.np.get(), S.ioff.get(), S.nitems.get(),
                 S.item_rot.get(), S.in_entries.get(), pending, S.rbase.get(), S.rlen.get(), B.off.get(),
@@ -1927,10 +1922,11 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     c1 = EventPool::get().take();
     cudaEventRecord(c0, s);
   }
-  if (K == 2 && merge2_enabled())
-    PMMF_LAUNCH(k_merge2<false>, (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  if (merge2)
+    PMMF_LAUNCH(k_merge2<false>, (persistent_blocks<K, false>(true)), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   else
-    PMMF_LAUNCH((k_merge_p<K, false>), (persistent_blocks<K, false>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+    PMMF_LAUNCH((k_merge_p<K, false>), (persistent_blocks<K, false>(false)), kThreads, 0, s, A, S.nitems.get(),
+                S.ovf.get());
   if (c0) {
     cudaEventRecord(c1, s);
     S.cev.push_back({c0, c1});
@@ -1944,10 +1940,11 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
     e1 = EventPool::get().take();
     cudaEventRecord(e0, s);
   }
-  if (K == 2 && merge2_enabled())
-    PMMF_LAUNCH(k_merge2<true>, (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+  if (merge2)
+    PMMF_LAUNCH(k_merge2<true>, (persistent_blocks<K, true>(true)), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
   else
-    PMMF_LAUNCH((k_merge_p<K, true>), (persistent_blocks<K, true>()), kThreads, 0, s, A, S.nitems.get(), S.ovf.get());
+    PMMF_LAUNCH((k_merge_p<K, true>), (persistent_blocks<K, true>(false)), kThreads, 0, s, A, S.nitems.get(),
+                S.ovf.get());
   if (e0) {
     cudaEventRecord(e1, s);
     S.ev.push_back({e0, e1});

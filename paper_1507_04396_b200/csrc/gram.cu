@@ -538,10 +538,9 @@ void gram_sparse(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 
   if (owner_smem > 48 * 1024)
     PMMF_CUDA(cudaFuncSetAttribute(k_gram_owner, cudaFuncAttributeMaxDynamicSharedMemorySize, owner_smem));
   // PMMF_B200_GRAM_PIPE: 0 = plain kernel, 1 / 2 = pipelined with L1 / L2 accumulator prefetch, 3 = pipelined, none
-  static const int pipe = [] {
-    const char* e = std::getenv("PMMF_B200_GRAM_PIPE");
-    return e ? std::atoi(e) : 3;  // measured, config 4 gram phase: 0: 150, 1: 143.8, 2: 146.1, 3: 142.9 ms
-  }();
+  // (read per call; measured, config 4 gram phase: 0: 150, 1: 143.8, 2: 146.1, 3: 142.9 ms)
+  const char* pipe_env = std::getenv("PMMF_B200_GRAM_PIPE");
+  const int pipe = pipe_env ? std::atoi(pipe_env) : 3;
 #define PMMF_OWNER_ARGS                                                                                              \
   col0, ncols, e0, a.ptr.get(), a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco, dct, dcc, G
   if (pipe == 1)

@@ -117,3 +117,27 @@ def test_level_loop_hybrid(name, below, monkeypatch):
     monkeypatch.setenv("PMMF_B200_BATCH_NNZ", "5000")
     inp, params, part = cases.build(name)
     oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
+
+
+@pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "partitioned_input",
+                                  "undersize_repair", "oversize_recursion"])
+@pytest.mark.parametrize("hook", ["chunk32", "merge2_off", "alloc_unfused", "chunk32_alloc_unfused",
+                                  "gram_pipe0", "gram_pipe1", "gram_pipe2"])
+def test_rotation_stream_variants(name, hook, monkeypatch):
+    """The k = 2 ring merge kernel with every rotation cut into 32-row
+    partitions (multi-partition count pass + allocation by the last counting
+    warp on small inputs), its fallbacks (generic merge kernel, separate
+    allocation launch) and the sparse Gram owner kernel variants — bit-exact."""
+    if "chunk32" in hook:
+        monkeypatch.setenv("PMMF_B200_MERGE_CHUNK", "32")
+        monkeypatch.setenv("PMMF_B200_BATCH_NNZ", "4000")
+    if hook == "merge2_off":
+        monkeypatch.setenv("PMMF_B200_MERGE2", "0")
+        monkeypatch.setenv("PMMF_B200_MERGE_CHUNK", "32")
+    if "alloc_unfused" in hook:
+        monkeypatch.setenv("PMMF_B200_FUSED_ALLOC", "0")
+    if hook.startswith("gram_pipe"):
+        monkeypatch.setenv("PMMF_B200_GRAM_PIPE", hook[-1])
+        monkeypatch.setenv("PMMF_B200_GRAM_DENSE_RATIO", "0")  # sparse Gram for every cluster
+    inp, params, part = cases.build(name)
+    oracles.assert_same(oracles.factorize("gpu", inp, params, part), oracles.factorize("oracle", inp, params, part))
