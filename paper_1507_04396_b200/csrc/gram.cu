@@ -98,6 +98,24 @@ __global__ void k_gram_owner(i64 col0, i64 ncols, i64 e0, const i64* __restrict_
   }
 }
 
+// Products of an owner column (sum of its rows' run lengths): the sort key of
+// the heaviest-first column order below.
+__global__ void k_owner_cost(i64 col0, i64 ncols, i64 e0, const i64* __restrict__ ptr,
+                             const int32_t* __restrict__ run_lo, const int32_t* __restrict__ run_hi,
+                             int32_t* __restrict__ cost, int32_t* __restrict__ idx) {
+  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= ncols) return;
+  const i64 J = col0 + w;
+  i64 c = 0;
+  for (i64 e = ptr[J] + lane; e < ptr[J + 1]; e += 32) c += run_hi[e - e0] - run_lo[e - e0];
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) {
+    cost[w] = static_cast<int32_t>(c < 0x7fffffff ? c : 0x7fffffff);
+    idx[w] = static_cast<int32_t>(w);
+  }
+}
+
 // Software-pipelined k_gram_owner (same sums in the same order).  The plain
 // kernel pays three dependent global round trips per row of the owner column
 // (run bounds -> run entries -> accumulator), ~31 rows in a row on config 4.
@@ -111,10 +129,13 @@ __global__ void k_gram_owner_pipe(i64 col0, i64 ncols, i64 e0, const i64* __rest
                                   const int32_t* __restrict__ run_hi, const int32_t* __restrict__ csr_col,
                                   const double* __restrict__ csr_val, const int32_t* __restrict__ col_cluster_off,
                                   const int64_t* __restrict__ col_tile, const int32_t* __restrict__ col_c,
-                                  double* __restrict__ G) {
-  const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
+                                  double* __restrict__ G, const int32_t* __restrict__ order) {
+  const i64 w0 = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= ncols) return;
+  if (w0 >= ncols) return;
+  // optional heaviest-first column order (ncu: achieved occupancy 32% of a
+  // possible 62% in column order); measured slower, off by default
+  const i64 w = order ? order[w0] : w0;
   const i64 J = col0 + w;
   const int32_t cbase = col_cluster_off[w];
   const i64 a = J - cbase;
@@ -543,12 +564,28 @@ void gram_sparse(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 
   const int pipe = pipe_env ? std::atoi(pipe_env) : 3;
 #define PMMF_OWNER_ARGS                                                                                              \
   col0, ncols, e0, a.ptr.get(), a.val.get(), run_lo.get(), run_hi.get(), csr_col.get(), csr_val.get(), dcco, dct, dcc, G
+  DBuf<int32_t> order;
+  const char* lpt_env = std::getenv("PMMF_B200_GRAM_LPT");
+  // opt-in (PMMF_B200_GRAM_LPT=1), measured and rejected: gram phase 145 -> 153-159 ms on config 4
+  if (pipe != 0 && lpt_env && lpt_env[0] == '1' && ncols > 4096) {
+    DBuf<int32_t> cost(ncols, s), cost2(ncols, s), idx0(ncols, s);
+    order.alloc(ncols, s);
+    PMMF_LAUNCH(k_owner_cost, blocks_for(ncols * 32, kThreads), kThreads, 0, s, col0, ncols, e0, a.ptr.get(),
+                run_lo.get(), run_hi.get(), cost.get(), idx0.get());
+    size_t tmp = 0;
+    PMMF_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, cost.get(), cost2.get(), idx0.get(), order.get(),
+                                                        static_cast<int64_t>(ncols), 0, 31, s));
+    DBuf<unsigned char> t(static_cast<i64>(tmp) + 1, s);
+    PMMF_CUDA(cub::DeviceRadixSort::SortPairsDescending(t.get(), tmp, cost.get(), cost2.get(), idx0.get(), order.get(),
+                                                        static_cast<int64_t>(ncols), 0, 31, s));
+  }
+  const int32_t* dord = order.get();
   if (pipe == 1)
-    PMMF_LAUNCH(k_gram_owner_pipe<1>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
+    PMMF_LAUNCH(k_gram_owner_pipe<1>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS, dord);
   else if (pipe == 2)
-    PMMF_LAUNCH(k_gram_owner_pipe<2>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
+    PMMF_LAUNCH(k_gram_owner_pipe<2>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS, dord);
   else if (pipe == 3)
-    PMMF_LAUNCH(k_gram_owner_pipe<0>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
+    PMMF_LAUNCH(k_gram_owner_pipe<0>, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS, dord);
   else
     PMMF_LAUNCH(k_gram_owner, blocks_for(ncols * 32, kThreads), kThreads, owner_smem, s, PMMF_OWNER_ARGS);
 #undef PMMF_OWNER_ARGS
