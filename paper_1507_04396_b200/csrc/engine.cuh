@@ -45,8 +45,10 @@ struct Numbering {
   DBuf<int32_t> d_blk;             // stage id -> cluster (row block)
   DBuf<int32_t> d_s2g;             // stage id -> global
   DBuf<int32_t> d_g2s;             // global -> stage id (-1 when absent)
+  i64 n_global = 0;                // build_device: g2s stays on the device until host_g2s()
   i64 size() const { return static_cast<i64>(s2g.size()); }
   i64 clusters() const { return static_cast<i64>(off.size()) - 1; }
+  const std::vector<i64>& host_g2s();  // the host mirror of global -> stage, downloaded on first use
   // from host cluster lists (validated: the input partition)
   void build(const std::vector<std::vector<i64>>& clusters, i64 n, cudaStream_t s);
   // from a device member list (a stage partition built on the device) and

@@ -311,6 +311,9 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   PMMF_CUDA(cudaStreamCreateWithFlags(&side_holder.st, cudaStreamNonBlocking));
   const cudaStream_t side = side_holder.st;
   std::vector<uint8_t> gone(static_cast<size_t>(std::max<i64>(n, 1)), 0);
+  // reserved once: reserve(size + ne) per stage reallocated and copied the
+  // whole list every stage (2-5 ms each, also in the tiny late stages)
+  R->diag.reserve(static_cast<size_t>(std::max<i64>(n, 0)));
   for (int stage_no = 1; stage_no <= p.n_stages && !R->trivial; ++stage_no) {
     if (static_cast<i64>(active.size()) <= p.core_min) break;
     const auto t_stage = clk::now();
@@ -552,12 +555,22 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
     std::vector<int32_t> elim_loc = so.elim_loc.to_host(std::max<i64>(slots, 1));
     std::vector<int32_t> order_sid;  // eliminated stage ids, stage elimination order
     std::vector<int32_t> order_g;
-    for (i64 u = 0; u < rc; ++u)
-      for (i64 e = 0; e < nelim[u]; ++e) {
-        const i64 sid = cur.off[u] + elim_loc[out_base[u] + e];
-        order_sid.push_back(static_cast<int32_t>(sid));
-        order_g.push_back(static_cast<int32_t>(cur.s2g[sid]));
+    {
+      size_t total = 0;
+      for (i64 u = 0; u < rc; ++u) total += static_cast<size_t>(nelim[u]);
+      order_sid.resize(total);
+      order_g.resize(total);
+      size_t w = 0;
+      for (i64 u = 0; u < rc; ++u) {
+        const i64 o = cur.off[u];
+        const int32_t* el = elim_loc.data() + out_base[u];
+        for (i64 e = 0; e < nelim[u]; ++e, ++w) {
+          const i64 sid = o + el[e];
+          order_sid[w] = static_cast<int32_t>(sid);
+          order_g[w] = static_cast<int32_t>(cur.s2g[sid]);
+        }
       }
+    }
     // The rotation records (global ids, k x k blocks) are only reported:
     // a worker thread copies them through pinned staging on a side stream and
     // assembles them while the device runs the stage apply (which reads the
@@ -766,26 +779,28 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
       PMMF_CUDA(cudaMemcpyAsync(hmd, mass.get(), sizeof(double) * ne, cudaMemcpyDeviceToHost, s));
       PMMF_CUDA(cudaMemcpyAsync(hmd + ne, diag.get(), sizeof(double) * ne, cudaMemcpyDeviceToHost, s));
       PMMF_CUDA(cudaStreamSynchronize(s));
+      PMMF_TRACE("[pmmf]   bookkeeping: masses on the host at %.2f ms\n", ms_since(t_res));
       const double* hm = hmd;
       const double* hd = hmd + ne;
       st.elim_idx.assign(order_g.begin(), order_g.end());
       st.elim_diag.assign(hd, hd + ne);
       st.elim_mass.assign(hm, hm + ne);
-      R->diag.reserve(R->diag.size() + static_cast<size_t>(ne));
       for (i64 r = 0; r < ne; ++r) {
         R->residual_sq += 2.0 * hm[r];
         R->diag.push_back({order_g[r], hd[r]});
       }
     }
+    PMMF_TRACE("[pmmf]   bookkeeping: stage records filled at %.2f ms\n", ms_since(t_res));
     {
       for (int32_t g : order_g) gone[g] = 1;
-      std::vector<i64> next;
-      next.reserve(active.size() - order_g.size());
-      for (i64 g : active)
-        if (!gone[g]) next.push_back(g);
+      std::vector<i64> next(active.size() - order_g.size());
+      size_t w = 0;
+      for (const i64 g : active)
+        if (!gone[g]) next[w++] = g;
       active = std::move(next);
       for (int32_t g : order_g) gone[g] = 0;
     }
+    PMMF_TRACE("[pmmf]   bookkeeping: active set filtered at %.2f ms\n", ms_since(t_res));
     records.get();  // rotation records assembled (rethrows a copy failure)
     PMMF_TRACE("[pmmf] stage %d: residual + bookkeeping %.2f ms\n", stage_no, ms_since(t_res));
     if (trace_on()) {
@@ -809,8 +824,9 @@ std::unique_ptr<Result> factorize_device(const pmmf_b200_coo* in, const pmmf_b20
   R->core.assign(static_cast<size_t>(g * g), 0.0);
   if (g > 0) {
     std::vector<int32_t> col_sid(static_cast<size_t>(g)), pos(static_cast<size_t>(cur.size()), -1);
+    const std::vector<i64>& g2s_h = cur.host_g2s();
     for (i64 a = 0; a < g; ++a) {
-      col_sid[a] = static_cast<int32_t>(cur.g2s[active[a]]);
+      col_sid[a] = static_cast<int32_t>(g2s_h[active[a]]);
       pos[col_sid[a]] = static_cast<int32_t>(a);
     }
     DBuf<int32_t> dcs(g, s), dpos(std::max<i64>(cur.size(), 1), s);
