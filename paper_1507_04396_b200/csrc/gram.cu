@@ -499,6 +499,22 @@ std::atomic<int>& dense_gram_mode() {
   return m;
 }
 
+// Per-column cluster info from the cluster offsets (block per cluster): was
+// built column by column on the host and uploaded from pageable memory
+// (16 MB at n = 2^20, every stage).
+__global__ void k_col_info(const i64* __restrict__ off, const i64* __restrict__ tile, i64 col0, i64 tile0,
+                           int32_t* __restrict__ cco, int32_t* __restrict__ cc, int64_t* __restrict__ ct) {
+  const i64 b = off[blockIdx.x], e = off[blockIdx.x + 1];
+  for (i64 J = b + threadIdx.x; J < e; J += blockDim.x) {
+    cco[J - col0] = static_cast<int32_t>(b);
+    cc[J - col0] = static_cast<int32_t>(e - b);
+    ct[J - col0] = tile[blockIdx.x] - tile0;
+  }
+}
+__global__ void k_col_seg(const i64* __restrict__ off, i64 col0, int32_t* __restrict__ seg) {
+  const i64 b = off[blockIdx.x], e = off[blockIdx.x + 1];
+  for (i64 J = b + threadIdx.x; J < e; J += blockDim.x) seg[J - col0] = static_cast<int32_t>(blockIdx.x);
+}
 __global__ void k_ptr_at(i64 n, const i64* __restrict__ ptr, const i64* __restrict__ cols, i64* __restrict__ out) {
   const i64 i = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
   if (i < n) out[i] = ptr[cols[i]];
@@ -518,11 +534,12 @@ void gram_sparse(const Csc& a, const std::vector<i64>& off, i64 v0, i64 v1, i64 
   const i64 nseg = v1 - v0;
   const int rb = std::max(1, bits_for(std::max<i64>(N - 1, 1)));
   const int sb = std::max(1, bits_for(std::max<i64>(nseg - 1, 1)));
-  std::vector<int32_t> seg(static_cast<size_t>(ncols));
-  for (i64 u = v0; u < v1; ++u)
-    for (i64 J = off[u]; J < off[u + 1]; ++J) seg[J - col0] = static_cast<int32_t>(u - v0);
   DBuf<int32_t> dseg(ncols, s);
-  dseg.upload(seg);
+  {
+    DBuf<i64> doff(nseg + 1, s);
+    doff.upload(off.data() + v0, nseg + 1);
+    PMMF_LAUNCH(k_col_seg, static_cast<unsigned>(nseg), 256, 0, s, doff.get(), col0, dseg.get());
+  }
   DBuf<int32_t> idx(ne, s), idx2(ne, s), ecol(ne, s), run_lo(ne, s), run_hi(ne, s);
   auto sorted_runs = [&](auto zero_key) {
     using KeyT = decltype(zero_key);
@@ -698,24 +715,16 @@ void gram_tiles(const Csc& a, const std::vector<i64>& off, i64 u0, i64 u1, const
   if (ncols <= 0) return;
   const i64 nb = u1 - u0;
   // per-column cluster info
-  std::vector<int32_t> cco(static_cast<size_t>(ncols)), cc(static_cast<size_t>(ncols));
-  std::vector<int64_t> ct(static_cast<size_t>(ncols));
-  for (i64 u = u0; u < u1; ++u)
-    for (i64 J = off[u]; J < off[u + 1]; ++J) {
-      cco[J - col0] = static_cast<int32_t>(off[u]);
-      cc[J - col0] = static_cast<int32_t>(off[u + 1] - off[u]);
-      ct[J - col0] = tile_off[u] - tile_off[u0];
-    }
   DBuf<int32_t> dcco(ncols, s), dcc(ncols, s);
   DBuf<int64_t> dct(ncols, s);
-  dcco.upload(cco);
-  dcc.upload(cc);
-  dct.upload(ct);
   // entry offsets at the cluster boundaries
   std::vector<i64> eptr;
   {
-    DBuf<i64> cols(nb + 1, s), at(nb + 1, s);
+    DBuf<i64> cols(nb + 1, s), at(nb + 1, s), dtile(nb + 1, s);
     cols.upload(off.data() + u0, nb + 1);
+    dtile.upload(tile_off.data() + u0, nb + 1);
+    PMMF_LAUNCH(k_col_info, static_cast<unsigned>(nb), 256, 0, s, cols.get(), dtile.get(), col0, tile_off[u0],
+                dcco.get(), dcc.get(), dct.get());
     PMMF_LAUNCH(k_ptr_at, blocks_for(nb + 1, kThreads), kThreads, 0, s, nb + 1, a.ptr.get(), cols.get(), at.get());
     eptr = at.to_host(nb + 1);
   }
