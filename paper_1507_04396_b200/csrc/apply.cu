@@ -94,6 +94,11 @@ struct PassArgs {
   // counts a rotation's last partition allocates it (rot_alloc_warp), so the
   // level needs no separate allocation launch (nullptr: k_rot_alloc runs)
   int32_t* ndone;
+  // k = 2: the partition size of this level, chosen by k_level_setup (a level
+  // that would leave most warps without a partition is cut finer); nullptr:
+  // `chunk` applies
+  int32_t* chunk_d;
+  int fine_chunk, fine_items;  // rows per partition of a level below fine_items default-size partitions
 };
 
 // Row range of partition p of rotation t: split points are rows of the
@@ -367,6 +372,7 @@ __global__ void k_nparts(PassArgs A, int64_t* __restrict__ nparts, unsigned long
   }
   nparts[i] = max(1, (Lmax + A.chunk - 1) / A.chunk);
   if (A.ndone) A.ndone[i] = 0;
+  if (i == 0 && A.chunk_d) *A.chunk_d = A.chunk;
   atomicAdd(in_entries, S);
 }
 
@@ -386,6 +392,8 @@ __global__ void k_item_rot(i64 nrot, const int64_t* __restrict__ ioff, const int
 // have a few hundred rotations).
 constexpr int kSetupThreads = 1024;
 constexpr i64 kSetupMax = 8 * kSetupThreads;
+constexpr int kFineChunk = 128;   // rows per partition of a level below kFineItems default-size partitions
+constexpr int kFineItems = 2048;  // (the merge grid holds 4,736 warps)
 template <int K>
 __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64_t* __restrict__ np,
                                                                int64_t* __restrict__ ioff, int64_t* __restrict__ nitems,
@@ -397,7 +405,7 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
   using BlockScan = cub::BlockScan<int64_t, kSetupThreads>;
   __shared__ typename BlockScan::TempStorage scan;
   __shared__ int64_t s_run;
-  __shared__ int s_nq;
+  __shared__ int s_nq, s_items;
   __shared__ int64_t q_start[kSetupThreads];
   __shared__ int32_t q_len[kSetupThreads], q_rot[kSetupThreads];
   // the previous level's commit (k_commit_level), deferred into this launch:
@@ -417,9 +425,32 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
   if (threadIdx.x == 0) {
     s_run = 0;
     s_nq = 0;
+    s_items = 0;
   }
   unsigned long long ins = 0;
   __syncthreads();
+  // Partition size of the level.  With the default size a level of few, short
+  // rotations gives most of the grid's warps nothing and its launch lasts as
+  // long as one warp's 16-window merge; below kFineItems partitions the level
+  // is cut into kFineChunk-row partitions instead (same results for any size).
+  int chunk = A.chunk;
+  if (A.chunk_d != nullptr && A.chunk <= A.fine_chunk) {
+    if (threadIdx.x == 0) *A.chunk_d = chunk;
+  } else if (A.chunk_d != nullptr) {
+    int mine = 0;
+    for (i64 i = threadIdx.x; i < nrot; i += kSetupThreads) {
+      const int t = A.rots[i];
+      int Lmax = 0;
+#pragma unroll
+      for (int b = 0; b < K; ++b) Lmax = max(Lmax, A.len[A.ids[static_cast<i64>(t) * K + b] - A.col0]);
+      mine += max(1, (Lmax + A.chunk - 1) / A.chunk);
+    }
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_items, mine);
+    __syncthreads();
+    if (s_items < A.fine_items) chunk = A.fine_chunk;
+    if (threadIdx.x == 0) *A.chunk_d = chunk;
+  }
   for (i64 base = 0; base < nrot; base += kSetupThreads) {
     const i64 i = base + threadIdx.x;
     int64_t v = 0;
@@ -432,7 +463,7 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
         Lmax = max(Lmax, L);
         ins += static_cast<unsigned long long>(L);
       }
-      v = max(1, (Lmax + A.chunk - 1) / A.chunk);
+      v = max(1, (Lmax + chunk - 1) / chunk);
       np[i] = v;
       if (A.ndone) A.ndone[i] = 0;
     }
@@ -922,6 +953,7 @@ __global__ void __launch_bounds__(kThreads, kMerge2Occ) k_merge2(PassArgs A, con
   __shared__ double ring_v[kMerge2Warps][2][kWrite ? kRing : 1];
   if (*reinterpret_cast<volatile const int32_t*>(ovf) != INT_MAX) return;
   const i64 nitems = *nitems_d;
+  const int chunk = A.chunk_d ? *A.chunk_d : A.chunk;  // this level's partition size (k_level_setup)
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const i64 nw = (static_cast<i64>(gridDim.x) * blockDim.x) >> 5;
   const i64 w = (blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x) >> 5;
@@ -979,8 +1011,8 @@ __global__ void __launch_bounds__(kThreads, kMerge2Occ) k_merge2(PassArgs A, con
         const int lg = L1 > L0 ? 1 : 0;
         const i64 ls = lg ? s1 : s0;
         const i64 os = lg ? s0 : s1, oe = os + (lg ? L0 : L1);
-        const i64 lo_l = ls + static_cast<i64>(p) * A.chunk;
-        const i64 hi_l = p == np - 1 ? ls + (lg ? L1 : L0) : ls + static_cast<i64>(p + 1) * A.chunk;
+        const i64 lo_l = ls + static_cast<i64>(p) * chunk;
+        const i64 hi_l = p == np - 1 ? ls + (lg ? L1 : L0) : ls + static_cast<i64>(p + 1) * chunk;
         const i64 lo_o = p == 0 ? os : warp_search_g(A.arow, os, oe, __ldg(A.arow + lo_l));
         const i64 hi_o = p == np - 1 ? oe : warp_search_g(A.arow, os, oe, __ldg(A.arow + hi_l));
         beg[0] = lg ? lo_o : lo_l;
@@ -1766,7 +1798,7 @@ struct LevelScratch {
   DBuf<int64_t> np, ioff, nitems, cnt, pos;
   DBuf<int32_t> item_rot;
   DBuf<i64> rbase;
-  DBuf<int32_t> rlen, ovf, ndone;
+  DBuf<int32_t> rlen, ovf, ndone, chunk_d;
   DBuf<unsigned long long> cursor, in_entries;
   DBuf<unsigned char> scan_tmp;
   size_t scan_bytes = 0;
@@ -1784,6 +1816,16 @@ struct LevelScratch {
 // allocation launch per level.
 inline bool merge2_enabled() {
   const char* e = std::getenv("PMMF_B200_MERGE2");
+  return !(e && e[0] == '0');
+}
+inline int fine_param(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : dflt;
+  return v >= lo && v <= hi ? v : dflt;
+}
+// k = 2: levels of few partitions are cut finer (PMMF_B200_FINE_LEVELS=0: one size).
+inline bool fine_levels_enabled() {
+  const char* e = std::getenv("PMMF_B200_FINE_LEVELS");
   return !(e && e[0] == '0');
 }
 // k = 2: a rotation's arena allocation runs inside the count pass.
@@ -1900,6 +1942,9 @@ void run_level(Batch& B, LevelScratch& S, const LevelPlan& plan, const int32_t* 
   A.rlen = S.rlen.get();
   const bool merge2 = K == 2 && merge2_enabled();
   A.ndone = (merge2 && fused_alloc_enabled()) ? S.ndone.get() : nullptr;
+  A.chunk_d = (merge2 && fine_levels_enabled()) ? S.chunk_d.get() : nullptr;
+  A.fine_chunk = fine_param("PMMF_B200_FINE_CHUNK", kFineChunk, 32, 512);
+  A.fine_items = fine_param("PMMF_B200_FINE_ITEMS", kFineItems, 1, 8192);
   if (nrot <= kSetupMax && !std::getenv("PMMF_B200_NO_LEVEL_SETUP")) {
     PMMF_LAUNCH(k_level_setup<K>, 1, kSetupThreads, 0, s, A, S.np.get(), S.ioff.get(), S.nitems.get(),
                 S.item_rot.get(), S.in_entries.get(), pending, S.rbase.get(), S.rlen.get(), B.off.get(),
@@ -2166,7 +2211,11 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     LevelScratch S;
     const int K = plan.k;
     auto size_items = [&] {
-      S.max_items = max_rot + B.cap / merge_chunk() + 1;
+      // + the finest cut of a small level (k_level_setup): fewer than
+      // fine_items default-size partitions, each at most chunk / fine_chunk + 1 finer ones
+      S.max_items = max_rot + B.cap / merge_chunk() + 1 +
+                    static_cast<i64>(fine_param("PMMF_B200_FINE_ITEMS", kFineItems, 1, 8192)) *
+                        (merge_chunk() / fine_param("PMMF_B200_FINE_CHUNK", kFineChunk, 32, 512) + 1);
       S.cnt.alloc(K * S.max_items, s);
       S.pos.alloc(K * S.max_items, s);
       S.item_rot.alloc(S.max_items, s);
@@ -2178,6 +2227,7 @@ void rotate_pass(std::vector<Piece>& out, const Csc& in, const std::vector<i64>&
     S.rbase.alloc(K * max_rot, s);
     S.rlen.alloc(K * max_rot, s);
     S.ndone.alloc(max_rot, s);
+    S.chunk_d.alloc(1, s);
     S.ovf.alloc(1, s);
     S.cursor.alloc(1, s);
     S.in_entries.alloc(2, s);

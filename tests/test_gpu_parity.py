@@ -122,7 +122,7 @@ def test_level_loop_hybrid(name, below, monkeypatch):
 @pytest.mark.parametrize("name", ["rmat12_m16", "grid64_m16", "dense256_m2", "partitioned_input",
                                   "undersize_repair", "oversize_recursion"])
 @pytest.mark.parametrize("hook", ["chunk32", "merge2_off", "alloc_unfused", "chunk32_alloc_unfused",
-                                  "gram_pipe0", "gram_pipe1", "gram_pipe2"])
+                                  "gram_pipe0", "gram_pipe1", "gram_pipe2", "fine_off", "fine_32_8192"])
 def test_rotation_stream_variants(name, hook, monkeypatch):
     """The k = 2 ring merge kernel with every rotation cut into 32-row
     partitions (multi-partition count pass + allocation by the last counting
@@ -136,6 +136,12 @@ def test_rotation_stream_variants(name, hook, monkeypatch):
         monkeypatch.setenv("PMMF_B200_MERGE_CHUNK", "32")
     if "alloc_unfused" in hook:
         monkeypatch.setenv("PMMF_B200_FUSED_ALLOC", "0")
+    if hook == "fine_off":  # one partition size for every level
+        monkeypatch.setenv("PMMF_B200_FINE_LEVELS", "0")
+    if hook == "fine_32_8192":  # every level below 8192 partitions cut into 32-row partitions
+        monkeypatch.setenv("PMMF_B200_FINE_CHUNK", "32")
+        monkeypatch.setenv("PMMF_B200_FINE_ITEMS", "8192")
+        monkeypatch.setenv("PMMF_B200_BATCH_NNZ", "4000")
     if hook.startswith("gram_pipe"):
         monkeypatch.setenv("PMMF_B200_GRAM_PIPE", hook[-1])
         monkeypatch.setenv("PMMF_B200_GRAM_DENSE_RATIO", "0")  # sparse Gram for every cluster
