@@ -408,10 +408,31 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
   __shared__ int s_nq, s_items;
   __shared__ int64_t q_start[kSetupThreads];
   __shared__ int32_t q_len[kSetupThreads], q_rot[kSetupThreads];
+  // Most levels fit one tile of kSetupThreads rotations and the launch is a
+  // chain of dependent loads (rotation -> ids -> column length, for the commit
+  // and again for this level): the first tile's rotation and id loads of both
+  // are issued together, before the commit's stores.
+  const i64 nrot = A.nrot;
+  const i64 i0 = threadIdx.x;
+  const bool do_commit = P.nrot > 0 && *reinterpret_cast<volatile const int32_t*>(P.ovf) == INT_MAX;
+  int at = -1, pt = -1;
+  if (i0 < nrot) at = A.rots[i0];
+  if (do_commit && i0 < P.nrot) pt = P.rots[i0];
+  int aid[K];
+#pragma unroll
+  for (int b = 0; b < K; ++b) aid[b] = at >= 0 ? A.ids[static_cast<i64>(at) * K + b] - static_cast<int>(A.col0) : 0;
   // the previous level's commit (k_commit_level), deferred into this launch:
   // its outputs' (off, len) must be in place before this level reads len
-  if (P.nrot > 0 && *reinterpret_cast<volatile const int32_t*>(P.ovf) == INT_MAX)
-    for (i64 i = threadIdx.x; i < P.nrot; i += blockDim.x) {
+  if (pt >= 0) {
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+      const int id = P.ids[static_cast<i64>(pt) * K + a] - static_cast<int>(P.col0);
+      off[id] = rbase[K * i0 + a];
+      len[id] = rlen[K * i0 + a];
+    }
+  }
+  if (do_commit)
+    for (i64 i = i0 + blockDim.x; i < P.nrot; i += blockDim.x) {
       const int t = P.rots[i];
 #pragma unroll
       for (int a = 0; a < K; ++a) {
@@ -421,7 +442,17 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
       }
     }
   __syncthreads();
-  const i64 nrot = A.nrot;
+  // first tile: this thread's rotation, from the ids loaded above
+  int Lmax0 = 0;
+  unsigned long long Lsum0 = 0;
+  if (at >= 0) {
+#pragma unroll
+    for (int b = 0; b < K; ++b) {
+      const int L = A.len[aid[b]];
+      Lmax0 = max(Lmax0, L);
+      Lsum0 += static_cast<unsigned long long>(L);
+    }
+  }
   if (threadIdx.x == 0) {
     s_run = 0;
     s_nq = 0;
@@ -437,8 +468,8 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
   if (A.chunk_d != nullptr && A.chunk <= A.fine_chunk) {
     if (threadIdx.x == 0) *A.chunk_d = chunk;
   } else if (A.chunk_d != nullptr) {
-    int mine = 0;
-    for (i64 i = threadIdx.x; i < nrot; i += kSetupThreads) {
+    int mine = at >= 0 ? max(1, (Lmax0 + A.chunk - 1) / A.chunk) : 0;
+    for (i64 i = i0 + kSetupThreads; i < nrot; i += kSetupThreads) {
       const int t = A.rots[i];
       int Lmax = 0;
 #pragma unroll
@@ -455,13 +486,18 @@ __global__ void __launch_bounds__(kSetupThreads) k_level_setup(PassArgs A, int64
     const i64 i = base + threadIdx.x;
     int64_t v = 0;
     if (i < nrot) {
-      const int t = A.rots[i];
-      int Lmax = 0;
+      int Lmax = Lmax0;
+      if (base == 0) {
+        ins += Lsum0;
+      } else {
+        const int t = A.rots[i];
+        Lmax = 0;
 #pragma unroll
-      for (int b = 0; b < K; ++b) {
-        const int L = A.len[A.ids[static_cast<i64>(t) * K + b] - A.col0];
-        Lmax = max(Lmax, L);
-        ins += static_cast<unsigned long long>(L);
+        for (int b = 0; b < K; ++b) {
+          const int L = A.len[A.ids[static_cast<i64>(t) * K + b] - A.col0];
+          Lmax = max(Lmax, L);
+          ins += static_cast<unsigned long long>(L);
+        }
       }
       v = max(1, (Lmax + chunk - 1) / chunk);
       np[i] = v;
