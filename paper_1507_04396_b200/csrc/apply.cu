@@ -77,7 +77,7 @@ struct PassArgs {
   i64 nrot;              // rotations in level
   i64 nitems;            // total partitions
   int64_t* cnt;          // K * nitems kept counts, layout [K*ioff_t + a*np_t + p]
-  const int64_t* pos;    // exclusive scan of cnt (write pass)
+  int64_t* pos;          // exclusive scan of cnt (write pass; written by the allocation)
   i64 base;              // arena offset of this level's outputs (write pass)
   int32_t* wrow;
   double* wval;
@@ -551,7 +551,7 @@ __global__ void k_items(i64 nrot, const int64_t* __restrict__ ioff, const int64_
 __device__ __forceinline__ void rot_alloc_warp2(const PassArgs& A, i64 i, i64 io, i64 np) {
   const int lane = threadIdx.x & 31;
   const i64 f = 2 * io;
-  int64_t* pos = const_cast<int64_t*>(A.pos);
+  int64_t* pos = A.pos;
   i64 run = 0;
   for (i64 p0 = 0; p0 < np; p0 += 128) {
     i64 c[4];
